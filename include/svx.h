@@ -1,0 +1,189 @@
+/*
+ * svx.h -- C ABI of the B200-native SLIM-VDB integration engine (libsvx.so).
+ *
+ * This is the drop-in boundary for the reference's per-frame integration hot
+ * path.  The reference (semvox, /root/reference/pkg) exposes that path through
+ * a Python backend-module protocol (pkg/src/semvox/backend.py:1-7) whose
+ * compiled member is the Cython GridCore + integrate_points
+ * (pkg/src/semvox/_core.pyx:79-472, 621-858), driven by
+ * semvox_bindings.Mapper (pkg/bindings/src/semvox_bindings/__init__.py:58-201).
+ * Each entry point below cites the reference interface it replaces.
+ *
+ * Conventions
+ *   - Plain C types only; no torch/CUDA types in signatures.  Streams are
+ *     passed as `void*` (a cudaStream_t; NULL = the legacy default stream).
+ *   - Input/output array pointers may be HOST or DEVICE memory: the library
+ *     inspects each pointer and stages host buffers through device memory on
+ *     the caller's stream.  Device pointers are borrowed for the call only.
+ *   - Every call returns an svx_status.  On failure a thread-local message is
+ *     available from svx_last_error().  Status codes map 1:1 onto the
+ *     reference's exception classes (pkg/src/semvox/errors.py:4-25).
+ *   - One host thread per map handle (the reference Mapper is
+ *     "single-threaded from the scripting side", bindings/__init__.py:14-16).
+ */
+#ifndef SVX_H
+#define SVX_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SVX_ABI_VERSION 1
+
+/* Status codes -> semvox.errors classes (errors.py:4-25). */
+typedef enum {
+    SVX_OK = 0,
+    SVX_E_CONFIG = 1,   /* ConfigError          (errors.py:12) */
+    SVX_E_PAYLOAD = 2,  /* PayloadMismatchError (errors.py:16) */
+    SVX_E_INPUT = 3,    /* UserInputError       (errors.py:8)  */
+    SVX_E_RANGE = 4,    /* OutOfRangeError      (errors.py:24) */
+    SVX_E_FORMAT = 5,   /* FormatError          (errors.py:20) */
+    SVX_E_INTERNAL = 6, /* SemvoxError          (errors.py:4)  */
+    SVX_E_CUDA = 7      /* SemvoxError (device failure; message carries the CUDA error) */
+} svx_status;
+
+/* Semantic payload kind (grid.py:26-28 KIND_TSDF/KIND_CLOSED/KIND_OPEN). */
+enum { SVX_SEM_NONE = 0, SVX_SEM_CLOSED = 1, SVX_SEM_OPEN = 2 };
+
+/* Element type codes for arrays crossing the boundary. */
+enum { SVX_F32 = 0, SVX_F64 = 1 };
+
+/*
+ * Map construction parameters.  Mirrors the union of FusionConfig,
+ * ClosedSetConfig and OpenSetConfig (config.py:36-110) as routed by
+ * Mapper.__init__ (bindings/__init__.py:77-116); validation of the values
+ * (messages included) happens on the host side before svx_create.
+ */
+typedef struct {
+    double voxel_size;       /* FusionConfig.voxel_size */
+    double truncation;       /* FusionConfig.truncation */
+    double max_range;        /* FusionConfig.max_range  */
+    int32_t weight_fn;       /* 0 constant_one, 1 linear_dropoff (fusion.py:270) */
+    int32_t space_carving;   /* FusionConfig.space_carving */
+    int32_t sem_kind;        /* SVX_SEM_* */
+    int32_t num_classes;     /* ClosedSetConfig.num_classes (closed) */
+    int32_t last_wins;       /* ClosedSetConfig.fusion == "last_wins" */
+    int32_t count_dtype;     /* SVX_F32 / SVX_F64: ClosedSetConfig.count_dtype */
+    int32_t feature_dim;     /* OpenSetConfig.feature_dim (open) */
+    int32_t state_dtype;     /* SVX_F32 / SVX_F64: OpenSetConfig.state_dtype */
+    double prior_beta;       /* OpenSetConfig.prior_beta (background of beta) */
+    double lambda_floor;     /* OpenSetConfig.lambda_floor */
+    int32_t tsdf_dtype;      /* SVX_F64: reference layout (grid.py:45-47, bit-exact);
+                                SVX_F32: compact fp32 d/w (f64 math, f32 store) */
+    int32_t device;          /* CUDA device ordinal */
+    int64_t reserve_voxels;  /* initial voxel-pool capacity (0 = default) */
+    int64_t reserve_blocks;  /* initial block-pool capacity (0 = default) */
+} svx_config;
+
+/*
+ * Per-frame report.  Fields points_in..touched_voxels are
+ * IntegrationReport (fusion.py:103-117); band_hits/touched_voxels follow the
+ * reference's kernel report (_core.pyx:666,747).
+ */
+typedef struct {
+    int64_t points_in;
+    int64_t points_used;
+    int64_t skipped_nonfinite;
+    int64_t skipped_range;
+    int64_t skipped_degenerate;
+    int64_t skipped_bad_label;
+    int64_t band_hits;
+    int64_t touched_voxels;
+    int64_t new_blocks;      /* leaves allocated by this frame */
+    int64_t new_voxels;      /* voxels activated by this frame */
+    double kernel_ms;        /* device time of the frame (CUDA events) */
+} svx_report;
+
+/* Map occupancy (grid.py:194-202 MemoryStats; evalbench.py:297-327). */
+typedef struct {
+    int64_t leaf_count;      /* allocated 8^3 blocks */
+    int64_t active_voxels;
+    int64_t resident_bytes;  /* device bytes held by live blocks + voxel payloads */
+    int64_t payload_bytes_per_voxel;
+    int64_t frames_integrated;
+    int64_t hash_capacity;
+    int64_t voxel_capacity;
+    int64_t block_capacity;
+} svx_stats;
+
+typedef struct svx_map svx_map;
+
+/* ---- lifetime ---------------------------------------------------------- */
+
+/* Replaces make_grids (fusion.py:296-314) + GridCore.__init__ (_core.pyx:104-141). */
+svx_status svx_create(const svx_config* cfg, svx_map** out);
+svx_status svx_destroy(svx_map* map);
+
+/* ---- integration ---------------------------------------------------------
+ * Replaces integrate_frame (fusion.py:200-293) from the world transform on,
+ * including backend.integrate_points (_core.pyx:621-858 / _pycore.py:449-539).
+ *   points   (n,3) SVX_F32|SVX_F64, sensor frame
+ *   pose     4x4 row-major sensor-to-world, already validated/orthonormalised
+ *            on the host (fusion.py:31-77)
+ *   labels   (n,) int32 class ids 1..k (closed) or NULL
+ *   feats    (n,D) SVX_F32|SVX_F64 (open) or NULL
+ * The transform is p_w = ((R0*x + R1*y) + R2*z) + t without FMA contraction
+ * (identity rotations are exact, matching numpy's BLAS result).
+ */
+svx_status svx_integrate(svx_map* map, const void* points, int32_t points_dtype, int64_t n,
+                         const double pose[16], const int32_t* labels, const void* feats,
+                         int32_t feats_dtype, void* stream, svx_report* report);
+
+/* Same, for points already in the world frame with the sensor origin given:
+ * the reference's backend seam (fusion.py:229-263 -> integrate_points), where
+ * delta = p - origin, t = sqrt((dx*dx + dy*dy) + dz*dz), u = delta / t. */
+svx_status svx_integrate_world(svx_map* map, const void* points_world, int32_t points_dtype,
+                               int64_t n, const double origin[3], const int32_t* labels,
+                               const void* feats, int32_t feats_dtype, void* stream,
+                               svx_report* report);
+
+/* ---- queries ---------------------------------------------------------------
+ * Active order is leaf-allocation then slot order, identical to
+ * GridCore.active_slots (_core.pyx:424-444) + slots_to_coords (:446-463).
+ */
+svx_status svx_stats_get(svx_map* map, svx_stats* out);
+svx_status svx_active_count(svx_map* map, int64_t* count);
+
+/* SparseGrid.active_values (grid.py:163-168).  Outputs (any may be NULL):
+ *   coords (count,3) int64; d, w (count,) in tsdf_dtype; sem0 (count,C|D) and
+ *   sem1 (count,D) in count_dtype/state_dtype.  `capacity` = rows the buffers
+ *   hold; fails with SVX_E_INPUT if smaller than the active count. */
+svx_status svx_export_active(svx_map* map, int64_t capacity, int64_t* coords, void* d, void* w,
+                             void* sem0, void* sem1, void* stream);
+
+/* SparseGrid.probe_many (grid.py:176-190) via GridCore.probe_coords
+ * (_core.pyx:324-375): background values where inactive; never allocates. */
+svx_status svx_probe(svx_map* map, const int64_t* coords, int64_t m, void* d, void* w,
+                     void* sem0, void* sem1, uint8_t* active, void* stream);
+
+/* Mapper.query (bindings/__init__.py:153-169) = cosine_to_embeddings
+ * (gaussian.py:158-170) of every active mean against one query (D,) f64;
+ * sims (count,) f64 in active order, NaN where the mean is all zero. */
+svx_status svx_query_cosine(svx_map* map, const double* query, int64_t capacity, double* sims,
+                            void* stream);
+
+/* classify_means (gaussian.py:132-155) over all active voxels, weights = the
+ * TSDF weight (mesh.py:419-445).  emb (k,D) f64.  labels (count,) int32
+ * (0 = reject), best (count,) f64; sims (count,k) f64 optional. */
+svx_status svx_classify(svx_map* map, const double* emb, int32_t k, double temperature,
+                        double confidence_threshold, int64_t capacity, int32_t* labels,
+                        double* best, double* sims, void* stream);
+
+/* Closed-set readout over active voxels: mode 0 = dirichlet.label_map
+ * (argmax+1, ties to lowest, dirichlet.py:81-88); mode 1 = evalbench.grid_labels
+ * (0 when all counts are zero, evalbench.py:30-55). */
+svx_status svx_label_map(svx_map* map, int32_t mode, int64_t capacity, int32_t* labels,
+                         void* stream);
+
+/* ---- diagnostics --------------------------------------------------------- */
+const char* svx_last_error(void);
+int32_t svx_abi_version(void);
+/* Number of kernels this library launched since load (evidence counter). */
+int64_t svx_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SVX_H */

@@ -1,0 +1,27 @@
+"""B200-native SLIM-VDB integration engine (arxiv 2512.12945 hot path).
+
+Public surface mirrors the reference's scripting facade
+(pkg/bindings/src/semvox_bindings/__init__.py) for the integration path:
+``Mapper`` plus the semvox error classes and config records.  The compute
+path is libsvx.so (hand-written sm_100a CUDA behind a C ABI, include/svx.h).
+"""
+
+from .config import ClosedSetConfig, EngineConfig, FusionConfig, OpenSetConfig
+from .errors import (
+    ConfigError,
+    FormatError,
+    OutOfRangeError,
+    PayloadMismatchError,
+    SemvoxError,
+    UserInputError,
+)
+from .mapper import GridView, IntegrationReport, Mapper, validate_rotation
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "Mapper", "GridView", "IntegrationReport", "validate_rotation",
+    "FusionConfig", "ClosedSetConfig", "OpenSetConfig", "EngineConfig",
+    "SemvoxError", "UserInputError", "ConfigError", "PayloadMismatchError",
+    "FormatError", "OutOfRangeError",
+]

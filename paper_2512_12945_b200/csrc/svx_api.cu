@@ -1,0 +1,714 @@
+// svx_api.cu -- C ABI entry points and the per-frame orchestration.
+//
+// Frame pipeline on the caller's stream:
+//   K1a count   validation masks + DDA row count + frame bbox   (svx_march.cu)
+//   scan        row offsets                                       (CUB)
+//   K1b fill    (voxel key, point) rows                           (svx_march.cu)
+//   K2  sort    stable radix sort on the packed voxel key         (CUB)
+//   K3  group   run-length encode -> unique voxels + row counts   (CUB)
+//   K4  blocks  leaf hash find-or-insert, first-occurrence ids    (svx_update.cu)
+//   K5/6 update fused TSDF + closed/open semantic update          (svx_update.cu)
+#include <cuda_runtime.h>
+#include <limits.h>
+#include <math.h>
+#include <string.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cub/cub.cuh>
+#include <string>
+
+#include "svx_internal.cuh"
+
+namespace svx {
+
+static thread_local std::string g_error;
+static std::atomic<long long> g_launches{0};
+
+void set_error(const std::string& msg) { g_error = msg; }
+
+svx_status fail(svx_status code, const std::string& msg) {
+    g_error = msg;
+    return code;
+}
+
+void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+svx_status ensure(DevBuf& buf, size_t bytes, cudaStream_t s, bool keep, int fill) {
+    if (bytes == 0) bytes = 16;
+    if (buf.p && buf.bytes >= bytes) return SVX_OK;
+    size_t nb = std::max(bytes, buf.bytes * 2);
+    void* np = nullptr;
+    cudaError_t e = cudaMalloc(&np, nb);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(SVX_E_CUDA, std::string("device allocation of ") + std::to_string(nb) +
+                                    " bytes failed: " + cudaGetErrorString(e));
+    }
+    size_t old = 0;
+    if (keep && buf.p && buf.bytes) {
+        old = buf.bytes;
+        SVX_CUDA(cudaMemcpyAsync(np, buf.p, old, cudaMemcpyDeviceToDevice, s));
+    }
+    if (fill >= 0) SVX_CUDA(cudaMemsetAsync((char*)np + old, fill, nb - old, s));
+    if (buf.p) {
+        SVX_CUDA(cudaStreamSynchronize(s));
+        SVX_CUDA(cudaFree(buf.p));
+    }
+    buf.p = np;
+    buf.bytes = nb;
+    return SVX_OK;
+}
+
+void release(DevBuf& buf) {
+    if (buf.p) cudaFree(buf.p);
+    buf.p = nullptr;
+    buf.bytes = 0;
+}
+
+namespace {
+
+__global__ void k_iota(int64_t n, unsigned* out) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = (unsigned)i;
+}
+
+bool is_device_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes a;
+    cudaError_t e = cudaPointerGetAttributes(&a, p);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// Device view of a caller array: device pointers pass through, host arrays
+// are copied into `stage` on the stream.
+svx_status stage_in(const void* p, size_t bytes, DevBuf& stage, cudaStream_t s, const void** out) {
+    if (!p || bytes == 0) {
+        *out = p;
+        return SVX_OK;
+    }
+    if (is_device_ptr(p)) {
+        *out = p;
+        return SVX_OK;
+    }
+    SVX_TRY(ensure(stage, bytes, s));
+    SVX_CUDA(cudaMemcpyAsync(stage.p, p, bytes, cudaMemcpyHostToDevice, s));
+    *out = stage.p;
+    return SVX_OK;
+}
+
+int bitlen(long long v) {
+    int b = 0;
+    while (v > 0) {
+        ++b;
+        v >>= 1;
+    }
+    return b;
+}
+
+size_t tsdf_elem(const svx_map* m) { return m->cfg.tsdf_dtype == SVX_F64 ? 8 : 4; }
+size_t sem_elem(const svx_map* m) {
+    if (m->cfg.sem_kind == SVX_SEM_CLOSED) return m->cfg.count_dtype == SVX_F64 ? 8 : 4;
+    if (m->cfg.sem_kind == SVX_SEM_OPEN) return m->cfg.state_dtype == SVX_F64 ? 8 : 4;
+    return 0;
+}
+
+// Voxel-pool capacity: grow by doubling, zero-filled (closed counts and open
+// means have a zero background; voxel ids are never recycled).
+svx_status reserve_voxels(svx_map* m, int64_t need, cudaStream_t s) {
+    if (need <= m->vcap) return SVX_OK;
+    int64_t cap = std::max<int64_t>(need, 2 * m->vcap);
+    const size_t te = tsdf_elem(m), se = sem_elem(m);
+    SVX_TRY(ensure(m->vd, te * cap, s, true));
+    SVX_TRY(ensure(m->vw, te * cap, s, true));
+    if (m->cfg.sem_kind != SVX_SEM_NONE)
+        SVX_TRY(ensure(m->s0, se * (size_t)m->payload_d * cap, s, true, 0));
+    if (m->cfg.sem_kind == SVX_SEM_OPEN)
+        SVX_TRY(ensure(m->s1, se * (size_t)m->payload_d * cap, s, true, 0));
+    m->vcap = cap;
+    return SVX_OK;
+}
+
+svx_status reserve_blocks(svx_map* m, int64_t need, cudaStream_t s) {
+    if (need > m->bcap) {
+        int64_t cap = std::max<int64_t>(need, 2 * m->bcap);
+        SVX_TRY(ensure(m->bcoord, sizeof(int4) * cap, s, true));
+        SVX_TRY(ensure(m->bmask, sizeof(unsigned long long) * kMaskWords * cap, s, true, 0));
+        SVX_TRY(ensure(m->bslot, sizeof(int) * kLeafVolume * cap, s, true, 0xFF));
+        m->bcap = cap;
+    }
+    // keep the leaf hash at <= 50% load for the worst case of this frame
+    int64_t want = 1024;
+    while (want < 2 * need) want <<= 1;
+    if (want > m->hcap) {
+        DevBuf nt;
+        SVX_TRY(ensure(nt, sizeof(int4) * want, s, false, 0xFF));
+        SVX_TRY(launch_rehash(m, ptr<int4>(nt), want, s));
+        SVX_CUDA(cudaStreamSynchronize(s));
+        release(m->hash);
+        m->hash = nt;
+        m->hcap = want;
+    }
+    return SVX_OK;
+}
+
+svx_status integrate_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n,
+                          const PoseParams& pp, const int32_t* labels_in, const void* feats_in,
+                          int feats_f64, cudaStream_t s, svx_report* rep) {
+    svx_report r;
+    memset(&r, 0, sizeof(r));
+    r.points_in = n;
+    const int kind = m->cfg.sem_kind;
+    if (kind == SVX_SEM_CLOSED && !labels_in)
+        return fail(SVX_E_PAYLOAD, "closed-set grid requires per-point labels");
+    if (kind == SVX_SEM_OPEN && !feats_in)
+        return fail(SVX_E_PAYLOAD, "open-set grid requires per-point features");
+    if (n < 0) return fail(SVX_E_INPUT, "negative point count");
+    if (n >= (int64_t)INT_MAX) return fail(SVX_E_INPUT, "point count exceeds 2^31-1");
+    if (n == 0) {
+        m->frames++;
+        if (rep) *rep = r;
+        return SVX_OK;
+    }
+    SVX_CUDA(cudaEventRecord(m->ev0, s));
+    const void* pts;
+    const void* feats = nullptr;
+    const void* labv = nullptr;
+    SVX_TRY(stage_in(pts_in, (size_t)n * 3 * (pts_f64 ? 8 : 4), m->in_pts, s, &pts));
+    if (kind == SVX_SEM_CLOSED)
+        SVX_TRY(stage_in(labels_in, (size_t)n * 4, m->in_lab, s, &labv));
+    if (kind == SVX_SEM_OPEN)
+        SVX_TRY(stage_in(feats_in, (size_t)n * m->payload_d * (feats_f64 ? 8 : 4), m->in_feat, s,
+                         &feats));
+    const int32_t* labels = (const int32_t*)labv;
+
+    SVX_TRY(ensure(m->ray, sizeof(double4) * n, s));
+    SVX_TRY(ensure(m->cnt, sizeof(int) * n, s));
+    SVX_TRY(ensure(m->off, sizeof(long long) * (n + 1), s));
+
+    FrameCtr* hc = m->h_ctr;
+    memset(hc, 0, sizeof(FrameCtr));
+    for (int a = 0; a < 3; ++a) {
+        hc->bbox_min[a] = LLONG_MAX;
+        hc->bbox_max[a] = LLONG_MIN;
+    }
+    FrameCtr* dc = ptr<FrameCtr>(m->ctr);
+    SVX_CUDA(cudaMemcpyAsync(dc, hc, sizeof(FrameCtr), cudaMemcpyHostToDevice, s));
+
+    // K1a: masks, ray setup, row counts, bbox
+    SVX_TRY(launch_count(m, pts, pts_f64, n, pp, labels, feats, feats_f64, s));
+    size_t tmp = 0;
+    SVX_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, ptr<int>(m->cnt), ptr<long long>(m->off),
+                                           (int)n, s));
+    SVX_TRY(ensure(m->cubtmp, tmp, s));
+    SVX_CUDA(cub::DeviceScan::ExclusiveSum(m->cubtmp.p, tmp, ptr<int>(m->cnt),
+                                           ptr<long long>(m->off), (int)n, s));
+    count_launch();
+    SVX_CUDA(cudaMemcpyAsync(hc, dc, sizeof(FrameCtr), cudaMemcpyDeviceToHost, s));
+    SVX_CUDA(cudaStreamSynchronize(s));
+
+    if (hc->err_budget)
+        return fail(SVX_E_INTERNAL, "ray band exceeds step budget; shrink max_range or grow voxels");
+    r.skipped_nonfinite = (int64_t)hc->nonfinite;
+    r.skipped_range = (int64_t)hc->range;
+    r.skipped_degenerate = (int64_t)hc->degenerate;
+    r.skipped_bad_label = (int64_t)hc->bad_label;
+    r.points_used = (int64_t)hc->used;
+    r.band_hits = (int64_t)hc->band_hits;
+    const int64_t R = (int64_t)hc->rows;
+    if (R == 0) {
+        SVX_CUDA(cudaEventRecord(m->ev1, s));
+        SVX_CUDA(cudaEventSynchronize(m->ev1));
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, m->ev0, m->ev1);
+        r.kernel_ms = ms;
+        m->frames++;
+        if (rep) *rep = r;
+        return SVX_OK;
+    }
+    if (R >= (int64_t)INT_MAX) return fail(SVX_E_INPUT, "band rows per frame exceed 2^31-1");
+    long long ext[3];
+    for (int a = 0; a < 3; ++a) ext[a] = hc->bbox_max[a] - hc->bbox_min[a];
+    if (std::max(ext[0], std::max(ext[1], ext[2])) >= (1LL << kPackBits))
+        return fail(SVX_E_INTERNAL,
+                    "frame voxel extent exceeds 2^21 per axis; shrink max_range or grow voxels");
+    for (int a = 0; a < 3; ++a)
+        if (llabs(hc->bbox_min[a]) >= kCoordLimit || llabs(hc->bbox_max[a]) >= kCoordLimit)
+            return fail(SVX_E_RANGE, "voxel coordinate beyond +/-2^30 addressable range");
+    KeyPack kp;
+    for (int a = 0; a < 3; ++a) kp.mn[a] = (int)hc->bbox_min[a];
+    const int bx = bitlen(ext[0]), by = bitlen(ext[1]), bz = bitlen(ext[2]);
+    kp.bz = bz;
+    kp.byz = by + bz;
+    kp.nbits = bx + by + bz;
+
+    // K1b: rows in (point, step) order
+    SVX_TRY(ensure(m->keys0, 8 * R, s));
+    SVX_TRY(ensure(m->keys1, 8 * R, s));
+    SVX_TRY(ensure(m->rid0, 4 * R, s));
+    SVX_TRY(ensure(m->rid1, 4 * R, s));
+    SVX_TRY(launch_fill(m, n, pp, kp, s));
+
+    // K2: stable sort by voxel key -> (voxel, point, step) order
+    unsigned long long* skeys = ptr<unsigned long long>(m->keys0);
+    m->srid = ptr<int>(m->rid0);
+    if (kp.nbits > 0) {
+        cub::DoubleBuffer<unsigned long long> dk(ptr<unsigned long long>(m->keys0),
+                                                 ptr<unsigned long long>(m->keys1));
+        cub::DoubleBuffer<int> dv(ptr<int>(m->rid0), ptr<int>(m->rid1));
+        SVX_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, (int)R, 0, kp.nbits, s));
+        SVX_TRY(ensure(m->cubtmp, tmp, s));
+        SVX_CUDA(cub::DeviceRadixSort::SortPairs(m->cubtmp.p, tmp, dk, dv, (int)R, 0, kp.nbits, s));
+        count_launch();
+        skeys = dk.Current();
+        m->srid = dv.Current();
+    }
+
+    // K3: unique voxels and their row runs
+    SVX_TRY(ensure(m->ukeys, 8 * R, s));
+    SVX_TRY(ensure(m->runlen, 4 * R, s));
+    SVX_TRY(ensure(m->gstart, 8 * (R + 1), s));
+    SVX_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, tmp, skeys, ptr<unsigned long long>(m->ukeys),
+                                                ptr<int>(m->runlen), &dc->n_groups, (int)R, s));
+    SVX_TRY(ensure(m->cubtmp, tmp, s));
+    SVX_CUDA(cub::DeviceRunLengthEncode::Encode(m->cubtmp.p, tmp, skeys,
+                                                ptr<unsigned long long>(m->ukeys),
+                                                ptr<int>(m->runlen), &dc->n_groups, (int)R, s));
+    count_launch();
+    SVX_CUDA(cudaMemcpyAsync(&hc->n_groups, &dc->n_groups, sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost, s));
+    SVX_CUDA(cudaStreamSynchronize(s));
+    const int64_t U = (int64_t)hc->n_groups;
+    SVX_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, ptr<int>(m->runlen),
+                                           ptr<long long>(m->gstart), (int)U, s));
+    SVX_TRY(ensure(m->cubtmp, tmp, s));
+    SVX_CUDA(cub::DeviceScan::ExclusiveSum(m->cubtmp.p, tmp, ptr<int>(m->runlen),
+                                           ptr<long long>(m->gstart), (int)U, s));
+    count_launch();
+
+    // capacity for the worst case (every voxel and leaf new)
+    SVX_TRY(reserve_blocks(m, m->nblocks + U, s));
+    SVX_TRY(reserve_voxels(m, m->nvox + U, s));
+    SVX_TRY(ensure(m->gblock, 4 * U, s));
+    SVX_TRY(ensure(m->gvid, 4 * U, s));
+    SVX_TRY(ensure(m->gnew, 4 * U, s));
+    SVX_TRY(ensure(m->grank, 4 * U, s));
+    SVX_TRY(ensure(m->newpos, 4 * U, s));
+    SVX_TRY(ensure(m->newcoord, sizeof(int4) * U, s));
+    SVX_TRY(ensure(m->newfirst, 4 * U, s));
+    SVX_TRY(ensure(m->newfirst2, 4 * U, s));
+    SVX_TRY(ensure(m->neworder, 4 * U, s));
+    SVX_TRY(ensure(m->neworder2, 4 * U, s));
+    SVX_TRY(ensure(m->tmp2id, 4 * U, s));
+    SVX_CUDA(cudaMemsetAsync(m->newfirst.p, 0xFF, 4 * U, s));
+
+    // K4: leaves
+    SVX_TRY(launch_blocks(m, U, kp, s));
+    SVX_CUDA(cudaMemcpyAsync(&hc->n_new_blocks, &dc->n_new_blocks, sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost, s));
+    SVX_CUDA(cudaStreamSynchronize(s));
+    const int64_t nnew = (int64_t)hc->n_new_blocks;
+    if (nnew > 0) {
+        k_iota<<<grid_for(nnew, 256), 256, 0, s>>>(nnew, ptr<unsigned>(m->neworder));
+        SVX_LAUNCHED();
+        SVX_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, ptr<unsigned>(m->newfirst),
+                                                 ptr<unsigned>(m->newfirst2),
+                                                 ptr<unsigned>(m->neworder),
+                                                 ptr<unsigned>(m->neworder2), (int)nnew, 0,
+                                                 std::max(1, bitlen(U)), s));
+        SVX_TRY(ensure(m->cubtmp, tmp, s));
+        SVX_CUDA(cub::DeviceRadixSort::SortPairs(m->cubtmp.p, tmp, ptr<unsigned>(m->newfirst),
+                                                 ptr<unsigned>(m->newfirst2),
+                                                 ptr<unsigned>(m->neworder),
+                                                 ptr<unsigned>(m->neworder2), (int)nnew, 0,
+                                                 std::max(1, bitlen(U)), s));
+        count_launch();
+        SVX_TRY(launch_assign_blocks(m, nnew, ptr<unsigned>(m->neworder2), s));
+        m->nblocks += nnew;
+    }
+    // voxels: lookup, first-occurrence ids for new ones, activation
+    SVX_TRY(launch_resolve(m, U, kp, s));
+    SVX_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, ptr<int>(m->gnew), ptr<int>(m->grank),
+                                           (int)U, s));
+    SVX_TRY(ensure(m->cubtmp, tmp, s));
+    SVX_CUDA(cub::DeviceScan::ExclusiveSum(m->cubtmp.p, tmp, ptr<int>(m->gnew), ptr<int>(m->grank),
+                                           (int)U, s));
+    count_launch();
+    SVX_TRY(launch_activate(m, U, kp, s));
+
+    // K5/K6: fused update
+    SVX_TRY(launch_update(m, U, kp, pp, labels, feats, feats_f64, s));
+
+    SVX_CUDA(cudaMemcpyAsync(hc, dc, sizeof(FrameCtr), cudaMemcpyDeviceToHost, s));
+    SVX_CUDA(cudaEventRecord(m->ev1, s));
+    SVX_CUDA(cudaEventSynchronize(m->ev1));
+    float ms = 0.f;
+    SVX_CUDA(cudaEventElapsedTime(&ms, m->ev0, m->ev1));
+    m->nvox += (int64_t)hc->n_new_voxels;
+    m->frames++;
+    r.touched_voxels = U;
+    r.new_blocks = nnew;
+    r.new_voxels = (int64_t)hc->n_new_voxels;
+    r.kernel_ms = ms;
+    if (rep) *rep = r;
+    return SVX_OK;
+}
+
+// Output staging: device pointers are written directly; host outputs go
+// through device scratch and are copied back at the end of the call.
+struct OutStage {
+    DevBuf buf;
+    void* user = nullptr;
+    size_t bytes = 0;
+    bool host = false;
+};
+
+svx_status out_prepare(OutStage& o, void* user, size_t bytes, cudaStream_t s, void** dev) {
+    o.user = user;
+    o.bytes = bytes;
+    if (!user || bytes == 0) {
+        *dev = user;
+        return SVX_OK;
+    }
+    if (is_device_ptr(user)) {
+        *dev = user;
+        return SVX_OK;
+    }
+    o.host = true;
+    SVX_TRY(ensure(o.buf, bytes, s));
+    *dev = o.buf.p;
+    return SVX_OK;
+}
+
+svx_status out_finish(OutStage& o, cudaStream_t s) {
+    if (o.host && o.user && o.bytes) {
+        SVX_CUDA(cudaMemcpyAsync(o.user, o.buf.p, o.bytes, cudaMemcpyDeviceToHost, s));
+    }
+    return SVX_OK;
+}
+
+void out_release(OutStage* o, int n) {
+    for (int i = 0; i < n; ++i) release(o[i].buf);
+}
+
+svx_status set_device(const svx_map* m) {
+    SVX_CUDA(cudaSetDevice(m->cfg.device));
+    return SVX_OK;
+}
+
+}  // namespace
+}  // namespace svx
+
+using namespace svx;
+
+extern "C" {
+
+const char* svx_last_error(void) { return g_error.c_str(); }
+int32_t svx_abi_version(void) { return SVX_ABI_VERSION; }
+int64_t svx_kernel_launches(void) { return g_launches.load(); }
+
+svx_status svx_create(const svx_config* cfg, svx_map** out) {
+    if (!cfg || !out) return fail(SVX_E_INPUT, "null argument");
+    *out = nullptr;
+    if (!(cfg->voxel_size > 0)) return fail(SVX_E_CONFIG, "voxel_size must be positive");
+    if (!(cfg->truncation > 0)) return fail(SVX_E_CONFIG, "truncation must be positive");
+    if (!(cfg->max_range > 0)) return fail(SVX_E_CONFIG, "max_range must be positive");
+    if (cfg->weight_fn != 0 && cfg->weight_fn != 1) return fail(SVX_E_CONFIG, "weight_fn must be 0 or 1");
+    if (cfg->sem_kind == SVX_SEM_CLOSED && cfg->num_classes < 1)
+        return fail(SVX_E_CONFIG, "num_classes must be >= 1");
+    if (cfg->sem_kind == SVX_SEM_OPEN && cfg->feature_dim < 1)
+        return fail(SVX_E_CONFIG, "feature_dim must be >= 1");
+    if (cfg->sem_kind < 0 || cfg->sem_kind > 2) return fail(SVX_E_CONFIG, "unknown semantic kind");
+    cudaError_t e = cudaSetDevice(cfg->device);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(SVX_E_CUDA, std::string("cudaSetDevice failed: ") + cudaGetErrorString(e));
+    }
+    svx_map* m = new svx_map();
+    m->cfg = *cfg;
+    m->payload_d = cfg->sem_kind == SVX_SEM_CLOSED ? cfg->num_classes
+                   : cfg->sem_kind == SVX_SEM_OPEN ? cfg->feature_dim : 0;
+    cudaStream_t s = 0;
+    svx_status st = SVX_OK;
+    auto bail = [&](svx_status code) {
+        svx_destroy(m);
+        return code;
+    };
+    if (cudaMallocHost((void**)&m->h_ctr, sizeof(FrameCtr)) != cudaSuccess) {
+        cudaGetLastError();
+        return bail(fail(SVX_E_CUDA, "pinned allocation failed"));
+    }
+    if ((st = ensure(m->ctr, sizeof(FrameCtr), s)) != SVX_OK) return bail(st);
+    if (cudaEventCreate(&m->ev0) != cudaSuccess || cudaEventCreate(&m->ev1) != cudaSuccess) {
+        cudaGetLastError();
+        return bail(fail(SVX_E_CUDA, "event creation failed"));
+    }
+    int64_t rb = cfg->reserve_blocks > 0 ? cfg->reserve_blocks : 1024;
+    int64_t rv = cfg->reserve_voxels > 0 ? cfg->reserve_voxels : 65536;
+    if ((st = reserve_blocks(m, rb, s)) != SVX_OK) return bail(st);
+    if ((st = reserve_voxels(m, rv, s)) != SVX_OK) return bail(st);
+    if (cudaStreamSynchronize(s) != cudaSuccess) {
+        cudaGetLastError();
+        return bail(fail(SVX_E_CUDA, "initial allocation failed"));
+    }
+    *out = m;
+    return SVX_OK;
+}
+
+svx_status svx_destroy(svx_map* m) {
+    if (!m) return SVX_OK;
+    cudaSetDevice(m->cfg.device);
+    DevBuf* bufs[] = {&m->hash, &m->bcoord, &m->bmask, &m->bslot, &m->vd, &m->vw, &m->s0, &m->s1,
+                      &m->in_pts, &m->in_lab, &m->in_feat, &m->ray, &m->cnt, &m->off, &m->keys0,
+                      &m->keys1, &m->rid0, &m->rid1, &m->ukeys, &m->runlen, &m->gstart,
+                      &m->gblock, &m->gvid, &m->gnew, &m->grank, &m->newpos, &m->newcoord,
+                      &m->newfirst, &m->newfirst2, &m->neworder, &m->neworder2, &m->tmp2id,
+                      &m->cubtmp, &m->ctr, &m->act_cnt, &m->act_off, &m->act_vid, &m->act_coord,
+                      &m->q_buf, &m->out_buf};
+    for (DevBuf* b : bufs) release(*b);
+    if (m->h_ctr) cudaFreeHost(m->h_ctr);
+    if (m->ev0) cudaEventDestroy(m->ev0);
+    if (m->ev1) cudaEventDestroy(m->ev1);
+    delete m;
+    return SVX_OK;
+}
+
+svx_status svx_integrate(svx_map* m, const void* points, int32_t points_dtype, int64_t n,
+                         const double pose[16], const int32_t* labels, const void* feats,
+                         int32_t feats_dtype, void* stream, svx_report* report) {
+    if (!m || !pose || (n > 0 && !points)) return fail(SVX_E_INPUT, "null argument");
+    SVX_TRY(set_device(m));
+    PoseParams pp;
+    for (int r = 0; r < 3; ++r) {
+        for (int c = 0; c < 3; ++c) pp.R[3 * r + c] = pose[4 * r + c];
+        pp.t[r] = pose[4 * r + 3];
+    }
+    pp.sensor = 1;
+    return integrate_impl(m, points, points_dtype == SVX_F64, n, pp, labels, feats,
+                          feats_dtype == SVX_F64, (cudaStream_t)stream, report);
+}
+
+svx_status svx_integrate_world(svx_map* m, const void* points_world, int32_t points_dtype,
+                               int64_t n, const double origin[3], const int32_t* labels,
+                               const void* feats, int32_t feats_dtype, void* stream,
+                               svx_report* report) {
+    if (!m || !origin || (n > 0 && !points_world)) return fail(SVX_E_INPUT, "null argument");
+    SVX_TRY(set_device(m));
+    PoseParams pp;
+    memset(&pp, 0, sizeof(pp));
+    pp.R[0] = pp.R[4] = pp.R[8] = 1.0;
+    for (int a = 0; a < 3; ++a) pp.t[a] = origin[a];
+    pp.sensor = 0;
+    return integrate_impl(m, points_world, points_dtype == SVX_F64, n, pp, labels, feats,
+                          feats_dtype == SVX_F64, (cudaStream_t)stream, report);
+}
+
+svx_status svx_stats_get(svx_map* m, svx_stats* out) {
+    if (!m || !out) return fail(SVX_E_INPUT, "null argument");
+    const int64_t te = (int64_t)tsdf_elem(m), se = (int64_t)sem_elem(m);
+    int64_t per_vox = 2 * te + se * m->payload_d * (m->cfg.sem_kind == SVX_SEM_OPEN ? 2 : 1);
+    out->leaf_count = m->nblocks;
+    out->active_voxels = m->nvox;
+    out->resident_bytes = m->nblocks * (int64_t)(sizeof(int4) + 8 * kMaskWords + 4 * kLeafVolume) +
+                          m->nvox * per_vox + m->hcap * (int64_t)sizeof(int4);
+    out->payload_bytes_per_voxel = per_vox;
+    out->frames_integrated = m->frames;
+    out->hash_capacity = m->hcap;
+    out->voxel_capacity = m->vcap;
+    out->block_capacity = m->bcap;
+    return SVX_OK;
+}
+
+svx_status svx_active_count(svx_map* m, int64_t* count) {
+    if (!m || !count) return fail(SVX_E_INPUT, "null argument");
+    *count = m->nvox;
+    return SVX_OK;
+}
+
+svx_status svx_export_active(svx_map* m, int64_t capacity, int64_t* coords, void* d, void* w,
+                             void* sem0, void* sem1, void* stream) {
+    if (!m) return fail(SVX_E_INPUT, "null argument");
+    SVX_TRY(set_device(m));
+    cudaStream_t s = (cudaStream_t)stream;
+    int64_t count = 0;
+    SVX_TRY(build_active_list(m, &count, s));
+    if (capacity < count) return fail(SVX_E_INPUT, "output capacity smaller than active count");
+    const size_t te = tsdf_elem(m), se = sem_elem(m);
+    OutStage o[5];
+    void *dc, *dd, *dw, *ds0, *ds1;
+    svx_status st = SVX_OK;
+    if ((st = out_prepare(o[0], coords, 24 * count, s, &dc)) ||
+        (st = out_prepare(o[1], d, te * count, s, &dd)) ||
+        (st = out_prepare(o[2], w, te * count, s, &dw)) ||
+        (st = out_prepare(o[3], sem0, se * m->payload_d * count, s, &ds0)) ||
+        (st = out_prepare(o[4], m->cfg.sem_kind == SVX_SEM_OPEN ? sem1 : nullptr,
+                          se * m->payload_d * count, s, &ds1)) ||
+        (st = launch_export(m, count, (int64_t*)dc, dd, dw, ds0, ds1, s))) {
+        out_release(o, 5);
+        return st;
+    }
+    for (int i = 0; i < 5 && st == SVX_OK; ++i) st = out_finish(o[i], s);
+    cudaError_t e = cudaStreamSynchronize(s);
+    out_release(o, 5);
+    if (st) return st;
+    if (e != cudaSuccess) return fail(SVX_E_CUDA, std::string("export: ") + cudaGetErrorString(e));
+    return SVX_OK;
+}
+
+svx_status svx_probe(svx_map* m, const int64_t* coords, int64_t cnt, void* d, void* w, void* sem0,
+                     void* sem1, uint8_t* active, void* stream) {
+    if (!m || (cnt > 0 && !coords)) return fail(SVX_E_INPUT, "null argument");
+    SVX_TRY(set_device(m));
+    cudaStream_t s = (cudaStream_t)stream;
+    if (cnt == 0) return SVX_OK;
+    DevBuf cstage;
+    const void* dcoords = nullptr;
+    svx_status st = stage_in(coords, 24 * cnt, cstage, s, &dcoords);
+    if (st) return st;
+    const size_t te = tsdf_elem(m), se = sem_elem(m);
+    OutStage o[5];
+    void *dd, *dw, *ds0, *ds1, *da;
+    if ((st = out_prepare(o[0], d, te * cnt, s, &dd)) ||
+        (st = out_prepare(o[1], w, te * cnt, s, &dw)) ||
+        (st = out_prepare(o[2], sem0, se * m->payload_d * cnt, s, &ds0)) ||
+        (st = out_prepare(o[3], m->cfg.sem_kind == SVX_SEM_OPEN ? sem1 : nullptr,
+                          se * m->payload_d * cnt, s, &ds1)) ||
+        (st = out_prepare(o[4], active, cnt, s, &da)) ||
+        (st = launch_probe(m, (const int64_t*)dcoords, cnt, dd, dw, ds0, ds1, (uint8_t*)da, s))) {
+        out_release(o, 5);
+        release(cstage);
+        return st;
+    }
+    for (int i = 0; i < 5 && st == SVX_OK; ++i) st = out_finish(o[i], s);
+    cudaError_t e = cudaStreamSynchronize(s);
+    out_release(o, 5);
+    release(cstage);
+    if (st) return st;
+    if (e != cudaSuccess) return fail(SVX_E_CUDA, std::string("probe: ") + cudaGetErrorString(e));
+    return SVX_OK;
+}
+
+svx_status svx_query_cosine(svx_map* m, const double* query, int64_t capacity, double* sims,
+                            void* stream) {
+    if (!m || !query) return fail(SVX_E_INPUT, "null argument");
+    if (m->cfg.sem_kind != SVX_SEM_OPEN)
+        return fail(SVX_E_PAYLOAD, "embedding query needs an open-set map");
+    SVX_TRY(set_device(m));
+    cudaStream_t s = (cudaStream_t)stream;
+    const int D = m->payload_d;
+    // query norm on the host (D doubles)
+    double* hq = new double[D];
+    if (is_device_ptr(query)) {
+        cudaError_t e = cudaMemcpy(hq, query, 8 * D, cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) { delete[] hq; return fail(SVX_E_CUDA, cudaGetErrorString(e)); }
+    } else {
+        memcpy(hq, query, 8 * D);
+    }
+    double nn = 0.0;
+    for (int c = 0; c < D; ++c) nn += hq[c] * hq[c];
+    const double qn = sqrt(nn);
+    if (qn == 0.0) { delete[] hq; return fail(SVX_E_INTERNAL, "zero-norm label embedding"); }
+    svx_status st = ensure(m->q_buf, 8 * D, s);
+    if (st) { delete[] hq; return st; }
+    cudaError_t e = cudaMemcpyAsync(m->q_buf.p, hq, 8 * D, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    delete[] hq;
+    if (e != cudaSuccess) return fail(SVX_E_CUDA, cudaGetErrorString(e));
+    int64_t count = 0;
+    SVX_TRY(build_active_list(m, &count, s));
+    if (capacity < count) return fail(SVX_E_INPUT, "output capacity smaller than active count");
+    OutStage o;
+    void* ds;
+    if ((st = out_prepare(o, sims, 8 * count, s, &ds)) ||
+        (st = launch_cosine(m, count, ptr<double>(m->q_buf), qn, (double*)ds, s)) ||
+        (st = out_finish(o, s))) {
+        release(o.buf);
+        return st;
+    }
+    e = cudaStreamSynchronize(s);
+    release(o.buf);
+    if (e != cudaSuccess) return fail(SVX_E_CUDA, std::string("query: ") + cudaGetErrorString(e));
+    return SVX_OK;
+}
+
+svx_status svx_classify(svx_map* m, const double* emb, int32_t k, double temperature,
+                        double confidence_threshold, int64_t capacity, int32_t* labels,
+                        double* best, double* sims, void* stream) {
+    if (!m || !emb || !labels || !best || k < 1) return fail(SVX_E_INPUT, "null argument");
+    if (m->cfg.sem_kind != SVX_SEM_OPEN)
+        return fail(SVX_E_PAYLOAD, "classification needs an open-set map");
+    SVX_TRY(set_device(m));
+    cudaStream_t s = (cudaStream_t)stream;
+    const int D = m->payload_d;
+    const size_t eb = (size_t)8 * D * k;
+    double* he = new double[(size_t)D * k + k];
+    if (is_device_ptr(emb)) {
+        cudaError_t e = cudaMemcpy(he, emb, eb, cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) { delete[] he; return fail(SVX_E_CUDA, cudaGetErrorString(e)); }
+    } else {
+        memcpy(he, emb, eb);
+    }
+    double* en = he + (size_t)D * k;
+    for (int j = 0; j < k; ++j) {
+        double nn = 0.0;
+        for (int c = 0; c < D; ++c) nn += he[(size_t)j * D + c] * he[(size_t)j * D + c];
+        en[j] = sqrt(nn);
+        if (en[j] == 0.0) { delete[] he; return fail(SVX_E_INTERNAL, "zero-norm label embedding"); }
+    }
+    svx_status st = ensure(m->q_buf, eb + 8 * k, s);
+    if (st) { delete[] he; return st; }
+    cudaError_t e = cudaMemcpyAsync(m->q_buf.p, he, eb + 8 * k, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    delete[] he;
+    if (e != cudaSuccess) return fail(SVX_E_CUDA, cudaGetErrorString(e));
+    int64_t count = 0;
+    SVX_TRY(build_active_list(m, &count, s));
+    if (capacity < count) return fail(SVX_E_INPUT, "output capacity smaller than active count");
+    OutStage o[3];
+    void *dl, *db, *dsm;
+    if ((st = out_prepare(o[0], labels, 4 * count, s, &dl)) ||
+        (st = out_prepare(o[1], best, 8 * count, s, &db)) ||
+        (st = out_prepare(o[2], sims, 8 * count * k, s, &dsm)) ||
+        (st = launch_classify(m, count, ptr<double>(m->q_buf), ptr<double>(m->q_buf) + (size_t)D * k,
+                              k, temperature, confidence_threshold, (int32_t*)dl, (double*)db,
+                              (double*)dsm, s))) {
+        out_release(o, 3);
+        return st;
+    }
+    for (int i = 0; i < 3 && st == SVX_OK; ++i) st = out_finish(o[i], s);
+    e = cudaStreamSynchronize(s);
+    out_release(o, 3);
+    if (st) return st;
+    if (e != cudaSuccess) return fail(SVX_E_CUDA, std::string("classify: ") + cudaGetErrorString(e));
+    return SVX_OK;
+}
+
+svx_status svx_label_map(svx_map* m, int32_t mode, int64_t capacity, int32_t* labels,
+                         void* stream) {
+    if (!m || !labels) return fail(SVX_E_INPUT, "null argument");
+    if (m->cfg.sem_kind != SVX_SEM_CLOSED)
+        return fail(SVX_E_PAYLOAD, "label map needs a closed-set map");
+    SVX_TRY(set_device(m));
+    cudaStream_t s = (cudaStream_t)stream;
+    int64_t count = 0;
+    SVX_TRY(build_active_list(m, &count, s));
+    if (capacity < count) return fail(SVX_E_INPUT, "output capacity smaller than active count");
+    OutStage o;
+    void* dl;
+    svx_status st;
+    if ((st = out_prepare(o, labels, 4 * count, s, &dl)) ||
+        (st = launch_label_map(m, count, mode, (int32_t*)dl, s)) || (st = out_finish(o, s))) {
+        release(o.buf);
+        return st;
+    }
+    cudaError_t e = cudaStreamSynchronize(s);
+    release(o.buf);
+    if (e != cudaSuccess) return fail(SVX_E_CUDA, std::string("label map: ") + cudaGetErrorString(e));
+    return SVX_OK;
+}
+
+}  // extern "C"

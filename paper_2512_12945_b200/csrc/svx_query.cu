@@ -1,0 +1,384 @@
+// svx_query.cu -- voxel and label queries (K7, K8 v1).
+//
+// Active enumeration reproduces GridCore.active_slots (_core.pyx:424-444):
+// leaves in allocation order, slots ascending.  Reads never allocate.
+#include <math.h>
+
+#include <cub/cub.cuh>
+
+#include "svx_internal.cuh"
+
+namespace svx {
+namespace {
+
+__global__ void k_popc(int64_t nblocks, const unsigned long long* __restrict__ bmask,
+                       int* __restrict__ cnt) {
+    int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= nblocks) return;
+    int c = 0;
+#pragma unroll
+    for (int w = 0; w < kMaskWords; ++w) c += __popcll(bmask[b * kMaskWords + w]);
+    cnt[b] = c;
+}
+
+// One warp per leaf: lanes cover 32 slots at a time, ballot/popc give ranks.
+__global__ void k_list(int64_t nblocks, const unsigned long long* __restrict__ bmask,
+                       const int* __restrict__ bslot, const int4* __restrict__ bcoord,
+                       const long long* __restrict__ off, int* __restrict__ act_vid,
+                       long long* __restrict__ act_coord) {
+    int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (b >= nblocks) return;
+    long long pos = off[b];
+    int4 bc = bcoord[b];
+    for (int half = 0; half < 16; ++half) {
+        unsigned long long word = bmask[b * kMaskWords + (half >> 1)];
+        unsigned bits = (unsigned)(word >> (32 * (half & 1)));
+        if (!bits) continue;
+        if ((bits >> lane) & 1u) {
+            int slot = half * 32 + lane;
+            long long p = pos + __popc(bits & ((1u << lane) - 1u));
+            act_vid[p] = bslot[b * kLeafVolume + slot];
+            act_coord[3 * p] = ((long long)bc.x << kLeafLog2) + ((slot >> 6) & 7);
+            act_coord[3 * p + 1] = ((long long)bc.y << kLeafLog2) + ((slot >> 3) & 7);
+            act_coord[3 * p + 2] = ((long long)bc.z << kLeafLog2) + (slot & 7);
+        }
+        pos += __popc(bits);
+    }
+}
+
+template <class T>
+__global__ void k_gather_rows(int64_t count, int width, const int* __restrict__ act_vid,
+                              const T* __restrict__ src, T* __restrict__ dst) {
+    int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t total = count * width;
+    for (; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
+        int64_t i = idx / width;
+        int c = (int)(idx - i * width);
+        dst[idx] = src[(int64_t)act_vid[i] * width + c];
+    }
+}
+
+__global__ void k_copy_coords(int64_t count, const long long* __restrict__ src,
+                              long long* __restrict__ dst) {
+    int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx < 3 * count) dst[idx] = src[idx];
+}
+
+__global__ void k_probe_vid(int64_t cnt, const long long* __restrict__ coords,
+                            const int4* __restrict__ table, int64_t mask,
+                            const int* __restrict__ bslot, int* __restrict__ vid_out,
+                            uint8_t* __restrict__ active) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= cnt) return;
+    long long x = coords[3 * i], y = coords[3 * i + 1], z = coords[3 * i + 2];
+    int blk = hash_find(table, mask, (int)(x >> kLeafLog2), (int)(y >> kLeafLog2),
+                        (int)(z >> kLeafLog2));
+    int vid = -1;
+    if (blk >= 0) {
+        int slot = (int)(((x & 7) << 6) | ((y & 7) << 3) | (z & 7));
+        vid = bslot[(int64_t)blk * kLeafVolume + slot];
+    }
+    vid_out[i] = vid;
+    if (active) active[i] = vid >= 0;
+}
+
+template <class T>
+__global__ void k_probe_rows(int64_t cnt, int width, const int* __restrict__ vid,
+                             const T* __restrict__ src, T bg, T* __restrict__ dst) {
+    int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t total = cnt * width;
+    for (; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
+        int64_t i = idx / width;
+        int c = (int)(idx - i * width);
+        int v = vid[i];
+        dst[idx] = v >= 0 ? src[(int64_t)v * width + c] : bg;
+    }
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// cosine_to_embeddings (gaussian.py:158-170) against one query; one warp per voxel.
+template <class TS>
+__global__ void k_cosine(int64_t count, int D, const int* __restrict__ act_vid,
+                         const TS* __restrict__ mean, const double* __restrict__ q, double qn,
+                         double* __restrict__ sims) {
+    int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (i >= count) return;
+    const TS* row = mean + (int64_t)act_vid[i] * D;
+    double dot = 0.0, nn = 0.0;
+    for (int c = lane; c < D; c += 32) {
+        double mv = (double)row[c];
+        dot += mv * q[c];
+        nn += mv * mv;
+    }
+    dot = warp_sum(dot);
+    nn = warp_sum(nn);
+    if (lane == 0) {
+        double mn = sqrt(nn);
+        sims[i] = mn == 0.0 ? NAN : dot / (mn * qn);
+    }
+}
+
+// classify_means (gaussian.py:132-155), weights = TSDF weight.  One warp per
+// voxel: similarities are warp-reduced dot products; lane (j % 32) caches
+// similarity j (up to 32*kCache of them) for the softmax pass.
+constexpr int kCache = 8;
+
+template <class TS, class TD>
+__global__ void k_classify(int64_t count, int D, int k, const int* __restrict__ act_vid,
+                           const TS* __restrict__ mean, const TD* __restrict__ vw,
+                           const double* __restrict__ emb, const double* __restrict__ en,
+                           double tau, double tp, int32_t* __restrict__ labels,
+                           double* __restrict__ best, double* __restrict__ sims_out) {
+    int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (i >= count) return;
+    const int vid = act_vid[i];
+    const TS* row = mean + (int64_t)vid * D;
+    double nn = 0.0;
+    for (int c = lane; c < D; c += 32) {
+        double mv = (double)row[c];
+        nn += mv * mv;
+    }
+    nn = warp_sum(nn);
+    const double mn = sqrt(nn);
+    const double wgt = (double)vw[vid];
+    const bool ok = mn != 0.0 && wgt > 0.0;
+    double cache[kCache];
+    double lmax = -INFINITY;
+    for (int j = 0; j < k; ++j) {
+        const double* e = emb + (int64_t)j * D;
+        double dot = 0.0;
+        for (int c = lane; c < D; c += 32) dot += (double)row[c] * e[c];
+        dot = warp_sum(dot);
+        double sj = mn == 0.0 ? NAN : dot / (mn * en[j]);
+        if (sims_out && lane == 0) sims_out[i * k + j] = sj;
+        if (lane == (j & 31) && (j >> 5) < kCache) cache[j >> 5] = sj;
+        double lj = sj / tau;
+        lmax = lj > lmax ? lj : lmax;
+    }
+    if (!ok) {
+        if (lane == 0) { labels[i] = 0; best[i] = 0.0; }
+        return;
+    }
+    // softmax: e_j = exp(l_j - lmax); label = first j attaining max e_j (np.argmax on probs)
+    double den = 0.0;
+    int arg = 0x7fffffff;
+    double emax = -1.0;
+    for (int j0 = 0; j0 < k; j0 += 32) {
+        int j = j0 + lane;
+        double ej = 0.0;
+        if (j < k) {
+            double sj;
+            if ((j >> 5) < kCache) {
+                sj = cache[j >> 5];
+            } else {
+                const double* e = emb + (int64_t)j * D;
+                double dot = 0.0;
+                for (int c = 0; c < D; ++c) dot += (double)row[c] * e[c];
+                sj = dot / (mn * en[j]);
+            }
+            ej = exp(sj / tau - lmax);
+            den += ej;
+            if (ej > emax) { emax = ej; arg = j; }
+        }
+    }
+    den = warp_sum(den);
+    for (int o = 16; o > 0; o >>= 1) {
+        double oe = __shfl_xor_sync(0xffffffffu, emax, o);
+        int oa = __shfl_xor_sync(0xffffffffu, arg, o);
+        if (oe > emax || (oe == emax && oa < arg)) { emax = oe; arg = oa; }
+    }
+    if (lane == 0) {
+        double top = emax / den;
+        labels[i] = top < tp ? 0 : arg + 1;
+        best[i] = top;
+    }
+}
+
+template <class TC>
+__global__ void k_label_map(int64_t count, int C, int mode, const int* __restrict__ act_vid,
+                            const TC* __restrict__ counts, int32_t* __restrict__ labels) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const TC* row = counts + (int64_t)act_vid[i] * C;
+    TC bestv = row[0];
+    int arg = 0;
+    double total = (double)row[0];
+    for (int c = 1; c < C; ++c) {
+        TC v = row[c];
+        total += (double)v;
+        if (v > bestv) { bestv = v; arg = c; }
+    }
+    labels[i] = (mode == 1 && !(total > 0.0)) ? 0 : arg + 1;
+}
+
+}  // namespace
+
+svx_status build_active_list(svx_map* m, int64_t* count, cudaStream_t s) {
+    const int64_t nb = m->nblocks;
+    *count = m->nvox;
+    if (nb == 0 || m->nvox == 0) return SVX_OK;
+    SVX_TRY(ensure(m->act_cnt, sizeof(int) * nb, s));
+    SVX_TRY(ensure(m->act_off, sizeof(long long) * nb, s));
+    SVX_TRY(ensure(m->act_vid, sizeof(int) * m->nvox, s));
+    SVX_TRY(ensure(m->act_coord, sizeof(long long) * 3 * m->nvox, s));
+    const int T = 256;
+    k_popc<<<grid_for(nb, T), T, 0, s>>>(nb, ptr<unsigned long long>(m->bmask), ptr<int>(m->act_cnt));
+    SVX_LAUNCHED();
+    size_t tmp = 0;
+    SVX_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, ptr<int>(m->act_cnt),
+                                           ptr<long long>(m->act_off), (int)nb, s));
+    SVX_TRY(ensure(m->cubtmp, tmp, s));
+    SVX_CUDA(cub::DeviceScan::ExclusiveSum(m->cubtmp.p, tmp, ptr<int>(m->act_cnt),
+                                           ptr<long long>(m->act_off), (int)nb, s));
+    count_launch();
+    k_list<<<grid_for(nb * 32, T), T, 0, s>>>(nb, ptr<unsigned long long>(m->bmask),
+                                             ptr<int>(m->bslot), ptr<int4>(m->bcoord),
+                                             ptr<long long>(m->act_off), ptr<int>(m->act_vid),
+                                             ptr<long long>(m->act_coord));
+    SVX_LAUNCHED();
+    return SVX_OK;
+}
+
+template <class T>
+static svx_status gather_rows(int64_t count, int width, const int* vid, const void* src, void* dst,
+                              cudaStream_t s) {
+    if (!dst || count == 0) return SVX_OK;
+    int64_t total = count * width;
+    int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 32);
+    k_gather_rows<T><<<blocks, 256, 0, s>>>(count, width, vid, (const T*)src, (T*)dst);
+    SVX_LAUNCHED();
+    return SVX_OK;
+}
+
+static svx_status gather_typed(int f64, int64_t count, int width, const int* vid, const void* src,
+                               void* dst, cudaStream_t s) {
+    return f64 ? gather_rows<double>(count, width, vid, src, dst, s)
+               : gather_rows<float>(count, width, vid, src, dst, s);
+}
+
+svx_status launch_export(svx_map* m, int64_t count, int64_t* coords, void* d, void* w, void* sem0,
+                         void* sem1, cudaStream_t s) {
+    if (count == 0) return SVX_OK;
+    const int* vid = ptr<int>(m->act_vid);
+    if (coords) {
+        k_copy_coords<<<grid_for(3 * count, 256), 256, 0, s>>>(count, ptr<long long>(m->act_coord),
+                                                              (long long*)coords);
+        SVX_LAUNCHED();
+    }
+    const int td64 = m->cfg.tsdf_dtype == SVX_F64;
+    SVX_TRY(gather_typed(td64, count, 1, vid, m->vd.p, d, s));
+    SVX_TRY(gather_typed(td64, count, 1, vid, m->vw.p, w, s));
+    if (m->cfg.sem_kind == SVX_SEM_CLOSED) {
+        SVX_TRY(gather_typed(m->cfg.count_dtype == SVX_F64, count, m->payload_d, vid, m->s0.p,
+                             sem0, s));
+    } else if (m->cfg.sem_kind == SVX_SEM_OPEN) {
+        const int s64 = m->cfg.state_dtype == SVX_F64;
+        SVX_TRY(gather_typed(s64, count, m->payload_d, vid, m->s0.p, sem0, s));
+        SVX_TRY(gather_typed(s64, count, m->payload_d, vid, m->s1.p, sem1, s));
+    }
+    return SVX_OK;
+}
+
+template <class T>
+static svx_status probe_rows(int64_t cnt, int width, const int* vid, const void* src, double bg,
+                             void* dst, cudaStream_t s) {
+    if (!dst || cnt == 0) return SVX_OK;
+    int64_t total = cnt * width;
+    int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 32);
+    k_probe_rows<T><<<blocks, 256, 0, s>>>(cnt, width, vid, (const T*)src, (T)bg, (T*)dst);
+    SVX_LAUNCHED();
+    return SVX_OK;
+}
+
+static svx_status probe_typed(int f64, int64_t cnt, int width, const int* vid, const void* src,
+                              double bg, void* dst, cudaStream_t s) {
+    return f64 ? probe_rows<double>(cnt, width, vid, src, bg, dst, s)
+               : probe_rows<float>(cnt, width, vid, src, bg, dst, s);
+}
+
+svx_status launch_probe(svx_map* m, const int64_t* coords, int64_t cnt, void* d, void* w,
+                        void* sem0, void* sem1, uint8_t* active, cudaStream_t s) {
+    if (cnt == 0) return SVX_OK;
+    SVX_TRY(ensure(m->out_buf, sizeof(int) * cnt, s));
+    int* vid = ptr<int>(m->out_buf);
+    if (m->hcap == 0) {
+        SVX_CUDA(cudaMemsetAsync(vid, 0xFF, sizeof(int) * cnt, s));
+        if (active) SVX_CUDA(cudaMemsetAsync(active, 0, cnt, s));
+    } else {
+        k_probe_vid<<<grid_for(cnt, 256), 256, 0, s>>>(cnt, (const long long*)coords,
+                                                       ptr<int4>(m->hash), m->hcap - 1,
+                                                       ptr<int>(m->bslot), vid, active);
+        SVX_LAUNCHED();
+    }
+    const int td64 = m->cfg.tsdf_dtype == SVX_F64;
+    SVX_TRY(probe_typed(td64, cnt, 1, vid, m->vd.p, m->cfg.truncation, d, s));
+    SVX_TRY(probe_typed(td64, cnt, 1, vid, m->vw.p, 0.0, w, s));
+    if (m->cfg.sem_kind == SVX_SEM_CLOSED) {
+        SVX_TRY(probe_typed(m->cfg.count_dtype == SVX_F64, cnt, m->payload_d, vid, m->s0.p, 0.0,
+                            sem0, s));
+    } else if (m->cfg.sem_kind == SVX_SEM_OPEN) {
+        const int s64 = m->cfg.state_dtype == SVX_F64;
+        SVX_TRY(probe_typed(s64, cnt, m->payload_d, vid, m->s0.p, 0.0, sem0, s));
+        SVX_TRY(probe_typed(s64, cnt, m->payload_d, vid, m->s1.p, m->cfg.prior_beta, sem1, s));
+    }
+    return SVX_OK;
+}
+
+svx_status launch_cosine(svx_map* m, int64_t count, const double* q, double qn, double* sims,
+                         cudaStream_t s) {
+    if (count == 0) return SVX_OK;
+    const int T = 256;
+    if (m->cfg.state_dtype == SVX_F64)
+        k_cosine<double><<<grid_for(count * 32, T), T, 0, s>>>(
+            count, m->payload_d, ptr<int>(m->act_vid), ptr<double>(m->s0), q, qn, sims);
+    else
+        k_cosine<float><<<grid_for(count * 32, T), T, 0, s>>>(
+            count, m->payload_d, ptr<int>(m->act_vid), ptr<float>(m->s0), q, qn, sims);
+    SVX_LAUNCHED();
+    return SVX_OK;
+}
+
+template <class TS, class TD>
+static svx_status classify_t(svx_map* m, int64_t count, const double* emb, const double* en, int k,
+                             double tau, double tp, int32_t* labels, double* best, double* sims,
+                             cudaStream_t s) {
+    const int T = 256;
+    k_classify<TS, TD><<<grid_for(count * 32, T), T, 0, s>>>(
+        count, m->payload_d, k, ptr<int>(m->act_vid), ptr<TS>(m->s0), ptr<TD>(m->vw), emb, en,
+        tau, tp, labels, best, sims);
+    SVX_LAUNCHED();
+    return SVX_OK;
+}
+
+svx_status launch_classify(svx_map* m, int64_t count, const double* emb, const double* en, int k,
+                           double tau, double tp, int32_t* labels, double* best, double* sims,
+                           cudaStream_t s) {
+    if (count == 0) return SVX_OK;
+    const bool s64 = m->cfg.state_dtype == SVX_F64, t64 = m->cfg.tsdf_dtype == SVX_F64;
+    if (s64 && t64) return classify_t<double, double>(m, count, emb, en, k, tau, tp, labels, best, sims, s);
+    if (s64) return classify_t<double, float>(m, count, emb, en, k, tau, tp, labels, best, sims, s);
+    if (t64) return classify_t<float, double>(m, count, emb, en, k, tau, tp, labels, best, sims, s);
+    return classify_t<float, float>(m, count, emb, en, k, tau, tp, labels, best, sims, s);
+}
+
+svx_status launch_label_map(svx_map* m, int64_t count, int mode, int32_t* labels, cudaStream_t s) {
+    if (count == 0) return SVX_OK;
+    const int T = 256;
+    if (m->cfg.count_dtype == SVX_F64)
+        k_label_map<double><<<grid_for(count, T), T, 0, s>>>(count, m->payload_d, mode,
+                                                             ptr<int>(m->act_vid), ptr<double>(m->s0), labels);
+    else
+        k_label_map<float><<<grid_for(count, T), T, 0, s>>>(count, m->payload_d, mode,
+                                                            ptr<int>(m->act_vid), ptr<float>(m->s0), labels);
+    SVX_LAUNCHED();
+    return SVX_OK;
+}
+
+}  // namespace svx

@@ -1,0 +1,614 @@
+"""``Mapper``: the drop-in mapping API over the B200 engine.
+
+Mirrors ``semvox_bindings.Mapper`` (pkg/bindings/src/semvox_bindings/__init__.py:58-201):
+flat-config routing and its errors, ``integrate(points, pose, labels=|features=)``
+returning an ``IntegrationReport``, ``query``, ``stats``, ``config`` and
+``grids``.  Host-side work is limited to what the reference does on the host
+before its kernel (frame validation, fusion.py:31-92, 173-224); everything from
+the world transform on runs in libsvx.so on the GPU.  Arrays may be numpy
+arrays (copied by the engine) or CUDA torch tensors (used in place, on torch's
+current stream).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+import hashlib
+import struct
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from ._lib import SEM_CLOSED, SEM_NONE, SEM_OPEN, SVX_F32, SVX_F64, check, lib
+from .config import ClosedSetConfig, EngineConfig, FusionConfig, OpenSetConfig
+from .errors import ConfigError, OutOfRangeError, PayloadMismatchError, UserInputError
+
+KIND_TSDF, KIND_CLOSED, KIND_OPEN = 0, 1, 2   # grid.py:26-28
+KIND_NAMES = {KIND_TSDF: "tsdf", KIND_CLOSED: "closed", KIND_OPEN: "open"}
+COORD_LIMIT = 1 << 30                          # coords.py:41
+LEAF_LOG2, INTERNAL_LOG2 = 3, 4                # config.py:26-27
+_MAGIC = b"SLVG"                               # grid.py:31
+
+_FUSION_KEYS = {f.name for f in dataclasses.fields(FusionConfig)}
+_CLOSED_KEYS = {f.name for f in dataclasses.fields(ClosedSetConfig)}
+_OPEN_KEYS = {f.name for f in dataclasses.fields(OpenSetConfig)}
+_ENGINE_KEYS = {f.name for f in dataclasses.fields(EngineConfig)}
+_MAPPER_KEYS = {"threads", "backend", "map_bounds"}
+
+_ROT_PASS, _ROT_FIX = 1e-4, 1e-3               # fusion.py:27-28
+
+
+@dataclass
+class IntegrationReport:
+    """Per-frame counts (fusion.py:103-117) plus engine extras."""
+
+    points_in: int = 0
+    points_used: int = 0
+    skipped_nonfinite: int = 0
+    skipped_range: int = 0
+    skipped_degenerate: int = 0
+    skipped_bad_label: int = 0
+    band_hits: int = 0
+    touched_voxels: int = 0
+    prep_ms: float = 0.0
+    kernel_ms: float = 0.0
+    new_blocks: int = 0
+    new_voxels: int = 0
+
+    def as_dict(self):
+        return dict(self.__dict__)
+
+
+@dataclass
+class MemoryStats:
+    """grid.py:80-86."""
+
+    leaf_count: int
+    internal_count: int
+    root_entries: int
+    active_voxels: int
+    resident_bytes: int
+
+
+@dataclass
+class TsdfPayload:
+    truncation: float
+    kind: int = KIND_TSDF
+
+
+@dataclass
+class ClosedPayload:
+    cfg: ClosedSetConfig
+    kind: int = KIND_CLOSED
+
+
+@dataclass
+class OpenPayload:
+    cfg: OpenSetConfig
+    kind: int = KIND_OPEN
+
+
+def validate_rotation(R, context: str = "pose"):
+    """Accept within 1e-4 of orthonormal, polar-fix within 1e-3, else reject
+    (fusion.py:31-49)."""
+    R = np.asarray(R, np.float64)
+    if R.shape != (3, 3) or not np.isfinite(R).all():
+        raise UserInputError(f"{context}: rotation block must be finite 3x3")
+    err = float(np.abs(R @ R.T - np.eye(3)).max())
+    if np.linalg.det(R) <= 0:
+        raise UserInputError(f"{context}: rotation determinant not positive (mirrored)")
+    if err <= _ROT_PASS:
+        return R
+    if err <= _ROT_FIX:
+        u, _, vt = np.linalg.svd(R)
+        fixed = u @ vt
+        if np.linalg.det(fixed) <= 0:
+            raise UserInputError(f"{context}: rotation not fixable by polar projection")
+        return fixed
+    raise UserInputError(f"{context}: rotation block off orthonormal by {err:.2e} (> 1e-3)")
+
+
+def _check_pose(pose, frame_id):
+    pose = np.asarray(pose, np.float64)
+    if pose.shape != (4, 4):
+        raise UserInputError(f"pose must be 4x4, got {pose.shape}")
+    if not np.isfinite(pose).all():
+        raise UserInputError("pose contains non-finite values")
+    if not np.allclose(pose[3], (0, 0, 0, 1), atol=1e-9):
+        raise UserInputError("pose bottom row must be [0 0 0 1]")
+    fixed = np.array(pose, np.float64, copy=True, order="C")
+    fixed[:3, :3] = validate_rotation(pose[:3, :3], f"frame {frame_id} pose")
+    return fixed
+
+
+def _is_torch(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
+class _Arg:
+    """A contiguous array handed to the C ABI: numpy (host) or CUDA tensor."""
+
+    def __init__(self, x, kind: str):
+        self.keep = None
+        self.cuda = False
+        if _is_torch(x):
+            import torch
+
+            if kind == "int32":
+                t = x if x.dtype == torch.int32 else x.to(torch.int32)
+                self.code = None
+            elif x.dtype in (torch.float32, torch.float64):
+                t = x
+                self.code = SVX_F64 if x.dtype == torch.float64 else SVX_F32
+            else:
+                t = x.to(torch.float64)
+                self.code = SVX_F64
+            t = t.contiguous()
+            if not t.is_cuda:
+                t = t.numpy()
+                self.keep = t
+                self.ptr = t.ctypes.data if t.size else None
+                self.shape = t.shape
+                return
+            self.keep = t
+            self.cuda = True
+            self.ptr = t.data_ptr() if t.numel() else None
+            self.shape = tuple(t.shape)
+            return
+        if kind == "int32":
+            a = np.ascontiguousarray(x, np.int32)
+            self.code = None
+        else:
+            a = np.asarray(x)
+            if a.dtype not in (np.float32, np.float64):
+                a = a.astype(np.float64)
+            a = np.ascontiguousarray(a)
+            self.code = SVX_F64 if a.dtype == np.float64 else SVX_F32
+        self.keep = a
+        self.ptr = a.ctypes.data if a.size else None
+        self.shape = a.shape
+
+    def finite_host(self):
+        return None if self.cuda else self.keep
+
+
+def _stream_for(args):
+    if any(a is not None and a.cuda for a in args):
+        import torch
+
+        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    return None
+
+
+class Mapper:
+    """One mapping run on one GPU: a TSDF grid plus an optional semantic grid.
+
+    Configuration is one flat mapping (keyword arguments override it), routed
+    by field name exactly like the reference (bindings/__init__.py:77-116).
+    Extra engine keys: ``tsdf_dtype`` ("float64" reference layout, default, or
+    "float32" compact), ``device``, ``reserve_voxels``, ``reserve_blocks``.
+    ``backend`` accepts None/"auto"/"cuda" (there is one engine); ``threads``
+    is validated and has no effect (device parallelism never changes bits).
+    """
+
+    def __init__(self, config=None, /, **overrides):
+        self._handle = None
+        merged = {}
+        if config is not None:
+            merged.update(config)
+        merged.update(overrides)
+        unknown = (set(merged) - _FUSION_KEYS - _CLOSED_KEYS - _OPEN_KEYS - _MAPPER_KEYS
+                   - _ENGINE_KEYS)
+        if unknown:
+            raise ConfigError("unknown config keys: " + ", ".join(sorted(unknown)))
+        threads = merged.pop("threads", 1)
+        if not isinstance(threads, (int, np.integer)) or threads < 1:
+            raise ConfigError(f"threads must be an integer >= 1, got {threads!r}")
+        self._threads = int(threads)
+        backend = merged.pop("backend", None)
+        if backend not in (None, "auto", "cuda"):
+            raise ConfigError(f"unknown backend {backend!r} (expected auto or cuda)")
+        self._map_bounds = merged.pop("map_bounds", None)
+
+        fusion_kw = {k: v for k, v in merged.items() if k in _FUSION_KEYS}
+        closed_kw = {k: v for k, v in merged.items() if k in _CLOSED_KEYS}
+        open_kw = {k: v for k, v in merged.items() if k in _OPEN_KEYS}
+        engine_kw = {k: v for k, v in merged.items() if k in _ENGINE_KEYS}
+        closed = open_set = None
+        if closed_kw.get("num_classes", 0):
+            closed = ClosedSetConfig(**closed_kw)
+        elif closed_kw:
+            raise ConfigError("closed-set keys %s need num_classes >= 1"
+                              % ", ".join(sorted(closed_kw)))
+        if open_kw.get("feature_dim", 0):
+            open_set = OpenSetConfig(**open_kw)
+        elif open_kw:
+            raise ConfigError("open-set keys %s need feature_dim >= 1"
+                              % ", ".join(sorted(open_kw)))
+        self._cfg = FusionConfig(**fusion_kw)
+        self._cfg.validate()                                   # make_grids, fusion.py:304
+        if closed is not None and open_set is not None:        # fusion.py:305-306
+            raise UserInputError("a run is closed-set or open-set, not both")
+        if closed is not None:
+            closed.validate()
+        if open_set is not None:
+            open_set.validate()
+        self._engine = EngineConfig(**engine_kw)
+        self._engine.validate()
+        self._closed, self._open = closed, open_set
+        self._frames = 0
+
+        c = _lib.SvxConfig()
+        c.voxel_size = float(self._cfg.voxel_size)
+        c.truncation = float(self._cfg.truncation)
+        c.max_range = float(self._cfg.max_range)
+        c.weight_fn = 0 if self._cfg.weight_fn == "constant_one" else 1
+        c.space_carving = int(bool(self._cfg.space_carving))
+        c.sem_kind = SEM_CLOSED if closed else (SEM_OPEN if open_set else SEM_NONE)
+        if closed is not None:
+            c.num_classes = int(closed.num_classes)
+            c.last_wins = int(closed.fusion == "last_wins")
+            c.count_dtype = SVX_F64 if np.dtype(closed.count_dtype) == np.float64 else SVX_F32
+        if open_set is not None:
+            c.feature_dim = int(open_set.feature_dim)
+            c.state_dtype = SVX_F64 if np.dtype(open_set.state_dtype) == np.float64 else SVX_F32
+            c.prior_beta = float(open_set.prior_beta)
+            c.lambda_floor = float(open_set.lambda_floor)
+        else:
+            c.lambda_floor = 1e-3
+        c.tsdf_dtype = SVX_F64 if np.dtype(self._engine.tsdf_dtype) == np.float64 else SVX_F32
+        c.device = int(self._engine.device)
+        c.reserve_voxels = int(self._engine.reserve_voxels)
+        c.reserve_blocks = int(self._engine.reserve_blocks)
+        self._c = c
+        h = ctypes.c_void_p()
+        check(lib.svx_create(ctypes.byref(c), ctypes.byref(h)))
+        self._handle = h
+        self._tsdf_view = GridView(self, KIND_TSDF)
+        self._sem_view = None
+        if closed is not None:
+            self._sem_view = GridView(self, KIND_CLOSED)
+        elif open_set is not None:
+            self._sem_view = GridView(self, KIND_OPEN)
+
+    def __del__(self):
+        h = getattr(self, "_handle", None)
+        if h is not None and lib is not None:
+            lib.svx_destroy(h)
+            self._handle = None
+
+    # -- reference surface ---------------------------------------------------
+
+    @property
+    def config(self) -> FusionConfig:
+        return self._cfg
+
+    @property
+    def grids(self):
+        """(tsdf, semantic) views over the device grids (semantic None for a
+        geometry-only run); they read the live map, they are not copies."""
+        return self._tsdf_view, self._sem_view
+
+    @property
+    def sem_kind(self) -> str | None:
+        return "closed" if self._closed else ("open" if self._open else None)
+
+    def _payload_args(self, n, labels, features, frame_id):
+        if labels is not None and features is not None:
+            raise PayloadMismatchError("frame carries both labels and features")
+        lab = feat = None
+        if labels is not None:
+            lab = _Arg(labels, "int32")
+            if tuple(lab.shape) != (n,):
+                raise PayloadMismatchError(f"labels shape {tuple(lab.shape)} != point count {n}")
+        if features is not None:
+            feat = _Arg(features, "float")
+            if len(feat.shape) != 2 or feat.shape[0] != n:
+                raise PayloadMismatchError(
+                    f"features shape {tuple(feat.shape)} incompatible with {n} points")
+        # _check_grids (fusion.py:173-197)
+        if self._closed is not None and lab is None:
+            raise PayloadMismatchError("closed-set grid requires per-point labels")
+        if self._open is not None:
+            if feat is None:
+                raise PayloadMismatchError("open-set grid requires per-point features")
+            if feat.shape[1] != self._open.feature_dim:
+                raise PayloadMismatchError(
+                    f"feature dim {feat.shape[1]} != grid dim {self._open.feature_dim}")
+        if self._closed is None:
+            lab = None
+        if self._open is None:
+            feat = None
+        return lab, feat
+
+    def _points_arg(self, points):
+        pts = _Arg(points, "float")
+        if len(pts.shape) != 2 or pts.shape[1] != 3:
+            raise UserInputError(f"points must be (n, 3), got {tuple(pts.shape)}")
+        return pts
+
+    def _run(self, fn, pts, vec, lab, feat):
+        rep = _lib.SvxReport()
+        stream = _stream_for([pts, lab, feat])
+        n = int(pts.shape[0])
+        arr = (ctypes.c_double * len(vec))(*[float(v) for v in vec])
+        check(fn(self._handle, pts.ptr, pts.code, n, arr,
+                 lab.ptr if lab is not None else None,
+                 feat.ptr if feat is not None else None,
+                 feat.code if feat is not None else SVX_F32, stream, ctypes.byref(rep)))
+        self._frames += 1
+        return IntegrationReport(
+            points_in=rep.points_in, points_used=rep.points_used,
+            skipped_nonfinite=rep.skipped_nonfinite, skipped_range=rep.skipped_range,
+            skipped_degenerate=rep.skipped_degenerate, skipped_bad_label=rep.skipped_bad_label,
+            band_hits=rep.band_hits, touched_voxels=rep.touched_voxels,
+            kernel_ms=rep.kernel_ms, new_blocks=rep.new_blocks, new_voxels=rep.new_voxels)
+
+    def integrate(self, points, pose, labels=None, features=None):
+        """Fuse one frame of sensor-frame points (n, 3) under a 4x4
+        sensor-to-world pose, with integer ``labels`` (closed-set) or float
+        ``features`` (open-set).  Same contract as bindings/__init__.py:131-142
+        and integrate_frame (fusion.py:200-293)."""
+        pts = self._points_arg(points)
+        pose = _check_pose(pose, self._frames)
+        lab, feat = self._payload_args(int(pts.shape[0]), labels, features, self._frames)
+        return self._run(lib.svx_integrate, pts, pose.reshape(-1), lab, feat)
+
+    def integrate_world(self, points_world, origin, labels=None, features=None):
+        """Fuse world-frame points observed from ``origin``: the reference's
+        backend seam (fusion.py:229-289 -> integrate_points) with
+        delta = p - origin, t = |delta|, u = delta / t."""
+        pts = self._points_arg(points_world)
+        o = np.asarray(origin, np.float64).reshape(-1)
+        if o.shape != (3,) or not np.isfinite(o).all():
+            raise UserInputError("origin must be a finite 3-vector")
+        lab, feat = self._payload_args(int(pts.shape[0]), labels, features, self._frames)
+        return self._run(lib.svx_integrate_world, pts, o, lab, feat)
+
+    def query(self, embedding):
+        """Cosine of every active voxel mean against one embedding, in active
+        order: (coords (n, 3) int64, sims (n,) float64); NaN for a zero mean
+        (bindings/__init__.py:153-169)."""
+        if self._open is None:
+            raise PayloadMismatchError("embedding query needs an open-set map")
+        q = np.ascontiguousarray(embedding, np.float64).reshape(-1)
+        dim = self._open.feature_dim
+        if q.shape[0] != dim:
+            raise PayloadMismatchError(f"query vector has dim {q.shape[0]}, map stores {dim}")
+        n = self.active_count()
+        coords = self._tsdf_view.active_coords()
+        sims = np.empty(n, np.float64)
+        check(lib.svx_query_cosine(self._handle, q.ctypes.data, n,
+                                   sims.ctypes.data if n else None, None))
+        return coords, sims
+
+    def classify(self, embeddings, temperature=None, confidence_threshold=None,
+                 return_sims=False):
+        """classify_means (gaussian.py:132-155) over all active voxels with the
+        TSDF weight as the observation weight (mesh.py:419-445): (labels
+        (n,) int32 with 0 = reject, best (n,) float64[, sims (n, k)])."""
+        if self._open is None:
+            raise PayloadMismatchError("classification needs an open-set map")
+        emb = np.ascontiguousarray(embeddings, np.float64)
+        if emb.ndim != 2 or emb.shape[1] != self._open.feature_dim:
+            raise PayloadMismatchError(
+                f"embeddings shape {emb.shape} incompatible with feature dim "
+                f"{self._open.feature_dim}")
+        tau = self._open.temperature if temperature is None else float(temperature)
+        tp = (self._open.confidence_threshold if confidence_threshold is None
+              else float(confidence_threshold))
+        n = self.active_count()
+        k = emb.shape[0]
+        labels = np.empty(n, np.int32)
+        best = np.empty(n, np.float64)
+        sims = np.empty((n, k), np.float64) if return_sims else None
+        check(lib.svx_classify(self._handle, emb.ctypes.data, k, tau, tp, n,
+                               labels.ctypes.data if n else None,
+                               best.ctypes.data if n else None,
+                               sims.ctypes.data if (return_sims and n) else None, None))
+        return (labels, best, sims) if return_sims else (labels, best)
+
+    def label_map(self, zero_if_empty=False):
+        """Closed-set argmax labels in active order: dirichlet.label_map
+        (dirichlet.py:81-88), or evalbench.grid_labels (0 where no counts,
+        evalbench.py:30-55) with ``zero_if_empty``.  Returns (coords, labels)."""
+        if self._closed is None:
+            raise PayloadMismatchError("label map needs a closed-set map")
+        n = self.active_count()
+        labels = np.empty(n, np.int32)
+        check(lib.svx_label_map(self._handle, 1 if zero_if_empty else 0, n,
+                                labels.ctypes.data if n else None, None))
+        return self._tsdf_view.active_coords(), labels
+
+    def active_count(self) -> int:
+        c = ctypes.c_int64()
+        check(lib.svx_active_count(self._handle, ctypes.byref(c)))
+        return int(c.value)
+
+    def engine_stats(self) -> dict:
+        s = _lib.SvxStats()
+        check(lib.svx_stats_get(self._handle, ctypes.byref(s)))
+        return {f: int(getattr(s, f)) for f, _ in s._fields_}
+
+    def stats(self) -> dict:
+        """sparsity_report of the TSDF grid (evalbench.py:297-327) plus
+        frames_integrated and semantic_active_voxels (bindings/__init__.py:171-181)."""
+        report = dict(_sparsity_report(self._tsdf_view, self._map_bounds))
+        report["frames_integrated"] = self._frames
+        if self._sem_view is not None:
+            report["semantic_active_voxels"] = self._sem_view.memory_stats().active_voxels
+        return report
+
+    def save(self, path):
+        raise NotImplementedError(".slvg snapshot export is not part of this build (SURVEY §8(f)-2)")
+
+    def extract(self, *args, **kwargs):
+        raise NotImplementedError("mesh extraction is not part of this build (SURVEY §8(f)-3)")
+
+    # -- bulk export -----------------------------------------------------------
+
+    def _export(self):
+        """(coords, d, w, sem0, sem1) of all active voxels in active order."""
+        n = self.active_count()
+        tdt = np.float64 if self._c.tsdf_dtype == SVX_F64 else np.float32
+        coords = np.empty((n, 3), np.int64)
+        d = np.empty(n, tdt)
+        w = np.empty(n, tdt)
+        sem0 = sem1 = None
+        if self._closed is not None:
+            sem0 = np.empty((n, self._closed.num_classes), np.dtype(self._closed.count_dtype))
+        if self._open is not None:
+            sdt = np.dtype(self._open.state_dtype)
+            sem0 = np.empty((n, self._open.feature_dim), sdt)
+            sem1 = np.empty((n, self._open.feature_dim), sdt)
+
+        def p(a):
+            return a.ctypes.data if (a is not None and a.size) else None
+
+        check(lib.svx_export_active(self._handle, n, p(coords), p(d), p(w), p(sem0), p(sem1),
+                                    None))
+        return coords, d, w, sem0, sem1
+
+    def _probe(self, coords):
+        coords = np.ascontiguousarray(np.atleast_2d(coords), np.int64)
+        if coords.size and np.abs(coords).max() >= COORD_LIMIT:
+            raise OutOfRangeError("voxel coordinate beyond +/-2^30 addressable range")
+        m = coords.shape[0]
+        tdt = np.float64 if self._c.tsdf_dtype == SVX_F64 else np.float32
+        d = np.empty(m, tdt)
+        w = np.empty(m, tdt)
+        active = np.empty(m, np.uint8)
+        sem0 = sem1 = None
+        if self._closed is not None:
+            sem0 = np.empty((m, self._closed.num_classes), np.dtype(self._closed.count_dtype))
+        if self._open is not None:
+            sdt = np.dtype(self._open.state_dtype)
+            sem0 = np.empty((m, self._open.feature_dim), sdt)
+            sem1 = np.empty((m, self._open.feature_dim), sdt)
+
+        def p(a):
+            return a.ctypes.data if (a is not None and a.size) else None
+
+        check(lib.svx_probe(self._handle, p(coords), m, p(d), p(w), p(sem0), p(sem1),
+                            p(active), None))
+        return d, w, sem0, sem1, active.astype(bool)
+
+
+class GridView:
+    """Read-only SparseGrid-like view (grid.py:89-215) of one payload of a
+    Mapper's device map.  TSDF fields are returned as float64 like the
+    reference's payload (grid.py:45-47)."""
+
+    def __init__(self, mapper: Mapper, kind: int):
+        self._m = mapper
+        self.kind = kind
+        self.voxel_size = float(mapper._cfg.voxel_size)
+        if kind == KIND_TSDF:
+            self.payload = TsdfPayload(float(mapper._cfg.truncation))
+        elif kind == KIND_CLOSED:
+            self.payload = ClosedPayload(mapper._closed)
+        else:
+            self.payload = OpenPayload(mapper._open)
+
+    @property
+    def kind_name(self):
+        return KIND_NAMES[self.kind]
+
+    def _fields(self, d, w, sem0, sem1):
+        if self.kind == KIND_TSDF:
+            return [np.asarray(d, np.float64), np.asarray(w, np.float64)]
+        if self.kind == KIND_CLOSED:
+            return [sem0]
+        return [sem0, sem1]
+
+    def active_values(self):
+        coords, d, w, sem0, sem1 = self._m._export()
+        return coords, self._fields(d, w, sem0, sem1)
+
+    def active_coords(self):
+        return self._m._export()[0]
+
+    def probe_many(self, coords):
+        d, w, sem0, sem1, active = self._m._probe(coords)
+        return self._fields(d, w, sem0, sem1), active
+
+    def get(self, coord):
+        vals, _ = self.probe_many(np.asarray(coord, np.int64).reshape(1, 3))
+        return tuple(v[0] for v in vals)
+
+    def memory_stats(self) -> MemoryStats:
+        st = self._m.engine_stats()
+        coords = self.active_coords()
+        internal = 0
+        if coords.shape[0]:
+            internal = int(np.unique(coords >> (LEAF_LOG2 + INTERNAL_LOG2), axis=0).shape[0])
+        te = 8 if self._m._c.tsdf_dtype == SVX_F64 else 4
+        per_tsdf = 2 * te
+        per_sem = st["payload_bytes_per_voxel"] - per_tsdf
+        leaf_bytes = st["leaf_count"] * (16 + 64 + 4 * 512)
+        hash_bytes = st["hash_capacity"] * 16
+        if self.kind == KIND_TSDF:
+            resident = leaf_bytes + hash_bytes + st["active_voxels"] * per_tsdf
+        else:
+            resident = st["active_voxels"] * per_sem
+        return MemoryStats(leaf_count=st["leaf_count"], internal_count=internal,
+                           root_entries=internal, active_voxels=st["active_voxels"],
+                           resident_bytes=int(resident))
+
+    def content_hash(self):
+        """Order-independent digest with the reference's layout (grid.py:204-215)."""
+        coords, vals = self.active_values()
+        order = np.lexsort((coords[:, 2], coords[:, 1], coords[:, 0]))
+        hs = hashlib.sha256()
+        hs.update(_MAGIC)
+        hs.update(_params_block(self.payload))
+        hs.update(struct.pack("<dBB", self.voxel_size, LEAF_LOG2, INTERNAL_LOG2))
+        hs.update(np.ascontiguousarray(coords[order]).tobytes())
+        for v in vals:
+            hs.update(np.ascontiguousarray(v[order]).tobytes())
+        return hs.hexdigest()
+
+
+def _dtype_code(name) -> int:
+    return 1 if np.dtype(name) == np.float64 else 0
+
+
+def _params_block(payload) -> bytes:
+    """Payload parameter bytes hashed by content_hash (grid.py:276-295)."""
+    if payload.kind == KIND_TSDF:
+        return struct.pack("<d", payload.truncation)
+    cfg = payload.cfg
+    if payload.kind == KIND_CLOSED:
+        return struct.pack("<IdBB", cfg.num_classes, cfg.prior_alpha,
+                           0 if cfg.fusion == "bayes" else 1, _dtype_code(cfg.count_dtype))
+    return struct.pack("<IddddB", cfg.feature_dim, cfg.prior_beta, cfg.lambda_floor,
+                       cfg.confidence_threshold, cfg.temperature, _dtype_code(cfg.state_dtype))
+
+
+def _sparsity_report(view: GridView, map_bounds=None) -> dict:
+    """evalbench.sparsity_report (evalbench.py:297-327) over a device grid."""
+    stats = view.memory_stats()
+    te = 8 if view._m._c.tsdf_dtype == SVX_F64 else 4
+    per_voxel = 2 * te
+    out = {
+        "active_voxels": stats.active_voxels,
+        "leaf_count": stats.leaf_count,
+        "internal_count": stats.internal_count,
+        "resident_bytes": stats.resident_bytes,
+        "payload_bytes_per_voxel": per_voxel,
+    }
+    coords = view.active_coords()
+    if coords.shape[0]:
+        ext = coords.max(axis=0) - coords.min(axis=0) + 1
+        dense_bbox = int(np.prod(ext.astype(np.float64)) * per_voxel)
+        out["dense_bbox_bytes"] = dense_bbox
+        out["ratio_bbox"] = stats.resident_bytes / dense_bbox if dense_bbox else np.inf
+    if map_bounds is not None:
+        lo, hi = np.asarray(map_bounds, np.float64)
+        nvox = np.prod(np.ceil((hi - lo) / view.voxel_size))
+        dense_bounds = int(nvox * per_voxel)
+        out["dense_bounds_bytes"] = dense_bounds
+        out["ratio_bounds"] = stats.resident_bytes / dense_bounds if dense_bounds else np.inf
+    return out

@@ -1,0 +1,264 @@
+"""Generate the golden fixtures that pin the oracle and the engine to the
+reference implementation itself.
+
+Runs ONLY in the build container, where the read-only reference package is
+importable (it does not exist on the GPU box):
+
+    PYTHONPATH=/root/reference/pkg/src:/root/reference/pkg/bindings/src \
+        python tests/golden/make_golden.py
+
+Each scenario stores its inputs (so tests never depend on re-generating
+them) and the reference's outputs:
+
+  api_*   drive ``semvox_bindings.Mapper.integrate`` (the reference's public
+          API, bindings/__init__.py:131-142) with identity-rotation poses, for
+          which the reference's BLAS world transform is exact;
+  seam_*  drive the reference backend seam ``integrate_points``
+          (fusion.py:278-289) with world-frame float32 points and the frame
+          prep of fusion.py:228-275 restated here (delta, t, masks, u), for
+          rotated trajectories whose BLAS transform is not reproducible.
+
+Outputs: per-frame IntegrationReport counts, active coords in the
+reference's active order, TSDF d/w (f64), semantic fields, content hashes,
+and readouts (label_map / grid_labels, cosine query, classify_means).
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, REPO)
+
+REF = os.environ.get("SEMVOX_REF", "/root/reference/pkg")
+for sub in ("src", "bindings/src"):
+    p = os.path.join(REF, sub)
+    if p not in sys.path:
+        sys.path.insert(0, p)
+
+import semvox  # noqa: E402
+import semvox_bindings as sb  # noqa: E402
+from semvox.dirichlet import label_map  # noqa: E402
+from semvox.evalbench import grid_labels  # noqa: E402
+from semvox.gaussian import classify_means, cosine_to_embeddings  # noqa: E402
+
+REPORT_KEYS = ("points_in", "points_used", "skipped_nonfinite", "skipped_range",
+               "skipped_degenerate", "skipped_bad_label", "band_hits", "touched_voxels")
+
+
+def _reports_array(reps):
+    return np.array([[getattr(r, k) if hasattr(r, k) else r[k] for k in REPORT_KEYS]
+                     for r in reps], np.int64)
+
+
+def _dump_state(out, tsdf, sem, sem_kind, queries=None, tau=0.01, tp=0.1):
+    coords, (d, w) = tsdf.active_values()
+    out["coords"] = np.asarray(coords, np.int64)
+    out["d"] = d
+    out["w"] = w
+    out["tsdf_hash"] = np.array(tsdf.content_hash())
+    if sem is None:
+        return
+    scoords, svals = sem.active_values()
+    assert np.array_equal(scoords, coords)
+    out["sem_hash"] = np.array(sem.content_hash())
+    if sem_kind == "closed":
+        out["counts"] = svals[0]
+        out["label_map"] = label_map(sem)[1].astype(np.int32)
+        out["grid_labels"] = grid_labels(sem)[1]
+    else:
+        out["mean"], out["beta"] = svals
+        if queries is not None:
+            out["queries"] = queries
+            out["cosine_q0"] = cosine_to_embeddings(svals[0], queries[:1])[:, 0]
+            lab, best = classify_means(svals[0], w, queries, tau, tp)
+            out["classify_labels"] = lab
+            out["classify_best"] = best
+
+
+def api_scenario(name, frames, mapper_kw, queries=None):
+    """frames: list of (points_sensor, pose, labels|None, feats|None)."""
+    m = sb.Mapper(**mapper_kw)
+    reps = []
+    for pts, pose, lab, feat in frames:
+        reps.append(m.integrate(pts, pose, labels=lab, features=feat))
+    tsdf, sem = m.grids
+    kind = "closed" if mapper_kw.get("num_classes") else ("open" if mapper_kw.get("feature_dim") else None)
+    out = {"mode": np.array("api"), "reports": _reports_array(reps)}
+    for i, (pts, pose, lab, feat) in enumerate(frames):
+        out[f"points_{i}"] = pts
+        out[f"pose_{i}"] = pose
+        if lab is not None:
+            out[f"labels_{i}"] = lab
+        if feat is not None:
+            out[f"features_{i}"] = feat
+    out["n_frames"] = np.array(len(frames))
+    out["mapper_kw"] = np.array(repr(mapper_kw))
+    _dump_state(out, tsdf, sem, kind, queries)
+    np.savez_compressed(os.path.join(HERE, name + ".npz"), **out)
+    print(name, "frames", len(frames), "active", out["coords"].shape[0])
+
+
+def seam_integrate(tsdf, sem, kind, fusion, pw, origin, labels, feats):
+    """fusion.py:228-293 from the world points on, then the backend seam."""
+    pw = np.asarray(pw, np.float64)
+    origin = np.asarray(origin, np.float64)
+    rep = {k: 0 for k in REPORT_KEYS}
+    rep["points_in"] = pw.shape[0]
+    finite = np.isfinite(pw).all(axis=1)
+    rep["skipped_nonfinite"] = int((~finite).sum())
+    delta = pw - origin
+    with np.errstate(invalid="ignore"):
+        t = np.sqrt((delta * delta).sum(axis=1))
+    t = np.where(np.isfinite(t), t, np.inf)
+    degenerate = finite & (t == 0.0)
+    rep["skipped_degenerate"] = int(degenerate.sum())
+    in_range = t <= fusion.max_range
+    rep["skipped_range"] = int((finite & ~degenerate & ~in_range).sum())
+    keep = finite & ~degenerate & in_range
+    if kind == "closed":
+        k = sem.payload.cfg.num_classes
+        good = (labels >= 1) & (labels <= k)
+        rep["skipped_bad_label"] = int((keep & ~good).sum())
+        keep &= good
+    elif kind == "open":
+        good = np.isfinite(feats).all(axis=1)
+        rep["skipped_bad_label"] = int((keep & ~good).sum())
+        keep &= good
+    idx = np.flatnonzero(keep)
+    rep["points_used"] = int(idx.shape[0])
+    if idx.shape[0] == 0:
+        return rep
+    tk = t[idx]
+    u = delta[idx] / tk[:, None]
+    params = {
+        "voxel_size": fusion.voxel_size, "truncation": fusion.truncation,
+        "weight_fn": 0 if fusion.weight_fn == "constant_one" else 1,
+        "space_carving": fusion.space_carving,
+        "num_classes": sem.payload.cfg.num_classes if kind == "closed" else 0,
+        "lambda_floor": sem.payload.cfg.lambda_floor if kind == "open" else 1e-3,
+        "last_wins": kind == "closed" and sem.payload.cfg.fusion == "last_wins",
+    }
+    kr = tsdf.backend.integrate_points(
+        tsdf.core, sem.core if sem is not None else None, kind, origin, u, tk,
+        np.ascontiguousarray(labels[idx], np.int32) if kind == "closed" else None,
+        np.ascontiguousarray(feats[idx], np.float64) if kind == "open" else None, params, 1)
+    rep["band_hits"] = kr["band_hits"]
+    rep["touched_voxels"] = kr["touched_voxels"]
+    return rep
+
+
+def seam_scenario(name, frames, mapper_kw, queries=None):
+    """frames: list of (points_world f32, origin, labels|None, feats|None)."""
+    fkw = {k: v for k, v in mapper_kw.items()
+           if k in ("voxel_size", "truncation", "weight_fn", "space_carving", "max_range")}
+    fusion = semvox.FusionConfig(**fkw)
+    closed = open_set = None
+    kind = None
+    if mapper_kw.get("num_classes"):
+        kind = "closed"
+        closed = semvox.ClosedSetConfig(num_classes=mapper_kw["num_classes"],
+                                        fusion=mapper_kw.get("fusion", "bayes"))
+    if mapper_kw.get("feature_dim"):
+        kind = "open"
+        open_set = semvox.OpenSetConfig(feature_dim=mapper_kw["feature_dim"])
+    tsdf, sem = semvox.make_grids(fusion, closed=closed, open_set=open_set)
+    reps = []
+    out = {"mode": np.array("seam")}
+    for i, (pw, origin, lab, feat) in enumerate(frames):
+        reps.append(seam_integrate(tsdf, sem, kind, fusion, pw, origin, lab, feat))
+        out[f"points_{i}"] = pw
+        out[f"origin_{i}"] = np.asarray(origin, np.float64)
+        if lab is not None:
+            out[f"labels_{i}"] = lab
+        if feat is not None:
+            out[f"features_{i}"] = feat
+    out["reports"] = _reports_array(reps)
+    out["n_frames"] = np.array(len(frames))
+    out["mapper_kw"] = np.array(repr(mapper_kw))
+    _dump_state(out, tsdf, sem, kind, queries)
+    np.savez_compressed(os.path.join(HERE, name + ".npz"), **out)
+    print(name, "frames", len(frames), "active", out["coords"].shape[0])
+
+
+def plane_frames(seed, n, frames, labels_k=0, feat_dim=0, with_bad=True):
+    """Sensor-frame points of the z = 0 square seen from above (identity
+    rotation), plus invalid rows exercising every skip counter."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for i in range(frames):
+        origin = np.array([0.1 * i, -0.05 * i, 2.0])
+        world = np.column_stack([rng.uniform(-1.0, 1.0, (n, 2)), rng.normal(0, 0.01, n)])
+        pts = world - origin
+        if with_bad:
+            pts[0] = np.nan                      # nonfinite
+            pts[1] = (0.0, 0.0, 0.0)             # degenerate
+            pts[2] = (50.0, 0.0, 0.0)            # out of range
+        pose = np.eye(4)
+        pose[:3, 3] = origin
+        lab = feat = None
+        if labels_k:
+            lab = rng.integers(1, labels_k + 1, n).astype(np.int32)
+            if with_bad:
+                lab[3] = 0
+                lab[4] = labels_k + 1
+        if feat_dim:
+            feat = rng.normal(size=(n, feat_dim)).astype(np.float32)
+            if with_bad:
+                feat[5, 0] = np.inf
+        out.append((pts, pose, lab, feat))
+    return out
+
+
+def main():
+    from paper_2512_12945_b200 import scenes
+
+    # -- API level ------------------------------------------------------------
+    api_scenario("api_closed_plane", plane_frames(0, 600, 4, labels_k=4),
+                 dict(voxel_size=0.05, truncation=0.15, num_classes=4))
+    api_scenario("api_open_plane", plane_frames(1, 400, 3, feat_dim=6),
+                 dict(voxel_size=0.05, truncation=0.15, feature_dim=6),
+                 queries=np.random.default_rng(5).normal(size=(4, 6)))
+    api_scenario("api_geometry_carving_dropoff", plane_frames(2, 300, 2),
+                 dict(voxel_size=0.05, truncation=0.15, space_carving=True,
+                      weight_fn="linear_dropoff"))
+    api_scenario("api_closed_lastwins_dropoff", plane_frames(3, 400, 3, labels_k=5),
+                 dict(voxel_size=0.04, truncation=0.12, num_classes=5, fusion="last_wins",
+                      weight_fn="linear_dropoff"))
+    wl = scenes.workload(2, small=True)
+    fr = []
+    for i in range(3):
+        f = wl.make_frame(i)
+        fr.append((f.points.numpy(), f.pose, f.labels.numpy(), None))
+    api_scenario("api_closed_lidar_small", fr, wl.mapper_kwargs)
+    # -- backend seam, rotated trajectories --------------------------------------
+    wl = scenes.workload(1, small=True)
+    fr = []
+    for i in range(3):
+        f = wl.make_frame(i)
+        fr.append((f.points_world.numpy(), f.origin, f.labels.numpy(), None))
+    seam_scenario("seam_closed_room_small", fr, wl.mapper_kwargs)
+    wl = scenes.workload(3, small=True)
+    fr = []
+    dim = 16   # keep the fixture small: first 16 embedding dims, every 2nd pixel
+    for i in range(2):
+        f = wl.make_frame(i)
+        fr.append((f.points_world.numpy()[::2], f.origin, None,
+                   np.ascontiguousarray(f.features.numpy()[::2, :dim])))
+    kw = dict(wl.mapper_kwargs, feature_dim=dim)
+    seam_scenario("seam_open_room_small", fr, kw,
+                  queries=np.ascontiguousarray(wl.queries[:4, :dim].numpy()))
+    wl = scenes.workload(4, small=True)
+    fr = []
+    for i in range(2):
+        f = wl.make_frame(i)
+        fr.append((f.points_world.numpy(), f.origin, f.labels.numpy(), None))
+    seam_scenario("seam_closed_city_small", fr, wl.mapper_kwargs)
+
+
+if __name__ == "__main__":
+    main()

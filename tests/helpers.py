@@ -1,0 +1,96 @@
+"""Shared test helpers: golden fixtures, replay on the oracle or the engine,
+and the comparators (bit-exact where the reference is exact, tolerance
+written out where it is not)."""
+
+from __future__ import annotations
+
+import ast
+import glob
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+GOLDEN = os.path.join(HERE, "golden")
+
+REPORT_KEYS = ("points_in", "points_used", "skipped_nonfinite", "skipped_range",
+               "skipped_degenerate", "skipped_bad_label", "band_hits", "touched_voxels")
+
+# Tolerances (north star: TSDF / weights / semantic statistics within 1e-5
+# relative; the absolute floor is 1e-5 * truncation for |d| -> 0).
+RTOL = 1e-5
+
+
+def golden_names():
+    return sorted(os.path.splitext(os.path.basename(p))[0]
+                  for p in glob.glob(os.path.join(GOLDEN, "*.npz")))
+
+
+def load_golden(name):
+    z = np.load(os.path.join(GOLDEN, name + ".npz"), allow_pickle=False)
+    g = {k: z[k] for k in z.files}
+    g["mapper_kw"] = ast.literal_eval(str(g["mapper_kw"]))
+    g["mode"] = str(g["mode"])
+    g["n_frames"] = int(g["n_frames"])
+    return g
+
+
+def frames_of(g):
+    for i in range(g["n_frames"]):
+        yield (g[f"points_{i}"], g.get(f"pose_{i}"), g.get(f"origin_{i}"), g.get(f"labels_{i}"),
+               g.get(f"features_{i}"))
+
+
+def oracle_for(g, **extra):
+    from oracle.oracle import OracleMap
+
+    kw = dict(g["mapper_kw"])
+    kw.update(extra)
+    return OracleMap(**kw)
+
+
+def replay_oracle(g, om):
+    reps = []
+    for pts, pose, origin, lab, feat in frames_of(g):
+        if g["mode"] == "api":
+            reps.append(om.integrate(pts, pose, labels=lab, features=feat))
+        else:
+            reps.append(om.integrate_world(pts, origin, labels=lab, features=feat))
+    return reps
+
+
+def replay_mapper(g, mapper, device_inputs=False):
+    """Feed a fixture through the engine's Mapper (host numpy arrays, or CUDA
+    tensors when device_inputs)."""
+    reps = []
+    for pts, pose, origin, lab, feat in frames_of(g):
+        if device_inputs:
+            import torch
+
+            pts = torch.as_tensor(np.ascontiguousarray(pts)).cuda()
+            lab = torch.as_tensor(lab).cuda() if lab is not None else None
+            feat = torch.as_tensor(np.ascontiguousarray(feat)).cuda() if feat is not None else None
+        if g["mode"] == "api":
+            reps.append(mapper.integrate(pts, pose, labels=lab, features=feat))
+        else:
+            reps.append(mapper.integrate_world(pts, origin, labels=lab, features=feat))
+    return reps
+
+
+def report_rows(reps):
+    out = []
+    for r in reps:
+        get = (lambda k: getattr(r, k))
+        out.append([int(get(k)) for k in REPORT_KEYS])
+    return np.array(out, np.int64)
+
+
+def assert_close_rel(a, b, rtol=RTOL, atol=0.0, what=""):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    assert a.shape == b.shape, (what, a.shape, b.shape)
+    err = np.abs(a - b)
+    tol = atol + rtol * np.abs(b)
+    bad = err > tol
+    assert not bad.any(), f"{what}: {int(bad.sum())} of {a.size} beyond rtol={rtol} atol={atol}; " \
+                          f"max err {err.max():.3e}"
