@@ -1,0 +1,485 @@
+#!/usr/bin/env python
+"""Benchmark of the SLIM-VDB per-frame integration hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+
+One step = one frame of the BASELINE workload integrated into the map
+(BASELINE.json configs[1] by default: closed-set 64x1024 LiDAR, identity
+rotations, through Mapper.integrate -> svx_integrate).  Prints ONE JSON line.
+
+ours:
+  value     points integrated/s with inputs resident in HBM; per-step CUDA
+            events on the launching stream; L2 flushed (256 MiB write)
+            between steps outside the events; max over ranks.
+  e2e       same metric through the public API from pinned HOST buffers:
+            H2D of points+labels and D2H of the frame report inside each step.
+  roofline  dominant stage (per-stage CUDA events inside libsvx) against the
+            measured HBM copy bandwidth (MEASURED_PEAKS.json).
+  cpu_baseline  the CPU oracle port (oracle/, OpenMP, all host threads) on a
+            bounded sample of the same frames (rank 0, N=1 only).
+reference:
+  times the reference's own CPU implementation (semvox built in
+  baseline/_ref, native backend, all host threads; else the oracle port) on
+  the same workload, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "points integrated/sec"
+UNIT = "points/s"
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--tsdf-dtype", default="float64")
+    ap.add_argument("--cpu-frames", type=int, default=0, help="oracle sample frames (0=auto)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# -- clocks during the timed region -------------------------------------------------
+
+class ClockSampler:
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index):
+        self.samples = []
+        self.reasons = 0
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= int(self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+            except Exception:
+                pass
+            self._stop.wait(0.05)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        reasons = [n for b, n in self.REASONS.items() if self.reasons & b and n != "gpu_idle"]
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# -- byte model (fixed fp32 state layout) ----------------------------
+
+def frame_bytes(rep, kind, C=0, D=0):
+    """bytes_frame = N_used*(12+P) + 2*U*S."""
+    if kind == "closed":
+        P, S = 4, 8 + 4 * C
+    elif kind == "open":
+        P, S = 4 * D, 8 + 8 * D
+    else:
+        P, S = 0, 8
+    return rep.points_used * (12 + P) + 2 * rep.touched_voxels * S
+
+
+def stage_bytes(stage, rep, kind, C, D, tsdf_elem):
+    """Algorithmic bytes one launch of a stage must move (DESIGN.md table)."""
+    n, used, R, U = rep.points_in, rep.points_used, rep.band_hits, rep.touched_voxels
+    P = 4 if kind == "closed" else (4 * D if kind == "open" else 0)
+    S = 2 * tsdf_elem + (4 * C if kind == "closed" else (8 * D if kind == "open" else 0))
+    return {
+        "count": n * (12 + P) + used * 32,          # read points(+labels), write ray table
+        "fill": used * 32 + R * 12,                  # read rays, write (key, point) rows
+        "sort": 2 * R * 12,                          # one read + one write of the rows
+        "group": R * 8 + U * 20,                     # read keys, write unique keys + runs
+        "leaves": U * 24,                            # read keys, write leaf ids (+hash probe)
+        "voxels": U * 24,
+        "update": 2 * U * S + R * (4 + (4 if kind == "closed" else 0)) + U * 20,
+    }[stage]
+
+
+def measured_peak():
+    p = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic(stage):
+    """dram bytes per launch from the committed ncu summary, if any."""
+    p = os.path.join(REPO, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as fh:
+            return json.load(fh).get(stage)
+    except Exception:
+        return None
+
+
+# -- workloads -----------------------------------------------------------------------
+
+def make_frames(cfg, count, device, start=0):
+    from paper_2512_12945_b200 import scenes
+
+    wl = scenes.workload(cfg, device=device)
+    frames = [wl.make_frame((start + i) % wl.n_frames) for i in range(count)]
+    return wl, frames
+
+
+def sem_kind_of(kw):
+    return "closed" if kw.get("num_classes") else ("open" if kw.get("feature_dim") else None)
+
+
+def run_oracle_sample(wl, frames, threads):
+    """Time the CPU oracle port on host copies of the frames."""
+    from oracle.oracle import OracleMap
+
+    om = OracleMap(**wl.mapper_kwargs, threads=threads)
+    used, secs = 0, 0.0
+    kind = sem_kind_of(wl.mapper_kwargs)
+    for f in frames:
+        pts = f.points.cpu().numpy()
+        lab = f.labels.cpu().numpy() if f.labels is not None else None
+        feat = f.features.cpu().numpy() if f.features is not None else None
+        t0 = time.perf_counter()
+        r = om.integrate(pts, f.pose, labels=lab if kind == "closed" else None,
+                         features=feat if kind == "open" else None)
+        secs += time.perf_counter() - t0
+        used += r.points_used
+    return used, secs
+
+
+# -- our arm ------------------------------------------------------------------------
+
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2512_12945_b200 import Mapper, _lib
+
+    K, W = args.steps, args.warmup
+    # replicas: rank r integrates its own stream of frames (weak scaling)
+    wl, frames = make_frames(args.config, W + K, dev, start=rank * (W + K))
+    kw = dict(wl.mapper_kwargs, tsdf_dtype=args.tsdf_dtype, device=local)
+    kind = sem_kind_of(kw)
+    C = kw.get("num_classes", 0)
+    D = kw.get("feature_dim", 0)
+    tsdf_elem = 8 if args.tsdf_dtype == "float64" else 4
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def integrate(m, f, host=None):
+        if host is not None:
+            pts, lab, feat = host
+        else:
+            pts, lab, feat = f.points, f.labels, f.features
+        return m.integrate(pts, f.pose, labels=lab if kind == "closed" else None,
+                           features=feat if kind == "open" else None)
+
+    # ---- device-resident pass ------------------------------------------------------
+    m = Mapper(**kw)
+    for f in frames[:W]:
+        integrate(m, f)
+    # pool headroom for the timed frames, so no growth copy lands inside them
+    st = m.engine_stats()
+    per_frame = max(1, st["active_voxels"] // max(W, 1))
+    m.reserve(st["active_voxels"] + 2 * per_frame * K, st["leaf_count"] * (1 + 2 * K // max(W, 1)))
+    m.set_profiling(True)
+    stream = torch.cuda.current_stream()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(K)]
+    reps, stage_hist = [], []
+    launches0 = _lib.kernel_launches()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(K):
+            flush.zero_()
+            evs[i][0].record(stream)
+            reps.append(integrate(m, frames[W + i]))
+            evs[i][1].record(stream)
+            stage_hist.append(m.stage_times())
+        torch.cuda.synchronize()
+    launches = _lib.kernel_launches() - launches0
+    if world > 1:
+        torch.distributed.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    total_ms = sum(step_ms)
+    used = sum(r.points_used for r in reps)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    u = torch.tensor([used], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        torch.distributed.all_reduce(u)
+    total_ms_max, used_all = float(t.item()), float(u.item())
+    value = used_all / (total_ms_max / 1e3)
+
+    # ---- roofline of the dominant stage -------------------------------------------
+    stages = list(_lib.STAGES)
+    mean_stage = {s: statistics.mean(h[s] for h in stage_hist) for s in stages}
+    dom = max(stages, key=lambda s: mean_stage[s])
+    dom_bytes = statistics.mean(stage_bytes(dom, r, kind, C, D, tsdf_elem) for r in reps)
+    peak, peak_src = measured_peak()
+    achieved = dom_bytes / (mean_stage[dom] / 1e3) / 1e9
+    fb = statistics.mean(frame_bytes(r, kind, C, D) for r in reps)
+    frame_gbs = fb / (statistics.mean(step_ms) / 1e3) / 1e9
+    traffic = ncu_traffic(dom)
+
+    # ---- e2e pass: host pinned buffers through the public API ---------------------------
+    e2e = None
+    if not args.no_e2e:
+        host = []
+        for f in frames:
+            pts = torch.empty(f.points.shape, dtype=f.points.dtype, pin_memory=True)
+            pts.copy_(f.points)
+            lab = feat = None
+            if f.labels is not None:
+                lab = torch.empty(f.labels.shape, dtype=f.labels.dtype, pin_memory=True)
+                lab.copy_(f.labels)
+            if f.features is not None:
+                feat = torch.empty(f.features.shape, dtype=f.features.dtype, pin_memory=True)
+                feat.copy_(f.features)
+            host.append((pts.numpy(), lab.numpy() if lab is not None else None,
+                         feat.numpy() if feat is not None else None))
+        m2 = Mapper(**kw)
+        for f, h in zip(frames[:W], host[:W]):
+            integrate(m2, f, h)
+        st = m2.engine_stats()
+        m2.reserve(st["active_voxels"] + 2 * per_frame * K,
+                   st["leaf_count"] * (1 + 2 * K // max(W, 1)))
+        dstream = torch.cuda.default_stream()
+        e_ms, e_used, h2d = 0.0, 0, 0
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        for i in range(K):
+            flush.zero_()
+            torch.cuda.synchronize()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(dstream)
+            r = integrate(m2, frames[W + i], host[W + i])
+            b.record(dstream)
+            b.synchronize()
+            e_ms += a.elapsed_time(b)
+            e_used += r.points_used
+            h2d += sum(x.nbytes for x in host[W + i] if x is not None)
+        te = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+        ue = torch.tensor([e_used], dtype=torch.float64, device=dev)
+        if world > 1:
+            torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
+            torch.distributed.all_reduce(ue)
+        e2e = {"value": float(ue.item()) / (float(te.item()) / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d // K), "d2h_bytes_per_step": 136,
+               "ms_per_step": float(te.item()) / K}
+        del m2
+
+    # ---- CPU baseline (rank 0, N=1) ---------------------------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        nf = args.cpu_frames or min(K + W, 30 if kind == "closed" else 4)
+        threads = host_threads()
+        cused, csecs = run_oracle_sample(wl, frames[:nf], threads)
+        cpu = {"value": cused / csecs, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"frames 0..{nf - 1} of {wl.name} through the C oracle "
+                         f"(oracle/svx_oracle.c, OpenMP x{threads}, {cpu_model()}), "
+                         f"{csecs:.1f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+            "warmup": W, "ms_per_step": total_ms_max / K, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {
+                "workload": wl.name, "points_per_frame": wl.points_per_frame,
+                "voxel_size": kw["voxel_size"], "truncation": kw["truncation"],
+                "num_classes": C or None, "feature_dim": D or None,
+                "tsdf_dtype": args.tsdf_dtype, "api": "Mapper.integrate -> svx_integrate",
+                "parallelism": f"replicas{world}" if world > 1 else "single",
+                "l2": "flushed between steps (256 MiB write, outside step events)",
+                "frames_timed": f"{W}..{W + K - 1}",
+            },
+            "ms_per_frame_p50": statistics.median(step_ms),
+            "points_used_per_frame": used / K,
+            "touched_voxels_per_frame": statistics.mean(r.touched_voxels for r in reps),
+            "band_rows_per_frame": statistics.mean(r.band_hits for r in reps),
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+                         "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                         "peak_source": peak_src,
+                         "bytes_per_launch": dom_bytes, "ms_per_launch": mean_stage[dom]},
+            "frame_roofline": {"bytes_per_frame": fb, "achieved": frame_gbs, "unit": "GB/s",
+                               "frac": frame_gbs / peak,
+                               "model": "N_used*(12+P) + 2*U*S, fp32 state (SURVEY 8d)"},
+            "stages_ms": {s: round(mean_stage[s], 4) for s in stages},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+# -- reference arm ------------------------------------------------------------------------
+
+def load_reference():
+    ref = os.path.join(REPO, "baseline", "_ref")
+    if os.path.isdir(os.path.join(ref, "semvox")):
+        sys.path.insert(0, ref)
+        try:
+            import semvox  # noqa: F401
+            from semvox.backend import NATIVE_AVAILABLE
+
+            return semvox, NATIVE_AVAILABLE
+        except Exception:
+            sys.path.remove(ref)
+    return None, False
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import torch
+
+    K, W = args.steps, args.warmup
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    wl, frames = make_frames(args.config, W + K, dev)
+    kw = wl.mapper_kwargs
+    kind = sem_kind_of(kw)
+    threads = host_threads()
+    semvox, native = load_reference()
+    used, secs = 0, 0.0
+    if semvox is not None:
+        fusion = semvox.FusionConfig(voxel_size=kw["voxel_size"], truncation=kw["truncation"],
+                                     max_range=kw["max_range"])
+        closed = semvox.ClosedSetConfig(num_classes=kw["num_classes"]) if kind == "closed" else None
+        open_set = semvox.OpenSetConfig(feature_dim=kw["feature_dim"]) if kind == "open" else None
+        tsdf, sem = semvox.make_grids(fusion, closed=closed, open_set=open_set,
+                                      backend="native" if native else "python")
+        for i, f in enumerate(frames):
+            pts = f.points.cpu().numpy()
+            lab = f.labels.cpu().numpy() if kind == "closed" else None
+            feat = f.features.cpu().numpy() if kind == "open" else None
+            t0 = time.perf_counter()
+            fr = semvox.Frame(points=pts, pose=f.pose, labels=lab, features=feat, frame_id=i)
+            r = semvox.integrate_frame(tsdf, sem, fr, fusion, threads=threads)
+            dt = time.perf_counter() - t0
+            if i >= W:
+                secs += dt
+                used += r.points_used
+        what = (f"semvox (reference) {'native Cython/C++ OpenMP' if native else 'numpy'} backend "
+                f"from baseline/_ref, integrate_frame per frame, threads={threads}, {cpu_model()}")
+        kind_s = "reference"
+    else:
+        from oracle.oracle import OracleMap
+
+        om = OracleMap(**kw, threads=threads)
+        for i, f in enumerate(frames):
+            t0 = time.perf_counter()
+            r = om.integrate(f.points.cpu().numpy(), f.pose,
+                             labels=f.labels.cpu().numpy() if kind == "closed" else None,
+                             features=f.features.cpu().numpy() if kind == "open" else None)
+            dt = time.perf_counter() - t0
+            if i >= W:
+                secs += dt
+                used += r.points_used
+        what = f"oracle port (oracle/svx_oracle.c) OpenMP x{threads}, {cpu_model()}"
+        kind_s = "port"
+    value = used / secs
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
+        "ms_per_step": secs * 1e3 / K, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+        "config": {"workload": wl.name, "points_per_frame": wl.points_per_frame,
+                   "voxel_size": kw["voxel_size"], "truncation": kw["truncation"],
+                   "frames_timed": f"{W}..{W + K - 1}"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind_s,
+                         "sample": what},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

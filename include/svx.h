@@ -115,6 +115,9 @@ typedef struct svx_map svx_map;
 /* Replaces make_grids (fusion.py:296-314) + GridCore.__init__ (_core.pyx:104-141). */
 svx_status svx_create(const svx_config* cfg, svx_map** out);
 svx_status svx_destroy(svx_map* map);
+/* Pre-size the voxel and leaf pools (and the leaf hash) so later frames do
+ * not pay pool growth (the reference grows by doubling, _core.pyx:154-183). */
+svx_status svx_reserve(svx_map* map, int64_t voxels, int64_t blocks);
 
 /* ---- integration ---------------------------------------------------------
  * Replaces integrate_frame (fusion.py:200-293) from the world transform on,
@@ -178,6 +181,17 @@ svx_status svx_label_map(svx_map* map, int32_t mode, int64_t capacity, int32_t* 
                          void* stream);
 
 /* ---- diagnostics --------------------------------------------------------- */
+/* Per-stage device timing of integrate calls (CUDA events on the caller's
+ * stream around each stage).  Stages, in order:
+ *   0 count (K1a + offsets scan)  1 fill (K1b)  2 sort (K2)  3 group (K3)
+ *   4 leaves (K4 hash + ordered allocation)  5 voxels (lookup + activation)
+ *   6 update (K5/K6 fused TSDF + semantic)
+ * svx_stage_times writes up to n last-frame stage times in ms and returns the
+ * number of stages (SVX_N_STAGES). */
+#define SVX_N_STAGES 7
+svx_status svx_set_profiling(svx_map* map, int32_t enable);
+int32_t svx_stage_times(svx_map* map, double* ms, int32_t n);
+
 const char* svx_last_error(void);
 int32_t svx_abi_version(void);
 /* Number of kernels this library launched since load (evidence counter). */

@@ -89,11 +89,15 @@ _SIGNATURES = {
     "svx_query_cosine": [_P, _P, _I64, _P, _P],
     "svx_classify": [_P, _P, _I32, _D, _D, _I64, _P, _P, _P, _P],
     "svx_label_map": [_P, _I32, _I64, _P, _P],
+    "svx_set_profiling": [_P, _I32],
+    "svx_reserve": [_P, _I64, _I64],
 }
 
-# every symbol include/svx.h declares (checked by tests/test_abi.py)
+STAGES = ("count", "fill", "sort", "group", "leaves", "voxels", "update")
+
+# every symbol include/svx.h declares (checked by tests/test_abi_and_config.py)
 EXPORTED = sorted(list(_SIGNATURES) + ["svx_last_error", "svx_abi_version",
-                                       "svx_kernel_launches"])
+                                       "svx_kernel_launches", "svx_stage_times"])
 
 
 def _load():
@@ -112,6 +116,8 @@ def _load():
     lib.svx_abi_version.restype = ctypes.c_int32
     lib.svx_kernel_launches.argtypes = []
     lib.svx_kernel_launches.restype = ctypes.c_int64
+    lib.svx_stage_times.argtypes = [_P, ctypes.POINTER(_D), _I32]
+    lib.svx_stage_times.restype = ctypes.c_int32
     return lib
 
 

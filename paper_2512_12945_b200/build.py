@@ -1,6 +1,6 @@
 """In-tree build of libsvx.so for sm_100a.
 
-    python -m paper_2512_12945_b200.build
+    python paper_2512_12945_b200/build.py [--force] [-v]
 
 Every translation unit is compiled with -fmad=false: the band walk, the
 per-voxel sums and the update arithmetic must round exactly like the

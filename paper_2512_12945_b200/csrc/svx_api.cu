@@ -156,6 +156,24 @@ svx_status reserve_blocks(svx_map* m, int64_t need, cudaStream_t s) {
     return SVX_OK;
 }
 
+#define STAGE_BEGIN(i) \
+    do { if (m->prof) { cudaEventRecord(m->st_ev[2 * (i)], s); m->st_mask |= 1u << (i); } } while (0)
+#define STAGE_END(i) \
+    do { if (m->prof) cudaEventRecord(m->st_ev[2 * (i) + 1], s); } while (0)
+
+void collect_stage_times(svx_map* m) {
+    for (int i = 0; i < SVX_N_STAGES; ++i) {
+        m->stage_ms[i] = 0.0;
+        if (!(m->st_mask & (1u << i))) continue;
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, m->st_ev[2 * i], m->st_ev[2 * i + 1]) == cudaSuccess)
+            m->stage_ms[i] = ms;
+        else
+            cudaGetLastError();
+    }
+    m->st_mask = 0;
+}
+
 svx_status integrate_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n,
                           const PoseParams& pp, const int32_t* labels_in, const void* feats_in,
                           int feats_f64, cudaStream_t s, svx_report* rep) {
@@ -200,6 +218,8 @@ svx_status integrate_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n
     SVX_CUDA(cudaMemcpyAsync(dc, hc, sizeof(FrameCtr), cudaMemcpyHostToDevice, s));
 
     // K1a: masks, ray setup, row counts, bbox
+    m->st_mask = 0;
+    STAGE_BEGIN(0);
     SVX_TRY(launch_count(m, pts, pts_f64, n, pp, labels, feats, feats_f64, s));
     size_t tmp = 0;
     SVX_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, ptr<int>(m->cnt), ptr<long long>(m->off),
@@ -208,6 +228,7 @@ svx_status integrate_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n
     SVX_CUDA(cub::DeviceScan::ExclusiveSum(m->cubtmp.p, tmp, ptr<int>(m->cnt),
                                            ptr<long long>(m->off), (int)n, s));
     count_launch();
+    STAGE_END(0);
     SVX_CUDA(cudaMemcpyAsync(hc, dc, sizeof(FrameCtr), cudaMemcpyDeviceToHost, s));
     SVX_CUDA(cudaStreamSynchronize(s));
 
@@ -225,6 +246,7 @@ svx_status integrate_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n
         SVX_CUDA(cudaEventSynchronize(m->ev1));
         float ms = 0.f;
         cudaEventElapsedTime(&ms, m->ev0, m->ev1);
+        if (m->prof) collect_stage_times(m);
         r.kernel_ms = ms;
         m->frames++;
         if (rep) *rep = r;
@@ -251,11 +273,14 @@ svx_status integrate_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n
     SVX_TRY(ensure(m->keys1, 8 * R, s));
     SVX_TRY(ensure(m->rid0, 4 * R, s));
     SVX_TRY(ensure(m->rid1, 4 * R, s));
+    STAGE_BEGIN(1);
     SVX_TRY(launch_fill(m, n, pp, kp, s));
+    STAGE_END(1);
 
     // K2: stable sort by voxel key -> (voxel, point, step) order
     unsigned long long* skeys = ptr<unsigned long long>(m->keys0);
     m->srid = ptr<int>(m->rid0);
+    STAGE_BEGIN(2);
     if (kp.nbits > 0) {
         cub::DoubleBuffer<unsigned long long> dk(ptr<unsigned long long>(m->keys0),
                                                  ptr<unsigned long long>(m->keys1));
@@ -267,11 +292,13 @@ svx_status integrate_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n
         skeys = dk.Current();
         m->srid = dv.Current();
     }
+    STAGE_END(2);
 
     // K3: unique voxels and their row runs
     SVX_TRY(ensure(m->ukeys, 8 * R, s));
     SVX_TRY(ensure(m->runlen, 4 * R, s));
     SVX_TRY(ensure(m->gstart, 8 * (R + 1), s));
+    STAGE_BEGIN(3);
     SVX_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, tmp, skeys, ptr<unsigned long long>(m->ukeys),
                                                 ptr<int>(m->runlen), &dc->n_groups, (int)R, s));
     SVX_TRY(ensure(m->cubtmp, tmp, s));
@@ -289,6 +316,7 @@ svx_status integrate_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n
     SVX_CUDA(cub::DeviceScan::ExclusiveSum(m->cubtmp.p, tmp, ptr<int>(m->runlen),
                                            ptr<long long>(m->gstart), (int)U, s));
     count_launch();
+    STAGE_END(3);
 
     // capacity for the worst case (every voxel and leaf new)
     SVX_TRY(reserve_blocks(m, m->nblocks + U, s));
@@ -307,6 +335,7 @@ svx_status integrate_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n
     SVX_CUDA(cudaMemsetAsync(m->newfirst.p, 0xFF, 4 * U, s));
 
     // K4: leaves
+    STAGE_BEGIN(4);
     SVX_TRY(launch_blocks(m, U, kp, s));
     SVX_CUDA(cudaMemcpyAsync(&hc->n_new_blocks, &dc->n_new_blocks, sizeof(unsigned long long),
                              cudaMemcpyDeviceToHost, s));
@@ -330,7 +359,9 @@ svx_status integrate_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n
         SVX_TRY(launch_assign_blocks(m, nnew, ptr<unsigned>(m->neworder2), s));
         m->nblocks += nnew;
     }
+    STAGE_END(4);
     // voxels: lookup, first-occurrence ids for new ones, activation
+    STAGE_BEGIN(5);
     SVX_TRY(launch_resolve(m, U, kp, s));
     SVX_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, ptr<int>(m->gnew), ptr<int>(m->grank),
                                            (int)U, s));
@@ -339,15 +370,19 @@ svx_status integrate_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n
                                            (int)U, s));
     count_launch();
     SVX_TRY(launch_activate(m, U, kp, s));
+    STAGE_END(5);
 
     // K5/K6: fused update
+    STAGE_BEGIN(6);
     SVX_TRY(launch_update(m, U, kp, pp, labels, feats, feats_f64, s));
+    STAGE_END(6);
 
     SVX_CUDA(cudaMemcpyAsync(hc, dc, sizeof(FrameCtr), cudaMemcpyDeviceToHost, s));
     SVX_CUDA(cudaEventRecord(m->ev1, s));
     SVX_CUDA(cudaEventSynchronize(m->ev1));
     float ms = 0.f;
     SVX_CUDA(cudaEventElapsedTime(&ms, m->ev0, m->ev1));
+    if (m->prof) collect_stage_times(m);
     m->nvox += (int64_t)hc->n_new_voxels;
     m->frames++;
     r.touched_voxels = U;
@@ -473,6 +508,8 @@ svx_status svx_destroy(svx_map* m) {
     if (m->h_ctr) cudaFreeHost(m->h_ctr);
     if (m->ev0) cudaEventDestroy(m->ev0);
     if (m->ev1) cudaEventDestroy(m->ev1);
+    for (cudaEvent_t e : m->st_ev)
+        if (e) cudaEventDestroy(e);
     delete m;
     return SVX_OK;
 }
@@ -505,6 +542,34 @@ svx_status svx_integrate_world(svx_map* m, const void* points_world, int32_t poi
     pp.sensor = 0;
     return integrate_impl(m, points_world, points_dtype == SVX_F64, n, pp, labels, feats,
                           feats_dtype == SVX_F64, (cudaStream_t)stream, report);
+}
+
+svx_status svx_reserve(svx_map* m, int64_t voxels, int64_t blocks) {
+    if (!m || voxels < 0 || blocks < 0) return fail(SVX_E_INPUT, "invalid reserve arguments");
+    SVX_TRY(set_device(m));
+    cudaStream_t s = 0;
+    SVX_TRY(reserve_blocks(m, std::max<int64_t>(blocks, m->nblocks), s));
+    SVX_TRY(reserve_voxels(m, std::max<int64_t>(voxels, m->nvox), s));
+    SVX_CUDA(cudaStreamSynchronize(s));
+    return SVX_OK;
+}
+
+svx_status svx_set_profiling(svx_map* m, int32_t enable) {
+    if (!m) return fail(SVX_E_INPUT, "null argument");
+    SVX_TRY(set_device(m));
+    if (enable) {
+        for (cudaEvent_t& e : m->st_ev)
+            if (!e) SVX_CUDA(cudaEventCreate(&e));
+    }
+    m->prof = enable != 0;
+    m->st_mask = 0;
+    return SVX_OK;
+}
+
+int32_t svx_stage_times(svx_map* m, double* ms, int32_t n) {
+    if (!m) return 0;
+    for (int i = 0; i < n && i < SVX_N_STAGES; ++i) ms[i] = m->stage_ms[i];
+    return SVX_N_STAGES;
 }
 
 svx_status svx_stats_get(svx_map* m, svx_stats* out) {

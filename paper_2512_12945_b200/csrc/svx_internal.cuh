@@ -102,6 +102,11 @@ struct svx_map {
     // query scratch
     svx::DevBuf act_cnt, act_off, act_vid, act_coord, q_buf, out_buf;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // optional per-stage timing (svx_set_profiling)
+    bool prof = false;
+    cudaEvent_t st_ev[2 * SVX_N_STAGES] = {};
+    unsigned st_mask = 0;
+    double stage_ms[SVX_N_STAGES] = {};
 };
 
 namespace svx {

@@ -422,6 +422,20 @@ class Mapper:
                                 labels.ctypes.data if n else None, None))
         return self._tsdf_view.active_coords(), labels
 
+    def reserve(self, voxels: int, blocks: int) -> None:
+        """Pre-size the device pools for `voxels` active voxels in `blocks` leaves."""
+        check(lib.svx_reserve(self._handle, int(voxels), int(blocks)))
+
+    def set_profiling(self, enable: bool = True) -> None:
+        """Record per-stage device times of each integrate (svx_set_profiling)."""
+        check(lib.svx_set_profiling(self._handle, int(bool(enable))))
+
+    def stage_times(self) -> dict:
+        """Last frame's per-stage device milliseconds (needs set_profiling)."""
+        buf = (ctypes.c_double * len(_lib.STAGES))()
+        lib.svx_stage_times(self._handle, buf, len(_lib.STAGES))
+        return {name: float(buf[i]) for i, name in enumerate(_lib.STAGES)}
+
     def active_count(self) -> int:
         c = ctypes.c_int64()
         check(lib.svx_active_count(self._handle, ctypes.byref(c)))
