@@ -183,12 +183,14 @@ svx_status svx_label_map(svx_map* map, int32_t mode, int64_t capacity, int32_t* 
 /* ---- diagnostics --------------------------------------------------------- */
 /* Per-stage device timing of integrate calls (CUDA events on the caller's
  * stream around each stage).  Stages, in order:
- *   0 count (K1a + offsets scan)  1 fill (K1b)  2 sort (K2)  3 group (K3)
- *   4 leaves (K4 hash + ordered allocation)  5 voxels (lookup + activation)
- *   6 update (K5/K6 fused TSDF + semantic)
+ *   0 march (K1: masks + band walk + voxel grouping counts)
+ *   1 compact (K2: touched-voxel list + row segments + gate)
+ *   2 scatter (K3: rows into voxel segments)
+ *   3 voxels (K4: leaf find-or-insert, voxel activation)
+ *   4 update (K5/K6: fused TSDF + semantic update)
  * svx_stage_times writes up to n last-frame stage times in ms and returns the
  * number of stages (SVX_N_STAGES). */
-#define SVX_N_STAGES 7
+#define SVX_N_STAGES 5
 svx_status svx_set_profiling(svx_map* map, int32_t enable);
 int32_t svx_stage_times(svx_map* map, double* ms, int32_t n);
 

@@ -1,13 +1,15 @@
 // svx_api.cu -- C ABI entry points and the per-frame orchestration.
 //
-// Frame pipeline on the caller's stream:
-//   K1a count   validation masks + DDA row count + frame bbox   (svx_march.cu)
-//   scan        row offsets                                       (CUB)
-//   K1b fill    (voxel key, point) rows                           (svx_march.cu)
-//   K2  sort    stable radix sort on the packed voxel key         (CUB)
-//   K3  group   run-length encode -> unique voxels + row counts   (CUB)
-//   K4  blocks  leaf hash find-or-insert, first-occurrence ids    (svx_update.cu)
-//   K5/6 update fused TSDF + closed/open semantic update          (svx_update.cu)
+// Frame pipeline on the caller's stream, one host synchronisation per frame
+// (DESIGN.md "Per-frame pipeline"):
+//   K1 march    masks, ray setup, fp64 band walk, frame-table insert + counts (svx_march.cu)
+//   K2 compact  touched voxels -> list + row segments; device-side gate        (svx_march.cu)
+//   K3 scatter  second walk: point index -> its voxel's segment                (svx_march.cu)
+//   K4 voxels   leaf find-or-insert + creation stamp, voxel activation         (svx_update.cu)
+//   K5 update   fused TSDF + closed/open update, rows re-sorted per voxel      (svx_update.cu)
+// Kernels after K1 size themselves from device counters; a frame whose
+// scratch was too small (or whose keys need a different base) is detected by
+// the gate before any map mutation and re-run.
 #include <cuda_runtime.h>
 #include <limits.h>
 #include <math.h>
@@ -68,11 +70,6 @@ void release(DevBuf& buf) {
 
 namespace {
 
-__global__ void k_iota(int64_t n, unsigned* out) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) out[i] = (unsigned)i;
-}
-
 bool is_device_ptr(const void* p) {
     if (!p) return false;
     cudaPointerAttributes a;
@@ -99,15 +96,6 @@ svx_status stage_in(const void* p, size_t bytes, DevBuf& stage, cudaStream_t s, 
     SVX_CUDA(cudaMemcpyAsync(stage.p, p, bytes, cudaMemcpyHostToDevice, s));
     *out = stage.p;
     return SVX_OK;
-}
-
-int bitlen(long long v) {
-    int b = 0;
-    while (v > 0) {
-        ++b;
-        v >>= 1;
-    }
-    return b;
 }
 
 size_t tsdf_elem(const svx_map* m) { return m->cfg.tsdf_dtype == SVX_F64 ? 8 : 4; }
@@ -137,6 +125,7 @@ svx_status reserve_blocks(svx_map* m, int64_t need, cudaStream_t s) {
     if (need > m->bcap) {
         int64_t cap = std::max<int64_t>(need, 2 * m->bcap);
         SVX_TRY(ensure(m->bcoord, sizeof(int4) * cap, s, true));
+        SVX_TRY(ensure(m->bkey, sizeof(unsigned long long) * cap, s, true, 0xFF));
         SVX_TRY(ensure(m->bmask, sizeof(unsigned long long) * kMaskWords * cap, s, true, 0));
         SVX_TRY(ensure(m->bslot, sizeof(int) * kLeafVolume * cap, s, true, 0xFF));
         m->bcap = cap;
@@ -153,6 +142,38 @@ svx_status reserve_blocks(svx_map* m, int64_t need, cudaStream_t s) {
         m->hash = nt;
         m->hcap = want;
     }
+    return SVX_OK;
+}
+
+// Per-frame scratch for `ucap` unique voxels / `rcap` rows / `n` points.
+svx_status reserve_frame(svx_map* m, int64_t n, cudaStream_t s) {
+    int64_t want = 1024;
+    while (want < 2 * (int64_t)m->ucap) want <<= 1;
+    if (want > m->fcap) {
+        release(m->fkey);
+        release(m->fcount);
+        release(m->fcur);
+        release(m->foff);
+        SVX_TRY(ensure(m->fkey, 8 * want, s, false, 0xFF));
+        SVX_TRY(ensure(m->fcount, 4 * want, s, false, 0));
+        SVX_TRY(ensure(m->fcur, 4 * want, s, false, 0));
+        SVX_TRY(ensure(m->foff, 4 * want, s));
+        m->fcap = want;
+    }
+    SVX_TRY(ensure(m->ulist, 4 * m->ucap, s));
+    SVX_TRY(ensure(m->ukey, 8 * m->ucap, s));
+    SVX_TRY(ensure(m->gvid, 4 * m->ucap, s));
+    SVX_TRY(ensure(m->longlist, 8 * m->ucap, s));   // long list, then huge list
+    SVX_TRY(ensure(m->srid, 4 * m->rcap, s));
+    SVX_TRY(ensure(m->bitmap, (size_t)4 * huge_warps() * ((n + 31) / 32 + 1), s));
+    SVX_TRY(ensure(m->ray, sizeof(double4) * n, s));
+    return SVX_OK;
+}
+
+svx_status clear_frame_table(svx_map* m, cudaStream_t s) {
+    SVX_CUDA(cudaMemsetAsync(m->fkey.p, 0xFF, 8 * m->fcap, s));
+    SVX_CUDA(cudaMemsetAsync(m->fcount.p, 0, 4 * m->fcap, s));
+    SVX_CUDA(cudaMemsetAsync(m->fcur.p, 0, 4 * m->fcap, s));
     return SVX_OK;
 }
 
@@ -173,6 +194,8 @@ void collect_stage_times(svx_map* m) {
     }
     m->st_mask = 0;
 }
+
+long long floor_div_voxel(double v, double h) { return (long long)floor(v / h); }
 
 svx_status integrate_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n,
                           const PoseParams& pp, const int32_t* labels_in, const void* feats_in,
@@ -204,191 +227,121 @@ svx_status integrate_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n
                          &feats));
     const int32_t* labels = (const int32_t*)labv;
 
-    SVX_TRY(ensure(m->ray, sizeof(double4) * n, s));
-    SVX_TRY(ensure(m->cnt, sizeof(int) * n, s));
-    SVX_TRY(ensure(m->off, sizeof(long long) * (n + 1), s));
+    // Capacity guesses for the first frame: a ray's band crosses at most
+    // 3 * (band length / h + 1) voxels; later frames adapt to what was seen.
+    const double h = m->cfg.voxel_size;
+    double band = m->cfg.space_carving ? m->cfg.max_range + m->cfg.truncation
+                                       : 2.0 * m->cfg.truncation;
+    uint64_t per_ray = (uint64_t)std::min(64.0, 3.0 * (band / h + 1.0) + 3.0);
+    m->rcap = std::max<uint64_t>(m->rcap, (uint64_t)n * per_ray);
+    m->ucap = std::max<uint64_t>(m->ucap, std::min<uint64_t>(m->rcap, (uint64_t)n * 16));
 
-    FrameCtr* hc = m->h_ctr;
-    memset(hc, 0, sizeof(FrameCtr));
-    for (int a = 0; a < 3; ++a) {
-        hc->bbox_min[a] = LLONG_MAX;
-        hc->bbox_max[a] = LLONG_MIN;
+    KeyPack kp;
+    {
+        const long long half = 1LL << (kPackBits - 1);
+        kp.base[0] = floor_div_voxel(pp.t[0], h) - half;
+        kp.base[1] = floor_div_voxel(pp.t[1], h) - half;
+        kp.base[2] = floor_div_voxel(pp.t[2], h) - half;
     }
+    FrameCtr* hc = m->h_ctr;
     FrameCtr* dc = ptr<FrameCtr>(m->ctr);
-    SVX_CUDA(cudaMemcpyAsync(dc, hc, sizeof(FrameCtr), cudaMemcpyHostToDevice, s));
+    for (int attempt = 0;; ++attempt) {
+        if (attempt >= 6) return fail(SVX_E_INTERNAL, "frame scratch could not be sized");
+        SVX_TRY(reserve_frame(m, n, s));
+        SVX_TRY(reserve_blocks(m, m->nblocks + (int64_t)m->ucap, s));
+        SVX_TRY(reserve_voxels(m, m->nvox + (int64_t)m->ucap, s));
+        FrameCaps fc;
+        fc.ucap = m->ucap;
+        fc.rcap = m->rcap;
+        fc.fmask = m->fcap - 1;
+        fc.frame = (int)m->frames;
 
-    // K1a: masks, ray setup, row counts, bbox
-    m->st_mask = 0;
-    STAGE_BEGIN(0);
-    SVX_TRY(launch_count(m, pts, pts_f64, n, pp, labels, feats, feats_f64, s));
-    size_t tmp = 0;
-    SVX_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, ptr<int>(m->cnt), ptr<long long>(m->off),
-                                           (int)n, s));
-    SVX_TRY(ensure(m->cubtmp, tmp, s));
-    SVX_CUDA(cub::DeviceScan::ExclusiveSum(m->cubtmp.p, tmp, ptr<int>(m->cnt),
-                                           ptr<long long>(m->off), (int)n, s));
-    count_launch();
-    STAGE_END(0);
-    SVX_CUDA(cudaMemcpyAsync(hc, dc, sizeof(FrameCtr), cudaMemcpyDeviceToHost, s));
-    SVX_CUDA(cudaStreamSynchronize(s));
+        memset(hc, 0, sizeof(FrameCtr));
+        for (int a = 0; a < 3; ++a) {
+            hc->bbox_min[a] = LLONG_MAX;
+            hc->bbox_max[a] = LLONG_MIN;
+        }
+        hc->nblocks = (unsigned long long)m->nblocks;
+        hc->nvox = (unsigned long long)m->nvox;
+        SVX_CUDA(cudaMemcpyAsync(dc, hc, sizeof(FrameCtr), cudaMemcpyHostToDevice, s));
 
-    if (hc->err_budget)
-        return fail(SVX_E_INTERNAL, "ray band exceeds step budget; shrink max_range or grow voxels");
+        m->st_mask = 0;
+        STAGE_BEGIN(0);
+        SVX_TRY(launch_march(m, pts, pts_f64, n, pp, kp, fc, labels, feats, feats_f64, s));
+        STAGE_END(0);
+        STAGE_BEGIN(1);
+        SVX_TRY(launch_compact(m, fc, s));
+        STAGE_END(1);
+        STAGE_BEGIN(2);
+        SVX_TRY(launch_scatter(m, n, pp, kp, fc, s));
+        STAGE_END(2);
+        STAGE_BEGIN(3);
+        SVX_TRY(launch_voxels(m, kp, fc, s));
+        STAGE_END(3);
+        STAGE_BEGIN(4);
+        SVX_TRY(launch_update(m, kp, pp, fc, labels, feats, feats_f64, n, s));
+        STAGE_END(4);
+        SVX_CUDA(cudaMemcpyAsync(hc, dc, sizeof(FrameCtr), cudaMemcpyDeviceToHost, s));
+        SVX_CUDA(cudaEventRecord(m->ev1, s));
+        SVX_CUDA(cudaEventSynchronize(m->ev1));
+
+        // the reference's pre-allocation checks, in its order (_core.pyx:661-712, :386-387)
+        if (hc->err_budget) {
+            SVX_TRY(clear_frame_table(m, s));
+            return fail(SVX_E_INTERNAL, "ray band exceeds step budget; shrink max_range or grow voxels");
+        }
+        if (hc->rows) {
+            bool extent = false, range = false;
+            for (int a = 0; a < 3; ++a) {
+                if (hc->bbox_max[a] - hc->bbox_min[a] >= (1LL << kPackBits)) extent = true;
+                if (llabs(hc->bbox_min[a]) >= kCoordLimit || llabs(hc->bbox_max[a]) >= kCoordLimit)
+                    range = true;
+            }
+            if (extent) {
+                SVX_TRY(clear_frame_table(m, s));
+                return fail(SVX_E_INTERNAL,
+                            "frame voxel extent exceeds 2^21 per axis; shrink max_range or grow voxels");
+            }
+            if (range) {
+                SVX_TRY(clear_frame_table(m, s));
+                return fail(SVX_E_RANGE, "voxel coordinate beyond +/-2^30 addressable range");
+            }
+        }
+        if (hc->abort) {
+            // retry with a re-based key (pack) or bigger scratch (capacity)
+            SVX_TRY(clear_frame_table(m, s));
+            if (hc->err_pack)
+                for (int a = 0; a < 3; ++a) kp.base[a] = hc->bbox_min[a];
+            if (hc->err_probe || hc->n_groups > m->ucap || hc->rows_c > m->rcap ||
+                hc->rows > m->rcap) {
+                m->rcap = std::max<uint64_t>(2 * m->rcap, hc->rows + hc->rows / 2);
+                m->ucap = std::max<uint64_t>(2 * m->ucap,
+                                             std::min<uint64_t>(m->rcap, hc->n_groups * 2));
+            }
+            SVX_CUDA(cudaStreamSynchronize(s));
+            continue;
+        }
+        break;
+    }
+    float ms = 0.f;
+    SVX_CUDA(cudaEventElapsedTime(&ms, m->ev0, m->ev1));
+    if (m->prof) collect_stage_times(m);
     r.skipped_nonfinite = (int64_t)hc->nonfinite;
     r.skipped_range = (int64_t)hc->range;
     r.skipped_degenerate = (int64_t)hc->degenerate;
     r.skipped_bad_label = (int64_t)hc->bad_label;
     r.points_used = (int64_t)hc->used;
     r.band_hits = (int64_t)hc->band_hits;
-    const int64_t R = (int64_t)hc->rows;
-    if (R == 0) {
-        SVX_CUDA(cudaEventRecord(m->ev1, s));
-        SVX_CUDA(cudaEventSynchronize(m->ev1));
-        float ms = 0.f;
-        cudaEventElapsedTime(&ms, m->ev0, m->ev1);
-        if (m->prof) collect_stage_times(m);
-        r.kernel_ms = ms;
-        m->frames++;
-        if (rep) *rep = r;
-        return SVX_OK;
-    }
-    if (R >= (int64_t)INT_MAX) return fail(SVX_E_INPUT, "band rows per frame exceed 2^31-1");
-    long long ext[3];
-    for (int a = 0; a < 3; ++a) ext[a] = hc->bbox_max[a] - hc->bbox_min[a];
-    if (std::max(ext[0], std::max(ext[1], ext[2])) >= (1LL << kPackBits))
-        return fail(SVX_E_INTERNAL,
-                    "frame voxel extent exceeds 2^21 per axis; shrink max_range or grow voxels");
-    for (int a = 0; a < 3; ++a)
-        if (llabs(hc->bbox_min[a]) >= kCoordLimit || llabs(hc->bbox_max[a]) >= kCoordLimit)
-            return fail(SVX_E_RANGE, "voxel coordinate beyond +/-2^30 addressable range");
-    KeyPack kp;
-    for (int a = 0; a < 3; ++a) kp.mn[a] = (int)hc->bbox_min[a];
-    const int bx = bitlen(ext[0]), by = bitlen(ext[1]), bz = bitlen(ext[2]);
-    kp.bz = bz;
-    kp.byz = by + bz;
-    kp.nbits = bx + by + bz;
-
-    // K1b: rows in (point, step) order
-    SVX_TRY(ensure(m->keys0, 8 * R, s));
-    SVX_TRY(ensure(m->keys1, 8 * R, s));
-    SVX_TRY(ensure(m->rid0, 4 * R, s));
-    SVX_TRY(ensure(m->rid1, 4 * R, s));
-    STAGE_BEGIN(1);
-    SVX_TRY(launch_fill(m, n, pp, kp, s));
-    STAGE_END(1);
-
-    // K2: stable sort by voxel key -> (voxel, point, step) order
-    unsigned long long* skeys = ptr<unsigned long long>(m->keys0);
-    m->srid = ptr<int>(m->rid0);
-    STAGE_BEGIN(2);
-    if (kp.nbits > 0) {
-        cub::DoubleBuffer<unsigned long long> dk(ptr<unsigned long long>(m->keys0),
-                                                 ptr<unsigned long long>(m->keys1));
-        cub::DoubleBuffer<int> dv(ptr<int>(m->rid0), ptr<int>(m->rid1));
-        SVX_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, (int)R, 0, kp.nbits, s));
-        SVX_TRY(ensure(m->cubtmp, tmp, s));
-        SVX_CUDA(cub::DeviceRadixSort::SortPairs(m->cubtmp.p, tmp, dk, dv, (int)R, 0, kp.nbits, s));
-        count_launch();
-        skeys = dk.Current();
-        m->srid = dv.Current();
-    }
-    STAGE_END(2);
-
-    // K3: unique voxels and their row runs
-    SVX_TRY(ensure(m->ukeys, 8 * R, s));
-    SVX_TRY(ensure(m->runlen, 4 * R, s));
-    SVX_TRY(ensure(m->gstart, 8 * (R + 1), s));
-    STAGE_BEGIN(3);
-    SVX_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, tmp, skeys, ptr<unsigned long long>(m->ukeys),
-                                                ptr<int>(m->runlen), &dc->n_groups, (int)R, s));
-    SVX_TRY(ensure(m->cubtmp, tmp, s));
-    SVX_CUDA(cub::DeviceRunLengthEncode::Encode(m->cubtmp.p, tmp, skeys,
-                                                ptr<unsigned long long>(m->ukeys),
-                                                ptr<int>(m->runlen), &dc->n_groups, (int)R, s));
-    count_launch();
-    SVX_CUDA(cudaMemcpyAsync(&hc->n_groups, &dc->n_groups, sizeof(unsigned long long),
-                             cudaMemcpyDeviceToHost, s));
-    SVX_CUDA(cudaStreamSynchronize(s));
-    const int64_t U = (int64_t)hc->n_groups;
-    SVX_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, ptr<int>(m->runlen),
-                                           ptr<long long>(m->gstart), (int)U, s));
-    SVX_TRY(ensure(m->cubtmp, tmp, s));
-    SVX_CUDA(cub::DeviceScan::ExclusiveSum(m->cubtmp.p, tmp, ptr<int>(m->runlen),
-                                           ptr<long long>(m->gstart), (int)U, s));
-    count_launch();
-    STAGE_END(3);
-
-    // capacity for the worst case (every voxel and leaf new)
-    SVX_TRY(reserve_blocks(m, m->nblocks + U, s));
-    SVX_TRY(reserve_voxels(m, m->nvox + U, s));
-    SVX_TRY(ensure(m->gblock, 4 * U, s));
-    SVX_TRY(ensure(m->gvid, 4 * U, s));
-    SVX_TRY(ensure(m->gnew, 4 * U, s));
-    SVX_TRY(ensure(m->grank, 4 * U, s));
-    SVX_TRY(ensure(m->newpos, 4 * U, s));
-    SVX_TRY(ensure(m->newcoord, sizeof(int4) * U, s));
-    SVX_TRY(ensure(m->newfirst, 4 * U, s));
-    SVX_TRY(ensure(m->newfirst2, 4 * U, s));
-    SVX_TRY(ensure(m->neworder, 4 * U, s));
-    SVX_TRY(ensure(m->neworder2, 4 * U, s));
-    SVX_TRY(ensure(m->tmp2id, 4 * U, s));
-    SVX_CUDA(cudaMemsetAsync(m->newfirst.p, 0xFF, 4 * U, s));
-
-    // K4: leaves
-    STAGE_BEGIN(4);
-    SVX_TRY(launch_blocks(m, U, kp, s));
-    SVX_CUDA(cudaMemcpyAsync(&hc->n_new_blocks, &dc->n_new_blocks, sizeof(unsigned long long),
-                             cudaMemcpyDeviceToHost, s));
-    SVX_CUDA(cudaStreamSynchronize(s));
-    const int64_t nnew = (int64_t)hc->n_new_blocks;
-    if (nnew > 0) {
-        k_iota<<<grid_for(nnew, 256), 256, 0, s>>>(nnew, ptr<unsigned>(m->neworder));
-        SVX_LAUNCHED();
-        SVX_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, ptr<unsigned>(m->newfirst),
-                                                 ptr<unsigned>(m->newfirst2),
-                                                 ptr<unsigned>(m->neworder),
-                                                 ptr<unsigned>(m->neworder2), (int)nnew, 0,
-                                                 std::max(1, bitlen(U)), s));
-        SVX_TRY(ensure(m->cubtmp, tmp, s));
-        SVX_CUDA(cub::DeviceRadixSort::SortPairs(m->cubtmp.p, tmp, ptr<unsigned>(m->newfirst),
-                                                 ptr<unsigned>(m->newfirst2),
-                                                 ptr<unsigned>(m->neworder),
-                                                 ptr<unsigned>(m->neworder2), (int)nnew, 0,
-                                                 std::max(1, bitlen(U)), s));
-        count_launch();
-        SVX_TRY(launch_assign_blocks(m, nnew, ptr<unsigned>(m->neworder2), s));
-        m->nblocks += nnew;
-    }
-    STAGE_END(4);
-    // voxels: lookup, first-occurrence ids for new ones, activation
-    STAGE_BEGIN(5);
-    SVX_TRY(launch_resolve(m, U, kp, s));
-    SVX_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, ptr<int>(m->gnew), ptr<int>(m->grank),
-                                           (int)U, s));
-    SVX_TRY(ensure(m->cubtmp, tmp, s));
-    SVX_CUDA(cub::DeviceScan::ExclusiveSum(m->cubtmp.p, tmp, ptr<int>(m->gnew), ptr<int>(m->grank),
-                                           (int)U, s));
-    count_launch();
-    SVX_TRY(launch_activate(m, U, kp, s));
-    STAGE_END(5);
-
-    // K5/K6: fused update
-    STAGE_BEGIN(6);
-    SVX_TRY(launch_update(m, U, kp, pp, labels, feats, feats_f64, s));
-    STAGE_END(6);
-
-    SVX_CUDA(cudaMemcpyAsync(hc, dc, sizeof(FrameCtr), cudaMemcpyDeviceToHost, s));
-    SVX_CUDA(cudaEventRecord(m->ev1, s));
-    SVX_CUDA(cudaEventSynchronize(m->ev1));
-    float ms = 0.f;
-    SVX_CUDA(cudaEventElapsedTime(&ms, m->ev0, m->ev1));
-    if (m->prof) collect_stage_times(m);
-    m->nvox += (int64_t)hc->n_new_voxels;
-    m->frames++;
-    r.touched_voxels = U;
-    r.new_blocks = nnew;
-    r.new_voxels = (int64_t)hc->n_new_voxels;
+    r.touched_voxels = (int64_t)hc->n_groups;
+    r.new_blocks = (int64_t)hc->nblocks - m->nblocks;
+    r.new_voxels = (int64_t)hc->nvox - m->nvox;
     r.kernel_ms = ms;
+    m->nblocks = (int64_t)hc->nblocks;
+    m->nvox = (int64_t)hc->nvox;
+    m->frames++;
+    // adapt the scratch to what this frame needed (headroom for the next)
+    if (hc->n_groups * 10 > m->ucap * 7) m->ucap = hc->n_groups * 2;
+    if (hc->rows_c * 10 > m->rcap * 8) m->rcap = hc->rows_c * 2;
     if (rep) *rep = r;
     return SVX_OK;
 }
@@ -497,13 +450,12 @@ svx_status svx_create(const svx_config* cfg, svx_map** out) {
 svx_status svx_destroy(svx_map* m) {
     if (!m) return SVX_OK;
     cudaSetDevice(m->cfg.device);
-    DevBuf* bufs[] = {&m->hash, &m->bcoord, &m->bmask, &m->bslot, &m->vd, &m->vw, &m->s0, &m->s1,
-                      &m->in_pts, &m->in_lab, &m->in_feat, &m->ray, &m->cnt, &m->off, &m->keys0,
-                      &m->keys1, &m->rid0, &m->rid1, &m->ukeys, &m->runlen, &m->gstart,
-                      &m->gblock, &m->gvid, &m->gnew, &m->grank, &m->newpos, &m->newcoord,
-                      &m->newfirst, &m->newfirst2, &m->neworder, &m->neworder2, &m->tmp2id,
-                      &m->cubtmp, &m->ctr, &m->act_cnt, &m->act_off, &m->act_vid, &m->act_coord,
-                      &m->q_buf, &m->out_buf};
+    DevBuf* bufs[] = {&m->hash, &m->bcoord, &m->bkey, &m->bmask, &m->bslot, &m->vd, &m->vw,
+                      &m->s0, &m->s1, &m->in_pts, &m->in_lab, &m->in_feat, &m->ray, &m->fkey,
+                      &m->fcount, &m->foff, &m->fcur, &m->ulist, &m->ukey, &m->gvid,
+                      &m->longlist, &m->srid, &m->bitmap, &m->cubtmp, &m->ctr, &m->ord0,
+                      &m->ord1, &m->ordk0, &m->ordk1, &m->ordf0, &m->ordf1, &m->act_cnt,
+                      &m->act_off, &m->act_vid, &m->act_coord, &m->q_buf, &m->out_buf};
     for (DevBuf* b : bufs) release(*b);
     if (m->h_ctr) cudaFreeHost(m->h_ctr);
     if (m->ev0) cudaEventDestroy(m->ev0);

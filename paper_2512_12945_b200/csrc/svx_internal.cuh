@@ -1,16 +1,19 @@
 // svx_internal.cuh -- shared definitions of the B200 integration engine.
 //
-// HBM layout (see DESIGN.md "Data layout"):
-//   block hash   int4[hcap]        {bx, by, bz, val}; val = block id, EMPTY, BUSY or PENDING
-//   block pool   int4 bcoord[bcap]  leaf coords (voxel >> 3), w = creation frame
-//                u64  bmask[bcap*8] 512-bit active mask (GridCore.leaf_mask, _core.pyx:92)
-//                i32  bslot[bcap*512] slot -> voxel id (-1 = inactive)
-//   voxel pool   d[vcap], w[vcap]        TSDF (f64 reference layout or f32 compact)
-//                sem0[vcap*C|D]          closed counts or open mean m
-//                sem1[vcap*D]            open scale beta
-// Voxel ids are dense, assigned in activation order and never recycled, so a
-// voxel's payload row is contiguous (the NanoVDB "index grid" idea) and the
-// open-set means form a dense (V, D) matrix for query scoring.
+// HBM layout (DESIGN.md "Data layout"):
+//   leaf hash    int4[hcap]          {lx, ly, lz, id}; id = EMPTY / BUSY / leaf id
+//   leaf pool    int4  bcoord[bcap]  leaf coords (voxel >> 3), w = creation frame
+//                u64   bkey[bcap]    creation stamp: min frame-key of its voxels in
+//                                    the creating frame (first-occurrence order)
+//                u64   bmask[bcap*8] 512-bit active mask (GridCore.leaf_mask, _core.pyx:92)
+//                i32   bslot[bcap*512] slot -> voxel id (-1 = inactive)
+//   voxel pool   d[vcap], w[vcap]    TSDF (f64 reference layout or f32 compact)
+//                sem0[vcap*C|D]      closed counts or open mean m
+//                sem1[vcap*D]        open scale beta
+//   frame hash   u64 fkey[fcap], u32 fcount/foff/fcur[fcap]  per-frame voxel groups
+// Voxel ids are dense and never recycled, so a voxel's payload row is
+// contiguous (the NanoVDB index-grid idea) and open-set means form a dense
+// (V, D) matrix for query scoring.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -23,19 +26,20 @@
 namespace svx {
 
 constexpr int kLeafLog2 = 3;                 // TreeConfig.leaf_log2 default (config.py:26)
-constexpr int kLeafSide = 1 << kLeafLog2;    // 8
 constexpr int kLeafVolume = 512;             // 8^3
 constexpr int kMaskWords = 8;                // 512 bits
-constexpr int kInternalLog2 = 4;             // TreeConfig.internal_log2 (config.py:27), stats only
 constexpr int64_t kCoordLimit = int64_t(1) << 30;   // coords.py:41 COORD_LIMIT
 constexpr int kPackBits = 21;                       // _core.pyx:34 PACK_BITS
+constexpr long long kPackMask = (1LL << kPackBits) - 1;
 constexpr int64_t kStepBudget = int64_t(1) << 20;   // _core.pyx:35 STEP_BUDGET
+constexpr unsigned long long kKeyEmpty = ~0ULL;
 
 constexpr int kHashEmpty = -1;
 constexpr int kHashBusy = -2;
-constexpr int kHashPendingBase = -3;  // PENDING(tmp) = -3 - tmp
 
-// Per-frame device counters, copied back once per frame.
+constexpr int kShortMax = 16;   // segments up to this many rows: thread-per-voxel update
+
+// Per-frame device counters and flags, copied back once per frame.
 struct FrameCtr {
     unsigned long long nonfinite;
     unsigned long long range;
@@ -43,14 +47,21 @@ struct FrameCtr {
     unsigned long long bad_label;
     unsigned long long used;
     unsigned long long band_hits;   // rows emitted before the w <= 0 drop
-    unsigned long long rows;        // rows kept (w > 0)
+    unsigned long long rows;        // rows kept (w > 0), counted by the march
+    unsigned long long n_groups;    // unique voxels (U), from the compaction
+    unsigned long long rows_c;      // rows (R), from the compaction
+    unsigned long long n_long;      // voxels routed to the long-segment update
+    unsigned long long n_huge;      // voxels routed to the huge-segment update
     unsigned long long n_new_blocks;
     unsigned long long n_new_voxels;
-    unsigned long long n_groups;    // written by RLE (num runs)
-    long long bbox_min[3];          // over kept rows (after the w <= 0 drop)
+    unsigned long long nblocks;     // device copy of the leaf count (allocation counter)
+    unsigned long long nvox;        // device copy of the voxel count (allocation counter)
+    long long bbox_min[3];          // over kept rows
     long long bbox_max[3];
     int err_budget;                 // a ray exceeded the DDA step budget
-    int pad[3];
+    int err_pack;                   // a key offset left the 21-bit field (retry with bbox base)
+    int err_probe;                  // frame hash full (retry with a bigger table)
+    int abort;                      // set by the compaction: skip all mutation
 };
 
 // Growable device buffer.
@@ -73,11 +84,31 @@ struct PoseParams {
     int sensor;      // 1: transform points by (R, t); 0: points already world, origin = t
 };
 
+// Frame key: voxel offsets from `base` packed 21 bits per axis, x-major, so
+// key order is the reference's lexicographic voxel order (_core.pyx:727-732).
 struct KeyPack {
-    int mn[3];
-    int bz, byz;     // shift amounts: key = (dx << byz) | (dy << bz) | dz
-    int nbits;
+    long long base[3];
 };
+
+// Capacities of the per-frame scratch for this attempt.
+struct FrameCaps {
+    unsigned long long ucap;   // unique voxels
+    unsigned long long rcap;   // rows
+    long long fmask;           // frame hash capacity - 1
+    int frame;                 // frame stamp
+};
+
+__host__ __device__ inline unsigned long long pack_key(long long dx, long long dy, long long dz) {
+    return ((unsigned long long)dx << (2 * kPackBits)) | ((unsigned long long)dy << kPackBits) |
+           (unsigned long long)dz;
+}
+
+__host__ __device__ inline void unpack_key(unsigned long long key, const KeyPack& kp, long long& x,
+                                           long long& y, long long& z) {
+    x = (long long)(key >> (2 * kPackBits)) + kp.base[0];
+    y = (long long)((key >> kPackBits) & kPackMask) + kp.base[1];
+    z = (long long)(key & kPackMask) + kp.base[2];
+}
 
 }  // namespace svx
 
@@ -86,21 +117,24 @@ struct svx_map {
     int payload_d = 0;     // C (closed) or D (open)
     // persistent state
     svx::DevBuf hash;  int64_t hcap = 0;
-    svx::DevBuf bcoord, bmask, bslot;  int64_t bcap = 0, nblocks = 0;
-    svx::DevBuf vd, vw, s0, s1;        int64_t vcap = 0, nvox = 0;
+    svx::DevBuf bcoord, bkey, bmask, bslot;  int64_t bcap = 0, nblocks = 0;
+    svx::DevBuf vd, vw, s0, s1;              int64_t vcap = 0, nvox = 0;
     int64_t frames = 0;
     // per-frame scratch
     svx::DevBuf in_pts, in_lab, in_feat;
-    svx::DevBuf ray, cnt, off;
-    svx::DevBuf keys0, keys1, rid0, rid1;
-    int* srid = nullptr;   // sorted row -> point index (one of rid0/rid1 after the sort)
-    svx::DevBuf ukeys, runlen, gstart, gblock, gvid, gnew, grank;
-    svx::DevBuf newpos, newcoord, newfirst, newfirst2, neworder, neworder2, tmp2id;
+    svx::DevBuf ray;
+    svx::DevBuf fkey, fcount, foff, fcur;  int64_t fcap = 0;
+    svx::DevBuf ulist, ukey, gvid, longlist, srid, bitmap;
+    uint64_t ucap = 0, rcap = 0;
     svx::DevBuf cubtmp;
     svx::DevBuf ctr;      // FrameCtr
     svx::FrameCtr* h_ctr = nullptr;  // pinned mirror
     // query scratch
+    svx::DevBuf ord0, ord1, ordk0, ordk1, ordf0, ordf1;  // leaf order (by creation stamp)
+    int64_t ord_nblocks = -1;
+    int* leaf_order = nullptr;
     svx::DevBuf act_cnt, act_off, act_vid, act_coord, q_buf, out_buf;
+    int64_t act_valid_frames = -1;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     // optional per-stage timing (svx_set_profiling)
     bool prof = false;
@@ -152,8 +186,9 @@ inline int grid_for(int64_t n, int threads) {
     return (int)(g < 1 ? 1 : g);
 }
 
-// ---- block hash ------------------------------------------------------------
-// 64-bit finaliser-style mix of the three leaf coordinates.
+constexpr int kPersistentBlocks = 148 * 8;   // grid-stride kernels over device-side counts
+
+// ---- hashing -----------------------------------------------------------------
 __host__ __device__ inline uint64_t block_hash(int a, int b, int c) {
     uint64_t h = (uint64_t)(uint32_t)a * 0xD6E8FEB86659FD93ULL;
     h += (uint64_t)(uint32_t)b * 0xA0761D6478BD642FULL;
@@ -165,7 +200,16 @@ __host__ __device__ inline uint64_t block_hash(int a, int b, int c) {
     return h;
 }
 
-// Read-only lookup (no concurrent inserts).  Returns block id or -1.
+__host__ __device__ inline uint64_t key_hash(unsigned long long k) {
+    k ^= k >> 33;
+    k *= 0xFF51AFD7ED558CCDULL;
+    k ^= k >> 33;
+    k *= 0xC4CEB9FE1A85EC53ULL;
+    k ^= k >> 33;
+    return k;
+}
+
+// Read-only leaf lookup (no concurrent inserts).  Returns leaf id or -1.
 __device__ inline int hash_find(const int4* __restrict__ table, int64_t mask, int a, int b, int c) {
     int64_t pos = (int64_t)(block_hash(a, b, c) & (uint64_t)mask);
     while (true) {
@@ -178,19 +222,19 @@ __device__ inline int hash_find(const int4* __restrict__ table, int64_t mask, in
 
 // ---- launchers implemented in the .cu files ---------------------------------
 // svx_march.cu
-svx_status launch_count(svx_map* m, const void* pts, int pts_f64, int64_t n, const PoseParams& pp,
-                        const int32_t* labels, const void* feats, int feats_f64,
-                        cudaStream_t s);
-svx_status launch_fill(svx_map* m, int64_t n, const PoseParams& pp, const KeyPack& kp,
-                       cudaStream_t s);
+svx_status launch_march(svx_map* m, const void* pts, int pts_f64, int64_t n, const PoseParams& pp,
+                        const KeyPack& kp, const FrameCaps& fc, const int32_t* labels,
+                        const void* feats, int feats_f64, cudaStream_t s);
+svx_status launch_compact(svx_map* m, const FrameCaps& fc, cudaStream_t s);
+svx_status launch_scatter(svx_map* m, int64_t n, const PoseParams& pp, const KeyPack& kp,
+                          const FrameCaps& fc, cudaStream_t s);
 // svx_update.cu
-svx_status launch_blocks(svx_map* m, int64_t U, const KeyPack& kp, cudaStream_t s);
-svx_status launch_assign_blocks(svx_map* m, int64_t nnew, const unsigned* order, cudaStream_t s);
-svx_status launch_resolve(svx_map* m, int64_t U, const KeyPack& kp, cudaStream_t s);
-svx_status launch_activate(svx_map* m, int64_t U, const KeyPack& kp, cudaStream_t s);
-svx_status launch_update(svx_map* m, int64_t U, const KeyPack& kp, const PoseParams& pp,
-                         const int32_t* labels, const void* feats, int feats_f64, cudaStream_t s);
+svx_status launch_voxels(svx_map* m, const KeyPack& kp, const FrameCaps& fc, cudaStream_t s);
+svx_status launch_update(svx_map* m, const KeyPack& kp, const PoseParams& pp, const FrameCaps& fc,
+                         const int32_t* labels, const void* feats, int feats_f64, int64_t n,
+                         cudaStream_t s);
 svx_status launch_rehash(svx_map* m, int4* new_table, int64_t new_cap, cudaStream_t s);
+int huge_warps();
 // svx_query.cu
 svx_status build_active_list(svx_map* m, int64_t* count, cudaStream_t s);
 svx_status launch_export(svx_map* m, int64_t count, int64_t* coords, void* d, void* w, void* sem0,

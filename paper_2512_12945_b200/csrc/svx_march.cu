@@ -1,16 +1,24 @@
-// svx_march.cu -- per-point preparation and the fp64 band ray-march (K1).
+// svx_march.cu -- per-point preparation, the fp64 band ray-march (K1), and
+// the per-frame voxel grouping (counting sort by voxel: K2 compact, K3
+// scatter).
 //
-// Compiled with -fmad=false: every double expression below is evaluated with
-// the same operation order and IEEE round-to-nearest steps as the reference's
+// Compiled with -fmad=false: every double expression is evaluated with the
+// operation order and IEEE round-to-nearest steps of the reference's
 // -ffp-contract=off C++ (_core.pyx:478-579, pkg/setup.py:14) and its numpy
 // twin (_pycore.py:326-396), so band membership and per-row distances are
 // bit-identical.
 //
-// Two passes over the rays (count, then fill after an exclusive scan) give
-// rows in (point, step) order, which a stable radix sort on the voxel key then
-// turns into the reference's canonical (voxel, point, step) order
-// (_core.pyx:715-738).
+// Grouping replaces the reference's global (voxel, point, step) sort
+// (_core.pyx:707-753): each band row inserts its voxel key into a per-frame
+// open-addressing table and bumps that voxel's row count (K1); one pass over
+// the table compacts the touched voxels and assigns each a contiguous row
+// segment (K2); a second march drops every row's point index into its
+// voxel's segment (K3).  Rows inside a segment are put back into point order
+// by the update kernels, which is all the reference's sort order is needed
+// for (sequential per-voxel sums).
 #include <math.h>
+
+#include <cub/block/block_scan.cuh>
 
 #include "svx_internal.cuh"
 
@@ -88,18 +96,46 @@ __device__ __forceinline__ long long dda_walk(double ox, double oy, double oz, d
     return cnt;
 }
 
-// Per-row weight under linear dropoff (row_distances_weights, _pycore.py:384-396).
-__device__ __forceinline__ double row_weight(long long ci, long long cj, long long ck, double ox,
-                                             double oy, double oz, double ux, double uy, double uz,
-                                             double ts, const MarchParams& mp) {
+// Row weight under linear dropoff (row_distances_weights, _pycore.py:384-396).
+__device__ __forceinline__ bool row_kept(long long ci, long long cj, long long ck, double ox,
+                                         double oy, double oz, double4 r, const MarchParams& mp) {
+    if (mp.wfn != 1) return true;
     double cx = ((double)ci + 0.5) * mp.h - ox;
     double cy = ((double)cj + 0.5) * mp.h - oy;
     double cz = ((double)ck + 0.5) * mp.h - oz;
-    double proj = cx * ux + cy * uy + cz * uz;
-    double d = ts - proj;
+    double proj = cx * r.x + cy * r.y + cz * r.z;
+    double d = r.w - proj;
     if (d < -mp.trunc) d = -mp.trunc;
     if (d > mp.trunc) d = mp.trunc;
-    return d >= 0.0 ? 1.0 : (mp.trunc + d) / mp.trunc;
+    double w = d >= 0.0 ? 1.0 : (mp.trunc + d) / mp.trunc;
+    return w > 0.0;
+}
+
+// Frame-table insert; returns the slot or -1 when the table is full.
+__device__ __forceinline__ long long frame_insert(unsigned long long* keys, long long mask,
+                                                  unsigned long long key) {
+    long long pos = (long long)(key_hash(key) & (unsigned long long)mask);
+    for (long long probe = 0; probe <= mask; ++probe) {
+        unsigned long long cur = keys[pos];
+        if (cur == key) return pos;
+        if (cur == kKeyEmpty) {
+            cur = atomicCAS(&keys[pos], kKeyEmpty, key);
+            if (cur == kKeyEmpty || cur == key) return pos;
+        }
+        pos = (pos + 1) & mask;
+    }
+    return -1;
+}
+
+__device__ __forceinline__ long long frame_find(const unsigned long long* __restrict__ keys,
+                                                long long mask, unsigned long long key) {
+    long long pos = (long long)(key_hash(key) & (unsigned long long)mask);
+    while (true) {
+        unsigned long long cur = keys[pos];
+        if (cur == key) return pos;
+        if (cur == kKeyEmpty) return -1;
+        pos = (pos + 1) & mask;
+    }
 }
 
 template <class P>
@@ -109,20 +145,21 @@ __device__ __forceinline__ void load_point(const P* pts, int64_t i, double& x, d
     z = (double)pts[3 * i + 2];
 }
 
-// Pass 1: validation masks (integrate_frame, fusion.py:228-256), ray setup
-// (fusion.py:262-263), band row count and frame bbox of kept rows.
+// K1: validation masks (integrate_frame, fusion.py:228-256), ray setup
+// (fusion.py:262-263), band walk, frame-table insert + per-voxel row count.
 template <class P, class Fe>
-__global__ void k_count(const P* __restrict__ pts, int64_t n, PoseParams pp, MarchParams mp,
-                        int sem_kind, const int32_t* __restrict__ labels, int num_classes,
-                        const Fe* __restrict__ feats, int D, double4* __restrict__ ray,
-                        int* __restrict__ cnt, FrameCtr* __restrict__ ctr) {
+__global__ void __launch_bounds__(256) k_march(
+    const P* __restrict__ pts, int64_t n, PoseParams pp, MarchParams mp, KeyPack kp, long long fmask,
+    int sem_kind, const int32_t* __restrict__ labels, int num_classes, const Fe* __restrict__ feats,
+    int D, double4* __restrict__ ray, unsigned long long* fkey, unsigned* fcount,
+    FrameCtr* __restrict__ ctr) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     bool live = i < n;
     unsigned c_nonfinite = 0, c_range = 0, c_degen = 0, c_badlab = 0, c_used = 0;
     unsigned long long c_hits = 0, c_rows = 0;
     long long mn0 = LLONG_MAX, mn1 = LLONG_MAX, mn2 = LLONG_MAX;
     long long mx0 = LLONG_MIN, mx1 = LLONG_MIN, mx2 = LLONG_MIN;
-    int budget = 0;
+    int budget = 0, packerr = 0, probeerr = 0;
     if (live) {
         double x, y, z;
         load_point(pts, i, x, y, z);
@@ -157,29 +194,36 @@ __global__ void k_count(const P* __restrict__ pts, int64_t n, PoseParams pp, Mar
             c_badlab = keep && !good;
             keep = keep && good;
         }
-        int rows = 0;
+        double4 r = make_double4(0.0, 0.0, 0.0, -1.0);
         if (keep) {
             c_used = 1;
-            double ux = dx / ts, uy = dy / ts, uz = dz / ts;
-            ray[i] = make_double4(ux, uy, uz, ts);
-            long long emitted = dda_walk(ox, oy, oz, ux, uy, uz, ts, mp,
+            r = make_double4(dx / ts, dy / ts, dz / ts, ts);
+            long long emitted = dda_walk(ox, oy, oz, r.x, r.y, r.z, ts, mp,
                 [&](long long ci, long long cj, long long ck) {
-                    if (mp.wfn == 1 &&
-                        !(row_weight(ci, cj, ck, ox, oy, oz, ux, uy, uz, ts, mp) > 0.0))
-                        return;
-                    ++rows;
+                    if (!row_kept(ci, cj, ck, ox, oy, oz, r, mp)) return;
+                    ++c_rows;
                     mn0 = min(mn0, ci); mn1 = min(mn1, cj); mn2 = min(mn2, ck);
                     mx0 = max(mx0, ci); mx1 = max(mx1, cj); mx2 = max(mx2, ck);
+                    long long ox_ = ci - kp.base[0], oy_ = cj - kp.base[1], oz_ = ck - kp.base[2];
+                    if (((ox_ | oy_ | oz_) & ~kPackMask) != 0) {
+                        packerr = 1;
+                        return;
+                    }
+                    long long s = frame_insert(fkey, fmask, pack_key(ox_, oy_, oz_));
+                    if (s < 0) {
+                        probeerr = 1;
+                        return;
+                    }
+                    atomicAdd(&fcount[s], 1u);
                 });
             if (emitted < 0) {
                 budget = 1;
-                rows = 0;
+                r.w = -1.0;   // nothing of this frame is applied anyway
             } else {
                 c_hits = (unsigned long long)emitted;
             }
-            c_rows = (unsigned long long)rows;
         }
-        cnt[i] = rows;
+        ray[i] = r;
     }
     // warp-aggregated counters
     const unsigned full = 0xffffffffu;
@@ -188,7 +232,7 @@ __global__ void k_count(const P* __restrict__ pts, int64_t n, PoseParams pp, Mar
     unsigned a_dg = __reduce_add_sync(full, c_degen);
     unsigned a_bl = __reduce_add_sync(full, c_badlab);
     unsigned a_us = __reduce_add_sync(full, c_used);
-    unsigned a_bu = __reduce_or_sync(full, (unsigned)budget);
+    unsigned a_er = __reduce_or_sync(full, (unsigned)(budget | (packerr << 1) | (probeerr << 2)));
     for (int o = 16; o > 0; o >>= 1) {
         c_hits += __shfl_xor_sync(full, c_hits, o);
         c_rows += __shfl_xor_sync(full, c_rows, o);
@@ -213,39 +257,108 @@ __global__ void k_count(const P* __restrict__ pts, int64_t n, PoseParams pp, Mar
             atomicMax(&ctr->bbox_max[0], mx0); atomicMax(&ctr->bbox_max[1], mx1);
             atomicMax(&ctr->bbox_max[2], mx2);
         }
-        if (a_bu) atomicOr(&ctr->err_budget, 1);
+        if (a_er & 1) atomicOr(&ctr->err_budget, 1);
+        if (a_er & 2) atomicOr(&ctr->err_pack, 1);
+        if (a_er & 4) atomicOr(&ctr->err_probe, 1);
     }
 }
 
-// Pass 2: write (voxel key, point index) rows at the ray's scanned offset.
-__global__ void k_fill(int64_t n, const double4* __restrict__ ray, const int* __restrict__ cnt,
-                       const long long* __restrict__ off, PoseParams pp, MarchParams mp, KeyPack kp,
-                       unsigned long long* __restrict__ keys, int* __restrict__ rid) {
+constexpr int kCompactThreads = 256;
+constexpr int kCompactPer = 4;
+
+// K2: one pass over the frame table.  Touched voxels are compacted into
+// ulist/ukey and each gets a contiguous segment of the row array; segment
+// order follows CTA arrival (no observable effect).
+__global__ void __launch_bounds__(kCompactThreads) k_compact(
+    const unsigned long long* __restrict__ fkey, const unsigned* __restrict__ fcount,
+    unsigned* __restrict__ foff, long long fcap, unsigned long long ucap, int* __restrict__ ulist,
+    unsigned long long* __restrict__ ukey, FrameCtr* ctr) {
+    using Scan = cub::BlockScan<unsigned long long, kCompactThreads>;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ unsigned long long s_ubase, s_rbase;
+    const long long base = ((long long)blockIdx.x * kCompactThreads + threadIdx.x) * kCompactPer;
+    unsigned long long kk[kCompactPer];
+    unsigned cc[kCompactPer];
+    unsigned occ = 0, rows = 0;
+#pragma unroll
+    for (int q = 0; q < kCompactPer; ++q) {
+        long long s = base + q;
+        kk[q] = s < fcap ? fkey[s] : kKeyEmpty;
+        cc[q] = kk[q] != kKeyEmpty ? fcount[s] : 0u;
+        occ += kk[q] != kKeyEmpty;
+        rows += cc[q];
+    }
+    // pack (occupied, rows) into one 64-bit scan
+    unsigned long long packed = ((unsigned long long)occ << 40) | rows, pre, total;
+    Scan(tmp).ExclusiveSum(packed, pre, total);
+    if (threadIdx.x == 0) {
+        unsigned long long tocc = total >> 40, trows = total & ((1ULL << 40) - 1);
+        s_ubase = tocc ? atomicAdd(&ctr->n_groups, tocc) : 0ULL;
+        s_rbase = trows ? atomicAdd(&ctr->rows_c, trows) : 0ULL;
+    }
+    __syncthreads();
+    unsigned long long u = s_ubase + (pre >> 40);
+    unsigned long long r = s_rbase + (pre & ((1ULL << 40) - 1));
+#pragma unroll
+    for (int q = 0; q < kCompactPer; ++q) {
+        if (kk[q] == kKeyEmpty) continue;
+        long long s = base + q;
+        if (u < ucap) {
+            ulist[u] = (int)s;
+            ukey[u] = kk[q];
+        }
+        foff[s] = (unsigned)r;
+        ++u;
+        r += cc[q];
+    }
+}
+
+// K3: second march; each kept row writes its point index into its voxel's
+// segment (arbitrary order within the segment).
+__global__ void __launch_bounds__(256) k_scatter(
+    int64_t n, const double4* __restrict__ ray, PoseParams pp, MarchParams mp, KeyPack kp,
+    long long fmask, const unsigned long long* __restrict__ fkey, const unsigned* __restrict__ foff,
+    unsigned* fcur, int* __restrict__ srid, FrameCaps fc, const FrameCtr* __restrict__ ctr) {
+    if (ctr->abort) return;
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n || cnt[i] == 0) return;
+    if (i >= n) return;
     const double4 r = ray[i];
+    if (!(r.w >= 0.0)) return;
     const double ox = pp.t[0], oy = pp.t[1], oz = pp.t[2];
-    long long o = off[i];
     dda_walk(ox, oy, oz, r.x, r.y, r.z, r.w, mp, [&](long long ci, long long cj, long long ck) {
-        if (mp.wfn == 1 && !(row_weight(ci, cj, ck, ox, oy, oz, r.x, r.y, r.z, r.w, mp) > 0.0))
-            return;
-        unsigned long long dx = (unsigned long long)(ci - kp.mn[0]);
-        unsigned long long dy = (unsigned long long)(cj - kp.mn[1]);
-        unsigned long long dz = (unsigned long long)(ck - kp.mn[2]);
-        keys[o] = (dx << kp.byz) | (dy << kp.bz) | dz;
-        rid[o] = (int)i;
-        ++o;
+        if (!row_kept(ci, cj, ck, ox, oy, oz, r, mp)) return;
+        unsigned long long key = pack_key(ci - kp.base[0], cj - kp.base[1], ck - kp.base[2]);
+        long long s = frame_find(fkey, fmask, key);
+        unsigned pos = foff[s] + atomicAdd(&fcur[s], 1u);
+        srid[pos] = (int)i;
     });
 }
 
+// Decide, once per frame on the device, whether the frame may mutate the map
+// (mirrors the reference's checks before any allocation, _core.pyx:661-712,
+// :386-387).
+__global__ void k_gate(FrameCtr* ctr, FrameCaps fc) {
+    int ab = ctr->err_budget | ctr->err_pack | ctr->err_probe;
+    if (ctr->n_groups > fc.ucap || ctr->rows_c > fc.rcap) ab = 1;
+    if (ctr->rows) {
+        for (int a = 0; a < 3; ++a) {
+            long long lo = ctr->bbox_min[a], hi = ctr->bbox_max[a];
+            if (hi - lo >= (1LL << kPackBits)) ab = 1;
+            if (llabs(lo) >= kCoordLimit || llabs(hi) >= kCoordLimit) ab = 1;
+        }
+    }
+    ctr->abort = ab;
+}
+
 template <class P, class Fe>
-svx_status count_t(svx_map* m, const P* pts, int64_t n, const PoseParams& pp, const MarchParams& mp,
-                   const int32_t* labels, const Fe* feats, cudaStream_t s) {
+svx_status march_t(svx_map* m, const P* pts, int64_t n, const PoseParams& pp, const MarchParams& mp,
+                   const KeyPack& kp, const FrameCaps& fc, const int32_t* labels, const Fe* feats,
+                   cudaStream_t s) {
     const int T = 256;
-    k_count<P, Fe><<<grid_for(n, T), T, 0, s>>>(pts, n, pp, mp, m->cfg.sem_kind, labels,
-                                                m->cfg.num_classes, feats, m->payload_d,
-                                                ptr<double4>(m->ray), ptr<int>(m->cnt),
-                                                ptr<FrameCtr>(m->ctr));
+    k_march<P, Fe><<<grid_for(n, T), T, 0, s>>>(
+        pts, n, pp, mp, kp, fc.fmask, m->cfg.sem_kind, labels, m->cfg.num_classes, feats,
+        m->payload_d, ptr<double4>(m->ray), ptr<unsigned long long>(m->fkey),
+        ptr<unsigned>(m->fcount), ptr<FrameCtr>(m->ctr));
     SVX_LAUNCHED();
     return SVX_OK;
 }
@@ -262,27 +375,40 @@ MarchParams march_params(const svx_map* m) {
 
 }  // namespace
 
-svx_status launch_count(svx_map* m, const void* pts, int pts_f64, int64_t n, const PoseParams& pp,
-                        const int32_t* labels, const void* feats, int feats_f64,
-                        cudaStream_t s) {
+svx_status launch_march(svx_map* m, const void* pts, int pts_f64, int64_t n, const PoseParams& pp,
+                        const KeyPack& kp, const FrameCaps& fc, const int32_t* labels,
+                        const void* feats, int feats_f64, cudaStream_t s) {
     MarchParams mp = march_params(m);
     if (pts_f64) {
         if (feats_f64)
-            return count_t(m, (const double*)pts, n, pp, mp, labels, (const double*)feats, s);
-        return count_t(m, (const double*)pts, n, pp, mp, labels, (const float*)feats, s);
+            return march_t(m, (const double*)pts, n, pp, mp, kp, fc, labels, (const double*)feats, s);
+        return march_t(m, (const double*)pts, n, pp, mp, kp, fc, labels, (const float*)feats, s);
     }
     if (feats_f64)
-        return count_t(m, (const float*)pts, n, pp, mp, labels, (const double*)feats, s);
-    return count_t(m, (const float*)pts, n, pp, mp, labels, (const float*)feats, s);
+        return march_t(m, (const float*)pts, n, pp, mp, kp, fc, labels, (const double*)feats, s);
+    return march_t(m, (const float*)pts, n, pp, mp, kp, fc, labels, (const float*)feats, s);
 }
 
-svx_status launch_fill(svx_map* m, int64_t n, const PoseParams& pp, const KeyPack& kp,
-                       cudaStream_t s) {
+svx_status launch_compact(svx_map* m, const FrameCaps& fc, cudaStream_t s) {
+    const long long per_block = (long long)kCompactThreads * kCompactPer;
+    const int blocks = (int)((m->fcap + per_block - 1) / per_block);
+    k_compact<<<blocks, kCompactThreads, 0, s>>>(
+        ptr<unsigned long long>(m->fkey), ptr<unsigned>(m->fcount), ptr<unsigned>(m->foff), m->fcap,
+        fc.ucap, ptr<int>(m->ulist), ptr<unsigned long long>(m->ukey), ptr<FrameCtr>(m->ctr));
+    SVX_LAUNCHED();
+    k_gate<<<1, 1, 0, s>>>(ptr<FrameCtr>(m->ctr), fc);
+    SVX_LAUNCHED();
+    return SVX_OK;
+}
+
+svx_status launch_scatter(svx_map* m, int64_t n, const PoseParams& pp, const KeyPack& kp,
+                          const FrameCaps& fc, cudaStream_t s) {
     MarchParams mp = march_params(m);
     const int T = 256;
-    k_fill<<<grid_for(n, T), T, 0, s>>>(n, ptr<double4>(m->ray), ptr<int>(m->cnt),
-                                        ptr<long long>(m->off), pp, mp, kp,
-                                        ptr<unsigned long long>(m->keys0), ptr<int>(m->rid0));
+    k_scatter<<<grid_for(n, T), T, 0, s>>>(n, ptr<double4>(m->ray), pp, mp, kp, fc.fmask,
+                                           ptr<unsigned long long>(m->fkey),
+                                           ptr<unsigned>(m->foff), ptr<unsigned>(m->fcur),
+                                           ptr<int>(m->srid), fc, ptr<FrameCtr>(m->ctr));
     SVX_LAUNCHED();
     return SVX_OK;
 }

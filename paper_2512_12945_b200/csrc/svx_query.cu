@@ -1,7 +1,12 @@
 // svx_query.cu -- voxel and label queries (K7, K8 v1).
 //
 // Active enumeration reproduces GridCore.active_slots (_core.pyx:424-444):
-// leaves in allocation order, slots ascending.  Reads never allocate.
+// leaves in the reference's allocation order, slots ascending.  The engine
+// allocates leaf ids in arrival order during a frame and stamps every leaf
+// with (creation frame, first-occurrence key); the reference's order is
+// recovered here, off the integration path, by sorting each frame's new
+// leaves by that stamp (ids of one frame are contiguous, so the order is
+// extended incrementally).  Reads never allocate.
 #include <math.h>
 
 #include <cub/cub.cuh>
@@ -11,25 +16,46 @@
 namespace svx {
 namespace {
 
-__global__ void k_popc(int64_t nblocks, const unsigned long long* __restrict__ bmask,
-                       int* __restrict__ cnt) {
+__global__ void k_order_init(int64_t first, int64_t cnt, const int4* __restrict__ bcoord,
+                             const unsigned long long* __restrict__ bkey,
+                             unsigned long long* __restrict__ k0, unsigned* __restrict__ f0,
+                             int* __restrict__ id0) {
+    int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= cnt) return;
+    k0[j] = bkey[first + j];
+    id0[j] = (int)(first + j);
+    (void)f0;
+    (void)bcoord;
+}
+
+__global__ void k_order_frames(int64_t cnt, const int4* __restrict__ bcoord,
+                               const int* __restrict__ ids, unsigned* __restrict__ f) {
+    int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < cnt) f[j] = (unsigned)bcoord[ids[j]].w;
+}
+
+__global__ void k_popc(int64_t nblocks, const int* __restrict__ order,
+                       const unsigned long long* __restrict__ bmask, int* __restrict__ cnt) {
     int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= nblocks) return;
+    const int64_t leaf = order[b];
     int c = 0;
 #pragma unroll
-    for (int w = 0; w < kMaskWords; ++w) c += __popcll(bmask[b * kMaskWords + w]);
+    for (int w = 0; w < kMaskWords; ++w) c += __popcll(bmask[leaf * kMaskWords + w]);
     cnt[b] = c;
 }
 
 // One warp per leaf: lanes cover 32 slots at a time, ballot/popc give ranks.
-__global__ void k_list(int64_t nblocks, const unsigned long long* __restrict__ bmask,
+__global__ void k_list(int64_t nblocks, const int* __restrict__ order,
+                       const unsigned long long* __restrict__ bmask,
                        const int* __restrict__ bslot, const int4* __restrict__ bcoord,
                        const long long* __restrict__ off, int* __restrict__ act_vid,
                        long long* __restrict__ act_coord) {
-    int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int64_t ob = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     int lane = threadIdx.x & 31;
-    if (b >= nblocks) return;
-    long long pos = off[b];
+    if (ob >= nblocks) return;
+    long long pos = off[ob];
+    const int64_t b = order[ob];
     int4 bc = bcoord[b];
     for (int half = 0; half < 16; ++half) {
         unsigned long long word = bmask[b * kMaskWords + (half >> 1)];
@@ -220,16 +246,64 @@ __global__ void k_label_map(int64_t count, int C, int mode, const int* __restric
 
 }  // namespace
 
+// Extend the leaf order with the leaves created since the last query: sort
+// them by (creation frame, first-occurrence key) with two stable LSD passes.
+static svx_status build_leaf_order(svx_map* m, cudaStream_t s) {
+    const int64_t nb = m->nblocks;
+    int64_t first = m->ord_nblocks < 0 ? 0 : m->ord_nblocks;
+    SVX_TRY(ensure(m->ord0, sizeof(int) * nb, s, true));
+    const int64_t cnt = nb - first;
+    if (cnt <= 0) return SVX_OK;
+    SVX_TRY(ensure(m->ordk0, 8 * cnt, s));
+    SVX_TRY(ensure(m->ordk1, 8 * cnt, s));
+    SVX_TRY(ensure(m->ordf0, 4 * cnt, s));
+    SVX_TRY(ensure(m->ordf1, 4 * cnt, s));
+    SVX_TRY(ensure(m->ord1, 4 * cnt, s));
+    SVX_TRY(ensure(m->act_cnt, 4 * cnt, s));
+    int* idA = ptr<int>(m->ord1);
+    int* idB = ptr<int>(m->act_cnt);
+    const int T = 256;
+    k_order_init<<<grid_for(cnt, T), T, 0, s>>>(first, cnt, ptr<int4>(m->bcoord),
+                                                ptr<unsigned long long>(m->bkey),
+                                                ptr<unsigned long long>(m->ordk0),
+                                                ptr<unsigned>(m->ordf0), idA);
+    SVX_LAUNCHED();
+    size_t tmp = 0;
+    SVX_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, ptr<unsigned long long>(m->ordk0),
+                                             ptr<unsigned long long>(m->ordk1), idA, idB, (int)cnt,
+                                             0, 64, s));
+    SVX_TRY(ensure(m->cubtmp, tmp, s));
+    SVX_CUDA(cub::DeviceRadixSort::SortPairs(m->cubtmp.p, tmp, ptr<unsigned long long>(m->ordk0),
+                                             ptr<unsigned long long>(m->ordk1), idA, idB, (int)cnt,
+                                             0, 64, s));
+    count_launch();
+    k_order_frames<<<grid_for(cnt, T), T, 0, s>>>(cnt, ptr<int4>(m->bcoord), idB,
+                                                  ptr<unsigned>(m->ordf0));
+    SVX_LAUNCHED();
+    int* out = ptr<int>(m->ord0) + first;
+    SVX_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, ptr<unsigned>(m->ordf0),
+                                             ptr<unsigned>(m->ordf1), idB, out, (int)cnt, 0, 32, s));
+    SVX_TRY(ensure(m->cubtmp, tmp, s));
+    SVX_CUDA(cub::DeviceRadixSort::SortPairs(m->cubtmp.p, tmp, ptr<unsigned>(m->ordf0),
+                                             ptr<unsigned>(m->ordf1), idB, out, (int)cnt, 0, 32, s));
+    count_launch();
+    m->ord_nblocks = nb;
+    return SVX_OK;
+}
+
 svx_status build_active_list(svx_map* m, int64_t* count, cudaStream_t s) {
     const int64_t nb = m->nblocks;
     *count = m->nvox;
     if (nb == 0 || m->nvox == 0) return SVX_OK;
+    SVX_TRY(build_leaf_order(m, s));
     SVX_TRY(ensure(m->act_cnt, sizeof(int) * nb, s));
     SVX_TRY(ensure(m->act_off, sizeof(long long) * nb, s));
     SVX_TRY(ensure(m->act_vid, sizeof(int) * m->nvox, s));
     SVX_TRY(ensure(m->act_coord, sizeof(long long) * 3 * m->nvox, s));
     const int T = 256;
-    k_popc<<<grid_for(nb, T), T, 0, s>>>(nb, ptr<unsigned long long>(m->bmask), ptr<int>(m->act_cnt));
+    const int* order = ptr<int>(m->ord0);
+    k_popc<<<grid_for(nb, T), T, 0, s>>>(nb, order, ptr<unsigned long long>(m->bmask),
+                                         ptr<int>(m->act_cnt));
     SVX_LAUNCHED();
     size_t tmp = 0;
     SVX_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, ptr<int>(m->act_cnt),
@@ -238,7 +312,7 @@ svx_status build_active_list(svx_map* m, int64_t* count, cudaStream_t s) {
     SVX_CUDA(cub::DeviceScan::ExclusiveSum(m->cubtmp.p, tmp, ptr<int>(m->act_cnt),
                                            ptr<long long>(m->act_off), (int)nb, s));
     count_launch();
-    k_list<<<grid_for(nb * 32, T), T, 0, s>>>(nb, ptr<unsigned long long>(m->bmask),
+    k_list<<<grid_for(nb * 32, T), T, 0, s>>>(nb, order, ptr<unsigned long long>(m->bmask),
                                              ptr<int>(m->bslot), ptr<int4>(m->bcoord),
                                              ptr<long long>(m->act_off), ptr<int>(m->act_vid),
                                              ptr<long long>(m->act_coord));
