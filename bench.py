@@ -51,6 +51,8 @@ def parse_args():
     ap.add_argument("--cpu-frames", type=int, default=0, help="oracle sample frames (0=auto)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--profile-frames", type=int, default=5,
+                    help="extra frames run eagerly with per-stage events (roofline attribution)")
     return ap.parse_args()
 
 
@@ -151,13 +153,16 @@ def stage_bytes(stage, rep, kind, C, D, tsdf_elem):
     P = 4 if kind == "closed" else (4 * D if kind == "open" else 0)
     S = 2 * tsdf_elem + (4 * C if kind == "closed" else (8 * D if kind == "open" else 0))
     return {
-        "count": n * (12 + P) + used * 32,          # read points(+labels), write ray table
-        "fill": used * 32 + R * 12,                  # read rays, write (key, point) rows
-        "sort": 2 * R * 12,                          # one read + one write of the rows
-        "group": R * 8 + U * 20,                     # read keys, write unique keys + runs
-        "leaves": U * 24,                            # read keys, write leaf ids (+hash probe)
-        "voxels": U * 24,
-        "update": 2 * U * S + R * (4 + (4 if kind == "closed" else 0)) + U * 20,
+        # read points (+labels/features), write the ray table and row slots, one
+        # 8-byte key CAS + one 4-byte count per row into the frame table
+        "march": n * (12 + P) + used * 32 + R * (4 + 8 + 4),
+        # read the frame table (key + count per slot), write list + segment offsets
+        "compact": U * (8 + 4 + 4 + 4 + 8),
+        # read row slots, segment offset and cursor per row, write the point index
+        "scatter": R * (4 + 4 + 4 + 4),
+        # leaf lookup + voxel activation, read rows/rays/labels, read+write state
+        "update": 2 * U * S + R * (4 + 32 + (4 if kind == "closed" else 0)) + U * 40,
+        "update_b": 0,
     }[stage]
 
 
@@ -229,8 +234,9 @@ def run_ours(args):
     from paper_2512_12945_b200 import Mapper, _lib
 
     K, W = args.steps, args.warmup
+    P = args.profile_frames
     # replicas: rank r integrates its own stream of frames (weak scaling)
-    wl, frames = make_frames(args.config, W + K, dev, start=rank * (W + K))
+    wl, frames = make_frames(args.config, W + K + P, dev, start=rank * (W + K + P))
     kw = dict(wl.mapper_kwargs, tsdf_dtype=args.tsdf_dtype, device=local)
     kind = sem_kind_of(kw)
     C = kw.get("num_classes", 0)
@@ -253,8 +259,8 @@ def run_ours(args):
     # pool headroom for the timed frames, so no growth copy lands inside them
     st = m.engine_stats()
     per_frame = max(1, st["active_voxels"] // max(W, 1))
-    m.reserve(st["active_voxels"] + 2 * per_frame * K, st["leaf_count"] * (1 + 2 * K // max(W, 1)))
-    m.set_profiling(True)
+    m.reserve(st["active_voxels"] + 2 * per_frame * (K + P),
+              st["leaf_count"] * (1 + 2 * (K + P) // max(W, 1)))
     stream = torch.cuda.current_stream()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(K)]
@@ -269,7 +275,6 @@ def run_ours(args):
             evs[i][0].record(stream)
             reps.append(integrate(m, frames[W + i]))
             evs[i][1].record(stream)
-            stage_hist.append(m.stage_times())
         torch.cuda.synchronize()
     launches = _lib.kernel_launches() - launches0
     if world > 1:
@@ -285,13 +290,24 @@ def run_ours(args):
     total_ms_max, used_all = float(t.item()), float(u.item())
     value = used_all / (total_ms_max / 1e3)
 
+    # ---- per-stage device times: a separate eager pass over P further frames -------
+    m.set_profiling(True)
+    prof_reps = []
+    for f in frames[W + K:W + K + P]:
+        flush.zero_()
+        prof_reps.append(integrate(m, f))
+        stage_hist.append(m.stage_times())
+    m.set_profiling(False)
+    if not stage_hist:
+        stage_hist, prof_reps = [{s: 0.0 for s in _lib.STAGES}], reps[-1:]
+
     # ---- roofline of the dominant stage -------------------------------------------
     stages = list(_lib.STAGES)
     mean_stage = {s: statistics.mean(h[s] for h in stage_hist) for s in stages}
     dom = max(stages, key=lambda s: mean_stage[s])
-    dom_bytes = statistics.mean(stage_bytes(dom, r, kind, C, D, tsdf_elem) for r in reps)
+    dom_bytes = statistics.mean(stage_bytes(dom, r, kind, C, D, tsdf_elem) for r in prof_reps)
     peak, peak_src = measured_peak()
-    achieved = dom_bytes / (mean_stage[dom] / 1e3) / 1e9
+    achieved = dom_bytes / (mean_stage[dom] / 1e3) / 1e9 if mean_stage[dom] > 0 else 0.0
     fb = statistics.mean(frame_bytes(r, kind, C, D) for r in reps)
     frame_gbs = fb / (statistics.mean(step_ms) / 1e3) / 1e9
     traffic = ncu_traffic(dom)

@@ -186,8 +186,10 @@ svx_status svx_label_map(svx_map* map, int32_t mode, int64_t capacity, int32_t* 
  *   0 march (K1: masks + band walk + voxel grouping counts)
  *   1 compact (K2: touched-voxel list + row segments + gate)
  *   2 scatter (K3: rows into voxel segments)
- *   3 voxels (K4: leaf find-or-insert, voxel activation)
- *   4 update (K5/K6: fused TSDF + semantic update)
+ *   3 update (K4 leaf find-or-insert + voxel activation fused with the K5/K6
+ *      TSDF + semantic update of short segments / open-set voxels)
+ *   4 update_b (K5/K6 for long and huge segments)
+ * With profiling off, a frame is replayed as one captured CUDA graph.
  * svx_stage_times writes up to n last-frame stage times in ms and returns the
  * number of stages (SVX_N_STAGES). */
 #define SVX_N_STAGES 5

@@ -70,282 +70,6 @@ void release(DevBuf& buf) {
 
 namespace {
 
-bool is_device_ptr(const void* p) {
-    if (!p) return false;
-    cudaPointerAttributes a;
-    cudaError_t e = cudaPointerGetAttributes(&a, p);
-    if (e != cudaSuccess) {
-        cudaGetLastError();
-        return false;
-    }
-    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
-}
-
-// Device view of a caller array: device pointers pass through, host arrays
-// are copied into `stage` on the stream.
-svx_status stage_in(const void* p, size_t bytes, DevBuf& stage, cudaStream_t s, const void** out) {
-    if (!p || bytes == 0) {
-        *out = p;
-        return SVX_OK;
-    }
-    if (is_device_ptr(p)) {
-        *out = p;
-        return SVX_OK;
-    }
-    SVX_TRY(ensure(stage, bytes, s));
-    SVX_CUDA(cudaMemcpyAsync(stage.p, p, bytes, cudaMemcpyHostToDevice, s));
-    *out = stage.p;
-    return SVX_OK;
-}
-
-size_t tsdf_elem(const svx_map* m) { return m->cfg.tsdf_dtype == SVX_F64 ? 8 : 4; }
-size_t sem_elem(const svx_map* m) {
-    if (m->cfg.sem_kind == SVX_SEM_CLOSED) return m->cfg.count_dtype == SVX_F64 ? 8 : 4;
-    if (m->cfg.sem_kind == SVX_SEM_OPEN) return m->cfg.state_dtype == SVX_F64 ? 8 : 4;
-    return 0;
-}
-
-// Voxel-pool capacity: grow by doubling, zero-filled (closed counts and open
-// means have a zero background; voxel ids are never recycled).
-svx_status reserve_voxels(svx_map* m, int64_t need, cudaStream_t s) {
-    if (need <= m->vcap) return SVX_OK;
-    int64_t cap = std::max<int64_t>(need, 2 * m->vcap);
-    const size_t te = tsdf_elem(m), se = sem_elem(m);
-    SVX_TRY(ensure(m->vd, te * cap, s, true));
-    SVX_TRY(ensure(m->vw, te * cap, s, true));
-    if (m->cfg.sem_kind != SVX_SEM_NONE)
-        SVX_TRY(ensure(m->s0, se * (size_t)m->payload_d * cap, s, true, 0));
-    if (m->cfg.sem_kind == SVX_SEM_OPEN)
-        SVX_TRY(ensure(m->s1, se * (size_t)m->payload_d * cap, s, true, 0));
-    m->vcap = cap;
-    return SVX_OK;
-}
-
-svx_status reserve_blocks(svx_map* m, int64_t need, cudaStream_t s) {
-    if (need > m->bcap) {
-        int64_t cap = std::max<int64_t>(need, 2 * m->bcap);
-        SVX_TRY(ensure(m->bcoord, sizeof(int4) * cap, s, true));
-        SVX_TRY(ensure(m->bkey, sizeof(unsigned long long) * cap, s, true, 0xFF));
-        SVX_TRY(ensure(m->bmask, sizeof(unsigned long long) * kMaskWords * cap, s, true, 0));
-        SVX_TRY(ensure(m->bslot, sizeof(int) * kLeafVolume * cap, s, true, 0xFF));
-        m->bcap = cap;
-    }
-    // keep the leaf hash at <= 50% load for the worst case of this frame
-    int64_t want = 1024;
-    while (want < 2 * need) want <<= 1;
-    if (want > m->hcap) {
-        DevBuf nt;
-        SVX_TRY(ensure(nt, sizeof(int4) * want, s, false, 0xFF));
-        SVX_TRY(launch_rehash(m, ptr<int4>(nt), want, s));
-        SVX_CUDA(cudaStreamSynchronize(s));
-        release(m->hash);
-        m->hash = nt;
-        m->hcap = want;
-    }
-    return SVX_OK;
-}
-
-// Per-frame scratch for `ucap` unique voxels / `rcap` rows / `n` points.
-svx_status reserve_frame(svx_map* m, int64_t n, cudaStream_t s) {
-    int64_t want = 1024;
-    while (want < 2 * (int64_t)m->ucap) want <<= 1;
-    if (want > m->fcap) {
-        release(m->fkey);
-        release(m->fcount);
-        release(m->fcur);
-        release(m->foff);
-        SVX_TRY(ensure(m->fkey, 8 * want, s, false, 0xFF));
-        SVX_TRY(ensure(m->fcount, 4 * want, s, false, 0));
-        SVX_TRY(ensure(m->fcur, 4 * want, s, false, 0));
-        SVX_TRY(ensure(m->foff, 4 * want, s));
-        m->fcap = want;
-    }
-    SVX_TRY(ensure(m->ulist, 4 * m->ucap, s));
-    SVX_TRY(ensure(m->ukey, 8 * m->ucap, s));
-    SVX_TRY(ensure(m->gvid, 4 * m->ucap, s));
-    SVX_TRY(ensure(m->longlist, 8 * m->ucap, s));   // long list, then huge list
-    SVX_TRY(ensure(m->srid, 4 * m->rcap, s));
-    SVX_TRY(ensure(m->bitmap, (size_t)4 * huge_warps() * ((n + 31) / 32 + 1), s));
-    SVX_TRY(ensure(m->ray, sizeof(double4) * n, s));
-    return SVX_OK;
-}
-
-svx_status clear_frame_table(svx_map* m, cudaStream_t s) {
-    SVX_CUDA(cudaMemsetAsync(m->fkey.p, 0xFF, 8 * m->fcap, s));
-    SVX_CUDA(cudaMemsetAsync(m->fcount.p, 0, 4 * m->fcap, s));
-    SVX_CUDA(cudaMemsetAsync(m->fcur.p, 0, 4 * m->fcap, s));
-    return SVX_OK;
-}
-
-#define STAGE_BEGIN(i) \
-    do { if (m->prof) { cudaEventRecord(m->st_ev[2 * (i)], s); m->st_mask |= 1u << (i); } } while (0)
-#define STAGE_END(i) \
-    do { if (m->prof) cudaEventRecord(m->st_ev[2 * (i) + 1], s); } while (0)
-
-void collect_stage_times(svx_map* m) {
-    for (int i = 0; i < SVX_N_STAGES; ++i) {
-        m->stage_ms[i] = 0.0;
-        if (!(m->st_mask & (1u << i))) continue;
-        float ms = 0.f;
-        if (cudaEventElapsedTime(&ms, m->st_ev[2 * i], m->st_ev[2 * i + 1]) == cudaSuccess)
-            m->stage_ms[i] = ms;
-        else
-            cudaGetLastError();
-    }
-    m->st_mask = 0;
-}
-
-long long floor_div_voxel(double v, double h) { return (long long)floor(v / h); }
-
-svx_status integrate_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n,
-                          const PoseParams& pp, const int32_t* labels_in, const void* feats_in,
-                          int feats_f64, cudaStream_t s, svx_report* rep) {
-    svx_report r;
-    memset(&r, 0, sizeof(r));
-    r.points_in = n;
-    const int kind = m->cfg.sem_kind;
-    if (kind == SVX_SEM_CLOSED && !labels_in)
-        return fail(SVX_E_PAYLOAD, "closed-set grid requires per-point labels");
-    if (kind == SVX_SEM_OPEN && !feats_in)
-        return fail(SVX_E_PAYLOAD, "open-set grid requires per-point features");
-    if (n < 0) return fail(SVX_E_INPUT, "negative point count");
-    if (n >= (int64_t)INT_MAX) return fail(SVX_E_INPUT, "point count exceeds 2^31-1");
-    if (n == 0) {
-        m->frames++;
-        if (rep) *rep = r;
-        return SVX_OK;
-    }
-    SVX_CUDA(cudaEventRecord(m->ev0, s));
-    const void* pts;
-    const void* feats = nullptr;
-    const void* labv = nullptr;
-    SVX_TRY(stage_in(pts_in, (size_t)n * 3 * (pts_f64 ? 8 : 4), m->in_pts, s, &pts));
-    if (kind == SVX_SEM_CLOSED)
-        SVX_TRY(stage_in(labels_in, (size_t)n * 4, m->in_lab, s, &labv));
-    if (kind == SVX_SEM_OPEN)
-        SVX_TRY(stage_in(feats_in, (size_t)n * m->payload_d * (feats_f64 ? 8 : 4), m->in_feat, s,
-                         &feats));
-    const int32_t* labels = (const int32_t*)labv;
-
-    // Capacity guesses for the first frame: a ray's band crosses at most
-    // 3 * (band length / h + 1) voxels; later frames adapt to what was seen.
-    const double h = m->cfg.voxel_size;
-    double band = m->cfg.space_carving ? m->cfg.max_range + m->cfg.truncation
-                                       : 2.0 * m->cfg.truncation;
-    uint64_t per_ray = (uint64_t)std::min(64.0, 3.0 * (band / h + 1.0) + 3.0);
-    m->rcap = std::max<uint64_t>(m->rcap, (uint64_t)n * per_ray);
-    m->ucap = std::max<uint64_t>(m->ucap, std::min<uint64_t>(m->rcap, (uint64_t)n * 16));
-
-    KeyPack kp;
-    {
-        const long long half = 1LL << (kPackBits - 1);
-        kp.base[0] = floor_div_voxel(pp.t[0], h) - half;
-        kp.base[1] = floor_div_voxel(pp.t[1], h) - half;
-        kp.base[2] = floor_div_voxel(pp.t[2], h) - half;
-    }
-    FrameCtr* hc = m->h_ctr;
-    FrameCtr* dc = ptr<FrameCtr>(m->ctr);
-    for (int attempt = 0;; ++attempt) {
-        if (attempt >= 6) return fail(SVX_E_INTERNAL, "frame scratch could not be sized");
-        SVX_TRY(reserve_frame(m, n, s));
-        SVX_TRY(reserve_blocks(m, m->nblocks + (int64_t)m->ucap, s));
-        SVX_TRY(reserve_voxels(m, m->nvox + (int64_t)m->ucap, s));
-        FrameCaps fc;
-        fc.ucap = m->ucap;
-        fc.rcap = m->rcap;
-        fc.fmask = m->fcap - 1;
-        fc.frame = (int)m->frames;
-
-        memset(hc, 0, sizeof(FrameCtr));
-        for (int a = 0; a < 3; ++a) {
-            hc->bbox_min[a] = LLONG_MAX;
-            hc->bbox_max[a] = LLONG_MIN;
-        }
-        hc->nblocks = (unsigned long long)m->nblocks;
-        hc->nvox = (unsigned long long)m->nvox;
-        SVX_CUDA(cudaMemcpyAsync(dc, hc, sizeof(FrameCtr), cudaMemcpyHostToDevice, s));
-
-        m->st_mask = 0;
-        STAGE_BEGIN(0);
-        SVX_TRY(launch_march(m, pts, pts_f64, n, pp, kp, fc, labels, feats, feats_f64, s));
-        STAGE_END(0);
-        STAGE_BEGIN(1);
-        SVX_TRY(launch_compact(m, fc, s));
-        STAGE_END(1);
-        STAGE_BEGIN(2);
-        SVX_TRY(launch_scatter(m, n, pp, kp, fc, s));
-        STAGE_END(2);
-        STAGE_BEGIN(3);
-        SVX_TRY(launch_voxels(m, kp, fc, s));
-        STAGE_END(3);
-        STAGE_BEGIN(4);
-        SVX_TRY(launch_update(m, kp, pp, fc, labels, feats, feats_f64, n, s));
-        STAGE_END(4);
-        SVX_CUDA(cudaMemcpyAsync(hc, dc, sizeof(FrameCtr), cudaMemcpyDeviceToHost, s));
-        SVX_CUDA(cudaEventRecord(m->ev1, s));
-        SVX_CUDA(cudaEventSynchronize(m->ev1));
-
-        // the reference's pre-allocation checks, in its order (_core.pyx:661-712, :386-387)
-        if (hc->err_budget) {
-            SVX_TRY(clear_frame_table(m, s));
-            return fail(SVX_E_INTERNAL, "ray band exceeds step budget; shrink max_range or grow voxels");
-        }
-        if (hc->rows) {
-            bool extent = false, range = false;
-            for (int a = 0; a < 3; ++a) {
-                if (hc->bbox_max[a] - hc->bbox_min[a] >= (1LL << kPackBits)) extent = true;
-                if (llabs(hc->bbox_min[a]) >= kCoordLimit || llabs(hc->bbox_max[a]) >= kCoordLimit)
-                    range = true;
-            }
-            if (extent) {
-                SVX_TRY(clear_frame_table(m, s));
-                return fail(SVX_E_INTERNAL,
-                            "frame voxel extent exceeds 2^21 per axis; shrink max_range or grow voxels");
-            }
-            if (range) {
-                SVX_TRY(clear_frame_table(m, s));
-                return fail(SVX_E_RANGE, "voxel coordinate beyond +/-2^30 addressable range");
-            }
-        }
-        if (hc->abort) {
-            // retry with a re-based key (pack) or bigger scratch (capacity)
-            SVX_TRY(clear_frame_table(m, s));
-            if (hc->err_pack)
-                for (int a = 0; a < 3; ++a) kp.base[a] = hc->bbox_min[a];
-            if (hc->err_probe || hc->n_groups > m->ucap || hc->rows_c > m->rcap ||
-                hc->rows > m->rcap) {
-                m->rcap = std::max<uint64_t>(2 * m->rcap, hc->rows + hc->rows / 2);
-                m->ucap = std::max<uint64_t>(2 * m->ucap,
-                                             std::min<uint64_t>(m->rcap, hc->n_groups * 2));
-            }
-            SVX_CUDA(cudaStreamSynchronize(s));
-            continue;
-        }
-        break;
-    }
-    float ms = 0.f;
-    SVX_CUDA(cudaEventElapsedTime(&ms, m->ev0, m->ev1));
-    if (m->prof) collect_stage_times(m);
-    r.skipped_nonfinite = (int64_t)hc->nonfinite;
-    r.skipped_range = (int64_t)hc->range;
-    r.skipped_degenerate = (int64_t)hc->degenerate;
-    r.skipped_bad_label = (int64_t)hc->bad_label;
-    r.points_used = (int64_t)hc->used;
-    r.band_hits = (int64_t)hc->band_hits;
-    r.touched_voxels = (int64_t)hc->n_groups;
-    r.new_blocks = (int64_t)hc->nblocks - m->nblocks;
-    r.new_voxels = (int64_t)hc->nvox - m->nvox;
-    r.kernel_ms = ms;
-    m->nblocks = (int64_t)hc->nblocks;
-    m->nvox = (int64_t)hc->nvox;
-    m->frames++;
-    // adapt the scratch to what this frame needed (headroom for the next)
-    if (hc->n_groups * 10 > m->ucap * 7) m->ucap = hc->n_groups * 2;
-    if (hc->rows_c * 10 > m->rcap * 8) m->rcap = hc->rows_c * 2;
-    if (rep) *rep = r;
-    return SVX_OK;
-}
-
 // Output staging: device pointers are written directly; host outputs go
 // through device scratch and are copied back at the end of the call.
 struct OutStage {
@@ -431,9 +155,11 @@ svx_status svx_create(const svx_config* cfg, svx_map** out) {
         return bail(fail(SVX_E_CUDA, "pinned allocation failed"));
     }
     if ((st = ensure(m->ctr, sizeof(FrameCtr), s)) != SVX_OK) return bail(st);
-    if (cudaEventCreate(&m->ev0) != cudaSuccess || cudaEventCreate(&m->ev1) != cudaSuccess) {
+    if (cudaEventCreate(&m->ev0) != cudaSuccess || cudaEventCreate(&m->ev1) != cudaSuccess ||
+        cudaEventCreateWithFlags(&m->ev_in, cudaEventDisableTiming) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&m->gstream, cudaStreamNonBlocking) != cudaSuccess) {
         cudaGetLastError();
-        return bail(fail(SVX_E_CUDA, "event creation failed"));
+        return bail(fail(SVX_E_CUDA, "event/stream creation failed"));
     }
     int64_t rb = cfg->reserve_blocks > 0 ? cfg->reserve_blocks : 1024;
     int64_t rv = cfg->reserve_voxels > 0 ? cfg->reserve_voxels : 65536;
@@ -450,8 +176,9 @@ svx_status svx_create(const svx_config* cfg, svx_map** out) {
 svx_status svx_destroy(svx_map* m) {
     if (!m) return SVX_OK;
     cudaSetDevice(m->cfg.device);
-    DevBuf* bufs[] = {&m->hash, &m->bcoord, &m->bkey, &m->bmask, &m->bslot, &m->vd, &m->vw,
-                      &m->s0, &m->s1, &m->in_pts, &m->in_lab, &m->in_feat, &m->ray, &m->fkey,
+    DevBuf* bufs[] = {&m->hash, &m->bcoord, &m->bkey, &m->bmask, &m->bslot, &m->vt,
+                      &m->s0, &m->s1, &m->in_pts, &m->in_lab, &m->in_feat, &m->ray, &m->rcnt,
+                      &m->rowslot, &m->rowkey, &m->partials, &m->fkey,
                       &m->fcount, &m->foff, &m->fcur, &m->ulist, &m->ukey, &m->gvid,
                       &m->longlist, &m->srid, &m->bitmap, &m->cubtmp, &m->ctr, &m->ord0,
                       &m->ord1, &m->ordk0, &m->ordk1, &m->ordf0, &m->ordf1, &m->act_cnt,
@@ -460,6 +187,9 @@ svx_status svx_destroy(svx_map* m) {
     if (m->h_ctr) cudaFreeHost(m->h_ctr);
     if (m->ev0) cudaEventDestroy(m->ev0);
     if (m->ev1) cudaEventDestroy(m->ev1);
+    if (m->ev_in) cudaEventDestroy(m->ev_in);
+    if (m->gexec) cudaGraphExecDestroy(m->gexec);
+    if (m->gstream) cudaStreamDestroy(m->gstream);
     for (cudaEvent_t e : m->st_ev)
         if (e) cudaEventDestroy(e);
     delete m;

@@ -1,0 +1,396 @@
+// svx_frame.cu -- per-frame orchestration of the integration path.
+//
+// A frame is five kernels plus two small copies, all reading their per-frame
+// values from the device-side FrameCtr (svx_internal.cuh):
+//   H2D   frame parameters + zeroed counters (one pinned copy)
+//   K1    march    masks, ray setup, fp64 band walk, frame-table insert + counts
+//   K2    compact  touched voxels -> list + row segments; device-side gate
+//   K3    scatter  row point indices into their voxel segments
+//   K4/5a update   leaf + voxel resolution fused with short-segment / open updates
+//   K5b   update   long / huge segments
+//   D2H   counters (one pinned copy)
+// The sequence is captured once into a CUDA graph and replayed while buffer
+// addresses stay the same; the host synchronises once per frame to read the
+// report.  A frame whose scratch turned out too small (or whose keys need a
+// different base) is stopped by the gate before any map mutation and re-run.
+#include <cuda_runtime.h>
+#include <limits.h>
+#include <math.h>
+#include <string.h>
+
+#include <algorithm>
+
+#include "svx_internal.cuh"
+
+namespace svx {
+
+bool is_device_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes a;
+    cudaError_t e = cudaPointerGetAttributes(&a, p);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+svx_status stage_in(const void* p, size_t bytes, DevBuf& stage, cudaStream_t s, const void** out) {
+    if (!p || bytes == 0) {
+        *out = p;
+        return SVX_OK;
+    }
+    if (is_device_ptr(p)) {
+        *out = p;
+        return SVX_OK;
+    }
+    SVX_TRY(ensure(stage, bytes, s));
+    SVX_CUDA(cudaMemcpyAsync(stage.p, p, bytes, cudaMemcpyHostToDevice, s));
+    *out = stage.p;
+    return SVX_OK;
+}
+
+size_t tsdf_elem(const svx_map* m) { return m->cfg.tsdf_dtype == SVX_F64 ? 8 : 4; }
+
+size_t sem_elem(const svx_map* m) {
+    if (m->cfg.sem_kind == SVX_SEM_CLOSED) return m->cfg.count_dtype == SVX_F64 ? 8 : 4;
+    if (m->cfg.sem_kind == SVX_SEM_OPEN) return m->cfg.state_dtype == SVX_F64 ? 8 : 4;
+    return 0;
+}
+
+// Voxel-pool capacity: grow by doubling, zero-filled (closed counts and open
+// means have a zero background; voxel ids are never recycled).
+svx_status reserve_voxels(svx_map* m, int64_t need, cudaStream_t s) {
+    if (need <= m->vcap) return SVX_OK;
+    int64_t cap = std::max<int64_t>(need, 2 * m->vcap);
+    const size_t te = tsdf_elem(m), se = sem_elem(m);
+    SVX_TRY(ensure(m->vt, 2 * te * cap, s, true));
+    if (m->cfg.sem_kind != SVX_SEM_NONE)
+        SVX_TRY(ensure(m->s0, se * (size_t)m->payload_d * cap, s, true, 0));
+    if (m->cfg.sem_kind == SVX_SEM_OPEN)
+        SVX_TRY(ensure(m->s1, se * (size_t)m->payload_d * cap, s, true, 0));
+    m->vcap = cap;
+    return SVX_OK;
+}
+
+svx_status reserve_blocks(svx_map* m, int64_t need, cudaStream_t s) {
+    if (need > m->bcap) {
+        int64_t cap = std::max<int64_t>(need, 2 * m->bcap);
+        SVX_TRY(ensure(m->bcoord, sizeof(int4) * cap, s, true));
+        SVX_TRY(ensure(m->bkey, sizeof(unsigned long long) * cap, s, true, 0xFF));
+        SVX_TRY(ensure(m->bmask, sizeof(unsigned long long) * kMaskWords * cap, s, true, 0));
+        SVX_TRY(ensure(m->bslot, sizeof(int) * kLeafVolume * cap, s, true, 0xFF));
+        m->bcap = cap;
+    }
+    // keep the leaf hash at <= 50% load for the worst case of this frame
+    int64_t want = 1024;
+    while (want < 2 * need) want <<= 1;
+    if (want > m->hcap) {
+        DevBuf nt;
+        SVX_TRY(ensure(nt, sizeof(int4) * want, s, false, 0xFF));
+        SVX_TRY(launch_rehash(m, ptr<int4>(nt), want, s));
+        SVX_CUDA(cudaStreamSynchronize(s));
+        release(m->hash);
+        m->hash = nt;
+        m->hcap = want;
+    }
+    return SVX_OK;
+}
+
+// Per-frame scratch for ucap unique voxels / rcap rows / n points.
+static svx_status reserve_frame(svx_map* m, int64_t n, cudaStream_t s) {
+    // frame table at <= 2/3 load for ucap keys
+    int64_t want = 1024;
+    while (2 * want < 3 * (int64_t)m->ucap) want <<= 1;
+    if (want > m->fcap || 2 * want <= m->fcap) {
+        release(m->fkey);
+        release(m->fcount);
+        release(m->fcur);
+        release(m->foff);
+        SVX_TRY(ensure(m->fkey, 8 * want, s, false, 0xFF));
+        SVX_TRY(ensure(m->fcount, 4 * want, s, false, 0));
+        SVX_TRY(ensure(m->fcur, 4 * want, s, false, 0));
+        SVX_TRY(ensure(m->foff, 4 * want, s));
+        m->fcap = want;
+    }
+    m->npts_cap = std::max<int64_t>(m->npts_cap, n);
+    SVX_TRY(ensure(m->ulist, 4 * m->ucap, s));
+    SVX_TRY(ensure(m->ukey, 8 * m->ucap, s));
+    SVX_TRY(ensure(m->gvid, 4 * m->ucap, s));
+    SVX_TRY(ensure(m->longlist, 8 * m->ucap, s));   // long list, then huge list
+    SVX_TRY(ensure(m->srid, 4 * m->rcap, s));
+    SVX_TRY(ensure(m->bitmap, (size_t)4 * huge_warps() * ((m->npts_cap + 31) / 32 + 1), s));
+    SVX_TRY(ensure(m->ray, sizeof(double4) * m->npts_cap, s));
+    SVX_TRY(ensure(m->rcnt, sizeof(int) * m->npts_cap, s));
+    SVX_TRY(ensure(m->partials, partials_bytes(), s));
+    if (m->maxrows > 0) {
+        SVX_TRY(ensure(m->rowslot, sizeof(int) * m->npts_cap * m->maxrows, s));
+        SVX_TRY(ensure(m->rowkey, sizeof(unsigned long long) * m->npts_cap * m->maxrows, s));
+    }
+    return SVX_OK;
+}
+
+static svx_status clear_frame_table(svx_map* m, cudaStream_t s) {
+    SVX_CUDA(cudaMemsetAsync(m->fkey.p, 0xFF, 8 * m->fcap, s));
+    SVX_CUDA(cudaMemsetAsync(m->fcount.p, 0, 4 * m->fcap, s));
+    SVX_CUDA(cudaMemsetAsync(m->fcur.p, 0, 4 * m->fcap, s));
+    return SVX_OK;
+}
+
+// Everything a captured graph bakes in: buffer addresses, grid-determining
+// capacities and kernel template choices.
+static unsigned long long graph_signature(const svx_map* m, int pts_f64, int feats_f64) {
+    const void* ptrs[] = {m->ray.p,    m->rcnt.p,  m->rowslot.p, m->rowkey.p, m->partials.p,
+                          m->fkey.p,   m->fcount.p, m->foff.p,   m->fcur.p,  m->ulist.p,
+                          m->ukey.p,   m->gvid.p,  m->longlist.p, m->srid.p, m->bitmap.p,
+                          m->hash.p,   m->bcoord.p, m->bkey.p,   m->bmask.p, m->bslot.p,
+                          m->vt.p,     m->s0.p,    m->s1.p,      m->ctr.p};
+    unsigned long long h = 1469598103934665603ULL;
+    auto mix = [&](unsigned long long v) {
+        h ^= v;
+        h *= 1099511628211ULL;
+    };
+    for (const void* p : ptrs) mix((unsigned long long)(uintptr_t)p);
+    mix((unsigned long long)m->fcap);
+    mix(m->ucap);
+    mix((unsigned long long)m->npts_cap);
+    mix((unsigned long long)(m->maxrows > 0));
+    mix((unsigned long long)(pts_f64 * 2 + feats_f64));
+    return h;
+}
+
+#define STAGE_BEGIN(i) \
+    do { if (m->prof) { cudaEventRecord(m->st_ev[2 * (i)], s); m->st_mask |= 1u << (i); } } while (0)
+#define STAGE_END(i) \
+    do { if (m->prof) cudaEventRecord(m->st_ev[2 * (i) + 1], s); } while (0)
+
+// Enqueue one frame attempt on stream s (eager or under graph capture).
+static svx_status enqueue_frame(svx_map* m, int pts_f64, int feats_f64, cudaStream_t s) {
+    FrameCtr* dc = ptr<FrameCtr>(m->ctr);
+    SVX_CUDA(cudaMemcpyAsync(dc, m->h_ctr, sizeof(FrameCtr), cudaMemcpyHostToDevice, s));
+    STAGE_BEGIN(0);
+    SVX_TRY(launch_march(m, pts_f64, feats_f64, s));
+    STAGE_END(0);
+    STAGE_BEGIN(1);
+    SVX_TRY(launch_compact(m, s));
+    STAGE_END(1);
+    STAGE_BEGIN(2);
+    if (inline_singles(m)) SVX_TRY(launch_scatter_update(m, s));
+    else SVX_TRY(launch_scatter(m, m->maxrows > 0, s));
+    STAGE_END(2);
+    STAGE_BEGIN(3);
+    SVX_TRY(launch_update_a(m, feats_f64, s));
+    STAGE_END(3);
+    STAGE_BEGIN(4);
+    SVX_TRY(launch_update_b(m, feats_f64, s));
+    STAGE_END(4);
+    SVX_CUDA(cudaMemcpyAsync(m->h_ctr, dc, sizeof(FrameCtr), cudaMemcpyDeviceToHost, s));
+    return SVX_OK;
+}
+
+static void collect_stage_times(svx_map* m) {
+    for (int i = 0; i < SVX_N_STAGES; ++i) {
+        m->stage_ms[i] = 0.0;
+        if (!(m->st_mask & (1u << i))) continue;
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, m->st_ev[2 * i], m->st_ev[2 * i + 1]) == cudaSuccess)
+            m->stage_ms[i] = ms;
+        else
+            cudaGetLastError();
+    }
+    m->st_mask = 0;
+}
+
+// Run one frame attempt: replay (or capture) the graph on the map's own
+// stream, ordered after the caller's stream; profiling runs eagerly so each
+// stage can be bracketed with events.
+static svx_status run_frame(svx_map* m, int pts_f64, int feats_f64, cudaStream_t s) {
+    if (m->prof) {
+        m->st_mask = 0;
+        SVX_TRY(enqueue_frame(m, pts_f64, feats_f64, s));
+        SVX_CUDA(cudaEventRecord(m->ev1, s));
+        SVX_CUDA(cudaEventSynchronize(m->ev1));
+        collect_stage_times(m);
+        return SVX_OK;
+    }
+    const unsigned long long sig = graph_signature(m, pts_f64, feats_f64);
+    if (!m->gexec || sig != m->gsig) {
+        if (m->gexec) {
+            cudaGraphExecDestroy(m->gexec);
+            m->gexec = nullptr;
+        }
+        SVX_CUDA(cudaStreamBeginCapture(m->gstream, cudaStreamCaptureModeThreadLocal));
+        svx_status st = enqueue_frame(m, pts_f64, feats_f64, m->gstream);
+        cudaGraph_t g = nullptr;
+        cudaError_t e = cudaStreamEndCapture(m->gstream, &g);
+        if (st != SVX_OK) {
+            if (g) cudaGraphDestroy(g);
+            return st;
+        }
+        if (e != cudaSuccess) return fail(SVX_E_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+        e = cudaGraphInstantiate(&m->gexec, g, 0);
+        cudaGraphDestroy(g);
+        if (e != cudaSuccess) {
+            m->gexec = nullptr;
+            return fail(SVX_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+        }
+        m->gsig = sig;
+    }
+    SVX_CUDA(cudaEventRecord(m->ev_in, s));
+    SVX_CUDA(cudaStreamWaitEvent(m->gstream, m->ev_in, 0));
+    SVX_CUDA(cudaGraphLaunch(m->gexec, m->gstream));
+    count_launch(6);
+    SVX_CUDA(cudaEventRecord(m->ev1, m->gstream));
+    SVX_CUDA(cudaEventSynchronize(m->ev1));
+    return SVX_OK;
+}
+
+svx_status integrate_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n,
+                          const PoseParams& pp, const int32_t* labels_in, const void* feats_in,
+                          int feats_f64, cudaStream_t s, svx_report* rep) {
+    svx_report r;
+    memset(&r, 0, sizeof(r));
+    r.points_in = n;
+    const int kind = m->cfg.sem_kind;
+    if (kind == SVX_SEM_CLOSED && !labels_in)
+        return fail(SVX_E_PAYLOAD, "closed-set grid requires per-point labels");
+    if (kind == SVX_SEM_OPEN && !feats_in)
+        return fail(SVX_E_PAYLOAD, "open-set grid requires per-point features");
+    if (n < 0) return fail(SVX_E_INPUT, "negative point count");
+    if (n >= (int64_t)INT_MAX) return fail(SVX_E_INPUT, "point count exceeds 2^31-1");
+    if (n == 0) {
+        m->frames++;
+        if (rep) *rep = r;
+        return SVX_OK;
+    }
+    SVX_CUDA(cudaEventRecord(m->ev0, s));
+    const void* pts;
+    const void* feats = nullptr;
+    const void* labv = nullptr;
+    SVX_TRY(stage_in(pts_in, (size_t)n * 3 * (pts_f64 ? 8 : 4), m->in_pts, s, &pts));
+    if (kind == SVX_SEM_CLOSED) SVX_TRY(stage_in(labels_in, (size_t)n * 4, m->in_lab, s, &labv));
+    if (kind == SVX_SEM_OPEN)
+        SVX_TRY(stage_in(feats_in, (size_t)n * m->payload_d * (feats_f64 ? 8 : 4), m->in_feat, s,
+                         &feats));
+
+    // Scratch sizing.  A band of length L crosses at most 3 * (L / h + 1)
+    // voxels; without carving L = 2 * trunc, so each ray gets that many row
+    // slots and the scatter is one flat pass.  Carving bands are unbounded:
+    // the scatter re-walks them.  Capacities adapt to what frames need.
+    const double h = m->cfg.voxel_size;
+    if (m->maxrows < 0) {
+        const double bound = 3.0 * (2.0 * m->cfg.truncation / h + 1.0) + 3.0;
+        m->maxrows = (m->cfg.space_carving || bound > 64.0) ? 0 : (int)bound;
+    }
+    const double band = m->cfg.space_carving ? m->cfg.max_range + m->cfg.truncation
+                                             : 2.0 * m->cfg.truncation;
+    const uint64_t per_ray = (uint64_t)std::min(64.0, 3.0 * (band / h + 1.0) + 3.0);
+    if (m->rcap == 0) {   // first frame: worst-case guesses, adapted after each frame
+        m->rcap = (uint64_t)n * per_ray;
+        m->ucap = std::min<uint64_t>(m->rcap, (uint64_t)n * 16);
+    }
+
+    KeyPack kp;
+    {
+        const long long half = 1LL << (kPackBits - 1);
+        for (int a = 0; a < 3; ++a) kp.base[a] = (long long)floor(pp.t[a] / h) - half;
+    }
+    FrameCtr* hc = m->h_ctr;
+    for (int attempt = 0;; ++attempt) {
+        if (attempt >= 8) return fail(SVX_E_INTERNAL, "frame scratch could not be sized");
+        SVX_TRY(reserve_frame(m, n, s));
+        SVX_TRY(reserve_blocks(m, m->nblocks + (int64_t)m->ucap, s));
+        SVX_TRY(reserve_voxels(m, m->nvox + (int64_t)m->ucap, s));
+
+        memset(hc, 0, sizeof(FrameCtr));
+        for (int a = 0; a < 3; ++a) {
+            hc->bbox_min[a] = LLONG_MAX;
+            hc->bbox_max[a] = LLONG_MIN;
+        }
+        hc->nblocks = (unsigned long long)m->nblocks;
+        hc->nvox = (unsigned long long)m->nvox;
+        FrameParams& p = hc->p;
+        p.pts = pts;
+        p.labels = (const int32_t*)labv;
+        p.feats = feats;
+        p.n = n;
+        p.pp = pp;
+        p.kp = kp;
+        p.ucap = m->ucap;
+        p.rcap = m->rcap;
+        p.fmask = m->fcap - 1;
+        p.hmask = m->hcap - 1;
+        p.nblocks0 = m->nblocks;
+        p.frame = (int)m->frames;
+        p.maxrows = m->maxrows;
+
+        SVX_TRY(run_frame(m, pts_f64, feats_f64, s));
+
+        // the reference's pre-allocation checks, in its order (_core.pyx:661-712, :386-387)
+        if (hc->err_budget) {
+            SVX_TRY(clear_frame_table(m, s));
+            return fail(SVX_E_INTERNAL, "ray band exceeds step budget; shrink max_range or grow voxels");
+        }
+        if (hc->rows) {
+            bool extent = false, range = false;
+            for (int a = 0; a < 3; ++a) {
+                if (hc->bbox_max[a] - hc->bbox_min[a] >= (1LL << kPackBits)) extent = true;
+                if (llabs(hc->bbox_min[a]) >= kCoordLimit || llabs(hc->bbox_max[a]) >= kCoordLimit)
+                    range = true;
+            }
+            if (extent) {
+                SVX_TRY(clear_frame_table(m, s));
+                return fail(SVX_E_INTERNAL,
+                            "frame voxel extent exceeds 2^21 per axis; shrink max_range or grow voxels");
+            }
+            if (range) {
+                SVX_TRY(clear_frame_table(m, s));
+                return fail(SVX_E_RANGE, "voxel coordinate beyond +/-2^30 addressable range");
+            }
+        }
+        if (hc->abort) {
+            SVX_TRY(clear_frame_table(m, s));
+            if (hc->err_pack)
+                for (int a = 0; a < 3; ++a) kp.base[a] = hc->bbox_min[a];
+            if (hc->err_rows) m->maxrows = 0;
+            if (hc->err_probe || hc->n_groups > m->ucap || hc->rows_c > m->rcap ||
+                hc->rows > m->rcap) {
+                m->rcap = std::max<uint64_t>(2 * m->rcap, hc->rows + hc->rows / 2);
+                m->ucap = std::max<uint64_t>(2 * m->ucap,
+                                             std::min<uint64_t>(m->rcap, hc->n_groups * 2));
+            }
+            SVX_CUDA(cudaStreamSynchronize(s));
+            continue;
+        }
+        break;
+    }
+    float ms = 0.f;
+    SVX_CUDA(cudaEventElapsedTime(&ms, m->ev0, m->ev1));
+    r.skipped_nonfinite = (int64_t)hc->nonfinite;
+    r.skipped_range = (int64_t)hc->range;
+    r.skipped_degenerate = (int64_t)hc->degenerate;
+    r.skipped_bad_label = (int64_t)hc->bad_label;
+    r.points_used = (int64_t)hc->used;
+    r.band_hits = (int64_t)hc->band_hits;
+    r.touched_voxels = (int64_t)hc->n_groups;
+    r.new_blocks = (int64_t)hc->nblocks - m->nblocks;
+    r.new_voxels = (int64_t)hc->nvox - m->nvox;
+    r.kernel_ms = ms;
+    m->nblocks = (int64_t)hc->nblocks;
+    m->nvox = (int64_t)hc->nvox;
+    m->frames++;
+    // adapt the scratch to what this frame needed (headroom for the next)
+    // (grow when nearly full, shrink once when far too big: the first frame's
+    // worst-case guess would otherwise keep the frame table cold and large)
+    const uint64_t u_next = hc->n_groups + hc->n_groups / 2 + 4096;
+    const uint64_t r_next = hc->rows_c + hc->rows_c / 2 + 4096;
+    if (hc->n_groups * 10 > m->ucap * 8 || u_next * 3 < m->ucap * 2) m->ucap = u_next;
+    const uint64_t rows_seen = std::max<uint64_t>(hc->rows_c, hc->rows);
+    const uint64_t r_need = rows_seen + rows_seen / 2 + 4096;
+    if (rows_seen * 10 > m->rcap * 8 || r_need * 3 < m->rcap * 2) m->rcap = r_need;
+    (void)r_next;
+    if (rep) *rep = r;
+    return SVX_OK;
+}
+
+}  // namespace svx

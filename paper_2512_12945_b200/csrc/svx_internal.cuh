@@ -39,8 +39,48 @@ constexpr int kHashBusy = -2;
 
 constexpr int kShortMax = 16;   // segments up to this many rows: thread-per-voxel update
 
+struct PoseParams {
+    double R[9];
+    double t[3];
+    int sensor;      // 1: transform points by (R, t); 0: points already world, origin = t
+};
+
+// Frame key: voxel offsets from `base` packed 21 bits per axis, x-major, so
+// key order is the reference's lexicographic voxel order (_core.pyx:727-732).
+struct KeyPack {
+    long long base[3];
+};
+
+// Everything that changes from frame to frame lives in device memory, so one
+// captured CUDA graph replays every frame.
+struct FrameParams {
+    const void* pts;
+    const int32_t* labels;
+    const void* feats;
+    long long n;
+    PoseParams pp;
+    KeyPack kp;
+    unsigned long long ucap;   // unique voxels the scratch holds
+    unsigned long long rcap;   // rows the scratch holds
+    long long fmask;           // frame table capacity - 1
+    long long hmask;           // leaf hash capacity - 1
+    long long nblocks0;        // leaves before this frame (ids >= it are new)
+    int frame;                 // creation stamp for new leaves
+    int maxrows;               // row slots per ray (0: scatter re-walks the band)
+};
+
+// Per-CTA partial counters of the march, reduced by the gate (no
+// same-address atomics on the hot path).
+struct MarchPartial {
+    unsigned long long nonfinite, range, degenerate, bad_label, used, band_hits, rows;
+    long long bbox_min[3], bbox_max[3];
+    int errs;      // bit 0 budget, 1 pack, 2 probe, 3 rows
+    int pad;
+};
+
 // Per-frame device counters and flags, copied back once per frame.
 struct FrameCtr {
+    FrameParams p;
     unsigned long long nonfinite;
     unsigned long long range;
     unsigned long long degenerate;
@@ -49,7 +89,9 @@ struct FrameCtr {
     unsigned long long band_hits;   // rows emitted before the w <= 0 drop
     unsigned long long rows;        // rows kept (w > 0), counted by the march
     unsigned long long n_groups;    // unique voxels (U), from the compaction
-    unsigned long long rows_c;      // rows (R), from the compaction
+    unsigned long long n_list;      // voxels listed for the segment updates (U, or the
+                                    // multi-row ones when single-row voxels update inline)
+    unsigned long long rows_c;      // rows in listed segments, from the compaction
     unsigned long long n_long;      // voxels routed to the long-segment update
     unsigned long long n_huge;      // voxels routed to the huge-segment update
     unsigned long long n_new_blocks;
@@ -61,7 +103,9 @@ struct FrameCtr {
     int err_budget;                 // a ray exceeded the DDA step budget
     int err_pack;                   // a key offset left the 21-bit field (retry with bbox base)
     int err_probe;                  // frame hash full (retry with a bigger table)
-    int abort;                      // set by the compaction: skip all mutation
+    int err_rows;                   // a band exceeded maxrows (retry with the re-walk scatter)
+    int abort;                      // set by the gate: skip all mutation
+    int pad;
 };
 
 // Growable device buffer.
@@ -76,26 +120,6 @@ struct MarchParams {
     double max_range;
     int carving;
     int wfn;         // 0 constant_one, 1 linear_dropoff
-};
-
-struct PoseParams {
-    double R[9];
-    double t[3];
-    int sensor;      // 1: transform points by (R, t); 0: points already world, origin = t
-};
-
-// Frame key: voxel offsets from `base` packed 21 bits per axis, x-major, so
-// key order is the reference's lexicographic voxel order (_core.pyx:727-732).
-struct KeyPack {
-    long long base[3];
-};
-
-// Capacities of the per-frame scratch for this attempt.
-struct FrameCaps {
-    unsigned long long ucap;   // unique voxels
-    unsigned long long rcap;   // rows
-    long long fmask;           // frame hash capacity - 1
-    int frame;                 // frame stamp
 };
 
 __host__ __device__ inline unsigned long long pack_key(long long dx, long long dy, long long dz) {
@@ -118,14 +142,20 @@ struct svx_map {
     // persistent state
     svx::DevBuf hash;  int64_t hcap = 0;
     svx::DevBuf bcoord, bkey, bmask, bslot;  int64_t bcap = 0, nblocks = 0;
-    svx::DevBuf vd, vw, s0, s1;              int64_t vcap = 0, nvox = 0;
+    svx::DevBuf vt, s0, s1;                  int64_t vcap = 0, nvox = 0;  // vt: {d, w} per voxel
     int64_t frames = 0;
     // per-frame scratch
     svx::DevBuf in_pts, in_lab, in_feat;
-    svx::DevBuf ray;
+    svx::DevBuf ray, rcnt, rowslot, rowkey, partials;
     svx::DevBuf fkey, fcount, foff, fcur;  int64_t fcap = 0;
     svx::DevBuf ulist, ukey, gvid, longlist, srid, bitmap;
     uint64_t ucap = 0, rcap = 0;
+    int maxrows = -1;      // row slots per ray; 0 = re-walk scatter
+    int64_t npts_cap = 0;  // points the per-ray scratch holds
+    // captured frame graph (replayed while the layout is unchanged)
+    cudaStream_t gstream = nullptr;
+    cudaGraphExec_t gexec = nullptr;
+    unsigned long long gsig = 0;
     svx::DevBuf cubtmp;
     svx::DevBuf ctr;      // FrameCtr
     svx::FrameCtr* h_ctr = nullptr;  // pinned mirror
@@ -135,7 +165,7 @@ struct svx_map {
     int* leaf_order = nullptr;
     svx::DevBuf act_cnt, act_off, act_vid, act_coord, q_buf, out_buf;
     int64_t act_valid_frames = -1;
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_in = nullptr;
     // optional per-stage timing (svx_set_profiling)
     bool prof = false;
     cudaEvent_t st_ev[2 * SVX_N_STAGES] = {};
@@ -187,6 +217,12 @@ inline int grid_for(int64_t n, int threads) {
 }
 
 constexpr int kPersistentBlocks = 148 * 8;   // grid-stride kernels over device-side counts
+constexpr int kMarchBlocks = 148 * 4;        // march CTAs (one partial-counter record each)
+
+// TSDF state of one voxel, {d, w} interleaved so an update touches one sector.
+template <class T> struct Pair;
+template <> struct Pair<double> { using type = double2; };
+template <> struct Pair<float> { using type = float2; };
 
 // ---- hashing -----------------------------------------------------------------
 __host__ __device__ inline uint64_t block_hash(int a, int b, int c) {
@@ -220,19 +256,33 @@ __device__ inline int hash_find(const int4* __restrict__ table, int64_t mask, in
     }
 }
 
+// ---- svx_frame.cu ------------------------------------------------------------
+bool is_device_ptr(const void* p);
+svx_status stage_in(const void* p, size_t bytes, DevBuf& stage, cudaStream_t s, const void** out);
+size_t tsdf_elem(const svx_map* m);
+size_t sem_elem(const svx_map* m);
+svx_status reserve_voxels(svx_map* m, int64_t need, cudaStream_t s);
+svx_status reserve_blocks(svx_map* m, int64_t need, cudaStream_t s);
+svx_status integrate_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n,
+                          const PoseParams& pp, const int32_t* labels_in, const void* feats_in,
+                          int feats_f64, cudaStream_t s, svx_report* rep);
+
 // ---- launchers implemented in the .cu files ---------------------------------
 // svx_march.cu
-svx_status launch_march(svx_map* m, const void* pts, int pts_f64, int64_t n, const PoseParams& pp,
-                        const KeyPack& kp, const FrameCaps& fc, const int32_t* labels,
-                        const void* feats, int feats_f64, cudaStream_t s);
-svx_status launch_compact(svx_map* m, const FrameCaps& fc, cudaStream_t s);
-svx_status launch_scatter(svx_map* m, int64_t n, const PoseParams& pp, const KeyPack& kp,
-                          const FrameCaps& fc, cudaStream_t s);
-// svx_update.cu
-svx_status launch_voxels(svx_map* m, const KeyPack& kp, const FrameCaps& fc, cudaStream_t s);
-svx_status launch_update(svx_map* m, const KeyPack& kp, const PoseParams& pp, const FrameCaps& fc,
-                         const int32_t* labels, const void* feats, int feats_f64, int64_t n,
-                         cudaStream_t s);
+MarchParams march_params(const svx_map* m);
+svx_status launch_march(svx_map* m, int pts_f64, int feats_f64, cudaStream_t s);
+svx_status launch_compact(svx_map* m, cudaStream_t s);
+svx_status launch_scatter(svx_map* m, bool flat, cudaStream_t s);
+size_t partials_bytes();
+// Single-row voxels of bounded (non-carving) closed/geometry frames are
+// updated inline by the scatter pass; everything else goes through segments.
+inline int inline_singles(const svx_map* m) {
+    return m->maxrows > 0 && m->cfg.sem_kind != SVX_SEM_OPEN;
+}
+svx_status launch_scatter_update(svx_map* m, cudaStream_t s);
+// svx_update.cu: stage A = resolve + short/open updates, stage B = long/huge
+svx_status launch_update_a(svx_map* m, int feats_f64, cudaStream_t s);
+svx_status launch_update_b(svx_map* m, int feats_f64, cudaStream_t s);
 svx_status launch_rehash(svx_map* m, int4* new_table, int64_t new_cap, cudaStream_t s);
 int huge_warps();
 // svx_query.cu

@@ -74,14 +74,14 @@ __global__ void k_list(int64_t nblocks, const int* __restrict__ order,
 }
 
 template <class T>
-__global__ void k_gather_rows(int64_t count, int width, const int* __restrict__ act_vid,
+__global__ void k_gather_rows(int64_t count, int width, int sstride, const int* __restrict__ act_vid,
                               const T* __restrict__ src, T* __restrict__ dst) {
     int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int64_t total = count * width;
     for (; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
         int64_t i = idx / width;
         int c = (int)(idx - i * width);
-        dst[idx] = src[(int64_t)act_vid[i] * width + c];
+        dst[idx] = src[(int64_t)act_vid[i] * sstride + c];
     }
 }
 
@@ -110,7 +110,7 @@ __global__ void k_probe_vid(int64_t cnt, const long long* __restrict__ coords,
 }
 
 template <class T>
-__global__ void k_probe_rows(int64_t cnt, int width, const int* __restrict__ vid,
+__global__ void k_probe_rows(int64_t cnt, int width, int sstride, const int* __restrict__ vid,
                              const T* __restrict__ src, T bg, T* __restrict__ dst) {
     int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int64_t total = cnt * width;
@@ -118,7 +118,7 @@ __global__ void k_probe_rows(int64_t cnt, int width, const int* __restrict__ vid
         int64_t i = idx / width;
         int c = (int)(idx - i * width);
         int v = vid[i];
-        dst[idx] = v >= 0 ? src[(int64_t)v * width + c] : bg;
+        dst[idx] = v >= 0 ? src[(int64_t)v * sstride + c] : bg;
     }
 }
 
@@ -173,7 +173,7 @@ __global__ void k_classify(int64_t count, int D, int k, const int* __restrict__ 
     }
     nn = warp_sum(nn);
     const double mn = sqrt(nn);
-    const double wgt = (double)vw[vid];
+    const double wgt = (double)vw[2 * (int64_t)vid + 1];   // {d, w} pairs
     const bool ok = mn != 0.0 && wgt > 0.0;
     double cache[kCache];
     double lmax = -INFINITY;
@@ -320,21 +320,24 @@ svx_status build_active_list(svx_map* m, int64_t* count, cudaStream_t s) {
     return SVX_OK;
 }
 
+// dst (count, width) <- rows vid * sstride + [0, width) of src; sstride < 0
+// means sstride = width.  src_off selects a column of interleaved records.
 template <class T>
 static svx_status gather_rows(int64_t count, int width, const int* vid, const void* src, void* dst,
-                              cudaStream_t s) {
+                              cudaStream_t s, int sstride = -1, int src_off = 0) {
     if (!dst || count == 0) return SVX_OK;
     int64_t total = count * width;
     int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 32);
-    k_gather_rows<T><<<blocks, 256, 0, s>>>(count, width, vid, (const T*)src, (T*)dst);
+    k_gather_rows<T><<<blocks, 256, 0, s>>>(count, width, sstride < 0 ? width : sstride, vid,
+                                            (const T*)src + src_off, (T*)dst);
     SVX_LAUNCHED();
     return SVX_OK;
 }
 
 static svx_status gather_typed(int f64, int64_t count, int width, const int* vid, const void* src,
-                               void* dst, cudaStream_t s) {
-    return f64 ? gather_rows<double>(count, width, vid, src, dst, s)
-               : gather_rows<float>(count, width, vid, src, dst, s);
+                               void* dst, cudaStream_t s, int sstride = -1, int src_off = 0) {
+    return f64 ? gather_rows<double>(count, width, vid, src, dst, s, sstride, src_off)
+               : gather_rows<float>(count, width, vid, src, dst, s, sstride, src_off);
 }
 
 svx_status launch_export(svx_map* m, int64_t count, int64_t* coords, void* d, void* w, void* sem0,
@@ -347,8 +350,8 @@ svx_status launch_export(svx_map* m, int64_t count, int64_t* coords, void* d, vo
         SVX_LAUNCHED();
     }
     const int td64 = m->cfg.tsdf_dtype == SVX_F64;
-    SVX_TRY(gather_typed(td64, count, 1, vid, m->vd.p, d, s));
-    SVX_TRY(gather_typed(td64, count, 1, vid, m->vw.p, w, s));
+    SVX_TRY(gather_typed(td64, count, 1, vid, m->vt.p, d, s, 2, 0));
+    SVX_TRY(gather_typed(td64, count, 1, vid, m->vt.p, w, s, 2, 1));
     if (m->cfg.sem_kind == SVX_SEM_CLOSED) {
         SVX_TRY(gather_typed(m->cfg.count_dtype == SVX_F64, count, m->payload_d, vid, m->s0.p,
                              sem0, s));
@@ -362,19 +365,21 @@ svx_status launch_export(svx_map* m, int64_t count, int64_t* coords, void* d, vo
 
 template <class T>
 static svx_status probe_rows(int64_t cnt, int width, const int* vid, const void* src, double bg,
-                             void* dst, cudaStream_t s) {
+                             void* dst, cudaStream_t s, int sstride = -1, int src_off = 0) {
     if (!dst || cnt == 0) return SVX_OK;
     int64_t total = cnt * width;
     int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 32);
-    k_probe_rows<T><<<blocks, 256, 0, s>>>(cnt, width, vid, (const T*)src, (T)bg, (T*)dst);
+    k_probe_rows<T><<<blocks, 256, 0, s>>>(cnt, width, sstride < 0 ? width : sstride, vid,
+                                           (const T*)src + src_off, (T)bg, (T*)dst);
     SVX_LAUNCHED();
     return SVX_OK;
 }
 
 static svx_status probe_typed(int f64, int64_t cnt, int width, const int* vid, const void* src,
-                              double bg, void* dst, cudaStream_t s) {
-    return f64 ? probe_rows<double>(cnt, width, vid, src, bg, dst, s)
-               : probe_rows<float>(cnt, width, vid, src, bg, dst, s);
+                              double bg, void* dst, cudaStream_t s, int sstride = -1,
+                              int src_off = 0) {
+    return f64 ? probe_rows<double>(cnt, width, vid, src, bg, dst, s, sstride, src_off)
+               : probe_rows<float>(cnt, width, vid, src, bg, dst, s, sstride, src_off);
 }
 
 svx_status launch_probe(svx_map* m, const int64_t* coords, int64_t cnt, void* d, void* w,
@@ -392,8 +397,8 @@ svx_status launch_probe(svx_map* m, const int64_t* coords, int64_t cnt, void* d,
         SVX_LAUNCHED();
     }
     const int td64 = m->cfg.tsdf_dtype == SVX_F64;
-    SVX_TRY(probe_typed(td64, cnt, 1, vid, m->vd.p, m->cfg.truncation, d, s));
-    SVX_TRY(probe_typed(td64, cnt, 1, vid, m->vw.p, 0.0, w, s));
+    SVX_TRY(probe_typed(td64, cnt, 1, vid, m->vt.p, m->cfg.truncation, d, s, 2, 0));
+    SVX_TRY(probe_typed(td64, cnt, 1, vid, m->vt.p, 0.0, w, s, 2, 1));
     if (m->cfg.sem_kind == SVX_SEM_CLOSED) {
         SVX_TRY(probe_typed(m->cfg.count_dtype == SVX_F64, cnt, m->payload_d, vid, m->s0.p, 0.0,
                             sem0, s));
@@ -425,7 +430,7 @@ static svx_status classify_t(svx_map* m, int64_t count, const double* emb, const
                              cudaStream_t s) {
     const int T = 256;
     k_classify<TS, TD><<<grid_for(count * 32, T), T, 0, s>>>(
-        count, m->payload_d, k, ptr<int>(m->act_vid), ptr<TS>(m->s0), ptr<TD>(m->vw), emb, en,
+        count, m->payload_d, k, ptr<int>(m->act_vid), ptr<TS>(m->s0), ptr<TD>(m->vt), emb, en,
         tau, tp, labels, best, sims);
     SVX_LAUNCHED();
     return SVX_OK;

@@ -1,4 +1,4 @@
-// svx_update.cu -- leaf allocation (K4) and the fused TSDF + semantic update
+// svx_update.cu -- leaf allocation (K4) fused with the TSDF + semantic update
 // (K5/K6).
 //
 // Compiled with -fmad=false.  Every voxel's rows are put back into point
@@ -7,13 +7,15 @@
 // restates apply_tsdf / apply_closed / apply_open (_pycore.py:399-446)
 // operation for operation, so stored values round identically.
 //
-// Segment lengths decide the execution shape:
+// Stage A resolves every touched voxel (leaf find-or-insert with its
+// creation stamp, voxel activation) and updates the ones it can finish:
 //   short  (<= kShortMax rows)   one thread per voxel, register insertion sort
+//   open                         one warp per voxel (lanes own feature dims)
+// Stage B finishes the rest:
 //   long   (<= kSmemMax rows)    one warp per voxel, shared-memory bitonic sort
 //   huge   (> kSmemMax rows)     one warp per voxel, point-index bitmap in global
 //                                scratch streamed in ascending chunks (space
 //                                carving sends every ray through the origin voxel)
-// Open-set voxels always take the warp shapes (lanes own feature dimensions).
 #include <math.h>
 
 #include "svx_internal.cuh"
@@ -29,14 +31,9 @@ __device__ __forceinline__ int slot_of(long long x, long long y, long long z) {
     return (int)(((x & 7) << 6) | ((y & 7) << 3) | (z & 7));
 }
 
-__device__ __forceinline__ bool frame_aborted(const FrameCtr* ctr) {
-    return *(volatile const int*)&ctr->abort != 0;
-}
-
 // counter += 1 for every converged lane, one atomic per warp; returns this
 // lane's ticket.
-__device__ __forceinline__ unsigned long long warp_aggregate_add(unsigned long long* counter,
-                                                                 unsigned long long /*one*/) {
+__device__ __forceinline__ unsigned long long warp_ticket(unsigned long long* counter) {
     const unsigned mask = __activemask();
     const int lane = threadIdx.x & 31;
     const int leader = __ffs(mask) - 1;
@@ -53,15 +50,25 @@ __device__ int leaf_find_or_insert(int4* table, long long mask, int a, int b, in
                                    int4* bcoord, FrameCtr* ctr) {
     long long pos = (long long)(block_hash(a, b, c) & (unsigned long long)mask);
     while (true) {
+        // Fast path: one 16-byte L2 read of the slot.  A published id (>= 0)
+        // was written after its key (release fence on the creating side), so
+        // a matching key is final -- almost every lookup ends here without a
+        // fence of its own.
+        const int4 sv = __ldcg(table + pos);
+        if (sv.w >= 0) {
+            if (sv.x == a && sv.y == b && sv.z == c) return sv.w;
+            pos = (pos + 1) & mask;
+            continue;
+        }
         volatile int* vw = &table[pos].w;
-        int v = *vw;
+        int v = sv.w;
         if (v == kHashEmpty) {
             int old = atomicCAS((int*)&table[pos].w, kHashEmpty, kHashBusy);
             if (old == kHashEmpty) {
                 table[pos].x = a;
                 table[pos].y = b;
                 table[pos].z = c;
-                int id = (int)warp_aggregate_add(&ctr->nblocks, 1ULL);
+                int id = (int)warp_ticket(&ctr->nblocks);
                 bcoord[id] = make_int4(a, b, c, frame);
                 __threadfence();
                 atomicExch((int*)&table[pos].w, id);
@@ -80,34 +87,34 @@ __device__ int leaf_find_or_insert(int4* table, long long mask, int a, int b, in
     }
 }
 
-// K4: per touched voxel -- leaf lookup/allocation, creation stamp for leaves
-// created this frame (their first-occurrence key), voxel activation.
-__global__ void __launch_bounds__(256) k_voxels(
-    const int* __restrict__ ulist, const unsigned long long* __restrict__ ukey, KeyPack kp,
-    int4* table, long long hmask, int frame, int4* bcoord, unsigned long long* bkey,
-    unsigned long long* bmask, int* bslot, int* __restrict__ gvid, FrameCtr* ctr) {
-    if (frame_aborted(ctr)) return;
-    const long long U = (long long)ctr->n_groups;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < U;
-         i += (long long)gridDim.x * blockDim.x) {
-        const unsigned long long key = ukey[i];
-        long long x, y, z;
-        unpack_key(key, kp, x, y, z);
-        const int id = leaf_find_or_insert(table, hmask, (int)(x >> kLeafLog2),
-                                           (int)(y >> kLeafLog2), (int)(z >> kLeafLog2), frame,
-                                           bcoord, ctr);
-        if (__ldcg(&bcoord[id].w) == frame) atomicMin(&bkey[id], key);
-        const int slot = slot_of(x, y, z);
-        int* sp = &bslot[(long long)id * kLeafVolume + slot];
-        int vid = *sp;
-        int isnew = vid < 0;
-        if (isnew) {
-            vid = (int)warp_aggregate_add(&ctr->nvox, 1ULL);
-            *sp = vid;
-            atomicOr(&bmask[(long long)id * kMaskWords + (slot >> 6)], 1ULL << (slot & 63));
-        }
-        gvid[i] = vid | (isnew ? (int)0x80000000 : 0);
-    }
+struct Maps {
+    int4* table;
+    int4* bcoord;
+    unsigned long long* bkey;
+    unsigned long long* bmask;
+    int* bslot;
+};
+
+// K4 for one voxel: its leaf (allocated in arrival order, stamped with the
+// voxel's frame key when the leaf is new this frame, which yields the
+// first-occurrence order the reference allocates in, _core.pyx:377-420) and
+// its voxel id (activated if new).  Returns vid, negative bit = new voxel.
+__device__ __forceinline__ int resolve_voxel(const Maps& mp, unsigned long long key, long long x,
+                                             long long y, long long z, long long hmask, int frame,
+                                             long long nblocks0, FrameCtr* ctr) {
+    const int id = leaf_find_or_insert(mp.table, hmask, (int)(x >> kLeafLog2),
+                                       (int)(y >> kLeafLog2), (int)(z >> kLeafLog2), frame,
+                                       mp.bcoord, ctr);
+    // leaves created this frame have ids past the frame's starting count
+    if (id >= nblocks0) atomicMin(&mp.bkey[id], key);
+    const int slot = slot_of(x, y, z);
+    int* sp = &mp.bslot[(long long)id * kLeafVolume + slot];
+    int vid = *sp;
+    if (vid >= 0) return vid;
+    vid = (int)warp_ticket(&ctr->nvox);
+    *sp = vid;
+    atomicOr(&mp.bmask[(long long)id * kMaskWords + (slot >> 6)], 1ULL << (slot & 63));
+    return vid | (int)0x80000000;
 }
 
 // Clamped projective distance and weight of one row (row_distances_weights,
@@ -126,20 +133,30 @@ __device__ __forceinline__ bool equals_stored(TD stored, double v) {
     return stored == (TD)v;
 }
 
-// apply_tsdf (_pycore.py:399-417) for one voxel; returns w_old.
+// apply_tsdf (_pycore.py:399-417) for one voxel; vt holds {d, w} pairs.
+// Returns w_old.
 template <class TD>
-__device__ __forceinline__ double apply_tsdf(TD* vd, TD* vw, int vid, bool isnew, double trunc,
-                                             double sw, double swd, double mind, double maxd) {
-    TD d_st = isnew ? (TD)trunc : vd[vid];
-    TD w_st = isnew ? (TD)0 : vw[vid];
-    double w_old = (double)w_st;
-    double d_old = (double)d_st;
+__device__ __forceinline__ double apply_tsdf(TD* vt, int vid, bool isnew, double trunc, double sw,
+                                             double swd, double mind, double maxd) {
+    using P2 = typename Pair<TD>::type;
+    P2* slot = reinterpret_cast<P2*>(vt) + vid;
+    P2 st;
+    if (isnew) {
+        st.x = (TD)trunc;
+        st.y = (TD)0;
+    } else {
+        st = *slot;
+    }
+    double w_old = (double)st.y;
+    double d_old = (double)st.x;
     double w_new = w_old + sw;
     double d_new = w_new > 0.0 ? (w_old * d_old + swd) / w_new : d_old;
-    bool cst = (mind == maxd) && (w_old == 0.0 || equals_stored<TD>(d_st, mind));
+    bool cst = (mind == maxd) && (w_old == 0.0 || equals_stored<TD>(st.x, mind));
     if (cst) d_new = mind;
-    vd[vid] = (TD)d_new;
-    vw[vid] = (TD)w_new;
+    P2 out;
+    out.x = (TD)d_new;
+    out.y = (TD)w_new;
+    *slot = out;
     return w_old;
 }
 
@@ -147,10 +164,8 @@ struct Center {
     double x, y, z;
 };
 
-__device__ __forceinline__ Center voxel_center(unsigned long long key, const KeyPack& kp, double h,
-                                               const PoseParams& pp) {
-    long long x, y, z;
-    unpack_key(key, kp, x, y, z);
+__device__ __forceinline__ Center center_of(long long x, long long y, long long z, double h,
+                                            const PoseParams& pp) {
     Center c;
     c.x = ((double)x + 0.5) * h - pp.t[0];
     c.y = ((double)y + 0.5) * h - pp.t[1];
@@ -168,7 +183,7 @@ __device__ __forceinline__ void clear_frame_slot(unsigned long long* fkey, unsig
 struct UpdateArgs {
     const int* ulist;
     const unsigned long long* ukey;
-    const int* gvid;
+    int* gvid;
     unsigned long long* fkey;
     unsigned* fcount;
     const unsigned* foff;
@@ -179,69 +194,172 @@ struct UpdateArgs {
     int* hugelist;
     unsigned* bitmap;     // kHugeWarps * bm_words
     long long bm_words;
-    KeyPack kp;
-    PoseParams pp;
+    Maps maps;
     double h, trunc;
     int wfn;
-    // closed
-    int sem_kind, last_wins, C;
-    const int32_t* labels;
-    // open
-    int D;
+    int sem_kind, last_wins, C;   // closed
+    int D;                        // open
     double lambda_floor, prior_beta;
     FrameCtr* ctr;
 };
 
-// ---- short segments: one thread per voxel -------------------------------------
+// ---- stage A, closed / geometry: one thread per voxel ------------------------
+
+// One row of a short segment: its point index and what the update needs of it.
+struct RowData {
+    double4 ray;
+    int rid;
+    int lab;
+};
 
 template <class TD, class TC>
-__global__ void __launch_bounds__(256) k_update_short(UpdateArgs a, TD* vd, TD* vw, TC* counts) {
-    if (frame_aborted(a.ctr)) return;
-    const long long U = (long long)a.ctr->n_groups;
+__global__ void __launch_bounds__(256) k_update_short(UpdateArgs a, TD* vt, TC* counts) {
+    FrameCtr* ctr = a.ctr;
+    if (ctr->abort) return;
+    const long long U = (long long)ctr->n_list;
+    const KeyPack kp = ctr->p.kp;
+    const PoseParams pp = ctr->p.pp;
+    const long long hmask = ctr->p.hmask;
+    const long long nblocks0 = ctr->p.nblocks0;
+    const int frame = ctr->p.frame;
+    const int32_t* __restrict__ labels = ctr->p.labels;
+    const bool closed = a.sem_kind == SVX_SEM_CLOSED;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < U;
          i += (long long)gridDim.x * blockDim.x) {
+        const unsigned long long key = a.ukey[i];
         const int s = a.ulist[i];
         const unsigned k = a.fcount[s];
+        const unsigned base = a.foff[s];
+        // Issue the row loads (point index -> ray, label) before the leaf
+        // resolution so the two dependent chains overlap.  Most LiDAR voxels
+        // have one or two rows; they stay in registers.
+        RowData r0, r1;
+        r0.rid = r1.rid = 0x7fffffff;
+        if (k <= (unsigned)kShortMax) {
+            r0.rid = a.srid[base];
+            if (k > 1) r1.rid = a.srid[base + 1];
+            r0.ray = a.ray[r0.rid];
+            if (closed) r0.lab = labels[r0.rid];
+            if (k > 1) {
+                r1.ray = a.ray[r1.rid];
+                if (closed) r1.lab = labels[r1.rid];
+            }
+        }
+        long long x, y, z;
+        unpack_key(key, kp, x, y, z);
+        const int g = resolve_voxel(a.maps, key, x, y, z, hmask, frame, nblocks0, ctr);
         if (k > (unsigned)kShortMax) {
-            if (k > (unsigned)kSmemMax) a.hugelist[warp_aggregate_add(&a.ctr->n_huge, 1ULL)] = (int)i;
-            else a.longlist[warp_aggregate_add(&a.ctr->n_long, 1ULL)] = (int)i;
+            a.gvid[i] = g;
+            if (k > (unsigned)kSmemMax) a.hugelist[warp_ticket(&ctr->n_huge)] = (int)i;
+            else a.longlist[warp_ticket(&ctr->n_long)] = (int)i;
             continue;
         }
-        const unsigned base = a.foff[s];
-        int r[kShortMax];
-        for (unsigned j = 0; j < k; ++j) {
-            int v = a.srid[base + j];
-            int p = (int)j;
-            while (p > 0 && r[p - 1] > v) {
-                r[p] = r[p - 1];
-                --p;
-            }
-            r[p] = v;
-        }
-        const Center c = voxel_center(a.ukey[i], a.kp, a.h, a.pp);
-        const int g = a.gvid[i];
+        const Center c = center_of(x, y, z, a.h, pp);
         const int vid = g & 0x7fffffff;
         const bool isnew = g < 0;
+        TC* crow = counts + (long long)vid * a.C;
         double sw = 0.0, swd = 0.0, mind = INFINITY, maxd = -INFINITY;
         int last_lab = 0;
-        TC* crow = counts + (long long)vid * a.C;
-        for (unsigned j = 0; j < k; ++j) {
-            const int rid = r[j];
+        auto fold = [&](const RowData& rd) {
             double d, w;
-            row_dw(c.x, c.y, c.z, a.ray[rid], a.trunc, a.wfn, d, w);
+            row_dw(c.x, c.y, c.z, rd.ray, a.trunc, a.wfn, d, w);
             sw += w;
             swd += w * d;
             mind = d < mind ? d : mind;
             maxd = d > maxd ? d : maxd;
-            if (a.sem_kind == SVX_SEM_CLOSED) {
-                const int lab = a.labels[rid];
-                if (a.last_wins) last_lab = lab;
-                else crow[lab - 1] += (TC)1;
+            if (closed) {
+                if (a.last_wins) last_lab = rd.lab;
+                else atomicAdd(&crow[rd.lab - 1], (TC)1);   // integer count: fire-and-forget
+            }
+        };
+        if (k <= 2) {
+            if (k == 2 && r1.rid < r0.rid) {
+                RowData t = r0;
+                r0 = r1;
+                r1 = t;
+            }
+            fold(r0);
+            if (k == 2) fold(r1);
+        } else {
+            int r[kShortMax];
+            for (unsigned j = 0; j < k; ++j) {
+                int v = a.srid[base + j];
+                int p = (int)j;
+                while (p > 0 && r[p - 1] > v) {
+                    r[p] = r[p - 1];
+                    --p;
+                }
+                r[p] = v;
+            }
+            for (unsigned j = 0; j < k; ++j) {
+                RowData rd;
+                rd.rid = r[j];
+                rd.ray = a.ray[rd.rid];
+                if (closed) rd.lab = labels[rd.rid];
+                fold(rd);
             }
         }
-        apply_tsdf<TD>(vd, vw, vid, isnew, a.trunc, sw, swd, mind, maxd);
-        if (a.sem_kind == SVX_SEM_CLOSED && a.last_wins) {
+        apply_tsdf<TD>(vt, vid, isnew, a.trunc, sw, swd, mind, maxd);
+        if (closed && a.last_wins) {
             for (int q = 0; q < a.C; ++q) crow[q] = (TC)(q == last_lab - 1 ? 1 : 0);
+        }
+        clear_frame_slot(a.fkey, a.fcount, a.fcur, s);
+    }
+}
+
+// ---- K3 fused with the update of single-row voxels (bounded, closed/geometry) ----
+// One thread per row slot, in point-major order: the row's voxel key, ray and
+// label are read coalesced.  A voxel with exactly one row needs no ordering:
+// its sums are the row's own (0.0 + w * d exactly as the reference's
+// sequential sum, _core.pyx:793-795), so it is resolved and updated right
+// here; rows of multi-row voxels are dropped into their segments.
+template <class TD, class TC>
+__global__ void __launch_bounds__(256) k_scatter_update(UpdateArgs a, const int* __restrict__ rcnt,
+                                                        const int* __restrict__ rowslot,
+                                                        const unsigned long long* __restrict__ rowkey,
+                                                        int* __restrict__ srid, TD* vt, TC* counts) {
+    FrameCtr* ctr = a.ctr;
+    if (ctr->abort) return;
+    const long long n = ctr->p.n;
+    const int maxrows = ctr->p.maxrows;
+    const KeyPack kp = ctr->p.kp;
+    const PoseParams pp = ctr->p.pp;
+    const long long hmask = ctr->p.hmask;
+    const long long nblocks0 = ctr->p.nblocks0;
+    const int frame = ctr->p.frame;
+    const int32_t* __restrict__ labels = ctr->p.labels;
+    const bool closed = a.sem_kind == SVX_SEM_CLOSED;
+    const long long total = n * maxrows;
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (long long)gridDim.x * blockDim.x) {
+        const long long i = t / maxrows;
+        const int j = (int)(t - i * maxrows);
+        if (j >= rcnt[i]) continue;
+        const int s = rowslot[t];
+        // speculative loads for the single-row case, overlapping the count read
+        const unsigned long long key = rowkey[t];
+        const double4 ry = a.ray[i];
+        const int lab = closed ? labels[i] : 0;
+        if (a.fcount[s] > 1u) {
+            const unsigned pos = a.foff[s] + atomicAdd(&a.fcur[s], 1u);
+            srid[pos] = (int)i;
+            continue;
+        }
+        long long x, y, z;
+        unpack_key(key, kp, x, y, z);
+        const int g = resolve_voxel(a.maps, key, x, y, z, hmask, frame, nblocks0, ctr);
+        const Center c = center_of(x, y, z, a.h, pp);
+        double d, w;
+        row_dw(c.x, c.y, c.z, ry, a.trunc, a.wfn, d, w);
+        const int vid = g & 0x7fffffff;
+        apply_tsdf<TD>(vt, vid, g < 0, a.trunc, 0.0 + w, 0.0 + w * d, d, d);
+        if (closed) {
+            TC* crow = counts + (long long)vid * a.C;
+            if (a.last_wins) {
+                for (int q = 0; q < a.C; ++q) crow[q] = (TC)(q == lab - 1 ? 1 : 0);
+            } else {
+                atomicAdd(&crow[lab - 1], (TC)1);
+            }
         }
         clear_frame_slot(a.fkey, a.fcount, a.fcur, s);
     }
@@ -250,10 +368,25 @@ __global__ void __launch_bounds__(256) k_update_short(UpdateArgs a, TD* vd, TD* 
 // ---- warp helpers ---------------------------------------------------------------
 
 // Sort one segment's point indices ascending into buf (k <= kSmemMax).
-__device__ __forceinline__ int warp_sort_segment(const int* __restrict__ srid, unsigned base, int k,
-                                                 int* buf) {
+__device__ __forceinline__ void warp_sort_segment(const int* __restrict__ srid, unsigned base, int k,
+                                                  int* buf) {
     const int lane = threadIdx.x & 31;
-    int P = 32;
+    if (k <= 32) {
+        // one element per lane: bitonic sort through shuffles
+        int v = lane < k ? srid[base + lane] : 0x7fffffff;
+        for (int kk = 2; kk <= 32; kk <<= 1) {
+            for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+                int o = __shfl_xor_sync(0xffffffffu, v, jj);
+                bool up = (lane & kk) == 0;
+                bool lower = (lane & jj) == 0;
+                v = (lower == up) ? min(v, o) : max(v, o);
+            }
+        }
+        buf[lane] = v;
+        __syncwarp();
+        return;
+    }
+    int P = 64;
     while (P < k) P <<= 1;
     for (int j = lane; j < P; j += 32) buf[j] = j < k ? srid[base + j] : 0x7fffffff;
     __syncwarp();
@@ -273,7 +406,6 @@ __device__ __forceinline__ int warp_sort_segment(const int* __restrict__ srid, u
             __syncwarp();
         }
     }
-    return k;
 }
 
 // Next ascending chunk (<= 1024 rows) of a huge segment from its point bitmap.
@@ -299,8 +431,7 @@ __device__ __forceinline__ int bitmap_chunk(const unsigned* bm, long long w0, lo
     return total;
 }
 
-// Build the point bitmap of a huge segment in this warp's scratch; returns
-// (minr, nwords).
+// Build the point bitmap of a huge segment in this warp's scratch.
 __device__ __forceinline__ void bitmap_build(const int* __restrict__ srid, unsigned base, unsigned k,
                                              unsigned* bm, int& minr, long long& nwords) {
     const int lane = threadIdx.x & 31;
@@ -335,9 +466,9 @@ struct TsdfAcc {
 // Fold an ordered chunk of rows into the TSDF sums (all lanes end with the
 // same sums); closed-set counts are integer increments (order-free).
 template <class TC>
-__device__ __forceinline__ void warp_tsdf_chunk(const UpdateArgs& a, const int* buf, int cnt,
-                                                const Center& c, TsdfAcc& acc, TC* crow,
-                                                bool count_labels) {
+__device__ __forceinline__ void warp_tsdf_chunk(const UpdateArgs& a, const int32_t* labels,
+                                                const int* buf, int cnt, const Center& c,
+                                                TsdfAcc& acc, TC* crow, bool count_labels) {
     const int lane = threadIdx.x & 31;
     for (int c0 = 0; c0 < cnt; c0 += 32) {
         const int j = c0 + lane;
@@ -347,7 +478,7 @@ __device__ __forceinline__ void warp_tsdf_chunk(const UpdateArgs& a, const int* 
             const int rid = buf[j];
             row_dw(c.x, c.y, c.z, a.ray[rid], a.trunc, a.wfn, d, w);
             if (count_labels) {
-                lab = a.labels[rid];
+                lab = labels[rid];
                 if (!a.last_wins) atomicAdd(&crow[lab - 1], (TC)1);
             }
         }
@@ -365,73 +496,72 @@ __device__ __forceinline__ void warp_tsdf_chunk(const UpdateArgs& a, const int* 
 }
 
 template <class TD, class TC>
-__device__ __forceinline__ void finish_closed(const UpdateArgs& a, TD* vd, TD* vw, TC* crow, int vid,
+__device__ __forceinline__ void finish_closed(const UpdateArgs& a, TD* vt, TC* crow, int vid,
                                               bool isnew, const TsdfAcc& acc) {
     const int lane = threadIdx.x & 31;
-    if (lane == 0) apply_tsdf<TD>(vd, vw, vid, isnew, a.trunc, acc.sw, acc.swd, acc.mind, acc.maxd);
+    if (lane == 0) apply_tsdf<TD>(vt,vid, isnew, a.trunc, acc.sw, acc.swd, acc.mind, acc.maxd);
     if (a.sem_kind == SVX_SEM_CLOSED && a.last_wins) {
         for (int q = lane; q < a.C; q += 32) crow[q] = (TC)(q == acc.last_lab - 1 ? 1 : 0);
     }
 }
 
-// ---- long segments (TSDF / closed): one warp per voxel ---------------------------
+// ---- stage B, closed / geometry: long and huge segments ---------------------------
 
 template <class TD, class TC>
-__global__ void __launch_bounds__(32 * kWarpsPerCta) k_update_long(UpdateArgs a, TD* vd, TD* vw,
+__global__ void __launch_bounds__(32 * kWarpsPerCta) k_update_long(UpdateArgs a, TD* vt,
                                                                    TC* counts) {
     __shared__ int sbuf[kWarpsPerCta][kSmemMax];
-    if (frame_aborted(a.ctr)) return;
+    FrameCtr* ctr = a.ctr;
+    if (ctr->abort) return;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     int* buf = sbuf[wib];
-    const long long L = (long long)a.ctr->n_long;
-    for (long long t = (long long)blockIdx.x * kWarpsPerCta + wib; t < L;
-         t += (long long)gridDim.x * kWarpsPerCta) {
+    const KeyPack kp = ctr->p.kp;
+    const PoseParams pp = ctr->p.pp;
+    const int32_t* labels = ctr->p.labels;
+    const long long gw = (long long)blockIdx.x * kWarpsPerCta + wib;
+    const long long nwarps = (long long)gridDim.x * kWarpsPerCta;
+    unsigned* bm = a.bitmap + (gw % kHugeWarps) * a.bm_words;
+    const long long L = (long long)ctr->n_long;
+    for (long long t = gw; t < L; t += nwarps) {
         const int i = a.longlist[t];
         const int s = a.ulist[i];
         const unsigned k = a.fcount[s];
         warp_sort_segment(a.srid, a.foff[s], (int)k, buf);
-        const Center c = voxel_center(a.ukey[i], a.kp, a.h, a.pp);
+        long long x, y, z;
+        unpack_key(a.ukey[i], kp, x, y, z);
+        const Center c = center_of(x, y, z, a.h, pp);
         const int g = a.gvid[i];
         const int vid = g & 0x7fffffff;
         TC* crow = counts + (long long)vid * a.C;
         TsdfAcc acc{0.0, 0.0, INFINITY, -INFINITY, 0};
-        warp_tsdf_chunk<TC>(a, buf, (int)k, c, acc, crow, a.sem_kind == SVX_SEM_CLOSED);
-        finish_closed<TD, TC>(a, vd, vw, crow, vid, g < 0, acc);
+        warp_tsdf_chunk<TC>(a, labels, buf, (int)k, c, acc, crow, a.sem_kind == SVX_SEM_CLOSED);
+        finish_closed<TD, TC>(a, vt,crow, vid, g < 0, acc);
         if (lane == 0) clear_frame_slot(a.fkey, a.fcount, a.fcur, s);
         __syncwarp();
     }
-}
-
-// ---- huge segments (TSDF / closed): bitmap-ordered streaming --------------------
-
-template <class TD, class TC>
-__global__ void __launch_bounds__(32 * kWarpsPerCta) k_update_huge(UpdateArgs a, TD* vd, TD* vw,
-                                                                   TC* counts) {
-    __shared__ int sbuf[kWarpsPerCta][kSmemMax];
-    if (frame_aborted(a.ctr)) return;
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    int* buf = sbuf[wib];
-    const long long gw = (long long)blockIdx.x * kWarpsPerCta + wib;
-    unsigned* bm = a.bitmap + gw * a.bm_words;
-    const long long Hn = (long long)a.ctr->n_huge;
-    for (long long t = gw; t < Hn; t += (long long)gridDim.x * kWarpsPerCta) {
+    // huge segments: only the first kHugeWarps warps own bitmap scratch
+    if (gw >= kHugeWarps) return;
+    const long long Hn = (long long)ctr->n_huge;
+    for (long long t = gw; t < Hn; t += kHugeWarps) {
         const int i = a.hugelist[t];
         const int s = a.ulist[i];
         const unsigned k = a.fcount[s];
         int minr;
         long long nwords;
         bitmap_build(a.srid, a.foff[s], k, bm, minr, nwords);
-        const Center c = voxel_center(a.ukey[i], a.kp, a.h, a.pp);
+        long long x, y, z;
+        unpack_key(a.ukey[i], kp, x, y, z);
+        const Center c = center_of(x, y, z, a.h, pp);
         const int g = a.gvid[i];
         const int vid = g & 0x7fffffff;
         TC* crow = counts + (long long)vid * a.C;
         TsdfAcc acc{0.0, 0.0, INFINITY, -INFINITY, 0};
         for (long long w0 = 0; w0 < nwords; w0 += 32) {
             const int cnt = bitmap_chunk(bm, w0, nwords, minr, buf);
-            if (cnt) warp_tsdf_chunk<TC>(a, buf, cnt, c, acc, crow, a.sem_kind == SVX_SEM_CLOSED);
+            if (cnt) warp_tsdf_chunk<TC>(a, labels, buf, cnt, c, acc, crow, a.sem_kind == SVX_SEM_CLOSED);
             __syncwarp();
         }
-        finish_closed<TD, TC>(a, vd, vw, crow, vid, g < 0, acc);
+        finish_closed<TD, TC>(a, vt,crow, vid, g < 0, acc);
         if (lane == 0) clear_frame_slot(a.fkey, a.fcount, a.fcur, s);
         __syncwarp();
     }
@@ -459,8 +589,8 @@ __device__ __forceinline__ void nig_apply(TS* mrow, TS* brow, int c, bool isnew,
     brow[c] = (TS)b_new;
 }
 
-// Per-dimension sequential sums over an ordered chunk (every lane owns
-// dims base + lane + 32 q).
+// Per-dimension sequential sums over an ordered chunk (lane owns dims
+// base + lane + 32 q).
 template <class Fe>
 __device__ __forceinline__ void open_chunk(const Fe* __restrict__ feats, int D, int base,
                                            const int* buf, int cnt, double* sz, double* sz2) {
@@ -480,12 +610,14 @@ __device__ __forceinline__ void open_chunk(const Fe* __restrict__ feats, int D, 
 }
 
 template <class TD, class TS, class Fe>
-__device__ __forceinline__ void open_voxel(const UpdateArgs& a, TD* vd, TD* vw, TS* mean, TS* beta,
-                                           const Fe* feats, int i, int s, unsigned k, int* buf,
-                                           unsigned* bm, bool huge) {
+__device__ __forceinline__ void open_voxel(const UpdateArgs& a, const KeyPack& kp,
+                                           const PoseParams& pp, TD* vt, TS* mean,
+                                           TS* beta, const Fe* feats, int i, int s, unsigned k,
+                                           int g, int* buf, unsigned* bm, bool huge) {
     const int lane = threadIdx.x & 31;
-    const Center c = voxel_center(a.ukey[i], a.kp, a.h, a.pp);
-    const int g = a.gvid[i];
+    long long x, y, z;
+    unpack_key(a.ukey[i], kp, x, y, z);
+    const Center c = center_of(x, y, z, a.h, pp);
     const int vid = g & 0x7fffffff;
     const bool isnew = g < 0;
     int minr = 0;
@@ -497,14 +629,14 @@ __device__ __forceinline__ void open_voxel(const UpdateArgs& a, TD* vd, TD* vw, 
     if (huge) {
         for (long long w0 = 0; w0 < nwords; w0 += 32) {
             const int cnt = bitmap_chunk(bm, w0, nwords, minr, buf);
-            if (cnt) warp_tsdf_chunk<float>(a, buf, cnt, c, acc, nullptr, false);
+            if (cnt) warp_tsdf_chunk<float>(a, nullptr, buf, cnt, c, acc, nullptr, false);
             __syncwarp();
         }
     } else {
-        warp_tsdf_chunk<float>(a, buf, (int)k, c, acc, nullptr, false);
+        warp_tsdf_chunk<float>(a, nullptr, buf, (int)k, c, acc, nullptr, false);
     }
     double w_old = 0.0;
-    if (lane == 0) w_old = apply_tsdf<TD>(vd, vw, vid, isnew, a.trunc, acc.sw, acc.swd, acc.mind, acc.maxd);
+    if (lane == 0) w_old = apply_tsdf<TD>(vt,vid, isnew, a.trunc, acc.sw, acc.swd, acc.mind, acc.maxd);
     w_old = __shfl_sync(0xffffffffu, w_old, 0);
     // NIG batch update with lambda from the pre-frame weight
     const double nobs = (double)k;
@@ -538,40 +670,63 @@ __device__ __forceinline__ void open_voxel(const UpdateArgs& a, TD* vd, TD* vw, 
     __syncwarp();
 }
 
+// stage A, open set: resolve + update every non-huge voxel
 template <class TD, class TS, class Fe>
-__global__ void __launch_bounds__(32 * kWarpsPerCta) k_update_open(UpdateArgs a, TD* vd, TD* vw,
-                                                                   TS* mean, TS* beta,
-                                                                   const Fe* __restrict__ feats) {
+__global__ void __launch_bounds__(32 * kWarpsPerCta) k_update_open(UpdateArgs a, TD* vt,
+                                                                   TS* mean, TS* beta) {
     __shared__ int sbuf[kWarpsPerCta][kSmemMax];
-    if (frame_aborted(a.ctr)) return;
+    FrameCtr* ctr = a.ctr;
+    if (ctr->abort) return;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const long long U = (long long)a.ctr->n_groups;
+    const long long U = (long long)ctr->n_list;
+    const KeyPack kp = ctr->p.kp;
+    const PoseParams pp = ctr->p.pp;
+    const long long hmask = ctr->p.hmask;
+    const int frame = ctr->p.frame;
+    const Fe* feats = (const Fe*)ctr->p.feats;
     for (long long i = (long long)blockIdx.x * kWarpsPerCta + wib; i < U;
          i += (long long)gridDim.x * kWarpsPerCta) {
         const int s = a.ulist[i];
         const unsigned k = a.fcount[s];
+        int g = 0;
+        if (lane == 0) {
+            const unsigned long long key = a.ukey[i];
+            long long x, y, z;
+            unpack_key(key, kp, x, y, z);
+            g = resolve_voxel(a.maps, key, x, y, z, hmask, frame, ctr->p.nblocks0, ctr);
+        }
+        g = __shfl_sync(0xffffffffu, g, 0);
         if (k > (unsigned)kSmemMax) {
-            if (lane == 0) a.hugelist[atomicAdd(&a.ctr->n_huge, 1ULL)] = (int)i;
+            if (lane == 0) {
+                a.gvid[i] = g;
+                a.hugelist[atomicAdd(&ctr->n_huge, 1ULL)] = (int)i;
+            }
             continue;
         }
-        open_voxel<TD, TS, Fe>(a, vd, vw, mean, beta, feats, (int)i, s, k, sbuf[wib], nullptr, false);
+        open_voxel<TD, TS, Fe>(a, kp, pp, vt,mean, beta, feats, (int)i, s, k, g, sbuf[wib],
+                               nullptr, false);
     }
 }
 
+// stage B, open set: huge segments
 template <class TD, class TS, class Fe>
-__global__ void __launch_bounds__(32 * kWarpsPerCta) k_update_open_huge(UpdateArgs a, TD* vd, TD* vw,
-                                                                        TS* mean, TS* beta,
-                                                                        const Fe* __restrict__ feats) {
+__global__ void __launch_bounds__(32 * kWarpsPerCta) k_update_open_huge(UpdateArgs a, TD* vt,
+                                                                        TS* mean, TS* beta) {
     __shared__ int sbuf[kWarpsPerCta][kSmemMax];
-    if (frame_aborted(a.ctr)) return;
+    FrameCtr* ctr = a.ctr;
+    if (ctr->abort) return;
     const int wib = threadIdx.x >> 5;
     const long long gw = (long long)blockIdx.x * kWarpsPerCta + wib;
     unsigned* bm = a.bitmap + gw * a.bm_words;
-    const long long Hn = (long long)a.ctr->n_huge;
+    const long long Hn = (long long)ctr->n_huge;
+    const KeyPack kp = ctr->p.kp;
+    const PoseParams pp = ctr->p.pp;
+    const Fe* feats = (const Fe*)ctr->p.feats;
     for (long long t = gw; t < Hn; t += (long long)gridDim.x * kWarpsPerCta) {
         const int i = a.hugelist[t];
         const int s = a.ulist[i];
-        open_voxel<TD, TS, Fe>(a, vd, vw, mean, beta, feats, i, s, a.fcount[s], sbuf[wib], bm, true);
+        open_voxel<TD, TS, Fe>(a, kp, pp, vt,mean, beta, feats, i, s, a.fcount[s], a.gvid[i],
+                               sbuf[wib], bm, true);
     }
 }
 
@@ -591,8 +746,7 @@ __global__ void k_rehash(int64_t nblocks, const int4* __restrict__ bcoord, int4*
     }
 }
 
-UpdateArgs make_args(svx_map* m, const KeyPack& kp, const PoseParams& pp, const int32_t* labels,
-                     int64_t n) {
+UpdateArgs make_args(svx_map* m) {
     UpdateArgs a;
     a.ulist = ptr<int>(m->ulist);
     a.ukey = ptr<unsigned long long>(m->ukey);
@@ -606,16 +760,18 @@ UpdateArgs make_args(svx_map* m, const KeyPack& kp, const PoseParams& pp, const 
     a.longlist = ptr<int>(m->longlist);
     a.hugelist = ptr<int>(m->longlist) + m->ucap;
     a.bitmap = ptr<unsigned>(m->bitmap);
-    a.bm_words = (n + 31) / 32 + 1;
-    a.kp = kp;
-    a.pp = pp;
+    a.bm_words = (m->npts_cap + 31) / 32 + 1;
+    a.maps.table = ptr<int4>(m->hash);
+    a.maps.bcoord = ptr<int4>(m->bcoord);
+    a.maps.bkey = ptr<unsigned long long>(m->bkey);
+    a.maps.bmask = ptr<unsigned long long>(m->bmask);
+    a.maps.bslot = ptr<int>(m->bslot);
     a.h = m->cfg.voxel_size;
     a.trunc = m->cfg.truncation;
     a.wfn = m->cfg.weight_fn;
     a.sem_kind = m->cfg.sem_kind;
     a.last_wins = m->cfg.last_wins;
     a.C = m->payload_d > 0 ? m->payload_d : 1;
-    a.labels = labels;
     a.D = m->payload_d;
     a.lambda_floor = m->cfg.lambda_floor;
     a.prior_beta = m->cfg.prior_beta;
@@ -625,70 +781,79 @@ UpdateArgs make_args(svx_map* m, const KeyPack& kp, const PoseParams& pp, const 
 
 constexpr int kShortBlocks = 148 * 8;
 constexpr int kLongBlocks = 148 * 4;
-constexpr int kHugeBlocks = kHugeWarps / kWarpsPerCta;
 
 template <class TD, class TC>
-svx_status update_closed_t(svx_map* m, const UpdateArgs& a, cudaStream_t s) {
-    TD* vd = ptr<TD>(m->vd);
-    TD* vw = ptr<TD>(m->vw);
-    TC* cnt = ptr<TC>(m->s0);
-    k_update_short<TD, TC><<<kShortBlocks, 256, 0, s>>>(a, vd, vw, cnt);
+svx_status closed_a(svx_map* m, cudaStream_t s) {
+    k_update_short<TD, TC><<<kShortBlocks, 256, 0, s>>>(make_args(m), ptr<TD>(m->vt),
+                                                        ptr<TC>(m->s0));
     SVX_LAUNCHED();
-    k_update_long<TD, TC><<<kLongBlocks, 32 * kWarpsPerCta, 0, s>>>(a, vd, vw, cnt);
-    SVX_LAUNCHED();
-    k_update_huge<TD, TC><<<kHugeBlocks, 32 * kWarpsPerCta, 0, s>>>(a, vd, vw, cnt);
+    return SVX_OK;
+}
+
+template <class TD, class TC>
+svx_status closed_b(svx_map* m, cudaStream_t s) {
+    k_update_long<TD, TC><<<kLongBlocks, 32 * kWarpsPerCta, 0, s>>>(make_args(m), ptr<TD>(m->vt),
+                                                                    ptr<TC>(m->s0));
     SVX_LAUNCHED();
     return SVX_OK;
 }
 
 template <class TD, class TS, class Fe>
-svx_status update_open_t(svx_map* m, const UpdateArgs& a, const Fe* feats, cudaStream_t s) {
-    TD* vd = ptr<TD>(m->vd);
-    TD* vw = ptr<TD>(m->vw);
+svx_status open_a(svx_map* m, cudaStream_t s) {
     k_update_open<TD, TS, Fe><<<kLongBlocks, 32 * kWarpsPerCta, 0, s>>>(
-        a, vd, vw, ptr<TS>(m->s0), ptr<TS>(m->s1), feats);
+        make_args(m), ptr<TD>(m->vt), ptr<TS>(m->s0), ptr<TS>(m->s1));
     SVX_LAUNCHED();
-    k_update_open_huge<TD, TS, Fe><<<kHugeBlocks, 32 * kWarpsPerCta, 0, s>>>(
-        a, vd, vw, ptr<TS>(m->s0), ptr<TS>(m->s1), feats);
+    return SVX_OK;
+}
+
+template <class TD, class TS, class Fe>
+svx_status open_b(svx_map* m, cudaStream_t s) {
+    k_update_open_huge<TD, TS, Fe><<<kHugeWarps / kWarpsPerCta, 32 * kWarpsPerCta, 0, s>>>(
+        make_args(m), ptr<TD>(m->vt), ptr<TS>(m->s0), ptr<TS>(m->s1));
     SVX_LAUNCHED();
     return SVX_OK;
 }
 
 template <class TD>
-svx_status update_td(svx_map* m, const UpdateArgs& a, const void* feats, int feats_f64,
-                     cudaStream_t s) {
+svx_status stage_td(svx_map* m, int feats_f64, bool b, cudaStream_t s) {
     if (m->cfg.sem_kind == SVX_SEM_OPEN) {
         const bool s64 = m->cfg.state_dtype == SVX_F64;
         if (s64) {
-            if (feats_f64) return update_open_t<TD, double, double>(m, a, (const double*)feats, s);
-            return update_open_t<TD, double, float>(m, a, (const float*)feats, s);
+            if (feats_f64) return b ? open_b<TD, double, double>(m, s) : open_a<TD, double, double>(m, s);
+            return b ? open_b<TD, double, float>(m, s) : open_a<TD, double, float>(m, s);
         }
-        if (feats_f64) return update_open_t<TD, float, double>(m, a, (const double*)feats, s);
-        return update_open_t<TD, float, float>(m, a, (const float*)feats, s);
+        if (feats_f64) return b ? open_b<TD, float, double>(m, s) : open_a<TD, float, double>(m, s);
+        return b ? open_b<TD, float, float>(m, s) : open_a<TD, float, float>(m, s);
     }
-    if (m->cfg.count_dtype == SVX_F64) return update_closed_t<TD, double>(m, a, s);
-    return update_closed_t<TD, float>(m, a, s);
+    if (m->cfg.count_dtype == SVX_F64) return b ? closed_b<TD, double>(m, s) : closed_a<TD, double>(m, s);
+    return b ? closed_b<TD, float>(m, s) : closed_a<TD, float>(m, s);
 }
 
 }  // namespace
 
-svx_status launch_voxels(svx_map* m, const KeyPack& kp, const FrameCaps& fc, cudaStream_t s) {
-    k_voxels<<<kPersistentBlocks, 256, 0, s>>>(
-        ptr<int>(m->ulist), ptr<unsigned long long>(m->ukey), kp, ptr<int4>(m->hash), m->hcap - 1,
-        fc.frame, ptr<int4>(m->bcoord), ptr<unsigned long long>(m->bkey),
-        ptr<unsigned long long>(m->bmask), ptr<int>(m->bslot), ptr<int>(m->gvid),
-        ptr<FrameCtr>(m->ctr));
+template <class TD, class TC>
+static svx_status scatter_update_t(svx_map* m, cudaStream_t s) {
+    k_scatter_update<TD, TC><<<kPersistentBlocks * 2, 256, 0, s>>>(
+        make_args(m), ptr<int>(m->rcnt), ptr<int>(m->rowslot), ptr<unsigned long long>(m->rowkey),
+        ptr<int>(m->srid), ptr<TD>(m->vt), ptr<TC>(m->s0));
     SVX_LAUNCHED();
     return SVX_OK;
 }
 
-svx_status launch_update(svx_map* m, const KeyPack& kp, const PoseParams& pp, const FrameCaps& fc,
-                         const int32_t* labels, const void* feats, int feats_f64, int64_t n,
-                         cudaStream_t s) {
-    (void)fc;
-    UpdateArgs a = make_args(m, kp, pp, labels, n);
-    if (m->cfg.tsdf_dtype == SVX_F64) return update_td<double>(m, a, feats, feats_f64, s);
-    return update_td<float>(m, a, feats, feats_f64, s);
+svx_status launch_scatter_update(svx_map* m, cudaStream_t s) {
+    const bool t64 = m->cfg.tsdf_dtype == SVX_F64, c64 = m->cfg.count_dtype == SVX_F64;
+    if (t64) return c64 ? scatter_update_t<double, double>(m, s) : scatter_update_t<double, float>(m, s);
+    return c64 ? scatter_update_t<float, double>(m, s) : scatter_update_t<float, float>(m, s);
+}
+
+svx_status launch_update_a(svx_map* m, int feats_f64, cudaStream_t s) {
+    if (m->cfg.tsdf_dtype == SVX_F64) return stage_td<double>(m, feats_f64, false, s);
+    return stage_td<float>(m, feats_f64, false, s);
+}
+
+svx_status launch_update_b(svx_map* m, int feats_f64, cudaStream_t s) {
+    if (m->cfg.tsdf_dtype == SVX_F64) return stage_td<double>(m, feats_f64, true, s);
+    return stage_td<float>(m, feats_f64, true, s);
 }
 
 svx_status launch_rehash(svx_map* m, int4* new_table, int64_t new_cap, cudaStream_t s) {

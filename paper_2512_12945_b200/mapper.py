@@ -15,6 +15,7 @@ from __future__ import annotations
 import ctypes
 import dataclasses
 import hashlib
+import math
 import struct
 from dataclasses import dataclass
 
@@ -111,9 +112,25 @@ def validate_rotation(R, context: str = "pose"):
 
 
 def _check_pose(pose, frame_id):
+    """Frame pose checks of fusion.py:68-77.  The common case (finite, exact
+    bottom row, rotation within 1e-4 of orthonormal) is decided with scalar
+    arithmetic; anything else takes the numpy path of validate_rotation."""
     pose = np.asarray(pose, np.float64)
     if pose.shape != (4, 4):
         raise UserInputError(f"pose must be 4x4, got {pose.shape}")
+    f = pose.ravel().tolist()
+    if all(math.isfinite(v) for v in f) and f[12:16] == [0.0, 0.0, 0.0, 1.0]:
+        r0, r1, r2 = f[0:3], f[4:7], f[8:11]
+        rows = (r0, r1, r2)
+        err = 0.0
+        for a in range(3):
+            for b in range(3):
+                dot = rows[a][0] * rows[b][0] + rows[a][1] * rows[b][1] + rows[a][2] * rows[b][2]
+                err = max(err, abs(dot - (1.0 if a == b else 0.0)))
+        det = (r0[0] * (r1[1] * r2[2] - r1[2] * r2[1]) - r0[1] * (r1[0] * r2[2] - r1[2] * r2[0])
+               + r0[2] * (r1[0] * r2[1] - r1[1] * r2[0]))
+        if err <= _ROT_PASS * 0.5 and det > 0.0:
+            return np.array(pose, np.float64, copy=True, order="C")
     if not np.isfinite(pose).all():
         raise UserInputError("pose contains non-finite values")
     if not np.allclose(pose[3], (0, 0, 0, 1), atol=1e-9):
@@ -333,7 +350,8 @@ class Mapper:
         rep = _lib.SvxReport()
         stream = _stream_for([pts, lab, feat])
         n = int(pts.shape[0])
-        arr = (ctypes.c_double * len(vec))(*[float(v) for v in vec])
+        vec = np.ascontiguousarray(vec, np.float64)
+        arr = vec.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
         check(fn(self._handle, pts.ptr, pts.code, n, arr,
                  lab.ptr if lab is not None else None,
                  feat.ptr if feat is not None else None,
