@@ -153,15 +153,14 @@ def stage_bytes(stage, rep, kind, C, D, tsdf_elem):
     P = 4 if kind == "closed" else (4 * D if kind == "open" else 0)
     S = 2 * tsdf_elem + (4 * C if kind == "closed" else (8 * D if kind == "open" else 0))
     return {
-        # read points (+labels/features), write the ray table and row slots, one
-        # 8-byte key CAS + one 4-byte count per row into the frame table
-        "march": n * (12 + P) + used * 32 + R * (4 + 8 + 4),
-        # read the frame table (key + count per slot), write list + segment offsets
-        "compact": U * (8 + 4 + 4 + 4 + 8),
-        # read row slots, segment offset and cursor per row, write the point index
-        "scatter": R * (4 + 4 + 4 + 4),
-        # leaf lookup + voxel activation, read rows/rays/labels, read+write state
-        "update": 2 * U * S + R * (4 + 32 + (4 if kind == "closed" else 0)) + U * 40,
+        # read points (+labels/features), write the ray table and one 8-byte key per row
+        "march": n * (12 + P) + used * 32 + R * 8,
+        # per row: key in, voxel id out, one count; per voxel: leaf lookup, slot, key
+        "resolve": R * (8 + 4 + 4) + U * (16 + 4 + 8 + 4),
+        # per row: voxel id + count in; single-row voxels also ray + label + state
+        "scatter": R * (4 + 4 + 4) + U * (32 + 2 * S),
+        # multi-row voxels: rows, rays, labels and state (upper bound: all voxels)
+        "update": 2 * U * S + R * (4 + 32 + (4 if kind == "closed" else 0)),
         "update_b": 0,
     }[stage]
 

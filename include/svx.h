@@ -183,12 +183,11 @@ svx_status svx_label_map(svx_map* map, int32_t mode, int64_t capacity, int32_t* 
 /* ---- diagnostics --------------------------------------------------------- */
 /* Per-stage device timing of integrate calls (CUDA events on the caller's
  * stream around each stage).  Stages, in order:
- *   0 march (K1: masks + band walk + voxel grouping counts)
- *   1 compact (K2: touched-voxel list + row segments + gate)
- *   2 scatter (K3: rows into voxel segments)
- *   3 update (K4 leaf find-or-insert + voxel activation fused with the K5/K6
- *      TSDF + semantic update of short segments / open-set voxels)
- *   4 update_b (K5/K6 for long and huge segments)
+ *   0 march (K1: masks + fp64 band walk -> row keys; gate)
+ *   1 resolve (K2: rows -> leaf/voxel ids, per-voxel counts; K3 row segments)
+ *   2 scatter (K4: rows into segments; single-row voxels updated in ray order)
+ *   3 update (K5: TSDF + semantic update of short segments / open-set voxels)
+ *   4 update_b (K5 for long and huge segments)
  * With profiling off, a frame is replayed as one captured CUDA graph.
  * svx_stage_times writes up to n last-frame stage times in ms and returns the
  * number of stages (SVX_N_STAGES). */

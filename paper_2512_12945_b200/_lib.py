@@ -93,7 +93,7 @@ _SIGNATURES = {
     "svx_reserve": [_P, _I64, _I64],
 }
 
-STAGES = ("march", "compact", "scatter", "update", "update_b")
+STAGES = ("march", "resolve", "scatter", "update", "update_b")
 
 # every symbol include/svx.h declares (checked by tests/test_abi_and_config.py)
 EXPORTED = sorted(list(_SIGNATURES) + ["svx_last_error", "svx_abi_version",

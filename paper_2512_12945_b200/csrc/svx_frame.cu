@@ -1,18 +1,19 @@
 // svx_frame.cu -- per-frame orchestration of the integration path.
 //
-// A frame is five kernels plus two small copies, all reading their per-frame
-// values from the device-side FrameCtr (svx_internal.cuh):
+// A frame is a short kernel chain plus two small copies, all reading their
+// per-frame values from the device-side FrameCtr (svx_internal.cuh):
 //   H2D   frame parameters + zeroed counters (one pinned copy)
-//   K1    march    masks, ray setup, fp64 band walk, frame-table insert + counts
-//   K2    compact  touched voxels -> list + row segments; device-side gate
-//   K3    scatter  row point indices into their voxel segments
-//   K4/5a update   leaf + voxel resolution fused with short-segment / open updates
-//   K5b   update   long / huge segments
+//   K1    march     masks, ray setup, fp64 band walk -> row keys     (svx_march.cu)
+//         gate      the reference's pre-allocation checks            (svx_march.cu)
+//   K2    resolve   rows -> leaf/voxel ids, per-voxel row counts     (svx_resolve.cu)
+//   K3    segments  multi-row voxels -> row segments                 (svx_resolve.cu)
+//   K4    scatter   rows -> segments; single-row voxels updated      (svx_update.cu)
+//   K5    update    fused TSDF + closed/open update per voxel        (svx_update.cu)
 //   D2H   counters (one pinned copy)
-// The sequence is captured once into a CUDA graph and replayed while buffer
+// The chain is captured once into a CUDA graph and replayed while buffer
 // addresses stay the same; the host synchronises once per frame to read the
-// report.  A frame whose scratch turned out too small (or whose keys need a
-// different base) is stopped by the gate before any map mutation and re-run.
+// report.  Error checks stop a frame before any map mutation; a frame whose
+// pools or row slots turned out too small is cleaned up and re-run.
 #include <cuda_runtime.h>
 #include <limits.h>
 #include <math.h>
@@ -58,8 +59,8 @@ size_t sem_elem(const svx_map* m) {
     return 0;
 }
 
-// Voxel-pool capacity: grow by doubling, zero-filled (closed counts and open
-// means have a zero background; voxel ids are never recycled).
+// Voxel-pool capacity: grow by doubling.  Closed counts and open means are
+// zero-filled (their background); the per-voxel frame counts start at zero.
 svx_status reserve_voxels(svx_map* m, int64_t need, cudaStream_t s) {
     if (need <= m->vcap) return SVX_OK;
     int64_t cap = std::max<int64_t>(need, 2 * m->vcap);
@@ -69,6 +70,10 @@ svx_status reserve_voxels(svx_map* m, int64_t need, cudaStream_t s) {
         SVX_TRY(ensure(m->s0, se * (size_t)m->payload_d * cap, s, true, 0));
     if (m->cfg.sem_kind == SVX_SEM_OPEN)
         SVX_TRY(ensure(m->s1, se * (size_t)m->payload_d * cap, s, true, 0));
+    SVX_TRY(ensure(m->vcnt, 4 * cap, s, true, 0));
+    SVX_TRY(ensure(m->vcur, 4 * cap, s, true, 0));
+    SVX_TRY(ensure(m->vseg, 4 * cap, s, true));
+    SVX_TRY(ensure(m->vkey, 8 * cap, s, true));
     m->vcap = cap;
     return SVX_OK;
 }
@@ -82,9 +87,9 @@ svx_status reserve_blocks(svx_map* m, int64_t need, cudaStream_t s) {
         SVX_TRY(ensure(m->bslot, sizeof(int) * kLeafVolume * cap, s, true, 0xFF));
         m->bcap = cap;
     }
-    // keep the leaf hash at <= 50% load for the worst case of this frame
+    // keep the leaf hash at <= 50% load when the pool is full
     int64_t want = 1024;
-    while (want < 2 * need) want <<= 1;
+    while (want < 2 * m->bcap) want <<= 1;
     if (want > m->hcap) {
         DevBuf nt;
         SVX_TRY(ensure(nt, sizeof(int4) * want, s, false, 0xFF));
@@ -97,64 +102,48 @@ svx_status reserve_blocks(svx_map* m, int64_t need, cudaStream_t s) {
     return SVX_OK;
 }
 
-// Per-frame scratch for ucap unique voxels / rcap rows / n points.
+// Per-frame scratch: per-ray arrays for npts_cap points, row arrays for the
+// row space (slot mode: npts_cap * maxrows, dense: rcap), lists for ucap.
 static svx_status reserve_frame(svx_map* m, int64_t n, cudaStream_t s) {
-    // frame table at <= 2/3 load for ucap keys
-    int64_t want = 1024;
-    while (2 * want < 3 * (int64_t)m->ucap) want <<= 1;
-    if (want > m->fcap || 2 * want <= m->fcap) {
-        release(m->fkey);
-        release(m->fcount);
-        release(m->fcur);
-        release(m->foff);
-        SVX_TRY(ensure(m->fkey, 8 * want, s, false, 0xFF));
-        SVX_TRY(ensure(m->fcount, 4 * want, s, false, 0));
-        SVX_TRY(ensure(m->fcur, 4 * want, s, false, 0));
-        SVX_TRY(ensure(m->foff, 4 * want, s));
-        m->fcap = want;
-    }
     m->npts_cap = std::max<int64_t>(m->npts_cap, n);
-    SVX_TRY(ensure(m->ulist, 4 * m->ucap, s));
-    SVX_TRY(ensure(m->ukey, 8 * m->ucap, s));
-    SVX_TRY(ensure(m->gvid, 4 * m->ucap, s));
-    SVX_TRY(ensure(m->longlist, 8 * m->ucap, s));   // long list, then huge list
-    SVX_TRY(ensure(m->srid, 4 * m->rcap, s));
-    SVX_TRY(ensure(m->bitmap, (size_t)4 * huge_warps() * ((m->npts_cap + 31) / 32 + 1), s));
+    const int64_t rows = (int64_t)m->rcap;
+    m->ucap = (uint64_t)rows;
     SVX_TRY(ensure(m->ray, sizeof(double4) * m->npts_cap, s));
     SVX_TRY(ensure(m->rcnt, sizeof(int) * m->npts_cap, s));
-    SVX_TRY(ensure(m->partials, partials_bytes(), s));
-    if (m->maxrows > 0) {
-        SVX_TRY(ensure(m->rowslot, sizeof(int) * m->npts_cap * m->maxrows, s));
-        SVX_TRY(ensure(m->rowkey, sizeof(unsigned long long) * m->npts_cap * m->maxrows, s));
+    SVX_TRY(ensure(m->partials, partials_bytes() + segment_partials_bytes(), s));
+    SVX_TRY(ensure(m->rowkey, sizeof(unsigned long long) * rows, s));
+    SVX_TRY(ensure(m->rowvid, sizeof(int) * rows, s));
+    SVX_TRY(ensure(m->tlist, sizeof(int) * rows, s));
+    SVX_TRY(ensure(m->mlist, sizeof(int) * rows, s));
+    SVX_TRY(ensure(m->longlist, 2 * sizeof(int) * rows, s));   // long list, then huge list
+    SVX_TRY(ensure(m->srid, sizeof(int) * rows, s));
+    SVX_TRY(ensure(m->bitmap, (size_t)4 * huge_warps() * ((m->npts_cap + 31) / 32 + 1), s));
+    SVX_TRY(ensure(m->rowray, sizeof(int) * rows, s));
+    if (m->maxrows == 0) {   // two-pass walk: per-ray offsets from a scan
+        SVX_TRY(ensure(m->roff, sizeof(long long) * m->npts_cap, s));
+        SVX_TRY(ensure(m->cubtmp, scan_temp_bytes(m->npts_cap), s));
     }
     return SVX_OK;
 }
 
-static svx_status clear_frame_table(svx_map* m, cudaStream_t s) {
-    SVX_CUDA(cudaMemsetAsync(m->fkey.p, 0xFF, 8 * m->fcap, s));
-    SVX_CUDA(cudaMemsetAsync(m->fcount.p, 0, 4 * m->fcap, s));
-    SVX_CUDA(cudaMemsetAsync(m->fcur.p, 0, 4 * m->fcap, s));
-    return SVX_OK;
-}
-
-// Everything a captured graph bakes in: buffer addresses, grid-determining
-// capacities and kernel template choices.
+// Everything a captured graph bakes in: buffer addresses, capacities that
+// size grids or index scratch, and kernel template choices.
 static unsigned long long graph_signature(const svx_map* m, int pts_f64, int feats_f64) {
-    const void* ptrs[] = {m->ray.p,    m->rcnt.p,  m->rowslot.p, m->rowkey.p, m->partials.p,
-                          m->fkey.p,   m->fcount.p, m->foff.p,   m->fcur.p,  m->ulist.p,
-                          m->ukey.p,   m->gvid.p,  m->longlist.p, m->srid.p, m->bitmap.p,
-                          m->hash.p,   m->bcoord.p, m->bkey.p,   m->bmask.p, m->bslot.p,
-                          m->vt.p,     m->s0.p,    m->s1.p,      m->ctr.p};
+    const void* ptrs[] = {m->ray.p,    m->rcnt.p,   m->roff.p,    m->rowkey.p, m->rowvid.p,
+                          m->rowray.p, m->partials.p, m->tlist.p, m->mlist.p,  m->longlist.p,
+                          m->srid.p,   m->bitmap.p, m->cubtmp.p,  m->hash.p,   m->bcoord.p,
+                          m->bkey.p,   m->bmask.p,  m->bslot.p,   m->vt.p,     m->s0.p,
+                          m->s1.p,     m->vcnt.p,   m->vseg.p,    m->vcur.p,   m->vkey.p,
+                          m->ctr.p};
     unsigned long long h = 1469598103934665603ULL;
     auto mix = [&](unsigned long long v) {
         h ^= v;
         h *= 1099511628211ULL;
     };
     for (const void* p : ptrs) mix((unsigned long long)(uintptr_t)p);
-    mix((unsigned long long)m->fcap);
     mix(m->ucap);
     mix((unsigned long long)m->npts_cap);
-    mix((unsigned long long)(m->maxrows > 0));
+    mix((unsigned long long)m->maxrows);
     mix((unsigned long long)(pts_f64 * 2 + feats_f64));
     return h;
 }
@@ -172,11 +161,11 @@ static svx_status enqueue_frame(svx_map* m, int pts_f64, int feats_f64, cudaStre
     SVX_TRY(launch_march(m, pts_f64, feats_f64, s));
     STAGE_END(0);
     STAGE_BEGIN(1);
-    SVX_TRY(launch_compact(m, s));
+    SVX_TRY(launch_resolve(m, s));
+    SVX_TRY(launch_segments(m, s));
     STAGE_END(1);
     STAGE_BEGIN(2);
-    if (inline_singles(m)) SVX_TRY(launch_scatter_update(m, s));
-    else SVX_TRY(launch_scatter(m, m->maxrows > 0, s));
+    SVX_TRY(launch_scatter(m, s));
     STAGE_END(2);
     STAGE_BEGIN(3);
     SVX_TRY(launch_update_a(m, feats_f64, s));
@@ -239,7 +228,7 @@ static svx_status run_frame(svx_map* m, int pts_f64, int feats_f64, cudaStream_t
     SVX_CUDA(cudaEventRecord(m->ev_in, s));
     SVX_CUDA(cudaStreamWaitEvent(m->gstream, m->ev_in, 0));
     SVX_CUDA(cudaGraphLaunch(m->gexec, m->gstream));
-    count_launch(6);
+    count_launch(8);
     SVX_CUDA(cudaEventRecord(m->ev1, m->gstream));
     SVX_CUDA(cudaEventSynchronize(m->ev1));
     return SVX_OK;
@@ -273,22 +262,16 @@ svx_status integrate_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n
         SVX_TRY(stage_in(feats_in, (size_t)n * m->payload_d * (feats_f64 ? 8 : 4), m->in_feat, s,
                          &feats));
 
-    // Scratch sizing.  A band of length L crosses at most 3 * (L / h + 1)
-    // voxels; without carving L = 2 * trunc, so each ray gets that many row
-    // slots and the scatter is one flat pass.  Carving bands are unbounded:
-    // the scatter re-walks them.  Capacities adapt to what frames need.
+    // Row space.  A band of length L crosses at most 3 * (L / h + 1) voxels;
+    // without carving L = 2 * trunc, so each ray gets that many row slots.
+    // Carving bands are unbounded: rows are counted, scanned and packed.
     const double h = m->cfg.voxel_size;
     if (m->maxrows < 0) {
         const double bound = 3.0 * (2.0 * m->cfg.truncation / h + 1.0) + 3.0;
-        m->maxrows = (m->cfg.space_carving || bound > 64.0) ? 0 : (int)bound;
+        m->maxrows = (m->cfg.space_carving || bound > 32.0) ? 0 : (int)bound;
     }
-    const double band = m->cfg.space_carving ? m->cfg.max_range + m->cfg.truncation
-                                             : 2.0 * m->cfg.truncation;
-    const uint64_t per_ray = (uint64_t)std::min(64.0, 3.0 * (band / h + 1.0) + 3.0);
-    if (m->rcap == 0) {   // first frame: worst-case guesses, adapted after each frame
-        m->rcap = (uint64_t)n * per_ray;
-        m->ucap = std::min<uint64_t>(m->rcap, (uint64_t)n * 16);
-    }
+    if (m->rcap == 0)   // first frame: the bound (bounded bands) or a guess; adapted per frame
+        m->rcap = m->maxrows > 0 ? (uint64_t)n * m->maxrows + 4096 : (uint64_t)n * 32 + 4096;
 
     KeyPack kp;
     {
@@ -296,11 +279,21 @@ svx_status integrate_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n
         for (int a = 0; a < 3; ++a) kp.base[a] = (long long)floor(pp.t[a] / h) - half;
     }
     FrameCtr* hc = m->h_ctr;
+    // counts before this frame (stamps, report); m->nblocks / m->nvox stay the
+    // live counts, including what a capacity-aborted attempt allocated
+    const int64_t nblocks0 = m->nblocks, nvox0 = m->nvox;
     for (int attempt = 0;; ++attempt) {
         if (attempt >= 8) return fail(SVX_E_INTERNAL, "frame scratch could not be sized");
         SVX_TRY(reserve_frame(m, n, s));
-        SVX_TRY(reserve_blocks(m, m->nblocks + (int64_t)m->ucap, s));
-        SVX_TRY(reserve_voxels(m, m->nvox + (int64_t)m->ucap, s));
+        // pool headroom: every row could open a voxel (closed/geometry), an
+        // eighth of them for open-set payloads; leaves get twice what recent
+        // frames created.  A shortfall is caught on the device and re-run.
+        const int64_t rows_bound = (int64_t)m->ucap;
+        const int64_t vhead = m->cfg.sem_kind == SVX_SEM_OPEN
+                                  ? std::max<int64_t>(rows_bound / 8, 1 << 16)
+                                  : rows_bound;
+        SVX_TRY(reserve_voxels(m, m->nvox + vhead, s));
+        SVX_TRY(reserve_blocks(m, m->nblocks + std::max<int64_t>(m->new_leaves_cap, 4096), s));
 
         memset(hc, 0, sizeof(FrameCtr));
         for (int a = 0; a < 3; ++a) {
@@ -318,19 +311,19 @@ svx_status integrate_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n
         p.kp = kp;
         p.ucap = m->ucap;
         p.rcap = m->rcap;
-        p.fmask = m->fcap - 1;
         p.hmask = m->hcap - 1;
-        p.nblocks0 = m->nblocks;
+        p.nblocks0 = nblocks0;
+        p.bcap = m->bcap;
+        p.vcap = m->vcap;
         p.frame = (int)m->frames;
         p.maxrows = m->maxrows;
+        p.inline_singles = inline_singles(m);
 
         SVX_TRY(run_frame(m, pts_f64, feats_f64, s));
 
         // the reference's pre-allocation checks, in its order (_core.pyx:661-712, :386-387)
-        if (hc->err_budget) {
-            SVX_TRY(clear_frame_table(m, s));
+        if (hc->err_budget)
             return fail(SVX_E_INTERNAL, "ray band exceeds step budget; shrink max_range or grow voxels");
-        }
         if (hc->rows) {
             bool extent = false, range = false;
             for (int a = 0; a < 3; ++a) {
@@ -338,28 +331,34 @@ svx_status integrate_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n
                 if (llabs(hc->bbox_min[a]) >= kCoordLimit || llabs(hc->bbox_max[a]) >= kCoordLimit)
                     range = true;
             }
-            if (extent) {
-                SVX_TRY(clear_frame_table(m, s));
+            if (extent)
                 return fail(SVX_E_INTERNAL,
                             "frame voxel extent exceeds 2^21 per axis; shrink max_range or grow voxels");
-            }
-            if (range) {
-                SVX_TRY(clear_frame_table(m, s));
-                return fail(SVX_E_RANGE, "voxel coordinate beyond +/-2^30 addressable range");
-            }
+            if (range) return fail(SVX_E_RANGE, "voxel coordinate beyond +/-2^30 addressable range");
         }
         if (hc->abort) {
-            SVX_TRY(clear_frame_table(m, s));
+            // stopped by the gate before any mutation: re-based keys (pack),
+            // dense rows (slot overflow) or a bigger dense row buffer
             if (hc->err_pack)
                 for (int a = 0; a < 3; ++a) kp.base[a] = hc->bbox_min[a];
-            if (hc->err_rows) m->maxrows = 0;
-            if (hc->err_probe || hc->n_groups > m->ucap || hc->rows_c > m->rcap ||
-                hc->rows > m->rcap) {
-                m->rcap = std::max<uint64_t>(2 * m->rcap, hc->rows + hc->rows / 2);
-                m->ucap = std::max<uint64_t>(2 * m->ucap,
-                                             std::min<uint64_t>(m->rcap, hc->n_groups * 2));
+            if (hc->err_rows) {
+                m->maxrows = 0;
+                m->rcap = std::max<uint64_t>(m->rcap, hc->rows + hc->rows / 2 + 4096);
             }
+            if (hc->err_cap) m->rcap = std::max<uint64_t>(2 * m->rcap, hc->rows + hc->rows / 2 + 4096);
+            continue;
+        }
+        if (hc->err_cap) {
+            // K2 ran out of leaf or voxel pool: give what it activated its
+            // background state, clear the frame counts, grow, run again (the
+            // allocation counters carry over)
+            SVX_TRY(launch_cleanup(m, s));
             SVX_CUDA(cudaStreamSynchronize(s));
+            m->nblocks = (int64_t)std::min<unsigned long long>(hc->nblocks, (unsigned long long)m->bcap);
+            m->nvox = (int64_t)std::min<unsigned long long>(hc->nvox, (unsigned long long)m->vcap);
+            m->ord_nblocks = std::min<int64_t>(m->ord_nblocks, nblocks0);
+            m->new_leaves_cap = std::max<int64_t>(2 * m->new_leaves_cap, m->bcap);
+            SVX_TRY(reserve_voxels(m, 2 * m->vcap, s));
             continue;
         }
         break;
@@ -372,23 +371,18 @@ svx_status integrate_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n
     r.skipped_bad_label = (int64_t)hc->bad_label;
     r.points_used = (int64_t)hc->used;
     r.band_hits = (int64_t)hc->band_hits;
-    r.touched_voxels = (int64_t)hc->n_groups;
-    r.new_blocks = (int64_t)hc->nblocks - m->nblocks;
-    r.new_voxels = (int64_t)hc->nvox - m->nvox;
+    r.touched_voxels = (int64_t)hc->n_touched;
+    r.new_blocks = (int64_t)hc->nblocks - nblocks0;
+    r.new_voxels = (int64_t)hc->nvox - nvox0;
     r.kernel_ms = ms;
+    m->new_leaves_cap = std::max<int64_t>(m->new_leaves_cap, 2 * r.new_blocks + 1024);
     m->nblocks = (int64_t)hc->nblocks;
     m->nvox = (int64_t)hc->nvox;
     m->frames++;
-    // adapt the scratch to what this frame needed (headroom for the next)
-    // (grow when nearly full, shrink once when far too big: the first frame's
-    // worst-case guess would otherwise keep the frame table cold and large)
-    const uint64_t u_next = hc->n_groups + hc->n_groups / 2 + 4096;
-    const uint64_t r_next = hc->rows_c + hc->rows_c / 2 + 4096;
-    if (hc->n_groups * 10 > m->ucap * 8 || u_next * 3 < m->ucap * 2) m->ucap = u_next;
-    const uint64_t rows_seen = std::max<uint64_t>(hc->rows_c, hc->rows);
-    const uint64_t r_need = rows_seen + rows_seen / 2 + 4096;
-    if (rows_seen * 10 > m->rcap * 8 || r_need * 3 < m->rcap * 2) m->rcap = r_need;
-    (void)r_next;
+    {   // row capacity for the next frame: 1.5x this one's rows
+        const uint64_t need = hc->rows + hc->rows / 2 + 4096;
+        if (hc->rows * 10 > m->rcap * 8 || need * 3 < m->rcap) m->rcap = need;
+    }
     if (rep) *rep = r;
     return SVX_OK;
 }

@@ -60,13 +60,16 @@ struct FrameParams {
     long long n;
     PoseParams pp;
     KeyPack kp;
-    unsigned long long ucap;   // unique voxels the scratch holds
-    unsigned long long rcap;   // rows the scratch holds
-    long long fmask;           // frame table capacity - 1
+    unsigned long long ucap;   // touched voxels the per-frame lists hold
+    unsigned long long rcap;   // rows the dense row arrays / segment buffer hold
     long long hmask;           // leaf hash capacity - 1
     long long nblocks0;        // leaves before this frame (ids >= it are new)
+    long long bcap;            // leaf pool capacity
+    long long vcap;            // voxel pool capacity
     int frame;                 // creation stamp for new leaves
-    int maxrows;               // row slots per ray (0: scatter re-walks the band)
+    int maxrows;               // row slots per ray; 0 = dense rows (two-pass walk)
+    int inline_singles;        // single-row voxels updated in the scatter (closed/geometry)
+    int pad;
 };
 
 // Per-CTA partial counters of the march, reduced by the gate (no
@@ -74,7 +77,7 @@ struct FrameParams {
 struct MarchPartial {
     unsigned long long nonfinite, range, degenerate, bad_label, used, band_hits, rows;
     long long bbox_min[3], bbox_max[3];
-    int errs;      // bit 0 budget, 1 pack, 2 probe, 3 rows
+    int errs;      // bit 0 budget, 1 pack, 3 row-slot overflow
     int pad;
 };
 
@@ -87,26 +90,48 @@ struct FrameCtr {
     unsigned long long bad_label;
     unsigned long long used;
     unsigned long long band_hits;   // rows emitted before the w <= 0 drop
-    unsigned long long rows;        // rows kept (w > 0), counted by the march
-    unsigned long long n_groups;    // unique voxels (U), from the compaction
-    unsigned long long n_list;      // voxels listed for the segment updates (U, or the
-                                    // multi-row ones when single-row voxels update inline)
-    unsigned long long rows_c;      // rows in listed segments, from the compaction
+    unsigned long long rows;        // rows kept (w > 0)
+    unsigned long long rows_alloc;  // dense row slots handed out by the tile walk
+    unsigned long long n_touched;   // unique voxels of the frame (U)
+    unsigned long long n_list;      // voxels listed for segment updates
+    unsigned long long rows_seg;    // rows placed in segments
     unsigned long long n_long;      // voxels routed to the long-segment update
     unsigned long long n_huge;      // voxels routed to the huge-segment update
-    unsigned long long n_new_blocks;
-    unsigned long long n_new_voxels;
-    unsigned long long nblocks;     // device copy of the leaf count (allocation counter)
-    unsigned long long nvox;        // device copy of the voxel count (allocation counter)
+    unsigned long long nblocks;     // leaf allocation counter (device copy)
+    unsigned long long nvox;        // voxel allocation counter (device copy)
     long long bbox_min[3];          // over kept rows
     long long bbox_max[3];
     int err_budget;                 // a ray exceeded the DDA step budget
     int err_pack;                   // a key offset left the 21-bit field (retry with bbox base)
-    int err_probe;                  // frame hash full (retry with a bigger table)
-    int err_rows;                   // a band exceeded maxrows (retry with the re-walk scatter)
+    int err_cap;                    // a pool / list / row buffer was too small (grow, retry)
+    int err_rows;                   // a band exceeded maxrows (retry with dense rows)
     int abort;                      // set by the gate: skip all mutation
     int pad;
 };
+
+// Per-voxel frame state (indexed by voxel id, zero between frames):
+//   vcnt  rows this frame; bit 31 = voxel allocated this frame
+//   vseg  base of the voxel's row segment;  vcur  fill cursor
+//   vkey  the voxel's frame key (written by its first toucher)
+constexpr unsigned kNewBit = 0x80000000u;
+
+// Row addressing: slot mode (bounded bands: ray i owns slots [i*maxrows, +rcnt[i]))
+// or dense mode (rows packed by a scan; rowray[r] = ray of row r).
+struct RowSpace {
+    int maxrows;
+    const int* rcnt;
+    const int* rowray;
+    long long total;
+};
+
+__device__ __forceinline__ bool row_ray(const RowSpace& rs, long long t, long long& i) {
+    if (rs.maxrows > 0) {
+        i = t / rs.maxrows;
+        return (int)(t - i * rs.maxrows) < rs.rcnt[i];
+    }
+    i = rs.rowray[t];
+    return true;
+}
 
 // Growable device buffer.
 struct DevBuf {
@@ -143,14 +168,15 @@ struct svx_map {
     svx::DevBuf hash;  int64_t hcap = 0;
     svx::DevBuf bcoord, bkey, bmask, bslot;  int64_t bcap = 0, nblocks = 0;
     svx::DevBuf vt, s0, s1;                  int64_t vcap = 0, nvox = 0;  // vt: {d, w} per voxel
+    svx::DevBuf vcnt, vseg, vcur, vkey;      // per-voxel frame state (see FrameCtr)
     int64_t frames = 0;
     // per-frame scratch
     svx::DevBuf in_pts, in_lab, in_feat;
-    svx::DevBuf ray, rcnt, rowslot, rowkey, partials;
-    svx::DevBuf fkey, fcount, foff, fcur;  int64_t fcap = 0;
-    svx::DevBuf ulist, ukey, gvid, longlist, srid, bitmap;
+    svx::DevBuf ray, rcnt, roff, rowkey, rowvid, rowray, partials;
+    svx::DevBuf tlist, mlist, longlist, srid, bitmap;
     uint64_t ucap = 0, rcap = 0;
-    int maxrows = -1;      // row slots per ray; 0 = re-walk scatter
+    int64_t new_leaves_cap = 0;   // leaf-pool headroom kept for one frame
+    int maxrows = -1;      // row slots per ray; 0 = dense rows
     int64_t npts_cap = 0;  // points the per-ray scratch holds
     // captured frame graph (replayed while the layout is unchanged)
     cudaStream_t gstream = nullptr;
@@ -268,19 +294,21 @@ svx_status integrate_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n
                           int feats_f64, cudaStream_t s, svx_report* rep);
 
 // ---- launchers implemented in the .cu files ---------------------------------
-// svx_march.cu
+// svx_march.cu: K1 walk (+ dense-row scan) and the gate
 MarchParams march_params(const svx_map* m);
 svx_status launch_march(svx_map* m, int pts_f64, int feats_f64, cudaStream_t s);
-svx_status launch_compact(svx_map* m, cudaStream_t s);
-svx_status launch_scatter(svx_map* m, bool flat, cudaStream_t s);
 size_t partials_bytes();
-// Single-row voxels of bounded (non-carving) closed/geometry frames are
-// updated inline by the scatter pass; everything else goes through segments.
-inline int inline_singles(const svx_map* m) {
-    return m->maxrows > 0 && m->cfg.sem_kind != SVX_SEM_OPEN;
-}
-svx_status launch_scatter_update(svx_map* m, cudaStream_t s);
-// svx_update.cu: stage A = resolve + short/open updates, stage B = long/huge
+// svx_resolve.cu: K2 voxel resolution + per-voxel counts, K3 segments
+svx_status launch_resolve(svx_map* m, cudaStream_t s);
+svx_status launch_segments(svx_map* m, cudaStream_t s);
+svx_status launch_cleanup(svx_map* m, cudaStream_t s);   // undo a capacity-aborted attempt
+size_t segment_partials_bytes();
+size_t scan_temp_bytes(int64_t n);
+// Single-row voxels of closed/geometry frames are updated inline by the
+// scatter pass; open-set voxels always go through segments.
+inline int inline_singles(const svx_map* m) { return m->cfg.sem_kind != SVX_SEM_OPEN; }
+// svx_update.cu: K4 scatter (+ single-row updates), K5 segment updates
+svx_status launch_scatter(svx_map* m, cudaStream_t s);
 svx_status launch_update_a(svx_map* m, int feats_f64, cudaStream_t s);
 svx_status launch_update_b(svx_map* m, int feats_f64, cudaStream_t s);
 svx_status launch_rehash(svx_map* m, int4* new_table, int64_t new_cap, cudaStream_t s);

@@ -1,6 +1,5 @@
-// svx_march.cu -- per-point preparation, the fp64 band ray-march (K1), and
-// the per-frame voxel grouping (counting sort by voxel: K2 compact, K3
-// scatter).
+// svx_march.cu -- per-point preparation and the fp64 band ray-march (K1),
+// plus the frame gate.
 //
 // Compiled with -fmad=false: every double expression is evaluated with the
 // operation order and IEEE round-to-nearest steps of the reference's
@@ -8,19 +7,12 @@
 // twin (_pycore.py:326-396), so band membership and per-row distances are
 // bit-identical.
 //
-// Grouping replaces the reference's global (voxel, point, step) sort
-// (_core.pyx:707-753): every band row inserts its voxel key into a per-frame
-// open-addressing table and bumps that voxel's row count (K1); a pass over
-// the table compacts the touched voxels and gives each a contiguous row
-// segment (K2); every row then drops its point index into its voxel's
-// segment (K3).  Rows inside a segment are put back into point order by the
-// update kernels -- the sequential per-voxel sums are all the reference's
-// sort order is needed for.
-//
-// Bounded bands (no space carving) split K1 into a compute-only walk that
-// writes each row's key into a per-ray slot array (K1a) and a flat,
-// fully parallel insert over all row slots (K1b); carving bands are
-// unbounded, so their walk inserts as it goes and K3 re-walks them.
+// The walk only computes: each kept row's voxel key and ray index are
+// written to dense row arrays (bounded bands: 128-ray tiles staged in shared
+// memory, one atomic per tile; unbounded bands, e.g. space carving: count,
+// scan, re-walk).  The
+// gate then applies the reference's pre-allocation checks before anything
+// touches the map.  Grouping rows by voxel happens in svx_resolve.cu.
 //
 // All per-frame values are read from the device-side FrameCtr so one
 // captured CUDA graph replays every frame; counters go to per-CTA partial
@@ -28,7 +20,7 @@
 #include <math.h>
 
 #include <cub/block/block_reduce.cuh>
-#include <cub/block/block_scan.cuh>
+#include <cub/device/device_scan.cuh>
 
 #include "svx_internal.cuh"
 
@@ -123,36 +115,6 @@ __device__ __forceinline__ bool row_kept(long long ci, long long cj, long long c
     return w > 0.0;
 }
 
-// Frame-table insert: speculative CAS on the home slot, linear probing on a
-// collision.  Returns the slot or -1 when the table is full.
-__device__ __forceinline__ long long frame_insert(unsigned long long* keys, long long mask,
-                                                  unsigned long long key) {
-    long long pos = (long long)(key_hash(key) & (unsigned long long)mask);
-    unsigned long long cur = atomicCAS(&keys[pos], kKeyEmpty, key);
-    if (cur == kKeyEmpty || cur == key) return pos;
-    for (long long probe = 0; probe < mask; ++probe) {
-        pos = (pos + 1) & mask;
-        cur = keys[pos];
-        if (cur == key) return pos;
-        if (cur == kKeyEmpty) {
-            cur = atomicCAS(&keys[pos], kKeyEmpty, key);
-            if (cur == kKeyEmpty || cur == key) return pos;
-        }
-    }
-    return -1;
-}
-
-__device__ __forceinline__ long long frame_find(const unsigned long long* __restrict__ keys,
-                                                long long mask, unsigned long long key) {
-    long long pos = (long long)(key_hash(key) & (unsigned long long)mask);
-    while (true) {
-        unsigned long long cur = keys[pos];
-        if (cur == key) return pos;
-        if (cur == kKeyEmpty) return -1;
-        pos = (pos + 1) & mask;
-    }
-}
-
 template <class P>
 __device__ __forceinline__ void load_point(const P* pts, long long i, double& x, double& y,
                                            double& z) {
@@ -180,10 +142,11 @@ struct OrOp {
     __device__ int operator()(int a, int b) const { return a | b; }
 };
 
+template <int kThreads>
 __device__ __forceinline__ void write_partial(const Tally& t, MarchPartial* out) {
-    using RU = cub::BlockReduce<unsigned long long, kMarchThreads>;
-    using RL = cub::BlockReduce<long long, kMarchThreads>;
-    using RI = cub::BlockReduce<int, kMarchThreads>;
+    using RU = cub::BlockReduce<unsigned long long, kThreads>;
+    using RL = cub::BlockReduce<long long, kThreads>;
+    using RI = cub::BlockReduce<int, kThreads>;
     __shared__ union {
         typename RU::TempStorage u;
         typename RL::TempStorage l;
@@ -263,94 +226,117 @@ __device__ __forceinline__ bool prepare_ray(long long i, const FrameParams& fp, 
     return keep;
 }
 
-// K1a (bounded bands): compute-only walk; row keys go to rowkey[i*maxrows+j].
+// K1 (bounded bands): compute-only walk over 128-ray tiles.  Each ray's row
+// keys are staged in shared memory; a block scan packs the tile's rows and
+// one atomic per tile reserves their place in the dense row arrays, which
+// are then written coalesced (rowkey, rowray).
+constexpr int kTileRays = 128;
+
 template <class P, class Fe>
-__global__ void __launch_bounds__(kMarchThreads) k_walk(MarchParams mp, int sem_kind,
-                                                        int num_classes, int D,
-                                                        double4* __restrict__ ray,
-                                                        int* __restrict__ rcnt,
-                                                        unsigned long long* __restrict__ rowkey,
-                                                        MarchPartial* __restrict__ partials,
-                                                        const FrameCtr* __restrict__ ctr) {
+__global__ void __launch_bounds__(kTileRays) k_walk(MarchParams mp, int sem_kind, int num_classes,
+                                                    int D, double4* __restrict__ ray,
+                                                    int* __restrict__ rcnt,
+                                                    unsigned long long* __restrict__ rowkey,
+                                                    int* __restrict__ rowray,
+                                                    MarchPartial* __restrict__ partials,
+                                                    FrameCtr* __restrict__ ctr) {
+    using Scan = cub::BlockScan<int, kTileRays>;
+    __shared__ typename Scan::TempStorage scan_tmp;
+    __shared__ unsigned long long s_base;
+    extern __shared__ unsigned long long s_keys[];   // kTileRays * maxrows keys, then ray ids
     const FrameParams fp = ctr->p;
     const long long n = fp.n;
     const int maxrows = fp.maxrows;
+    const unsigned long long rcap = fp.rcap;
+    int* s_ray = reinterpret_cast<int*>(s_keys + (size_t)kTileRays * maxrows);
+    unsigned long long* s_pack = s_keys;   // packed rows reuse the key area in place
     const double ox = fp.pp.t[0], oy = fp.pp.t[1], oz = fp.pp.t[2];
     Tally t;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (long long)gridDim.x * blockDim.x) {
-        double4 r;
+    const long long tiles = (n + kTileRays - 1) / kTileRays;
+    for (long long tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        const long long i = tile * kTileRays + threadIdx.x;
         int rows = 0;
-        if (prepare_ray<P, Fe>(i, fp, mp.max_range, sem_kind, num_classes, D, t, r)) {
-            unsigned long long* rk = rowkey + i * maxrows;
-            long long emitted = dda_walk(ox, oy, oz, r.x, r.y, r.z, r.w, mp,
-                [&](long long ci, long long cj, long long ck) {
-                    if (!row_kept(ci, cj, ck, ox, oy, oz, r, mp)) return;
-                    t.rows += 1;
-                    t.mn[0] = min(t.mn[0], ci); t.mn[1] = min(t.mn[1], cj); t.mn[2] = min(t.mn[2], ck);
-                    t.mx[0] = max(t.mx[0], ci); t.mx[1] = max(t.mx[1], cj); t.mx[2] = max(t.mx[2], ck);
-                    if (rows >= maxrows) {
-                        t.errs |= 8;
-                        return;
-                    }
-                    long long ox_ = ci - fp.kp.base[0], oy_ = cj - fp.kp.base[1], oz_ = ck - fp.kp.base[2];
-                    unsigned long long key = kKeyEmpty;
-                    if (((ox_ | oy_ | oz_) & ~kPackMask) != 0) t.errs |= 2;
-                    else key = pack_key(ox_, oy_, oz_);
-                    rk[rows++] = key;
-                });
-            if (emitted < 0) {
-                t.errs |= 1;
-                r.w = -1.0;
-                rows = 0;
-            } else {
-                t.band_hits += (unsigned long long)emitted;
+        unsigned long long* rk = s_keys + (size_t)threadIdx.x * maxrows;
+        if (i < n) {
+            double4 r;
+            if (prepare_ray<P, Fe>(i, fp, mp.max_range, sem_kind, num_classes, D, t, r)) {
+                long long emitted = dda_walk(ox, oy, oz, r.x, r.y, r.z, r.w, mp,
+                    [&](long long ci, long long cj, long long ck) {
+                        if (!row_kept(ci, cj, ck, ox, oy, oz, r, mp)) return;
+                        t.rows += 1;
+                        t.mn[0] = min(t.mn[0], ci); t.mn[1] = min(t.mn[1], cj); t.mn[2] = min(t.mn[2], ck);
+                        t.mx[0] = max(t.mx[0], ci); t.mx[1] = max(t.mx[1], cj); t.mx[2] = max(t.mx[2], ck);
+                        if (rows >= maxrows) {
+                            t.errs |= 8;
+                            return;
+                        }
+                        long long ox_ = ci - fp.kp.base[0], oy_ = cj - fp.kp.base[1], oz_ = ck - fp.kp.base[2];
+                        unsigned long long key = kKeyEmpty;
+                        if (((ox_ | oy_ | oz_) & ~kPackMask) != 0) t.errs |= 2;
+                        else key = pack_key(ox_, oy_, oz_);
+                        rk[rows++] = key;
+                    });
+                if (emitted < 0) {
+                    t.errs |= 1;
+                    r.w = -1.0;
+                    rows = 0;
+                } else {
+                    t.band_hits += (unsigned long long)emitted;
+                }
             }
+            ray[i] = r;
+            rcnt[i] = rows;
         }
-        ray[i] = r;
-        rcnt[i] = rows;
+        int off, total;
+        Scan(scan_tmp).ExclusiveSum(rows, off, total);
+        // pack this ray's keys to the front of the tile buffer, in ray order;
+        // keys are read into registers first (packing overlaps the source)
+        unsigned long long mine[64];
+#pragma unroll 1
+        for (int j = 0; j < rows; ++j) mine[j] = rk[j];
+        if (threadIdx.x == 0) s_base = total ? atomicAdd(&ctr->rows_alloc, (unsigned long long)total) : 0ULL;
+        __syncthreads();
+#pragma unroll 1
+        for (int j = 0; j < rows; ++j) {
+            s_pack[off + j] = mine[j];
+            s_ray[off + j] = (int)i;
+        }
+        __syncthreads();
+        const unsigned long long base = s_base;
+        if (base + (unsigned long long)total <= rcap) {
+            for (int e = threadIdx.x; e < total; e += kTileRays) {
+                rowkey[base + e] = s_pack[e];
+                rowray[base + e] = s_ray[e];
+            }
+        } else if (threadIdx.x == 0) {
+            atomicOr(&ctr->err_cap, 1);
+        }
+        __syncthreads();
     }
-    write_partial(t, partials + blockIdx.x);
+    write_partial<kTileRays>(t, partials + blockIdx.x);
 }
 
-// K1b (bounded bands): one thread per row slot inserts the key and counts it.
-__global__ void __launch_bounds__(256) k_insert(const int* __restrict__ rcnt,
-                                                const unsigned long long* __restrict__ rowkey,
-                                                int* __restrict__ rowslot, unsigned long long* fkey,
-                                                unsigned* fcount, FrameCtr* ctr) {
-    const long long n = ctr->p.n;
-    const int maxrows = ctr->p.maxrows;
-    const long long fmask = ctr->p.fmask;
-    const long long total = n * maxrows;
-    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
-         t += (long long)gridDim.x * blockDim.x) {
-        const long long i = t / maxrows;
-        const int j = (int)(t - i * maxrows);
-        if (j >= rcnt[i]) continue;
-        const unsigned long long key = rowkey[t];
-        if (key == kKeyEmpty) continue;          // pack error: the frame is re-run
-        const long long s = frame_insert(fkey, fmask, key);
-        if (s < 0) {
-            atomicOr(&ctr->err_probe, 1);
-            continue;
-        }
-        atomicAdd(&fcount[s], 1u);
-        rowslot[t] = (int)s;
-    }
-}
 
-// K1 (space carving, unbounded bands): walk and insert in one pass.
+// K1 (dense mode, e.g. space carving's unbounded bands), pass 1: count kept
+// rows per ray (rcnt is zero past n so a fixed-size scan covers it).
 template <class P, class Fe>
-__global__ void __launch_bounds__(kMarchThreads) k_walk_insert(
-    MarchParams mp, int sem_kind, int num_classes, int D, double4* __restrict__ ray,
-    int* __restrict__ rcnt, unsigned long long* fkey, unsigned* fcount,
-    MarchPartial* __restrict__ partials, const FrameCtr* __restrict__ ctr) {
+__global__ void __launch_bounds__(kMarchThreads) k_walk_count(MarchParams mp, int sem_kind,
+                                                              int num_classes, int D,
+                                                              long long npts_cap,
+                                                              double4* __restrict__ ray,
+                                                              int* __restrict__ rcnt,
+                                                              MarchPartial* __restrict__ partials,
+                                                              const FrameCtr* __restrict__ ctr) {
     const FrameParams fp = ctr->p;
     const long long n = fp.n;
     const double ox = fp.pp.t[0], oy = fp.pp.t[1], oz = fp.pp.t[2];
     Tally t;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < npts_cap;
          i += (long long)gridDim.x * blockDim.x) {
+        if (i >= n) {
+            rcnt[i] = 0;
+            continue;
+        }
         double4 r;
         int rows = 0;
         if (prepare_ray<P, Fe>(i, fp, mp.max_range, sem_kind, num_classes, D, t, r)) {
@@ -361,17 +347,7 @@ __global__ void __launch_bounds__(kMarchThreads) k_walk_insert(
                     t.mn[0] = min(t.mn[0], ci); t.mn[1] = min(t.mn[1], cj); t.mn[2] = min(t.mn[2], ck);
                     t.mx[0] = max(t.mx[0], ci); t.mx[1] = max(t.mx[1], cj); t.mx[2] = max(t.mx[2], ck);
                     long long ox_ = ci - fp.kp.base[0], oy_ = cj - fp.kp.base[1], oz_ = ck - fp.kp.base[2];
-                    if (((ox_ | oy_ | oz_) & ~kPackMask) != 0) {
-                        t.errs |= 2;
-                        return;
-                    }
-                    if (t.errs & 4) return;   // table full: the frame is re-run anyway
-                    long long s = frame_insert(fkey, fp.fmask, pack_key(ox_, oy_, oz_));
-                    if (s < 0) {
-                        t.errs |= 4;
-                        return;
-                    }
-                    atomicAdd(&fcount[s], 1u);
+                    if (((ox_ | oy_ | oz_) & ~kPackMask) != 0) t.errs |= 2;
                     ++rows;
                 });
             if (emitted < 0) {
@@ -385,131 +361,41 @@ __global__ void __launch_bounds__(kMarchThreads) k_walk_insert(
         ray[i] = r;
         rcnt[i] = rows;
     }
-    write_partial(t, partials + blockIdx.x);
+    write_partial<kMarchThreads>(t, partials + blockIdx.x);
 }
 
-constexpr int kCompactThreads = 256;
-constexpr int kCompactTile = kCompactThreads * 4;
-constexpr int kCompactBlocks = 148 * 2;
-
-// K2a: per-CTA totals over a contiguous table chunk: touched voxels, listed
-// voxels (all, or only multi-row ones when single-row voxels are updated
-// inline by the scatter) and the rows of the listed ones.
-__global__ void __launch_bounds__(kCompactThreads) k_compact_count(
-    const unsigned long long* __restrict__ fkey, const unsigned* __restrict__ fcount,
-    long long fcap, long long chunk, int multi_only, unsigned long long* __restrict__ part) {
-    using R = cub::BlockReduce<unsigned long long, kCompactThreads>;
-    __shared__ typename R::TempStorage tmp;
-    const long long lo = (long long)blockIdx.x * chunk;
-    const long long hi = min(fcap, lo + chunk);
-    unsigned long long occ = 0, listed = 0, rows = 0;
-    for (long long s = lo + threadIdx.x; s < hi; s += kCompactThreads) {
-        const unsigned long long k = fkey[s];
-        if (k != kKeyEmpty) {
-            occ += 1;
-            const unsigned c = fcount[s];
-            if (!multi_only || c > 1u) {
-                listed += 1;
-                rows += c;
-            }
-        }
-    }
-    unsigned long long packed = R(tmp).Sum((listed << 40) | rows);
-    __syncthreads();
-    unsigned long long o = R(tmp).Sum(occ);
-    if (threadIdx.x == 0) {
-        part[2 * blockIdx.x] = packed;
-        part[2 * blockIdx.x + 1] = o;
-    }
-}
-
-__device__ void gate_body(const MarchPartial* __restrict__ parts, int nparts, FrameCtr* ctr);
-
-// K2b: each CTA scans its chunk again with its exclusive base; listed
-// voxels are compacted into ulist/ukey and get contiguous row segments.
-__global__ void __launch_bounds__(kCompactThreads) k_compact_write(
-    const unsigned long long* __restrict__ fkey, const unsigned* __restrict__ fcount,
-    unsigned* __restrict__ foff, long long fcap, long long chunk, int multi_only,
-    const unsigned long long* __restrict__ part, int* __restrict__ ulist,
-    unsigned long long* __restrict__ ukey, const MarchPartial* __restrict__ mparts, int nmparts,
-    FrameCtr* ctr) {
-    using Scan = cub::BlockScan<unsigned long long, kCompactThreads>;
-    using R = cub::BlockReduce<unsigned long long, kCompactThreads>;
-    __shared__ union {
-        typename Scan::TempStorage scan;
-        typename R::TempStorage red;
-    } tmp;
-    __shared__ unsigned long long s_base, s_occ;
-    const unsigned long long ucap = ctr->p.ucap;
-    const unsigned long long low40 = (1ULL << 40) - 1;
-    // exclusive base of this CTA: sum of the earlier CTAs' packed totals
-    unsigned long long acc = 0, occ_all = 0;
-    const bool last = blockIdx.x == gridDim.x - 1;
-    for (int b = threadIdx.x; b < (int)gridDim.x; b += kCompactThreads) {
-        if (b < (int)blockIdx.x) acc += part[2 * b];
-        if (last) occ_all += part[2 * b + 1];
-    }
-    acc = R(tmp.red).Sum(acc);
-    __syncthreads();
-    occ_all = R(tmp.red).Sum(occ_all);
-    if (threadIdx.x == 0) {
-        s_base = acc;
-        s_occ = occ_all;
-    }
-    __syncthreads();
-    unsigned long long base = s_base;
-    const long long lo = (long long)blockIdx.x * chunk;
-    const long long hi = min(fcap, lo + chunk);
-    for (long long t0 = lo; t0 < hi; t0 += kCompactTile) {
-        const long long s0 = t0 + (long long)threadIdx.x * 4;
-        unsigned long long kk[4];
-        unsigned cc[4];
-        bool li[4];
-        unsigned cnt = 0, rows = 0;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const long long s = s0 + q;
-            kk[q] = s < hi ? fkey[s] : kKeyEmpty;
-            cc[q] = kk[q] != kKeyEmpty ? fcount[s] : 0u;
-            li[q] = kk[q] != kKeyEmpty && (!multi_only || cc[q] > 1u);
-            cnt += li[q];
-            rows += li[q] ? cc[q] : 0u;
-        }
-        unsigned long long pre, total;
-        __syncthreads();
-        Scan(tmp.scan).ExclusiveSum(((unsigned long long)cnt << 40) | rows, pre, total);
-        unsigned long long u = (base >> 40) + (pre >> 40);
-        unsigned long long r = (base & low40) + (pre & low40);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            if (!li[q]) continue;
-            const long long s = s0 + q;
-            if (u < ucap) {
-                ulist[u] = (int)s;
-                ukey[u] = kk[q];
-            }
-            foff[s] = (unsigned)r;
-            ++u;
-            r += cc[q];
-        }
-        base += total;
-    }
-    if (last) {
-        if (threadIdx.x == 0) {
-            ctr->n_groups = s_occ;
-            ctr->n_list = base >> 40;
-            ctr->rows_c = base & low40;
-        }
-        __syncthreads();
-        gate_body(mparts, nmparts, ctr);
+// K1 (dense mode), pass 2: re-walk and write each kept row at its scanned offset.
+__global__ void __launch_bounds__(kMarchThreads) k_walk_write(MarchParams mp,
+                                                              const double4* __restrict__ ray,
+                                                              const int* __restrict__ rcnt,
+                                                              const long long* __restrict__ roff,
+                                                              unsigned long long* __restrict__ rowkey,
+                                                              int* __restrict__ rowray,
+                                                              const FrameCtr* __restrict__ ctr) {
+    if (ctr->abort) return;
+    const FrameParams fp = ctr->p;
+    const long long n = fp.n;
+    const double ox = fp.pp.t[0], oy = fp.pp.t[1], oz = fp.pp.t[2];
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        if (rcnt[i] == 0) continue;
+        const double4 r = ray[i];
+        long long o = roff[i];
+        dda_walk(ox, oy, oz, r.x, r.y, r.z, r.w, mp, [&](long long ci, long long cj, long long ck) {
+            if (!row_kept(ci, cj, ck, ox, oy, oz, r, mp)) return;
+            rowkey[o] = pack_key(ci - fp.kp.base[0], cj - fp.kp.base[1], ck - fp.kp.base[2]);
+            rowray[o] = (int)i;
+            ++o;
+        });
     }
 }
 
 // Reduce the march partials and decide, once per frame on the device, whether
-// the frame may mutate the map (the reference's checks before any
-// allocation, _core.pyx:661-712, :386-387).  The host reports the reason.
-// Run by the last CTA of the compaction (256 threads) once the totals are in.
-__device__ void gate_body(const MarchPartial* __restrict__ parts, int nparts, FrameCtr* ctr) {
+// the frame may mutate the map -- the reference's checks before any
+// allocation (_core.pyx:661-712, :386-387) plus the dense row capacity.  The
+// host reports the reason after the frame.
+__global__ void __launch_bounds__(256) k_gate(const MarchPartial* __restrict__ parts, int nparts,
+                                              FrameCtr* ctr) {
     using RU = cub::BlockReduce<unsigned long long, 256>;
     using RL = cub::BlockReduce<long long, 256>;
     __shared__ union {
@@ -552,10 +438,12 @@ __device__ void gate_body(const MarchPartial* __restrict__ parts, int nparts, Fr
     for (int w = 1; w < 8; ++w) errs |= s_err[w];
     if (errs & 1) ctr->err_budget = 1;
     if (errs & 2) ctr->err_pack = 1;
-    if (errs & 4) ctr->err_probe = 1;
     if (errs & 8) ctr->err_rows = 1;
-    int ab = ctr->err_budget | ctr->err_pack | ctr->err_probe | ctr->err_rows;
-    if (ctr->n_list > ctr->p.ucap || ctr->n_groups > ctr->p.ucap || ctr->rows_c > ctr->p.rcap) ab = 1;
+    int ab = ctr->err_budget | ctr->err_pack | ctr->err_rows;
+    if (ctr->rows > ctr->p.rcap) {
+        ctr->err_cap = 1;
+        ab = 1;
+    }
     if (ctr->rows) {
         for (int a = 0; a < 3; ++a) {
             long long lo = ctr->bbox_min[a], hi = ctr->bbox_max[a];
@@ -566,74 +454,35 @@ __device__ void gate_body(const MarchPartial* __restrict__ parts, int nparts, Fr
     ctr->abort = ab;
 }
 
-// K3 (bounded bands): one thread per row slot -- fully parallel.
-__global__ void __launch_bounds__(256) k_scatter_flat(const int* __restrict__ rcnt,
-                                                      const int* __restrict__ rowslot,
-                                                      const unsigned* __restrict__ foff,
-                                                      unsigned* fcur, int* __restrict__ srid,
-                                                      const FrameCtr* __restrict__ ctr) {
-    if (ctr->abort) return;
-    const long long n = ctr->p.n;
-    const int maxrows = ctr->p.maxrows;
-    const long long total = n * maxrows;
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) {
-        const long long i = t / maxrows;
-        const int j = (int)(t - i * maxrows);
-        if (j >= rcnt[i]) continue;
-        const int s = rowslot[t];
-        const unsigned pos = foff[s] + atomicAdd(&fcur[s], 1u);
-        srid[pos] = (int)i;
-    }
-}
-
-// K3 (space carving): re-walk each ray and look its voxels up again.
-__global__ void __launch_bounds__(256) k_scatter_walk(const double4* __restrict__ ray,
-                                                      MarchParams mp,
-                                                      const unsigned long long* __restrict__ fkey,
-                                                      const unsigned* __restrict__ foff,
-                                                      unsigned* fcur, int* __restrict__ srid,
-                                                      const FrameCtr* __restrict__ ctr) {
-    if (ctr->abort) return;
-    const long long n = ctr->p.n;
-    const PoseParams pp = ctr->p.pp;
-    const KeyPack kp = ctr->p.kp;
-    const long long fmask = ctr->p.fmask;
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-        const double4 r = ray[i];
-        if (!(r.w >= 0.0)) continue;
-        const double ox = pp.t[0], oy = pp.t[1], oz = pp.t[2];
-        dda_walk(ox, oy, oz, r.x, r.y, r.z, r.w, mp, [&](long long ci, long long cj, long long ck) {
-            if (!row_kept(ci, cj, ck, ox, oy, oz, r, mp)) return;
-            unsigned long long key = pack_key(ci - kp.base[0], cj - kp.base[1], ck - kp.base[2]);
-            long long s = frame_find(fkey, fmask, key);
-            unsigned pos = foff[s] + atomicAdd(&fcur[s], 1u);
-            srid[pos] = (int)i;
-        });
-    }
-}
-
 template <class P, class Fe>
 svx_status march_t(svx_map* m, cudaStream_t s) {
     const MarchParams mp = march_params(m);
     MarchPartial* parts = ptr<MarchPartial>(m->partials);
+    FrameCtr* dc = ptr<FrameCtr>(m->ctr);
     if (m->maxrows > 0) {
-        k_walk<P, Fe><<<kMarchBlocks, kMarchThreads, 0, s>>>(
+        const size_t smem = (size_t)kTileRays * m->maxrows * (sizeof(unsigned long long) + sizeof(int));
+        k_walk<P, Fe><<<kMarchBlocks, kTileRays, smem, s>>>(
             mp, m->cfg.sem_kind, m->cfg.num_classes, m->payload_d, ptr<double4>(m->ray),
-            ptr<int>(m->rcnt), ptr<unsigned long long>(m->rowkey), parts, ptr<FrameCtr>(m->ctr));
+            ptr<int>(m->rcnt), ptr<unsigned long long>(m->rowkey), ptr<int>(m->rowray), parts, dc);
         SVX_LAUNCHED();
-        k_insert<<<kPersistentBlocks * 2, 256, 0, s>>>(
-            ptr<int>(m->rcnt), ptr<unsigned long long>(m->rowkey), ptr<int>(m->rowslot),
-            ptr<unsigned long long>(m->fkey), ptr<unsigned>(m->fcount), ptr<FrameCtr>(m->ctr));
+        k_gate<<<1, 256, 0, s>>>(parts, kMarchBlocks, dc);
         SVX_LAUNCHED();
-    } else {
-        k_walk_insert<P, Fe><<<kMarchBlocks, kMarchThreads, 0, s>>>(
-            mp, m->cfg.sem_kind, m->cfg.num_classes, m->payload_d, ptr<double4>(m->ray),
-            ptr<int>(m->rcnt), ptr<unsigned long long>(m->fkey), ptr<unsigned>(m->fcount), parts,
-            ptr<FrameCtr>(m->ctr));
-        SVX_LAUNCHED();
+        return SVX_OK;
     }
+    k_walk_count<P, Fe><<<kMarchBlocks, kMarchThreads, 0, s>>>(
+        mp, m->cfg.sem_kind, m->cfg.num_classes, m->payload_d, m->npts_cap, ptr<double4>(m->ray),
+        ptr<int>(m->rcnt), parts, dc);
+    SVX_LAUNCHED();
+    size_t tmp = m->cubtmp.bytes;
+    SVX_CUDA(cub::DeviceScan::ExclusiveSum(m->cubtmp.p, tmp, ptr<int>(m->rcnt),
+                                           ptr<long long>(m->roff), (int)m->npts_cap, s));
+    count_launch();
+    k_gate<<<1, 256, 0, s>>>(parts, kMarchBlocks, dc);
+    SVX_LAUNCHED();
+    k_walk_write<<<kMarchBlocks, kMarchThreads, 0, s>>>(
+        mp, ptr<double4>(m->ray), ptr<int>(m->rcnt), ptr<long long>(m->roff),
+        ptr<unsigned long long>(m->rowkey), ptr<int>(m->rowray), dc);
+    SVX_LAUNCHED();
     return SVX_OK;
 }
 
@@ -658,41 +507,12 @@ svx_status launch_march(svx_map* m, int pts_f64, int feats_f64, cudaStream_t s) 
     return march_t<float, float>(m, s);
 }
 
-svx_status launch_compact(svx_map* m, cudaStream_t s) {
-    long long chunk = (m->fcap + kCompactBlocks - 1) / kCompactBlocks;
-    chunk = (chunk + kCompactTile - 1) / kCompactTile * kCompactTile;
-    const int blocks = (int)((m->fcap + chunk - 1) / chunk);
-    unsigned long long* part = ptr<unsigned long long>(m->partials) +
-                               (sizeof(MarchPartial) * kMarchBlocks) / sizeof(unsigned long long);
-    const int multi_only = inline_singles(m);
-    k_compact_count<<<blocks, kCompactThreads, 0, s>>>(
-        ptr<unsigned long long>(m->fkey), ptr<unsigned>(m->fcount), m->fcap, chunk, multi_only, part);
-    SVX_LAUNCHED();
-    k_compact_write<<<blocks, kCompactThreads, 0, s>>>(
-        ptr<unsigned long long>(m->fkey), ptr<unsigned>(m->fcount), ptr<unsigned>(m->foff), m->fcap,
-        chunk, multi_only, part, ptr<int>(m->ulist), ptr<unsigned long long>(m->ukey),
-        ptr<MarchPartial>(m->partials), kMarchBlocks, ptr<FrameCtr>(m->ctr));
-    SVX_LAUNCHED();
-    return SVX_OK;
-}
+size_t partials_bytes() { return sizeof(MarchPartial) * kMarchBlocks; }
 
-svx_status launch_scatter(svx_map* m, bool flat, cudaStream_t s) {
-    if (flat) {
-        k_scatter_flat<<<kPersistentBlocks * 2, 256, 0, s>>>(
-            ptr<int>(m->rcnt), ptr<int>(m->rowslot), ptr<unsigned>(m->foff), ptr<unsigned>(m->fcur),
-            ptr<int>(m->srid), ptr<FrameCtr>(m->ctr));
-    } else {
-        k_scatter_walk<<<kPersistentBlocks, 256, 0, s>>>(
-            ptr<double4>(m->ray), march_params(m), ptr<unsigned long long>(m->fkey),
-            ptr<unsigned>(m->foff), ptr<unsigned>(m->fcur), ptr<int>(m->srid),
-            ptr<FrameCtr>(m->ctr));
-    }
-    SVX_LAUNCHED();
-    return SVX_OK;
-}
-
-size_t partials_bytes() {
-    return sizeof(MarchPartial) * kMarchBlocks + sizeof(unsigned long long) * kCompactBlocks * 2;
+size_t scan_temp_bytes(int64_t n) {
+    size_t tmp = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp, (const int*)nullptr, (long long*)nullptr, (int)n);
+    return tmp;
 }
 
 }  // namespace svx

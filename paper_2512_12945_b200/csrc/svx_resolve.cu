@@ -1,0 +1,365 @@
+// svx_resolve.cu -- K2: rows -> persistent voxel ids (leaf find-or-insert,
+// voxel activation) and per-voxel row counts; K3: row segments.
+//
+// This is where the reference's grouping (_core.pyx:707-753) and allocation
+// (ensure_coords, _core.pyx:377-420; _resolve_leaf_alloc :248-280) happen.
+// Rows are grouped by the voxel's persistent id rather than by a per-frame
+// key table: each row resolves its voxel once (lanes of a warp that hit the
+// same voxel, or the same leaf, share one lookup), counts itself in the
+// voxel's vcnt and the voxel's first toucher appends it to the frame's
+// touched list.  Only voxels with several rows need a segment (their rows
+// are re-sorted by point index later); single-row voxels of closed/geometry
+// maps are finished in ray order by the scatter.
+//
+// Leaf order: new leaves take arrival-order ids and record (creation frame,
+// smallest frame key of their voxels); frame keys are x-major offsets from
+// one base, so that stamp is the reference's first-occurrence order and
+// queries recover the reference's allocation order from it (svx_query.cu).
+//
+// Capacity: pools are sized before the frame from the previous frames; a
+// pool that still runs out sets err_cap, rolls its claim back, and the host
+// cleans up (launch_cleanup), grows and re-runs the frame.
+#include <cub/block/block_reduce.cuh>
+#include <cub/block/block_scan.cuh>
+
+#include "svx_internal.cuh"
+
+namespace svx {
+namespace {
+
+constexpr int kResolveThreads = 256;
+constexpr int kSegThreads = 256;
+constexpr int kSegTile = kSegThreads * 4;
+constexpr int kSegBlocks = 148 * 2;
+
+__device__ __forceinline__ int slot_of(long long x, long long y, long long z) {
+    return (int)(((x & 7) << 6) | ((y & 7) << 3) | (z & 7));
+}
+
+// counter += 1 for every converged lane, one atomic per warp; returns this
+// lane's ticket.
+__device__ __forceinline__ unsigned long long warp_ticket(unsigned long long* counter) {
+    const unsigned mask = __activemask();
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(mask) - 1;
+    const unsigned rank = __popc(mask & ((1u << lane) - 1u));
+    unsigned long long base = 0;
+    if (lane == leader) base = atomicAdd(counter, (unsigned long long)__popc(mask));
+    base = __shfl_sync(mask, base, leader);
+    return base + rank;
+}
+
+// Leaf find-or-insert.  A claimed slot stays BUSY until the new leaf's id,
+// coordinates and creation frame are written; then the id is published.
+// Returns -1 (and sets err_cap) when the leaf pool is full.
+__device__ int leaf_find_or_insert(int4* table, long long mask, int a, int b, int c, int frame,
+                                   long long bcap, int4* bcoord, FrameCtr* ctr) {
+    long long pos = (long long)(block_hash(a, b, c) & (unsigned long long)mask);
+    while (true) {
+        // Fast path: one 16-byte L2 read.  A published id was written after
+        // its key (release fence on the creating side), so a matching key is
+        // final -- almost every lookup ends here.
+        const int4 sv = __ldcg(table + pos);
+        if (sv.w >= 0) {
+            if (sv.x == a && sv.y == b && sv.z == c) return sv.w;
+            pos = (pos + 1) & mask;
+            continue;
+        }
+        volatile int* vw = &table[pos].w;
+        int v = sv.w;
+        if (v == kHashEmpty) {
+            int old = atomicCAS((int*)&table[pos].w, kHashEmpty, kHashBusy);
+            if (old == kHashEmpty) {
+                const long long id = (long long)warp_ticket(&ctr->nblocks);
+                if (id >= bcap) {
+                    atomicExch((int*)&table[pos].w, kHashEmpty);
+                    atomicOr(&ctr->err_cap, 1);
+                    return -1;
+                }
+                table[pos].x = a;
+                table[pos].y = b;
+                table[pos].z = c;
+                bcoord[id] = make_int4(a, b, c, frame);
+                __threadfence();
+                atomicExch((int*)&table[pos].w, (int)id);
+                return (int)id;
+            }
+            v = old;
+        }
+        while (v == kHashBusy) {
+            __nanosleep(20);
+            v = *vw;
+        }
+        if (v == kHashEmpty) {   // a creator rolled back (pool full)
+            atomicOr(&ctr->err_cap, 1);
+            return -1;
+        }
+        __threadfence();
+        volatile int* key = &table[pos].x;
+        if (key[0] == a && key[1] == b && key[2] == c) return v;
+        pos = (pos + 1) & mask;
+    }
+}
+
+// Voxel find-or-activate inside a leaf (GridCore.activate_slot semantics,
+// _core.pyx:312-322).  A new voxel is marked in its frame count (kNewBit) so
+// the update uses background state (grid.py:37-77).  Returns -1 when the
+// voxel pool is full.
+__device__ int voxel_find_or_alloc(int* bslot, unsigned long long* bmask, long long id, int slot,
+                                   long long vcap, unsigned* vcnt, FrameCtr* ctr) {
+    int* sp = &bslot[id * kLeafVolume + slot];
+    int v = __ldcg(sp);
+    if (v >= 0) return v;
+    if (v == -1) {
+        const int old = atomicCAS(sp, -1, -2);
+        if (old == -1) {
+            const long long vid = (long long)warp_ticket(&ctr->nvox);
+            if (vid >= vcap) {
+                atomicExch(sp, -1);
+                atomicOr(&ctr->err_cap, 1);
+                return -1;
+            }
+            atomicOr(&vcnt[vid], kNewBit);
+            atomicOr(&bmask[id * kMaskWords + (slot >> 6)], 1ULL << (slot & 63));
+            __threadfence();
+            atomicExch(sp, (int)vid);
+            return (int)vid;
+        }
+        v = old;
+    }
+    volatile int* vsp = sp;
+    while (v == -2) {
+        __nanosleep(20);
+        v = *vsp;
+    }
+    if (v < 0) atomicOr(&ctr->err_cap, 1);
+    return v;
+}
+
+// K2: one thread per row.  Lanes that hit the same voxel elect one leader
+// (one lookup, one count of popc(peers)); voxel leaders that share a leaf
+// elect one leaf lookup.
+__global__ void __launch_bounds__(kResolveThreads) k_resolve(
+    const int* __restrict__ rcnt, const int* __restrict__ rowray,
+    const unsigned long long* __restrict__ rowkey, int* __restrict__ rowvid, int4* table,
+    int4* bcoord, unsigned long long* bkey, unsigned long long* bmask, int* bslot, unsigned* vcnt,
+    unsigned long long* __restrict__ vkey, int* __restrict__ tlist, FrameCtr* ctr) {
+    if (ctr->abort | ctr->err_cap) return;
+    const FrameParams& fp = ctr->p;
+    RowSpace rs;
+    rs.maxrows = 0;   // rows are dense in every mode
+    rs.rcnt = rcnt;
+    rs.rowray = rowray;
+    rs.total = (long long)ctr->rows;
+    const KeyPack kp = fp.kp;
+    const long long hmask = fp.hmask, bcap = fp.bcap, vcap = fp.vcap, nblocks0 = fp.nblocks0;
+    const int frame = fp.frame;
+    const int lane = threadIdx.x & 31;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    const long long total_r = (rs.total + 31) & ~31LL;   // warp-uniform trip count
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total_r; t += stride) {
+        long long i = 0;
+        bool valid = t < rs.total && row_ray(rs, t, i);
+        const unsigned long long key = valid ? rowkey[t] : kKeyEmpty;
+        valid = valid && key != kKeyEmpty;
+        long long x = 0, y = 0, z = 0;
+        if (valid) unpack_key(key, kp, x, y, z);
+        const unsigned full = 0xffffffffu;
+        const unsigned vpeers = __match_any_sync(full, valid ? key : (kKeyEmpty ^ (unsigned long long)lane));
+        const int vleader = __ffs(vpeers) - 1;
+        const bool is_vl = valid && lane == vleader;
+        // exact leaf identity: leaf coords relative to the base's leaf, 19 bits each
+        const unsigned long long lkey =
+            is_vl ? (((unsigned long long)((x >> kLeafLog2) - (kp.base[0] >> kLeafLog2)) << 38) |
+                     ((unsigned long long)((y >> kLeafLog2) - (kp.base[1] >> kLeafLog2)) << 19) |
+                     (unsigned long long)((z >> kLeafLog2) - (kp.base[2] >> kLeafLog2)))
+                  : (~0ULL ^ (unsigned long long)lane);
+        const unsigned lpeers = __match_any_sync(full, lkey);
+        const int lleader = __ffs(lpeers) - 1;
+        int id = -1;
+        if (is_vl && lane == lleader) {
+            id = leaf_find_or_insert(table, hmask, (int)(x >> kLeafLog2), (int)(y >> kLeafLog2),
+                                     (int)(z >> kLeafLog2), frame, bcap, bcoord, ctr);
+        }
+        id = __shfl_sync(full, id, lleader);
+        int vid = -1;
+        if (is_vl && id >= 0) {
+            if (id >= nblocks0) atomicMin(&bkey[id], key);
+            vid = voxel_find_or_alloc(bslot, bmask, id, slot_of(x, y, z), vcap, vcnt, ctr);
+            if (vid >= 0) {
+                const unsigned c = atomicAdd(&vcnt[vid], (unsigned)__popc(vpeers));
+                if ((c & ~kNewBit) == 0u) {
+                    vkey[vid] = key;
+                    tlist[warp_ticket(&ctr->n_touched)] = vid;
+                }
+            }
+        }
+        vid = __shfl_sync(full, vid, vleader);
+        if (valid) rowvid[t] = vid;
+    }
+}
+
+// K3a: per-CTA totals over a contiguous chunk of the touched list: listed
+// voxels (multi-row ones, or all for open-set maps) and their rows.
+__device__ __forceinline__ long long seg_chunk(long long n) {
+    long long chunk = (n + kSegBlocks - 1) / kSegBlocks;
+    return (chunk + kSegTile - 1) / kSegTile * kSegTile;
+}
+
+__global__ void __launch_bounds__(kSegThreads) k_seg_count(const int* __restrict__ tlist,
+                                                           const unsigned* __restrict__ vcnt,
+                                                           unsigned long long* __restrict__ part,
+                                                           const FrameCtr* __restrict__ ctr) {
+    using R = cub::BlockReduce<unsigned long long, kSegThreads>;
+    __shared__ typename R::TempStorage tmp;
+    if (ctr->abort | ctr->err_cap) return;
+    const long long n = (long long)ctr->n_touched;
+    const int singles = ctr->p.inline_singles;
+    const long long chunk = seg_chunk(n);
+    const long long lo = (long long)blockIdx.x * chunk, hi = min(n, lo + chunk);
+    unsigned long long listed = 0, rows = 0;
+    for (long long e = lo + threadIdx.x; e < hi; e += kSegThreads) {
+        const unsigned c = vcnt[tlist[e]] & ~kNewBit;
+        if (!singles || c > 1u) {
+            listed += 1;
+            rows += c;
+        }
+    }
+    const unsigned long long packed = R(tmp).Sum((listed << 40) | rows);
+    if (threadIdx.x == 0) part[blockIdx.x] = packed;
+}
+
+// K3b: each CTA rescans its chunk with its exclusive base; listed voxels go
+// to mlist and get contiguous row segments (vseg).
+__global__ void __launch_bounds__(kSegThreads) k_seg_write(const int* __restrict__ tlist,
+                                                           const unsigned* __restrict__ vcnt,
+                                                           unsigned* __restrict__ vseg,
+                                                           const unsigned long long* __restrict__ part,
+                                                           int* __restrict__ mlist, FrameCtr* ctr) {
+    using Scan = cub::BlockScan<unsigned long long, kSegThreads>;
+    using R = cub::BlockReduce<unsigned long long, kSegThreads>;
+    __shared__ union {
+        typename Scan::TempStorage scan;
+        typename R::TempStorage red;
+    } tmp;
+    __shared__ unsigned long long s_base;
+    if (ctr->abort | ctr->err_cap) return;
+    const long long n = (long long)ctr->n_touched;
+    const int singles = ctr->p.inline_singles;
+    const unsigned long long low40 = (1ULL << 40) - 1;
+    unsigned long long acc = 0;
+    for (int b = threadIdx.x; b < (int)blockIdx.x; b += kSegThreads) acc += part[b];
+    acc = R(tmp.red).Sum(acc);
+    if (threadIdx.x == 0) s_base = acc;
+    __syncthreads();
+    unsigned long long base = s_base;
+    const long long chunk = seg_chunk(n);
+    const long long lo = (long long)blockIdx.x * chunk, hi = min(n, lo + chunk);
+    for (long long t0 = lo; t0 < hi; t0 += kSegTile) {
+        const long long e0 = t0 + (long long)threadIdx.x * 4;
+        int vv[4];
+        unsigned cc[4];
+        bool li[4];
+        unsigned cnt = 0, rows = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const long long e = e0 + q;
+            vv[q] = e < hi ? tlist[e] : -1;
+            cc[q] = vv[q] >= 0 ? (vcnt[vv[q]] & ~kNewBit) : 0u;
+            li[q] = vv[q] >= 0 && (!singles || cc[q] > 1u);
+            cnt += li[q];
+            rows += li[q] ? cc[q] : 0u;
+        }
+        unsigned long long pre, total;
+        __syncthreads();
+        Scan(tmp.scan).ExclusiveSum(((unsigned long long)cnt << 40) | rows, pre, total);
+        unsigned long long u = (base >> 40) + (pre >> 40);
+        unsigned long long r = (base & low40) + (pre & low40);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if (!li[q]) continue;
+            mlist[u] = vv[q];
+            vseg[vv[q]] = (unsigned)r;
+            ++u;
+            r += cc[q];
+        }
+        base += total;
+    }
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
+        ctr->n_list = base >> 40;
+        ctr->rows_seg = base & low40;
+    }
+}
+
+// After a capacity abort: give the voxels activated by the failed attempt
+// their background state (they stay active and are found again by the
+// retry) and clear the per-voxel frame counts.
+template <class TD, class TS>
+__global__ void k_cleanup(const int* __restrict__ tlist, unsigned* vcnt, unsigned* vcur, TD* vt,
+                          TS* mean, TS* beta, int D, double trunc, double prior_beta,
+                          const FrameCtr* __restrict__ ctr) {
+    const long long n = (long long)ctr->n_touched;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int vid = tlist[e];
+        if (vcnt[vid] & kNewBit) {
+            vt[2 * (long long)vid] = (TD)trunc;
+            vt[2 * (long long)vid + 1] = (TD)0;
+            if (mean) {
+                for (int c = 0; c < D; ++c) {
+                    mean[(long long)vid * D + c] = (TS)0;
+                    beta[(long long)vid * D + c] = (TS)prior_beta;
+                }
+            }
+        }
+        vcnt[vid] = 0u;
+        vcur[vid] = 0u;
+    }
+}
+
+template <class TD, class TS>
+svx_status cleanup_t(svx_map* m, cudaStream_t s) {
+    const bool open = m->cfg.sem_kind == SVX_SEM_OPEN;
+    k_cleanup<TD, TS><<<kPersistentBlocks, 256, 0, s>>>(
+        ptr<int>(m->tlist), ptr<unsigned>(m->vcnt), ptr<unsigned>(m->vcur), ptr<TD>(m->vt),
+        open ? ptr<TS>(m->s0) : nullptr, open ? ptr<TS>(m->s1) : nullptr, m->payload_d,
+        m->cfg.truncation, m->cfg.prior_beta, ptr<FrameCtr>(m->ctr));
+    SVX_LAUNCHED();
+    return SVX_OK;
+}
+
+}  // namespace
+
+svx_status launch_resolve(svx_map* m, cudaStream_t s) {
+    k_resolve<<<kPersistentBlocks * 2, kResolveThreads, 0, s>>>(
+        ptr<int>(m->rcnt), ptr<int>(m->rowray), ptr<unsigned long long>(m->rowkey),
+        ptr<int>(m->rowvid), ptr<int4>(m->hash), ptr<int4>(m->bcoord),
+        ptr<unsigned long long>(m->bkey), ptr<unsigned long long>(m->bmask), ptr<int>(m->bslot),
+        ptr<unsigned>(m->vcnt), ptr<unsigned long long>(m->vkey), ptr<int>(m->tlist),
+        ptr<FrameCtr>(m->ctr));
+    SVX_LAUNCHED();
+    return SVX_OK;
+}
+
+svx_status launch_segments(svx_map* m, cudaStream_t s) {
+    unsigned long long* part =
+        reinterpret_cast<unsigned long long*>(ptr<char>(m->partials) + partials_bytes());
+    k_seg_count<<<kSegBlocks, kSegThreads, 0, s>>>(ptr<int>(m->tlist), ptr<unsigned>(m->vcnt), part,
+                                                   ptr<FrameCtr>(m->ctr));
+    SVX_LAUNCHED();
+    k_seg_write<<<kSegBlocks, kSegThreads, 0, s>>>(ptr<int>(m->tlist), ptr<unsigned>(m->vcnt),
+                                                   ptr<unsigned>(m->vseg), part, ptr<int>(m->mlist),
+                                                   ptr<FrameCtr>(m->ctr));
+    SVX_LAUNCHED();
+    return SVX_OK;
+}
+
+svx_status launch_cleanup(svx_map* m, cudaStream_t s) {
+    const bool t64 = m->cfg.tsdf_dtype == SVX_F64, s64 = m->cfg.state_dtype == SVX_F64;
+    if (t64) return s64 ? cleanup_t<double, double>(m, s) : cleanup_t<double, float>(m, s);
+    return s64 ? cleanup_t<float, double>(m, s) : cleanup_t<float, float>(m, s);
+}
+
+size_t segment_partials_bytes() { return sizeof(unsigned long long) * kSegBlocks; }
+
+}  // namespace svx

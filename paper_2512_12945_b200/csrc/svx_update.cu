@@ -1,21 +1,21 @@
-// svx_update.cu -- leaf allocation (K4) fused with the TSDF + semantic update
-// (K5/K6).
+// svx_update.cu -- K4 scatter (+ single-row voxel updates) and K5 the fused
+// TSDF + semantic update of the voxels with several rows.
 //
-// Compiled with -fmad=false.  Every voxel's rows are put back into point
-// order (the reference's (voxel, point, step) order) and reduced
-// sequentially in fp64 exactly like _core.pyx:759-843; the apply arithmetic
-// restates apply_tsdf / apply_closed / apply_open (_pycore.py:399-446)
-// operation for operation, so stored values round identically.
+// Compiled with -fmad=false.  Every voxel's rows are reduced in ascending
+// point order -- the reference's (voxel, point, step) order, since a ray
+// visits a voxel at most once -- with sequential fp64 sums exactly like
+// _core.pyx:759-843; the apply arithmetic restates apply_tsdf /
+// apply_closed / apply_open (_pycore.py:399-446) operation for operation,
+// so stored values round identically.
 //
-// Stage A resolves every touched voxel (leaf find-or-insert with its
-// creation stamp, voxel activation) and updates the ones it can finish:
-//   short  (<= kShortMax rows)   one thread per voxel, register insertion sort
-//   open                         one warp per voxel (lanes own feature dims)
-// Stage B finishes the rest:
-//   long   (<= kSmemMax rows)    one warp per voxel, shared-memory bitonic sort
-//   huge   (> kSmemMax rows)     one warp per voxel, point-index bitmap in global
-//                                scratch streamed in ascending chunks (space
-//                                carving sends every ray through the origin voxel)
+// Execution shapes by rows per voxel:
+//   1      (closed/geometry)  finished by the scatter thread, in ray order
+//   <= 16                      one thread per voxel, register insertion sort
+//   <= 1024                    one warp per voxel, shared-memory bitonic sort
+//   larger                     one warp per voxel, point-index bitmap in global
+//                              scratch streamed in ascending chunks (space
+//                              carving sends every ray through the origin voxel)
+// Open-set voxels always take the warp shapes (lanes own feature dims).
 #include <math.h>
 
 #include "svx_internal.cuh"
@@ -26,10 +26,6 @@ namespace {
 constexpr int kSmemMax = 1024;                   // rows per warp buffer (4 KB)
 constexpr int kWarpsPerCta = 8;
 constexpr int kHugeWarps = 128;                  // warps that share the bitmap scratch
-
-__device__ __forceinline__ int slot_of(long long x, long long y, long long z) {
-    return (int)(((x & 7) << 6) | ((y & 7) << 3) | (z & 7));
-}
 
 // counter += 1 for every converged lane, one atomic per warp; returns this
 // lane's ticket.
@@ -42,79 +38,6 @@ __device__ __forceinline__ unsigned long long warp_ticket(unsigned long long* co
     if (lane == leader) base = atomicAdd(counter, (unsigned long long)__popc(mask));
     base = __shfl_sync(mask, base, leader);
     return base + rank;
-}
-
-// Leaf find-or-insert.  A claimed slot stays BUSY until the new leaf's id,
-// coordinates and creation frame are written; then the id is published.
-__device__ int leaf_find_or_insert(int4* table, long long mask, int a, int b, int c, int frame,
-                                   int4* bcoord, FrameCtr* ctr) {
-    long long pos = (long long)(block_hash(a, b, c) & (unsigned long long)mask);
-    while (true) {
-        // Fast path: one 16-byte L2 read of the slot.  A published id (>= 0)
-        // was written after its key (release fence on the creating side), so
-        // a matching key is final -- almost every lookup ends here without a
-        // fence of its own.
-        const int4 sv = __ldcg(table + pos);
-        if (sv.w >= 0) {
-            if (sv.x == a && sv.y == b && sv.z == c) return sv.w;
-            pos = (pos + 1) & mask;
-            continue;
-        }
-        volatile int* vw = &table[pos].w;
-        int v = sv.w;
-        if (v == kHashEmpty) {
-            int old = atomicCAS((int*)&table[pos].w, kHashEmpty, kHashBusy);
-            if (old == kHashEmpty) {
-                table[pos].x = a;
-                table[pos].y = b;
-                table[pos].z = c;
-                int id = (int)warp_ticket(&ctr->nblocks);
-                bcoord[id] = make_int4(a, b, c, frame);
-                __threadfence();
-                atomicExch((int*)&table[pos].w, id);
-                return id;
-            }
-            v = old;
-        }
-        while (v == kHashBusy) {
-            __nanosleep(20);
-            v = *vw;
-        }
-        __threadfence();
-        volatile int* key = &table[pos].x;
-        if (key[0] == a && key[1] == b && key[2] == c) return v;
-        pos = (pos + 1) & mask;
-    }
-}
-
-struct Maps {
-    int4* table;
-    int4* bcoord;
-    unsigned long long* bkey;
-    unsigned long long* bmask;
-    int* bslot;
-};
-
-// K4 for one voxel: its leaf (allocated in arrival order, stamped with the
-// voxel's frame key when the leaf is new this frame, which yields the
-// first-occurrence order the reference allocates in, _core.pyx:377-420) and
-// its voxel id (activated if new).  Returns vid, negative bit = new voxel.
-__device__ __forceinline__ int resolve_voxel(const Maps& mp, unsigned long long key, long long x,
-                                             long long y, long long z, long long hmask, int frame,
-                                             long long nblocks0, FrameCtr* ctr) {
-    const int id = leaf_find_or_insert(mp.table, hmask, (int)(x >> kLeafLog2),
-                                       (int)(y >> kLeafLog2), (int)(z >> kLeafLog2), frame,
-                                       mp.bcoord, ctr);
-    // leaves created this frame have ids past the frame's starting count
-    if (id >= nblocks0) atomicMin(&mp.bkey[id], key);
-    const int slot = slot_of(x, y, z);
-    int* sp = &mp.bslot[(long long)id * kLeafVolume + slot];
-    int vid = *sp;
-    if (vid >= 0) return vid;
-    vid = (int)warp_ticket(&ctr->nvox);
-    *sp = vid;
-    atomicOr(&mp.bmask[(long long)id * kMaskWords + (slot >> 6)], 1ULL << (slot & 63));
-    return vid | (int)0x80000000;
 }
 
 // Clamped projective distance and weight of one row (row_distances_weights,
@@ -164,8 +87,10 @@ struct Center {
     double x, y, z;
 };
 
-__device__ __forceinline__ Center center_of(long long x, long long y, long long z, double h,
+__device__ __forceinline__ Center center_of(unsigned long long key, const KeyPack& kp, double h,
                                             const PoseParams& pp) {
+    long long x, y, z;
+    unpack_key(key, kp, x, y, z);
     Center c;
     c.x = ((double)x + 0.5) * h - pp.t[0];
     c.y = ((double)y + 0.5) * h - pp.t[1];
@@ -173,28 +98,18 @@ __device__ __forceinline__ Center center_of(long long x, long long y, long long 
     return c;
 }
 
-__device__ __forceinline__ void clear_frame_slot(unsigned long long* fkey, unsigned* fcount,
-                                                 unsigned* fcur, int s) {
-    fkey[s] = kKeyEmpty;
-    fcount[s] = 0u;
-    fcur[s] = 0u;
-}
-
 struct UpdateArgs {
-    const int* ulist;
-    const unsigned long long* ukey;
-    int* gvid;
-    unsigned long long* fkey;
-    unsigned* fcount;
-    const unsigned* foff;
-    unsigned* fcur;
+    const int* mlist;
+    unsigned* vcnt;
+    const unsigned* vseg;
+    unsigned* vcur;
+    const unsigned long long* vkey;
     const int* srid;
     const double4* ray;
     int* longlist;
     int* hugelist;
     unsigned* bitmap;     // kHugeWarps * bm_words
     long long bm_words;
-    Maps maps;
     double h, trunc;
     int wfn;
     int sem_kind, last_wins, C;   // closed
@@ -203,165 +118,120 @@ struct UpdateArgs {
     FrameCtr* ctr;
 };
 
-// ---- stage A, closed / geometry: one thread per voxel ------------------------
+__device__ __forceinline__ void clear_voxel_frame(const UpdateArgs& a, int vid) {
+    a.vcnt[vid] = 0u;
+    a.vcur[vid] = 0u;
+}
 
-// One row of a short segment: its point index and what the update needs of it.
-struct RowData {
-    double4 ray;
-    int rid;
-    int lab;
-};
+// ---- K4: scatter, single-row voxels finished in ray order --------------------------
+// One thread per row.  A voxel with exactly one row needs no ordering: its
+// sums are the row's own (0.0 + w * d exactly as the reference's sequential
+// sum, _core.pyx:793-795), so closed/geometry maps update it right here;
+// rows of other voxels go to their voxel's segment.
+template <class TD, class TC>
+__global__ void __launch_bounds__(256) k_scatter(UpdateArgs a, const int* __restrict__ rcnt,
+                                                 const int* __restrict__ rowray,
+                                                 const unsigned long long* __restrict__ rowkey,
+                                                 const int* __restrict__ rowvid,
+                                                 int* __restrict__ srid, TD* vt, TC* counts) {
+    FrameCtr* ctr = a.ctr;
+    if (ctr->abort | ctr->err_cap) return;
+    const FrameParams& fp = ctr->p;
+    RowSpace rs;
+    rs.maxrows = 0;   // rows are dense in every mode
+    rs.rcnt = rcnt;
+    rs.rowray = rowray;
+    rs.total = (long long)ctr->rows;
+    const KeyPack kp = fp.kp;
+    const PoseParams pp = fp.pp;
+    const int32_t* __restrict__ labels = fp.labels;
+    const bool singles = fp.inline_singles;
+    const bool closed = a.sem_kind == SVX_SEM_CLOSED;
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < rs.total;
+         t += (long long)gridDim.x * blockDim.x) {
+        long long i;
+        if (!row_ray(rs, t, i)) continue;
+        const int vid = rowvid[t];
+        const unsigned c = a.vcnt[vid];
+        if (!singles || (c & ~kNewBit) > 1u) {
+            const unsigned pos = a.vseg[vid] + atomicAdd(&a.vcur[vid], 1u);
+            srid[pos] = (int)i;
+            continue;
+        }
+        const unsigned long long key = rowkey[t];
+        const double4 ry = a.ray[i];
+        const Center cc = center_of(key, kp, a.h, pp);
+        double d, w;
+        row_dw(cc.x, cc.y, cc.z, ry, a.trunc, a.wfn, d, w);
+        apply_tsdf<TD>(vt, vid, (c & kNewBit) != 0u, a.trunc, 0.0 + w, 0.0 + w * d, d, d);
+        if (closed) {
+            const int lab = labels[i];
+            TC* crow = counts + (long long)vid * a.C;
+            if (a.last_wins) {
+                for (int q = 0; q < a.C; ++q) crow[q] = (TC)(q == lab - 1 ? 1 : 0);
+            } else {
+                atomicAdd(&crow[lab - 1], (TC)1);   // integer count: fire-and-forget
+            }
+        }
+        a.vcnt[vid] = 0u;
+    }
+}
+
+// ---- K5 short: one thread per multi-row voxel (closed / geometry) ----------------
 
 template <class TD, class TC>
 __global__ void __launch_bounds__(256) k_update_short(UpdateArgs a, TD* vt, TC* counts) {
     FrameCtr* ctr = a.ctr;
-    if (ctr->abort) return;
-    const long long U = (long long)ctr->n_list;
+    if (ctr->abort | ctr->err_cap) return;
+    const long long L = (long long)ctr->n_list;
     const KeyPack kp = ctr->p.kp;
     const PoseParams pp = ctr->p.pp;
-    const long long hmask = ctr->p.hmask;
-    const long long nblocks0 = ctr->p.nblocks0;
-    const int frame = ctr->p.frame;
     const int32_t* __restrict__ labels = ctr->p.labels;
     const bool closed = a.sem_kind == SVX_SEM_CLOSED;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < U;
-         i += (long long)gridDim.x * blockDim.x) {
-        const unsigned long long key = a.ukey[i];
-        const int s = a.ulist[i];
-        const unsigned k = a.fcount[s];
-        const unsigned base = a.foff[s];
-        // Issue the row loads (point index -> ray, label) before the leaf
-        // resolution so the two dependent chains overlap.  Most LiDAR voxels
-        // have one or two rows; they stay in registers.
-        RowData r0, r1;
-        r0.rid = r1.rid = 0x7fffffff;
-        if (k <= (unsigned)kShortMax) {
-            r0.rid = a.srid[base];
-            if (k > 1) r1.rid = a.srid[base + 1];
-            r0.ray = a.ray[r0.rid];
-            if (closed) r0.lab = labels[r0.rid];
-            if (k > 1) {
-                r1.ray = a.ray[r1.rid];
-                if (closed) r1.lab = labels[r1.rid];
-            }
-        }
-        long long x, y, z;
-        unpack_key(key, kp, x, y, z);
-        const int g = resolve_voxel(a.maps, key, x, y, z, hmask, frame, nblocks0, ctr);
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < L;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int vid = a.mlist[e];
+        const unsigned c = a.vcnt[vid];
+        const unsigned k = c & ~kNewBit;
         if (k > (unsigned)kShortMax) {
-            a.gvid[i] = g;
-            if (k > (unsigned)kSmemMax) a.hugelist[warp_ticket(&ctr->n_huge)] = (int)i;
-            else a.longlist[warp_ticket(&ctr->n_long)] = (int)i;
+            if (k > (unsigned)kSmemMax) a.hugelist[warp_ticket(&ctr->n_huge)] = (int)e;
+            else a.longlist[warp_ticket(&ctr->n_long)] = (int)e;
             continue;
         }
-        const Center c = center_of(x, y, z, a.h, pp);
-        const int vid = g & 0x7fffffff;
-        const bool isnew = g < 0;
-        TC* crow = counts + (long long)vid * a.C;
+        const unsigned base = a.vseg[vid];
+        int r[kShortMax];
+        for (unsigned j = 0; j < k; ++j) {
+            int v = a.srid[base + j];
+            int p = (int)j;
+            while (p > 0 && r[p - 1] > v) {
+                r[p] = r[p - 1];
+                --p;
+            }
+            r[p] = v;
+        }
+        const Center cc = center_of(a.vkey[vid], kp, a.h, pp);
         double sw = 0.0, swd = 0.0, mind = INFINITY, maxd = -INFINITY;
         int last_lab = 0;
-        auto fold = [&](const RowData& rd) {
+        TC* crow = counts + (long long)vid * a.C;
+        for (unsigned j = 0; j < k; ++j) {
+            const int rid = r[j];
             double d, w;
-            row_dw(c.x, c.y, c.z, rd.ray, a.trunc, a.wfn, d, w);
+            row_dw(cc.x, cc.y, cc.z, a.ray[rid], a.trunc, a.wfn, d, w);
             sw += w;
             swd += w * d;
             mind = d < mind ? d : mind;
             maxd = d > maxd ? d : maxd;
             if (closed) {
-                if (a.last_wins) last_lab = rd.lab;
-                else atomicAdd(&crow[rd.lab - 1], (TC)1);   // integer count: fire-and-forget
-            }
-        };
-        if (k <= 2) {
-            if (k == 2 && r1.rid < r0.rid) {
-                RowData t = r0;
-                r0 = r1;
-                r1 = t;
-            }
-            fold(r0);
-            if (k == 2) fold(r1);
-        } else {
-            int r[kShortMax];
-            for (unsigned j = 0; j < k; ++j) {
-                int v = a.srid[base + j];
-                int p = (int)j;
-                while (p > 0 && r[p - 1] > v) {
-                    r[p] = r[p - 1];
-                    --p;
-                }
-                r[p] = v;
-            }
-            for (unsigned j = 0; j < k; ++j) {
-                RowData rd;
-                rd.rid = r[j];
-                rd.ray = a.ray[rd.rid];
-                if (closed) rd.lab = labels[rd.rid];
-                fold(rd);
+                const int lab = labels[rid];
+                if (a.last_wins) last_lab = lab;
+                else atomicAdd(&crow[lab - 1], (TC)1);
             }
         }
-        apply_tsdf<TD>(vt, vid, isnew, a.trunc, sw, swd, mind, maxd);
+        apply_tsdf<TD>(vt, vid, (c & kNewBit) != 0u, a.trunc, sw, swd, mind, maxd);
         if (closed && a.last_wins) {
             for (int q = 0; q < a.C; ++q) crow[q] = (TC)(q == last_lab - 1 ? 1 : 0);
         }
-        clear_frame_slot(a.fkey, a.fcount, a.fcur, s);
-    }
-}
-
-// ---- K3 fused with the update of single-row voxels (bounded, closed/geometry) ----
-// One thread per row slot, in point-major order: the row's voxel key, ray and
-// label are read coalesced.  A voxel with exactly one row needs no ordering:
-// its sums are the row's own (0.0 + w * d exactly as the reference's
-// sequential sum, _core.pyx:793-795), so it is resolved and updated right
-// here; rows of multi-row voxels are dropped into their segments.
-template <class TD, class TC>
-__global__ void __launch_bounds__(256) k_scatter_update(UpdateArgs a, const int* __restrict__ rcnt,
-                                                        const int* __restrict__ rowslot,
-                                                        const unsigned long long* __restrict__ rowkey,
-                                                        int* __restrict__ srid, TD* vt, TC* counts) {
-    FrameCtr* ctr = a.ctr;
-    if (ctr->abort) return;
-    const long long n = ctr->p.n;
-    const int maxrows = ctr->p.maxrows;
-    const KeyPack kp = ctr->p.kp;
-    const PoseParams pp = ctr->p.pp;
-    const long long hmask = ctr->p.hmask;
-    const long long nblocks0 = ctr->p.nblocks0;
-    const int frame = ctr->p.frame;
-    const int32_t* __restrict__ labels = ctr->p.labels;
-    const bool closed = a.sem_kind == SVX_SEM_CLOSED;
-    const long long total = n * maxrows;
-    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
-         t += (long long)gridDim.x * blockDim.x) {
-        const long long i = t / maxrows;
-        const int j = (int)(t - i * maxrows);
-        if (j >= rcnt[i]) continue;
-        const int s = rowslot[t];
-        // speculative loads for the single-row case, overlapping the count read
-        const unsigned long long key = rowkey[t];
-        const double4 ry = a.ray[i];
-        const int lab = closed ? labels[i] : 0;
-        if (a.fcount[s] > 1u) {
-            const unsigned pos = a.foff[s] + atomicAdd(&a.fcur[s], 1u);
-            srid[pos] = (int)i;
-            continue;
-        }
-        long long x, y, z;
-        unpack_key(key, kp, x, y, z);
-        const int g = resolve_voxel(a.maps, key, x, y, z, hmask, frame, nblocks0, ctr);
-        const Center c = center_of(x, y, z, a.h, pp);
-        double d, w;
-        row_dw(c.x, c.y, c.z, ry, a.trunc, a.wfn, d, w);
-        const int vid = g & 0x7fffffff;
-        apply_tsdf<TD>(vt, vid, g < 0, a.trunc, 0.0 + w, 0.0 + w * d, d, d);
-        if (closed) {
-            TC* crow = counts + (long long)vid * a.C;
-            if (a.last_wins) {
-                for (int q = 0; q < a.C; ++q) crow[q] = (TC)(q == lab - 1 ? 1 : 0);
-            } else {
-                atomicAdd(&crow[lab - 1], (TC)1);
-            }
-        }
-        clear_frame_slot(a.fkey, a.fcount, a.fcur, s);
+        clear_voxel_frame(a, vid);
     }
 }
 
@@ -499,75 +369,70 @@ template <class TD, class TC>
 __device__ __forceinline__ void finish_closed(const UpdateArgs& a, TD* vt, TC* crow, int vid,
                                               bool isnew, const TsdfAcc& acc) {
     const int lane = threadIdx.x & 31;
-    if (lane == 0) apply_tsdf<TD>(vt,vid, isnew, a.trunc, acc.sw, acc.swd, acc.mind, acc.maxd);
+    if (lane == 0) apply_tsdf<TD>(vt, vid, isnew, a.trunc, acc.sw, acc.swd, acc.mind, acc.maxd);
     if (a.sem_kind == SVX_SEM_CLOSED && a.last_wins) {
         for (int q = lane; q < a.C; q += 32) crow[q] = (TC)(q == acc.last_lab - 1 ? 1 : 0);
     }
 }
 
-// ---- stage B, closed / geometry: long and huge segments ---------------------------
+// ---- K5 long / huge (closed / geometry): one warp per voxel --------------------
 
 template <class TD, class TC>
 __global__ void __launch_bounds__(32 * kWarpsPerCta) k_update_long(UpdateArgs a, TD* vt,
                                                                    TC* counts) {
     __shared__ int sbuf[kWarpsPerCta][kSmemMax];
     FrameCtr* ctr = a.ctr;
-    if (ctr->abort) return;
+    if (ctr->abort | ctr->err_cap) return;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     int* buf = sbuf[wib];
     const KeyPack kp = ctr->p.kp;
     const PoseParams pp = ctr->p.pp;
     const int32_t* labels = ctr->p.labels;
+    const bool closed = a.sem_kind == SVX_SEM_CLOSED;
     const long long gw = (long long)blockIdx.x * kWarpsPerCta + wib;
     const long long nwarps = (long long)gridDim.x * kWarpsPerCta;
-    unsigned* bm = a.bitmap + (gw % kHugeWarps) * a.bm_words;
     const long long L = (long long)ctr->n_long;
     for (long long t = gw; t < L; t += nwarps) {
-        const int i = a.longlist[t];
-        const int s = a.ulist[i];
-        const unsigned k = a.fcount[s];
-        warp_sort_segment(a.srid, a.foff[s], (int)k, buf);
-        long long x, y, z;
-        unpack_key(a.ukey[i], kp, x, y, z);
-        const Center c = center_of(x, y, z, a.h, pp);
-        const int g = a.gvid[i];
-        const int vid = g & 0x7fffffff;
+        const int vid = a.mlist[a.longlist[t]];
+        const unsigned c = a.vcnt[vid];
+        const unsigned k = c & ~kNewBit;
+        warp_sort_segment(a.srid, a.vseg[vid], (int)k, buf);
+        const Center cc = center_of(a.vkey[vid], kp, a.h, pp);
         TC* crow = counts + (long long)vid * a.C;
         TsdfAcc acc{0.0, 0.0, INFINITY, -INFINITY, 0};
-        warp_tsdf_chunk<TC>(a, labels, buf, (int)k, c, acc, crow, a.sem_kind == SVX_SEM_CLOSED);
-        finish_closed<TD, TC>(a, vt,crow, vid, g < 0, acc);
-        if (lane == 0) clear_frame_slot(a.fkey, a.fcount, a.fcur, s);
+        warp_tsdf_chunk<TC>(a, labels, buf, (int)k, cc, acc, crow, closed);
+        finish_closed<TD, TC>(a, vt, crow, vid, (c & kNewBit) != 0u, acc);
+        __syncwarp();
+        if (lane == 0) clear_voxel_frame(a, vid);
         __syncwarp();
     }
     // huge segments: only the first kHugeWarps warps own bitmap scratch
     if (gw >= kHugeWarps) return;
+    unsigned* bm = a.bitmap + gw * a.bm_words;
     const long long Hn = (long long)ctr->n_huge;
     for (long long t = gw; t < Hn; t += kHugeWarps) {
-        const int i = a.hugelist[t];
-        const int s = a.ulist[i];
-        const unsigned k = a.fcount[s];
+        const int vid = a.mlist[a.hugelist[t]];
+        const unsigned c = a.vcnt[vid];
+        const unsigned k = c & ~kNewBit;
         int minr;
         long long nwords;
-        bitmap_build(a.srid, a.foff[s], k, bm, minr, nwords);
-        long long x, y, z;
-        unpack_key(a.ukey[i], kp, x, y, z);
-        const Center c = center_of(x, y, z, a.h, pp);
-        const int g = a.gvid[i];
-        const int vid = g & 0x7fffffff;
+        bitmap_build(a.srid, a.vseg[vid], k, bm, minr, nwords);
+        const Center cc = center_of(a.vkey[vid], kp, a.h, pp);
         TC* crow = counts + (long long)vid * a.C;
         TsdfAcc acc{0.0, 0.0, INFINITY, -INFINITY, 0};
         for (long long w0 = 0; w0 < nwords; w0 += 32) {
             const int cnt = bitmap_chunk(bm, w0, nwords, minr, buf);
-            if (cnt) warp_tsdf_chunk<TC>(a, labels, buf, cnt, c, acc, crow, a.sem_kind == SVX_SEM_CLOSED);
+            if (cnt) warp_tsdf_chunk<TC>(a, labels, buf, cnt, cc, acc, crow, closed);
             __syncwarp();
         }
-        finish_closed<TD, TC>(a, vt,crow, vid, g < 0, acc);
-        if (lane == 0) clear_frame_slot(a.fkey, a.fcount, a.fcur, s);
+        finish_closed<TD, TC>(a, vt, crow, vid, (c & kNewBit) != 0u, acc);
+        __syncwarp();
+        if (lane == 0) clear_voxel_frame(a, vid);
         __syncwarp();
     }
 }
 
-// ---- open set: one warp per voxel, lanes own feature dimensions ------------------
+// ---- K5 open set: one warp per voxel, lanes own feature dimensions ------------
 
 constexpr int kOpenPer = 8;   // dims per lane per pass (256 dims per pass)
 
@@ -611,34 +476,32 @@ __device__ __forceinline__ void open_chunk(const Fe* __restrict__ feats, int D, 
 
 template <class TD, class TS, class Fe>
 __device__ __forceinline__ void open_voxel(const UpdateArgs& a, const KeyPack& kp,
-                                           const PoseParams& pp, TD* vt, TS* mean,
-                                           TS* beta, const Fe* feats, int i, int s, unsigned k,
-                                           int g, int* buf, unsigned* bm, bool huge) {
+                                           const PoseParams& pp, TD* vt, TS* mean, TS* beta,
+                                           const Fe* feats, int vid, unsigned c, int* buf,
+                                           unsigned* bm, bool huge) {
     const int lane = threadIdx.x & 31;
-    long long x, y, z;
-    unpack_key(a.ukey[i], kp, x, y, z);
-    const Center c = center_of(x, y, z, a.h, pp);
-    const int vid = g & 0x7fffffff;
-    const bool isnew = g < 0;
+    const unsigned k = c & ~kNewBit;
+    const bool isnew = (c & kNewBit) != 0u;
+    const Center cc = center_of(a.vkey[vid], kp, a.h, pp);
     int minr = 0;
     long long nwords = 0;
-    if (huge) bitmap_build(a.srid, a.foff[s], k, bm, minr, nwords);
-    else warp_sort_segment(a.srid, a.foff[s], (int)k, buf);
+    if (huge) bitmap_build(a.srid, a.vseg[vid], k, bm, minr, nwords);
+    else warp_sort_segment(a.srid, a.vseg[vid], (int)k, buf);
     // TSDF sums in point order
     TsdfAcc acc{0.0, 0.0, INFINITY, -INFINITY, 0};
     if (huge) {
         for (long long w0 = 0; w0 < nwords; w0 += 32) {
             const int cnt = bitmap_chunk(bm, w0, nwords, minr, buf);
-            if (cnt) warp_tsdf_chunk<float>(a, nullptr, buf, cnt, c, acc, nullptr, false);
+            if (cnt) warp_tsdf_chunk<float>(a, nullptr, buf, cnt, cc, acc, nullptr, false);
             __syncwarp();
         }
     } else {
-        warp_tsdf_chunk<float>(a, nullptr, buf, (int)k, c, acc, nullptr, false);
+        warp_tsdf_chunk<float>(a, nullptr, buf, (int)k, cc, acc, nullptr, false);
     }
     double w_old = 0.0;
-    if (lane == 0) w_old = apply_tsdf<TD>(vt,vid, isnew, a.trunc, acc.sw, acc.swd, acc.mind, acc.maxd);
+    if (lane == 0) w_old = apply_tsdf<TD>(vt, vid, isnew, a.trunc, acc.sw, acc.swd, acc.mind, acc.maxd);
     w_old = __shfl_sync(0xffffffffu, w_old, 0);
-    // NIG batch update with lambda from the pre-frame weight
+    // NIG batch update with lambda from the pre-frame weight (_pycore.py:438)
     const double nobs = (double)k;
     const double lam = fmax(w_old, a.lambda_floor);
     const double lam_post = lam + nobs;
@@ -661,60 +524,46 @@ __device__ __forceinline__ void open_voxel(const UpdateArgs& a, const KeyPack& k
         }
 #pragma unroll
         for (int q = 0; q < kOpenPer; ++q) {
-            const int cc = base + lane + 32 * q;
-            if (cc < a.D) nig_apply<TS>(mrow, brow, cc, isnew, sz[q], sz2[q], lam, lam_post, coef,
-                                        nobs, b_bg);
+            const int col = base + lane + 32 * q;
+            if (col < a.D) nig_apply<TS>(mrow, brow, col, isnew, sz[q], sz2[q], lam, lam_post, coef,
+                                         nobs, b_bg);
         }
     }
-    if (lane == 0) clear_frame_slot(a.fkey, a.fcount, a.fcur, s);
+    __syncwarp();
+    if (lane == 0) clear_voxel_frame(a, vid);
     __syncwarp();
 }
 
-// stage A, open set: resolve + update every non-huge voxel
+// K5 open: every listed voxel; huge segments are deferred to k_update_open_huge.
 template <class TD, class TS, class Fe>
-__global__ void __launch_bounds__(32 * kWarpsPerCta) k_update_open(UpdateArgs a, TD* vt,
-                                                                   TS* mean, TS* beta) {
+__global__ void __launch_bounds__(32 * kWarpsPerCta) k_update_open(UpdateArgs a, TD* vt, TS* mean,
+                                                                   TS* beta) {
     __shared__ int sbuf[kWarpsPerCta][kSmemMax];
     FrameCtr* ctr = a.ctr;
-    if (ctr->abort) return;
+    if (ctr->abort | ctr->err_cap) return;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const long long U = (long long)ctr->n_list;
+    const long long L = (long long)ctr->n_list;
     const KeyPack kp = ctr->p.kp;
     const PoseParams pp = ctr->p.pp;
-    const long long hmask = ctr->p.hmask;
-    const int frame = ctr->p.frame;
     const Fe* feats = (const Fe*)ctr->p.feats;
-    for (long long i = (long long)blockIdx.x * kWarpsPerCta + wib; i < U;
-         i += (long long)gridDim.x * kWarpsPerCta) {
-        const int s = a.ulist[i];
-        const unsigned k = a.fcount[s];
-        int g = 0;
-        if (lane == 0) {
-            const unsigned long long key = a.ukey[i];
-            long long x, y, z;
-            unpack_key(key, kp, x, y, z);
-            g = resolve_voxel(a.maps, key, x, y, z, hmask, frame, ctr->p.nblocks0, ctr);
-        }
-        g = __shfl_sync(0xffffffffu, g, 0);
-        if (k > (unsigned)kSmemMax) {
-            if (lane == 0) {
-                a.gvid[i] = g;
-                a.hugelist[atomicAdd(&ctr->n_huge, 1ULL)] = (int)i;
-            }
+    for (long long e = (long long)blockIdx.x * kWarpsPerCta + wib; e < L;
+         e += (long long)gridDim.x * kWarpsPerCta) {
+        const int vid = a.mlist[e];
+        const unsigned c = a.vcnt[vid];
+        if ((c & ~kNewBit) > (unsigned)kSmemMax) {
+            if (lane == 0) a.hugelist[atomicAdd(&ctr->n_huge, 1ULL)] = (int)e;
             continue;
         }
-        open_voxel<TD, TS, Fe>(a, kp, pp, vt,mean, beta, feats, (int)i, s, k, g, sbuf[wib],
-                               nullptr, false);
+        open_voxel<TD, TS, Fe>(a, kp, pp, vt, mean, beta, feats, vid, c, sbuf[wib], nullptr, false);
     }
 }
 
-// stage B, open set: huge segments
 template <class TD, class TS, class Fe>
 __global__ void __launch_bounds__(32 * kWarpsPerCta) k_update_open_huge(UpdateArgs a, TD* vt,
                                                                         TS* mean, TS* beta) {
     __shared__ int sbuf[kWarpsPerCta][kSmemMax];
     FrameCtr* ctr = a.ctr;
-    if (ctr->abort) return;
+    if (ctr->abort | ctr->err_cap) return;
     const int wib = threadIdx.x >> 5;
     const long long gw = (long long)blockIdx.x * kWarpsPerCta + wib;
     unsigned* bm = a.bitmap + gw * a.bm_words;
@@ -723,10 +572,9 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) k_update_open_huge(UpdateAr
     const PoseParams pp = ctr->p.pp;
     const Fe* feats = (const Fe*)ctr->p.feats;
     for (long long t = gw; t < Hn; t += (long long)gridDim.x * kWarpsPerCta) {
-        const int i = a.hugelist[t];
-        const int s = a.ulist[i];
-        open_voxel<TD, TS, Fe>(a, kp, pp, vt,mean, beta, feats, i, s, a.fcount[s], a.gvid[i],
-                               sbuf[wib], bm, true);
+        const int vid = a.mlist[a.hugelist[t]];
+        open_voxel<TD, TS, Fe>(a, kp, pp, vt, mean, beta, feats, vid, a.vcnt[vid], sbuf[wib], bm,
+                               true);
     }
 }
 
@@ -748,24 +596,17 @@ __global__ void k_rehash(int64_t nblocks, const int4* __restrict__ bcoord, int4*
 
 UpdateArgs make_args(svx_map* m) {
     UpdateArgs a;
-    a.ulist = ptr<int>(m->ulist);
-    a.ukey = ptr<unsigned long long>(m->ukey);
-    a.gvid = ptr<int>(m->gvid);
-    a.fkey = ptr<unsigned long long>(m->fkey);
-    a.fcount = ptr<unsigned>(m->fcount);
-    a.foff = ptr<unsigned>(m->foff);
-    a.fcur = ptr<unsigned>(m->fcur);
+    a.mlist = ptr<int>(m->mlist);
+    a.vcnt = ptr<unsigned>(m->vcnt);
+    a.vseg = ptr<unsigned>(m->vseg);
+    a.vcur = ptr<unsigned>(m->vcur);
+    a.vkey = ptr<unsigned long long>(m->vkey);
     a.srid = ptr<int>(m->srid);
     a.ray = ptr<double4>(m->ray);
     a.longlist = ptr<int>(m->longlist);
     a.hugelist = ptr<int>(m->longlist) + m->ucap;
     a.bitmap = ptr<unsigned>(m->bitmap);
     a.bm_words = (m->npts_cap + 31) / 32 + 1;
-    a.maps.table = ptr<int4>(m->hash);
-    a.maps.bcoord = ptr<int4>(m->bcoord);
-    a.maps.bkey = ptr<unsigned long long>(m->bkey);
-    a.maps.bmask = ptr<unsigned long long>(m->bmask);
-    a.maps.bslot = ptr<int>(m->bslot);
     a.h = m->cfg.voxel_size;
     a.trunc = m->cfg.truncation;
     a.wfn = m->cfg.weight_fn;
@@ -781,6 +622,15 @@ UpdateArgs make_args(svx_map* m) {
 
 constexpr int kShortBlocks = 148 * 8;
 constexpr int kLongBlocks = 148 * 4;
+
+template <class TD, class TC>
+svx_status scatter_t(svx_map* m, cudaStream_t s) {
+    k_scatter<TD, TC><<<kPersistentBlocks * 2, 256, 0, s>>>(
+        make_args(m), ptr<int>(m->rcnt), ptr<int>(m->rowray), ptr<unsigned long long>(m->rowkey),
+        ptr<int>(m->rowvid), ptr<int>(m->srid), ptr<TD>(m->vt), ptr<TC>(m->s0));
+    SVX_LAUNCHED();
+    return SVX_OK;
+}
 
 template <class TD, class TC>
 svx_status closed_a(svx_map* m, cudaStream_t s) {
@@ -831,19 +681,10 @@ svx_status stage_td(svx_map* m, int feats_f64, bool b, cudaStream_t s) {
 
 }  // namespace
 
-template <class TD, class TC>
-static svx_status scatter_update_t(svx_map* m, cudaStream_t s) {
-    k_scatter_update<TD, TC><<<kPersistentBlocks * 2, 256, 0, s>>>(
-        make_args(m), ptr<int>(m->rcnt), ptr<int>(m->rowslot), ptr<unsigned long long>(m->rowkey),
-        ptr<int>(m->srid), ptr<TD>(m->vt), ptr<TC>(m->s0));
-    SVX_LAUNCHED();
-    return SVX_OK;
-}
-
-svx_status launch_scatter_update(svx_map* m, cudaStream_t s) {
+svx_status launch_scatter(svx_map* m, cudaStream_t s) {
     const bool t64 = m->cfg.tsdf_dtype == SVX_F64, c64 = m->cfg.count_dtype == SVX_F64;
-    if (t64) return c64 ? scatter_update_t<double, double>(m, s) : scatter_update_t<double, float>(m, s);
-    return c64 ? scatter_update_t<float, double>(m, s) : scatter_update_t<float, float>(m, s);
+    if (t64) return c64 ? scatter_t<double, double>(m, s) : scatter_t<double, float>(m, s);
+    return c64 ? scatter_t<float, double>(m, s) : scatter_t<float, float>(m, s);
 }
 
 svx_status launch_update_a(svx_map* m, int feats_f64, cudaStream_t s) {
