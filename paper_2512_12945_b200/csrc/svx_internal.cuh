@@ -92,6 +92,8 @@ struct FrameCtr {
     unsigned long long band_hits;   // rows emitted before the w <= 0 drop
     unsigned long long rows;        // rows kept (w > 0)
     unsigned long long rows_alloc;  // dense row slots handed out by the tile walk
+    unsigned walk_done;             // walk CTAs finished (the last one runs the gate)
+    unsigned pad0;
     unsigned long long n_touched;   // unique voxels of the frame (U)
     unsigned long long n_list;      // voxels listed for segment updates
     unsigned long long rows_seg;    // rows placed in segments

@@ -226,6 +226,25 @@ __device__ __forceinline__ bool prepare_ray(long long i, const FrameParams& fp, 
     return keep;
 }
 
+template <int kThreads>
+__device__ void gate_body(const MarchPartial* __restrict__ parts, int nparts, FrameCtr* ctr);
+
+// Every CTA of a walk publishes its partial; the last one to finish runs the
+// gate over all of them.
+template <int kThreads>
+__device__ __forceinline__ void finish_walk(const Tally& t, MarchPartial* partials, FrameCtr* ctr) {
+    write_partial<kThreads>(t, partials + blockIdx.x);
+    __shared__ bool s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(&ctr->walk_done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (s_last) {
+        __threadfence();
+        gate_body<kThreads>(partials, gridDim.x, ctr);
+    }
+}
+
 // K1 (bounded bands): compute-only walk over 128-ray tiles.  Each ray's row
 // keys are staged in shared memory; a block scan packs the tile's rows and
 // one atomic per tile reserves their place in the dense row arrays, which
@@ -313,7 +332,7 @@ __global__ void __launch_bounds__(kTileRays) k_walk(MarchParams mp, int sem_kind
         }
         __syncthreads();
     }
-    write_partial<kTileRays>(t, partials + blockIdx.x);
+    finish_walk<kTileRays>(t, partials, ctr);
 }
 
 
@@ -326,7 +345,7 @@ __global__ void __launch_bounds__(kMarchThreads) k_walk_count(MarchParams mp, in
                                                               double4* __restrict__ ray,
                                                               int* __restrict__ rcnt,
                                                               MarchPartial* __restrict__ partials,
-                                                              const FrameCtr* __restrict__ ctr) {
+                                                              FrameCtr* __restrict__ ctr) {
     const FrameParams fp = ctr->p;
     const long long n = fp.n;
     const double ox = fp.pp.t[0], oy = fp.pp.t[1], oz = fp.pp.t[2];
@@ -361,7 +380,7 @@ __global__ void __launch_bounds__(kMarchThreads) k_walk_count(MarchParams mp, in
         ray[i] = r;
         rcnt[i] = rows;
     }
-    write_partial<kMarchThreads>(t, partials + blockIdx.x);
+    finish_walk<kMarchThreads>(t, partials, ctr);
 }
 
 // K1 (dense mode), pass 2: re-walk and write each kept row at its scanned offset.
@@ -394,10 +413,11 @@ __global__ void __launch_bounds__(kMarchThreads) k_walk_write(MarchParams mp,
 // the frame may mutate the map -- the reference's checks before any
 // allocation (_core.pyx:661-712, :386-387) plus the dense row capacity.  The
 // host reports the reason after the frame.
-__global__ void __launch_bounds__(256) k_gate(const MarchPartial* __restrict__ parts, int nparts,
-                                              FrameCtr* ctr) {
-    using RU = cub::BlockReduce<unsigned long long, 256>;
-    using RL = cub::BlockReduce<long long, 256>;
+// Run by the last CTA of the walk to finish (no separate launch).
+template <int kThreads>
+__device__ void gate_body(const MarchPartial* __restrict__ parts, int nparts, FrameCtr* ctr) {
+    using RU = cub::BlockReduce<unsigned long long, kThreads>;
+    using RL = cub::BlockReduce<long long, kThreads>;
     __shared__ union {
         typename RU::TempStorage u;
         typename RL::TempStorage l;
@@ -405,7 +425,7 @@ __global__ void __launch_bounds__(256) k_gate(const MarchPartial* __restrict__ p
     unsigned long long v[7] = {0, 0, 0, 0, 0, 0, 0};
     long long mn[3] = {LLONG_MAX, LLONG_MAX, LLONG_MAX}, mx[3] = {LLONG_MIN, LLONG_MIN, LLONG_MIN};
     int errs = 0;
-    for (int b = threadIdx.x; b < nparts; b += 256) {
+    for (int b = threadIdx.x; b < nparts; b += kThreads) {
         const MarchPartial& p = parts[b];
         v[0] += p.nonfinite; v[1] += p.range; v[2] += p.degenerate; v[3] += p.bad_label;
         v[4] += p.used; v[5] += p.band_hits; v[6] += p.rows;
@@ -431,11 +451,11 @@ __global__ void __launch_bounds__(256) k_gate(const MarchPartial* __restrict__ p
         __syncthreads();
     }
     errs = __reduce_or_sync(0xffffffffu, (unsigned)errs);
-    __shared__ int s_err[8];
+    __shared__ int s_err[kThreads / 32];
     if ((threadIdx.x & 31) == 0) s_err[threadIdx.x >> 5] = errs;
     __syncthreads();
     if (threadIdx.x != 0) return;
-    for (int w = 1; w < 8; ++w) errs |= s_err[w];
+    for (int w = 1; w < kThreads / 32; ++w) errs |= s_err[w];
     if (errs & 1) ctr->err_budget = 1;
     if (errs & 2) ctr->err_pack = 1;
     if (errs & 8) ctr->err_rows = 1;
@@ -465,8 +485,6 @@ svx_status march_t(svx_map* m, cudaStream_t s) {
             mp, m->cfg.sem_kind, m->cfg.num_classes, m->payload_d, ptr<double4>(m->ray),
             ptr<int>(m->rcnt), ptr<unsigned long long>(m->rowkey), ptr<int>(m->rowray), parts, dc);
         SVX_LAUNCHED();
-        k_gate<<<1, 256, 0, s>>>(parts, kMarchBlocks, dc);
-        SVX_LAUNCHED();
         return SVX_OK;
     }
     k_walk_count<P, Fe><<<kMarchBlocks, kMarchThreads, 0, s>>>(
@@ -477,8 +495,6 @@ svx_status march_t(svx_map* m, cudaStream_t s) {
     SVX_CUDA(cub::DeviceScan::ExclusiveSum(m->cubtmp.p, tmp, ptr<int>(m->rcnt),
                                            ptr<long long>(m->roff), (int)m->npts_cap, s));
     count_launch();
-    k_gate<<<1, 256, 0, s>>>(parts, kMarchBlocks, dc);
-    SVX_LAUNCHED();
     k_walk_write<<<kMarchBlocks, kMarchThreads, 0, s>>>(
         mp, ptr<double4>(m->ray), ptr<int>(m->rcnt), ptr<long long>(m->roff),
         ptr<unsigned long long>(m->rowkey), ptr<int>(m->rowray), dc);

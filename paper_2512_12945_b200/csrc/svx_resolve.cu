@@ -49,6 +49,22 @@ __device__ __forceinline__ unsigned long long warp_ticket(unsigned long long* co
     return base + rank;
 }
 
+// 16-byte volatile store / load of a hash slot (one transaction each).
+__device__ __forceinline__ void st_slot(int4* p, int4 v) {
+    asm volatile("st.volatile.global.v4.s32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
+__device__ __forceinline__ int4 ld_slot(const int4* p) {
+    int4 v;
+    asm volatile("ld.volatile.global.v4.s32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p)
+                 : "memory");
+    return v;
+}
+
 // Leaf find-or-insert.  A claimed slot stays BUSY until the new leaf's id,
 // coordinates and creation frame are written; then the id is published.
 // Returns -1 (and sets err_cap) when the leaf pool is full.
@@ -76,12 +92,10 @@ __device__ int leaf_find_or_insert(int4* table, long long mask, int a, int b, in
                     atomicOr(&ctr->err_cap, 1);
                     return -1;
                 }
-                table[pos].x = a;
-                table[pos].y = b;
-                table[pos].z = c;
                 bcoord[id] = make_int4(a, b, c, frame);
-                __threadfence();
-                atomicExch((int*)&table[pos].w, (int)id);
+                // publish key and id with one 16-byte store: a reader sees the
+                // slot either BUSY or complete (no fence on the creating side)
+                st_slot(table + pos, make_int4(a, b, c, (int)id));
                 return (int)id;
             }
             v = old;
@@ -94,108 +108,162 @@ __device__ int leaf_find_or_insert(int4* table, long long mask, int a, int b, in
             atomicOr(&ctr->err_cap, 1);
             return -1;
         }
-        __threadfence();
-        volatile int* key = &table[pos].x;
-        if (key[0] == a && key[1] == b && key[2] == c) return v;
+        const int4 full = ld_slot(table + pos);
+        if (full.x == a && full.y == b && full.z == c) return full.w;
         pos = (pos + 1) & mask;
     }
 }
 
-// Voxel find-or-activate inside a leaf (GridCore.activate_slot semantics,
-// _core.pyx:312-322).  A new voxel is marked in its frame count (kNewBit) so
-// the update uses background state (grid.py:37-77).  Returns -1 when the
-// voxel pool is full.
-__device__ int voxel_find_or_alloc(int* bslot, unsigned long long* bmask, long long id, int slot,
-                                   long long vcap, unsigned* vcnt, FrameCtr* ctr) {
-    int* sp = &bslot[id * kLeafVolume + slot];
-    int v = __ldcg(sp);
-    if (v >= 0) return v;
-    if (v == -1) {
-        const int old = atomicCAS(sp, -1, -2);
-        if (old == -1) {
-            const long long vid = (long long)warp_ticket(&ctr->nvox);
-            if (vid >= vcap) {
-                atomicExch(sp, -1);
-                atomicOr(&ctr->err_cap, 1);
-                return -1;
-            }
-            atomicOr(&vcnt[vid], kNewBit);
-            atomicOr(&bmask[id * kMaskWords + (slot >> 6)], 1ULL << (slot & 63));
-            __threadfence();
-            atomicExch(sp, (int)vid);
-            return (int)vid;
-        }
-        v = old;
-    }
-    volatile int* vsp = sp;
-    while (v == -2) {
-        __nanosleep(20);
-        v = *vsp;
-    }
-    if (v < 0) atomicOr(&ctr->err_cap, 1);
-    return v;
-}
-
-// K2: one thread per row.  Lanes that hit the same voxel elect one leader
-// (one lookup, one count of popc(peers)); voxel leaders that share a leaf
-// elect one leaf lookup.
+// K2: rows -> voxel ids, in CTA-synchronous tiles of 256 rows so that every
+// allocation counter (leaves, voxels, touched list) is bumped once per tile
+// after a block scan -- never per thread.  Within a warp, lanes that hit the
+// same voxel elect one leader (one lookup, one count of popc(peers)), and
+// voxel leaders that share a leaf elect one leaf lookup.  A slot claimed by
+// another CTA (BUSY) is waited for after this tile's own claims are
+// published, so no thread ever waits across a barrier.
 __global__ void __launch_bounds__(kResolveThreads) k_resolve(
-    const int* __restrict__ rcnt, const int* __restrict__ rowray,
     const unsigned long long* __restrict__ rowkey, int* __restrict__ rowvid, int4* table,
     int4* bcoord, unsigned long long* bkey, unsigned long long* bmask, int* bslot, unsigned* vcnt,
     unsigned long long* __restrict__ vkey, int* __restrict__ tlist, FrameCtr* ctr) {
-    if (ctr->abort | ctr->err_cap) return;
+    using Scan = cub::BlockScan<int, kResolveThreads>;
+    __shared__ typename Scan::TempStorage scan_tmp;
+    __shared__ unsigned long long s_base;
+    if (ctr->abort) return;
     const FrameParams& fp = ctr->p;
-    RowSpace rs;
-    rs.maxrows = 0;   // rows are dense in every mode
-    rs.rcnt = rcnt;
-    rs.rowray = rowray;
-    rs.total = (long long)ctr->rows;
+    const long long total = (long long)ctr->rows;
     const KeyPack kp = fp.kp;
     const long long hmask = fp.hmask, bcap = fp.bcap, vcap = fp.vcap, nblocks0 = fp.nblocks0;
     const int frame = fp.frame;
     const int lane = threadIdx.x & 31;
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    const long long total_r = (rs.total + 31) & ~31LL;   // warp-uniform trip count
-    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total_r; t += stride) {
-        long long i = 0;
-        bool valid = t < rs.total && row_ray(rs, t, i);
+    const unsigned full = 0xffffffffu;
+    for (long long tile = blockIdx.x; tile * kResolveThreads < total; tile += gridDim.x) {
+        const long long t = tile * kResolveThreads + threadIdx.x;
+        const bool valid = t < total;
         const unsigned long long key = valid ? rowkey[t] : kKeyEmpty;
-        valid = valid && key != kKeyEmpty;
         long long x = 0, y = 0, z = 0;
         if (valid) unpack_key(key, kp, x, y, z);
-        const unsigned full = 0xffffffffu;
         const unsigned vpeers = __match_any_sync(full, valid ? key : (kKeyEmpty ^ (unsigned long long)lane));
         const int vleader = __ffs(vpeers) - 1;
         const bool is_vl = valid && lane == vleader;
         // exact leaf identity: leaf coords relative to the base's leaf, 19 bits each
+        const int la = (int)(x >> kLeafLog2), lb = (int)(y >> kLeafLog2), lc = (int)(z >> kLeafLog2);
         const unsigned long long lkey =
-            is_vl ? (((unsigned long long)((x >> kLeafLog2) - (kp.base[0] >> kLeafLog2)) << 38) |
-                     ((unsigned long long)((y >> kLeafLog2) - (kp.base[1] >> kLeafLog2)) << 19) |
-                     (unsigned long long)((z >> kLeafLog2) - (kp.base[2] >> kLeafLog2)))
+            is_vl ? (((unsigned long long)(la - (kp.base[0] >> kLeafLog2)) << 38) |
+                     ((unsigned long long)(lb - (kp.base[1] >> kLeafLog2)) << 19) |
+                     (unsigned long long)(lc - (kp.base[2] >> kLeafLog2)))
                   : (~0ULL ^ (unsigned long long)lane);
         const unsigned lpeers = __match_any_sync(full, lkey);
         const int lleader = __ffs(lpeers) - 1;
-        int id = -1;
-        if (is_vl && lane == lleader) {
-            id = leaf_find_or_insert(table, hmask, (int)(x >> kLeafLog2), (int)(y >> kLeafLog2),
-                                     (int)(z >> kLeafLog2), frame, bcap, bcoord, ctr);
+        const bool is_ll = is_vl && lane == lleader;
+
+        // ---- leaves: find, or claim an empty slot; ids for the tile's claims
+        int id = -1, lstate = 0;   // 1 = claimed here, 2 = another CTA's claim
+        long long lpos = 0;
+        if (is_ll) {
+            lpos = (long long)(block_hash(la, lb, lc) & (unsigned long long)hmask);
+            while (true) {
+                const int4 sv = __ldcg(table + lpos);
+                if (sv.w >= 0) {
+                    if (sv.x == la && sv.y == lb && sv.z == lc) { id = sv.w; break; }
+                    lpos = (lpos + 1) & hmask;
+                    continue;
+                }
+                if (sv.w == kHashBusy) { lstate = 2; break; }
+                const int old = atomicCAS(&table[lpos].w, kHashEmpty, kHashBusy);
+                if (old == kHashEmpty) { lstate = 1; break; }
+                // lost the race for this slot: look at it again
+            }
+        }
+        int rank, cnt;
+        Scan(scan_tmp).ExclusiveSum(lstate == 1 ? 1 : 0, rank, cnt);
+        if (threadIdx.x == 0 && cnt) s_base = atomicAdd(&ctr->nblocks, (unsigned long long)cnt);
+        __syncthreads();
+        if (lstate == 1) {
+            const long long nid = (long long)s_base + rank;
+            if (nid >= bcap) {
+                atomicExch(&table[lpos].w, kHashEmpty);
+                atomicOr(&ctr->err_cap, 1);
+            } else {
+                bcoord[nid] = make_int4(la, lb, lc, frame);
+                st_slot(table + lpos, make_int4(la, lb, lc, (int)nid));   // key + id in one store
+                id = (int)nid;
+            }
+        }
+        __syncthreads();
+        if (lstate == 2) {   // another CTA is publishing this slot (maybe another key)
+            volatile int* vw = &table[lpos].w;
+            int v = *vw;
+            while (v == kHashBusy) {
+                __nanosleep(32);
+                v = *vw;
+            }
+            const int4 sv = ld_slot(table + lpos);
+            if (v >= 0 && sv.x == la && sv.y == lb && sv.z == lc) id = v;
+            else id = leaf_find_or_insert(table, hmask, la, lb, lc, frame, bcap, bcoord, ctr);
         }
         id = __shfl_sync(full, id, lleader);
-        int vid = -1;
+
+        // ---- voxels: find, or claim an inactive slot; ids for the tile's claims
+        int vid = -1, vstate = 0;
+        int* sp = nullptr;
+        const int slot = slot_of(x, y, z);   // GridCore.activate_slot, _core.pyx:312-322
         if (is_vl && id >= 0) {
             if (id >= nblocks0) atomicMin(&bkey[id], key);
-            vid = voxel_find_or_alloc(bslot, bmask, id, slot_of(x, y, z), vcap, vcnt, ctr);
-            if (vid >= 0) {
-                const unsigned c = atomicAdd(&vcnt[vid], (unsigned)__popc(vpeers));
-                if ((c & ~kNewBit) == 0u) {
-                    vkey[vid] = key;
-                    tlist[warp_ticket(&ctr->n_touched)] = vid;
-                }
+            sp = &bslot[(long long)id * kLeafVolume + slot];
+            int v = __ldcg(sp);
+            if (v == -1) {
+                v = atomicCAS(sp, -1, -2);
+                if (v == -1) vstate = 1;
             }
+            if (vstate == 0) {
+                if (v >= 0) vid = v;
+                else vstate = 2;   // another CTA claimed it
+            }
+        }
+        Scan(scan_tmp).ExclusiveSum(vstate == 1 ? 1 : 0, rank, cnt);
+        if (threadIdx.x == 0 && cnt) s_base = atomicAdd(&ctr->nvox, (unsigned long long)cnt);
+        __syncthreads();
+        bool created = false;
+        if (vstate == 1) {
+            const long long nv = (long long)s_base + rank;
+            if (nv >= vcap) {
+                atomicExch(sp, -1);
+                atomicOr(&ctr->err_cap, 1);
+            } else {
+                atomicOr(&bmask[(long long)id * kMaskWords + (slot >> 6)], 1ULL << (slot & 63));
+                atomicExch(sp, (int)nv);
+                vid = (int)nv;
+                created = true;
+            }
+        }
+        __syncthreads();
+        if (vstate == 2) {
+            volatile int* vsp = sp;
+            int v = *vsp;
+            while (v == -2) {
+                __nanosleep(32);
+                v = *vsp;
+            }
+            if (v >= 0) vid = v;
+            else atomicOr(&ctr->err_cap, 1);
+        }
+
+        // ---- counts; the voxel's first toucher this frame lists it
+        bool first = false;
+        if (is_vl && vid >= 0) {
+            const unsigned c = atomicAdd(&vcnt[vid], (unsigned)__popc(vpeers) + (created ? kNewBit : 0u));
+            first = (c & ~kNewBit) == 0u;
+        }
+        Scan(scan_tmp).ExclusiveSum(first ? 1 : 0, rank, cnt);
+        if (threadIdx.x == 0 && cnt) s_base = atomicAdd(&ctr->n_touched, (unsigned long long)cnt);
+        __syncthreads();
+        if (first) {
+            vkey[vid] = key;
+            tlist[s_base + rank] = vid;
         }
         vid = __shfl_sync(full, vid, vleader);
         if (valid) rowvid[t] = vid;
+        __syncthreads();
     }
 }
 
@@ -331,9 +399,8 @@ svx_status cleanup_t(svx_map* m, cudaStream_t s) {
 }  // namespace
 
 svx_status launch_resolve(svx_map* m, cudaStream_t s) {
-    k_resolve<<<kPersistentBlocks * 2, kResolveThreads, 0, s>>>(
-        ptr<int>(m->rcnt), ptr<int>(m->rowray), ptr<unsigned long long>(m->rowkey),
-        ptr<int>(m->rowvid), ptr<int4>(m->hash), ptr<int4>(m->bcoord),
+    k_resolve<<<kPersistentBlocks, kResolveThreads, 0, s>>>(
+        ptr<unsigned long long>(m->rowkey), ptr<int>(m->rowvid), ptr<int4>(m->hash), ptr<int4>(m->bcoord),
         ptr<unsigned long long>(m->bkey), ptr<unsigned long long>(m->bmask), ptr<int>(m->bslot),
         ptr<unsigned>(m->vcnt), ptr<unsigned long long>(m->vkey), ptr<int>(m->tlist),
         ptr<FrameCtr>(m->ctr));
