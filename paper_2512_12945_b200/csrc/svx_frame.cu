@@ -110,7 +110,7 @@ static svx_status reserve_frame(svx_map* m, int64_t n, cudaStream_t s) {
     m->ucap = (uint64_t)rows;
     SVX_TRY(ensure(m->ray, sizeof(double4) * m->npts_cap, s));
     SVX_TRY(ensure(m->rcnt, sizeof(int) * m->npts_cap, s));
-    SVX_TRY(ensure(m->partials, partials_bytes() + segment_partials_bytes(), s));
+    SVX_TRY(ensure(m->partials, partials_bytes() + segment_status_bytes(m->ucap), s, false, 0));
     SVX_TRY(ensure(m->rowkey, sizeof(unsigned long long) * rows, s));
     SVX_TRY(ensure(m->rowvid, sizeof(int) * rows, s));
     SVX_TRY(ensure(m->tlist, sizeof(int) * rows, s));
@@ -318,6 +318,7 @@ svx_status integrate_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n
         p.frame = (int)m->frames;
         p.maxrows = m->maxrows;
         p.inline_singles = inline_singles(m);
+        p.seq = ++m->seq;
 
         SVX_TRY(run_frame(m, pts_f64, feats_f64, s));
 

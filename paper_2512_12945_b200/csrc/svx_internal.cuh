@@ -69,7 +69,7 @@ struct FrameParams {
     int frame;                 // creation stamp for new leaves
     int maxrows;               // row slots per ray; 0 = dense rows (two-pass walk)
     int inline_singles;        // single-row voxels updated in the scatter (closed/geometry)
-    int pad;
+    unsigned seq;              // launch sequence number (epoch of the segment-scan status)
 };
 
 // Per-CTA partial counters of the march, reduced by the gate (no
@@ -93,7 +93,7 @@ struct FrameCtr {
     unsigned long long rows;        // rows kept (w > 0)
     unsigned long long rows_alloc;  // dense row slots handed out by the tile walk
     unsigned walk_done;             // walk CTAs finished (the last one runs the gate)
-    unsigned pad0;
+    unsigned seg_tiles;             // segment-scan tiles claimed
     unsigned long long n_touched;   // unique voxels of the frame (U)
     unsigned long long n_list;      // voxels listed for segment updates
     unsigned long long rows_seg;    // rows placed in segments
@@ -172,6 +172,7 @@ struct svx_map {
     svx::DevBuf vt, s0, s1;                  int64_t vcap = 0, nvox = 0;  // vt: {d, w} per voxel
     svx::DevBuf vcnt, vseg, vcur, vkey;      // per-voxel frame state (see FrameCtr)
     int64_t frames = 0;
+    unsigned seq = 0;   // frame launches so far (attempts included)
     // per-frame scratch
     svx::DevBuf in_pts, in_lab, in_feat;
     svx::DevBuf ray, rcnt, roff, rowkey, rowvid, rowray, partials;
@@ -304,7 +305,7 @@ size_t partials_bytes();
 svx_status launch_resolve(svx_map* m, cudaStream_t s);
 svx_status launch_segments(svx_map* m, cudaStream_t s);
 svx_status launch_cleanup(svx_map* m, cudaStream_t s);   // undo a capacity-aborted attempt
-size_t segment_partials_bytes();
+size_t segment_status_bytes(unsigned long long ucap);
 size_t scan_temp_bytes(int64_t n);
 // Single-row voxels of closed/geometry frames are updated inline by the
 // scatter pass; open-set voxels always go through segments.

@@ -252,7 +252,7 @@ __device__ __forceinline__ void finish_walk(const Tally& t, MarchPartial* partia
 constexpr int kTileRays = 128;
 
 template <class P, class Fe>
-__global__ void __launch_bounds__(kTileRays) k_walk(MarchParams mp, int sem_kind, int num_classes,
+__global__ void __launch_bounds__(kTileRays, 4) k_walk(MarchParams mp, int sem_kind, int num_classes,
                                                     int D, double4* __restrict__ ray,
                                                     int* __restrict__ rcnt,
                                                     unsigned long long* __restrict__ rowkey,
@@ -262,13 +262,13 @@ __global__ void __launch_bounds__(kTileRays) k_walk(MarchParams mp, int sem_kind
     using Scan = cub::BlockScan<int, kTileRays>;
     __shared__ typename Scan::TempStorage scan_tmp;
     __shared__ unsigned long long s_base;
-    extern __shared__ unsigned long long s_keys[];   // kTileRays * maxrows keys, then ray ids
+    __shared__ int s_off[kTileRays];
+    extern __shared__ unsigned long long s_keys[];   // kTileRays * maxrows keys, then row owners
     const FrameParams fp = ctr->p;
     const long long n = fp.n;
     const int maxrows = fp.maxrows;
     const unsigned long long rcap = fp.rcap;
-    int* s_ray = reinterpret_cast<int*>(s_keys + (size_t)kTileRays * maxrows);
-    unsigned long long* s_pack = s_keys;   // packed rows reuse the key area in place
+    unsigned char* s_own = reinterpret_cast<unsigned char*>(s_keys + (size_t)kTileRays * maxrows);
     const double ox = fp.pp.t[0], oy = fp.pp.t[1], oz = fp.pp.t[2];
     Tally t;
     const long long tiles = (n + kTileRays - 1) / kTileRays;
@@ -308,24 +308,20 @@ __global__ void __launch_bounds__(kTileRays) k_walk(MarchParams mp, int sem_kind
         }
         int off, total;
         Scan(scan_tmp).ExclusiveSum(rows, off, total);
-        // pack this ray's keys to the front of the tile buffer, in ray order;
-        // keys are read into registers first (packing overlaps the source)
-        unsigned long long mine[64];
-#pragma unroll 1
-        for (int j = 0; j < rows; ++j) mine[j] = rk[j];
+        // packed row e of the tile belongs to the thread whose range holds it:
+        // record the owner of each packed row, then copy out coalesced
+        s_off[threadIdx.x] = off;
         if (threadIdx.x == 0) s_base = total ? atomicAdd(&ctr->rows_alloc, (unsigned long long)total) : 0ULL;
-        __syncthreads();
 #pragma unroll 1
-        for (int j = 0; j < rows; ++j) {
-            s_pack[off + j] = mine[j];
-            s_ray[off + j] = (int)i;
-        }
+        for (int j = 0; j < rows; ++j) s_own[off + j] = (unsigned char)threadIdx.x;
         __syncthreads();
         const unsigned long long base = s_base;
+        const long long ray0 = tile * kTileRays;
         if (base + (unsigned long long)total <= rcap) {
             for (int e = threadIdx.x; e < total; e += kTileRays) {
-                rowkey[base + e] = s_pack[e];
-                rowray[base + e] = s_ray[e];
+                const int o = s_own[e];
+                rowkey[base + e] = s_keys[(size_t)o * maxrows + (e - s_off[o])];
+                rowray[base + e] = (int)(ray0 + o);
             }
         } else if (threadIdx.x == 0) {
             atomicOr(&ctr->err_cap, 1);
@@ -480,7 +476,7 @@ svx_status march_t(svx_map* m, cudaStream_t s) {
     MarchPartial* parts = ptr<MarchPartial>(m->partials);
     FrameCtr* dc = ptr<FrameCtr>(m->ctr);
     if (m->maxrows > 0) {
-        const size_t smem = (size_t)kTileRays * m->maxrows * (sizeof(unsigned long long) + sizeof(int));
+        const size_t smem = (size_t)kTileRays * m->maxrows * (sizeof(unsigned long long) + 1);
         k_walk<P, Fe><<<kMarchBlocks, kTileRays, smem, s>>>(
             mp, m->cfg.sem_kind, m->cfg.num_classes, m->payload_d, ptr<double4>(m->ray),
             ptr<int>(m->rcnt), ptr<unsigned long long>(m->rowkey), ptr<int>(m->rowray), parts, dc);

@@ -30,7 +30,7 @@ namespace {
 constexpr int kResolveThreads = 256;
 constexpr int kSegThreads = 256;
 constexpr int kSegTile = kSegThreads * 4;
-constexpr int kSegBlocks = 148 * 2;
+constexpr int kSegBlocks = 148 * 4;
 
 __device__ __forceinline__ int slot_of(long long x, long long y, long long z) {
     return (int)(((x & 7) << 6) | ((y & 7) << 3) | (z & 7));
@@ -72,9 +72,9 @@ __device__ int leaf_find_or_insert(int4* table, long long mask, int a, int b, in
                                    long long bcap, int4* bcoord, FrameCtr* ctr) {
     long long pos = (long long)(block_hash(a, b, c) & (unsigned long long)mask);
     while (true) {
-        // Fast path: one 16-byte L2 read.  A published id was written after
-        // its key (release fence on the creating side), so a matching key is
-        // final -- almost every lookup ends here.
+        // Fast path: one 16-byte L2 read.  Key and id are published together
+        // by one 16-byte store, so a matching key is final -- almost every
+        // lookup ends here.
         const int4 sv = __ldcg(table + pos);
         if (sv.w >= 0) {
             if (sv.x == a && sv.y == b && sv.z == c) return sv.w;
@@ -267,64 +267,49 @@ __global__ void __launch_bounds__(kResolveThreads) k_resolve(
     }
 }
 
-// K3a: per-CTA totals over a contiguous chunk of the touched list: listed
-// voxels (multi-row ones, or all for open-set maps) and their rows.
-__device__ __forceinline__ long long seg_chunk(long long n) {
-    long long chunk = (n + kSegBlocks - 1) / kSegBlocks;
-    return (chunk + kSegTile - 1) / kSegTile * kSegTile;
+// K3: one pass over the touched list with a decoupled look-back scan.
+// Listed voxels (multi-row ones, or all for open-set maps) go to mlist in
+// touched-list order and get contiguous row segments (vseg).  Tiles are
+// claimed in order from a frame counter, so a tile only ever waits on tiles
+// already running.  Tile status words are 16-byte {tag, value} records
+// written and read with one transaction; tag = seq << 2 | flag (1 = tile
+// aggregate, 2 = inclusive prefix), so records of earlier launches never
+// match and the array needs no clearing.  value = listed << 40 | rows.
+struct alignas(16) SegStatus {
+    unsigned long long tag, val;
+};
+
+__device__ __forceinline__ void st_status(SegStatus* p, unsigned long long tag, unsigned long long v) {
+    asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(tag), "l"(v) : "memory");
 }
 
-__global__ void __launch_bounds__(kSegThreads) k_seg_count(const int* __restrict__ tlist,
-                                                           const unsigned* __restrict__ vcnt,
-                                                           unsigned long long* __restrict__ part,
-                                                           const FrameCtr* __restrict__ ctr) {
-    using R = cub::BlockReduce<unsigned long long, kSegThreads>;
-    __shared__ typename R::TempStorage tmp;
-    if (ctr->abort | ctr->err_cap) return;
-    const long long n = (long long)ctr->n_touched;
-    const int singles = ctr->p.inline_singles;
-    const long long chunk = seg_chunk(n);
-    const long long lo = (long long)blockIdx.x * chunk, hi = min(n, lo + chunk);
-    unsigned long long listed = 0, rows = 0;
-    for (long long e = lo + threadIdx.x; e < hi; e += kSegThreads) {
-        const unsigned c = vcnt[tlist[e]] & ~kNewBit;
-        if (!singles || c > 1u) {
-            listed += 1;
-            rows += c;
-        }
-    }
-    const unsigned long long packed = R(tmp).Sum((listed << 40) | rows);
-    if (threadIdx.x == 0) part[blockIdx.x] = packed;
+__device__ __forceinline__ void ld_status(const SegStatus* p, unsigned long long& tag,
+                                          unsigned long long& v) {
+    asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(tag), "=l"(v) : "l"(p) : "memory");
 }
 
-// K3b: each CTA rescans its chunk with its exclusive base; listed voxels go
-// to mlist and get contiguous row segments (vseg).
-__global__ void __launch_bounds__(kSegThreads) k_seg_write(const int* __restrict__ tlist,
-                                                           const unsigned* __restrict__ vcnt,
-                                                           unsigned* __restrict__ vseg,
-                                                           const unsigned long long* __restrict__ part,
-                                                           int* __restrict__ mlist, FrameCtr* ctr) {
+__global__ void __launch_bounds__(kSegThreads) k_seg(const int* __restrict__ tlist,
+                                                     const unsigned* __restrict__ vcnt,
+                                                     unsigned* __restrict__ vseg,
+                                                     int* __restrict__ mlist,
+                                                     SegStatus* __restrict__ status, FrameCtr* ctr) {
     using Scan = cub::BlockScan<unsigned long long, kSegThreads>;
-    using R = cub::BlockReduce<unsigned long long, kSegThreads>;
-    __shared__ union {
-        typename Scan::TempStorage scan;
-        typename R::TempStorage red;
-    } tmp;
-    __shared__ unsigned long long s_base;
+    __shared__ typename Scan::TempStorage scan_tmp;
+    __shared__ unsigned long long s_prefix;
+    __shared__ long long s_tile;
     if (ctr->abort | ctr->err_cap) return;
     const long long n = (long long)ctr->n_touched;
     const int singles = ctr->p.inline_singles;
+    const unsigned long long seq = ctr->p.seq;
     const unsigned long long low40 = (1ULL << 40) - 1;
-    unsigned long long acc = 0;
-    for (int b = threadIdx.x; b < (int)blockIdx.x; b += kSegThreads) acc += part[b];
-    acc = R(tmp.red).Sum(acc);
-    if (threadIdx.x == 0) s_base = acc;
-    __syncthreads();
-    unsigned long long base = s_base;
-    const long long chunk = seg_chunk(n);
-    const long long lo = (long long)blockIdx.x * chunk, hi = min(n, lo + chunk);
-    for (long long t0 = lo; t0 < hi; t0 += kSegTile) {
-        const long long e0 = t0 + (long long)threadIdx.x * 4;
+    const long long ntiles = (n + kSegTile - 1) / kSegTile;
+    const int lane = threadIdx.x & 31;
+    while (true) {
+        if (threadIdx.x == 0) s_tile = (long long)atomicAdd(&ctr->seg_tiles, 1u);
+        __syncthreads();
+        const long long tile = s_tile;
+        if (tile >= ntiles) break;
+        const long long e0 = tile * kSegTile + (long long)threadIdx.x * 4;
         int vv[4];
         unsigned cc[4];
         bool li[4];
@@ -332,17 +317,51 @@ __global__ void __launch_bounds__(kSegThreads) k_seg_write(const int* __restrict
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const long long e = e0 + q;
-            vv[q] = e < hi ? tlist[e] : -1;
+            vv[q] = e < n ? tlist[e] : -1;
             cc[q] = vv[q] >= 0 ? (vcnt[vv[q]] & ~kNewBit) : 0u;
             li[q] = vv[q] >= 0 && (!singles || cc[q] > 1u);
             cnt += li[q];
             rows += li[q] ? cc[q] : 0u;
         }
-        unsigned long long pre, total;
+        unsigned long long pre, agg;
+        Scan(scan_tmp).ExclusiveSum(((unsigned long long)cnt << 40) | rows, pre, agg);
+        if (threadIdx.x < 32) {
+            unsigned long long prefix = 0;
+            if (tile == 0) {
+                if (lane == 0) st_status(status, seq << 2 | 2, agg);
+            } else {
+                if (lane == 0) st_status(status + tile, seq << 2 | 1, agg);
+                // look back 32 tiles at a time until an inclusive prefix
+                long long hi = tile - 1;
+                while (true) {
+                    const long long p = hi - lane;
+                    unsigned long long tag = seq << 2 | 2, v = 0;
+                    if (p >= 0) ld_status(status + p, tag, v);
+                    const unsigned ready = __ballot_sync(0xffffffffu, (tag >> 2) == seq && (tag & 3) != 0);
+                    const unsigned incl = __ballot_sync(0xffffffffu, (tag >> 2) == seq && (tag & 3) == 2);
+                    // lanes up to the first inclusive one must all be ready
+                    const unsigned upto = incl ? (incl & (0u - incl)) * 2u - 1u : 0xffffffffu;
+                    if ((ready & upto) != upto) continue;   // a predecessor not yet published
+                    unsigned long long part = ((upto >> lane) & 1u) ? v : 0ULL;
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+                    prefix += part;
+                    if (incl) break;
+                    hi -= 32;
+                }
+                if (lane == 0) st_status(status + tile, seq << 2 | 2, prefix + agg);
+            }
+            if (lane == 0) {
+                s_prefix = prefix;
+                if (tile == ntiles - 1) {
+                    ctr->n_list = (prefix + agg) >> 40;
+                    ctr->rows_seg = (prefix + agg) & low40;
+                }
+            }
+        }
         __syncthreads();
-        Scan(tmp.scan).ExclusiveSum(((unsigned long long)cnt << 40) | rows, pre, total);
-        unsigned long long u = (base >> 40) + (pre >> 40);
-        unsigned long long r = (base & low40) + (pre & low40);
+        const unsigned long long base = s_prefix + pre;
+        unsigned long long u = base >> 40, r = base & low40;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             if (!li[q]) continue;
@@ -351,11 +370,6 @@ __global__ void __launch_bounds__(kSegThreads) k_seg_write(const int* __restrict
             ++u;
             r += cc[q];
         }
-        base += total;
-    }
-    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
-        ctr->n_list = base >> 40;
-        ctr->rows_seg = base & low40;
     }
 }
 
@@ -409,14 +423,11 @@ svx_status launch_resolve(svx_map* m, cudaStream_t s) {
 }
 
 svx_status launch_segments(svx_map* m, cudaStream_t s) {
-    unsigned long long* part =
-        reinterpret_cast<unsigned long long*>(ptr<char>(m->partials) + partials_bytes());
-    k_seg_count<<<kSegBlocks, kSegThreads, 0, s>>>(ptr<int>(m->tlist), ptr<unsigned>(m->vcnt), part,
-                                                   ptr<FrameCtr>(m->ctr));
-    SVX_LAUNCHED();
-    k_seg_write<<<kSegBlocks, kSegThreads, 0, s>>>(ptr<int>(m->tlist), ptr<unsigned>(m->vcnt),
-                                                   ptr<unsigned>(m->vseg), part, ptr<int>(m->mlist),
-                                                   ptr<FrameCtr>(m->ctr));
+    SegStatus* status =
+        reinterpret_cast<SegStatus*>(ptr<char>(m->partials) + partials_bytes());
+    k_seg<<<kSegBlocks, kSegThreads, 0, s>>>(ptr<int>(m->tlist), ptr<unsigned>(m->vcnt),
+                                             ptr<unsigned>(m->vseg), ptr<int>(m->mlist), status,
+                                             ptr<FrameCtr>(m->ctr));
     SVX_LAUNCHED();
     return SVX_OK;
 }
@@ -427,6 +438,8 @@ svx_status launch_cleanup(svx_map* m, cudaStream_t s) {
     return s64 ? cleanup_t<float, double>(m, s) : cleanup_t<float, float>(m, s);
 }
 
-size_t segment_partials_bytes() { return sizeof(unsigned long long) * kSegBlocks; }
+size_t segment_status_bytes(unsigned long long ucap) {
+    return sizeof(SegStatus) * (ucap / kSegTile + 2);
+}
 
 }  // namespace svx
