@@ -142,6 +142,72 @@ svx_status svx_integrate_world(svx_map* map, const void* points_world, int32_t p
                                const void* feats, int32_t feats_dtype, void* stream,
                                svx_report* report);
 
+/* ---- sharded integration (no reference counterpart) -----------
+ * A map sharded over G ranks (one GPU each): rank r holds the leaves with
+ * svx_leaf_owner(leaf, G) == r.  Each frame is split into G contiguous point
+ * slices; rank r marches slice r and a frame takes four calls per rank with
+ * two host collectives in between, done by the caller's transport
+ * (torch.distributed over NCCL, or gloo):
+ *
+ *   svx_shard_march   march this rank's slice (masks, fp64 band walk) and
+ *                     fill its local summary
+ *   -- all-reduce the summaries: counters summed, bbox_min min, bbox_max and
+ *      flags max
+ *   svx_shard_plan    apply the reference's frame checks to the global
+ *                     summary (every rank fails identically, before any map
+ *                     mutation); bucket this rank's rows by owning rank and
+ *                     return the send size per destination.  *remarch = 1
+ *                     asks for svx_shard_march again with key_base =
+ *                     global bbox_min (packed-key window overflow).
+ *   svx_shard_pack    write the send buffer: per destination, the points
+ *                     that have rows there (ray direction, distance, label or
+ *                     feature) and the rows (voxel key, point)
+ *   -- all-to-all of the sizes, then of the buffers (rank order)
+ *   svx_shard_apply   resolve, group and update the received rows -- this
+ *                     rank's leaves only -- exactly as svx_integrate does.
+ *
+ * Points keep their global order (slices are contiguous and concatenated in
+ * rank order), so every voxel's rows are reduced in the reference's
+ * (voxel, point) order and the union of the shards equals the single-GPU map
+ * bit for bit.  svx_export_leaf_stamps gives the keys that merge the shards'
+ * active lists into the reference's global active order. */
+#define SVX_MAX_SHARDS 16
+
+typedef struct svx_shard_summary {
+    int64_t points_in;     /* slice sizes (summed) */
+    int64_t nonfinite, range, degenerate, bad_label, used, band_hits, rows; /* summed */
+    int64_t bbox_min[3];   /* min over ranks (INT64_MAX when no rows) */
+    int64_t bbox_max[3];   /* max over ranks (INT64_MIN when no rows) */
+    int64_t err_budget;    /* max over ranks */
+    int64_t err_pack;      /* max over ranks */
+} svx_shard_summary;
+
+int32_t svx_leaf_owner(int64_t bx, int64_t by, int64_t bz, int32_t nranks);
+
+/* pose (4x4, sensor-frame points) or, when pose is NULL, origin (world-frame
+ * points, svx_integrate_world semantics).  Slice r must hold the frame's
+ * points [n*r/G, n*(r+1)/G) (any contiguous split in rank order works).
+ * key_base NULL = the default packed-key window.  All four calls of a frame
+ * must use the same stream. */
+svx_status svx_shard_march(svx_map* map, const void* points, int32_t points_dtype, int64_t n,
+                           const double pose[16], const double origin[3],
+                           const int32_t* labels, const void* feats, int32_t feats_dtype,
+                           const int64_t key_base[3], void* stream, svx_shard_summary* local);
+svx_status svx_shard_plan(svx_map* map, const svx_shard_summary* global, int32_t rank,
+                          int32_t nranks, int64_t* send_bytes, int32_t* remarch);
+/* send: device buffer of at least sum(send_bytes) bytes, 16-byte aligned. */
+svx_status svx_shard_pack(svx_map* map, void* send, int64_t capacity, void* stream);
+/* recv: device buffer holding recv_bytes[s] bytes from each source s, in
+ * rank order, 16-byte aligned. */
+svx_status svx_shard_apply(svx_map* map, const void* recv, const int64_t* recv_bytes,
+                           int32_t nranks, void* stream, svx_report* report);
+
+/* Per leaf, in this map's active (leaf) order: creation frame, the leaf's
+ * smallest packed key in that frame, and its active voxel count.  Sorting
+ * the concatenated shards' leaves by (frame, key) gives the global order. */
+svx_status svx_export_leaf_stamps(svx_map* map, int64_t capacity, int32_t* frame, uint64_t* key,
+                                  int32_t* count, int64_t* nleaves, void* stream);
+
 /* ---- queries ---------------------------------------------------------------
  * Active order is leaf-allocation then slot order, identical to
  * GridCore.active_slots (_core.pyx:424-444) + slots_to_coords (:446-463).

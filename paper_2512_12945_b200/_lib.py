@@ -69,6 +69,28 @@ class SvxStats(ctypes.Structure):
     ]
 
 
+MAX_SHARDS = 16
+
+
+class SvxShardSummary(ctypes.Structure):
+    """svx_shard_summary: one rank's march counters, reduced across ranks."""
+
+    _fields_ = [
+        ("points_in", ctypes.c_int64),
+        ("nonfinite", ctypes.c_int64),
+        ("range", ctypes.c_int64),
+        ("degenerate", ctypes.c_int64),
+        ("bad_label", ctypes.c_int64),
+        ("used", ctypes.c_int64),
+        ("band_hits", ctypes.c_int64),
+        ("rows", ctypes.c_int64),
+        ("bbox_min", ctypes.c_int64 * 3),
+        ("bbox_max", ctypes.c_int64 * 3),
+        ("err_budget", ctypes.c_int64),
+        ("err_pack", ctypes.c_int64),
+    ]
+
+
 _P = ctypes.c_void_p
 _I32 = ctypes.c_int32
 _I64 = ctypes.c_int64
@@ -91,13 +113,21 @@ _SIGNATURES = {
     "svx_label_map": [_P, _I32, _I64, _P, _P],
     "svx_set_profiling": [_P, _I32],
     "svx_reserve": [_P, _I64, _I64],
+    "svx_shard_march": [_P, _P, _I32, _I64, ctypes.POINTER(_D), ctypes.POINTER(_D), _P, _P, _I32,
+                        ctypes.POINTER(_I64), _P, ctypes.POINTER(SvxShardSummary)],
+    "svx_shard_plan": [_P, ctypes.POINTER(SvxShardSummary), _I32, _I32, ctypes.POINTER(_I64),
+                       ctypes.POINTER(_I32)],
+    "svx_shard_pack": [_P, _P, _I64, _P],
+    "svx_shard_apply": [_P, _P, ctypes.POINTER(_I64), _I32, _P, ctypes.POINTER(SvxReport)],
+    "svx_export_leaf_stamps": [_P, _I64, _P, _P, _P, ctypes.POINTER(_I64), _P],
 }
 
 STAGES = ("march", "resolve", "scatter", "update", "update_b")
 
 # every symbol include/svx.h declares (checked by tests/test_abi_and_config.py)
 EXPORTED = sorted(list(_SIGNATURES) + ["svx_last_error", "svx_abi_version",
-                                       "svx_kernel_launches", "svx_stage_times"])
+                                       "svx_kernel_launches", "svx_stage_times",
+                                       "svx_leaf_owner"])
 
 
 def _load():
@@ -118,6 +148,8 @@ def _load():
     lib.svx_kernel_launches.restype = ctypes.c_int64
     lib.svx_stage_times.argtypes = [_P, ctypes.POINTER(_D), _I32]
     lib.svx_stage_times.restype = ctypes.c_int32
+    lib.svx_leaf_owner.argtypes = [_I64, _I64, _I64, _I32]
+    lib.svx_leaf_owner.restype = ctypes.c_int32
     return lib
 
 

@@ -458,4 +458,86 @@ svx_status svx_label_map(svx_map* m, int32_t mode, int64_t capacity, int32_t* la
     return SVX_OK;
 }
 
+// ---- sharded integration ---------------------------------------------------
+
+int32_t svx_leaf_owner(int64_t bx, int64_t by, int64_t bz, int32_t nranks) {
+    if (nranks < 1) return -1;
+    return leaf_owner(bx, by, bz, nranks);
+}
+
+svx_status svx_shard_march(svx_map* m, const void* points, int32_t points_dtype, int64_t n,
+                           const double pose[16], const double origin[3], const int32_t* labels,
+                           const void* feats, int32_t feats_dtype, const int64_t key_base[3],
+                           void* stream, svx_shard_summary* local) {
+    if (!m || !local || (!pose && !origin) || (n > 0 && !points))
+        return fail(SVX_E_INPUT, "null argument");
+    SVX_TRY(set_device(m));
+    PoseParams pp;
+    memset(&pp, 0, sizeof(pp));
+    if (pose) {
+        for (int r = 0; r < 3; ++r) {
+            for (int c = 0; c < 3; ++c) pp.R[3 * r + c] = pose[4 * r + c];
+            pp.t[r] = pose[4 * r + 3];
+        }
+        pp.sensor = 1;
+    } else {
+        pp.R[0] = pp.R[4] = pp.R[8] = 1.0;
+        for (int a = 0; a < 3; ++a) pp.t[a] = origin[a];
+        pp.sensor = 0;
+    }
+    return shard_march(m, points, points_dtype == SVX_F64, n, pp, labels, feats,
+                       feats_dtype == SVX_F64, key_base, (cudaStream_t)stream, local);
+}
+
+svx_status svx_shard_plan(svx_map* m, const svx_shard_summary* global, int32_t rank,
+                          int32_t nranks, int64_t* send_bytes, int32_t* remarch) {
+    if (!m || !global || !send_bytes || !remarch) return fail(SVX_E_INPUT, "null argument");
+    SVX_TRY(set_device(m));
+    int rm = 0;
+    svx_status st = shard_plan(m, global, rank, nranks, send_bytes, &rm, (cudaStream_t)0);
+    *remarch = rm;
+    return st;
+}
+
+svx_status svx_shard_pack(svx_map* m, void* send, int64_t capacity, void* stream) {
+    if (!m) return fail(SVX_E_INPUT, "null argument");
+    SVX_TRY(set_device(m));
+    return shard_pack(m, send, capacity, (cudaStream_t)stream);
+}
+
+svx_status svx_shard_apply(svx_map* m, const void* recv, const int64_t* recv_bytes, int32_t nranks,
+                           void* stream, svx_report* report) {
+    if (!m || !recv_bytes) return fail(SVX_E_INPUT, "null argument");
+    SVX_TRY(set_device(m));
+    return shard_apply(m, recv, recv_bytes, nranks, (cudaStream_t)stream, report);
+}
+
+svx_status svx_export_leaf_stamps(svx_map* m, int64_t capacity, int32_t* frame, uint64_t* key,
+                                  int32_t* count, int64_t* nleaves, void* stream) {
+    if (!m || !nleaves) return fail(SVX_E_INPUT, "null argument");
+    SVX_TRY(set_device(m));
+    cudaStream_t s = (cudaStream_t)stream;
+    int64_t vox = 0;
+    SVX_TRY(build_active_list(m, &vox, s));
+    const int64_t nb = vox ? m->nblocks : 0;
+    *nleaves = nb;
+    if (capacity < nb) return fail(SVX_E_INPUT, "output capacity smaller than leaf count");
+    OutStage o[3];
+    void *df, *dk, *dn;
+    svx_status st = SVX_OK;
+    if ((st = out_prepare(o[0], frame, 4 * nb, s, &df)) ||
+        (st = out_prepare(o[1], key, 8 * nb, s, &dk)) ||
+        (st = out_prepare(o[2], count, 4 * nb, s, &dn)) ||
+        (st = launch_leaf_stamps(m, (int32_t*)df, (uint64_t*)dk, (int32_t*)dn, s))) {
+        out_release(o, 3);
+        return st;
+    }
+    for (int i = 0; i < 3 && st == SVX_OK; ++i) st = out_finish(o[i], s);
+    cudaError_t e = cudaStreamSynchronize(s);
+    out_release(o, 3);
+    if (st) return st;
+    if (e != cudaSuccess) return fail(SVX_E_CUDA, std::string("leaf stamps: ") + cudaGetErrorString(e));
+    return SVX_OK;
+}
+
 }  // extern "C"

@@ -104,7 +104,7 @@ svx_status reserve_blocks(svx_map* m, int64_t need, cudaStream_t s) {
 
 // Per-frame scratch: per-ray arrays for npts_cap points, row arrays for the
 // row space (slot mode: npts_cap * maxrows, dense: rcap), lists for ucap.
-static svx_status reserve_frame(svx_map* m, int64_t n, cudaStream_t s) {
+svx_status reserve_frame(svx_map* m, int64_t n, cudaStream_t s) {
     m->npts_cap = std::max<int64_t>(m->npts_cap, n);
     const int64_t rows = (int64_t)m->rcap;
     m->ucap = (uint64_t)rows;
@@ -234,6 +234,91 @@ static svx_status run_frame(svx_map* m, int pts_f64, int feats_f64, cudaStream_t
     return SVX_OK;
 }
 
+// Row space.  A band of length L crosses at most 3 * (L / h + 1) voxels;
+// without carving L = 2 * trunc, so each ray gets that many row slots.
+// Carving bands are unbounded: rows are counted, scanned and packed.
+void init_row_space(svx_map* m, int64_t n) {
+    const double h = m->cfg.voxel_size;
+    if (m->maxrows < 0) {
+        const double bound = 3.0 * (2.0 * m->cfg.truncation / h + 1.0) + 3.0;
+        m->maxrows = (m->cfg.space_carving || bound > 32.0) ? 0 : (int)bound;
+    }
+    if (m->rcap == 0)   // first frame: the bound (bounded bands) or a guess; adapted per frame
+        m->rcap = m->maxrows > 0 ? (uint64_t)n * m->maxrows + 4096 : (uint64_t)n * 32 + 4096;
+}
+
+// Pool headroom: every row could open a voxel (closed/geometry), an eighth
+// of them for open-set payloads; leaves get twice what recent frames
+// created.  A shortfall is caught on the device and the frame re-run.
+svx_status reserve_pools(svx_map* m, cudaStream_t s) {
+    const int64_t rows_bound = (int64_t)m->ucap;
+    const int64_t vhead = m->cfg.sem_kind == SVX_SEM_OPEN ? std::max<int64_t>(rows_bound / 8, 1 << 16)
+                                                          : rows_bound;
+    SVX_TRY(reserve_voxels(m, m->nvox + vhead, s));
+    SVX_TRY(reserve_blocks(m, m->nblocks + std::max<int64_t>(m->new_leaves_cap, 4096), s));
+    return SVX_OK;
+}
+
+// Zeroed counters with the live pool counts; FrameParams are filled by the caller.
+void reset_ctr(svx_map* m) {
+    FrameCtr* hc = m->h_ctr;
+    memset(hc, 0, sizeof(FrameCtr));
+    for (int a = 0; a < 3; ++a) {
+        hc->bbox_min[a] = LLONG_MAX;
+        hc->bbox_max[a] = LLONG_MIN;
+    }
+    hc->nblocks = (unsigned long long)m->nblocks;
+    hc->nvox = (unsigned long long)m->nvox;
+    FrameParams& p = hc->p;
+    p.ucap = m->ucap;
+    p.rcap = m->rcap;
+    p.hmask = m->hcap - 1;
+    p.bcap = m->bcap;
+    p.vcap = m->vcap;
+    p.frame = (int)m->frames;
+    p.maxrows = m->maxrows;
+    p.inline_singles = inline_singles(m);
+    p.seq = ++m->seq;
+}
+
+// K2 ran out of leaf or voxel pool: give what it activated its background
+// state, clear the frame counts and grow; the allocation counters carry over
+// and the caller runs the frame again.
+svx_status recover_capacity(svx_map* m, int64_t nblocks0, cudaStream_t s) {
+    FrameCtr* hc = m->h_ctr;
+    SVX_TRY(launch_cleanup(m, s));
+    SVX_CUDA(cudaStreamSynchronize(s));
+    m->nblocks = (int64_t)std::min<unsigned long long>(hc->nblocks, (unsigned long long)m->bcap);
+    m->nvox = (int64_t)std::min<unsigned long long>(hc->nvox, (unsigned long long)m->vcap);
+    m->ord_nblocks = std::min<int64_t>(m->ord_nblocks, nblocks0);
+    m->new_leaves_cap = std::max<int64_t>(2 * m->new_leaves_cap, m->bcap);
+    SVX_TRY(reserve_voxels(m, 2 * m->vcap, s));
+    return SVX_OK;
+}
+
+// Report fields of the map side and the capacities for the next frame.
+void finish_frame(svx_map* m, int64_t nblocks0, int64_t nvox0, svx_report& r) {
+    FrameCtr* hc = m->h_ctr;
+    r.touched_voxels = (int64_t)hc->n_touched;
+    r.new_blocks = (int64_t)hc->nblocks - nblocks0;
+    r.new_voxels = (int64_t)hc->nvox - nvox0;
+    m->new_leaves_cap = std::max<int64_t>(m->new_leaves_cap, 2 * r.new_blocks + 1024);
+    m->nblocks = (int64_t)hc->nblocks;
+    m->nvox = (int64_t)hc->nvox;
+    m->frames++;
+    // row capacity for the next frame: 1.5x this one's rows
+    const uint64_t need = hc->rows + hc->rows / 2 + 4096;
+    if (hc->rows * 10 > m->rcap * 8 || need * 3 < m->rcap) m->rcap = need;
+}
+
+// Packed keys are offsets from the sensor's voxel minus 2^20 per axis.
+KeyPack default_key_pack(const svx_map* m, const PoseParams& pp) {
+    KeyPack kp;
+    const long long half = 1LL << (kPackBits - 1);
+    for (int a = 0; a < 3; ++a) kp.base[a] = (long long)floor(pp.t[a] / m->cfg.voxel_size) - half;
+    return kp;
+}
+
 svx_status integrate_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n,
                           const PoseParams& pp, const int32_t* labels_in, const void* feats_in,
                           int feats_f64, cudaStream_t s, svx_report* rep) {
@@ -241,9 +326,10 @@ svx_status integrate_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n
     memset(&r, 0, sizeof(r));
     r.points_in = n;
     const int kind = m->cfg.sem_kind;
-    if (kind == SVX_SEM_CLOSED && !labels_in)
+    // (an empty payload array arrives as NULL; presence is checked on the host)
+    if (kind == SVX_SEM_CLOSED && !labels_in && n > 0)
         return fail(SVX_E_PAYLOAD, "closed-set grid requires per-point labels");
-    if (kind == SVX_SEM_OPEN && !feats_in)
+    if (kind == SVX_SEM_OPEN && !feats_in && n > 0)
         return fail(SVX_E_PAYLOAD, "open-set grid requires per-point features");
     if (n < 0) return fail(SVX_E_INPUT, "negative point count");
     if (n >= (int64_t)INT_MAX) return fail(SVX_E_INPUT, "point count exceeds 2^31-1");
@@ -261,23 +347,8 @@ svx_status integrate_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n
     if (kind == SVX_SEM_OPEN)
         SVX_TRY(stage_in(feats_in, (size_t)n * m->payload_d * (feats_f64 ? 8 : 4), m->in_feat, s,
                          &feats));
-
-    // Row space.  A band of length L crosses at most 3 * (L / h + 1) voxels;
-    // without carving L = 2 * trunc, so each ray gets that many row slots.
-    // Carving bands are unbounded: rows are counted, scanned and packed.
-    const double h = m->cfg.voxel_size;
-    if (m->maxrows < 0) {
-        const double bound = 3.0 * (2.0 * m->cfg.truncation / h + 1.0) + 3.0;
-        m->maxrows = (m->cfg.space_carving || bound > 32.0) ? 0 : (int)bound;
-    }
-    if (m->rcap == 0)   // first frame: the bound (bounded bands) or a guess; adapted per frame
-        m->rcap = m->maxrows > 0 ? (uint64_t)n * m->maxrows + 4096 : (uint64_t)n * 32 + 4096;
-
-    KeyPack kp;
-    {
-        const long long half = 1LL << (kPackBits - 1);
-        for (int a = 0; a < 3; ++a) kp.base[a] = (long long)floor(pp.t[a] / h) - half;
-    }
+    init_row_space(m, n);
+    KeyPack kp = default_key_pack(m, pp);
     FrameCtr* hc = m->h_ctr;
     // counts before this frame (stamps, report); m->nblocks / m->nvox stay the
     // live counts, including what a capacity-aborted attempt allocated
@@ -285,23 +356,8 @@ svx_status integrate_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n
     for (int attempt = 0;; ++attempt) {
         if (attempt >= 8) return fail(SVX_E_INTERNAL, "frame scratch could not be sized");
         SVX_TRY(reserve_frame(m, n, s));
-        // pool headroom: every row could open a voxel (closed/geometry), an
-        // eighth of them for open-set payloads; leaves get twice what recent
-        // frames created.  A shortfall is caught on the device and re-run.
-        const int64_t rows_bound = (int64_t)m->ucap;
-        const int64_t vhead = m->cfg.sem_kind == SVX_SEM_OPEN
-                                  ? std::max<int64_t>(rows_bound / 8, 1 << 16)
-                                  : rows_bound;
-        SVX_TRY(reserve_voxels(m, m->nvox + vhead, s));
-        SVX_TRY(reserve_blocks(m, m->nblocks + std::max<int64_t>(m->new_leaves_cap, 4096), s));
-
-        memset(hc, 0, sizeof(FrameCtr));
-        for (int a = 0; a < 3; ++a) {
-            hc->bbox_min[a] = LLONG_MAX;
-            hc->bbox_max[a] = LLONG_MIN;
-        }
-        hc->nblocks = (unsigned long long)m->nblocks;
-        hc->nvox = (unsigned long long)m->nvox;
+        SVX_TRY(reserve_pools(m, s));
+        reset_ctr(m);
         FrameParams& p = hc->p;
         p.pts = pts;
         p.labels = (const int32_t*)labv;
@@ -309,16 +365,7 @@ svx_status integrate_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n
         p.n = n;
         p.pp = pp;
         p.kp = kp;
-        p.ucap = m->ucap;
-        p.rcap = m->rcap;
-        p.hmask = m->hcap - 1;
         p.nblocks0 = nblocks0;
-        p.bcap = m->bcap;
-        p.vcap = m->vcap;
-        p.frame = (int)m->frames;
-        p.maxrows = m->maxrows;
-        p.inline_singles = inline_singles(m);
-        p.seq = ++m->seq;
 
         SVX_TRY(run_frame(m, pts_f64, feats_f64, s));
 
@@ -350,16 +397,7 @@ svx_status integrate_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n
             continue;
         }
         if (hc->err_cap) {
-            // K2 ran out of leaf or voxel pool: give what it activated its
-            // background state, clear the frame counts, grow, run again (the
-            // allocation counters carry over)
-            SVX_TRY(launch_cleanup(m, s));
-            SVX_CUDA(cudaStreamSynchronize(s));
-            m->nblocks = (int64_t)std::min<unsigned long long>(hc->nblocks, (unsigned long long)m->bcap);
-            m->nvox = (int64_t)std::min<unsigned long long>(hc->nvox, (unsigned long long)m->vcap);
-            m->ord_nblocks = std::min<int64_t>(m->ord_nblocks, nblocks0);
-            m->new_leaves_cap = std::max<int64_t>(2 * m->new_leaves_cap, m->bcap);
-            SVX_TRY(reserve_voxels(m, 2 * m->vcap, s));
+            SVX_TRY(recover_capacity(m, nblocks0, s));
             continue;
         }
         break;
@@ -372,18 +410,8 @@ svx_status integrate_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n
     r.skipped_bad_label = (int64_t)hc->bad_label;
     r.points_used = (int64_t)hc->used;
     r.band_hits = (int64_t)hc->band_hits;
-    r.touched_voxels = (int64_t)hc->n_touched;
-    r.new_blocks = (int64_t)hc->nblocks - nblocks0;
-    r.new_voxels = (int64_t)hc->nvox - nvox0;
     r.kernel_ms = ms;
-    m->new_leaves_cap = std::max<int64_t>(m->new_leaves_cap, 2 * r.new_blocks + 1024);
-    m->nblocks = (int64_t)hc->nblocks;
-    m->nvox = (int64_t)hc->nvox;
-    m->frames++;
-    {   // row capacity for the next frame: 1.5x this one's rows
-        const uint64_t need = hc->rows + hc->rows / 2 + 4096;
-        if (hc->rows * 10 > m->rcap * 8 || need * 3 < m->rcap) m->rcap = need;
-    }
+    finish_frame(m, nblocks0, nvox0, r);
     if (rep) *rep = r;
     return SVX_OK;
 }

@@ -200,6 +200,20 @@ struct svx_map {
     cudaEvent_t st_ev[2 * SVX_N_STAGES] = {};
     unsigned st_mask = 0;
     double stage_ms[SVX_N_STAGES] = {};
+    // sharded integration (svx_shard.cu): state between a frame's calls
+    int shard_phase = 0;          // 0 idle, 1 marched, 2 planned, 3 packed
+    int shard_g = 1, shard_rank = 0;
+    int64_t shard_n = 0;          // points in this rank's slice
+    int64_t shard_rows = 0;       // rows this rank marched
+    int shard_pts_f64 = 0, shard_feats_f64 = 0;
+    const void* shard_lab = nullptr;    // the slice's staged payload
+    const void* shard_feat = nullptr;
+    svx::PoseParams shard_pp{};
+    svx::KeyPack shard_kp{};
+    svx_shard_summary shard_sum{};      // the frame's global summary
+    svx::DevBuf sh_mask, sh_pos, sh_tiles, sh_meta;
+    int64_t sh_npts[SVX_MAX_SHARDS] = {}, sh_nrows[SVX_MAX_SHARDS] = {};
+    int64_t sh_bytes[SVX_MAX_SHARDS] = {};
 };
 
 namespace svx {
@@ -222,6 +236,34 @@ void count_launch(int n = 1);
         svx_status _s = (expr);           \
         if (_s != SVX_OK) return _s;      \
     } while (0)
+
+// Programmatic dependent launch: kernels of the frame pipeline are launched
+// with programmatic stream serialization, so a kernel's CTAs are scheduled
+// while its predecessor drains (hiding the launch gap inside the graph).
+// Each such kernel calls grid_dep_wait() before it reads anything; that
+// returns once the predecessor grid has completed and its writes are visible.
+// The kernel first lets its successor be scheduled (launch_dependents), so
+// the successor's launch overlaps this kernel's tail.
+__device__ __forceinline__ void grid_dep_wait() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+template <class... KArgs, class... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), unsigned grid, unsigned block, size_t smem,
+                              cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at{};
+    at.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at.val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = &at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
 
 #define SVX_LAUNCHED()                                                                      \
     do {                                                                                    \
@@ -316,8 +358,35 @@ svx_status launch_update_a(svx_map* m, int feats_f64, cudaStream_t s);
 svx_status launch_update_b(svx_map* m, int feats_f64, cudaStream_t s);
 svx_status launch_rehash(svx_map* m, int4* new_table, int64_t new_cap, cudaStream_t s);
 int huge_warps();
+
+// frame driver pieces shared by svx_integrate and the sharded calls (svx_frame.cu)
+void init_row_space(svx_map* m, int64_t n);
+svx_status reserve_frame(svx_map* m, int64_t n, cudaStream_t s);
+svx_status reserve_pools(svx_map* m, cudaStream_t s);
+void reset_ctr(svx_map* m);
+svx_status recover_capacity(svx_map* m, int64_t nblocks0, cudaStream_t s);
+void finish_frame(svx_map* m, int64_t nblocks0, int64_t nvox0, svx_report& r);
+KeyPack default_key_pack(const svx_map* m, const PoseParams& pp);
+
+// Owning rank of a leaf in a sharded map: high hash bits, independent of the
+// low bits that place the leaf in its owner's hash table.
+__host__ __device__ inline int leaf_owner(long long a, long long b, long long c, int g) {
+    return (int)((block_hash((int)a, (int)b, (int)c) >> 32) % (uint64_t)g);
+}
 // svx_query.cu
 svx_status build_active_list(svx_map* m, int64_t* count, cudaStream_t s);
+svx_status launch_leaf_stamps(svx_map* m, int32_t* frame, uint64_t* key, int32_t* count,
+                              cudaStream_t s);
+
+// sharded integration (svx_shard.cu)
+svx_status shard_march(svx_map* m, const void* pts, int pts_f64, int64_t n, const PoseParams& pp,
+                       const int32_t* labels, const void* feats, int feats_f64,
+                       const int64_t* key_base, cudaStream_t s, svx_shard_summary* out);
+svx_status shard_plan(svx_map* m, const svx_shard_summary* global, int rank, int nranks,
+                      int64_t* send_bytes, int* remarch, cudaStream_t s);
+svx_status shard_pack(svx_map* m, void* send, int64_t capacity, cudaStream_t s);
+svx_status shard_apply(svx_map* m, const void* recv, const int64_t* recv_bytes, int nranks,
+                       cudaStream_t s, svx_report* rep);
 svx_status launch_export(svx_map* m, int64_t count, int64_t* coords, void* d, void* w, void* sem0,
                          void* sem1, cudaStream_t s);
 svx_status launch_probe(svx_map* m, const int64_t* coords, int64_t cnt, void* d, void* w,

@@ -259,6 +259,7 @@ __global__ void __launch_bounds__(kTileRays, 4) k_walk(MarchParams mp, int sem_k
                                                     int* __restrict__ rowray,
                                                     MarchPartial* __restrict__ partials,
                                                     FrameCtr* __restrict__ ctr) {
+    grid_dep_wait();
     using Scan = cub::BlockScan<int, kTileRays>;
     __shared__ typename Scan::TempStorage scan_tmp;
     __shared__ unsigned long long s_base;
@@ -342,6 +343,7 @@ __global__ void __launch_bounds__(kMarchThreads) k_walk_count(MarchParams mp, in
                                                               int* __restrict__ rcnt,
                                                               MarchPartial* __restrict__ partials,
                                                               FrameCtr* __restrict__ ctr) {
+    grid_dep_wait();
     const FrameParams fp = ctr->p;
     const long long n = fp.n;
     const double ox = fp.pp.t[0], oy = fp.pp.t[1], oz = fp.pp.t[2];
@@ -387,6 +389,7 @@ __global__ void __launch_bounds__(kMarchThreads) k_walk_write(MarchParams mp,
                                                               unsigned long long* __restrict__ rowkey,
                                                               int* __restrict__ rowray,
                                                               const FrameCtr* __restrict__ ctr) {
+    grid_dep_wait();
     if (ctr->abort) return;
     const FrameParams fp = ctr->p;
     const long long n = fp.n;
@@ -477,23 +480,23 @@ svx_status march_t(svx_map* m, cudaStream_t s) {
     FrameCtr* dc = ptr<FrameCtr>(m->ctr);
     if (m->maxrows > 0) {
         const size_t smem = (size_t)kTileRays * m->maxrows * (sizeof(unsigned long long) + 1);
-        k_walk<P, Fe><<<kMarchBlocks, kTileRays, smem, s>>>(
+        SVX_CUDA(launch_pdl(k_walk<P, Fe>, kMarchBlocks, kTileRays, smem, s, 
             mp, m->cfg.sem_kind, m->cfg.num_classes, m->payload_d, ptr<double4>(m->ray),
-            ptr<int>(m->rcnt), ptr<unsigned long long>(m->rowkey), ptr<int>(m->rowray), parts, dc);
+            ptr<int>(m->rcnt), ptr<unsigned long long>(m->rowkey), ptr<int>(m->rowray), parts, dc));
         SVX_LAUNCHED();
         return SVX_OK;
     }
-    k_walk_count<P, Fe><<<kMarchBlocks, kMarchThreads, 0, s>>>(
+    SVX_CUDA(launch_pdl(k_walk_count<P, Fe>, kMarchBlocks, kMarchThreads, 0, s, 
         mp, m->cfg.sem_kind, m->cfg.num_classes, m->payload_d, m->npts_cap, ptr<double4>(m->ray),
-        ptr<int>(m->rcnt), parts, dc);
+        ptr<int>(m->rcnt), parts, dc));
     SVX_LAUNCHED();
     size_t tmp = m->cubtmp.bytes;
     SVX_CUDA(cub::DeviceScan::ExclusiveSum(m->cubtmp.p, tmp, ptr<int>(m->rcnt),
                                            ptr<long long>(m->roff), (int)m->npts_cap, s));
     count_launch();
-    k_walk_write<<<kMarchBlocks, kMarchThreads, 0, s>>>(
+    SVX_CUDA(launch_pdl(k_walk_write, kMarchBlocks, kMarchThreads, 0, s, 
         mp, ptr<double4>(m->ray), ptr<int>(m->rcnt), ptr<long long>(m->roff),
-        ptr<unsigned long long>(m->rowkey), ptr<int>(m->rowray), dc);
+        ptr<unsigned long long>(m->rowkey), ptr<int>(m->rowray), dc));
     SVX_LAUNCHED();
     return SVX_OK;
 }

@@ -45,6 +45,20 @@ __global__ void k_popc(int64_t nblocks, const int* __restrict__ order,
     cnt[b] = c;
 }
 
+// Leaf stamps in active order (merge keys of a sharded map's active lists).
+__global__ void k_leaf_stamps(int64_t nblocks, const int* __restrict__ order,
+                              const int4* __restrict__ bcoord,
+                              const unsigned long long* __restrict__ bkey,
+                              const int* __restrict__ cnt, int32_t* __restrict__ frame,
+                              uint64_t* __restrict__ key, int32_t* __restrict__ count) {
+    int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nblocks) return;
+    const int leaf = order[q];
+    if (frame) frame[q] = bcoord[leaf].w;
+    if (key) key[q] = bkey[leaf];
+    if (count) count[q] = cnt[q];
+}
+
 // One warp per leaf: lanes cover 32 slots at a time, ballot/popc give ranks.
 __global__ void k_list(int64_t nblocks, const int* __restrict__ order,
                        const unsigned long long* __restrict__ bmask,
@@ -316,6 +330,18 @@ svx_status build_active_list(svx_map* m, int64_t* count, cudaStream_t s) {
                                              ptr<int>(m->bslot), ptr<int4>(m->bcoord),
                                              ptr<long long>(m->act_off), ptr<int>(m->act_vid),
                                              ptr<long long>(m->act_coord));
+    SVX_LAUNCHED();
+    return SVX_OK;
+}
+
+svx_status launch_leaf_stamps(svx_map* m, int32_t* frame, uint64_t* key, int32_t* count,
+                              cudaStream_t s) {
+    const int64_t nb = m->nblocks;
+    if (nb == 0 || m->nvox == 0) return SVX_OK;
+    const int T = 256;
+    k_leaf_stamps<<<grid_for(nb, T), T, 0, s>>>(nb, ptr<int>(m->ord0), ptr<int4>(m->bcoord),
+                                               ptr<unsigned long long>(m->bkey),
+                                               ptr<int>(m->act_cnt), frame, key, count);
     SVX_LAUNCHED();
     return SVX_OK;
 }

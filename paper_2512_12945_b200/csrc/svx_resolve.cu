@@ -125,6 +125,7 @@ __global__ void __launch_bounds__(kResolveThreads) k_resolve(
     const unsigned long long* __restrict__ rowkey, int* __restrict__ rowvid, int4* table,
     int4* bcoord, unsigned long long* bkey, unsigned long long* bmask, int* bslot, unsigned* vcnt,
     unsigned long long* __restrict__ vkey, int* __restrict__ tlist, FrameCtr* ctr) {
+    grid_dep_wait();
     using Scan = cub::BlockScan<int, kResolveThreads>;
     __shared__ typename Scan::TempStorage scan_tmp;
     __shared__ unsigned long long s_base;
@@ -293,6 +294,7 @@ __global__ void __launch_bounds__(kSegThreads) k_seg(const int* __restrict__ tli
                                                      unsigned* __restrict__ vseg,
                                                      int* __restrict__ mlist,
                                                      SegStatus* __restrict__ status, FrameCtr* ctr) {
+    grid_dep_wait();
     using Scan = cub::BlockScan<unsigned long long, kSegThreads>;
     __shared__ typename Scan::TempStorage scan_tmp;
     __shared__ unsigned long long s_prefix;
@@ -413,11 +415,11 @@ svx_status cleanup_t(svx_map* m, cudaStream_t s) {
 }  // namespace
 
 svx_status launch_resolve(svx_map* m, cudaStream_t s) {
-    k_resolve<<<kPersistentBlocks, kResolveThreads, 0, s>>>(
+    SVX_CUDA(launch_pdl(k_resolve, kPersistentBlocks, kResolveThreads, 0, s, 
         ptr<unsigned long long>(m->rowkey), ptr<int>(m->rowvid), ptr<int4>(m->hash), ptr<int4>(m->bcoord),
         ptr<unsigned long long>(m->bkey), ptr<unsigned long long>(m->bmask), ptr<int>(m->bslot),
         ptr<unsigned>(m->vcnt), ptr<unsigned long long>(m->vkey), ptr<int>(m->tlist),
-        ptr<FrameCtr>(m->ctr));
+        ptr<FrameCtr>(m->ctr)));
     SVX_LAUNCHED();
     return SVX_OK;
 }
@@ -425,9 +427,9 @@ svx_status launch_resolve(svx_map* m, cudaStream_t s) {
 svx_status launch_segments(svx_map* m, cudaStream_t s) {
     SegStatus* status =
         reinterpret_cast<SegStatus*>(ptr<char>(m->partials) + partials_bytes());
-    k_seg<<<kSegBlocks, kSegThreads, 0, s>>>(ptr<int>(m->tlist), ptr<unsigned>(m->vcnt),
+    SVX_CUDA(launch_pdl(k_seg, kSegBlocks, kSegThreads, 0, s, ptr<int>(m->tlist), ptr<unsigned>(m->vcnt),
                                              ptr<unsigned>(m->vseg), ptr<int>(m->mlist), status,
-                                             ptr<FrameCtr>(m->ctr));
+                                             ptr<FrameCtr>(m->ctr)));
     SVX_LAUNCHED();
     return SVX_OK;
 }

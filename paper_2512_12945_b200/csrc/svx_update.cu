@@ -134,6 +134,7 @@ __global__ void __launch_bounds__(256) k_scatter(UpdateArgs a, const int* __rest
                                                  const unsigned long long* __restrict__ rowkey,
                                                  const int* __restrict__ rowvid,
                                                  int* __restrict__ srid, TD* vt, TC* counts) {
+    grid_dep_wait();
     FrameCtr* ctr = a.ctr;
     if (ctr->abort | ctr->err_cap) return;
     const FrameParams& fp = ctr->p;
@@ -181,6 +182,7 @@ __global__ void __launch_bounds__(256) k_scatter(UpdateArgs a, const int* __rest
 
 template <class TD, class TC>
 __global__ void __launch_bounds__(256) k_update_short(UpdateArgs a, TD* vt, TC* counts) {
+    grid_dep_wait();
     FrameCtr* ctr = a.ctr;
     if (ctr->abort | ctr->err_cap) return;
     const long long L = (long long)ctr->n_list;
@@ -380,6 +382,7 @@ __device__ __forceinline__ void finish_closed(const UpdateArgs& a, TD* vt, TC* c
 template <class TD, class TC>
 __global__ void __launch_bounds__(32 * kWarpsPerCta) k_update_long(UpdateArgs a, TD* vt,
                                                                    TC* counts) {
+    grid_dep_wait();
     __shared__ int sbuf[kWarpsPerCta][kSmemMax];
     FrameCtr* ctr = a.ctr;
     if (ctr->abort | ctr->err_cap) return;
@@ -538,6 +541,7 @@ __device__ __forceinline__ void open_voxel(const UpdateArgs& a, const KeyPack& k
 template <class TD, class TS, class Fe>
 __global__ void __launch_bounds__(32 * kWarpsPerCta) k_update_open(UpdateArgs a, TD* vt, TS* mean,
                                                                    TS* beta) {
+    grid_dep_wait();
     __shared__ int sbuf[kWarpsPerCta][kSmemMax];
     FrameCtr* ctr = a.ctr;
     if (ctr->abort | ctr->err_cap) return;
@@ -561,6 +565,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) k_update_open(UpdateArgs a,
 template <class TD, class TS, class Fe>
 __global__ void __launch_bounds__(32 * kWarpsPerCta) k_update_open_huge(UpdateArgs a, TD* vt,
                                                                         TS* mean, TS* beta) {
+    grid_dep_wait();
     __shared__ int sbuf[kWarpsPerCta][kSmemMax];
     FrameCtr* ctr = a.ctr;
     if (ctr->abort | ctr->err_cap) return;
@@ -625,41 +630,41 @@ constexpr int kLongBlocks = 148 * 4;
 
 template <class TD, class TC>
 svx_status scatter_t(svx_map* m, cudaStream_t s) {
-    k_scatter<TD, TC><<<kPersistentBlocks * 2, 256, 0, s>>>(
+    SVX_CUDA(launch_pdl(k_scatter<TD, TC>, kPersistentBlocks * 2, 256, 0, s, 
         make_args(m), ptr<int>(m->rcnt), ptr<int>(m->rowray), ptr<unsigned long long>(m->rowkey),
-        ptr<int>(m->rowvid), ptr<int>(m->srid), ptr<TD>(m->vt), ptr<TC>(m->s0));
+        ptr<int>(m->rowvid), ptr<int>(m->srid), ptr<TD>(m->vt), ptr<TC>(m->s0)));
     SVX_LAUNCHED();
     return SVX_OK;
 }
 
 template <class TD, class TC>
 svx_status closed_a(svx_map* m, cudaStream_t s) {
-    k_update_short<TD, TC><<<kShortBlocks, 256, 0, s>>>(make_args(m), ptr<TD>(m->vt),
-                                                        ptr<TC>(m->s0));
+    SVX_CUDA(launch_pdl(k_update_short<TD, TC>, kShortBlocks, 256, 0, s, make_args(m), ptr<TD>(m->vt),
+                                                        ptr<TC>(m->s0)));
     SVX_LAUNCHED();
     return SVX_OK;
 }
 
 template <class TD, class TC>
 svx_status closed_b(svx_map* m, cudaStream_t s) {
-    k_update_long<TD, TC><<<kLongBlocks, 32 * kWarpsPerCta, 0, s>>>(make_args(m), ptr<TD>(m->vt),
-                                                                    ptr<TC>(m->s0));
+    SVX_CUDA(launch_pdl(k_update_long<TD, TC>, kLongBlocks, 32 * kWarpsPerCta, 0, s, make_args(m), ptr<TD>(m->vt),
+                                                                    ptr<TC>(m->s0)));
     SVX_LAUNCHED();
     return SVX_OK;
 }
 
 template <class TD, class TS, class Fe>
 svx_status open_a(svx_map* m, cudaStream_t s) {
-    k_update_open<TD, TS, Fe><<<kLongBlocks, 32 * kWarpsPerCta, 0, s>>>(
-        make_args(m), ptr<TD>(m->vt), ptr<TS>(m->s0), ptr<TS>(m->s1));
+    SVX_CUDA(launch_pdl(k_update_open<TD, TS, Fe>, kLongBlocks, 32 * kWarpsPerCta, 0, s, 
+        make_args(m), ptr<TD>(m->vt), ptr<TS>(m->s0), ptr<TS>(m->s1)));
     SVX_LAUNCHED();
     return SVX_OK;
 }
 
 template <class TD, class TS, class Fe>
 svx_status open_b(svx_map* m, cudaStream_t s) {
-    k_update_open_huge<TD, TS, Fe><<<kHugeWarps / kWarpsPerCta, 32 * kWarpsPerCta, 0, s>>>(
-        make_args(m), ptr<TD>(m->vt), ptr<TS>(m->s0), ptr<TS>(m->s1));
+    SVX_CUDA(launch_pdl(k_update_open_huge<TD, TS, Fe>, kHugeWarps / kWarpsPerCta, 32 * kWarpsPerCta, 0, s, 
+        make_args(m), ptr<TD>(m->vt), ptr<TS>(m->s0), ptr<TS>(m->s1)));
     SVX_LAUNCHED();
     return SVX_OK;
 }

@@ -592,15 +592,20 @@ class GridView:
     def content_hash(self):
         """Order-independent digest with the reference's layout (grid.py:204-215)."""
         coords, vals = self.active_values()
-        order = np.lexsort((coords[:, 2], coords[:, 1], coords[:, 0]))
-        hs = hashlib.sha256()
-        hs.update(_MAGIC)
-        hs.update(_params_block(self.payload))
-        hs.update(struct.pack("<dBB", self.voxel_size, LEAF_LOG2, INTERNAL_LOG2))
-        hs.update(np.ascontiguousarray(coords[order]).tobytes())
-        for v in vals:
-            hs.update(np.ascontiguousarray(v[order]).tobytes())
-        return hs.hexdigest()
+        return content_hash_of(coords, vals, self.payload, self.voxel_size)
+
+
+def content_hash_of(coords, vals, payload, voxel_size: float) -> str:
+    """content_hash (grid.py:204-215) of active coords + field arrays."""
+    order = np.lexsort((coords[:, 2], coords[:, 1], coords[:, 0]))
+    hs = hashlib.sha256()
+    hs.update(_MAGIC)
+    hs.update(_params_block(payload))
+    hs.update(struct.pack("<dBB", voxel_size, LEAF_LOG2, INTERNAL_LOG2))
+    hs.update(np.ascontiguousarray(coords[order]).tobytes())
+    for v in vals:
+        hs.update(np.ascontiguousarray(v[order]).tobytes())
+    return hs.hexdigest()
 
 
 def _dtype_code(name) -> int:
