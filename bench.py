@@ -10,7 +10,10 @@ rotations, through Mapper.integrate -> svx_integrate).  Prints ONE JSON line.
 ours:
   value     points integrated/s with inputs resident in HBM; per-step CUDA
             events on the launching stream; L2 flushed (256 MiB write)
-            between steps outside the events; max over ranks.
+            between steps outside the events; max over ranks.  With N > 1
+            (torchrun) the map is sharded by leaf ownership: every rank gets
+            the same frames, marches its slice, and rows go to their owners by
+            NCCL all-to-all (paper_2512_12945_b200/sharded.py; strong scaling).
   e2e       same metric through the public API from pinned HOST buffers:
             H2D of points+labels and D2H of the frame report inside each step.
   roofline  dominant stage (per-stage CUDA events inside libsvx) against the
@@ -136,7 +139,7 @@ class ClockSampler:
 
 # -- byte model (fixed fp32 state layout) ----------------------------
 
-def frame_bytes(rep, kind, C=0, D=0):
+def frame_bytes(used, touched, kind, C=0, D=0):
     """bytes_frame = N_used*(12+P) + 2*U*S."""
     if kind == "closed":
         P, S = 4, 8 + 4 * C
@@ -144,7 +147,7 @@ def frame_bytes(rep, kind, C=0, D=0):
         P, S = 4 * D, 8 + 8 * D
     else:
         P, S = 0, 8
-    return rep.points_used * (12 + P) + 2 * rep.touched_voxels * S
+    return used * (12 + P) + 2 * touched * S
 
 
 def stage_bytes(stage, rep, kind, C, D, tsdf_elem):
@@ -231,11 +234,15 @@ def run_ours(args):
 
         dist.init_process_group("nccl", device_id=dev)
     from paper_2512_12945_b200 import Mapper, _lib
+    from paper_2512_12945_b200.sharded import DistTransport, ShardedMapper
 
     K, W = args.steps, args.warmup
-    P = args.profile_frames
-    # replicas: rank r integrates its own stream of frames (weak scaling)
-    wl, frames = make_frames(args.config, W + K + P, dev, start=rank * (W + K + P))
+    # N > 1: one map sharded by leaf ownership; every rank gets the same frame
+    # stream, marches its slice and exchanges rows over NCCL (strong scaling:
+    # the work per frame is fixed).  Stage profiling covers the 1-GPU path.
+    sharded = world > 1
+    P = 0 if sharded else args.profile_frames
+    wl, frames = make_frames(args.config, W + K + P, dev)
     kw = dict(wl.mapper_kwargs, tsdf_dtype=args.tsdf_dtype, device=local)
     kind = sem_kind_of(kw)
     C = kw.get("num_classes", 0)
@@ -248,11 +255,17 @@ def run_ours(args):
             pts, lab, feat = host
         else:
             pts, lab, feat = f.points, f.labels, f.features
+        extra = {"reduce_report": False} if sharded else {}
         return m.integrate(pts, f.pose, labels=lab if kind == "closed" else None,
-                           features=feat if kind == "open" else None)
+                           features=feat if kind == "open" else None, **extra)
+
+    def new_map():
+        if sharded:
+            return ShardedMapper(**kw, rank=rank, world=world, transport=DistTransport())
+        return Mapper(**kw)
 
     # ---- device-resident pass ------------------------------------------------------
-    m = Mapper(**kw)
+    m = new_map()
     for f in frames[:W]:
         integrate(m, f)
     # pool headroom for the timed frames, so no growth copy lands inside them
@@ -280,14 +293,15 @@ def run_ours(args):
         torch.distributed.barrier()
     step_ms = [a.elapsed_time(b) for a, b in evs]
     total_ms = sum(step_ms)
-    used = sum(r.points_used for r in reps)
+    used = sum(r.points_used for r in reps)   # whole frames (global counts) in both modes
+    touched = sum(r.touched_voxels for r in reps)
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-    u = torch.tensor([used], dtype=torch.float64, device=dev)
-    if world > 1:
+    tv = torch.tensor([touched], dtype=torch.float64, device=dev)
+    if sharded:
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        torch.distributed.all_reduce(u)
-    total_ms_max, used_all = float(t.item()), float(u.item())
-    value = used_all / (total_ms_max / 1e3)
+        torch.distributed.all_reduce(tv)   # each voxel is owned by one rank
+    total_ms_max, touched_all = float(t.item()), float(tv.item())
+    value = used / (total_ms_max / 1e3)
 
     # ---- per-stage device times: a separate eager pass over P further frames -------
     m.set_profiling(True)
@@ -307,8 +321,8 @@ def run_ours(args):
     dom_bytes = statistics.mean(stage_bytes(dom, r, kind, C, D, tsdf_elem) for r in prof_reps)
     peak, peak_src = measured_peak()
     achieved = dom_bytes / (mean_stage[dom] / 1e3) / 1e9 if mean_stage[dom] > 0 else 0.0
-    fb = statistics.mean(frame_bytes(r, kind, C, D) for r in reps)
-    frame_gbs = fb / (statistics.mean(step_ms) / 1e3) / 1e9
+    fb = frame_bytes(used / K, touched_all / K, kind, C, D)   # mean frame, global counts
+    frame_gbs = fb / (total_ms_max / K / 1e3) / 1e9
     traffic = ncu_traffic(dom)
 
     # ---- e2e pass: host pinned buffers through the public API ---------------------------
@@ -327,7 +341,7 @@ def run_ours(args):
                 feat.copy_(f.features)
             host.append((pts.numpy(), lab.numpy() if lab is not None else None,
                          feat.numpy() if feat is not None else None))
-        m2 = Mapper(**kw)
+        m2 = new_map()
         for f, h in zip(frames[:W], host[:W]):
             integrate(m2, f, h)
         st = m2.engine_stats()
@@ -351,11 +365,9 @@ def run_ours(args):
             e_used += r.points_used
             h2d += sum(x.nbytes for x in host[W + i] if x is not None)
         te = torch.tensor([e_ms], dtype=torch.float64, device=dev)
-        ue = torch.tensor([e_used], dtype=torch.float64, device=dev)
         if world > 1:
             torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
-            torch.distributed.all_reduce(ue)
-        e2e = {"value": float(ue.item()) / (float(te.item()) / 1e3), "unit": UNIT,
+        e2e = {"value": e_used / (float(te.item()) / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d // K), "d2h_bytes_per_step": 136,
                "ms_per_step": float(te.item()) / K}
         del m2
@@ -375,26 +387,34 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
             "warmup": W, "ms_per_step": total_ms_max / K, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
             "config": {
                 "workload": wl.name, "points_per_frame": wl.points_per_frame,
                 "voxel_size": kw["voxel_size"], "truncation": kw["truncation"],
                 "num_classes": C or None, "feature_dim": D or None,
-                "tsdf_dtype": args.tsdf_dtype, "api": "Mapper.integrate -> svx_integrate",
-                "parallelism": f"replicas{world}" if world > 1 else "single",
+                "tsdf_dtype": args.tsdf_dtype,
+                "api": ("ShardedMapper.integrate -> svx_shard_{march,plan,pack,apply} + NCCL "
+                        "all-to-all" if sharded else "Mapper.integrate -> svx_integrate"),
+                "parallelism": f"leaf-shard{world}" if sharded else "single",
                 "l2": "flushed between steps (256 MiB write, outside step events)",
                 "frames_timed": f"{W}..{W + K - 1}",
             },
             "ms_per_frame_p50": statistics.median(step_ms),
             "points_used_per_frame": used / K,
-            "touched_voxels_per_frame": statistics.mean(r.touched_voxels for r in reps),
+            "touched_voxels_per_frame": touched_all / K,
             "band_rows_per_frame": statistics.mean(r.band_hits for r in reps),
-            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
-                         "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
-                         "peak_source": peak_src,
-                         "bytes_per_launch": dom_bytes, "ms_per_launch": mean_stage[dom]},
+            "roofline": ({"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+                          "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                          "peak_source": peak_src,
+                          "bytes_per_launch": dom_bytes, "ms_per_launch": mean_stage[dom]}
+                         if not sharded else
+                         {"bound": "hbm", "kernel": "whole frame (per-rank peak x ranks)",
+                          "achieved": frame_gbs, "peak": peak * world, "unit": "GB/s",
+                          "frac": frame_gbs / (peak * world), "traffic": None,
+                          "peak_source": peak_src}),
             "frame_roofline": {"bytes_per_frame": fb, "achieved": frame_gbs, "unit": "GB/s",
-                               "frac": frame_gbs / peak,
+                               "frac": frame_gbs / (peak * world),
                                "model": "N_used*(12+P) + 2*U*S, fp32 state (SURVEY 8d)"},
             "stages_ms": {s: round(mean_stage[s], 4) for s in stages},
             "cpu_baseline": cpu,

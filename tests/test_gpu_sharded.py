@@ -234,3 +234,64 @@ def test_empty_and_tiny_frames():
         assert np.array_equal(report_rows([r1]), report_rows([r2]))
     _assert_union_equals(single, shards)
     assert all(s.stats()["frames_integrated"] == 3 for s in shards)
+
+
+def _dist_worker(rank, world, port, kw, seed, out):
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2512_12945_b200.sharded import DistTransport, ShardedMapper
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        m = ShardedMapper(**kw, rank=rank, world=world, transport=DistTransport())
+        rng = np.random.default_rng(seed)
+        reps = []
+        for pts, origin in _frames(seed, 3000, 3):
+            lab, _ = _payload(kw, rng, pts.shape[0])
+            reps.append(m.integrate_world(pts, origin, labels=lab))
+        merged = m.global_export()
+        out.put((rank, report_rows(reps).tolist(),
+                 None if merged is None else [a.tobytes() for a in merged if a is not None]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_dist_driver_two_processes_gloo():
+    """ShardedMapper.integrate through DistTransport in two processes (gloo
+    collectives; both ranks on cuda:0, kernels independent) == one Mapper."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    from paper_2512_12945_b200 import Mapper
+
+    kw = CASES["closed"]
+    seed = 21
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_dist_worker, args=(r, 2, port, kw, seed, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict((r[0], r[1:]) for r in (q.get(timeout=300) for _ in range(2)))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    single = Mapper(**kw)
+    rng = np.random.default_rng(seed)
+    reps = []
+    for pts, origin in _frames(seed, 3000, 3):
+        lab, _ = _payload(kw, rng, pts.shape[0])
+        reps.append(single.integrate_world(pts, origin, labels=lab))
+    for r in range(2):
+        assert res[r][0] == report_rows(reps).tolist()
+    assert res[0][1] == [a.tobytes() for a in single._export() if a is not None]
+    assert res[1][1] is None
