@@ -106,6 +106,8 @@ typedef struct {
     int64_t hash_capacity;
     int64_t voxel_capacity;
     int64_t block_capacity;
+    int64_t frames_slot_mode;     /* frames finished in slot mode (svx_set_update_mode) */
+    int64_t slot_overflow_reruns; /* slot-mode attempts re-run in segment mode */
 } svx_stats;
 
 typedef struct svx_map svx_map;
@@ -259,6 +261,21 @@ svx_status svx_label_map(svx_map* map, int32_t mode, int64_t capacity, int32_t* 
  * number of stages (SVX_N_STAGES). */
 #define SVX_N_STAGES 5
 svx_status svx_set_profiling(svx_map* map, int32_t enable);
+
+/* Row-grouping strategy of closed-set / geometry maps with bounded bands.
+ *   SVX_UPDATE_AUTO      slot mode while recent frames average <= 3 rows per
+ *                        touched voxel (LiDAR), segment mode otherwise
+ *   SVX_UPDATE_SEGMENTS  always segments (K3 scan, K4 scatter, K5 sorted update)
+ *   SVX_UPDATE_SLOTS     always try slot mode (K2 writes point indices into the
+ *                        voxel's 16-entry slot record; K5 per touched voxel)
+ * A slot-mode frame with a voxel of more than 16 rows stops before any payload
+ * changes and is re-run in segment mode, so all three give identical maps.
+ * Open-set and space-carving maps always use segments.  The reference has no
+ * equivalent knob (its grouping is one sort, _core.pyx:707-753). */
+#define SVX_UPDATE_AUTO 0
+#define SVX_UPDATE_SEGMENTS 1
+#define SVX_UPDATE_SLOTS 2
+svx_status svx_set_update_mode(svx_map* map, int32_t mode);
 int32_t svx_stage_times(svx_map* map, double* ms, int32_t n);
 
 const char* svx_last_error(void);

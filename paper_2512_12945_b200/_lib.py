@@ -66,6 +66,8 @@ class SvxStats(ctypes.Structure):
         ("hash_capacity", ctypes.c_int64),
         ("voxel_capacity", ctypes.c_int64),
         ("block_capacity", ctypes.c_int64),
+        ("frames_slot_mode", ctypes.c_int64),
+        ("slot_overflow_reruns", ctypes.c_int64),
     ]
 
 
@@ -112,6 +114,7 @@ _SIGNATURES = {
     "svx_classify": [_P, _P, _I32, _D, _D, _I64, _P, _P, _P, _P],
     "svx_label_map": [_P, _I32, _I64, _P, _P],
     "svx_set_profiling": [_P, _I32],
+    "svx_set_update_mode": [_P, _I32],
     "svx_reserve": [_P, _I64, _I64],
     "svx_shard_march": [_P, _P, _I32, _I64, ctypes.POINTER(_D), ctypes.POINTER(_D), _P, _P, _I32,
                         ctypes.POINTER(_I64), _P, ctypes.POINTER(SvxShardSummary)],

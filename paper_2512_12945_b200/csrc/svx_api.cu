@@ -177,7 +177,7 @@ svx_status svx_destroy(svx_map* m) {
     if (!m) return SVX_OK;
     cudaSetDevice(m->cfg.device);
     DevBuf* bufs[] = {&m->hash, &m->bcoord, &m->bkey, &m->bmask, &m->bslot, &m->vt,
-                      &m->s0, &m->s1, &m->vcnt, &m->vseg, &m->vcur, &m->vkey, &m->in_pts,
+                      &m->s0, &m->s1, &m->vcnt, &m->vseg, &m->vcur, &m->vkey, &m->vslot, &m->in_pts,
                       &m->in_lab, &m->in_feat, &m->ray, &m->rcnt, &m->roff, &m->rowkey,
                       &m->rowvid, &m->rowray, &m->partials, &m->tlist, &m->mlist,
                       &m->longlist, &m->srid, &m->bitmap, &m->cubtmp, &m->ctr, &m->ord0,
@@ -188,7 +188,8 @@ svx_status svx_destroy(svx_map* m) {
     if (m->ev0) cudaEventDestroy(m->ev0);
     if (m->ev1) cudaEventDestroy(m->ev1);
     if (m->ev_in) cudaEventDestroy(m->ev_in);
-    if (m->gexec) cudaGraphExecDestroy(m->gexec);
+    for (cudaGraphExec_t g : m->gexec)
+        if (g) cudaGraphExecDestroy(g);
     if (m->gstream) cudaStreamDestroy(m->gstream);
     for (cudaEvent_t e : m->st_ev)
         if (e) cudaEventDestroy(e);
@@ -248,6 +249,13 @@ svx_status svx_set_profiling(svx_map* m, int32_t enable) {
     return SVX_OK;
 }
 
+svx_status svx_set_update_mode(svx_map* m, int32_t mode) {
+    if (!m) return fail(SVX_E_INPUT, "null argument");
+    if (mode < SVX_UPDATE_AUTO || mode > SVX_UPDATE_SLOTS) return fail(SVX_E_INPUT, "unknown update mode");
+    m->mode_pref = mode;
+    return SVX_OK;
+}
+
 int32_t svx_stage_times(svx_map* m, double* ms, int32_t n) {
     if (!m) return 0;
     for (int i = 0; i < n && i < SVX_N_STAGES; ++i) ms[i] = m->stage_ms[i];
@@ -267,6 +275,8 @@ svx_status svx_stats_get(svx_map* m, svx_stats* out) {
     out->hash_capacity = m->hcap;
     out->voxel_capacity = m->vcap;
     out->block_capacity = m->bcap;
+    out->frames_slot_mode = m->n_slot_frames;
+    out->slot_overflow_reruns = m->n_slot_reruns;
     return SVX_OK;
 }
 

@@ -74,6 +74,8 @@ svx_status reserve_voxels(svx_map* m, int64_t need, cudaStream_t s) {
     SVX_TRY(ensure(m->vcur, 4 * cap, s, true, 0));
     SVX_TRY(ensure(m->vseg, 4 * cap, s, true));
     SVX_TRY(ensure(m->vkey, 8 * cap, s, true));
+    if (m->cfg.sem_kind != SVX_SEM_OPEN && !m->cfg.space_carving)   // per-frame contents only
+        SVX_TRY(ensure(m->vslot, sizeof(int) * kSlots * cap, s));
     m->vcap = cap;
     return SVX_OK;
 }
@@ -134,7 +136,7 @@ static unsigned long long graph_signature(const svx_map* m, int pts_f64, int fea
                           m->srid.p,   m->bitmap.p, m->cubtmp.p,  m->hash.p,   m->bcoord.p,
                           m->bkey.p,   m->bmask.p,  m->bslot.p,   m->vt.p,     m->s0.p,
                           m->s1.p,     m->vcnt.p,   m->vseg.p,    m->vcur.p,   m->vkey.p,
-                          m->ctr.p};
+                          m->vslot.p,  m->ctr.p};
     unsigned long long h = 1469598103934665603ULL;
     auto mix = [&](unsigned long long v) {
         h ^= v;
@@ -162,6 +164,14 @@ static svx_status enqueue_frame(svx_map* m, int pts_f64, int feats_f64, cudaStre
     STAGE_END(0);
     STAGE_BEGIN(1);
     SVX_TRY(launch_resolve(m, s));
+    if (m->frame_slots) {
+        STAGE_END(1);
+        STAGE_BEGIN(3);
+        SVX_TRY(launch_update_slots(m, s));
+        STAGE_END(3);
+        SVX_CUDA(cudaMemcpyAsync(m->h_ctr, dc, sizeof(FrameCtr), cudaMemcpyDeviceToHost, s));
+        return SVX_OK;
+    }
     SVX_TRY(launch_segments(m, s));
     STAGE_END(1);
     STAGE_BEGIN(2);
@@ -203,10 +213,12 @@ static svx_status run_frame(svx_map* m, int pts_f64, int feats_f64, cudaStream_t
         return SVX_OK;
     }
     const unsigned long long sig = graph_signature(m, pts_f64, feats_f64);
-    if (!m->gexec || sig != m->gsig) {
-        if (m->gexec) {
-            cudaGraphExecDestroy(m->gexec);
-            m->gexec = nullptr;
+    const int gm = m->frame_slots ? 1 : 0;
+    cudaGraphExec_t& gexec = m->gexec[gm];
+    if (!gexec || sig != m->gsig[gm]) {
+        if (gexec) {
+            cudaGraphExecDestroy(gexec);
+            gexec = nullptr;
         }
         SVX_CUDA(cudaStreamBeginCapture(m->gstream, cudaStreamCaptureModeThreadLocal));
         svx_status st = enqueue_frame(m, pts_f64, feats_f64, m->gstream);
@@ -217,18 +229,18 @@ static svx_status run_frame(svx_map* m, int pts_f64, int feats_f64, cudaStream_t
             return st;
         }
         if (e != cudaSuccess) return fail(SVX_E_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
-        e = cudaGraphInstantiate(&m->gexec, g, 0);
+        e = cudaGraphInstantiate(&gexec, g, 0);
         cudaGraphDestroy(g);
         if (e != cudaSuccess) {
-            m->gexec = nullptr;
+            gexec = nullptr;
             return fail(SVX_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
         }
-        m->gsig = sig;
+        m->gsig[gm] = sig;
     }
     SVX_CUDA(cudaEventRecord(m->ev_in, s));
     SVX_CUDA(cudaStreamWaitEvent(m->gstream, m->ev_in, 0));
-    SVX_CUDA(cudaGraphLaunch(m->gexec, m->gstream));
-    count_launch(8);
+    SVX_CUDA(cudaGraphLaunch(gexec, m->gstream));
+    count_launch(gm ? 3 : 6);
     SVX_CUDA(cudaEventRecord(m->ev1, m->gstream));
     SVX_CUDA(cudaEventSynchronize(m->ev1));
     return SVX_OK;
@@ -278,6 +290,7 @@ void reset_ctr(svx_map* m) {
     p.frame = (int)m->frames;
     p.maxrows = m->maxrows;
     p.inline_singles = inline_singles(m);
+    p.slots = m->frame_slots;
     p.seq = ++m->seq;
 }
 
@@ -296,6 +309,33 @@ svx_status recover_capacity(svx_map* m, int64_t nblocks0, cudaStream_t s) {
     return SVX_OK;
 }
 
+// Slot mode stopped before any payload change (a voxel got more than kSlots
+// rows): same cleanup as a capacity abort, then the caller re-runs the frame
+// in segment mode and stays there for a while.
+svx_status recover_slots(svx_map* m, int64_t nblocks0, cudaStream_t s) {
+    FrameCtr* hc = m->h_ctr;
+    SVX_TRY(launch_cleanup(m, s));
+    SVX_CUDA(cudaStreamSynchronize(s));
+    m->nblocks = (int64_t)std::min<unsigned long long>(hc->nblocks, (unsigned long long)m->bcap);
+    m->nvox = (int64_t)std::min<unsigned long long>(hc->nvox, (unsigned long long)m->vcap);
+    m->ord_nblocks = std::min<int64_t>(m->ord_nblocks, nblocks0);
+    m->slot_hold = 32;
+    m->frame_retry_segments = 1;
+    m->n_slot_reruns++;
+    return SVX_OK;
+}
+
+// Slot mode for bounded-band closed/geometry maps whose recent frames fit
+// kSlots rows per voxel (LiDAR: ~1.6 rows per voxel); depth cameras (~17
+// rows per voxel), open-set and carving maps use segments.
+int choose_slots(const svx_map* m) {
+    if (m->cfg.sem_kind == SVX_SEM_OPEN || m->cfg.space_carving || m->maxrows <= 0) return 0;
+    if (m->mode_pref == SVX_UPDATE_SEGMENTS) return 0;
+    if (m->mode_pref == SVX_UPDATE_SLOTS) return m->frame_retry_segments ? 0 : 1;
+    if (m->slot_hold > 0) return 0;
+    return m->last_rows <= 3 * m->last_touched ? 1 : 0;
+}
+
 // Report fields of the map side and the capacities for the next frame.
 void finish_frame(svx_map* m, int64_t nblocks0, int64_t nvox0, svx_report& r) {
     FrameCtr* hc = m->h_ctr;
@@ -306,6 +346,10 @@ void finish_frame(svx_map* m, int64_t nblocks0, int64_t nvox0, svx_report& r) {
     m->nblocks = (int64_t)hc->nblocks;
     m->nvox = (int64_t)hc->nvox;
     m->frames++;
+    m->n_slot_frames += m->frame_slots;
+    m->last_rows = (int64_t)hc->rows;
+    m->last_touched = (int64_t)hc->n_touched;
+    if (m->slot_hold > 0) --m->slot_hold;
     // row capacity for the next frame: 1.5x this one's rows
     const uint64_t need = hc->rows + hc->rows / 2 + 4096;
     if (hc->rows * 10 > m->rcap * 8 || need * 3 < m->rcap) m->rcap = need;
@@ -353,10 +397,12 @@ svx_status integrate_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n
     // counts before this frame (stamps, report); m->nblocks / m->nvox stay the
     // live counts, including what a capacity-aborted attempt allocated
     const int64_t nblocks0 = m->nblocks, nvox0 = m->nvox;
+    m->frame_retry_segments = 0;
     for (int attempt = 0;; ++attempt) {
         if (attempt >= 8) return fail(SVX_E_INTERNAL, "frame scratch could not be sized");
         SVX_TRY(reserve_frame(m, n, s));
         SVX_TRY(reserve_pools(m, s));
+        m->frame_slots = choose_slots(m);
         reset_ctr(m);
         FrameParams& p = hc->p;
         p.pts = pts;
@@ -398,6 +444,10 @@ svx_status integrate_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n
         }
         if (hc->err_cap) {
             SVX_TRY(recover_capacity(m, nblocks0, s));
+            continue;
+        }
+        if (hc->err_slots) {
+            SVX_TRY(recover_slots(m, nblocks0, s));
             continue;
         }
         break;

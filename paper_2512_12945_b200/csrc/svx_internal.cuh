@@ -38,6 +38,12 @@ constexpr int kHashEmpty = -1;
 constexpr int kHashBusy = -2;
 
 constexpr int kShortMax = 16;   // segments up to this many rows: thread-per-voxel update
+// Slot mode (LiDAR-like frames, few rows per voxel): K2 writes each row's point
+// index straight into its voxel's slot record (kSlots ints, one 64-byte line)
+// and one thread per touched voxel finishes it -- no segment scan, no scatter.
+// A voxel with more rows stops the attempt before any payload changes; the
+// frame re-runs in segment mode.
+constexpr int kSlots = 16;
 
 struct PoseParams {
     double R[9];
@@ -69,6 +75,7 @@ struct FrameParams {
     int frame;                 // creation stamp for new leaves
     int maxrows;               // row slots per ray; 0 = dense rows (two-pass walk)
     int inline_singles;        // single-row voxels updated in the scatter (closed/geometry)
+    int slots;                 // 1: slot mode (K2 fills vslot; K5 = k_update_slots)
     unsigned seq;              // launch sequence number (epoch of the segment-scan status)
 };
 
@@ -108,7 +115,7 @@ struct FrameCtr {
     int err_cap;                    // a pool / list / row buffer was too small (grow, retry)
     int err_rows;                   // a band exceeded maxrows (retry with dense rows)
     int abort;                      // set by the gate: skip all mutation
-    int pad;
+    int err_slots;                  // slot mode: a voxel got more than kSlots rows (re-run in segment mode)
 };
 
 // Per-voxel frame state (indexed by voxel id, zero between frames):
@@ -171,6 +178,13 @@ struct svx_map {
     svx::DevBuf bcoord, bkey, bmask, bslot;  int64_t bcap = 0, nblocks = 0;
     svx::DevBuf vt, s0, s1;                  int64_t vcap = 0, nvox = 0;  // vt: {d, w} per voxel
     svx::DevBuf vcnt, vseg, vcur, vkey;      // per-voxel frame state (see FrameCtr)
+    svx::DevBuf vslot;                       // slot mode: kSlots point indices per voxel
+    int64_t n_slot_frames = 0, n_slot_reruns = 0;
+    int mode_pref = 0;      // SVX_UPDATE_AUTO / SEGMENTS / SLOTS
+    int slot_hold = 0;      // frames to stay in segment mode after a slot overflow
+    int64_t last_rows = 0, last_touched = 0;   // previous frame's rows and touched voxels
+    int frame_slots = 0;    // mode of the attempt being run
+    int frame_retry_segments = 0;   // this frame overflowed its slots: re-run with segments
     int64_t frames = 0;
     unsigned seq = 0;   // frame launches so far (attempts included)
     // per-frame scratch
@@ -183,8 +197,8 @@ struct svx_map {
     int64_t npts_cap = 0;  // points the per-ray scratch holds
     // captured frame graph (replayed while the layout is unchanged)
     cudaStream_t gstream = nullptr;
-    cudaGraphExec_t gexec = nullptr;
-    unsigned long long gsig = 0;
+    cudaGraphExec_t gexec[2] = {nullptr, nullptr};   // per mode: segment, slot
+    unsigned long long gsig[2] = {0, 0};
     svx::DevBuf cubtmp;
     svx::DevBuf ctr;      // FrameCtr
     svx::FrameCtr* h_ctr = nullptr;  // pinned mirror
@@ -356,6 +370,7 @@ inline int inline_singles(const svx_map* m) { return m->cfg.sem_kind != SVX_SEM_
 svx_status launch_scatter(svx_map* m, cudaStream_t s);
 svx_status launch_update_a(svx_map* m, int feats_f64, cudaStream_t s);
 svx_status launch_update_b(svx_map* m, int feats_f64, cudaStream_t s);
+svx_status launch_update_slots(svx_map* m, cudaStream_t s);
 svx_status launch_rehash(svx_map* m, int4* new_table, int64_t new_cap, cudaStream_t s);
 int huge_warps();
 
@@ -365,6 +380,8 @@ svx_status reserve_frame(svx_map* m, int64_t n, cudaStream_t s);
 svx_status reserve_pools(svx_map* m, cudaStream_t s);
 void reset_ctr(svx_map* m);
 svx_status recover_capacity(svx_map* m, int64_t nblocks0, cudaStream_t s);
+svx_status recover_slots(svx_map* m, int64_t nblocks0, cudaStream_t s);
+int choose_slots(const svx_map* m);
 void finish_frame(svx_map* m, int64_t nblocks0, int64_t nvox0, svx_report& r);
 KeyPack default_key_pack(const svx_map* m, const PoseParams& pp);
 

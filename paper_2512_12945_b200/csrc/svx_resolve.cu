@@ -122,8 +122,9 @@ __device__ int leaf_find_or_insert(int4* table, long long mask, int a, int b, in
 // another CTA (BUSY) is waited for after this tile's own claims are
 // published, so no thread ever waits across a barrier.
 __global__ void __launch_bounds__(kResolveThreads) k_resolve(
-    const unsigned long long* __restrict__ rowkey, int* __restrict__ rowvid, int4* table,
-    int4* bcoord, unsigned long long* bkey, unsigned long long* bmask, int* bslot, unsigned* vcnt,
+    const unsigned long long* __restrict__ rowkey, const int* __restrict__ rowray,
+    int* __restrict__ rowvid, int* __restrict__ vslot, int4* table, int4* bcoord,
+    unsigned long long* bkey, unsigned long long* bmask, int* bslot, unsigned* vcnt,
     unsigned long long* __restrict__ vkey, int* __restrict__ tlist, FrameCtr* ctr) {
     grid_dep_wait();
     using Scan = cub::BlockScan<int, kResolveThreads>;
@@ -135,12 +136,14 @@ __global__ void __launch_bounds__(kResolveThreads) k_resolve(
     const KeyPack kp = fp.kp;
     const long long hmask = fp.hmask, bcap = fp.bcap, vcap = fp.vcap, nblocks0 = fp.nblocks0;
     const int frame = fp.frame;
+    const bool slots = fp.slots != 0;
     const int lane = threadIdx.x & 31;
     const unsigned full = 0xffffffffu;
     for (long long tile = blockIdx.x; tile * kResolveThreads < total; tile += gridDim.x) {
         const long long t = tile * kResolveThreads + threadIdx.x;
         const bool valid = t < total;
         const unsigned long long key = valid ? rowkey[t] : kKeyEmpty;
+        const int pidx = (valid && slots) ? rowray[t] : 0;
         long long x = 0, y = 0, z = 0;
         if (valid) unpack_key(key, kp, x, y, z);
         const unsigned vpeers = __match_any_sync(full, valid ? key : (kKeyEmpty ^ (unsigned long long)lane));
@@ -251,9 +254,11 @@ __global__ void __launch_bounds__(kResolveThreads) k_resolve(
 
         // ---- counts; the voxel's first toucher this frame lists it
         bool first = false;
+        unsigned cbase = 0;
         if (is_vl && vid >= 0) {
             const unsigned c = atomicAdd(&vcnt[vid], (unsigned)__popc(vpeers) + (created ? kNewBit : 0u));
-            first = (c & ~kNewBit) == 0u;
+            cbase = c & ~kNewBit;
+            first = cbase == 0u;
         }
         Scan(scan_tmp).ExclusiveSum(first ? 1 : 0, rank, cnt);
         if (threadIdx.x == 0 && cnt) s_base = atomicAdd(&ctr->n_touched, (unsigned long long)cnt);
@@ -263,7 +268,17 @@ __global__ void __launch_bounds__(kResolveThreads) k_resolve(
             tlist[s_base + rank] = vid;
         }
         vid = __shfl_sync(full, vid, vleader);
-        if (valid) rowvid[t] = vid;
+        if (slots) {
+            // this row's rank among the voxel's rows = its slot (order is
+            // restored by point index in k_update_slots)
+            cbase = __shfl_sync(full, cbase, vleader) + __popc(vpeers & ((1u << lane) - 1u));
+            if (valid && vid >= 0) {
+                if (cbase < (unsigned)kSlots) vslot[(long long)vid * kSlots + cbase] = pidx;
+                else ctr->err_slots = 1;
+            }
+        } else if (valid) {
+            rowvid[t] = vid;
+        }
         __syncthreads();
     }
 }
@@ -416,7 +431,8 @@ svx_status cleanup_t(svx_map* m, cudaStream_t s) {
 
 svx_status launch_resolve(svx_map* m, cudaStream_t s) {
     SVX_CUDA(launch_pdl(k_resolve, kPersistentBlocks, kResolveThreads, 0, s, 
-        ptr<unsigned long long>(m->rowkey), ptr<int>(m->rowvid), ptr<int4>(m->hash), ptr<int4>(m->bcoord),
+        ptr<unsigned long long>(m->rowkey), ptr<int>(m->rowray), ptr<int>(m->rowvid), ptr<int>(m->vslot),
+        ptr<int4>(m->hash), ptr<int4>(m->bcoord),
         ptr<unsigned long long>(m->bkey), ptr<unsigned long long>(m->bmask), ptr<int>(m->bslot),
         ptr<unsigned>(m->vcnt), ptr<unsigned long long>(m->vkey), ptr<int>(m->tlist),
         ptr<FrameCtr>(m->ctr)));

@@ -545,6 +545,7 @@ svx_status shard_apply(svx_map* m, const void* recv, const int64_t* recv_bytes, 
         p.pp = m->shard_pp;
         p.kp = m->shard_kp;
         p.nblocks0 = nblocks0;
+        p.slots = 0;   // shard sections always take the segment path
         hc->rows = (unsigned long long)R;
         hc->rows_alloc = (unsigned long long)R;
         FrameCtr* dc = ptr<FrameCtr>(m->ctr);

@@ -237,6 +237,136 @@ __global__ void __launch_bounds__(256) k_update_short(UpdateArgs a, TD* vt, TC* 
     }
 }
 
+// ---- K5 slot mode: one thread per touched voxel (closed / geometry) --------------
+// Rows arrive in vslot in arbitrary order; a fixed compare-exchange network
+// (bitonic, N in {2, 4, 8, 16}) puts their point indices in ascending order in
+// registers, then the sums run sequentially exactly as in k_update_short.
+// Every load a voxel needs (count, key, slots, TSDF pair) is issued before
+// the first use, and the k ray gathers are issued back to back.
+
+template <int N>
+__device__ __forceinline__ void sort_net(int (&r)[N]) {
+#pragma unroll
+    for (int kk = 2; kk <= N; kk <<= 1) {
+#pragma unroll
+        for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+#pragma unroll
+            for (int i = 0; i < N; ++i) {
+                const int l = i ^ jj;
+                if (l > i) {
+                    const int a = r[i], b = r[l];
+                    const bool up = (i & kk) == 0;
+                    r[i] = up ? min(a, b) : max(a, b);
+                    r[l] = up ? max(a, b) : min(a, b);
+                }
+            }
+        }
+    }
+}
+
+template <int N, class TD, class TC>
+__device__ __forceinline__ void slot_voxel(const UpdateArgs& a, const int* __restrict__ vslot,
+                                           const int32_t* __restrict__ labels, const KeyPack& kp,
+                                           const PoseParams& pp, TD* vt, TC* counts, int vid,
+                                           unsigned k, bool isnew, unsigned long long key,
+                                           typename Pair<TD>::type st, bool closed) {
+    int r[N];
+    const int* sl = vslot + (long long)vid * kSlots;
+    if (N == 2) {
+        const int2 v = *reinterpret_cast<const int2*>(sl);
+        r[0] = v.x;
+        r[1] = k > 1u ? v.y : 0x7fffffff;
+    } else {
+#pragma unroll
+        for (int q = 0; q < N / 4; ++q) {
+            const int4 v = reinterpret_cast<const int4*>(sl)[q];
+            r[4 * q + 0] = (unsigned)(4 * q + 0) < k ? v.x : 0x7fffffff;
+            r[4 * q + 1] = (unsigned)(4 * q + 1) < k ? v.y : 0x7fffffff;
+            r[4 * q + 2] = (unsigned)(4 * q + 2) < k ? v.z : 0x7fffffff;
+            r[4 * q + 3] = (unsigned)(4 * q + 3) < k ? v.w : 0x7fffffff;
+        }
+    }
+    sort_net<N>(r);
+    // gathers in chunks of 4 rows (registers stay bounded for N = 8, 16)
+    const Center cc = center_of(key, kp, a.h, pp);
+    double sw = 0.0, swd = 0.0, mind = INFINITY, maxd = -INFINITY;
+    TC* crow = counts + (long long)vid * a.C;
+    int last = 0;
+#pragma unroll
+    for (int j0 = 0; j0 < N; j0 += 4) {
+        if ((unsigned)j0 < k) {
+            double4 ry[4];
+            int lab[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if (j0 + q < N && (unsigned)(j0 + q) < k) {
+                    ry[q] = a.ray[r[j0 + q]];
+                    lab[q] = closed ? labels[r[j0 + q]] : 0;
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if (j0 + q < N && (unsigned)(j0 + q) < k) {
+                    double d, w;
+                    row_dw(cc.x, cc.y, cc.z, ry[q], a.trunc, a.wfn, d, w);
+                    sw += w;
+                    swd += w * d;
+                    mind = d < mind ? d : mind;
+                    maxd = d > maxd ? d : maxd;
+                    if (closed) {
+                        if (a.last_wins) last = lab[q];
+                        else atomicAdd(&crow[lab[q] - 1], (TC)1);   // integer count: order-free
+                    }
+                }
+            }
+        }
+    }
+    // apply_tsdf (_pycore.py:399-417) on the pre-loaded pair
+    if (isnew) {
+        st.x = (TD)a.trunc;
+        st.y = (TD)0;
+    }
+    const double w_old = (double)st.y, d_old = (double)st.x;
+    const double w_new = w_old + sw;
+    double d_new = w_new > 0.0 ? (w_old * d_old + swd) / w_new : d_old;
+    if ((mind == maxd) && (w_old == 0.0 || equals_stored<TD>(st.x, mind))) d_new = mind;
+    typename Pair<TD>::type out;
+    out.x = (TD)d_new;
+    out.y = (TD)w_new;
+    reinterpret_cast<typename Pair<TD>::type*>(vt)[vid] = out;
+    if (closed && a.last_wins)
+        for (int q = 0; q < a.C; ++q) crow[q] = (TC)(q == last - 1 ? 1 : 0);
+}
+
+template <class TD, class TC>
+__global__ void __launch_bounds__(256, 3) k_update_slots(UpdateArgs a, const int* __restrict__ tlist,
+                                                      const int* __restrict__ vslot, TD* vt,
+                                                      TC* counts) {
+    grid_dep_wait();
+    FrameCtr* ctr = a.ctr;
+    if (ctr->abort | ctr->err_cap | ctr->err_slots) return;
+    const long long U = (long long)ctr->n_touched;
+    const KeyPack kp = ctr->p.kp;
+    const PoseParams pp = ctr->p.pp;
+    const int32_t* __restrict__ labels = ctr->p.labels;
+    const bool closed = a.sem_kind == SVX_SEM_CLOSED;
+    using P2 = typename Pair<TD>::type;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < U;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int vid = tlist[e];
+        const unsigned c = a.vcnt[vid];
+        const unsigned long long key = a.vkey[vid];
+        const P2 st = reinterpret_cast<const P2*>(vt)[vid];
+        const unsigned k = c & ~kNewBit;
+        const bool isnew = (c & kNewBit) != 0u;
+        if (k <= 2u) slot_voxel<2, TD, TC>(a, vslot, labels, kp, pp, vt, counts, vid, k, isnew, key, st, closed);
+        else if (k <= 4u) slot_voxel<4, TD, TC>(a, vslot, labels, kp, pp, vt, counts, vid, k, isnew, key, st, closed);
+        else if (k <= 8u) slot_voxel<8, TD, TC>(a, vslot, labels, kp, pp, vt, counts, vid, k, isnew, key, st, closed);
+        else slot_voxel<16, TD, TC>(a, vslot, labels, kp, pp, vt, counts, vid, k, isnew, key, st, closed);
+        a.vcnt[vid] = 0u;
+    }
+}
+
 // ---- warp helpers ---------------------------------------------------------------
 
 // Sort one segment's point indices ascending into buf (k <= kSmemMax).
@@ -669,6 +799,14 @@ svx_status open_b(svx_map* m, cudaStream_t s) {
     return SVX_OK;
 }
 
+template <class TD, class TC>
+svx_status slots_t(svx_map* m, cudaStream_t s) {
+    SVX_CUDA(launch_pdl(k_update_slots<TD, TC>, kShortBlocks, 256, 0, s, make_args(m),
+                        ptr<int>(m->tlist), ptr<int>(m->vslot), ptr<TD>(m->vt), ptr<TC>(m->s0)));
+    SVX_LAUNCHED();
+    return SVX_OK;
+}
+
 template <class TD>
 svx_status stage_td(svx_map* m, int feats_f64, bool b, cudaStream_t s) {
     if (m->cfg.sem_kind == SVX_SEM_OPEN) {
@@ -700,6 +838,12 @@ svx_status launch_update_a(svx_map* m, int feats_f64, cudaStream_t s) {
 svx_status launch_update_b(svx_map* m, int feats_f64, cudaStream_t s) {
     if (m->cfg.tsdf_dtype == SVX_F64) return stage_td<double>(m, feats_f64, true, s);
     return stage_td<float>(m, feats_f64, true, s);
+}
+
+svx_status launch_update_slots(svx_map* m, cudaStream_t s) {
+    const bool t64 = m->cfg.tsdf_dtype == SVX_F64, c64 = m->cfg.count_dtype == SVX_F64;
+    if (t64) return c64 ? slots_t<double, double>(m, s) : slots_t<double, float>(m, s);
+    return c64 ? slots_t<float, double>(m, s) : slots_t<float, float>(m, s);
 }
 
 svx_status launch_rehash(svx_map* m, int4* new_table, int64_t new_cap, cudaStream_t s) {

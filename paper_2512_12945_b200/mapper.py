@@ -444,6 +444,16 @@ class Mapper:
         """Pre-size the device pools for `voxels` active voxels in `blocks` leaves."""
         check(lib.svx_reserve(self._handle, int(voxels), int(blocks)))
 
+    _UPDATE_MODES = {"auto": 0, "segments": 1, "slots": 2}
+
+    def set_update_mode(self, mode: str = "auto") -> None:
+        """Row-grouping strategy of closed-set / geometry maps
+        (svx_set_update_mode): "auto", "segments" or "slots".  All three give
+        bit-identical maps; the choice only changes speed."""
+        if mode not in self._UPDATE_MODES:
+            raise ValueError(f"update mode must be one of {sorted(self._UPDATE_MODES)}")
+        check(lib.svx_set_update_mode(self._handle, self._UPDATE_MODES[mode]))
+
     def set_profiling(self, enable: bool = True) -> None:
         """Record per-stage device times of each integrate (svx_set_profiling)."""
         check(lib.svx_set_profiling(self._handle, int(bool(enable))))

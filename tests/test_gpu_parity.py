@@ -181,6 +181,57 @@ def test_workload_frames_vs_oracle(cfg):
         assert np.array_equal(s1, os1)
 
 
+@pytest.mark.parametrize("variant", ["bayes", "last_wins_dropoff", "geometry"])
+@pytest.mark.parametrize("cfg", [1, 2, 4])
+@pytest.mark.parametrize("mode", ["segments", "slots", "auto"])
+def test_update_modes_vs_oracle(mode, cfg, variant):
+    """Both row-grouping strategies (svx_set_update_mode) on full BASELINE
+    frames, bit-exact vs the oracle.  cfg1 (depth camera, ~17 rows per voxel)
+    forced into slot mode overflows the 16 slots and must re-run the frame in
+    segment mode without leaving a trace."""
+    from paper_2512_12945_b200 import Mapper, scenes
+    from oracle.oracle import OracleMap
+
+    wl = scenes.workload(cfg, device="cuda")
+    kw = dict(wl.mapper_kwargs)
+    if variant == "last_wins_dropoff":
+        kw.update(fusion="last_wins", weight_fn="linear_dropoff")
+    elif variant == "geometry":
+        kw.pop("num_classes", None)
+    m = Mapper(**kw)
+    m.set_update_mode(mode)
+    om = OracleMap(**kw)
+    for i in range(3):
+        f = wl.make_frame(i * 2)
+        lab = f.labels if variant != "geometry" else None
+        r1 = m.integrate_world(f.points_world, f.origin, labels=lab)
+        r2 = om.integrate_world(f.points_world.cpu().numpy(), f.origin,
+                                labels=lab.cpu().numpy() if lab is not None else None)
+        assert np.array_equal(report_rows([r1]), report_rows([r2]))
+    st = m.engine_stats()
+    if mode == "segments":
+        assert st["frames_slot_mode"] == 0
+    elif cfg == 1:   # depth camera: slot mode overflows, frames re-run with segments
+        assert st["frames_slot_mode"] == 0 and st["slot_overflow_reruns"] >= 1
+    else:            # LiDAR: every frame fits the slots
+        assert st["frames_slot_mode"] == 3 and st["slot_overflow_reruns"] == 0
+    c, d, w, s0, _ = m._export()
+    oc, od, ow, os0, _ = om.export()
+    assert np.array_equal(c, oc)
+    assert np.array_equal(d, od) and np.array_equal(w, ow)
+    if variant != "geometry":
+        assert np.array_equal(s0, os0)
+        assert np.array_equal(m.label_map()[1], om.label_map())
+
+
+def test_update_mode_argument():
+    from paper_2512_12945_b200 import Mapper
+
+    m = Mapper(voxel_size=0.1, truncation=0.3, num_classes=3)
+    with pytest.raises(ValueError):
+        m.set_update_mode("bogus")
+
+
 def test_sensor_frame_identity_pose_lidar_full():
     """cfg2 (straight road, identity rotation) through Mapper.integrate: the
     reference's own API path, bit-exact vs the oracle."""
