@@ -49,6 +49,10 @@ enum { SVX_SEM_NONE = 0, SVX_SEM_CLOSED = 1, SVX_SEM_OPEN = 2 };
 
 /* Element type codes for arrays crossing the boundary. */
 enum { SVX_F32 = 0, SVX_F64 = 1 };
+/* OR-ed into points_dtype / feats_dtype: every input array of the call is a
+ * device pointer (skips the per-call pointer-attribute queries).  Without it
+ * the library detects host arrays and stages them itself. */
+#define SVX_DEVICE_INPUTS 0x100
 
 /*
  * Map construction parameters.  Mirrors the union of FusionConfig,

@@ -125,6 +125,8 @@ _SIGNATURES = {
     "svx_export_leaf_stamps": [_P, _I64, _P, _P, _P, ctypes.POINTER(_I64), _P],
 }
 
+DEVICE_INPUTS = 0x100   # svx.h SVX_DEVICE_INPUTS
+
 STAGES = ("march", "resolve", "scatter", "update", "update_b")
 
 # every symbol include/svx.h declares (checked by tests/test_abi_and_config.py)

@@ -208,8 +208,9 @@ svx_status svx_integrate(svx_map* m, const void* points, int32_t points_dtype, i
         pp.t[r] = pose[4 * r + 3];
     }
     pp.sensor = 1;
-    return integrate_impl(m, points, points_dtype == SVX_F64, n, pp, labels, feats,
-                          feats_dtype == SVX_F64, (cudaStream_t)stream, report);
+    const int dev = (points_dtype & SVX_DEVICE_INPUTS) ? 1 : 0;
+    return integrate_impl(m, points, (points_dtype & 0xff) == SVX_F64, n, pp, labels, feats,
+                          (feats_dtype & 0xff) == SVX_F64, (cudaStream_t)stream, report, dev);
 }
 
 svx_status svx_integrate_world(svx_map* m, const void* points_world, int32_t points_dtype,
@@ -223,8 +224,9 @@ svx_status svx_integrate_world(svx_map* m, const void* points_world, int32_t poi
     pp.R[0] = pp.R[4] = pp.R[8] = 1.0;
     for (int a = 0; a < 3; ++a) pp.t[a] = origin[a];
     pp.sensor = 0;
-    return integrate_impl(m, points_world, points_dtype == SVX_F64, n, pp, labels, feats,
-                          feats_dtype == SVX_F64, (cudaStream_t)stream, report);
+    const int dev = (points_dtype & SVX_DEVICE_INPUTS) ? 1 : 0;
+    return integrate_impl(m, points_world, (points_dtype & 0xff) == SVX_F64, n, pp, labels, feats,
+                          (feats_dtype & 0xff) == SVX_F64, (cudaStream_t)stream, report, dev);
 }
 
 svx_status svx_reserve(svx_map* m, int64_t voxels, int64_t blocks) {

@@ -237,11 +237,10 @@ static svx_status run_frame(svx_map* m, int pts_f64, int feats_f64, cudaStream_t
         }
         m->gsig[gm] = sig;
     }
-    SVX_CUDA(cudaEventRecord(m->ev_in, s));
-    SVX_CUDA(cudaStreamWaitEvent(m->gstream, m->ev_in, 0));
-    SVX_CUDA(cudaGraphLaunch(gexec, m->gstream));
+    // the graph was captured on the map's own stream; it runs on the caller's
+    SVX_CUDA(cudaGraphLaunch(gexec, s));
     count_launch(gm ? 3 : 6);
-    SVX_CUDA(cudaEventRecord(m->ev1, m->gstream));
+    SVX_CUDA(cudaEventRecord(m->ev1, s));
     SVX_CUDA(cudaEventSynchronize(m->ev1));
     return SVX_OK;
 }
@@ -365,7 +364,7 @@ KeyPack default_key_pack(const svx_map* m, const PoseParams& pp) {
 
 svx_status integrate_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n,
                           const PoseParams& pp, const int32_t* labels_in, const void* feats_in,
-                          int feats_f64, cudaStream_t s, svx_report* rep) {
+                          int feats_f64, cudaStream_t s, svx_report* rep, int device_inputs) {
     svx_report r;
     memset(&r, 0, sizeof(r));
     r.points_in = n;
@@ -383,14 +382,16 @@ svx_status integrate_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n
         return SVX_OK;
     }
     SVX_CUDA(cudaEventRecord(m->ev0, s));
-    const void* pts;
-    const void* feats = nullptr;
-    const void* labv = nullptr;
-    SVX_TRY(stage_in(pts_in, (size_t)n * 3 * (pts_f64 ? 8 : 4), m->in_pts, s, &pts));
-    if (kind == SVX_SEM_CLOSED) SVX_TRY(stage_in(labels_in, (size_t)n * 4, m->in_lab, s, &labv));
-    if (kind == SVX_SEM_OPEN)
-        SVX_TRY(stage_in(feats_in, (size_t)n * m->payload_d * (feats_f64 ? 8 : 4), m->in_feat, s,
-                         &feats));
+    const void* pts = pts_in;
+    const void* feats = kind == SVX_SEM_OPEN ? feats_in : nullptr;
+    const void* labv = kind == SVX_SEM_CLOSED ? (const void*)labels_in : nullptr;
+    if (!device_inputs) {
+        SVX_TRY(stage_in(pts_in, (size_t)n * 3 * (pts_f64 ? 8 : 4), m->in_pts, s, &pts));
+        if (kind == SVX_SEM_CLOSED) SVX_TRY(stage_in(labels_in, (size_t)n * 4, m->in_lab, s, &labv));
+        if (kind == SVX_SEM_OPEN)
+            SVX_TRY(stage_in(feats_in, (size_t)n * m->payload_d * (feats_f64 ? 8 : 4), m->in_feat, s,
+                             &feats));
+    }
     init_row_space(m, n);
     KeyPack kp = default_key_pack(m, pp);
     FrameCtr* hc = m->h_ctr;

@@ -350,7 +350,7 @@ svx_status reserve_voxels(svx_map* m, int64_t need, cudaStream_t s);
 svx_status reserve_blocks(svx_map* m, int64_t need, cudaStream_t s);
 svx_status integrate_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n,
                           const PoseParams& pp, const int32_t* labels_in, const void* feats_in,
-                          int feats_f64, cudaStream_t s, svx_report* rep);
+                          int feats_f64, cudaStream_t s, svx_report* rep, int device_inputs = 0);
 
 // ---- launchers implemented in the .cu files ---------------------------------
 // svx_march.cu: K1 walk (+ dense-row scan) and the gate

@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(256) k_update_short(UpdateArgs a, TD* vt, TC* 
 
 // ---- K5 slot mode: one thread per touched voxel (closed / geometry) --------------
 // Rows arrive in vslot in arbitrary order; a fixed compare-exchange network
-// (bitonic, N in {2, 4, 8, 16}) puts their point indices in ascending order in
+// (bitonic, N in {2, 4}) puts their point indices in ascending order in
 // registers, then the sums run sequentially exactly as in k_update_short.
 // Every load a voxel needs (count, key, slots, TSDF pair) is issued before
 // the first use, and the k ray gathers are issued back to back.
@@ -338,10 +338,70 @@ __device__ __forceinline__ void slot_voxel(const UpdateArgs& a, const int* __res
         for (int q = 0; q < a.C; ++q) crow[q] = (TC)(q == last - 1 ? 1 : 0);
 }
 
+// Voxels of 5..kSlots rows (a few percent on LiDAR frames) are finished by
+// the whole warp: lanes own rows, a shuffle bitonic sort orders the point
+// indices, the sums run through shuffles in that order.
 template <class TD, class TC>
-__global__ void __launch_bounds__(256, 3) k_update_slots(UpdateArgs a, const int* __restrict__ tlist,
-                                                      const int* __restrict__ vslot, TD* vt,
-                                                      TC* counts) {
+__device__ __forceinline__ void slot_voxel_warp(const UpdateArgs& a, const int* __restrict__ vslot,
+                                                const int32_t* __restrict__ labels,
+                                                const KeyPack& kp, const PoseParams& pp, TD* vt,
+                                                TC* counts, int vid, unsigned k, bool isnew,
+                                                unsigned long long key,
+                                                typename Pair<TD>::type st, bool closed) {
+    const int lane = threadIdx.x & 31;
+    int v = (unsigned)lane < k ? vslot[(long long)vid * kSlots + lane] : 0x7fffffff;
+#pragma unroll
+    for (int kk = 2; kk <= 32; kk <<= 1) {
+#pragma unroll
+        for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+            const int o = __shfl_xor_sync(0xffffffffu, v, jj);
+            const bool up = (lane & kk) == 0;
+            const bool lower = (lane & jj) == 0;
+            v = (lower == up) ? min(v, o) : max(v, o);
+        }
+    }
+    const Center cc = center_of(key, kp, a.h, pp);
+    double d = 0.0, w = 0.0;
+    int lab = 0;
+    if ((unsigned)lane < k) {
+        row_dw(cc.x, cc.y, cc.z, a.ray[v], a.trunc, a.wfn, d, w);
+        if (closed) lab = labels[v];
+    }
+    double sw = 0.0, swd = 0.0, mind = INFINITY, maxd = -INFINITY;
+    for (unsigned q = 0; q < k; ++q) {
+        const double wq = __shfl_sync(0xffffffffu, w, q);
+        const double dq = __shfl_sync(0xffffffffu, d, q);
+        sw += wq;
+        swd += wq * dq;
+        mind = dq < mind ? dq : mind;
+        maxd = dq > maxd ? dq : maxd;
+    }
+    TC* crow = counts + (long long)vid * a.C;
+    if (closed && !a.last_wins && (unsigned)lane < k) atomicAdd(&crow[lab - 1], (TC)1);
+    const int last = __shfl_sync(0xffffffffu, lab, k - 1);
+    if (lane == 0) {
+        if (isnew) {
+            st.x = (TD)a.trunc;
+            st.y = (TD)0;
+        }
+        const double w_old = (double)st.y, d_old = (double)st.x;
+        const double w_new = w_old + sw;
+        double d_new = w_new > 0.0 ? (w_old * d_old + swd) / w_new : d_old;
+        if ((mind == maxd) && (w_old == 0.0 || equals_stored<TD>(st.x, mind))) d_new = mind;
+        typename Pair<TD>::type out;
+        out.x = (TD)d_new;
+        out.y = (TD)w_new;
+        reinterpret_cast<typename Pair<TD>::type*>(vt)[vid] = out;
+        a.vcnt[vid] = 0u;
+    }
+    if (closed && a.last_wins)
+        for (int q = lane; q < a.C; q += 32) crow[q] = (TC)(q == last - 1 ? 1 : 0);
+}
+
+template <class TD, class TC>
+__global__ void __launch_bounds__(256, 4) k_update_slots(UpdateArgs a, const int* __restrict__ tlist,
+                                                         const int* __restrict__ vslot, TD* vt,
+                                                         TC* counts) {
     grid_dep_wait();
     FrameCtr* ctr = a.ctr;
     if (ctr->abort | ctr->err_cap | ctr->err_slots) return;
@@ -350,20 +410,43 @@ __global__ void __launch_bounds__(256, 3) k_update_slots(UpdateArgs a, const int
     const PoseParams pp = ctr->p.pp;
     const int32_t* __restrict__ labels = ctr->p.labels;
     const bool closed = a.sem_kind == SVX_SEM_CLOSED;
+    const int lane = threadIdx.x & 31;
     using P2 = typename Pair<TD>::type;
-    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < U;
-         e += (long long)gridDim.x * blockDim.x) {
-        const int vid = tlist[e];
-        const unsigned c = a.vcnt[vid];
-        const unsigned long long key = a.vkey[vid];
-        const P2 st = reinterpret_cast<const P2*>(vt)[vid];
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    // warp-uniform trip count (the warp path below needs every lane)
+    for (long long base = (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < U;
+         base += stride) {
+        const long long e = base + lane;
+        int vid = 0;
+        unsigned c = 0u;
+        unsigned long long key = 0;
+        P2 st{};
+        if (e < U) {
+            vid = tlist[e];
+            c = a.vcnt[vid];
+            key = a.vkey[vid];
+            st = reinterpret_cast<const P2*>(vt)[vid];
+        }
         const unsigned k = c & ~kNewBit;
         const bool isnew = (c & kNewBit) != 0u;
-        if (k <= 2u) slot_voxel<2, TD, TC>(a, vslot, labels, kp, pp, vt, counts, vid, k, isnew, key, st, closed);
-        else if (k <= 4u) slot_voxel<4, TD, TC>(a, vslot, labels, kp, pp, vt, counts, vid, k, isnew, key, st, closed);
-        else if (k <= 8u) slot_voxel<8, TD, TC>(a, vslot, labels, kp, pp, vt, counts, vid, k, isnew, key, st, closed);
-        else slot_voxel<16, TD, TC>(a, vslot, labels, kp, pp, vt, counts, vid, k, isnew, key, st, closed);
-        a.vcnt[vid] = 0u;
+        if (e < U && k <= 4u) {
+            if (k <= 2u) slot_voxel<2, TD, TC>(a, vslot, labels, kp, pp, vt, counts, vid, k, isnew, key, st, closed);
+            else slot_voxel<4, TD, TC>(a, vslot, labels, kp, pp, vt, counts, vid, k, isnew, key, st, closed);
+            a.vcnt[vid] = 0u;
+        }
+        unsigned big = __ballot_sync(0xffffffffu, e < U && k > 4u);
+        while (big) {
+            const int src = __ffs(big) - 1;
+            big &= big - 1;
+            const int bv = __shfl_sync(0xffffffffu, vid, src);
+            const unsigned bc = __shfl_sync(0xffffffffu, c, src);
+            const unsigned long long bk = __shfl_sync(0xffffffffu, key, src);
+            P2 bst;
+            bst.x = __shfl_sync(0xffffffffu, st.x, src);
+            bst.y = __shfl_sync(0xffffffffu, st.y, src);
+            slot_voxel_warp<TD, TC>(a, vslot, labels, kp, pp, vt, counts, bv, bc & ~kNewBit,
+                                    (bc & kNewBit) != 0u, bk, bst, closed);
+        }
     }
 }
 

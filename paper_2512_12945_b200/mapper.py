@@ -171,6 +171,7 @@ class _Arg:
                 return
             self.keep = t
             self.cuda = True
+            self.dev = t.get_device()
             self.ptr = t.data_ptr() if t.numel() else None
             self.shape = tuple(t.shape)
             return
@@ -192,11 +193,22 @@ class _Arg:
 
 
 def _stream_for(args):
-    if any(a is not None and a.cuda for a in args):
-        import torch
+    """(stream handle, all inputs on `device`) for a call: torch's current
+    stream of the inputs' device when any input is a CUDA tensor."""
+    dev = None
+    all_dev = True
+    for a in args:
+        if a is None:
+            continue
+        if a.cuda:
+            dev = a.dev
+        else:
+            all_dev = False
+    if dev is None:
+        return None, False
+    import torch
 
-        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
-    return None
+    return ctypes.c_void_p(torch._C._cuda_getCurrentRawStream(dev)), all_dev
 
 
 class Mapper:
@@ -277,6 +289,7 @@ class Mapper:
             c.lambda_floor = 1e-3
         c.tsdf_dtype = SVX_F64 if np.dtype(self._engine.tsdf_dtype) == np.float64 else SVX_F32
         c.device = int(self._engine.device)
+        self._device = c.device
         c.reserve_voxels = int(self._engine.reserve_voxels)
         c.reserve_blocks = int(self._engine.reserve_blocks)
         self._c = c
@@ -348,11 +361,13 @@ class Mapper:
 
     def _run(self, fn, pts, vec, lab, feat):
         rep = _lib.SvxReport()
-        stream = _stream_for([pts, lab, feat])
+        stream, all_dev = _stream_for((pts, lab, feat))
+        # every input already on the map's GPU: skip the library's pointer checks
+        flag = _lib.DEVICE_INPUTS if all_dev and pts.dev == self._device else 0
         n = int(pts.shape[0])
         vec = np.ascontiguousarray(vec, np.float64)
         arr = vec.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
-        check(fn(self._handle, pts.ptr, pts.code, n, arr,
+        check(fn(self._handle, pts.ptr, pts.code | flag, n, arr,
                  lab.ptr if lab is not None else None,
                  feat.ptr if feat is not None else None,
                  feat.code if feat is not None else SVX_F32, stream, ctypes.byref(rep)))

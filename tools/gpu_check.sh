@@ -16,8 +16,10 @@ timeout 1500 python -m pytest tests -m gpu -x -q > "$OUT/${TAG}_pytest.log" 2>&1
 echo "pytest rc=$?" >> "$OUT/${TAG}_pytest.log"
 timeout 600 python bench.py > "$OUT/${TAG}_bench.json" 2> "$OUT/${TAG}_bench.err"
 echo "bench rc=$?" >> "$OUT/${TAG}_bench.err"
-timeout 600 python bench.py --impl reference --steps 5 --warmup 3 > "$OUT/${TAG}_bench_ref.json" 2> "$OUT/${TAG}_bench_ref.err"
-echo "ref rc=$?" >> "$OUT/${TAG}_bench_ref.err"
+timeout 300 python tools/host_overhead.py > "$OUT/${TAG}_host.txt" 2>&1
+timeout 300 python tools/host_overhead.py --mode segments >> "$OUT/${TAG}_host.txt" 2>&1
+[ -n "${WITH_REF:-}" ] && timeout 600 python bench.py --impl reference --steps 5 --warmup 3 > "$OUT/${TAG}_bench_ref.json" 2> "$OUT/${TAG}_bench_ref.err"
+echo "ref rc=$?" >> "$OUT/${TAG}_bench_ref.err" 2>/dev/null
 PCMD="python bench.py --steps 3 --warmup 3 --profile-frames 0 --no-cpu-baseline --no-e2e"
 if $PCMD > "$OUT/${TAG}_plain.log" 2>&1; then
   ncu --metrics gpu__time_duration.sum --clock-control none --csv \
