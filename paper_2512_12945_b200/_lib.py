@@ -102,9 +102,9 @@ _D = ctypes.c_double
 _SIGNATURES = {
     "svx_create": [ctypes.POINTER(SvxConfig), ctypes.POINTER(_P)],
     "svx_destroy": [_P],
-    "svx_integrate": [_P, _P, _I32, _I64, ctypes.POINTER(_D), _P, _P, _I32, _P,
-                      ctypes.POINTER(SvxReport)],
-    "svx_integrate_world": [_P, _P, _I32, _I64, ctypes.POINTER(_D), _P, _P, _I32, _P,
+    # pose / origin as a raw address (a numpy array's .ctypes.data)
+    "svx_integrate": [_P, _P, _I32, _I64, _P, _P, _P, _I32, _P, ctypes.POINTER(SvxReport)],
+    "svx_integrate_world": [_P, _P, _I32, _I64, _P, _P, _P, _I32, _P,
                             ctypes.POINTER(SvxReport)],
     "svx_stats_get": [_P, ctypes.POINTER(SvxStats)],
     "svx_active_count": [_P, ctypes.POINTER(_I64)],

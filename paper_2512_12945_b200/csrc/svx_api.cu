@@ -177,7 +177,7 @@ svx_status svx_destroy(svx_map* m) {
     if (!m) return SVX_OK;
     cudaSetDevice(m->cfg.device);
     DevBuf* bufs[] = {&m->hash, &m->bcoord, &m->bkey, &m->bmask, &m->bslot, &m->vt,
-                      &m->s0, &m->s1, &m->vcnt, &m->vseg, &m->vcur, &m->vkey, &m->vslot, &m->in_pts,
+                      &m->s0, &m->s1, &m->vrec, &m->vslot, &m->in_pts,
                       &m->in_lab, &m->in_feat, &m->ray, &m->rcnt, &m->roff, &m->rowkey,
                       &m->rowvid, &m->rowray, &m->partials, &m->tlist, &m->mlist,
                       &m->longlist, &m->srid, &m->bitmap, &m->cubtmp, &m->ctr, &m->ord0,

@@ -20,10 +20,22 @@
 #include <string.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 
 #include "svx_internal.cuh"
 
 namespace svx {
+
+// SVX_TRACE_HOST=1: per-frame host-side phase times (us) on stderr.
+static double now_us() {
+    return std::chrono::duration<double, std::micro>(
+               std::chrono::steady_clock::now().time_since_epoch())
+        .count();
+}
+static const bool g_trace_host = getenv("SVX_TRACE_HOST") != nullptr;
+static double g_t_launch0 = 0, g_t_launch1 = 0, g_t_synced = 0;
 
 bool is_device_ptr(const void* p) {
     if (!p) return false;
@@ -70,12 +82,9 @@ svx_status reserve_voxels(svx_map* m, int64_t need, cudaStream_t s) {
         SVX_TRY(ensure(m->s0, se * (size_t)m->payload_d * cap, s, true, 0));
     if (m->cfg.sem_kind == SVX_SEM_OPEN)
         SVX_TRY(ensure(m->s1, se * (size_t)m->payload_d * cap, s, true, 0));
-    SVX_TRY(ensure(m->vcnt, 4 * cap, s, true, 0));
-    SVX_TRY(ensure(m->vcur, 4 * cap, s, true, 0));
-    SVX_TRY(ensure(m->vseg, 4 * cap, s, true));
-    SVX_TRY(ensure(m->vkey, 8 * cap, s, true));
+    SVX_TRY(ensure(m->vrec, sizeof(VoxFrame) * cap, s, true, 0));
     if (m->cfg.sem_kind != SVX_SEM_OPEN && !m->cfg.space_carving)   // per-frame contents only
-        SVX_TRY(ensure(m->vslot, sizeof(int) * kSlots * cap, s));
+        SVX_TRY(ensure(m->vslot, sizeof(int) * kHiStride * cap, s));
     m->vcap = cap;
     return SVX_OK;
 }
@@ -135,8 +144,7 @@ static unsigned long long graph_signature(const svx_map* m, int pts_f64, int fea
                           m->rowray.p, m->partials.p, m->tlist.p, m->mlist.p,  m->longlist.p,
                           m->srid.p,   m->bitmap.p, m->cubtmp.p,  m->hash.p,   m->bcoord.p,
                           m->bkey.p,   m->bmask.p,  m->bslot.p,   m->vt.p,     m->s0.p,
-                          m->s1.p,     m->vcnt.p,   m->vseg.p,    m->vcur.p,   m->vkey.p,
-                          m->vslot.p,  m->ctr.p};
+                          m->s1.p,     m->vrec.p,   m->vslot.p,   m->ctr.p};
     unsigned long long h = 1469598103934665603ULL;
     auto mix = [&](unsigned long long v) {
         h ^= v;
@@ -238,10 +246,13 @@ static svx_status run_frame(svx_map* m, int pts_f64, int feats_f64, cudaStream_t
         m->gsig[gm] = sig;
     }
     // the graph was captured on the map's own stream; it runs on the caller's
+    if (g_trace_host) g_t_launch0 = now_us();
     SVX_CUDA(cudaGraphLaunch(gexec, s));
     count_launch(gm ? 3 : 6);
     SVX_CUDA(cudaEventRecord(m->ev1, s));
+    if (g_trace_host) g_t_launch1 = now_us();
     SVX_CUDA(cudaEventSynchronize(m->ev1));
+    if (g_trace_host) g_t_synced = now_us();
     return SVX_OK;
 }
 
@@ -365,6 +376,7 @@ KeyPack default_key_pack(const svx_map* m, const PoseParams& pp) {
 svx_status integrate_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n,
                           const PoseParams& pp, const int32_t* labels_in, const void* feats_in,
                           int feats_f64, cudaStream_t s, svx_report* rep, int device_inputs) {
+    const double t_enter = g_trace_host ? now_us() : 0.0;
     svx_report r;
     memset(&r, 0, sizeof(r));
     r.points_in = n;
@@ -464,6 +476,12 @@ svx_status integrate_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n
     r.kernel_ms = ms;
     finish_frame(m, nblocks0, nvox0, r);
     if (rep) *rep = r;
+    if (g_trace_host) {
+        const double t_exit = now_us();
+        fprintf(stderr, "svx host us: prep %.1f launch %.1f wait %.1f finish %.1f total %.1f device %.1f\n",
+                g_t_launch0 - t_enter, g_t_launch1 - g_t_launch0, g_t_synced - g_t_launch1,
+                t_exit - g_t_synced, t_exit - t_enter, 1e3 * ms);
+    }
     return SVX_OK;
 }
 

@@ -118,11 +118,25 @@ struct FrameCtr {
     int err_slots;                  // slot mode: a voxel got more than kSlots rows (re-run in segment mode)
 };
 
-// Per-voxel frame state (indexed by voxel id, zero between frames):
-//   vcnt  rows this frame; bit 31 = voxel allocated this frame
-//   vseg  base of the voxel's row segment;  vcur  fill cursor
-//   vkey  the voxel's frame key (written by its first toucher)
+// Per-voxel frame record (indexed by voxel id; cnt and cur are zero between
+// frames).  One 32-byte sector, so K2's count atomic, the first toucher's key
+// and the first slots land in one line, and the update reads it in one go.
+//   cnt   rows this frame; bit 31 = voxel allocated this frame
+//   seg   base of the voxel's row segment (segment mode)
+//   key   the voxel's frame key (written by its first toucher)
+//   cur   segment fill cursor (segment mode)
+//   slot  slot mode: point indices of rows 0..2; rows 3..15 go to vslot_hi
 constexpr unsigned kNewBit = 0x80000000u;
+constexpr int kRecSlots = 3;
+constexpr int kHiStride = 16;   // vslot_hi[vid * 16 + (j - 3)], 3 <= j < kSlots
+struct alignas(32) VoxFrame {
+    unsigned cnt;
+    unsigned seg;
+    unsigned long long key;
+    unsigned cur;
+    int slot[kRecSlots];
+};
+static_assert(sizeof(VoxFrame) == 32, "VoxFrame must be one sector");
 
 // Row addressing: slot mode (bounded bands: ray i owns slots [i*maxrows, +rcnt[i]))
 // or dense mode (rows packed by a scan; rowray[r] = ray of row r).
@@ -177,8 +191,8 @@ struct svx_map {
     svx::DevBuf hash;  int64_t hcap = 0;
     svx::DevBuf bcoord, bkey, bmask, bslot;  int64_t bcap = 0, nblocks = 0;
     svx::DevBuf vt, s0, s1;                  int64_t vcap = 0, nvox = 0;  // vt: {d, w} per voxel
-    svx::DevBuf vcnt, vseg, vcur, vkey;      // per-voxel frame state (see FrameCtr)
-    svx::DevBuf vslot;                       // slot mode: kSlots point indices per voxel
+    svx::DevBuf vrec;                        // per-voxel frame records (svx::VoxFrame)
+    svx::DevBuf vslot;                       // slot mode: rows 3..15 of each voxel
     int64_t n_slot_frames = 0, n_slot_reruns = 0;
     int mode_pref = 0;      // SVX_UPDATE_AUTO / SEGMENTS / SLOTS
     int slot_hold = 0;      // frames to stay in segment mode after a slot overflow

@@ -124,8 +124,8 @@ __device__ int leaf_find_or_insert(int4* table, long long mask, int a, int b, in
 __global__ void __launch_bounds__(kResolveThreads) k_resolve(
     const unsigned long long* __restrict__ rowkey, const int* __restrict__ rowray,
     int* __restrict__ rowvid, int* __restrict__ vslot, int4* table, int4* bcoord,
-    unsigned long long* bkey, unsigned long long* bmask, int* bslot, unsigned* vcnt,
-    unsigned long long* __restrict__ vkey, int* __restrict__ tlist, FrameCtr* ctr) {
+    unsigned long long* bkey, unsigned long long* bmask, int* bslot, VoxFrame* rec,
+    int* __restrict__ tlist, FrameCtr* ctr) {
     grid_dep_wait();
     using Scan = cub::BlockScan<int, kResolveThreads>;
     __shared__ typename Scan::TempStorage scan_tmp;
@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(kResolveThreads) k_resolve(
         bool first = false;
         unsigned cbase = 0;
         if (is_vl && vid >= 0) {
-            const unsigned c = atomicAdd(&vcnt[vid], (unsigned)__popc(vpeers) + (created ? kNewBit : 0u));
+            const unsigned c = atomicAdd(&rec[vid].cnt, (unsigned)__popc(vpeers) + (created ? kNewBit : 0u));
             cbase = c & ~kNewBit;
             first = cbase == 0u;
         }
@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(kResolveThreads) k_resolve(
         if (threadIdx.x == 0 && cnt) s_base = atomicAdd(&ctr->n_touched, (unsigned long long)cnt);
         __syncthreads();
         if (first) {
-            vkey[vid] = key;
+            rec[vid].key = key;
             tlist[s_base + rank] = vid;
         }
         vid = __shfl_sync(full, vid, vleader);
@@ -273,7 +273,8 @@ __global__ void __launch_bounds__(kResolveThreads) k_resolve(
             // restored by point index in k_update_slots)
             cbase = __shfl_sync(full, cbase, vleader) + __popc(vpeers & ((1u << lane) - 1u));
             if (valid && vid >= 0) {
-                if (cbase < (unsigned)kSlots) vslot[(long long)vid * kSlots + cbase] = pidx;
+                if (cbase < (unsigned)kRecSlots) rec[vid].slot[cbase] = pidx;
+                else if (cbase < (unsigned)kSlots) vslot[(long long)vid * kHiStride + (cbase - kRecSlots)] = pidx;
                 else ctr->err_slots = 1;
             }
         } else if (valid) {
@@ -305,8 +306,7 @@ __device__ __forceinline__ void ld_status(const SegStatus* p, unsigned long long
 }
 
 __global__ void __launch_bounds__(kSegThreads) k_seg(const int* __restrict__ tlist,
-                                                     const unsigned* __restrict__ vcnt,
-                                                     unsigned* __restrict__ vseg,
+                                                     VoxFrame* __restrict__ rec,
                                                      int* __restrict__ mlist,
                                                      SegStatus* __restrict__ status, FrameCtr* ctr) {
     grid_dep_wait();
@@ -335,7 +335,7 @@ __global__ void __launch_bounds__(kSegThreads) k_seg(const int* __restrict__ tli
         for (int q = 0; q < 4; ++q) {
             const long long e = e0 + q;
             vv[q] = e < n ? tlist[e] : -1;
-            cc[q] = vv[q] >= 0 ? (vcnt[vv[q]] & ~kNewBit) : 0u;
+            cc[q] = vv[q] >= 0 ? (rec[vv[q]].cnt & ~kNewBit) : 0u;
             li[q] = vv[q] >= 0 && (!singles || cc[q] > 1u);
             cnt += li[q];
             rows += li[q] ? cc[q] : 0u;
@@ -383,7 +383,7 @@ __global__ void __launch_bounds__(kSegThreads) k_seg(const int* __restrict__ tli
         for (int q = 0; q < 4; ++q) {
             if (!li[q]) continue;
             mlist[u] = vv[q];
-            vseg[vv[q]] = (unsigned)r;
+            rec[vv[q]].seg = (unsigned)r;
             ++u;
             r += cc[q];
         }
@@ -394,14 +394,14 @@ __global__ void __launch_bounds__(kSegThreads) k_seg(const int* __restrict__ tli
 // their background state (they stay active and are found again by the
 // retry) and clear the per-voxel frame counts.
 template <class TD, class TS>
-__global__ void k_cleanup(const int* __restrict__ tlist, unsigned* vcnt, unsigned* vcur, TD* vt,
+__global__ void k_cleanup(const int* __restrict__ tlist, VoxFrame* rec, TD* vt,
                           TS* mean, TS* beta, int D, double trunc, double prior_beta,
                           const FrameCtr* __restrict__ ctr) {
     const long long n = (long long)ctr->n_touched;
     for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n;
          e += (long long)gridDim.x * blockDim.x) {
         const int vid = tlist[e];
-        if (vcnt[vid] & kNewBit) {
+        if (rec[vid].cnt & kNewBit) {
             vt[2 * (long long)vid] = (TD)trunc;
             vt[2 * (long long)vid + 1] = (TD)0;
             if (mean) {
@@ -411,8 +411,8 @@ __global__ void k_cleanup(const int* __restrict__ tlist, unsigned* vcnt, unsigne
                 }
             }
         }
-        vcnt[vid] = 0u;
-        vcur[vid] = 0u;
+        rec[vid].cnt = 0u;
+        rec[vid].cur = 0u;
     }
 }
 
@@ -420,7 +420,7 @@ template <class TD, class TS>
 svx_status cleanup_t(svx_map* m, cudaStream_t s) {
     const bool open = m->cfg.sem_kind == SVX_SEM_OPEN;
     k_cleanup<TD, TS><<<kPersistentBlocks, 256, 0, s>>>(
-        ptr<int>(m->tlist), ptr<unsigned>(m->vcnt), ptr<unsigned>(m->vcur), ptr<TD>(m->vt),
+        ptr<int>(m->tlist), ptr<VoxFrame>(m->vrec), ptr<TD>(m->vt),
         open ? ptr<TS>(m->s0) : nullptr, open ? ptr<TS>(m->s1) : nullptr, m->payload_d,
         m->cfg.truncation, m->cfg.prior_beta, ptr<FrameCtr>(m->ctr));
     SVX_LAUNCHED();
@@ -434,7 +434,7 @@ svx_status launch_resolve(svx_map* m, cudaStream_t s) {
         ptr<unsigned long long>(m->rowkey), ptr<int>(m->rowray), ptr<int>(m->rowvid), ptr<int>(m->vslot),
         ptr<int4>(m->hash), ptr<int4>(m->bcoord),
         ptr<unsigned long long>(m->bkey), ptr<unsigned long long>(m->bmask), ptr<int>(m->bslot),
-        ptr<unsigned>(m->vcnt), ptr<unsigned long long>(m->vkey), ptr<int>(m->tlist),
+        ptr<VoxFrame>(m->vrec), ptr<int>(m->tlist),
         ptr<FrameCtr>(m->ctr)));
     SVX_LAUNCHED();
     return SVX_OK;
@@ -443,8 +443,8 @@ svx_status launch_resolve(svx_map* m, cudaStream_t s) {
 svx_status launch_segments(svx_map* m, cudaStream_t s) {
     SegStatus* status =
         reinterpret_cast<SegStatus*>(ptr<char>(m->partials) + partials_bytes());
-    SVX_CUDA(launch_pdl(k_seg, kSegBlocks, kSegThreads, 0, s, ptr<int>(m->tlist), ptr<unsigned>(m->vcnt),
-                                             ptr<unsigned>(m->vseg), ptr<int>(m->mlist), status,
+    SVX_CUDA(launch_pdl(k_seg, kSegBlocks, kSegThreads, 0, s, ptr<int>(m->tlist), ptr<VoxFrame>(m->vrec),
+                                             ptr<int>(m->mlist), status,
                                              ptr<FrameCtr>(m->ctr)));
     SVX_LAUNCHED();
     return SVX_OK;

@@ -100,10 +100,7 @@ __device__ __forceinline__ Center center_of(unsigned long long key, const KeyPac
 
 struct UpdateArgs {
     const int* mlist;
-    unsigned* vcnt;
-    const unsigned* vseg;
-    unsigned* vcur;
-    const unsigned long long* vkey;
+    VoxFrame* rec;
     const int* srid;
     const double4* ray;
     int* longlist;
@@ -119,8 +116,8 @@ struct UpdateArgs {
 };
 
 __device__ __forceinline__ void clear_voxel_frame(const UpdateArgs& a, int vid) {
-    a.vcnt[vid] = 0u;
-    a.vcur[vid] = 0u;
+    a.rec[vid].cnt = 0u;
+    a.rec[vid].cur = 0u;
 }
 
 // ---- K4: scatter, single-row voxels finished in ray order --------------------------
@@ -153,9 +150,9 @@ __global__ void __launch_bounds__(256) k_scatter(UpdateArgs a, const int* __rest
         long long i;
         if (!row_ray(rs, t, i)) continue;
         const int vid = rowvid[t];
-        const unsigned c = a.vcnt[vid];
+        const unsigned c = a.rec[vid].cnt;
         if (!singles || (c & ~kNewBit) > 1u) {
-            const unsigned pos = a.vseg[vid] + atomicAdd(&a.vcur[vid], 1u);
+            const unsigned pos = a.rec[vid].seg + atomicAdd(&a.rec[vid].cur, 1u);
             srid[pos] = (int)i;
             continue;
         }
@@ -174,7 +171,7 @@ __global__ void __launch_bounds__(256) k_scatter(UpdateArgs a, const int* __rest
                 atomicAdd(&crow[lab - 1], (TC)1);   // integer count: fire-and-forget
             }
         }
-        a.vcnt[vid] = 0u;
+        a.rec[vid].cnt = 0u;
     }
 }
 
@@ -193,14 +190,14 @@ __global__ void __launch_bounds__(256) k_update_short(UpdateArgs a, TD* vt, TC* 
     for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < L;
          e += (long long)gridDim.x * blockDim.x) {
         const int vid = a.mlist[e];
-        const unsigned c = a.vcnt[vid];
+        const unsigned c = a.rec[vid].cnt;
         const unsigned k = c & ~kNewBit;
         if (k > (unsigned)kShortMax) {
             if (k > (unsigned)kSmemMax) a.hugelist[warp_ticket(&ctr->n_huge)] = (int)e;
             else a.longlist[warp_ticket(&ctr->n_long)] = (int)e;
             continue;
         }
-        const unsigned base = a.vseg[vid];
+        const unsigned base = a.rec[vid].seg;
         int r[kShortMax];
         for (unsigned j = 0; j < k; ++j) {
             int v = a.srid[base + j];
@@ -211,7 +208,7 @@ __global__ void __launch_bounds__(256) k_update_short(UpdateArgs a, TD* vt, TC* 
             }
             r[p] = v;
         }
-        const Center cc = center_of(a.vkey[vid], kp, a.h, pp);
+        const Center cc = center_of(a.rec[vid].key, kp, a.h, pp);
         double sw = 0.0, swd = 0.0, mind = INFINITY, maxd = -INFINITY;
         int last_lab = 0;
         TC* crow = counts + (long long)vid * a.C;
@@ -238,169 +235,52 @@ __global__ void __launch_bounds__(256) k_update_short(UpdateArgs a, TD* vt, TC* 
 }
 
 // ---- K5 slot mode: one thread per touched voxel (closed / geometry) --------------
-// Rows arrive in vslot in arbitrary order; a fixed compare-exchange network
-// (bitonic, N in {2, 4}) puts their point indices in ascending order in
-// registers, then the sums run sequentially exactly as in k_update_short.
-// Every load a voxel needs (count, key, slots, TSDF pair) is issued before
-// the first use, and the k ray gathers are issued back to back.
+// The voxel's frame record (count, key, rows 0..2) and its TSDF pair are read
+// together; rows arrive in arbitrary order and are put in ascending point
+// order before the sequential sums (the reference's (voxel, point) order), so
+// the arithmetic is exactly k_update_short's.  Voxels of up to 3 rows (~94%
+// on LiDAR frames) sort in registers; 4..16 rows take a local-array path.
 
-template <int N>
-__device__ __forceinline__ void sort_net(int (&r)[N]) {
-#pragma unroll
-    for (int kk = 2; kk <= N; kk <<= 1) {
-#pragma unroll
-        for (int jj = kk >> 1; jj > 0; jj >>= 1) {
-#pragma unroll
-            for (int i = 0; i < N; ++i) {
-                const int l = i ^ jj;
-                if (l > i) {
-                    const int a = r[i], b = r[l];
-                    const bool up = (i & kk) == 0;
-                    r[i] = up ? min(a, b) : max(a, b);
-                    r[l] = up ? max(a, b) : min(a, b);
-                }
-            }
-        }
-    }
-}
-
-template <int N, class TD, class TC>
-__device__ __forceinline__ void slot_voxel(const UpdateArgs& a, const int* __restrict__ vslot,
-                                           const int32_t* __restrict__ labels, const KeyPack& kp,
-                                           const PoseParams& pp, TD* vt, TC* counts, int vid,
-                                           unsigned k, bool isnew, unsigned long long key,
-                                           typename Pair<TD>::type st, bool closed) {
-    int r[N];
-    const int* sl = vslot + (long long)vid * kSlots;
-    if (N == 2) {
-        const int2 v = *reinterpret_cast<const int2*>(sl);
-        r[0] = v.x;
-        r[1] = k > 1u ? v.y : 0x7fffffff;
-    } else {
-#pragma unroll
-        for (int q = 0; q < N / 4; ++q) {
-            const int4 v = reinterpret_cast<const int4*>(sl)[q];
-            r[4 * q + 0] = (unsigned)(4 * q + 0) < k ? v.x : 0x7fffffff;
-            r[4 * q + 1] = (unsigned)(4 * q + 1) < k ? v.y : 0x7fffffff;
-            r[4 * q + 2] = (unsigned)(4 * q + 2) < k ? v.z : 0x7fffffff;
-            r[4 * q + 3] = (unsigned)(4 * q + 3) < k ? v.w : 0x7fffffff;
-        }
-    }
-    sort_net<N>(r);
-    // gathers in chunks of 4 rows (registers stay bounded for N = 8, 16)
-    const Center cc = center_of(key, kp, a.h, pp);
+template <class TC>
+struct RowAcc {
     double sw = 0.0, swd = 0.0, mind = INFINITY, maxd = -INFINITY;
-    TC* crow = counts + (long long)vid * a.C;
     int last = 0;
-#pragma unroll
-    for (int j0 = 0; j0 < N; j0 += 4) {
-        if ((unsigned)j0 < k) {
-            double4 ry[4];
-            int lab[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                if (j0 + q < N && (unsigned)(j0 + q) < k) {
-                    ry[q] = a.ray[r[j0 + q]];
-                    lab[q] = closed ? labels[r[j0 + q]] : 0;
-                }
-            }
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                if (j0 + q < N && (unsigned)(j0 + q) < k) {
-                    double d, w;
-                    row_dw(cc.x, cc.y, cc.z, ry[q], a.trunc, a.wfn, d, w);
-                    sw += w;
-                    swd += w * d;
-                    mind = d < mind ? d : mind;
-                    maxd = d > maxd ? d : maxd;
-                    if (closed) {
-                        if (a.last_wins) last = lab[q];
-                        else atomicAdd(&crow[lab[q] - 1], (TC)1);   // integer count: order-free
-                    }
-                }
-            }
-        }
-    }
-    // apply_tsdf (_pycore.py:399-417) on the pre-loaded pair
-    if (isnew) {
-        st.x = (TD)a.trunc;
-        st.y = (TD)0;
-    }
-    const double w_old = (double)st.y, d_old = (double)st.x;
-    const double w_new = w_old + sw;
-    double d_new = w_new > 0.0 ? (w_old * d_old + swd) / w_new : d_old;
-    if ((mind == maxd) && (w_old == 0.0 || equals_stored<TD>(st.x, mind))) d_new = mind;
-    typename Pair<TD>::type out;
-    out.x = (TD)d_new;
-    out.y = (TD)w_new;
-    reinterpret_cast<typename Pair<TD>::type*>(vt)[vid] = out;
-    if (closed && a.last_wins)
-        for (int q = 0; q < a.C; ++q) crow[q] = (TC)(q == last - 1 ? 1 : 0);
-}
+};
 
-// Voxels of 5..kSlots rows (a few percent on LiDAR frames) are finished by
-// the whole warp: lanes own rows, a shuffle bitonic sort orders the point
-// indices, the sums run through shuffles in that order.
-template <class TD, class TC>
-__device__ __forceinline__ void slot_voxel_warp(const UpdateArgs& a, const int* __restrict__ vslot,
-                                                const int32_t* __restrict__ labels,
-                                                const KeyPack& kp, const PoseParams& pp, TD* vt,
-                                                TC* counts, int vid, unsigned k, bool isnew,
-                                                unsigned long long key,
-                                                typename Pair<TD>::type st, bool closed) {
-    const int lane = threadIdx.x & 31;
-    int v = (unsigned)lane < k ? vslot[(long long)vid * kSlots + lane] : 0x7fffffff;
+// Fold up to 4 rows (point indices p[0..m), ascending) into the sums.
+template <class TC>
+__device__ __forceinline__ void fold_rows(const UpdateArgs& a, const int32_t* __restrict__ labels,
+                                          const Center& cc, const int (&p)[4], int m, TC* crow,
+                                          bool closed, RowAcc<TC>& acc) {
+    double4 ry[4];
+    int lab[4];
 #pragma unroll
-    for (int kk = 2; kk <= 32; kk <<= 1) {
-#pragma unroll
-        for (int jj = kk >> 1; jj > 0; jj >>= 1) {
-            const int o = __shfl_xor_sync(0xffffffffu, v, jj);
-            const bool up = (lane & kk) == 0;
-            const bool lower = (lane & jj) == 0;
-            v = (lower == up) ? min(v, o) : max(v, o);
+    for (int q = 0; q < 4; ++q) {
+        if (q < m) {
+            ry[q] = a.ray[p[q]];
+            lab[q] = closed ? labels[p[q]] : 0;
         }
     }
-    const Center cc = center_of(key, kp, a.h, pp);
-    double d = 0.0, w = 0.0;
-    int lab = 0;
-    if ((unsigned)lane < k) {
-        row_dw(cc.x, cc.y, cc.z, a.ray[v], a.trunc, a.wfn, d, w);
-        if (closed) lab = labels[v];
-    }
-    double sw = 0.0, swd = 0.0, mind = INFINITY, maxd = -INFINITY;
-    for (unsigned q = 0; q < k; ++q) {
-        const double wq = __shfl_sync(0xffffffffu, w, q);
-        const double dq = __shfl_sync(0xffffffffu, d, q);
-        sw += wq;
-        swd += wq * dq;
-        mind = dq < mind ? dq : mind;
-        maxd = dq > maxd ? dq : maxd;
-    }
-    TC* crow = counts + (long long)vid * a.C;
-    if (closed && !a.last_wins && (unsigned)lane < k) atomicAdd(&crow[lab - 1], (TC)1);
-    const int last = __shfl_sync(0xffffffffu, lab, k - 1);
-    if (lane == 0) {
-        if (isnew) {
-            st.x = (TD)a.trunc;
-            st.y = (TD)0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        if (q < m) {
+            double d, w;
+            row_dw(cc.x, cc.y, cc.z, ry[q], a.trunc, a.wfn, d, w);
+            acc.sw += w;
+            acc.swd += w * d;
+            acc.mind = d < acc.mind ? d : acc.mind;
+            acc.maxd = d > acc.maxd ? d : acc.maxd;
+            if (closed) {
+                if (a.last_wins) acc.last = lab[q];
+                else atomicAdd(&crow[lab[q] - 1], (TC)1);   // integer count: order-free
+            }
         }
-        const double w_old = (double)st.y, d_old = (double)st.x;
-        const double w_new = w_old + sw;
-        double d_new = w_new > 0.0 ? (w_old * d_old + swd) / w_new : d_old;
-        if ((mind == maxd) && (w_old == 0.0 || equals_stored<TD>(st.x, mind))) d_new = mind;
-        typename Pair<TD>::type out;
-        out.x = (TD)d_new;
-        out.y = (TD)w_new;
-        reinterpret_cast<typename Pair<TD>::type*>(vt)[vid] = out;
-        a.vcnt[vid] = 0u;
     }
-    if (closed && a.last_wins)
-        for (int q = lane; q < a.C; q += 32) crow[q] = (TC)(q == last - 1 ? 1 : 0);
 }
 
 template <class TD, class TC>
 __global__ void __launch_bounds__(256, 4) k_update_slots(UpdateArgs a, const int* __restrict__ tlist,
-                                                         const int* __restrict__ vslot, TD* vt,
+                                                         const int* __restrict__ vslot_hi, TD* vt,
                                                          TC* counts) {
     grid_dep_wait();
     FrameCtr* ctr = a.ctr;
@@ -410,43 +290,74 @@ __global__ void __launch_bounds__(256, 4) k_update_slots(UpdateArgs a, const int
     const PoseParams pp = ctr->p.pp;
     const int32_t* __restrict__ labels = ctr->p.labels;
     const bool closed = a.sem_kind == SVX_SEM_CLOSED;
-    const int lane = threadIdx.x & 31;
     using P2 = typename Pair<TD>::type;
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    // warp-uniform trip count (the warp path below needs every lane)
-    for (long long base = (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < U;
-         base += stride) {
-        const long long e = base + lane;
-        int vid = 0;
-        unsigned c = 0u;
-        unsigned long long key = 0;
-        P2 st{};
-        if (e < U) {
-            vid = tlist[e];
-            c = a.vcnt[vid];
-            key = a.vkey[vid];
-            st = reinterpret_cast<const P2*>(vt)[vid];
-        }
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < U;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int vid = tlist[e];
+        const int4 r0 = reinterpret_cast<const int4*>(a.rec + vid)[0];   // cnt, seg, key
+        const int4 r1 = reinterpret_cast<const int4*>(a.rec + vid)[1];   // cur, slot[0..2]
+        P2 st = reinterpret_cast<const P2*>(vt)[vid];
+        const unsigned c = (unsigned)r0.x;
         const unsigned k = c & ~kNewBit;
-        const bool isnew = (c & kNewBit) != 0u;
-        if (e < U && k <= 4u) {
-            if (k <= 2u) slot_voxel<2, TD, TC>(a, vslot, labels, kp, pp, vt, counts, vid, k, isnew, key, st, closed);
-            else slot_voxel<4, TD, TC>(a, vslot, labels, kp, pp, vt, counts, vid, k, isnew, key, st, closed);
-            a.vcnt[vid] = 0u;
+        const unsigned long long key =
+            ((unsigned long long)(unsigned)r0.w << 32) | (unsigned long long)(unsigned)r0.z;
+        const Center cc = center_of(key, kp, a.h, pp);
+        TC* crow = counts + (long long)vid * a.C;
+        RowAcc<TC> acc;
+        if (k <= 3u) {
+            int p[4] = {r1.y, k > 1u ? r1.z : 0x7fffffff, k > 2u ? r1.w : 0x7fffffff, 0x7fffffff};
+            // 3-element sorting network
+            int t0 = min(p[0], p[1]), t1 = max(p[0], p[1]);
+            p[0] = t0; p[1] = t1;
+            t0 = min(p[1], p[2]); t1 = max(p[1], p[2]);
+            p[1] = t0; p[2] = t1;
+            t0 = min(p[0], p[1]); t1 = max(p[0], p[1]);
+            p[0] = t0; p[1] = t1;
+            fold_rows<TC>(a, labels, cc, p, (int)k, crow, closed, acc);
+        } else {
+            int q[kSlots];
+            q[0] = r1.y;
+            q[1] = r1.z;
+            q[2] = r1.w;
+            const int* hi = vslot_hi + (long long)vid * kHiStride;
+#pragma unroll 1
+            for (unsigned j = kRecSlots; j < k; ++j) q[j] = hi[j - kRecSlots];
+#pragma unroll 1
+            for (unsigned j = 1; j < k; ++j) {   // insertion sort (k <= 16)
+                const int v = q[j];
+                int i = (int)j;
+                while (i > 0 && q[i - 1] > v) {
+                    q[i] = q[i - 1];
+                    --i;
+                }
+                q[i] = v;
+            }
+#pragma unroll 1
+            for (unsigned j0 = 0; j0 < k; j0 += 4) {
+                const int m = min(4, (int)(k - j0));
+                int p[4];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) p[t] = t < m ? q[j0 + t] : 0;
+                fold_rows<TC>(a, labels, cc, p, m, crow, closed, acc);
+            }
         }
-        unsigned big = __ballot_sync(0xffffffffu, e < U && k > 4u);
-        while (big) {
-            const int src = __ffs(big) - 1;
-            big &= big - 1;
-            const int bv = __shfl_sync(0xffffffffu, vid, src);
-            const unsigned bc = __shfl_sync(0xffffffffu, c, src);
-            const unsigned long long bk = __shfl_sync(0xffffffffu, key, src);
-            P2 bst;
-            bst.x = __shfl_sync(0xffffffffu, st.x, src);
-            bst.y = __shfl_sync(0xffffffffu, st.y, src);
-            slot_voxel_warp<TD, TC>(a, vslot, labels, kp, pp, vt, counts, bv, bc & ~kNewBit,
-                                    (bc & kNewBit) != 0u, bk, bst, closed);
+        // apply_tsdf (_pycore.py:399-417) on the pre-loaded pair
+        if (c & kNewBit) {
+            st.x = (TD)a.trunc;
+            st.y = (TD)0;
         }
+        const double w_old = (double)st.y, d_old = (double)st.x;
+        const double w_new = w_old + acc.sw;
+        double d_new = w_new > 0.0 ? (w_old * d_old + acc.swd) / w_new : d_old;
+        if ((acc.mind == acc.maxd) && (w_old == 0.0 || equals_stored<TD>(st.x, acc.mind)))
+            d_new = acc.mind;
+        P2 out;
+        out.x = (TD)d_new;
+        out.y = (TD)w_new;
+        reinterpret_cast<P2*>(vt)[vid] = out;
+        if (closed && a.last_wins)
+            for (int t = 0; t < a.C; ++t) crow[t] = (TC)(t == acc.last - 1 ? 1 : 0);
+        a.rec[vid].cnt = 0u;
     }
 }
 
@@ -610,10 +521,10 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) k_update_long(UpdateArgs a,
     const long long L = (long long)ctr->n_long;
     for (long long t = gw; t < L; t += nwarps) {
         const int vid = a.mlist[a.longlist[t]];
-        const unsigned c = a.vcnt[vid];
+        const unsigned c = a.rec[vid].cnt;
         const unsigned k = c & ~kNewBit;
-        warp_sort_segment(a.srid, a.vseg[vid], (int)k, buf);
-        const Center cc = center_of(a.vkey[vid], kp, a.h, pp);
+        warp_sort_segment(a.srid, a.rec[vid].seg, (int)k, buf);
+        const Center cc = center_of(a.rec[vid].key, kp, a.h, pp);
         TC* crow = counts + (long long)vid * a.C;
         TsdfAcc acc{0.0, 0.0, INFINITY, -INFINITY, 0};
         warp_tsdf_chunk<TC>(a, labels, buf, (int)k, cc, acc, crow, closed);
@@ -628,12 +539,12 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) k_update_long(UpdateArgs a,
     const long long Hn = (long long)ctr->n_huge;
     for (long long t = gw; t < Hn; t += kHugeWarps) {
         const int vid = a.mlist[a.hugelist[t]];
-        const unsigned c = a.vcnt[vid];
+        const unsigned c = a.rec[vid].cnt;
         const unsigned k = c & ~kNewBit;
         int minr;
         long long nwords;
-        bitmap_build(a.srid, a.vseg[vid], k, bm, minr, nwords);
-        const Center cc = center_of(a.vkey[vid], kp, a.h, pp);
+        bitmap_build(a.srid, a.rec[vid].seg, k, bm, minr, nwords);
+        const Center cc = center_of(a.rec[vid].key, kp, a.h, pp);
         TC* crow = counts + (long long)vid * a.C;
         TsdfAcc acc{0.0, 0.0, INFINITY, -INFINITY, 0};
         for (long long w0 = 0; w0 < nwords; w0 += 32) {
@@ -698,11 +609,11 @@ __device__ __forceinline__ void open_voxel(const UpdateArgs& a, const KeyPack& k
     const int lane = threadIdx.x & 31;
     const unsigned k = c & ~kNewBit;
     const bool isnew = (c & kNewBit) != 0u;
-    const Center cc = center_of(a.vkey[vid], kp, a.h, pp);
+    const Center cc = center_of(a.rec[vid].key, kp, a.h, pp);
     int minr = 0;
     long long nwords = 0;
-    if (huge) bitmap_build(a.srid, a.vseg[vid], k, bm, minr, nwords);
-    else warp_sort_segment(a.srid, a.vseg[vid], (int)k, buf);
+    if (huge) bitmap_build(a.srid, a.rec[vid].seg, k, bm, minr, nwords);
+    else warp_sort_segment(a.srid, a.rec[vid].seg, (int)k, buf);
     // TSDF sums in point order
     TsdfAcc acc{0.0, 0.0, INFINITY, -INFINITY, 0};
     if (huge) {
@@ -766,7 +677,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) k_update_open(UpdateArgs a,
     for (long long e = (long long)blockIdx.x * kWarpsPerCta + wib; e < L;
          e += (long long)gridDim.x * kWarpsPerCta) {
         const int vid = a.mlist[e];
-        const unsigned c = a.vcnt[vid];
+        const unsigned c = a.rec[vid].cnt;
         if ((c & ~kNewBit) > (unsigned)kSmemMax) {
             if (lane == 0) a.hugelist[atomicAdd(&ctr->n_huge, 1ULL)] = (int)e;
             continue;
@@ -791,7 +702,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) k_update_open_huge(UpdateAr
     const Fe* feats = (const Fe*)ctr->p.feats;
     for (long long t = gw; t < Hn; t += (long long)gridDim.x * kWarpsPerCta) {
         const int vid = a.mlist[a.hugelist[t]];
-        open_voxel<TD, TS, Fe>(a, kp, pp, vt, mean, beta, feats, vid, a.vcnt[vid], sbuf[wib], bm,
+        open_voxel<TD, TS, Fe>(a, kp, pp, vt, mean, beta, feats, vid, a.rec[vid].cnt, sbuf[wib], bm,
                                true);
     }
 }
@@ -815,10 +726,7 @@ __global__ void k_rehash(int64_t nblocks, const int4* __restrict__ bcoord, int4*
 UpdateArgs make_args(svx_map* m) {
     UpdateArgs a;
     a.mlist = ptr<int>(m->mlist);
-    a.vcnt = ptr<unsigned>(m->vcnt);
-    a.vseg = ptr<unsigned>(m->vseg);
-    a.vcur = ptr<unsigned>(m->vcur);
-    a.vkey = ptr<unsigned long long>(m->vkey);
+    a.rec = ptr<VoxFrame>(m->vrec);
     a.srid = ptr<int>(m->srid);
     a.ray = ptr<double4>(m->ray);
     a.longlist = ptr<int>(m->longlist);

@@ -119,18 +119,15 @@ def _check_pose(pose, frame_id):
     if pose.shape != (4, 4):
         raise UserInputError(f"pose must be 4x4, got {pose.shape}")
     f = pose.ravel().tolist()
-    if all(math.isfinite(v) for v in f) and f[12:16] == [0.0, 0.0, 0.0, 1.0]:
-        r0, r1, r2 = f[0:3], f[4:7], f[8:11]
-        rows = (r0, r1, r2)
-        err = 0.0
-        for a in range(3):
-            for b in range(3):
-                dot = rows[a][0] * rows[b][0] + rows[a][1] * rows[b][1] + rows[a][2] * rows[b][2]
-                err = max(err, abs(dot - (1.0 if a == b else 0.0)))
-        det = (r0[0] * (r1[1] * r2[2] - r1[2] * r2[1]) - r0[1] * (r1[0] * r2[2] - r1[2] * r2[0])
-               + r0[2] * (r1[0] * r2[1] - r1[1] * r2[0]))
+    a0, a1, a2, _, b0, b1, b2, _, c0, c1, c2, _, z0, z1, z2, z3 = f
+    if z0 == 0.0 and z1 == 0.0 and z2 == 0.0 and z3 == 1.0 and all(map(math.isfinite, f)):
+        # |R R^T - I| entrywise, straight-line
+        err = max(abs(a0 * a0 + a1 * a1 + a2 * a2 - 1.0), abs(b0 * b0 + b1 * b1 + b2 * b2 - 1.0),
+                  abs(c0 * c0 + c1 * c1 + c2 * c2 - 1.0), abs(a0 * b0 + a1 * b1 + a2 * b2),
+                  abs(a0 * c0 + a1 * c1 + a2 * c2), abs(b0 * c0 + b1 * c1 + b2 * c2))
+        det = a0 * (b1 * c2 - b2 * c1) - a1 * (b0 * c2 - b2 * c0) + a2 * (b0 * c1 - b1 * c0)
         if err <= _ROT_PASS * 0.5 and det > 0.0:
-            return np.array(pose, np.float64, copy=True, order="C")
+            return pose.copy(order="C")
     if not np.isfinite(pose).all():
         raise UserInputError("pose contains non-finite values")
     if not np.allclose(pose[3], (0, 0, 0, 1), atol=1e-9):
@@ -296,6 +293,8 @@ class Mapper:
         h = ctypes.c_void_p()
         check(lib.svx_create(ctypes.byref(c), ctypes.byref(h)))
         self._handle = h
+        self._rep = _lib.SvxReport()
+        self._rep_ref = ctypes.byref(self._rep)
         self._tsdf_view = GridView(self, KIND_TSDF)
         self._sem_view = None
         if closed is not None:
@@ -360,17 +359,16 @@ class Mapper:
         return pts
 
     def _run(self, fn, pts, vec, lab, feat):
-        rep = _lib.SvxReport()
+        rep = self._rep
         stream, all_dev = _stream_for((pts, lab, feat))
         # every input already on the map's GPU: skip the library's pointer checks
         flag = _lib.DEVICE_INPUTS if all_dev and pts.dev == self._device else 0
         n = int(pts.shape[0])
         vec = np.ascontiguousarray(vec, np.float64)
-        arr = vec.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
-        check(fn(self._handle, pts.ptr, pts.code | flag, n, arr,
+        check(fn(self._handle, pts.ptr, pts.code | flag, n, vec.ctypes.data,
                  lab.ptr if lab is not None else None,
                  feat.ptr if feat is not None else None,
-                 feat.code if feat is not None else SVX_F32, stream, ctypes.byref(rep)))
+                 feat.code if feat is not None else SVX_F32, stream, self._rep_ref))
         self._frames += 1
         return IntegrationReport(
             points_in=rep.points_in, points_used=rep.points_used,

@@ -18,6 +18,7 @@ timeout 600 python bench.py > "$OUT/${TAG}_bench.json" 2> "$OUT/${TAG}_bench.err
 echo "bench rc=$?" >> "$OUT/${TAG}_bench.err"
 timeout 300 python tools/host_overhead.py > "$OUT/${TAG}_host.txt" 2>&1
 timeout 300 python tools/host_overhead.py --mode segments >> "$OUT/${TAG}_host.txt" 2>&1
+SVX_TRACE_HOST=1 timeout 300 python tools/host_overhead.py --frames 12 > "$OUT/${TAG}_host_trace.txt" 2>&1
 [ -n "${WITH_REF:-}" ] && timeout 600 python bench.py --impl reference --steps 5 --warmup 3 > "$OUT/${TAG}_bench_ref.json" 2> "$OUT/${TAG}_bench_ref.err"
 echo "ref rc=$?" >> "$OUT/${TAG}_bench_ref.err" 2>/dev/null
 PCMD="python bench.py --steps 3 --warmup 3 --profile-frames 0 --no-cpu-baseline --no-e2e"

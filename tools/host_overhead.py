@@ -67,10 +67,11 @@ def main():
     rep = _lib.SvxReport()
     for f in frames[5:]:
         pose = np.ascontiguousarray(np.asarray(f.pose, np.float64).reshape(-1))
-        pp = pose.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+        pp = pose.ctypes.data
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        _lib.check(lib.svx_integrate(m2._handle, f.points.data_ptr(), 0, f.points.shape[0], pp,
+        _lib.check(lib.svx_integrate(m2._handle, f.points.data_ptr(), _lib.DEVICE_INPUTS,
+                                     f.points.shape[0], pp,
                                      f.labels.data_ptr(), None, 0, None, ctypes.byref(rep)))
         raw.append((time.perf_counter() - t0) * 1e3)
     med = statistics.median
