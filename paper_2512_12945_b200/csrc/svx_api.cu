@@ -179,7 +179,7 @@ svx_status svx_destroy(svx_map* m) {
     DevBuf* bufs[] = {&m->hash, &m->bcoord, &m->bkey, &m->bmask, &m->bslot, &m->vt,
                       &m->s0, &m->s1, &m->vrec, &m->vslot, &m->in_pts,
                       &m->in_lab, &m->in_feat, &m->ray, &m->rcnt, &m->roff, &m->rowkey,
-                      &m->rowvid, &m->rowray, &m->partials, &m->tlist, &m->mlist,
+                      &m->rowvid, &m->rowray, &m->rowd, &m->rowlab, &m->partials, &m->tlist, &m->mlist,
                       &m->longlist, &m->srid, &m->bitmap, &m->cubtmp, &m->ctr, &m->ord0,
                       &m->ord1, &m->ordk0, &m->ordk1, &m->ordf0, &m->ordf1, &m->act_cnt,
                       &m->act_off, &m->act_vid, &m->act_coord, &m->q_buf, &m->out_buf};

@@ -84,7 +84,7 @@ svx_status reserve_voxels(svx_map* m, int64_t need, cudaStream_t s) {
         SVX_TRY(ensure(m->s1, se * (size_t)m->payload_d * cap, s, true, 0));
     SVX_TRY(ensure(m->vrec, sizeof(VoxFrame) * cap, s, true, 0));
     if (m->cfg.sem_kind != SVX_SEM_OPEN && !m->cfg.space_carving)   // per-frame contents only
-        SVX_TRY(ensure(m->vslot, sizeof(int) * kHiStride * cap, s));
+        SVX_TRY(ensure(m->vslot, sizeof(RowSlot) * kSlots * cap, s));
     m->vcap = cap;
     return SVX_OK;
 }
@@ -130,6 +130,10 @@ svx_status reserve_frame(svx_map* m, int64_t n, cudaStream_t s) {
     SVX_TRY(ensure(m->srid, sizeof(int) * rows, s));
     SVX_TRY(ensure(m->bitmap, (size_t)4 * huge_warps() * ((m->npts_cap + 31) / 32 + 1), s));
     SVX_TRY(ensure(m->rowray, sizeof(int) * rows, s));
+    if (m->cfg.sem_kind != SVX_SEM_OPEN && !m->cfg.space_carving) {   // slot mode row payload
+        SVX_TRY(ensure(m->rowd, sizeof(double) * rows, s));
+        SVX_TRY(ensure(m->rowlab, sizeof(int) * rows, s));
+    }
     if (m->maxrows == 0) {   // two-pass walk: per-ray offsets from a scan
         SVX_TRY(ensure(m->roff, sizeof(long long) * m->npts_cap, s));
         SVX_TRY(ensure(m->cubtmp, scan_temp_bytes(m->npts_cap), s));
@@ -144,7 +148,8 @@ static unsigned long long graph_signature(const svx_map* m, int pts_f64, int fea
                           m->rowray.p, m->partials.p, m->tlist.p, m->mlist.p,  m->longlist.p,
                           m->srid.p,   m->bitmap.p, m->cubtmp.p,  m->hash.p,   m->bcoord.p,
                           m->bkey.p,   m->bmask.p,  m->bslot.p,   m->vt.p,     m->s0.p,
-                          m->s1.p,     m->vrec.p,   m->vslot.p,   m->ctr.p};
+                          m->s1.p,     m->vrec.p,   m->vslot.p,   m->rowd.p,   m->rowlab.p,
+                          m->ctr.p};
     unsigned long long h = 1469598103934665603ULL;
     auto mix = [&](unsigned long long v) {
         h ^= v;

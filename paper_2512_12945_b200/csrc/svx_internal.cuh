@@ -125,16 +125,21 @@ struct FrameCtr {
 //   seg   base of the voxel's row segment (segment mode)
 //   key   the voxel's frame key (written by its first toucher)
 //   cur   segment fill cursor (segment mode)
-//   slot  slot mode: point indices of rows 0..2; rows 3..15 go to vslot_hi
+// Slot mode keeps each voxel's rows in vslot[vid * kSlots + j] = RowSlot
+// {point, label, d}: the row's distance was computed by the walk, so the
+// update reads everything it needs from the slots (rows 0-1 share a sector).
 constexpr unsigned kNewBit = 0x80000000u;
-constexpr int kRecSlots = 3;
-constexpr int kHiStride = 16;   // vslot_hi[vid * 16 + (j - 3)], 3 <= j < kSlots
 struct alignas(32) VoxFrame {
     unsigned cnt;
     unsigned seg;
     unsigned long long key;
     unsigned cur;
-    int slot[kRecSlots];
+    unsigned pad[3];
+};
+struct alignas(16) RowSlot {
+    int point;
+    int label;
+    double d;
 };
 static_assert(sizeof(VoxFrame) == 32, "VoxFrame must be one sector");
 
@@ -192,7 +197,7 @@ struct svx_map {
     svx::DevBuf bcoord, bkey, bmask, bslot;  int64_t bcap = 0, nblocks = 0;
     svx::DevBuf vt, s0, s1;                  int64_t vcap = 0, nvox = 0;  // vt: {d, w} per voxel
     svx::DevBuf vrec;                        // per-voxel frame records (svx::VoxFrame)
-    svx::DevBuf vslot;                       // slot mode: rows 3..15 of each voxel
+    svx::DevBuf vslot;                       // slot mode: kSlots RowSlots per voxel
     int64_t n_slot_frames = 0, n_slot_reruns = 0;
     int mode_pref = 0;      // SVX_UPDATE_AUTO / SEGMENTS / SLOTS
     int slot_hold = 0;      // frames to stay in segment mode after a slot overflow
@@ -203,7 +208,7 @@ struct svx_map {
     unsigned seq = 0;   // frame launches so far (attempts included)
     // per-frame scratch
     svx::DevBuf in_pts, in_lab, in_feat;
-    svx::DevBuf ray, rcnt, roff, rowkey, rowvid, rowray, partials;
+    svx::DevBuf ray, rcnt, roff, rowkey, rowvid, rowray, rowd, rowlab, partials;
     svx::DevBuf tlist, mlist, longlist, srid, bitmap;
     uint64_t ucap = 0, rcap = 0;
     int64_t new_leaves_cap = 0;   // leaf-pool headroom kept for one frame

@@ -251,12 +251,17 @@ __device__ __forceinline__ void finish_walk(const Tally& t, MarchPartial* partia
 // are then written coalesced (rowkey, rowray).
 constexpr int kTileRays = 128;
 
+// Slot mode also writes each row's clamped distance d (row_distances_weights,
+// _pycore.py:384-396, the same expression K5 would evaluate) and its point's
+// label, so the slot update needs no gathers.
 template <class P, class Fe>
 __global__ void __launch_bounds__(kTileRays, 4) k_walk(MarchParams mp, int sem_kind, int num_classes,
                                                     int D, double4* __restrict__ ray,
                                                     int* __restrict__ rcnt,
                                                     unsigned long long* __restrict__ rowkey,
                                                     int* __restrict__ rowray,
+                                                    double* __restrict__ rowd,
+                                                    int* __restrict__ rowlab,
                                                     MarchPartial* __restrict__ partials,
                                                     FrameCtr* __restrict__ ctr) {
     grid_dep_wait();
@@ -264,10 +269,13 @@ __global__ void __launch_bounds__(kTileRays, 4) k_walk(MarchParams mp, int sem_k
     __shared__ typename Scan::TempStorage scan_tmp;
     __shared__ unsigned long long s_base;
     __shared__ int s_off[kTileRays];
+    __shared__ double4 s_ray[kTileRays];
+    __shared__ int s_lab[kTileRays];
     extern __shared__ unsigned long long s_keys[];   // kTileRays * maxrows keys, then row owners
     const FrameParams fp = ctr->p;
     const long long n = fp.n;
     const int maxrows = fp.maxrows;
+    const bool slots = fp.slots != 0;
     const unsigned long long rcap = fp.rcap;
     unsigned char* s_own = reinterpret_cast<unsigned char*>(s_keys + (size_t)kTileRays * maxrows);
     const double ox = fp.pp.t[0], oy = fp.pp.t[1], oz = fp.pp.t[2];
@@ -306,6 +314,10 @@ __global__ void __launch_bounds__(kTileRays, 4) k_walk(MarchParams mp, int sem_k
             }
             ray[i] = r;
             rcnt[i] = rows;
+            if (slots) {
+                s_ray[threadIdx.x] = r;
+                s_lab[threadIdx.x] = sem_kind == SVX_SEM_CLOSED ? fp.labels[i] : 0;
+            }
         }
         int off, total;
         Scan(scan_tmp).ExclusiveSum(rows, off, total);
@@ -321,8 +333,24 @@ __global__ void __launch_bounds__(kTileRays, 4) k_walk(MarchParams mp, int sem_k
         if (base + (unsigned long long)total <= rcap) {
             for (int e = threadIdx.x; e < total; e += kTileRays) {
                 const int o = s_own[e];
-                rowkey[base + e] = s_keys[(size_t)o * maxrows + (e - s_off[o])];
+                const unsigned long long key = s_keys[(size_t)o * maxrows + (e - s_off[o])];
+                rowkey[base + e] = key;
                 rowray[base + e] = (int)(ray0 + o);
+                if (slots) {
+                    // d of this row exactly as row_dw evaluates it from the voxel centre
+                    long long x, y, z;
+                    unpack_key(key, fp.kp, x, y, z);
+                    const double4 r = s_ray[o];
+                    const double cx = ((double)x + 0.5) * mp.h - ox;
+                    const double cy = ((double)y + 0.5) * mp.h - oy;
+                    const double cz = ((double)z + 0.5) * mp.h - oz;
+                    const double proj = cx * r.x + cy * r.y + cz * r.z;
+                    double d = r.w - proj;
+                    if (d < -mp.trunc) d = -mp.trunc;
+                    if (d > mp.trunc) d = mp.trunc;
+                    rowd[base + e] = d;
+                    rowlab[base + e] = s_lab[o];
+                }
             }
         } else if (threadIdx.x == 0) {
             atomicOr(&ctr->err_cap, 1);
@@ -482,7 +510,8 @@ svx_status march_t(svx_map* m, cudaStream_t s) {
         const size_t smem = (size_t)kTileRays * m->maxrows * (sizeof(unsigned long long) + 1);
         SVX_CUDA(launch_pdl(k_walk<P, Fe>, kMarchBlocks, kTileRays, smem, s, 
             mp, m->cfg.sem_kind, m->cfg.num_classes, m->payload_d, ptr<double4>(m->ray),
-            ptr<int>(m->rcnt), ptr<unsigned long long>(m->rowkey), ptr<int>(m->rowray), parts, dc));
+            ptr<int>(m->rcnt), ptr<unsigned long long>(m->rowkey), ptr<int>(m->rowray),
+            ptr<double>(m->rowd), ptr<int>(m->rowlab), parts, dc));
         SVX_LAUNCHED();
         return SVX_OK;
     }

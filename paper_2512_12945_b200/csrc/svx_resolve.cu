@@ -123,7 +123,8 @@ __device__ int leaf_find_or_insert(int4* table, long long mask, int a, int b, in
 // published, so no thread ever waits across a barrier.
 __global__ void __launch_bounds__(kResolveThreads) k_resolve(
     const unsigned long long* __restrict__ rowkey, const int* __restrict__ rowray,
-    int* __restrict__ rowvid, int* __restrict__ vslot, int4* table, int4* bcoord,
+    const double* __restrict__ rowd, const int* __restrict__ rowlab,
+    int* __restrict__ rowvid, RowSlot* __restrict__ vslot, int4* table, int4* bcoord,
     unsigned long long* bkey, unsigned long long* bmask, int* bslot, VoxFrame* rec,
     int* __restrict__ tlist, FrameCtr* ctr) {
     grid_dep_wait();
@@ -143,7 +144,12 @@ __global__ void __launch_bounds__(kResolveThreads) k_resolve(
         const long long t = tile * kResolveThreads + threadIdx.x;
         const bool valid = t < total;
         const unsigned long long key = valid ? rowkey[t] : kKeyEmpty;
-        const int pidx = (valid && slots) ? rowray[t] : 0;
+        RowSlot rsl{0, 0, 0.0};
+        if (valid && slots) {
+            rsl.point = rowray[t];
+            rsl.label = rowlab[t];
+            rsl.d = rowd[t];
+        }
         long long x = 0, y = 0, z = 0;
         if (valid) unpack_key(key, kp, x, y, z);
         const unsigned vpeers = __match_any_sync(full, valid ? key : (kKeyEmpty ^ (unsigned long long)lane));
@@ -273,8 +279,7 @@ __global__ void __launch_bounds__(kResolveThreads) k_resolve(
             // restored by point index in k_update_slots)
             cbase = __shfl_sync(full, cbase, vleader) + __popc(vpeers & ((1u << lane) - 1u));
             if (valid && vid >= 0) {
-                if (cbase < (unsigned)kRecSlots) rec[vid].slot[cbase] = pidx;
-                else if (cbase < (unsigned)kSlots) vslot[(long long)vid * kHiStride + (cbase - kRecSlots)] = pidx;
+                if (cbase < (unsigned)kSlots) vslot[(long long)vid * kSlots + cbase] = rsl;
                 else ctr->err_slots = 1;
             }
         } else if (valid) {
@@ -431,7 +436,8 @@ svx_status cleanup_t(svx_map* m, cudaStream_t s) {
 
 svx_status launch_resolve(svx_map* m, cudaStream_t s) {
     SVX_CUDA(launch_pdl(k_resolve, kPersistentBlocks, kResolveThreads, 0, s, 
-        ptr<unsigned long long>(m->rowkey), ptr<int>(m->rowray), ptr<int>(m->rowvid), ptr<int>(m->vslot),
+        ptr<unsigned long long>(m->rowkey), ptr<int>(m->rowray), ptr<double>(m->rowd), ptr<int>(m->rowlab),
+        ptr<int>(m->rowvid), ptr<RowSlot>(m->vslot),
         ptr<int4>(m->hash), ptr<int4>(m->bcoord),
         ptr<unsigned long long>(m->bkey), ptr<unsigned long long>(m->bmask), ptr<int>(m->bslot),
         ptr<VoxFrame>(m->vrec), ptr<int>(m->tlist),

@@ -308,6 +308,7 @@ svx_status shard_march(svx_map* m, const void* pts_in, int pts_f64, int64_t n, c
     for (int attempt = 0;; ++attempt) {
         if (attempt >= 8) return fail(SVX_E_INTERNAL, "frame scratch could not be sized");
         SVX_TRY(reserve_frame(m, n, s));
+        m->frame_slots = 0;   // shard rows travel without d / labels; owners use segments
         reset_ctr(m);
         FrameParams& p = hc->p;
         p.pts = pts;

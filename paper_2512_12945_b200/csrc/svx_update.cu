@@ -235,111 +235,96 @@ __global__ void __launch_bounds__(256) k_update_short(UpdateArgs a, TD* vt, TC* 
 }
 
 // ---- K5 slot mode: one thread per touched voxel (closed / geometry) --------------
-// The voxel's frame record (count, key, rows 0..2) and its TSDF pair are read
-// together; rows arrive in arbitrary order and are put in ascending point
-// order before the sequential sums (the reference's (voxel, point) order), so
-// the arithmetic is exactly k_update_short's.  Voxels of up to 3 rows (~94%
-// on LiDAR frames) sort in registers; 4..16 rows take a local-array path.
+// Each voxel's rows sit in its slots as {point, label, d} (d computed by the
+// walk), so a voxel needs its count, its TSDF pair and its slots -- three
+// independent loads, no gathers.  Rows are folded in ascending point order
+// (the reference's (voxel, point) order) with the sequential sums of
+// k_update_short; two rows need no sort for the sums (IEEE addition is
+// commutative) but are ordered anyway for last-wins.
 
-template <class TC>
 struct RowAcc {
     double sw = 0.0, swd = 0.0, mind = INFINITY, maxd = -INFINITY;
     int last = 0;
 };
 
-// Fold up to 4 rows (point indices p[0..m), ascending) into the sums.
 template <class TC>
-__device__ __forceinline__ void fold_rows(const UpdateArgs& a, const int32_t* __restrict__ labels,
-                                          const Center& cc, const int (&p)[4], int m, TC* crow,
-                                          bool closed, RowAcc<TC>& acc) {
-    double4 ry[4];
-    int lab[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        if (q < m) {
-            ry[q] = a.ray[p[q]];
-            lab[q] = closed ? labels[p[q]] : 0;
-        }
-    }
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        if (q < m) {
-            double d, w;
-            row_dw(cc.x, cc.y, cc.z, ry[q], a.trunc, a.wfn, d, w);
-            acc.sw += w;
-            acc.swd += w * d;
-            acc.mind = d < acc.mind ? d : acc.mind;
-            acc.maxd = d > acc.maxd ? d : acc.maxd;
-            if (closed) {
-                if (a.last_wins) acc.last = lab[q];
-                else atomicAdd(&crow[lab[q] - 1], (TC)1);   // integer count: order-free
-            }
-        }
+__device__ __forceinline__ void fold_row(const UpdateArgs& a, double d, int lab, TC* crow,
+                                         bool closed, RowAcc& acc) {
+    // weight of row_dw (_pycore.py:384-396) from the stored clamped distance
+    const double w = (a.wfn == 1) ? (d >= 0.0 ? 1.0 : (a.trunc + d) / a.trunc) : 1.0;
+    acc.sw += w;
+    acc.swd += w * d;
+    acc.mind = d < acc.mind ? d : acc.mind;
+    acc.maxd = d > acc.maxd ? d : acc.maxd;
+    if (closed) {
+        if (a.last_wins) acc.last = lab;
+        else atomicAdd(&crow[lab - 1], (TC)1);   // integer count: order-free
     }
 }
 
+__device__ __forceinline__ RowSlot ld_slot16(const RowSlot* p) {
+    const int4 v = *reinterpret_cast<const int4*>(p);
+    RowSlot r;
+    r.point = v.x;
+    r.label = v.y;
+    r.d = __hiloint2double(v.w, v.z);
+    return r;
+}
+
 template <class TD, class TC>
-__global__ void __launch_bounds__(256, 4) k_update_slots(UpdateArgs a, const int* __restrict__ tlist,
-                                                         const int* __restrict__ vslot_hi, TD* vt,
-                                                         TC* counts) {
+__global__ void __launch_bounds__(256) k_update_slots(UpdateArgs a, const int* __restrict__ tlist,
+                                                      const RowSlot* __restrict__ vslot, TD* vt,
+                                                      TC* counts) {
     grid_dep_wait();
     FrameCtr* ctr = a.ctr;
     if (ctr->abort | ctr->err_cap | ctr->err_slots) return;
     const long long U = (long long)ctr->n_touched;
-    const KeyPack kp = ctr->p.kp;
-    const PoseParams pp = ctr->p.pp;
-    const int32_t* __restrict__ labels = ctr->p.labels;
     const bool closed = a.sem_kind == SVX_SEM_CLOSED;
     using P2 = typename Pair<TD>::type;
     for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < U;
          e += (long long)gridDim.x * blockDim.x) {
         const int vid = tlist[e];
-        const int4 r0 = reinterpret_cast<const int4*>(a.rec + vid)[0];   // cnt, seg, key
-        const int4 r1 = reinterpret_cast<const int4*>(a.rec + vid)[1];   // cur, slot[0..2]
+        const unsigned c = a.rec[vid].cnt;
         P2 st = reinterpret_cast<const P2*>(vt)[vid];
-        const unsigned c = (unsigned)r0.x;
+        const RowSlot* sl = vslot + (long long)vid * kSlots;
+        RowSlot s0 = ld_slot16(sl), s1 = ld_slot16(sl + 1);   // rows 0-1: one sector
         const unsigned k = c & ~kNewBit;
-        const unsigned long long key =
-            ((unsigned long long)(unsigned)r0.w << 32) | (unsigned long long)(unsigned)r0.z;
-        const Center cc = center_of(key, kp, a.h, pp);
         TC* crow = counts + (long long)vid * a.C;
-        RowAcc<TC> acc;
-        if (k <= 3u) {
-            int p[4] = {r1.y, k > 1u ? r1.z : 0x7fffffff, k > 2u ? r1.w : 0x7fffffff, 0x7fffffff};
-            // 3-element sorting network
-            int t0 = min(p[0], p[1]), t1 = max(p[0], p[1]);
-            p[0] = t0; p[1] = t1;
-            t0 = min(p[1], p[2]); t1 = max(p[1], p[2]);
-            p[1] = t0; p[2] = t1;
-            t0 = min(p[0], p[1]); t1 = max(p[0], p[1]);
-            p[0] = t0; p[1] = t1;
-            fold_rows<TC>(a, labels, cc, p, (int)k, crow, closed, acc);
+        RowAcc acc;
+        if (k <= 2u) {
+            if (k == 2u && s1.point < s0.point) {
+                const RowSlot t = s0;
+                s0 = s1;
+                s1 = t;
+            }
+            fold_row<TC>(a, s0.d, s0.label, crow, closed, acc);
+            if (k == 2u) fold_row<TC>(a, s1.d, s1.label, crow, closed, acc);
         } else {
-            int q[kSlots];
-            q[0] = r1.y;
-            q[1] = r1.z;
-            q[2] = r1.w;
-            const int* hi = vslot_hi + (long long)vid * kHiStride;
+            // 3..16 rows: insertion sort by point index in a local array
+            RowSlot q[kSlots];
+            q[0] = s0;
+            q[1] = s1;
 #pragma unroll 1
-            for (unsigned j = kRecSlots; j < k; ++j) q[j] = hi[j - kRecSlots];
-#pragma unroll 1
-            for (unsigned j = 1; j < k; ++j) {   // insertion sort (k <= 16)
-                const int v = q[j];
+            for (unsigned j = 2; j < k; ++j) {
+                const RowSlot v = ld_slot16(sl + j);
                 int i = (int)j;
-                while (i > 0 && q[i - 1] > v) {
+                while (i > 0 && q[i - 1].point > v.point) {
                     q[i] = q[i - 1];
                     --i;
                 }
                 q[i] = v;
             }
-#pragma unroll 1
-            for (unsigned j0 = 0; j0 < k; j0 += 4) {
-                const int m = min(4, (int)(k - j0));
-                int p[4];
-#pragma unroll
-                for (int t = 0; t < 4; ++t) p[t] = t < m ? q[j0 + t] : 0;
-                fold_rows<TC>(a, labels, cc, p, m, crow, closed, acc);
+            if (q[1].point < q[0].point) {   // rows 0-1 arrived unsorted
+                const RowSlot t = q[0];
+                int i = 0;
+                while (i + 1 < (int)k && q[i + 1].point < t.point) {
+                    q[i] = q[i + 1];
+                    ++i;
+                }
+                q[i] = t;
             }
+#pragma unroll 1
+            for (unsigned j = 0; j < k; ++j) fold_row<TC>(a, q[j].d, q[j].label, crow, closed, acc);
         }
         // apply_tsdf (_pycore.py:399-417) on the pre-loaded pair
         if (c & kNewBit) {
@@ -793,7 +778,7 @@ svx_status open_b(svx_map* m, cudaStream_t s) {
 template <class TD, class TC>
 svx_status slots_t(svx_map* m, cudaStream_t s) {
     SVX_CUDA(launch_pdl(k_update_slots<TD, TC>, kShortBlocks, 256, 0, s, make_args(m),
-                        ptr<int>(m->tlist), ptr<int>(m->vslot), ptr<TD>(m->vt), ptr<TC>(m->s0)));
+                        ptr<int>(m->tlist), ptr<RowSlot>(m->vslot), ptr<TD>(m->vt), ptr<TC>(m->s0)));
     SVX_LAUNCHED();
     return SVX_OK;
 }
