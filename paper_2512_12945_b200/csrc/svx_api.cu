@@ -180,7 +180,7 @@ svx_status svx_destroy(svx_map* m) {
                       &m->s0, &m->s1, &m->vrec, &m->vslot, &m->in_pts,
                       &m->in_lab, &m->in_feat, &m->ray, &m->rcnt, &m->roff, &m->rowkey,
                       &m->rowvid, &m->rowray, &m->rowd, &m->rowlab, &m->partials, &m->tlist, &m->mlist,
-                      &m->longlist, &m->srid, &m->bitmap, &m->cubtmp, &m->ctr, &m->ord0,
+                      &m->longlist, &m->srid, &m->bitmap, &m->rcount, &m->cubtmp, &m->ctr, &m->ord0,
                       &m->ord1, &m->ordk0, &m->ordk1, &m->ordf0, &m->ordf1, &m->act_cnt,
                       &m->act_off, &m->act_vid, &m->act_coord, &m->q_buf, &m->out_buf};
     for (DevBuf* b : bufs) release(*b);
@@ -270,7 +270,7 @@ svx_status svx_stats_get(svx_map* m, svx_stats* out) {
     int64_t per_vox = 2 * te + se * m->payload_d * (m->cfg.sem_kind == SVX_SEM_OPEN ? 2 : 1);
     out->leaf_count = m->nblocks;
     out->active_voxels = m->nvox;
-    out->resident_bytes = m->nblocks * (int64_t)(sizeof(int4) + 8 * kMaskWords + 4 * kLeafVolume) +
+    out->resident_bytes = m->nblocks * (int64_t)(sizeof(int4) + 8 * kMaskWords + 8 * kLeafVolume) +
                           m->nvox * per_vox + m->hcap * (int64_t)sizeof(int4);
     out->payload_bytes_per_voxel = per_vox;
     out->frames_integrated = m->frames;

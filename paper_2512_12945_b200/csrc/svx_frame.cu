@@ -95,7 +95,10 @@ svx_status reserve_blocks(svx_map* m, int64_t need, cudaStream_t s) {
         SVX_TRY(ensure(m->bcoord, sizeof(int4) * cap, s, true));
         SVX_TRY(ensure(m->bkey, sizeof(unsigned long long) * cap, s, true, 0xFF));
         SVX_TRY(ensure(m->bmask, sizeof(unsigned long long) * kMaskWords * cap, s, true, 0));
-        SVX_TRY(ensure(m->bslot, sizeof(int) * kLeafVolume * cap, s, true, 0xFF));
+        const int64_t old = m->bcap;
+        SVX_TRY(ensure(m->bslot, sizeof(unsigned long long) * kLeafVolume * cap, s, true));
+        SVX_TRY(launch_fill_u64(ptr<unsigned long long>(m->bslot) + old * kLeafVolume,
+                                (cap - old) * kLeafVolume, kSlotInactive, s));
         m->bcap = cap;
     }
     // keep the leaf hash at <= 50% load when the pool is full
@@ -124,7 +127,9 @@ svx_status reserve_frame(svx_map* m, int64_t n, cudaStream_t s) {
     SVX_TRY(ensure(m->partials, partials_bytes() + segment_status_bytes(m->ucap), s, false, 0));
     SVX_TRY(ensure(m->rowkey, sizeof(unsigned long long) * rows, s));
     SVX_TRY(ensure(m->rowvid, sizeof(int) * rows, s));
-    SVX_TRY(ensure(m->tlist, sizeof(int) * rows, s));
+    SVX_TRY(ensure(m->tlist, std::max<size_t>(sizeof(int) * rows,
+                                              sizeof(TouchEntry) * kPersistentBlocks * slot_region(rows)), s));
+    SVX_TRY(ensure(m->rcount, sizeof(unsigned) * kPersistentBlocks, s));
     SVX_TRY(ensure(m->mlist, sizeof(int) * rows, s));
     SVX_TRY(ensure(m->longlist, 2 * sizeof(int) * rows, s));   // long list, then huge list
     SVX_TRY(ensure(m->srid, sizeof(int) * rows, s));
@@ -145,7 +150,7 @@ svx_status reserve_frame(svx_map* m, int64_t n, cudaStream_t s) {
 // size grids or index scratch, and kernel template choices.
 static unsigned long long graph_signature(const svx_map* m, int pts_f64, int feats_f64) {
     const void* ptrs[] = {m->ray.p,    m->rcnt.p,   m->roff.p,    m->rowkey.p, m->rowvid.p,
-                          m->rowray.p, m->partials.p, m->tlist.p, m->mlist.p,  m->longlist.p,
+                          m->rowray.p, m->partials.p, m->tlist.p, m->mlist.p,  m->longlist.p, m->rcount.p,
                           m->srid.p,   m->bitmap.p, m->cubtmp.p,  m->hash.p,   m->bcoord.p,
                           m->bkey.p,   m->bmask.p,  m->bslot.p,   m->vt.p,     m->s0.p,
                           m->s1.p,     m->vrec.p,   m->vslot.p,   m->rowd.p,   m->rowlab.p,
@@ -306,6 +311,7 @@ void reset_ctr(svx_map* m) {
     p.maxrows = m->maxrows;
     p.inline_singles = inline_singles(m);
     p.slots = m->frame_slots;
+    p.region = slot_region(m->rcap);
     p.seq = ++m->seq;
 }
 

@@ -76,6 +76,7 @@ struct FrameParams {
     int maxrows;               // row slots per ray; 0 = dense rows (two-pass walk)
     int inline_singles;        // single-row voxels updated in the scatter (closed/geometry)
     int slots;                 // 1: slot mode (K2 fills vslot; K5 = k_update_slots)
+    long long region;          // slot mode: touched entries per K2 CTA (svx::slot_region)
     unsigned seq;              // launch sequence number (epoch of the segment-scan status)
 };
 
@@ -136,6 +137,15 @@ struct alignas(32) VoxFrame {
     unsigned cur;
     unsigned pad[3];
 };
+// Slot mode touched entry: the voxel id (bit 31 = created this frame;
+// 0xFFFFFFFF = its claim failed) and its bslot index (leaf * 512 + slot).
+struct TouchEntry {
+    unsigned vid;
+    unsigned bidx;
+};
+// bslot words: low half = voxel id, high half = slot-mode frame row count.
+constexpr unsigned long long kSlotInactive = 0x00000000FFFFFFFFULL;   // id -1, count 0
+constexpr unsigned long long kSlotClaim = 0x00000000FFFFFFFEULL;      // segment mode claim (-2)
 struct alignas(16) RowSlot {
     int point;
     int label;
@@ -209,7 +219,7 @@ struct svx_map {
     // per-frame scratch
     svx::DevBuf in_pts, in_lab, in_feat;
     svx::DevBuf ray, rcnt, roff, rowkey, rowvid, rowray, rowd, rowlab, partials;
-    svx::DevBuf tlist, mlist, longlist, srid, bitmap;
+    svx::DevBuf tlist, mlist, longlist, srid, bitmap, rcount;
     uint64_t ucap = 0, rcap = 0;
     int64_t new_leaves_cap = 0;   // leaf-pool headroom kept for one frame
     int maxrows = -1;      // row slots per ray; 0 = dense rows
@@ -321,6 +331,13 @@ inline int grid_for(int64_t n, int threads) {
 }
 
 constexpr int kPersistentBlocks = 148 * 8;   // grid-stride kernels over device-side counts
+constexpr int kResolveTile = 256;            // K2 rows per CTA step
+// Slot mode: K2 CTA b lists its touched voxels in tent[b * region, ...); a CTA
+// handles at most ceil(tiles / grid) tiles of kResolveTile rows.
+inline long long slot_region(unsigned long long rows_cap) {
+    const long long tiles = (long long)((rows_cap + kResolveTile - 1) / kResolveTile);
+    return ((tiles + kPersistentBlocks - 1) / kPersistentBlocks) * kResolveTile;
+}
 constexpr int kMarchBlocks = 148 * 4;        // march CTAs (one partial-counter record each)
 
 // TSDF state of one voxel, {d, w} interleaved so an update touches one sector.
@@ -391,6 +408,7 @@ svx_status launch_update_a(svx_map* m, int feats_f64, cudaStream_t s);
 svx_status launch_update_b(svx_map* m, int feats_f64, cudaStream_t s);
 svx_status launch_update_slots(svx_map* m, cudaStream_t s);
 svx_status launch_rehash(svx_map* m, int4* new_table, int64_t new_cap, cudaStream_t s);
+svx_status launch_fill_u64(unsigned long long* p, int64_t n, unsigned long long v, cudaStream_t s);
 int huge_warps();
 
 // frame driver pieces shared by svx_integrate and the sharded calls (svx_frame.cu)

@@ -62,7 +62,7 @@ __global__ void k_leaf_stamps(int64_t nblocks, const int* __restrict__ order,
 // One warp per leaf: lanes cover 32 slots at a time, ballot/popc give ranks.
 __global__ void k_list(int64_t nblocks, const int* __restrict__ order,
                        const unsigned long long* __restrict__ bmask,
-                       const int* __restrict__ bslot, const int4* __restrict__ bcoord,
+                       const unsigned long long* __restrict__ bslot, const int4* __restrict__ bcoord,
                        const long long* __restrict__ off, int* __restrict__ act_vid,
                        long long* __restrict__ act_coord) {
     int64_t ob = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -78,7 +78,7 @@ __global__ void k_list(int64_t nblocks, const int* __restrict__ order,
         if ((bits >> lane) & 1u) {
             int slot = half * 32 + lane;
             long long p = pos + __popc(bits & ((1u << lane) - 1u));
-            act_vid[p] = bslot[b * kLeafVolume + slot];
+            act_vid[p] = (int)(unsigned)bslot[b * kLeafVolume + slot];
             act_coord[3 * p] = ((long long)bc.x << kLeafLog2) + ((slot >> 6) & 7);
             act_coord[3 * p + 1] = ((long long)bc.y << kLeafLog2) + ((slot >> 3) & 7);
             act_coord[3 * p + 2] = ((long long)bc.z << kLeafLog2) + (slot & 7);
@@ -107,7 +107,7 @@ __global__ void k_copy_coords(int64_t count, const long long* __restrict__ src,
 
 __global__ void k_probe_vid(int64_t cnt, const long long* __restrict__ coords,
                             const int4* __restrict__ table, int64_t mask,
-                            const int* __restrict__ bslot, int* __restrict__ vid_out,
+                            const unsigned long long* __restrict__ bslot, int* __restrict__ vid_out,
                             uint8_t* __restrict__ active) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= cnt) return;
@@ -117,7 +117,7 @@ __global__ void k_probe_vid(int64_t cnt, const long long* __restrict__ coords,
     int vid = -1;
     if (blk >= 0) {
         int slot = (int)(((x & 7) << 6) | ((y & 7) << 3) | (z & 7));
-        vid = bslot[(int64_t)blk * kLeafVolume + slot];
+        vid = (int)(unsigned)bslot[(int64_t)blk * kLeafVolume + slot];
     }
     vid_out[i] = vid;
     if (active) active[i] = vid >= 0;
@@ -327,7 +327,7 @@ svx_status build_active_list(svx_map* m, int64_t* count, cudaStream_t s) {
                                            ptr<long long>(m->act_off), (int)nb, s));
     count_launch();
     k_list<<<grid_for(nb * 32, T), T, 0, s>>>(nb, order, ptr<unsigned long long>(m->bmask),
-                                             ptr<int>(m->bslot), ptr<int4>(m->bcoord),
+                                             ptr<unsigned long long>(m->bslot), ptr<int4>(m->bcoord),
                                              ptr<long long>(m->act_off), ptr<int>(m->act_vid),
                                              ptr<long long>(m->act_coord));
     SVX_LAUNCHED();
@@ -419,7 +419,7 @@ svx_status launch_probe(svx_map* m, const int64_t* coords, int64_t cnt, void* d,
     } else {
         k_probe_vid<<<grid_for(cnt, 256), 256, 0, s>>>(cnt, (const long long*)coords,
                                                        ptr<int4>(m->hash), m->hcap - 1,
-                                                       ptr<int>(m->bslot), vid, active);
+                                                       ptr<unsigned long long>(m->bslot), vid, active);
         SVX_LAUNCHED();
     }
     const int td64 = m->cfg.tsdf_dtype == SVX_F64;

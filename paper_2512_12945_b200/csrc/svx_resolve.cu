@@ -23,269 +23,59 @@
 #include <cub/block/block_scan.cuh>
 
 #include "svx_internal.cuh"
+#include "svx_resolve_tile.cuh"
 
 namespace svx {
 namespace {
 
-constexpr int kResolveThreads = 256;
+constexpr int kResolveThreads = kResolveTile;
 constexpr int kSegThreads = 256;
 constexpr int kSegTile = kSegThreads * 4;
 constexpr int kSegBlocks = 148 * 4;
 
-__device__ __forceinline__ int slot_of(long long x, long long y, long long z) {
-    return (int)(((x & 7) << 6) | ((y & 7) << 3) | (z & 7));
-}
-
-// counter += 1 for every converged lane, one atomic per warp; returns this
-// lane's ticket.
-__device__ __forceinline__ unsigned long long warp_ticket(unsigned long long* counter) {
-    const unsigned mask = __activemask();
-    const int lane = threadIdx.x & 31;
-    const int leader = __ffs(mask) - 1;
-    const unsigned rank = __popc(mask & ((1u << lane) - 1u));
-    unsigned long long base = 0;
-    if (lane == leader) base = atomicAdd(counter, (unsigned long long)__popc(mask));
-    base = __shfl_sync(mask, base, leader);
-    return base + rank;
-}
-
-// 16-byte volatile store / load of a hash slot (one transaction each).
-__device__ __forceinline__ void st_slot(int4* p, int4 v) {
-    asm volatile("st.volatile.global.v4.s32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y),
-                 "r"(v.z), "r"(v.w)
-                 : "memory");
-}
-
-__device__ __forceinline__ int4 ld_slot(const int4* p) {
-    int4 v;
-    asm volatile("ld.volatile.global.v4.s32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                 : "l"(p)
-                 : "memory");
-    return v;
-}
-
-// Leaf find-or-insert.  A claimed slot stays BUSY until the new leaf's id,
-// coordinates and creation frame are written; then the id is published.
-// Returns -1 (and sets err_cap) when the leaf pool is full.
-__device__ int leaf_find_or_insert(int4* table, long long mask, int a, int b, int c, int frame,
-                                   long long bcap, int4* bcoord, FrameCtr* ctr) {
-    long long pos = (long long)(block_hash(a, b, c) & (unsigned long long)mask);
-    while (true) {
-        // Fast path: one 16-byte L2 read.  Key and id are published together
-        // by one 16-byte store, so a matching key is final -- almost every
-        // lookup ends here.
-        const int4 sv = __ldcg(table + pos);
-        if (sv.w >= 0) {
-            if (sv.x == a && sv.y == b && sv.z == c) return sv.w;
-            pos = (pos + 1) & mask;
-            continue;
-        }
-        volatile int* vw = &table[pos].w;
-        int v = sv.w;
-        if (v == kHashEmpty) {
-            int old = atomicCAS((int*)&table[pos].w, kHashEmpty, kHashBusy);
-            if (old == kHashEmpty) {
-                const long long id = (long long)warp_ticket(&ctr->nblocks);
-                if (id >= bcap) {
-                    atomicExch((int*)&table[pos].w, kHashEmpty);
-                    atomicOr(&ctr->err_cap, 1);
-                    return -1;
-                }
-                bcoord[id] = make_int4(a, b, c, frame);
-                // publish key and id with one 16-byte store: a reader sees the
-                // slot either BUSY or complete (no fence on the creating side)
-                st_slot(table + pos, make_int4(a, b, c, (int)id));
-                return (int)id;
-            }
-            v = old;
-        }
-        while (v == kHashBusy) {
-            __nanosleep(20);
-            v = *vw;
-        }
-        if (v == kHashEmpty) {   // a creator rolled back (pool full)
-            atomicOr(&ctr->err_cap, 1);
-            return -1;
-        }
-        const int4 full = ld_slot(table + pos);
-        if (full.x == a && full.y == b && full.z == c) return full.w;
-        pos = (pos + 1) & mask;
-    }
-}
-
-// K2: rows -> voxel ids, in CTA-synchronous tiles of 256 rows so that every
-// allocation counter (leaves, voxels, touched list) is bumped once per tile
-// after a block scan -- never per thread.  Within a warp, lanes that hit the
-// same voxel elect one leader (one lookup, one count of popc(peers)), and
-// voxel leaders that share a leaf elect one leaf lookup.  A slot claimed by
-// another CTA (BUSY) is waited for after this tile's own claims are
-// published, so no thread ever waits across a barrier.
+// K2: rows -> voxel ids over CTA-synchronous tiles of 256 rows
+// (svx_resolve_tile.cuh).
 __global__ void __launch_bounds__(kResolveThreads) k_resolve(
     const unsigned long long* __restrict__ rowkey, const int* __restrict__ rowray,
-    const double* __restrict__ rowd, const int* __restrict__ rowlab,
-    int* __restrict__ rowvid, RowSlot* __restrict__ vslot, int4* table, int4* bcoord,
-    unsigned long long* bkey, unsigned long long* bmask, int* bslot, VoxFrame* rec,
-    int* __restrict__ tlist, FrameCtr* ctr) {
+    const double* __restrict__ rowd, const int* __restrict__ rowlab, rt::ResolveArgs ra) {
     grid_dep_wait();
     using Scan = cub::BlockScan<int, kResolveThreads>;
     __shared__ typename Scan::TempStorage scan_tmp;
     __shared__ unsigned long long s_base;
-    if (ctr->abort) return;
+    __shared__ unsigned s_tcount;
+    FrameCtr* ctr = ra.ctr;
+    if (threadIdx.x == 0) s_tcount = 0u;
+    if (ctr->abort) {
+        if (threadIdx.x == 0) ra.rcount[blockIdx.x] = 0u;
+        return;
+    }
     const FrameParams& fp = ctr->p;
     const long long total = (long long)ctr->rows;
-    const KeyPack kp = fp.kp;
-    const long long hmask = fp.hmask, bcap = fp.bcap, vcap = fp.vcap, nblocks0 = fp.nblocks0;
-    const int frame = fp.frame;
-    const bool slots = fp.slots != 0;
-    const int lane = threadIdx.x & 31;
-    const unsigned full = 0xffffffffu;
+    ra.kp = fp.kp;
+    ra.hmask = fp.hmask;
+    ra.bcap = fp.bcap;
+    ra.vcap = fp.vcap;
+    ra.nblocks0 = fp.nblocks0;
+    ra.frame = fp.frame;
+    ra.slots = fp.slots != 0;
+    ra.region = fp.region;
+    __syncthreads();
     for (long long tile = blockIdx.x; tile * kResolveThreads < total; tile += gridDim.x) {
         const long long t = tile * kResolveThreads + threadIdx.x;
         const bool valid = t < total;
         const unsigned long long key = valid ? rowkey[t] : kKeyEmpty;
         RowSlot rsl{0, 0, 0.0};
-        if (valid && slots) {
+        if (valid && ra.slots) {
             rsl.point = rowray[t];
             rsl.label = rowlab[t];
             rsl.d = rowd[t];
         }
-        long long x = 0, y = 0, z = 0;
-        if (valid) unpack_key(key, kp, x, y, z);
-        const unsigned vpeers = __match_any_sync(full, valid ? key : (kKeyEmpty ^ (unsigned long long)lane));
-        const int vleader = __ffs(vpeers) - 1;
-        const bool is_vl = valid && lane == vleader;
-        // exact leaf identity: leaf coords relative to the base's leaf, 19 bits each
-        const int la = (int)(x >> kLeafLog2), lb = (int)(y >> kLeafLog2), lc = (int)(z >> kLeafLog2);
-        const unsigned long long lkey =
-            is_vl ? (((unsigned long long)(la - (kp.base[0] >> kLeafLog2)) << 38) |
-                     ((unsigned long long)(lb - (kp.base[1] >> kLeafLog2)) << 19) |
-                     (unsigned long long)(lc - (kp.base[2] >> kLeafLog2)))
-                  : (~0ULL ^ (unsigned long long)lane);
-        const unsigned lpeers = __match_any_sync(full, lkey);
-        const int lleader = __ffs(lpeers) - 1;
-        const bool is_ll = is_vl && lane == lleader;
-
-        // ---- leaves: find, or claim an empty slot; ids for the tile's claims
-        int id = -1, lstate = 0;   // 1 = claimed here, 2 = another CTA's claim
-        long long lpos = 0;
-        if (is_ll) {
-            lpos = (long long)(block_hash(la, lb, lc) & (unsigned long long)hmask);
-            while (true) {
-                const int4 sv = __ldcg(table + lpos);
-                if (sv.w >= 0) {
-                    if (sv.x == la && sv.y == lb && sv.z == lc) { id = sv.w; break; }
-                    lpos = (lpos + 1) & hmask;
-                    continue;
-                }
-                if (sv.w == kHashBusy) { lstate = 2; break; }
-                const int old = atomicCAS(&table[lpos].w, kHashEmpty, kHashBusy);
-                if (old == kHashEmpty) { lstate = 1; break; }
-                // lost the race for this slot: look at it again
-            }
-        }
-        int rank, cnt;
-        Scan(scan_tmp).ExclusiveSum(lstate == 1 ? 1 : 0, rank, cnt);
-        if (threadIdx.x == 0 && cnt) s_base = atomicAdd(&ctr->nblocks, (unsigned long long)cnt);
+        rt::resolve_step<kResolveThreads>(ra, valid, key, rsl, t, scan_tmp, s_base, s_tcount);
         __syncthreads();
-        if (lstate == 1) {
-            const long long nid = (long long)s_base + rank;
-            if (nid >= bcap) {
-                atomicExch(&table[lpos].w, kHashEmpty);
-                atomicOr(&ctr->err_cap, 1);
-            } else {
-                bcoord[nid] = make_int4(la, lb, lc, frame);
-                st_slot(table + lpos, make_int4(la, lb, lc, (int)nid));   // key + id in one store
-                id = (int)nid;
-            }
-        }
-        __syncthreads();
-        if (lstate == 2) {   // another CTA is publishing this slot (maybe another key)
-            volatile int* vw = &table[lpos].w;
-            int v = *vw;
-            while (v == kHashBusy) {
-                __nanosleep(32);
-                v = *vw;
-            }
-            const int4 sv = ld_slot(table + lpos);
-            if (v >= 0 && sv.x == la && sv.y == lb && sv.z == lc) id = v;
-            else id = leaf_find_or_insert(table, hmask, la, lb, lc, frame, bcap, bcoord, ctr);
-        }
-        id = __shfl_sync(full, id, lleader);
-
-        // ---- voxels: find, or claim an inactive slot; ids for the tile's claims
-        int vid = -1, vstate = 0;
-        int* sp = nullptr;
-        const int slot = slot_of(x, y, z);   // GridCore.activate_slot, _core.pyx:312-322
-        if (is_vl && id >= 0) {
-            if (id >= nblocks0) atomicMin(&bkey[id], key);
-            sp = &bslot[(long long)id * kLeafVolume + slot];
-            int v = __ldcg(sp);
-            if (v == -1) {
-                v = atomicCAS(sp, -1, -2);
-                if (v == -1) vstate = 1;
-            }
-            if (vstate == 0) {
-                if (v >= 0) vid = v;
-                else vstate = 2;   // another CTA claimed it
-            }
-        }
-        Scan(scan_tmp).ExclusiveSum(vstate == 1 ? 1 : 0, rank, cnt);
-        if (threadIdx.x == 0 && cnt) s_base = atomicAdd(&ctr->nvox, (unsigned long long)cnt);
-        __syncthreads();
-        bool created = false;
-        if (vstate == 1) {
-            const long long nv = (long long)s_base + rank;
-            if (nv >= vcap) {
-                atomicExch(sp, -1);
-                atomicOr(&ctr->err_cap, 1);
-            } else {
-                atomicOr(&bmask[(long long)id * kMaskWords + (slot >> 6)], 1ULL << (slot & 63));
-                atomicExch(sp, (int)nv);
-                vid = (int)nv;
-                created = true;
-            }
-        }
-        __syncthreads();
-        if (vstate == 2) {
-            volatile int* vsp = sp;
-            int v = *vsp;
-            while (v == -2) {
-                __nanosleep(32);
-                v = *vsp;
-            }
-            if (v >= 0) vid = v;
-            else atomicOr(&ctr->err_cap, 1);
-        }
-
-        // ---- counts; the voxel's first toucher this frame lists it
-        bool first = false;
-        unsigned cbase = 0;
-        if (is_vl && vid >= 0) {
-            const unsigned c = atomicAdd(&rec[vid].cnt, (unsigned)__popc(vpeers) + (created ? kNewBit : 0u));
-            cbase = c & ~kNewBit;
-            first = cbase == 0u;
-        }
-        Scan(scan_tmp).ExclusiveSum(first ? 1 : 0, rank, cnt);
-        if (threadIdx.x == 0 && cnt) s_base = atomicAdd(&ctr->n_touched, (unsigned long long)cnt);
-        __syncthreads();
-        if (first) {
-            rec[vid].key = key;
-            tlist[s_base + rank] = vid;
-        }
-        vid = __shfl_sync(full, vid, vleader);
-        if (slots) {
-            // this row's rank among the voxel's rows = its slot (order is
-            // restored by point index in k_update_slots)
-            cbase = __shfl_sync(full, cbase, vleader) + __popc(vpeers & ((1u << lane) - 1u));
-            if (valid && vid >= 0) {
-                if (cbase < (unsigned)kSlots) vslot[(long long)vid * kSlots + cbase] = rsl;
-                else ctr->err_slots = 1;
-            }
-        } else if (valid) {
-            rowvid[t] = vid;
-        }
-        __syncthreads();
+    }
+    if (ra.slots && threadIdx.x == 0) {   // this CTA's touched region
+        ra.rcount[blockIdx.x] = s_tcount;
+        if (s_tcount) atomicAdd(&ctr->n_touched, (unsigned long long)s_tcount);
     }
 }
 
@@ -421,8 +211,38 @@ __global__ void k_cleanup(const int* __restrict__ tlist, VoxFrame* rec, TD* vt,
     }
 }
 
+// Slot mode: reset every listed voxel's bslot word (frame count 0; a failed
+// claim back to inactive) and give voxels created by the attempt their
+// background TSDF state (slot mode is closed/geometry: counts are untouched).
+template <class TD>
+__global__ void k_cleanup_slots(const TouchEntry* __restrict__ tent, const unsigned* __restrict__ rcount,
+                                long long region, unsigned long long* bslot, TD* vt, double trunc) {
+    const unsigned cnt = rcount[blockIdx.x];
+    const TouchEntry* te = tent + (long long)blockIdx.x * region;
+    for (unsigned e = threadIdx.x; e < cnt; e += blockDim.x) {
+        const TouchEntry en = te[e];
+        if (en.vid == 0xFFFFFFFFu) {
+            bslot[en.bidx] = kSlotInactive;
+            continue;
+        }
+        const unsigned vid = en.vid & ~kNewBit;
+        bslot[en.bidx] = (unsigned long long)vid;
+        if (en.vid & kNewBit) {
+            vt[2 * (long long)vid] = (TD)trunc;
+            vt[2 * (long long)vid + 1] = (TD)0;
+        }
+    }
+}
+
 template <class TD, class TS>
 svx_status cleanup_t(svx_map* m, cudaStream_t s) {
+    if (m->frame_slots) {
+        k_cleanup_slots<TD><<<kPersistentBlocks, 256, 0, s>>>(
+            ptr<TouchEntry>(m->tlist), ptr<unsigned>(m->rcount), slot_region(m->rcap),
+            ptr<unsigned long long>(m->bslot), ptr<TD>(m->vt), m->cfg.truncation);
+        SVX_LAUNCHED();
+        return SVX_OK;
+    }
     const bool open = m->cfg.sem_kind == SVX_SEM_OPEN;
     k_cleanup<TD, TS><<<kPersistentBlocks, 256, 0, s>>>(
         ptr<int>(m->tlist), ptr<VoxFrame>(m->vrec), ptr<TD>(m->vt),
@@ -434,14 +254,27 @@ svx_status cleanup_t(svx_map* m, cudaStream_t s) {
 
 }  // namespace
 
+rt::ResolveArgs resolve_args(svx_map* m) {
+    rt::ResolveArgs ra{};
+    ra.table = ptr<int4>(m->hash);
+    ra.bcoord = ptr<int4>(m->bcoord);
+    ra.bkey = ptr<unsigned long long>(m->bkey);
+    ra.bmask = ptr<unsigned long long>(m->bmask);
+    ra.bslot = ptr<unsigned long long>(m->bslot);
+    ra.rec = ptr<VoxFrame>(m->vrec);
+    ra.tlist = ptr<int>(m->tlist);
+    ra.tent = ptr<TouchEntry>(m->tlist);   // slot mode reuses the touched-list buffer
+    ra.rcount = ptr<unsigned>(m->rcount);
+    ra.vslot = ptr<RowSlot>(m->vslot);
+    ra.rowvid = ptr<int>(m->rowvid);
+    ra.ctr = ptr<FrameCtr>(m->ctr);
+    return ra;
+}
+
 svx_status launch_resolve(svx_map* m, cudaStream_t s) {
-    SVX_CUDA(launch_pdl(k_resolve, kPersistentBlocks, kResolveThreads, 0, s, 
-        ptr<unsigned long long>(m->rowkey), ptr<int>(m->rowray), ptr<double>(m->rowd), ptr<int>(m->rowlab),
-        ptr<int>(m->rowvid), ptr<RowSlot>(m->vslot),
-        ptr<int4>(m->hash), ptr<int4>(m->bcoord),
-        ptr<unsigned long long>(m->bkey), ptr<unsigned long long>(m->bmask), ptr<int>(m->bslot),
-        ptr<VoxFrame>(m->vrec), ptr<int>(m->tlist),
-        ptr<FrameCtr>(m->ctr)));
+    SVX_CUDA(launch_pdl(k_resolve, kPersistentBlocks, kResolveThreads, 0, s,
+        ptr<unsigned long long>(m->rowkey), ptr<int>(m->rowray), ptr<double>(m->rowd),
+        ptr<int>(m->rowlab), resolve_args(m)));
     SVX_LAUNCHED();
     return SVX_OK;
 }

@@ -18,6 +18,8 @@
 // Open-set voxels always take the warp shapes (lanes own feature dims).
 #include <math.h>
 
+#include <algorithm>
+
 #include "svx_internal.cuh"
 
 namespace svx {
@@ -272,23 +274,29 @@ __device__ __forceinline__ RowSlot ld_slot16(const RowSlot* p) {
 }
 
 template <class TD, class TC>
-__global__ void __launch_bounds__(256) k_update_slots(UpdateArgs a, const int* __restrict__ tlist,
+__global__ void __launch_bounds__(256) k_update_slots(UpdateArgs a, const TouchEntry* __restrict__ tent,
+                                                      const unsigned* __restrict__ rcount,
+                                                      unsigned long long* __restrict__ bslot,
                                                       const RowSlot* __restrict__ vslot, TD* vt,
                                                       TC* counts) {
     grid_dep_wait();
     FrameCtr* ctr = a.ctr;
     if (ctr->abort | ctr->err_cap | ctr->err_slots) return;
-    const long long U = (long long)ctr->n_touched;
     const bool closed = a.sem_kind == SVX_SEM_CLOSED;
+    const long long region = ctr->p.region;
     using P2 = typename Pair<TD>::type;
-    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < U;
-         e += (long long)gridDim.x * blockDim.x) {
-        const int vid = tlist[e];
-        const unsigned c = a.rec[vid].cnt;
+    // K2 CTA b listed its touched voxels in region b; this grid has the same size
+    const unsigned cnt = rcount[blockIdx.x];
+    const TouchEntry* te = tent + (long long)blockIdx.x * region;
+    for (unsigned e = threadIdx.x; e < cnt; e += blockDim.x) {
+        const TouchEntry en = te[e];
+        const int vid = (int)(en.vid & ~kNewBit);
+        const unsigned c = (unsigned)(bslot[en.bidx] >> 32) | (en.vid & kNewBit);
         P2 st = reinterpret_cast<const P2*>(vt)[vid];
         const RowSlot* sl = vslot + (long long)vid * kSlots;
-        RowSlot s0 = ld_slot16(sl), s1 = ld_slot16(sl + 1);   // rows 0-1: one sector
+        RowSlot s0 = ld_slot16(sl), s1;
         const unsigned k = c & ~kNewBit;
+        if (k > 1u) s1 = ld_slot16(sl + 1);   // only rows that exist (no partial-sector reads)
         TC* crow = counts + (long long)vid * a.C;
         RowAcc acc;
         if (k <= 2u) {
@@ -302,8 +310,9 @@ __global__ void __launch_bounds__(256) k_update_slots(UpdateArgs a, const int* _
         } else {
             // 3..16 rows: insertion sort by point index in a local array
             RowSlot q[kSlots];
-            q[0] = s0;
-            q[1] = s1;
+            const bool sw01 = s1.point < s0.point;
+            q[0] = sw01 ? s1 : s0;
+            q[1] = sw01 ? s0 : s1;
 #pragma unroll 1
             for (unsigned j = 2; j < k; ++j) {
                 const RowSlot v = ld_slot16(sl + j);
@@ -313,15 +322,6 @@ __global__ void __launch_bounds__(256) k_update_slots(UpdateArgs a, const int* _
                     --i;
                 }
                 q[i] = v;
-            }
-            if (q[1].point < q[0].point) {   // rows 0-1 arrived unsorted
-                const RowSlot t = q[0];
-                int i = 0;
-                while (i + 1 < (int)k && q[i + 1].point < t.point) {
-                    q[i] = q[i + 1];
-                    ++i;
-                }
-                q[i] = t;
             }
 #pragma unroll 1
             for (unsigned j = 0; j < k; ++j) fold_row<TC>(a, q[j].d, q[j].label, crow, closed, acc);
@@ -342,7 +342,7 @@ __global__ void __launch_bounds__(256) k_update_slots(UpdateArgs a, const int* _
         reinterpret_cast<P2*>(vt)[vid] = out;
         if (closed && a.last_wins)
             for (int t = 0; t < a.C; ++t) crow[t] = (TC)(t == acc.last - 1 ? 1 : 0);
-        a.rec[vid].cnt = 0u;
+        bslot[en.bidx] = (unsigned long long)(unsigned)vid;   // frame count back to 0
     }
 }
 
@@ -708,6 +708,12 @@ __global__ void k_rehash(int64_t nblocks, const int4* __restrict__ bcoord, int4*
     }
 }
 
+__global__ void k_fill_u64(unsigned long long* p, long long n, unsigned long long v) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        p[i] = v;
+}
+
 UpdateArgs make_args(svx_map* m) {
     UpdateArgs a;
     a.mlist = ptr<int>(m->mlist);
@@ -777,8 +783,10 @@ svx_status open_b(svx_map* m, cudaStream_t s) {
 
 template <class TD, class TC>
 svx_status slots_t(svx_map* m, cudaStream_t s) {
-    SVX_CUDA(launch_pdl(k_update_slots<TD, TC>, kShortBlocks, 256, 0, s, make_args(m),
-                        ptr<int>(m->tlist), ptr<RowSlot>(m->vslot), ptr<TD>(m->vt), ptr<TC>(m->s0)));
+    SVX_CUDA(launch_pdl(k_update_slots<TD, TC>, kPersistentBlocks, 256, 0, s, make_args(m),
+                        ptr<TouchEntry>(m->tlist), ptr<unsigned>(m->rcount),
+                        ptr<unsigned long long>(m->bslot), ptr<RowSlot>(m->vslot), ptr<TD>(m->vt),
+                        ptr<TC>(m->s0)));
     SVX_LAUNCHED();
     return SVX_OK;
 }
@@ -827,6 +835,13 @@ svx_status launch_rehash(svx_map* m, int4* new_table, int64_t new_cap, cudaStrea
     if (m->nblocks == 0) return SVX_OK;
     k_rehash<<<grid_for(m->nblocks, T), T, 0, s>>>(m->nblocks, ptr<int4>(m->bcoord), new_table,
                                                    new_cap - 1);
+    SVX_LAUNCHED();
+    return SVX_OK;
+}
+
+svx_status launch_fill_u64(unsigned long long* p, int64_t n, unsigned long long v, cudaStream_t s) {
+    if (n <= 0) return SVX_OK;
+    k_fill_u64<<<(int)std::min<int64_t>((n + 255) / 256, kPersistentBlocks), 256, 0, s>>>(p, n, v);
     SVX_LAUNCHED();
     return SVX_OK;
 }
