@@ -226,8 +226,9 @@ struct svx_map {
     int64_t npts_cap = 0;  // points the per-ray scratch holds
     // captured frame graph (replayed while the layout is unchanged)
     cudaStream_t gstream = nullptr;
-    cudaGraphExec_t gexec[2] = {nullptr, nullptr};   // per mode: segment, slot
-    unsigned long long gsig[2] = {0, 0};
+    cudaGraphExec_t gexec[4] = {};   // segment, slot; +2: with stage events (profiling)
+    unsigned long long gsig[4] = {};
+    unsigned gstmask[4] = {};
     svx::DevBuf cubtmp;
     svx::DevBuf ctr;      // FrameCtr
     svx::FrameCtr* h_ctr = nullptr;  // pinned mirror
