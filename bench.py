@@ -158,7 +158,7 @@ def stage_bytes(stage, rep, kind, C, D, tsdf_elem):
     S = 2 * tsdf_elem + (4 * C if kind == "closed" else (8 * D if kind == "open" else 0))
     return {
         # read points (+labels/features), write the ray table and one 8-byte key per row
-        "march": n * (12 + P) + used * 32 + R * 8,
+        "walk": n * (12 + P) + used * 32 + R * 8,
         # per row: key in, voxel id out, one count; per voxel: leaf lookup, slot, key
         "resolve": R * (8 + 4 + 4) + U * (16 + 4 + 8 + 4),
         # per row: voxel id + count in; single-row voxels also ray + label + state
@@ -166,6 +166,7 @@ def stage_bytes(stage, rep, kind, C, D, tsdf_elem):
         # multi-row voxels: rows, rays, labels and state (upper bound: all voxels)
         "update": 2 * U * S + R * (4 + 32 + (4 if kind == "closed" else 0)),
         "update_b": 0,
+        "seg": U * 8,
     }[stage]
 
 
@@ -326,7 +327,7 @@ def run_ours(args):
     # ---- roofline of the dominant stage -------------------------------------------
     stages = list(_lib.STAGES)
     mean_stage = {s: statistics.mean(h[s] for h in stage_hist) for s in stages}
-    dom = max(stages, key=lambda s: mean_stage[s])
+    dom = max(_lib.KERNEL_STAGES, key=lambda s: mean_stage[s])
     dom_bytes = statistics.mean(stage_bytes(dom, r, kind, C, D, tsdf_elem) for r in prof_reps)
     peak, peak_src = measured_peak()
     achieved = dom_bytes / (mean_stage[dom] / 1e3) / 1e9 if mean_stage[dom] > 0 else 0.0

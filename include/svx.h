@@ -253,17 +253,19 @@ svx_status svx_label_map(svx_map* map, int32_t mode, int64_t capacity, int32_t* 
                          void* stream);
 
 /* ---- diagnostics --------------------------------------------------------- */
-/* Per-stage device timing of integrate calls (CUDA events on the caller's
- * stream around each stage).  Stages, in order:
- *   0 march (K1: masks + fp64 band walk -> row keys; gate)
- *   1 resolve (K2: rows -> leaf/voxel ids, per-voxel counts; K3 row segments)
- *   2 scatter (K4: rows into segments; single-row voxels updated in ray order)
- *   3 update (K5: TSDF + semantic update of short segments / open-set voxels)
- *   4 update_b (K5 for long and huge segments)
- * With profiling off, a frame is replayed as one captured CUDA graph.
- * svx_stage_times writes up to n last-frame stage times in ms and returns the
- * number of stages (SVX_N_STAGES). */
-#define SVX_N_STAGES 5
+/* Per-kernel device timing of integrate calls.  With profiling on, each kernel
+ * of the frame graph records its span [first CTA start, last warp end] with
+ * %globaltimer (the graph, caches and programmatic overlap are unchanged).
+ * Entries, in order (ms; 0 when the kernel did not run):
+ *   0 walk     (K1: masks + fp64 band walk -> row keys; gate)
+ *   1 resolve  (K2: rows -> leaf/voxel ids, per-voxel counts)
+ *   2 seg      (K3: row segments; segment mode)
+ *   3 scatter  (K4: rows into segments; segment mode)
+ *   4 update   (K5: slot update, short segments, or open-set voxels)
+ *   5 update_b (K5: long and huge segments)
+ *   6 frame    (first kernel start to last kernel end)
+ * svx_stage_times writes up to n last-frame values and returns SVX_N_STAGES. */
+#define SVX_N_STAGES 7
 svx_status svx_set_profiling(svx_map* map, int32_t enable);
 
 /* Row-grouping strategy of closed-set / geometry maps with bounded bands.

@@ -127,7 +127,8 @@ _SIGNATURES = {
 
 DEVICE_INPUTS = 0x100   # svx.h SVX_DEVICE_INPUTS
 
-STAGES = ("march", "resolve", "scatter", "update", "update_b")
+STAGES = ("walk", "resolve", "seg", "scatter", "update", "update_b", "frame")
+KERNEL_STAGES = STAGES[:-1]
 
 # every symbol include/svx.h declares (checked by tests/test_abi_and_config.py)
 EXPORTED = sorted(list(_SIGNATURES) + ["svx_last_error", "svx_abi_version",

@@ -191,8 +191,6 @@ svx_status svx_destroy(svx_map* m) {
     for (cudaGraphExec_t g : m->gexec)
         if (g) cudaGraphExecDestroy(g);
     if (m->gstream) cudaStreamDestroy(m->gstream);
-    for (cudaEvent_t e : m->st_ev)
-        if (e) cudaEventDestroy(e);
     delete m;
     return SVX_OK;
 }
@@ -242,12 +240,7 @@ svx_status svx_reserve(svx_map* m, int64_t voxels, int64_t blocks) {
 svx_status svx_set_profiling(svx_map* m, int32_t enable) {
     if (!m) return fail(SVX_E_INPUT, "null argument");
     SVX_TRY(set_device(m));
-    if (enable) {
-        for (cudaEvent_t& e : m->st_ev)
-            if (!e) SVX_CUDA(cudaEventCreate(&e));
-    }
     m->prof = enable != 0;
-    m->st_mask = 0;
     return SVX_OK;
 }
 

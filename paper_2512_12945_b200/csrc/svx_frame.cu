@@ -168,65 +168,47 @@ static unsigned long long graph_signature(const svx_map* m, int pts_f64, int fea
     return h;
 }
 
-#define STAGE_BEGIN(i) \
-    do { if (m->prof) { cudaEventRecord(m->st_ev[2 * (i)], s); m->st_mask |= 1u << (i); } } while (0)
-#define STAGE_END(i) \
-    do { if (m->prof) cudaEventRecord(m->st_ev[2 * (i) + 1], s); } while (0)
 
 // Enqueue one frame attempt on stream s (eager or under graph capture).
 static svx_status enqueue_frame(svx_map* m, int pts_f64, int feats_f64, cudaStream_t s) {
     FrameCtr* dc = ptr<FrameCtr>(m->ctr);
     SVX_CUDA(cudaMemcpyAsync(dc, m->h_ctr, sizeof(FrameCtr), cudaMemcpyHostToDevice, s));
-    STAGE_BEGIN(0);
     SVX_TRY(launch_march(m, pts_f64, feats_f64, s));
-    STAGE_END(0);
-    STAGE_BEGIN(1);
     SVX_TRY(launch_resolve(m, s));
     if (m->frame_slots) {
-        STAGE_END(1);
-        STAGE_BEGIN(3);
         SVX_TRY(launch_update_slots(m, s));
-        STAGE_END(3);
         SVX_CUDA(cudaMemcpyAsync(m->h_ctr, dc, sizeof(FrameCtr), cudaMemcpyDeviceToHost, s));
         return SVX_OK;
     }
     SVX_TRY(launch_segments(m, s));
-    STAGE_END(1);
-    STAGE_BEGIN(2);
     SVX_TRY(launch_scatter(m, s));
-    STAGE_END(2);
-    STAGE_BEGIN(3);
     SVX_TRY(launch_update_a(m, feats_f64, s));
-    STAGE_END(3);
-    STAGE_BEGIN(4);
     SVX_TRY(launch_update_b(m, feats_f64, s));
-    STAGE_END(4);
     SVX_CUDA(cudaMemcpyAsync(m->h_ctr, dc, sizeof(FrameCtr), cudaMemcpyDeviceToHost, s));
     return SVX_OK;
 }
 
+// Profiling: per-kernel spans recorded by the kernels themselves (KSpan),
+// plus the frame span from the first kernel start to the last kernel end.
 static void collect_stage_times(svx_map* m) {
-    for (int i = 0; i < SVX_N_STAGES; ++i) {
-        m->stage_ms[i] = 0.0;
-        if (!(m->st_mask & (1u << i))) continue;
-        float ms = 0.f;
-        if (cudaEventElapsedTime(&ms, m->st_ev[2 * i], m->st_ev[2 * i + 1]) == cudaSuccess)
-            m->stage_ms[i] = ms;
-        else
-            cudaGetLastError();
+    const FrameCtr* hc = m->h_ctr;
+    unsigned long long t0 = ~0ULL, t1 = 0;
+    for (int i = 0; i < kSpanKernels; ++i) {
+        const unsigned long long a = hc->kspan[i][0], b = hc->kspan[i][1];
+        m->stage_ms[i] = (a != ~0ULL && b > a) ? (double)(b - a) * 1e-6 : 0.0;
+        if (a != ~0ULL && b > a) {
+            t0 = a < t0 ? a : t0;
+            t1 = b > t1 ? b : t1;
+        }
     }
-    m->st_mask = 0;
+    m->stage_ms[kSpanKernels] = t1 > t0 ? (double)(t1 - t0) * 1e-6 : 0.0;
 }
 
 // Run one frame attempt: replay (or capture, on the map's own stream) the
 // frame graph on the caller's stream.
 static svx_status run_frame(svx_map* m, int pts_f64, int feats_f64, cudaStream_t s) {
-    // Profiling: the same graph with event-record nodes between the stages
-    // (times inside one graph launch, caches as in the real pipeline; only the
-    // programmatic overlap across a stage boundary is lost).
-    const unsigned long long sig = graph_signature(m, pts_f64, feats_f64) ^ (m->prof ? 0x9E37ULL : 0ULL);
-    const int gm = (m->frame_slots ? 1 : 0) + (m->prof ? 2 : 0);
-    if (m->prof) m->st_mask = 0;
+    const unsigned long long sig = graph_signature(m, pts_f64, feats_f64);
+    const int gm = m->frame_slots ? 1 : 0;
     cudaGraphExec_t& gexec = m->gexec[gm];
     if (!gexec || sig != m->gsig[gm]) {
         if (gexec) {
@@ -249,13 +231,11 @@ static svx_status run_frame(svx_map* m, int pts_f64, int feats_f64, cudaStream_t
             return fail(SVX_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
         }
         m->gsig[gm] = sig;
-        m->gstmask[gm] = m->st_mask;   // stages with event nodes in this graph
     }
-    m->st_mask = m->gstmask[gm];
     // the graph was captured on the map's own stream; it runs on the caller's
     if (g_trace_host) g_t_launch0 = now_us();
     SVX_CUDA(cudaGraphLaunch(gexec, s));
-    count_launch((gm & 1) ? 3 : 6);
+    count_launch(gm ? 3 : 6);
     SVX_CUDA(cudaEventRecord(m->ev1, s));
     if (g_trace_host) g_t_launch1 = now_us();
     SVX_CUDA(cudaEventSynchronize(m->ev1));
@@ -309,6 +289,11 @@ void reset_ctr(svx_map* m) {
     p.maxrows = m->maxrows;
     p.inline_singles = inline_singles(m);
     p.slots = m->frame_slots;
+    p.prof = m->prof ? 1 : 0;
+    for (int i = 0; i < kSpanKernels; ++i) {
+        hc->kspan[i][0] = ~0ULL;
+        hc->kspan[i][1] = 0ULL;
+    }
     p.region = slot_region(m->rcap);
     p.seq = ++m->seq;
 }

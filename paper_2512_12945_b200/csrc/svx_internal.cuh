@@ -77,8 +77,12 @@ struct FrameParams {
     int inline_singles;        // single-row voxels updated in the scatter (closed/geometry)
     int slots;                 // 1: slot mode (K2 fills vslot; K5 = k_update_slots)
     long long region;          // slot mode: touched entries per K2 CTA (svx::slot_region)
+    int prof;                  // record kernel spans (FrameCtr.kspan)
     unsigned seq;              // launch sequence number (epoch of the segment-scan status)
 };
+
+// Kernels with recorded spans in profiling mode (svx_stage_spans order).
+enum KSpanId { kSpanWalk = 0, kSpanResolve, kSpanSeg, kSpanScatter, kSpanUpdate, kSpanUpdateB, kSpanKernels };
 
 // Per-CTA partial counters of the march, reduced by the gate (no
 // same-address atomics on the hot path).
@@ -117,6 +121,9 @@ struct FrameCtr {
     int err_rows;                   // a band exceeded maxrows (retry with dense rows)
     int abort;                      // set by the gate: skip all mutation
     int err_slots;                  // slot mode: a voxel got more than kSlots rows (re-run in segment mode)
+    // profiling (FrameParams.prof): per kernel [first CTA start, last warp end]
+    // in %globaltimer ns; kernels overlap under programmatic dependent launch
+    unsigned long long kspan[kSpanKernels][2];
 };
 
 // Per-voxel frame record (indexed by voxel id; cnt and cur are zero between
@@ -226,9 +233,8 @@ struct svx_map {
     int64_t npts_cap = 0;  // points the per-ray scratch holds
     // captured frame graph (replayed while the layout is unchanged)
     cudaStream_t gstream = nullptr;
-    cudaGraphExec_t gexec[4] = {};   // segment, slot; +2: with stage events (profiling)
-    unsigned long long gsig[4] = {};
-    unsigned gstmask[4] = {};
+    cudaGraphExec_t gexec[2] = {};   // segment mode, slot mode
+    unsigned long long gsig[2] = {};
     svx::DevBuf cubtmp;
     svx::DevBuf ctr;      // FrameCtr
     svx::FrameCtr* h_ctr = nullptr;  // pinned mirror
@@ -239,10 +245,8 @@ struct svx_map {
     svx::DevBuf act_cnt, act_off, act_vid, act_coord, q_buf, out_buf;
     int64_t act_valid_frames = -1;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_in = nullptr;
-    // optional per-stage timing (svx_set_profiling)
+    // optional per-kernel timing (svx_set_profiling; FrameCtr.kspan)
     bool prof = false;
-    cudaEvent_t st_ev[2 * SVX_N_STAGES] = {};
-    unsigned st_mask = 0;
     double stage_ms[SVX_N_STAGES] = {};
     // sharded integration (svx_shard.cu): state between a frame's calls
     int shard_phase = 0;          // 0 idle, 1 marched, 2 planned, 3 packed
@@ -292,6 +296,26 @@ __device__ __forceinline__ void grid_dep_wait() {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
 }
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Profiling span of one kernel: construct after grid_dep_wait(); the CTA's
+// thread 0 records the start, every warp's lane 0 the end (destructor, so
+// early returns are covered).  No cost beyond one branch when profiling is off.
+struct KSpan {
+    unsigned long long* span;
+    __device__ __forceinline__ KSpan(FrameCtr* ctr, int k)
+        : span(ctr->p.prof ? ctr->kspan[k] : nullptr) {
+        if (span && threadIdx.x == 0) atomicMin(span, globaltimer());
+    }
+    __device__ __forceinline__ ~KSpan() {
+        if (span && (threadIdx.x & 31) == 0) atomicMax(span + 1, globaltimer());
+    }
+};
 
 template <class... KArgs, class... Args>
 inline cudaError_t launch_pdl(void (*kernel)(KArgs...), unsigned grid, unsigned block, size_t smem,

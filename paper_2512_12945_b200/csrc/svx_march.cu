@@ -265,6 +265,7 @@ __global__ void __launch_bounds__(kTileRays, 4) k_walk(MarchParams mp, int sem_k
                                                     MarchPartial* __restrict__ partials,
                                                     FrameCtr* __restrict__ ctr) {
     grid_dep_wait();
+    KSpan _ks(ctr, kSpanWalk);
     using Scan = cub::BlockScan<int, kTileRays>;
     __shared__ typename Scan::TempStorage scan_tmp;
     __shared__ unsigned long long s_base;
@@ -372,6 +373,7 @@ __global__ void __launch_bounds__(kMarchThreads) k_walk_count(MarchParams mp, in
                                                               MarchPartial* __restrict__ partials,
                                                               FrameCtr* __restrict__ ctr) {
     grid_dep_wait();
+    KSpan _ks(ctr, kSpanWalk);
     const FrameParams fp = ctr->p;
     const long long n = fp.n;
     const double ox = fp.pp.t[0], oy = fp.pp.t[1], oz = fp.pp.t[2];
@@ -418,6 +420,7 @@ __global__ void __launch_bounds__(kMarchThreads) k_walk_write(MarchParams mp,
                                                               int* __restrict__ rowray,
                                                               const FrameCtr* __restrict__ ctr) {
     grid_dep_wait();
+    KSpan _ks(const_cast<FrameCtr*>(ctr), kSpanWalk);
     if (ctr->abort) return;
     const FrameParams fp = ctr->p;
     const long long n = fp.n;

@@ -44,6 +44,7 @@ __global__ void __launch_bounds__(kResolveThreads) k_resolve(
     __shared__ unsigned long long s_base;
     __shared__ unsigned s_tcount;
     FrameCtr* ctr = ra.ctr;
+    KSpan _ks(ctr, kSpanResolve);
     if (threadIdx.x == 0) s_tcount = 0u;
     if (ctr->abort) {
         if (threadIdx.x == 0) ra.rcount[blockIdx.x] = 0u;
@@ -105,6 +106,7 @@ __global__ void __launch_bounds__(kSegThreads) k_seg(const int* __restrict__ tli
                                                      int* __restrict__ mlist,
                                                      SegStatus* __restrict__ status, FrameCtr* ctr) {
     grid_dep_wait();
+    KSpan _ks(ctr, kSpanSeg);
     using Scan = cub::BlockScan<unsigned long long, kSegThreads>;
     __shared__ typename Scan::TempStorage scan_tmp;
     __shared__ unsigned long long s_prefix;

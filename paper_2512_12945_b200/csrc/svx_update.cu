@@ -135,6 +135,7 @@ __global__ void __launch_bounds__(256) k_scatter(UpdateArgs a, const int* __rest
                                                  int* __restrict__ srid, TD* vt, TC* counts) {
     grid_dep_wait();
     FrameCtr* ctr = a.ctr;
+    KSpan _ks(ctr, kSpanScatter);
     if (ctr->abort | ctr->err_cap) return;
     const FrameParams& fp = ctr->p;
     RowSpace rs;
@@ -183,6 +184,7 @@ template <class TD, class TC>
 __global__ void __launch_bounds__(256) k_update_short(UpdateArgs a, TD* vt, TC* counts) {
     grid_dep_wait();
     FrameCtr* ctr = a.ctr;
+    KSpan _ks(ctr, kSpanUpdate);
     if (ctr->abort | ctr->err_cap) return;
     const long long L = (long long)ctr->n_list;
     const KeyPack kp = ctr->p.kp;
@@ -281,6 +283,7 @@ __global__ void __launch_bounds__(256) k_update_slots(UpdateArgs a, const TouchE
                                                       TC* counts) {
     grid_dep_wait();
     FrameCtr* ctr = a.ctr;
+    KSpan _ks(ctr, kSpanUpdate);
     if (ctr->abort | ctr->err_cap | ctr->err_slots) return;
     const bool closed = a.sem_kind == SVX_SEM_CLOSED;
     const long long region = ctr->p.region;
@@ -494,6 +497,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) k_update_long(UpdateArgs a,
     grid_dep_wait();
     __shared__ int sbuf[kWarpsPerCta][kSmemMax];
     FrameCtr* ctr = a.ctr;
+    KSpan _ks(ctr, kSpanUpdateB);
     if (ctr->abort | ctr->err_cap) return;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     int* buf = sbuf[wib];
@@ -653,6 +657,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) k_update_open(UpdateArgs a,
     grid_dep_wait();
     __shared__ int sbuf[kWarpsPerCta][kSmemMax];
     FrameCtr* ctr = a.ctr;
+    KSpan _ks(ctr, kSpanUpdate);
     if (ctr->abort | ctr->err_cap) return;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const long long L = (long long)ctr->n_list;
@@ -677,6 +682,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) k_update_open_huge(UpdateAr
     grid_dep_wait();
     __shared__ int sbuf[kWarpsPerCta][kSmemMax];
     FrameCtr* ctr = a.ctr;
+    KSpan _ks(ctr, kSpanUpdateB);
     if (ctr->abort | ctr->err_cap) return;
     const int wib = threadIdx.x >> 5;
     const long long gw = (long long)blockIdx.x * kWarpsPerCta + wib;

@@ -75,6 +75,15 @@ def main():
                                      f.labels.data_ptr(), None, 0, None, ctypes.byref(rep)))
         raw.append((time.perf_counter() - t0) * 1e3)
     med = statistics.median
+    # kernel spans inside the frame graph (profiling mode)
+    m.set_profiling(True)
+    spans = []
+    for f in frames[5:]:
+        m.integrate(f.points, f.pose, labels=f.labels)
+        spans.append(m.stage_times())
+    m.set_profiling(False)
+    print("kernel spans (median us): " + ", ".join(
+        f"{k} {1e3 * med([sp[k] for sp in spans]):.1f}" for k in _lib.STAGES))
     print(f"config {args.config} mode {args.mode}: per frame (median ms) "
           f"integrate wall {med(wall):.4f}, device (kernel_ms) {med(dev):.4f}, "
           f"raw C call {med(raw):.4f}, python arg handling {med(py):.4f}; "
