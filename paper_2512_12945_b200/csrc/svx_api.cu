@@ -185,6 +185,8 @@ svx_status svx_destroy(svx_map* m) {
                       &m->act_off, &m->act_vid, &m->act_coord, &m->q_buf, &m->out_buf};
     for (DevBuf* b : bufs) release(*b);
     if (m->h_ctr) cudaFreeHost(m->h_ctr);
+    if (m->h_kspan) cudaFreeHost(m->h_kspan);
+    release(m->kspan);
     if (m->ev0) cudaEventDestroy(m->ev0);
     if (m->ev1) cudaEventDestroy(m->ev1);
     if (m->ev_in) cudaEventDestroy(m->ev_in);
@@ -240,6 +242,11 @@ svx_status svx_reserve(svx_map* m, int64_t voxels, int64_t blocks) {
 svx_status svx_set_profiling(svx_map* m, int32_t enable) {
     if (!m) return fail(SVX_E_INPUT, "null argument");
     SVX_TRY(set_device(m));
+    if (enable && !m->h_kspan) {
+        const size_t n = (size_t)kSpanKernels * 2 * kSpanMaxCtas * sizeof(unsigned long long);
+        SVX_TRY(ensure(m->kspan, n, 0));
+        SVX_CUDA(cudaMallocHost((void**)&m->h_kspan, n));
+    }
     m->prof = enable != 0;
     return SVX_OK;
 }

@@ -190,18 +190,25 @@ static svx_status enqueue_frame(svx_map* m, int pts_f64, int feats_f64, cudaStre
 
 // Profiling: per-kernel spans recorded by the kernels themselves (KSpan),
 // plus the frame span from the first kernel start to the last kernel end.
-static void collect_stage_times(svx_map* m) {
-    const FrameCtr* hc = m->h_ctr;
+static svx_status collect_stage_times(svx_map* m) {
+    const size_t n = (size_t)kSpanKernels * 2 * kSpanMaxCtas;
+    SVX_CUDA(cudaMemcpy(m->h_kspan, m->kspan.p, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
     unsigned long long t0 = ~0ULL, t1 = 0;
-    for (int i = 0; i < kSpanKernels; ++i) {
-        const unsigned long long a = hc->kspan[i][0], b = hc->kspan[i][1];
-        m->stage_ms[i] = (a != ~0ULL && b > a) ? (double)(b - a) * 1e-6 : 0.0;
+    for (int k = 0; k < kSpanKernels; ++k) {
+        unsigned long long a = ~0ULL, b = 0;
+        const unsigned long long* st = m->h_kspan + (size_t)k * 2 * kSpanMaxCtas;
+        for (int c = 0; c < kSpanMaxCtas; ++c) {
+            if (st[c] && st[c] < a) a = st[c];
+            if (st[kSpanMaxCtas + c] > b) b = st[kSpanMaxCtas + c];
+        }
+        m->stage_ms[k] = (a != ~0ULL && b > a) ? (double)(b - a) * 1e-6 : 0.0;
         if (a != ~0ULL && b > a) {
             t0 = a < t0 ? a : t0;
             t1 = b > t1 ? b : t1;
         }
     }
     m->stage_ms[kSpanKernels] = t1 > t0 ? (double)(t1 - t0) * 1e-6 : 0.0;
+    return SVX_OK;
 }
 
 // Run one frame attempt: replay (or capture, on the map's own stream) the
@@ -232,6 +239,10 @@ static svx_status run_frame(svx_map* m, int pts_f64, int feats_f64, cudaStream_t
         }
         m->gsig[gm] = sig;
     }
+    if (m->prof) {
+        const size_t n = (size_t)kSpanKernels * 2 * kSpanMaxCtas * sizeof(unsigned long long);
+        SVX_CUDA(cudaMemsetAsync(m->kspan.p, 0, n, s));
+    }
     // the graph was captured on the map's own stream; it runs on the caller's
     if (g_trace_host) g_t_launch0 = now_us();
     SVX_CUDA(cudaGraphLaunch(gexec, s));
@@ -240,7 +251,7 @@ static svx_status run_frame(svx_map* m, int pts_f64, int feats_f64, cudaStream_t
     if (g_trace_host) g_t_launch1 = now_us();
     SVX_CUDA(cudaEventSynchronize(m->ev1));
     if (g_trace_host) g_t_synced = now_us();
-    if (m->prof) collect_stage_times(m);
+    if (m->prof) SVX_TRY(collect_stage_times(m));
     return SVX_OK;
 }
 
@@ -289,11 +300,7 @@ void reset_ctr(svx_map* m) {
     p.maxrows = m->maxrows;
     p.inline_singles = inline_singles(m);
     p.slots = m->frame_slots;
-    p.prof = m->prof ? 1 : 0;
-    for (int i = 0; i < kSpanKernels; ++i) {
-        hc->kspan[i][0] = ~0ULL;
-        hc->kspan[i][1] = 0ULL;
-    }
+    p.kspan = m->prof ? ptr<unsigned long long>(m->kspan) : nullptr;
     p.region = slot_region(m->rcap);
     p.seq = ++m->seq;
 }

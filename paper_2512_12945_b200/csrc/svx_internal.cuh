@@ -77,12 +77,13 @@ struct FrameParams {
     int inline_singles;        // single-row voxels updated in the scatter (closed/geometry)
     int slots;                 // 1: slot mode (K2 fills vslot; K5 = k_update_slots)
     long long region;          // slot mode: touched entries per K2 CTA (svx::slot_region)
-    int prof;                  // record kernel spans (FrameCtr.kspan)
+    unsigned long long* kspan; // profiling: per-CTA start/end times (KSpan), else null
     unsigned seq;              // launch sequence number (epoch of the segment-scan status)
 };
 
-// Kernels with recorded spans in profiling mode (svx_stage_spans order).
+// Kernels with recorded spans in profiling mode (svx_stage_times order).
 enum KSpanId { kSpanWalk = 0, kSpanResolve, kSpanSeg, kSpanScatter, kSpanUpdate, kSpanUpdateB, kSpanKernels };
+constexpr int kSpanMaxCtas = 4096;   // per-CTA records per kernel and edge
 
 // Per-CTA partial counters of the march, reduced by the gate (no
 // same-address atomics on the hot path).
@@ -121,9 +122,6 @@ struct FrameCtr {
     int err_rows;                   // a band exceeded maxrows (retry with dense rows)
     int abort;                      // set by the gate: skip all mutation
     int err_slots;                  // slot mode: a voxel got more than kSlots rows (re-run in segment mode)
-    // profiling (FrameParams.prof): per kernel [first CTA start, last warp end]
-    // in %globaltimer ns; kernels overlap under programmatic dependent launch
-    unsigned long long kspan[kSpanKernels][2];
 };
 
 // Per-voxel frame record (indexed by voxel id; cnt and cur are zero between
@@ -248,6 +246,8 @@ struct svx_map {
     // optional per-kernel timing (svx_set_profiling; FrameCtr.kspan)
     bool prof = false;
     double stage_ms[SVX_N_STAGES] = {};
+    svx::DevBuf kspan;                       // kSpanKernels x 2 x kSpanMaxCtas u64
+    unsigned long long* h_kspan = nullptr;   // host copy
     // sharded integration (svx_shard.cu): state between a frame's calls
     int shard_phase = 0;          // 0 idle, 1 marched, 2 planned, 3 packed
     int shard_g = 1, shard_rank = 0;
@@ -303,17 +303,22 @@ __device__ __forceinline__ unsigned long long globaltimer() {
     return t;
 }
 
-// Profiling span of one kernel: construct after grid_dep_wait(); the CTA's
-// thread 0 records the start, every warp's lane 0 the end (destructor, so
-// early returns are covered).  No cost beyond one branch when profiling is off.
+// Profiling span of one kernel: construct after grid_dep_wait(); each CTA's
+// thread 0 stores its start and (destructor, so early returns are covered)
+// its end time into its own record -- plain stores, no contention; the host
+// reduces them to [first start, last end].  One branch when profiling is off.
 struct KSpan {
-    unsigned long long* span;
-    __device__ __forceinline__ KSpan(FrameCtr* ctr, int k)
-        : span(ctr->p.prof ? ctr->kspan[k] : nullptr) {
-        if (span && threadIdx.x == 0) atomicMin(span, globaltimer());
+    unsigned long long* rec;
+    __device__ __forceinline__ KSpan(FrameCtr* ctr, int k) : rec(ctr->p.kspan) {
+        if (rec && threadIdx.x == 0 && blockIdx.x < kSpanMaxCtas) {
+            rec += (size_t)k * 2 * kSpanMaxCtas + blockIdx.x;
+            rec[0] = globaltimer();
+        } else {
+            rec = nullptr;
+        }
     }
     __device__ __forceinline__ ~KSpan() {
-        if (span && (threadIdx.x & 31) == 0) atomicMax(span + 1, globaltimer());
+        if (rec) rec[kSpanMaxCtas] = globaltimer();
     }
 };
 
