@@ -107,6 +107,7 @@ struct UpdateArgs {
     const double4* ray;
     int* longlist;
     int* hugelist;
+    TouchEntry* hugelist2;   // slot mode: voxels of 5..16 rows
     unsigned* bitmap;     // kHugeWarps * bm_words
     long long bm_words;
     double h, trunc;
@@ -297,38 +298,36 @@ __global__ void __launch_bounds__(256) k_update_slots(UpdateArgs a, const TouchE
         const unsigned c = (unsigned)(bslot[en.bidx] >> 32) | (en.vid & kNewBit);
         P2 st = reinterpret_cast<const P2*>(vt)[vid];
         const RowSlot* sl = vslot + (long long)vid * kSlots;
-        RowSlot s0 = ld_slot16(sl), s1;
         const unsigned k = c & ~kNewBit;
-        if (k > 1u) s1 = ld_slot16(sl + 1);   // only rows that exist (no partial-sector reads)
+        if (k > 4u) {   // 5..16 rows (a few percent): one warp per voxel in k_update_slots_long
+            a.hugelist2[warp_ticket(&ctr->n_long)] = en;
+            continue;
+        }
+        // rows in registers; only slots that exist are read (no partial-sector reads)
+        RowSlot q0 = ld_slot16(sl), q1, q2, q3;
+        q1.point = q2.point = q3.point = 0x7fffffff;
+        if (k > 1u) q1 = ld_slot16(sl + 1);
+        if (k > 2u) q2 = ld_slot16(sl + 2);
+        if (k > 3u) q3 = ld_slot16(sl + 3);
         TC* crow = counts + (long long)vid * a.C;
         RowAcc acc;
-        if (k <= 2u) {
-            if (k == 2u && s1.point < s0.point) {
-                const RowSlot t = s0;
-                s0 = s1;
-                s1 = t;
+        // 4-element sorting network on the point index (5 compare-exchanges)
+        auto cx = [](RowSlot& x, RowSlot& y) {
+            if (y.point < x.point) {
+                const RowSlot t = x;
+                x = y;
+                y = t;
             }
-            fold_row<TC>(a, s0.d, s0.label, crow, closed, acc);
-            if (k == 2u) fold_row<TC>(a, s1.d, s1.label, crow, closed, acc);
-        } else {
-            // 3..16 rows: insertion sort by point index in a local array
-            RowSlot q[kSlots];
-            const bool sw01 = s1.point < s0.point;
-            q[0] = sw01 ? s1 : s0;
-            q[1] = sw01 ? s0 : s1;
-#pragma unroll 1
-            for (unsigned j = 2; j < k; ++j) {
-                const RowSlot v = ld_slot16(sl + j);
-                int i = (int)j;
-                while (i > 0 && q[i - 1].point > v.point) {
-                    q[i] = q[i - 1];
-                    --i;
-                }
-                q[i] = v;
-            }
-#pragma unroll 1
-            for (unsigned j = 0; j < k; ++j) fold_row<TC>(a, q[j].d, q[j].label, crow, closed, acc);
-        }
+        };
+        cx(q0, q1);
+        cx(q2, q3);
+        cx(q0, q2);
+        cx(q1, q3);
+        cx(q1, q2);
+        fold_row<TC>(a, q0.d, q0.label, crow, closed, acc);
+        if (k > 1u) fold_row<TC>(a, q1.d, q1.label, crow, closed, acc);
+        if (k > 2u) fold_row<TC>(a, q2.d, q2.label, crow, closed, acc);
+        if (k > 3u) fold_row<TC>(a, q3.d, q3.label, crow, closed, acc);
         // apply_tsdf (_pycore.py:399-417) on the pre-loaded pair
         if (c & kNewBit) {
             st.x = (TD)a.trunc;
@@ -346,6 +345,78 @@ __global__ void __launch_bounds__(256) k_update_slots(UpdateArgs a, const TouchE
         if (closed && a.last_wins)
             for (int t = 0; t < a.C; ++t) crow[t] = (TC)(t == acc.last - 1 ? 1 : 0);
         bslot[en.bidx] = (unsigned long long)(unsigned)vid;   // frame count back to 0
+    }
+}
+
+// Slot-mode voxels of 5..16 rows: one warp per voxel; lanes own rows, a
+// shuffle bitonic sort on (point, lane) orders them, the sums run in that
+// order through shuffles.
+template <class TD, class TC>
+__global__ void __launch_bounds__(256) k_update_slots_long(UpdateArgs a,
+                                                           unsigned long long* __restrict__ bslot,
+                                                           const RowSlot* __restrict__ vslot, TD* vt,
+                                                           TC* counts) {
+    grid_dep_wait();
+    FrameCtr* ctr = a.ctr;
+    KSpan _ks(ctr, kSpanUpdateB);
+    if (ctr->abort | ctr->err_cap | ctr->err_slots) return;
+    const bool closed = a.sem_kind == SVX_SEM_CLOSED;
+    const int lane = threadIdx.x & 31;
+    using P2 = typename Pair<TD>::type;
+    const long long L = (long long)ctr->n_long;
+    for (long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < L;
+         w += ((long long)gridDim.x * blockDim.x) >> 5) {
+        const TouchEntry en = a.hugelist2[w];
+        const int vid = (int)(en.vid & ~kNewBit);
+        const unsigned k = (unsigned)(bslot[en.bidx] >> 32);
+        RowSlot r{0x7fffffff, 0, 0.0};
+        if ((unsigned)lane < k) r = ld_slot16(vslot + (long long)vid * kSlots + lane);
+        unsigned long long key = ((unsigned long long)(unsigned)r.point << 32) | (unsigned)lane;
+#pragma unroll
+        for (int kk = 2; kk <= 32; kk <<= 1) {
+#pragma unroll
+            for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+                const unsigned long long o = __shfl_xor_sync(0xffffffffu, key, jj);
+                const bool up = (lane & kk) == 0;
+                const bool lower = (lane & jj) == 0;
+                key = (lower == up) ? (key < o ? key : o) : (key > o ? key : o);
+            }
+        }
+        const int src = (int)(key & 31u);   // lane holding the lane-th smallest row
+        const double d = __shfl_sync(0xffffffffu, r.d, src);
+        const int lab = __shfl_sync(0xffffffffu, r.label, src);
+        const double w_row = (a.wfn == 1) ? (d >= 0.0 ? 1.0 : (a.trunc + d) / a.trunc) : 1.0;
+        RowAcc acc;
+        for (unsigned q = 0; q < k; ++q) {
+            const double wq = __shfl_sync(0xffffffffu, w_row, q);
+            const double dq = __shfl_sync(0xffffffffu, d, q);
+            acc.sw += wq;
+            acc.swd += wq * dq;
+            acc.mind = dq < acc.mind ? dq : acc.mind;
+            acc.maxd = dq > acc.maxd ? dq : acc.maxd;
+        }
+        TC* crow = counts + (long long)vid * a.C;
+        if (closed && !a.last_wins && (unsigned)lane < k) atomicAdd(&crow[lab - 1], (TC)1);
+        const int last = __shfl_sync(0xffffffffu, lab, k - 1);
+        if (lane == 0) {
+            P2 st = reinterpret_cast<const P2*>(vt)[vid];
+            if (en.vid & kNewBit) {
+                st.x = (TD)a.trunc;
+                st.y = (TD)0;
+            }
+            const double w_old = (double)st.y, d_old = (double)st.x;
+            const double w_new = w_old + acc.sw;
+            double d_new = w_new > 0.0 ? (w_old * d_old + acc.swd) / w_new : d_old;
+            if ((acc.mind == acc.maxd) && (w_old == 0.0 || equals_stored<TD>(st.x, acc.mind)))
+                d_new = acc.mind;
+            P2 out;
+            out.x = (TD)d_new;
+            out.y = (TD)w_new;
+            reinterpret_cast<P2*>(vt)[vid] = out;
+            bslot[en.bidx] = (unsigned long long)(unsigned)vid;
+        }
+        if (closed && a.last_wins)
+            for (int t = lane; t < a.C; t += 32) crow[t] = (TC)(t == last - 1 ? 1 : 0);
     }
 }
 
@@ -728,6 +799,7 @@ UpdateArgs make_args(svx_map* m) {
     a.ray = ptr<double4>(m->ray);
     a.longlist = ptr<int>(m->longlist);
     a.hugelist = ptr<int>(m->longlist) + m->ucap;
+    a.hugelist2 = ptr<TouchEntry>(m->longlist);
     a.bitmap = ptr<unsigned>(m->bitmap);
     a.bm_words = (m->npts_cap + 31) / 32 + 1;
     a.h = m->cfg.voxel_size;
@@ -791,6 +863,10 @@ template <class TD, class TC>
 svx_status slots_t(svx_map* m, cudaStream_t s) {
     SVX_CUDA(launch_pdl(k_update_slots<TD, TC>, kPersistentBlocks, 256, 0, s, make_args(m),
                         ptr<TouchEntry>(m->tlist), ptr<unsigned>(m->rcount),
+                        ptr<unsigned long long>(m->bslot), ptr<RowSlot>(m->vslot), ptr<TD>(m->vt),
+                        ptr<TC>(m->s0)));
+    SVX_LAUNCHED();
+    SVX_CUDA(launch_pdl(k_update_slots_long<TD, TC>, 148 * 2, 256, 0, s, make_args(m),
                         ptr<unsigned long long>(m->bslot), ptr<RowSlot>(m->vslot), ptr<TD>(m->vt),
                         ptr<TC>(m->s0)));
     SVX_LAUNCHED();
