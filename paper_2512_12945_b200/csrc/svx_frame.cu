@@ -84,7 +84,7 @@ svx_status reserve_voxels(svx_map* m, int64_t need, cudaStream_t s) {
         SVX_TRY(ensure(m->s1, se * (size_t)m->payload_d * cap, s, true, 0));
     SVX_TRY(ensure(m->vrec, sizeof(VoxFrame) * cap, s, true, 0));
     if (m->cfg.sem_kind != SVX_SEM_OPEN && !m->cfg.space_carving)   // per-frame contents only
-        SVX_TRY(ensure(m->vslot, sizeof(RowSlot) * kSlots * cap, s));
+        SVX_TRY(ensure(m->vslot, sizeof(RowSlot) * kSlots * kSlotStride * cap, s));
     m->vcap = cap;
     return SVX_OK;
 }

@@ -44,6 +44,8 @@ constexpr int kShortMax = 16;   // segments up to this many rows: thread-per-vox
 // A voxel with more rows stops the attempt before any payload changes; the
 // frame re-runs in segment mode.
 constexpr int kSlots = 16;
+// RowSlot spacing in vslot (2 = one 32-byte sector per row; measured: no gain).
+constexpr int kSlotStride = 1;
 
 struct PoseParams {
     double R[9];
@@ -321,6 +323,18 @@ struct KSpan {
         if (rec) rec[kSpanMaxCtas] = globaltimer();
     }
 };
+
+// Per-CTA snapshot of the frame's counters and parameters in shared memory
+// (after grid_dep_wait(), by all threads): kernels read them from there
+// instead of every thread loading them from global memory.  Only fields that
+// are final before the kernel starts may be read from the snapshot.
+__device__ __forceinline__ void snapshot_ctr(const FrameCtr* g, FrameCtr& s) {
+    static_assert(sizeof(FrameCtr) % 8 == 0, "FrameCtr must be a whole number of words");
+    const unsigned long long* src = reinterpret_cast<const unsigned long long*>(g);
+    unsigned long long* dst = reinterpret_cast<unsigned long long*>(&s);
+    for (int i = threadIdx.x; i < (int)(sizeof(FrameCtr) / 8); i += blockDim.x) dst[i] = __ldcg(src + i);
+    __syncthreads();
+}
 
 template <class... KArgs, class... Args>
 inline cudaError_t launch_pdl(void (*kernel)(KArgs...), unsigned grid, unsigned block, size_t smem,

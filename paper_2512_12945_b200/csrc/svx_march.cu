@@ -266,6 +266,8 @@ __global__ void __launch_bounds__(kTileRays, 4) k_walk(MarchParams mp, int sem_k
                                                     FrameCtr* __restrict__ ctr) {
     grid_dep_wait();
     KSpan _ks(ctr, kSpanWalk);
+    __shared__ FrameCtr s_ctr_;
+    snapshot_ctr(ctr, s_ctr_);
     using Scan = cub::BlockScan<int, kTileRays>;
     __shared__ typename Scan::TempStorage scan_tmp;
     __shared__ unsigned long long s_base;
@@ -273,7 +275,7 @@ __global__ void __launch_bounds__(kTileRays, 4) k_walk(MarchParams mp, int sem_k
     __shared__ double4 s_ray[kTileRays];
     __shared__ int s_lab[kTileRays];
     extern __shared__ unsigned long long s_keys[];   // kTileRays * maxrows keys, then row owners
-    const FrameParams fp = ctr->p;
+    const FrameParams& fp = s_ctr_.p;
     const long long n = fp.n;
     const int maxrows = fp.maxrows;
     const bool slots = fp.slots != 0;
@@ -374,7 +376,9 @@ __global__ void __launch_bounds__(kMarchThreads) k_walk_count(MarchParams mp, in
                                                               FrameCtr* __restrict__ ctr) {
     grid_dep_wait();
     KSpan _ks(ctr, kSpanWalk);
-    const FrameParams fp = ctr->p;
+    __shared__ FrameCtr s_ctr_;
+    snapshot_ctr(ctr, s_ctr_);
+    const FrameParams& fp = s_ctr_.p;
     const long long n = fp.n;
     const double ox = fp.pp.t[0], oy = fp.pp.t[1], oz = fp.pp.t[2];
     Tally t;
@@ -421,8 +425,10 @@ __global__ void __launch_bounds__(kMarchThreads) k_walk_write(MarchParams mp,
                                                               const FrameCtr* __restrict__ ctr) {
     grid_dep_wait();
     KSpan _ks(const_cast<FrameCtr*>(ctr), kSpanWalk);
-    if (ctr->abort) return;
-    const FrameParams fp = ctr->p;
+    __shared__ FrameCtr s_ctr_;
+    snapshot_ctr(ctr, s_ctr_);
+    if (s_ctr_.abort) return;
+    const FrameParams& fp = s_ctr_.p;
     const long long n = fp.n;
     const double ox = fp.pp.t[0], oy = fp.pp.t[1], oz = fp.pp.t[2];
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;

@@ -45,13 +45,16 @@ __global__ void __launch_bounds__(kResolveThreads) k_resolve(
     __shared__ unsigned s_tcount;
     FrameCtr* ctr = ra.ctr;
     KSpan _ks(ctr, kSpanResolve);
+    __shared__ FrameCtr s_ctr_;
+    snapshot_ctr(ctr, s_ctr_);
+    const FrameCtr* cv = &s_ctr_;
     if (threadIdx.x == 0) s_tcount = 0u;
-    if (ctr->abort) {
+    if (cv->abort) {
         if (threadIdx.x == 0) ra.rcount[blockIdx.x] = 0u;
         return;
     }
-    const FrameParams& fp = ctr->p;
-    const long long total = (long long)ctr->rows;
+    const FrameParams& fp = cv->p;
+    const long long total = (long long)cv->rows;
     ra.kp = fp.kp;
     ra.hmask = fp.hmask;
     ra.bcap = fp.bcap;
@@ -107,14 +110,17 @@ __global__ void __launch_bounds__(kSegThreads) k_seg(const int* __restrict__ tli
                                                      SegStatus* __restrict__ status, FrameCtr* ctr) {
     grid_dep_wait();
     KSpan _ks(ctr, kSpanSeg);
+    __shared__ FrameCtr s_ctr_;
+    snapshot_ctr(ctr, s_ctr_);
+    const FrameCtr* cv = &s_ctr_;
     using Scan = cub::BlockScan<unsigned long long, kSegThreads>;
     __shared__ typename Scan::TempStorage scan_tmp;
     __shared__ unsigned long long s_prefix;
     __shared__ long long s_tile;
-    if (ctr->abort | ctr->err_cap) return;
-    const long long n = (long long)ctr->n_touched;
-    const int singles = ctr->p.inline_singles;
-    const unsigned long long seq = ctr->p.seq;
+    if (cv->abort | cv->err_cap) return;
+    const long long n = (long long)cv->n_touched;
+    const int singles = cv->p.inline_singles;
+    const unsigned long long seq = cv->p.seq;
     const unsigned long long low40 = (1ULL << 40) - 1;
     const long long ntiles = (n + kSegTile - 1) / kSegTile;
     const int lane = threadIdx.x & 31;

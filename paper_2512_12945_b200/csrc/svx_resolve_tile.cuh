@@ -313,7 +313,11 @@ __device__ __forceinline__ void resolve_step(const ResolveArgs& ra, bool valid,
         // restored by point index in k_update_slots)
         cbase = __shfl_sync(full, cbase, vleader) + __popc(vpeers & ((1u << lane) - 1u));
         if (valid && vid >= 0) {
-            if (cbase < (unsigned)kSlots) vslot[(long long)vid * kSlots + cbase] = rsl;
+            if (cbase < (unsigned)kSlots) {
+                RowSlot* dst = vslot + ((long long)vid * kSlots + cbase) * kSlotStride;
+                dst[0] = rsl;
+                if (kSlotStride == 2) dst[1] = RowSlot{0, 0, 0.0};
+            }
             else ctr->err_slots = 1;
         }
     } else if (valid) {

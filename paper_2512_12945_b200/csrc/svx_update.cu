@@ -137,13 +137,16 @@ __global__ void __launch_bounds__(256) k_scatter(UpdateArgs a, const int* __rest
     grid_dep_wait();
     FrameCtr* ctr = a.ctr;
     KSpan _ks(ctr, kSpanScatter);
-    if (ctr->abort | ctr->err_cap) return;
-    const FrameParams& fp = ctr->p;
+    __shared__ FrameCtr s_ctr_;
+    snapshot_ctr(ctr, s_ctr_);
+    const FrameCtr* cv = &s_ctr_;
+    if (cv->abort | cv->err_cap) return;
+    const FrameParams& fp = cv->p;
     RowSpace rs;
     rs.maxrows = 0;   // rows are dense in every mode
     rs.rcnt = rcnt;
     rs.rowray = rowray;
-    rs.total = (long long)ctr->rows;
+    rs.total = (long long)cv->rows;
     const KeyPack kp = fp.kp;
     const PoseParams pp = fp.pp;
     const int32_t* __restrict__ labels = fp.labels;
@@ -186,11 +189,14 @@ __global__ void __launch_bounds__(256) k_update_short(UpdateArgs a, TD* vt, TC* 
     grid_dep_wait();
     FrameCtr* ctr = a.ctr;
     KSpan _ks(ctr, kSpanUpdate);
-    if (ctr->abort | ctr->err_cap) return;
-    const long long L = (long long)ctr->n_list;
-    const KeyPack kp = ctr->p.kp;
-    const PoseParams pp = ctr->p.pp;
-    const int32_t* __restrict__ labels = ctr->p.labels;
+    __shared__ FrameCtr s_ctr_;
+    snapshot_ctr(ctr, s_ctr_);
+    const FrameCtr* cv = &s_ctr_;
+    if (cv->abort | cv->err_cap) return;
+    const long long L = (long long)cv->n_list;
+    const KeyPack kp = cv->p.kp;
+    const PoseParams pp = cv->p.pp;
+    const int32_t* __restrict__ labels = cv->p.labels;
     const bool closed = a.sem_kind == SVX_SEM_CLOSED;
     for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < L;
          e += (long long)gridDim.x * blockDim.x) {
@@ -277,7 +283,7 @@ __device__ __forceinline__ RowSlot ld_slot16(const RowSlot* p) {
 }
 
 template <class TD, class TC>
-__global__ void __launch_bounds__(256) k_update_slots(UpdateArgs a, const TouchEntry* __restrict__ tent,
+__global__ void __launch_bounds__(256, 4) k_update_slots(UpdateArgs a, const TouchEntry* __restrict__ tent,
                                                       const unsigned* __restrict__ rcount,
                                                       unsigned long long* __restrict__ bslot,
                                                       const RowSlot* __restrict__ vslot, TD* vt,
@@ -285,9 +291,12 @@ __global__ void __launch_bounds__(256) k_update_slots(UpdateArgs a, const TouchE
     grid_dep_wait();
     FrameCtr* ctr = a.ctr;
     KSpan _ks(ctr, kSpanUpdate);
-    if (ctr->abort | ctr->err_cap | ctr->err_slots) return;
+    __shared__ FrameCtr s_ctr_;
+    snapshot_ctr(ctr, s_ctr_);
+    const FrameCtr* cv = &s_ctr_;
+    if (cv->abort | cv->err_cap | cv->err_slots) return;
     const bool closed = a.sem_kind == SVX_SEM_CLOSED;
-    const long long region = ctr->p.region;
+    const long long region = cv->p.region;
     using P2 = typename Pair<TD>::type;
     // K2 CTA b listed its touched voxels in region b; this grid has the same size
     const unsigned cnt = rcount[blockIdx.x];
@@ -297,20 +306,52 @@ __global__ void __launch_bounds__(256) k_update_slots(UpdateArgs a, const TouchE
         const int vid = (int)(en.vid & ~kNewBit);
         const unsigned c = (unsigned)(bslot[en.bidx] >> 32) | (en.vid & kNewBit);
         P2 st = reinterpret_cast<const P2*>(vt)[vid];
-        const RowSlot* sl = vslot + (long long)vid * kSlots;
+        const RowSlot* sl = vslot + (long long)vid * kSlots * kSlotStride;
         const unsigned k = c & ~kNewBit;
-        if (k > 4u) {   // 5..16 rows (a few percent): one warp per voxel in k_update_slots_long
+        if (k > 8u) {   // 9..16 rows (rare): one warp per voxel in k_update_slots_long
             a.hugelist2[warp_ticket(&ctr->n_long)] = en;
             continue;
         }
+        TC* crow = counts + (long long)vid * a.C;
+        RowAcc acc;
+        if (k > 4u) {
+            // 5..8 rows: sort (point, slot) keys in registers, then fold the rows
+            // in that order (their slots were just read: L1/L2 hits)
+            unsigned long long key[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                key[j] = (unsigned)j < k ? (((unsigned long long)(unsigned)sl[j * kSlotStride].point << 3) | (unsigned)j)
+                                         : ~0ULL;
+#pragma unroll
+            for (int kk = 2; kk <= 8; kk <<= 1) {
+#pragma unroll
+                for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const int l = i ^ jj;
+                        if (l > i) {
+                            const unsigned long long x = key[i], y = key[l];
+                            const bool up = (i & kk) == 0;
+                            key[i] = up ? (x < y ? x : y) : (x > y ? x : y);
+                            key[l] = up ? (x > y ? x : y) : (x < y ? x : y);
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                if ((unsigned)j < k) {
+                    const RowSlot r = ld_slot16(sl + (int)(key[j] & 7u) * kSlotStride);
+                    fold_row<TC>(a, r.d, r.label, crow, closed, acc);
+                }
+            }
+        } else {
         // rows in registers; only slots that exist are read (no partial-sector reads)
         RowSlot q0 = ld_slot16(sl), q1, q2, q3;
         q1.point = q2.point = q3.point = 0x7fffffff;
-        if (k > 1u) q1 = ld_slot16(sl + 1);
-        if (k > 2u) q2 = ld_slot16(sl + 2);
-        if (k > 3u) q3 = ld_slot16(sl + 3);
-        TC* crow = counts + (long long)vid * a.C;
-        RowAcc acc;
+        if (k > 1u) q1 = ld_slot16(sl + 1 * kSlotStride);
+        if (k > 2u) q2 = ld_slot16(sl + 2 * kSlotStride);
+        if (k > 3u) q3 = ld_slot16(sl + 3 * kSlotStride);
         // 4-element sorting network on the point index (5 compare-exchanges)
         auto cx = [](RowSlot& x, RowSlot& y) {
             if (y.point < x.point) {
@@ -328,6 +369,7 @@ __global__ void __launch_bounds__(256) k_update_slots(UpdateArgs a, const TouchE
         if (k > 1u) fold_row<TC>(a, q1.d, q1.label, crow, closed, acc);
         if (k > 2u) fold_row<TC>(a, q2.d, q2.label, crow, closed, acc);
         if (k > 3u) fold_row<TC>(a, q3.d, q3.label, crow, closed, acc);
+        }
         // apply_tsdf (_pycore.py:399-417) on the pre-loaded pair
         if (c & kNewBit) {
             st.x = (TD)a.trunc;
@@ -348,7 +390,7 @@ __global__ void __launch_bounds__(256) k_update_slots(UpdateArgs a, const TouchE
     }
 }
 
-// Slot-mode voxels of 5..16 rows: one warp per voxel; lanes own rows, a
+// Slot-mode voxels of 9..16 rows: one warp per voxel; lanes own rows, a
 // shuffle bitonic sort on (point, lane) orders them, the sums run in that
 // order through shuffles.
 template <class TD, class TC>
@@ -359,18 +401,21 @@ __global__ void __launch_bounds__(256) k_update_slots_long(UpdateArgs a,
     grid_dep_wait();
     FrameCtr* ctr = a.ctr;
     KSpan _ks(ctr, kSpanUpdateB);
-    if (ctr->abort | ctr->err_cap | ctr->err_slots) return;
+    __shared__ FrameCtr s_ctr_;
+    snapshot_ctr(ctr, s_ctr_);
+    const FrameCtr* cv = &s_ctr_;
+    if (cv->abort | cv->err_cap | cv->err_slots) return;
     const bool closed = a.sem_kind == SVX_SEM_CLOSED;
     const int lane = threadIdx.x & 31;
     using P2 = typename Pair<TD>::type;
-    const long long L = (long long)ctr->n_long;
+    const long long L = (long long)cv->n_long;
     for (long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < L;
          w += ((long long)gridDim.x * blockDim.x) >> 5) {
         const TouchEntry en = a.hugelist2[w];
         const int vid = (int)(en.vid & ~kNewBit);
         const unsigned k = (unsigned)(bslot[en.bidx] >> 32);
         RowSlot r{0x7fffffff, 0, 0.0};
-        if ((unsigned)lane < k) r = ld_slot16(vslot + (long long)vid * kSlots + lane);
+        if ((unsigned)lane < k) r = ld_slot16(vslot + ((long long)vid * kSlots + lane) * kSlotStride);
         unsigned long long key = ((unsigned long long)(unsigned)r.point << 32) | (unsigned)lane;
 #pragma unroll
         for (int kk = 2; kk <= 32; kk <<= 1) {
@@ -569,16 +614,19 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) k_update_long(UpdateArgs a,
     __shared__ int sbuf[kWarpsPerCta][kSmemMax];
     FrameCtr* ctr = a.ctr;
     KSpan _ks(ctr, kSpanUpdateB);
-    if (ctr->abort | ctr->err_cap) return;
+    __shared__ FrameCtr s_ctr_;
+    snapshot_ctr(ctr, s_ctr_);
+    const FrameCtr* cv = &s_ctr_;
+    if (cv->abort | cv->err_cap) return;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     int* buf = sbuf[wib];
-    const KeyPack kp = ctr->p.kp;
-    const PoseParams pp = ctr->p.pp;
-    const int32_t* labels = ctr->p.labels;
+    const KeyPack kp = cv->p.kp;
+    const PoseParams pp = cv->p.pp;
+    const int32_t* labels = cv->p.labels;
     const bool closed = a.sem_kind == SVX_SEM_CLOSED;
     const long long gw = (long long)blockIdx.x * kWarpsPerCta + wib;
     const long long nwarps = (long long)gridDim.x * kWarpsPerCta;
-    const long long L = (long long)ctr->n_long;
+    const long long L = (long long)cv->n_long;
     for (long long t = gw; t < L; t += nwarps) {
         const int vid = a.mlist[a.longlist[t]];
         const unsigned c = a.rec[vid].cnt;
@@ -596,7 +644,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) k_update_long(UpdateArgs a,
     // huge segments: only the first kHugeWarps warps own bitmap scratch
     if (gw >= kHugeWarps) return;
     unsigned* bm = a.bitmap + gw * a.bm_words;
-    const long long Hn = (long long)ctr->n_huge;
+    const long long Hn = (long long)cv->n_huge;
     for (long long t = gw; t < Hn; t += kHugeWarps) {
         const int vid = a.mlist[a.hugelist[t]];
         const unsigned c = a.rec[vid].cnt;
@@ -729,12 +777,15 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) k_update_open(UpdateArgs a,
     __shared__ int sbuf[kWarpsPerCta][kSmemMax];
     FrameCtr* ctr = a.ctr;
     KSpan _ks(ctr, kSpanUpdate);
-    if (ctr->abort | ctr->err_cap) return;
+    __shared__ FrameCtr s_ctr_;
+    snapshot_ctr(ctr, s_ctr_);
+    const FrameCtr* cv = &s_ctr_;
+    if (cv->abort | cv->err_cap) return;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const long long L = (long long)ctr->n_list;
-    const KeyPack kp = ctr->p.kp;
-    const PoseParams pp = ctr->p.pp;
-    const Fe* feats = (const Fe*)ctr->p.feats;
+    const long long L = (long long)cv->n_list;
+    const KeyPack kp = cv->p.kp;
+    const PoseParams pp = cv->p.pp;
+    const Fe* feats = (const Fe*)cv->p.feats;
     for (long long e = (long long)blockIdx.x * kWarpsPerCta + wib; e < L;
          e += (long long)gridDim.x * kWarpsPerCta) {
         const int vid = a.mlist[e];
@@ -754,14 +805,17 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) k_update_open_huge(UpdateAr
     __shared__ int sbuf[kWarpsPerCta][kSmemMax];
     FrameCtr* ctr = a.ctr;
     KSpan _ks(ctr, kSpanUpdateB);
-    if (ctr->abort | ctr->err_cap) return;
+    __shared__ FrameCtr s_ctr_;
+    snapshot_ctr(ctr, s_ctr_);
+    const FrameCtr* cv = &s_ctr_;
+    if (cv->abort | cv->err_cap) return;
     const int wib = threadIdx.x >> 5;
     const long long gw = (long long)blockIdx.x * kWarpsPerCta + wib;
     unsigned* bm = a.bitmap + gw * a.bm_words;
-    const long long Hn = (long long)ctr->n_huge;
-    const KeyPack kp = ctr->p.kp;
-    const PoseParams pp = ctr->p.pp;
-    const Fe* feats = (const Fe*)ctr->p.feats;
+    const long long Hn = (long long)cv->n_huge;
+    const KeyPack kp = cv->p.kp;
+    const PoseParams pp = cv->p.pp;
+    const Fe* feats = (const Fe*)cv->p.feats;
     for (long long t = gw; t < Hn; t += (long long)gridDim.x * kWarpsPerCta) {
         const int vid = a.mlist[a.hugelist[t]];
         open_voxel<TD, TS, Fe>(a, kp, pp, vt, mean, beta, feats, vid, a.rec[vid].cnt, sbuf[wib], bm,
