@@ -150,10 +150,12 @@ svx_status svx_create(const svx_config* cfg, svx_map** out) {
         svx_destroy(m);
         return code;
     };
-    if (cudaMallocHost((void**)&m->h_ctr, sizeof(FrameCtr)) != cudaSuccess) {
+    if (cudaHostAlloc((void**)&m->h_ctr, sizeof(FrameCtr), cudaHostAllocMapped) != cudaSuccess ||
+        cudaHostGetDevicePointer((void**)&m->d_hctr, m->h_ctr, 0) != cudaSuccess) {
         cudaGetLastError();
-        return bail(fail(SVX_E_CUDA, "pinned allocation failed"));
+        return bail(fail(SVX_E_CUDA, "pinned mapped allocation failed"));
     }
+    memset(m->h_ctr, 0, sizeof(FrameCtr));
     if ((st = ensure(m->ctr, sizeof(FrameCtr), s)) != SVX_OK) return bail(st);
     if (cudaEventCreate(&m->ev0) != cudaSuccess || cudaEventCreate(&m->ev1) != cudaSuccess ||
         cudaEventCreateWithFlags(&m->ev_in, cudaEventDisableTiming) != cudaSuccess ||

@@ -169,22 +169,35 @@ static unsigned long long graph_signature(const svx_map* m, int pts_f64, int fea
 }
 
 
-// Enqueue one frame attempt on stream s (eager or under graph capture).
+// Enqueue one frame attempt on stream s (under graph capture).  No copy
+// nodes: the first kernel reads the parameters from the mapped host
+// FrameCtr, the last kernel's epilogue writes the counters back into it.
 static svx_status enqueue_frame(svx_map* m, int pts_f64, int feats_f64, cudaStream_t s) {
-    FrameCtr* dc = ptr<FrameCtr>(m->ctr);
-    SVX_CUDA(cudaMemcpyAsync(dc, m->h_ctr, sizeof(FrameCtr), cudaMemcpyHostToDevice, s));
     SVX_TRY(launch_march(m, pts_f64, feats_f64, s));
     SVX_TRY(launch_resolve(m, s));
-    if (m->frame_slots) {
-        SVX_TRY(launch_update_slots(m, s));
-        SVX_CUDA(cudaMemcpyAsync(m->h_ctr, dc, sizeof(FrameCtr), cudaMemcpyDeviceToHost, s));
-        return SVX_OK;
-    }
+    if (m->frame_slots) return launch_update_slots(m, s);
     SVX_TRY(launch_segments(m, s));
     SVX_TRY(launch_scatter(m, s));
     SVX_TRY(launch_update_a(m, feats_f64, s));
     SVX_TRY(launch_update_b(m, feats_f64, s));
-    SVX_CUDA(cudaMemcpyAsync(m->h_ctr, dc, sizeof(FrameCtr), cudaMemcpyDeviceToHost, s));
+    return SVX_OK;
+}
+
+// Bring the device FrameCtr to the reset state the graph frames assume
+// (after the sharded calls or a host-side change of the live pool counts).
+svx_status clean_ctr(svx_map* m, cudaStream_t s) {
+    if (m->ctr_clean) return SVX_OK;
+    FrameCtr img;
+    memset(&img, 0, sizeof(img));
+    for (int a = 0; a < 3; ++a) {
+        img.bbox_min[a] = LLONG_MAX;
+        img.bbox_max[a] = LLONG_MIN;
+    }
+    img.nblocks = (unsigned long long)m->nblocks;
+    img.nvox = (unsigned long long)m->nvox;
+    SVX_CUDA(cudaMemcpyAsync(m->ctr.p, &img, sizeof(img), cudaMemcpyHostToDevice, s));
+    SVX_CUDA(cudaStreamSynchronize(s));
+    m->ctr_clean = true;
     return SVX_OK;
 }
 
@@ -243,6 +256,7 @@ static svx_status run_frame(svx_map* m, int pts_f64, int feats_f64, cudaStream_t
         const size_t n = (size_t)kSpanKernels * 2 * kSpanMaxCtas * sizeof(unsigned long long);
         SVX_CUDA(cudaMemsetAsync(m->kspan.p, 0, n, s));
     }
+    SVX_TRY(clean_ctr(m, s));
     // the graph was captured on the map's own stream; it runs on the caller's
     if (g_trace_host) g_t_launch0 = now_us();
     SVX_CUDA(cudaGraphLaunch(gexec, s));
@@ -301,6 +315,8 @@ void reset_ctr(svx_map* m) {
     p.inline_singles = inline_singles(m);
     p.slots = m->frame_slots;
     p.kspan = m->prof ? ptr<unsigned long long>(m->kspan) : nullptr;
+    p.mirror = m->d_hctr;
+    p.epilogue = 1;   // graph frames; the sharded calls copy explicitly and set 0
     p.region = slot_region(m->rcap);
     p.seq = ++m->seq;
 }
@@ -315,6 +331,7 @@ svx_status recover_capacity(svx_map* m, int64_t nblocks0, cudaStream_t s) {
     m->nblocks = (int64_t)std::min<unsigned long long>(hc->nblocks, (unsigned long long)m->bcap);
     m->nvox = (int64_t)std::min<unsigned long long>(hc->nvox, (unsigned long long)m->vcap);
     m->ord_nblocks = std::min<int64_t>(m->ord_nblocks, nblocks0);
+    m->ctr_clean = false;   // live counts may have been clamped to the pools
     m->new_leaves_cap = std::max<int64_t>(2 * m->new_leaves_cap, m->bcap);
     SVX_TRY(reserve_voxels(m, 2 * m->vcap, s));
     return SVX_OK;
@@ -330,6 +347,7 @@ svx_status recover_slots(svx_map* m, int64_t nblocks0, cudaStream_t s) {
     m->nblocks = (int64_t)std::min<unsigned long long>(hc->nblocks, (unsigned long long)m->bcap);
     m->nvox = (int64_t)std::min<unsigned long long>(hc->nvox, (unsigned long long)m->vcap);
     m->ord_nblocks = std::min<int64_t>(m->ord_nblocks, nblocks0);
+    m->ctr_clean = false;
     m->slot_hold = 32;
     m->frame_retry_segments = 1;
     m->n_slot_reruns++;

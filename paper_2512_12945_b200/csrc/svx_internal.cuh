@@ -17,6 +17,8 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <limits.h>
+#include <stddef.h>
 #include <stdint.h>
 
 #include <string>
@@ -80,6 +82,8 @@ struct FrameParams {
     int slots;                 // 1: slot mode (K2 fills vslot; K5 = k_update_slots)
     long long region;          // slot mode: touched entries per K2 CTA (svx::slot_region)
     unsigned long long* kspan; // profiling: per-CTA start/end times (KSpan), else null
+    void* mirror;              // graph frames: device address of the mapped host FrameCtr
+    int epilogue;              // 1: the frame's last kernel publishes + resets the counters
     unsigned seq;              // launch sequence number (epoch of the segment-scan status)
 };
 
@@ -124,6 +128,8 @@ struct FrameCtr {
     int err_rows;                   // a band exceeded maxrows (retry with dense rows)
     int abort;                      // set by the gate: skip all mutation
     int err_slots;                  // slot mode: a voxel got more than kSlots rows (re-run in segment mode)
+    unsigned epi_done;              // CTAs of the last kernel finished (frame_epilogue)
+    unsigned pad_;
 };
 
 // Per-voxel frame record (indexed by voxel id; cnt and cur are zero between
@@ -237,7 +243,9 @@ struct svx_map {
     unsigned long long gsig[2] = {};
     svx::DevBuf cubtmp;
     svx::DevBuf ctr;      // FrameCtr
-    svx::FrameCtr* h_ctr = nullptr;  // pinned mirror
+    svx::FrameCtr* h_ctr = nullptr;  // pinned, mapped mirror (host side)
+    svx::FrameCtr* d_hctr = nullptr; // its device address
+    bool ctr_clean = false;          // device FrameCtr is in the reset state
     // query scratch
     svx::DevBuf ord0, ord1, ordk0, ordk1, ordf0, ordf1;  // leaf order (by creation stamp)
     int64_t ord_nblocks = -1;
@@ -311,7 +319,12 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 // reduces them to [first start, last end].  One branch when profiling is off.
 struct KSpan {
     unsigned long long* rec;
-    __device__ __forceinline__ KSpan(FrameCtr* ctr, int k) : rec(ctr->p.kspan) {
+    __device__ __forceinline__ KSpan(FrameCtr* ctr, int k) : rec(ctr->p.kspan) { start(k); }
+    // first kernel of a frame: parameters from its snapshot
+    __device__ __forceinline__ KSpan(const FrameCtr* snap, FrameCtr*, int k) : rec(snap->p.kspan) {
+        start(k);
+    }
+    __device__ __forceinline__ void start(int k) {
         if (rec && threadIdx.x == 0 && blockIdx.x < kSpanMaxCtas) {
             rec += (size_t)k * 2 * kSpanMaxCtas + blockIdx.x;
             rec[0] = globaltimer();
@@ -334,6 +347,65 @@ __device__ __forceinline__ void snapshot_ctr(const FrameCtr* g, FrameCtr& s) {
     unsigned long long* dst = reinterpret_cast<unsigned long long*>(&s);
     for (int i = threadIdx.x; i < (int)(sizeof(FrameCtr) / 8); i += blockDim.x) dst[i] = __ldcg(src + i);
     __syncthreads();
+}
+
+// First kernel of a frame: counters from the device FrameCtr (reset state),
+// parameters from the host mirror (mapped memory, written by the host before
+// the launch); CTA 0 publishes the parameters to the device FrameCtr for the
+// later kernels.  All threads call it.
+__device__ __forceinline__ void load_frame_params(FrameCtr* ctr, FrameCtr& s, const FrameParams* hp) {
+    snapshot_ctr(ctr, s);
+    const unsigned long long* src = reinterpret_cast<const unsigned long long*>(hp);
+    unsigned long long* dst = reinterpret_cast<unsigned long long*>(&s.p);
+    static_assert(sizeof(FrameParams) % 8 == 0, "FrameParams must be a whole number of words");
+    for (int i = threadIdx.x; i < (int)(sizeof(FrameParams) / 8); i += blockDim.x) dst[i] = __ldcv(src + i);
+    __syncthreads();
+    if (blockIdx.x == 0) {
+        unsigned long long* g = reinterpret_cast<unsigned long long*>(&ctr->p);
+        for (int i = threadIdx.x; i < (int)(sizeof(FrameParams) / 8); i += blockDim.x) g[i] = dst[i];
+    }
+}
+
+// Graph frames have no copy nodes.  The first kernel reads the frame's
+// parameters from the mapped host FrameCtr (load_frame_params) and publishes
+// them to the device FrameCtr; the last kernel's last CTA copies the device
+// FrameCtr to the mapped host FrameCtr (the host reads it after the frame's
+// event) and resets the device counters for the next frame.  The live pool
+// counters (nblocks, nvox) carry over.
+__device__ __forceinline__ void reset_ctr_device(FrameCtr* ctr) {
+    unsigned long long* w = reinterpret_cast<unsigned long long*>(ctr);
+    const int first = (int)(offsetof(FrameCtr, nonfinite) / 8);
+    const int total = (int)(sizeof(FrameCtr) / 8);
+    const int keep0 = (int)(offsetof(FrameCtr, nblocks) / 8), keep1 = (int)(offsetof(FrameCtr, nvox) / 8);
+    const int bb0 = (int)(offsetof(FrameCtr, bbox_min) / 8), bb1 = (int)(offsetof(FrameCtr, bbox_max) / 8);
+    for (int i = first + (int)threadIdx.x; i < total; i += blockDim.x) {
+        if (i == keep0 || i == keep1) continue;
+        unsigned long long v = 0ULL;
+        if (i >= bb0 && i < bb0 + 3) v = (unsigned long long)LLONG_MAX;
+        if (i >= bb1 && i < bb1 + 3) v = (unsigned long long)LLONG_MIN;
+        w[i] = v;
+    }
+}
+
+// Called by every thread of the frame's last kernel, after its work (no
+// early returns before it).  `epi` = FrameParams.epilogue.
+__device__ __forceinline__ void frame_epilogue(FrameCtr* ctr, int epi, void* mirror) {
+    if (!epi) return;
+    __shared__ bool s_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(&ctr->epi_done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const unsigned long long* src = reinterpret_cast<const unsigned long long*>(ctr);
+    unsigned long long* dst = reinterpret_cast<unsigned long long*>(mirror);
+    for (int i = threadIdx.x; i < (int)(sizeof(FrameCtr) / 8); i += blockDim.x) dst[i] = __ldcg(src + i);
+    __syncthreads();
+    reset_ctr_device(ctr);
+    __threadfence_system();
 }
 
 template <class... KArgs, class... Args>
@@ -462,6 +534,7 @@ svx_status reserve_pools(svx_map* m, cudaStream_t s);
 void reset_ctr(svx_map* m);
 svx_status recover_capacity(svx_map* m, int64_t nblocks0, cudaStream_t s);
 svx_status recover_slots(svx_map* m, int64_t nblocks0, cudaStream_t s);
+svx_status clean_ctr(svx_map* m, cudaStream_t s);
 int choose_slots(const svx_map* m);
 void finish_frame(svx_map* m, int64_t nblocks0, int64_t nvox0, svx_report& r);
 KeyPack default_key_pack(const svx_map* m, const PoseParams& pp);

@@ -263,11 +263,12 @@ __global__ void __launch_bounds__(kTileRays, 4) k_walk(MarchParams mp, int sem_k
                                                     double* __restrict__ rowd,
                                                     int* __restrict__ rowlab,
                                                     MarchPartial* __restrict__ partials,
-                                                    FrameCtr* __restrict__ ctr) {
+                                                    FrameCtr* __restrict__ ctr,
+                                                    const FrameParams* __restrict__ hp) {
     grid_dep_wait();
-    KSpan _ks(ctr, kSpanWalk);
     __shared__ FrameCtr s_ctr_;
-    snapshot_ctr(ctr, s_ctr_);
+    load_frame_params(ctr, s_ctr_, hp);
+    KSpan _ks(&s_ctr_, ctr, kSpanWalk);
     using Scan = cub::BlockScan<int, kTileRays>;
     __shared__ typename Scan::TempStorage scan_tmp;
     __shared__ unsigned long long s_base;
@@ -373,11 +374,12 @@ __global__ void __launch_bounds__(kMarchThreads) k_walk_count(MarchParams mp, in
                                                               double4* __restrict__ ray,
                                                               int* __restrict__ rcnt,
                                                               MarchPartial* __restrict__ partials,
-                                                              FrameCtr* __restrict__ ctr) {
+                                                              FrameCtr* __restrict__ ctr,
+                                                              const FrameParams* __restrict__ hp) {
     grid_dep_wait();
-    KSpan _ks(ctr, kSpanWalk);
     __shared__ FrameCtr s_ctr_;
-    snapshot_ctr(ctr, s_ctr_);
+    load_frame_params(ctr, s_ctr_, hp);
+    KSpan _ks(&s_ctr_, ctr, kSpanWalk);
     const FrameParams& fp = s_ctr_.p;
     const long long n = fp.n;
     const double ox = fp.pp.t[0], oy = fp.pp.t[1], oz = fp.pp.t[2];
@@ -520,13 +522,13 @@ svx_status march_t(svx_map* m, cudaStream_t s) {
         SVX_CUDA(launch_pdl(k_walk<P, Fe>, kMarchBlocks, kTileRays, smem, s, 
             mp, m->cfg.sem_kind, m->cfg.num_classes, m->payload_d, ptr<double4>(m->ray),
             ptr<int>(m->rcnt), ptr<unsigned long long>(m->rowkey), ptr<int>(m->rowray),
-            ptr<double>(m->rowd), ptr<int>(m->rowlab), parts, dc));
+            ptr<double>(m->rowd), ptr<int>(m->rowlab), parts, dc, &m->d_hctr->p));
         SVX_LAUNCHED();
         return SVX_OK;
     }
     SVX_CUDA(launch_pdl(k_walk_count<P, Fe>, kMarchBlocks, kMarchThreads, 0, s, 
         mp, m->cfg.sem_kind, m->cfg.num_classes, m->payload_d, m->npts_cap, ptr<double4>(m->ray),
-        ptr<int>(m->rcnt), parts, dc));
+        ptr<int>(m->rcnt), parts, dc, &m->d_hctr->p));
     SVX_LAUNCHED();
     size_t tmp = m->cubtmp.bytes;
     SVX_CUDA(cub::DeviceScan::ExclusiveSum(m->cubtmp.p, tmp, ptr<int>(m->rcnt),

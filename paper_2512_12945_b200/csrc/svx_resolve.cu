@@ -197,10 +197,8 @@ __global__ void __launch_bounds__(kSegThreads) k_seg(const int* __restrict__ tli
 // their background state (they stay active and are found again by the
 // retry) and clear the per-voxel frame counts.
 template <class TD, class TS>
-__global__ void k_cleanup(const int* __restrict__ tlist, VoxFrame* rec, TD* vt,
-                          TS* mean, TS* beta, int D, double trunc, double prior_beta,
-                          const FrameCtr* __restrict__ ctr) {
-    const long long n = (long long)ctr->n_touched;
+__global__ void k_cleanup(long long n, const int* __restrict__ tlist, VoxFrame* rec, TD* vt,
+                          TS* mean, TS* beta, int D, double trunc, double prior_beta) {
     for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n;
          e += (long long)gridDim.x * blockDim.x) {
         const int vid = tlist[e];
@@ -253,9 +251,9 @@ svx_status cleanup_t(svx_map* m, cudaStream_t s) {
     }
     const bool open = m->cfg.sem_kind == SVX_SEM_OPEN;
     k_cleanup<TD, TS><<<kPersistentBlocks, 256, 0, s>>>(
-        ptr<int>(m->tlist), ptr<VoxFrame>(m->vrec), ptr<TD>(m->vt),
+        (long long)m->h_ctr->n_touched, ptr<int>(m->tlist), ptr<VoxFrame>(m->vrec), ptr<TD>(m->vt),
         open ? ptr<TS>(m->s0) : nullptr, open ? ptr<TS>(m->s1) : nullptr, m->payload_d,
-        m->cfg.truncation, m->cfg.prior_beta, ptr<FrameCtr>(m->ctr));
+        m->cfg.truncation, m->cfg.prior_beta);
     SVX_LAUNCHED();
     return SVX_OK;
 }

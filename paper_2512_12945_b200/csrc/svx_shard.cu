@@ -319,6 +319,8 @@ svx_status shard_march(svx_map* m, const void* pts_in, int pts_f64, int64_t n, c
         p.kp = kp;
         p.nblocks0 = m->nblocks;
         FrameCtr* dc = ptr<FrameCtr>(m->ctr);
+        hc->p.epilogue = 0;   // explicit copies here, no graph epilogue
+        m->ctr_clean = false;
         SVX_CUDA(cudaMemcpyAsync(dc, hc, sizeof(FrameCtr), cudaMemcpyHostToDevice, s));
         SVX_TRY(launch_march(m, pts_f64, feats_f64, s));
         SVX_CUDA(cudaMemcpyAsync(hc, dc, sizeof(FrameCtr), cudaMemcpyDeviceToHost, s));
@@ -550,6 +552,8 @@ svx_status shard_apply(svx_map* m, const void* recv, const int64_t* recv_bytes, 
         hc->rows = (unsigned long long)R;
         hc->rows_alloc = (unsigned long long)R;
         FrameCtr* dc = ptr<FrameCtr>(m->ctr);
+        hc->p.epilogue = 0;   // explicit copies here, no graph epilogue
+        m->ctr_clean = false;
         SVX_CUDA(cudaMemcpyAsync(dc, hc, sizeof(FrameCtr), cudaMemcpyHostToDevice, s));
         SVX_TRY(launch_resolve(m, s));
         SVX_TRY(launch_segments(m, s));

@@ -394,7 +394,7 @@ __global__ void __launch_bounds__(256, 4) k_update_slots(UpdateArgs a, const Tou
 // shuffle bitonic sort on (point, lane) orders them, the sums run in that
 // order through shuffles.
 template <class TD, class TC>
-__global__ void __launch_bounds__(256) k_update_slots_long(UpdateArgs a,
+__device__ __forceinline__ void k_update_slots_long_body(UpdateArgs a,
                                                            unsigned long long* __restrict__ bslot,
                                                            const RowSlot* __restrict__ vslot, TD* vt,
                                                            TC* counts) {
@@ -463,6 +463,12 @@ __global__ void __launch_bounds__(256) k_update_slots_long(UpdateArgs a,
         if (closed && a.last_wins)
             for (int t = lane; t < a.C; t += 32) crow[t] = (TC)(t == last - 1 ? 1 : 0);
     }
+}
+
+template <class TD, class TC>
+__global__ void __launch_bounds__(256) k_update_slots_long(UpdateArgs a, unsigned long long* __restrict__ bslot, const RowSlot* __restrict__ vslot, TD* vt, TC* counts) {
+    k_update_slots_long_body(a, bslot, vslot, vt, counts);
+    frame_epilogue(a.ctr, a.ctr->p.epilogue, a.ctr->p.mirror);
 }
 
 // ---- warp helpers ---------------------------------------------------------------
@@ -608,7 +614,7 @@ __device__ __forceinline__ void finish_closed(const UpdateArgs& a, TD* vt, TC* c
 // ---- K5 long / huge (closed / geometry): one warp per voxel --------------------
 
 template <class TD, class TC>
-__global__ void __launch_bounds__(32 * kWarpsPerCta) k_update_long(UpdateArgs a, TD* vt,
+__device__ __forceinline__ void k_update_long_body(UpdateArgs a, TD* vt,
                                                                    TC* counts) {
     grid_dep_wait();
     __shared__ int sbuf[kWarpsPerCta][kSmemMax];
@@ -665,6 +671,12 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) k_update_long(UpdateArgs a,
         if (lane == 0) clear_voxel_frame(a, vid);
         __syncwarp();
     }
+}
+
+template <class TD, class TC>
+__global__ void __launch_bounds__(32 * kWarpsPerCta) k_update_long(UpdateArgs a, TD* vt, TC* counts) {
+    k_update_long_body(a, vt, counts);
+    frame_epilogue(a.ctr, a.ctr->p.epilogue, a.ctr->p.mirror);
 }
 
 // ---- K5 open set: one warp per voxel, lanes own feature dimensions ------------
@@ -799,7 +811,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) k_update_open(UpdateArgs a,
 }
 
 template <class TD, class TS, class Fe>
-__global__ void __launch_bounds__(32 * kWarpsPerCta) k_update_open_huge(UpdateArgs a, TD* vt,
+__device__ __forceinline__ void k_update_open_huge_body(UpdateArgs a, TD* vt,
                                                                         TS* mean, TS* beta) {
     grid_dep_wait();
     __shared__ int sbuf[kWarpsPerCta][kSmemMax];
@@ -821,6 +833,12 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) k_update_open_huge(UpdateAr
         open_voxel<TD, TS, Fe>(a, kp, pp, vt, mean, beta, feats, vid, a.rec[vid].cnt, sbuf[wib], bm,
                                true);
     }
+}
+
+template <class TD, class TS, class Fe>
+__global__ void __launch_bounds__(32 * kWarpsPerCta) k_update_open_huge(UpdateArgs a, TD* vt, TS* mean, TS* beta) {
+    k_update_open_huge_body<TD, TS, Fe>(a, vt, mean, beta);
+    frame_epilogue(a.ctr, a.ctr->p.epilogue, a.ctr->p.mirror);
 }
 
 __global__ void k_rehash(int64_t nblocks, const int4* __restrict__ bcoord, int4* table,
