@@ -194,6 +194,8 @@ svx_status svx_destroy(svx_map* m) {
     if (m->ev_in) cudaEventDestroy(m->ev_in);
     for (cudaGraphExec_t g : m->gexec)
         if (g) cudaGraphExecDestroy(g);
+    for (cudaGraph_t g : m->graph)
+        if (g) cudaGraphDestroy(g);
     if (m->gstream) cudaStreamDestroy(m->gstream);
     delete m;
     return SVX_OK;

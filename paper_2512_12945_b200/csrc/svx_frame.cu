@@ -235,6 +235,10 @@ static svx_status run_frame(svx_map* m, int pts_f64, int feats_f64, cudaStream_t
             cudaGraphExecDestroy(gexec);
             gexec = nullptr;
         }
+        if (m->graph[gm]) {
+            cudaGraphDestroy(m->graph[gm]);
+            m->graph[gm] = nullptr;
+        }
         SVX_CUDA(cudaStreamBeginCapture(m->gstream, cudaStreamCaptureModeThreadLocal));
         svx_status st = enqueue_frame(m, pts_f64, feats_f64, m->gstream);
         cudaGraph_t g = nullptr;
@@ -244,13 +248,38 @@ static svx_status run_frame(svx_map* m, int pts_f64, int feats_f64, cudaStream_t
             return st;
         }
         if (e != cudaSuccess) return fail(SVX_E_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+        // the frame's first kernel is the graph's only root
+        size_t nroots = 1;
+        cudaGraphNode_t root = nullptr;
+        e = cudaGraphGetRootNodes(g, &root, &nroots);
+        cudaGraphNodeType ty;
+        if (e != cudaSuccess || nroots != 1 || cudaGraphNodeGetType(root, &ty) != cudaSuccess ||
+            ty != cudaGraphNodeTypeKernel) {
+            cudaGraphDestroy(g);
+            return fail(SVX_E_INTERNAL, "frame graph: expected one root kernel node");
+        }
         e = cudaGraphInstantiate(&gexec, g, 0);
-        cudaGraphDestroy(g);
         if (e != cudaSuccess) {
+            cudaGraphDestroy(g);
             gexec = nullptr;
             return fail(SVX_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
         }
+        m->graph[gm] = g;
+        m->walk_node[gm] = root;
+        m->walk_nargs[gm] = m->first_nargs;
         m->gsig[gm] = sig;
+    }
+    {   // this frame's parameters into the first kernel's FrameParams argument
+        cudaKernelNodeParams kp;
+        SVX_CUDA(cudaGraphKernelNodeGetParams(m->walk_node[gm], &kp));
+        void* args[16];
+        const int na = m->walk_nargs[gm];
+        if (na < 1 || na > 16) return fail(SVX_E_INTERNAL, "frame graph: bad first-kernel arity");
+        for (int i = 0; i < na - 1; ++i) args[i] = kp.kernelParams[i];
+        args[na - 1] = &m->h_ctr->p;
+        kp.kernelParams = args;
+        kp.extra = nullptr;
+        SVX_CUDA(cudaGraphExecKernelNodeSetParams(gexec, m->walk_node[gm], &kp));
     }
     if (m->prof) {
         const size_t n = (size_t)kSpanKernels * 2 * kSpanMaxCtas * sizeof(unsigned long long);

@@ -240,6 +240,10 @@ struct svx_map {
     // captured frame graph (replayed while the layout is unchanged)
     cudaStream_t gstream = nullptr;
     cudaGraphExec_t gexec[2] = {};   // segment mode, slot mode
+    cudaGraph_t graph[2] = {};       // kept: its first-kernel node is updated per frame
+    cudaGraphNode_t walk_node[2] = {};
+    int walk_nargs[2] = {};          // parameters of that kernel (FrameParams is the last)
+    int first_nargs = 0;             // set by launch_march for the kernel it launched first
     unsigned long long gsig[2] = {};
     svx::DevBuf cubtmp;
     svx::DevBuf ctr;      // FrameCtr
@@ -350,15 +354,16 @@ __device__ __forceinline__ void snapshot_ctr(const FrameCtr* g, FrameCtr& s) {
 }
 
 // First kernel of a frame: counters from the device FrameCtr (reset state),
-// parameters from the host mirror (mapped memory, written by the host before
-// the launch); CTA 0 publishes the parameters to the device FrameCtr for the
-// later kernels.  All threads call it.
-__device__ __forceinline__ void load_frame_params(FrameCtr* ctr, FrameCtr& s, const FrameParams* hp) {
+// parameters from the kernel's own FrameParams argument (updated in the
+// instantiated graph before each launch, cudaGraphExecKernelNodeSetParams);
+// CTA 0 publishes them to the device FrameCtr for the later kernels.  All
+// threads call it.
+__device__ __forceinline__ void load_frame_params(FrameCtr* ctr, FrameCtr& s, const FrameParams& fpk) {
     snapshot_ctr(ctr, s);
-    const unsigned long long* src = reinterpret_cast<const unsigned long long*>(hp);
+    const unsigned long long* src = reinterpret_cast<const unsigned long long*>(&fpk);
     unsigned long long* dst = reinterpret_cast<unsigned long long*>(&s.p);
     static_assert(sizeof(FrameParams) % 8 == 0, "FrameParams must be a whole number of words");
-    for (int i = threadIdx.x; i < (int)(sizeof(FrameParams) / 8); i += blockDim.x) dst[i] = __ldcv(src + i);
+    for (int i = threadIdx.x; i < (int)(sizeof(FrameParams) / 8); i += blockDim.x) dst[i] = src[i];
     __syncthreads();
     if (blockIdx.x == 0) {
         unsigned long long* g = reinterpret_cast<unsigned long long*>(&ctr->p);
@@ -366,9 +371,9 @@ __device__ __forceinline__ void load_frame_params(FrameCtr* ctr, FrameCtr& s, co
     }
 }
 
-// Graph frames have no copy nodes.  The first kernel reads the frame's
-// parameters from the mapped host FrameCtr (load_frame_params) and publishes
-// them to the device FrameCtr; the last kernel's last CTA copies the device
+// Graph frames have no copy nodes.  The first kernel gets the frame's
+// parameters as its argument (load_frame_params) and publishes them to the
+// device FrameCtr; the last kernel's last CTA copies the device
 // FrameCtr to the mapped host FrameCtr (the host reads it after the frame's
 // event) and resets the device counters for the next frame.  The live pool
 // counters (nblocks, nvox) carry over.

@@ -264,10 +264,10 @@ __global__ void __launch_bounds__(kTileRays, 4) k_walk(MarchParams mp, int sem_k
                                                     int* __restrict__ rowlab,
                                                     MarchPartial* __restrict__ partials,
                                                     FrameCtr* __restrict__ ctr,
-                                                    const FrameParams* __restrict__ hp) {
+                                                    const __grid_constant__ FrameParams fpk) {
     grid_dep_wait();
     __shared__ FrameCtr s_ctr_;
-    load_frame_params(ctr, s_ctr_, hp);
+    load_frame_params(ctr, s_ctr_, fpk);
     KSpan _ks(&s_ctr_, ctr, kSpanWalk);
     using Scan = cub::BlockScan<int, kTileRays>;
     __shared__ typename Scan::TempStorage scan_tmp;
@@ -375,10 +375,10 @@ __global__ void __launch_bounds__(kMarchThreads) k_walk_count(MarchParams mp, in
                                                               int* __restrict__ rcnt,
                                                               MarchPartial* __restrict__ partials,
                                                               FrameCtr* __restrict__ ctr,
-                                                              const FrameParams* __restrict__ hp) {
+                                                              const __grid_constant__ FrameParams fpk) {
     grid_dep_wait();
     __shared__ FrameCtr s_ctr_;
-    load_frame_params(ctr, s_ctr_, hp);
+    load_frame_params(ctr, s_ctr_, fpk);
     KSpan _ks(&s_ctr_, ctr, kSpanWalk);
     const FrameParams& fp = s_ctr_.p;
     const long long n = fp.n;
@@ -522,13 +522,15 @@ svx_status march_t(svx_map* m, cudaStream_t s) {
         SVX_CUDA(launch_pdl(k_walk<P, Fe>, kMarchBlocks, kTileRays, smem, s, 
             mp, m->cfg.sem_kind, m->cfg.num_classes, m->payload_d, ptr<double4>(m->ray),
             ptr<int>(m->rcnt), ptr<unsigned long long>(m->rowkey), ptr<int>(m->rowray),
-            ptr<double>(m->rowd), ptr<int>(m->rowlab), parts, dc, &m->d_hctr->p));
+            ptr<double>(m->rowd), ptr<int>(m->rowlab), parts, dc, m->h_ctr->p));
+        m->first_nargs = 13;
         SVX_LAUNCHED();
         return SVX_OK;
     }
     SVX_CUDA(launch_pdl(k_walk_count<P, Fe>, kMarchBlocks, kMarchThreads, 0, s, 
         mp, m->cfg.sem_kind, m->cfg.num_classes, m->payload_d, m->npts_cap, ptr<double4>(m->ray),
-        ptr<int>(m->rcnt), parts, dc, &m->d_hctr->p));
+        ptr<int>(m->rcnt), parts, dc, m->h_ctr->p));
+    m->first_nargs = 10;
     SVX_LAUNCHED();
     size_t tmp = m->cubtmp.bytes;
     SVX_CUDA(cub::DeviceScan::ExclusiveSum(m->cubtmp.p, tmp, ptr<int>(m->rcnt),
