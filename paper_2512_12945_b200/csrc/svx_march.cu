@@ -142,39 +142,65 @@ struct OrOp {
     __device__ int operator()(int a, int b) const { return a | b; }
 };
 
+// Reduce the CTA's tallies (warp shuffles, one shared-memory round) and add
+// them to the frame counters: sums by RED, the row bounding box by atomic
+// min/max, error bits by atomic or.  No per-CTA partial records.
 template <int kThreads>
-__device__ __forceinline__ void write_partial(const Tally& t, MarchPartial* out) {
-    using RU = cub::BlockReduce<unsigned long long, kThreads>;
-    using RL = cub::BlockReduce<long long, kThreads>;
-    using RI = cub::BlockReduce<int, kThreads>;
-    __shared__ union {
-        typename RU::TempStorage u;
-        typename RL::TempStorage l;
-        typename RI::TempStorage i;
-    } tmp;
-    __shared__ MarchPartial res;
-    const unsigned long long uv[7] = {t.nonfinite, t.range, t.degenerate, t.bad_label,
-                                      t.used, t.band_hits, t.rows};
-    unsigned long long* ud[7] = {&res.nonfinite, &res.range, &res.degenerate, &res.bad_label,
-                                 &res.used, &res.band_hits, &res.rows};
-    for (int q = 0; q < 7; ++q) {
-        unsigned long long v = RU(tmp.u).Sum(uv[q]);
-        if (threadIdx.x == 0) *ud[q] = v;
-        __syncthreads();
+__device__ __forceinline__ void publish_tally(const Tally& t, FrameCtr* ctr) {
+    constexpr int kWarps = kThreads / 32;
+    __shared__ unsigned long long s_sum[kWarps][7];
+    __shared__ long long s_mn[kWarps][3], s_mx[kWarps][3];
+    __shared__ int s_err[kWarps];
+    unsigned long long v[7] = {t.nonfinite, t.range, t.degenerate, t.bad_label, t.used, t.band_hits, t.rows};
+    long long mn[3] = {t.mn[0], t.mn[1], t.mn[2]}, mx[3] = {t.mx[0], t.mx[1], t.mx[2]};
+    int e = t.errs;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+        for (int q = 0; q < 7; ++q) v[q] += __shfl_xor_sync(0xffffffffu, v[q], o);
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            mn[a] = min(mn[a], __shfl_xor_sync(0xffffffffu, mn[a], o));
+            mx[a] = max(mx[a], __shfl_xor_sync(0xffffffffu, mx[a], o));
+        }
+        e |= __shfl_xor_sync(0xffffffffu, e, o);
     }
-    for (int a = 0; a < 3; ++a) {
-        long long v = RL(tmp.l).Reduce(t.mn[a], MinOp());
-        if (threadIdx.x == 0) res.bbox_min[a] = v;
-        __syncthreads();
-        v = RL(tmp.l).Reduce(t.mx[a], MaxOp());
-        if (threadIdx.x == 0) res.bbox_max[a] = v;
-        __syncthreads();
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+        for (int q = 0; q < 7; ++q) s_sum[w][q] = v[q];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            s_mn[w][a] = mn[a];
+            s_mx[w][a] = mx[a];
+        }
+        s_err[w] = e;
     }
-    int e = RI(tmp.i).Reduce(t.errs, OrOp());
+    __syncthreads();
     if (threadIdx.x == 0) {
-        res.errs = e;
-        res.pad = 0;
-        *out = res;
+        for (int x = 1; x < kWarps; ++x) {
+            for (int q = 0; q < 7; ++q) v[q] += s_sum[x][q];
+            for (int a = 0; a < 3; ++a) {
+                mn[a] = min(mn[a], s_mn[x][a]);
+                mx[a] = max(mx[a], s_mx[x][a]);
+            }
+            e |= s_err[x];
+        }
+        unsigned long long* dst[7] = {&ctr->nonfinite, &ctr->range, &ctr->degenerate, &ctr->bad_label,
+                                      &ctr->used, &ctr->band_hits, &ctr->rows};
+        for (int q = 0; q < 7; ++q)
+            if (v[q]) atomicAdd(dst[q], v[q]);
+        if (v[6]) {
+            for (int a = 0; a < 3; ++a) {
+                atomicMin(&ctr->bbox_min[a], mn[a]);
+                atomicMax(&ctr->bbox_max[a], mx[a]);
+            }
+        }
+        if (e) {
+            if (e & 1) atomicOr(&ctr->err_budget, 1);
+            if (e & 2) atomicOr(&ctr->err_pack, 1);
+            if (e & 8) atomicOr(&ctr->err_rows, 1);
+        }
     }
 }
 
@@ -226,22 +252,20 @@ __device__ __forceinline__ bool prepare_ray(long long i, const FrameParams& fp, 
     return keep;
 }
 
-template <int kThreads>
-__device__ void gate_body(const MarchPartial* __restrict__ parts, int nparts, FrameCtr* ctr);
+__device__ void gate_body(FrameCtr* ctr);
 
-// Every CTA of a walk publishes its partial; the last one to finish runs the
-// gate over all of them.
+// Every CTA of a walk adds its tallies; the last one to finish runs the gate.
 template <int kThreads>
-__device__ __forceinline__ void finish_walk(const Tally& t, MarchPartial* partials, FrameCtr* ctr) {
-    write_partial<kThreads>(t, partials + blockIdx.x);
+__device__ __forceinline__ void finish_walk(const Tally& t, MarchPartial*, FrameCtr* ctr) {
+    publish_tally<kThreads>(t, ctr);
     __shared__ bool s_last;
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) s_last = atomicAdd(&ctr->walk_done, 1u) == gridDim.x - 1;
     __syncthreads();
-    if (s_last) {
+    if (s_last && threadIdx.x == 0) {
         __threadfence();
-        gate_body<kThreads>(partials, gridDim.x, ctr);
+        gate_body(ctr);
     }
 }
 
@@ -292,12 +316,17 @@ __global__ void __launch_bounds__(kTileRays, 4) k_walk(MarchParams mp, int sem_k
         if (i < n) {
             double4 r;
             if (prepare_ray<P, Fe>(i, fp, mp.max_range, sem_kind, num_classes, D, t, r)) {
+                long long f0 = 0, f1 = 0, f2 = 0, l0 = 0, l1 = 0, l2 = 0;
+                int nk = 0;
                 long long emitted = dda_walk(ox, oy, oz, r.x, r.y, r.z, r.w, mp,
                     [&](long long ci, long long cj, long long ck) {
                         if (!row_kept(ci, cj, ck, ox, oy, oz, r, mp)) return;
                         t.rows += 1;
-                        t.mn[0] = min(t.mn[0], ci); t.mn[1] = min(t.mn[1], cj); t.mn[2] = min(t.mn[2], ck);
-                        t.mx[0] = max(t.mx[0], ci); t.mx[1] = max(t.mx[1], cj); t.mx[2] = max(t.mx[2], ck);
+                        // cells are monotonic per axis along a ray: its first and
+                        // last kept cells bound the band
+                        if (nk == 0) { f0 = ci; f1 = cj; f2 = ck; }
+                        l0 = ci; l1 = cj; l2 = ck;
+                        ++nk;
                         if (rows >= maxrows) {
                             t.errs |= 8;
                             return;
@@ -314,6 +343,11 @@ __global__ void __launch_bounds__(kTileRays, 4) k_walk(MarchParams mp, int sem_k
                     rows = 0;
                 } else {
                     t.band_hits += (unsigned long long)emitted;
+                }
+                if (nk) {
+                    t.mn[0] = min(t.mn[0], min(f0, l0)); t.mx[0] = max(t.mx[0], max(f0, l0));
+                    t.mn[1] = min(t.mn[1], min(f1, l1)); t.mx[1] = max(t.mx[1], max(f1, l1));
+                    t.mn[2] = min(t.mn[2], min(f2, l2)); t.mx[2] = max(t.mx[2], max(f2, l2));
                 }
             }
             ray[i] = r;
@@ -447,64 +481,22 @@ __global__ void __launch_bounds__(kMarchThreads) k_walk_write(MarchParams mp,
     }
 }
 
-// Reduce the march partials and decide, once per frame on the device, whether
-// the frame may mutate the map -- the reference's checks before any
-// allocation (_core.pyx:661-712, :386-387) plus the dense row capacity.  The
-// host reports the reason after the frame.
-// Run by the last CTA of the walk to finish (no separate launch).
-template <int kThreads>
-__device__ void gate_body(const MarchPartial* __restrict__ parts, int nparts, FrameCtr* ctr) {
-    using RU = cub::BlockReduce<unsigned long long, kThreads>;
-    using RL = cub::BlockReduce<long long, kThreads>;
-    __shared__ union {
-        typename RU::TempStorage u;
-        typename RL::TempStorage l;
-    } tmp;
-    unsigned long long v[7] = {0, 0, 0, 0, 0, 0, 0};
-    long long mn[3] = {LLONG_MAX, LLONG_MAX, LLONG_MAX}, mx[3] = {LLONG_MIN, LLONG_MIN, LLONG_MIN};
-    int errs = 0;
-    for (int b = threadIdx.x; b < nparts; b += kThreads) {
-        const MarchPartial& p = parts[b];
-        v[0] += p.nonfinite; v[1] += p.range; v[2] += p.degenerate; v[3] += p.bad_label;
-        v[4] += p.used; v[5] += p.band_hits; v[6] += p.rows;
-        for (int a = 0; a < 3; ++a) {
-            mn[a] = min(mn[a], p.bbox_min[a]);
-            mx[a] = max(mx[a], p.bbox_max[a]);
-        }
-        errs |= p.errs;
-    }
-    unsigned long long* dst[7] = {&ctr->nonfinite, &ctr->range, &ctr->degenerate, &ctr->bad_label,
-                                  &ctr->used, &ctr->band_hits, &ctr->rows};
-    for (int q = 0; q < 7; ++q) {
-        unsigned long long s = RU(tmp.u).Sum(v[q]);
-        if (threadIdx.x == 0) *dst[q] = s;
-        __syncthreads();
-    }
-    for (int a = 0; a < 3; ++a) {
-        long long s = RL(tmp.l).Reduce(mn[a], MinOp());
-        if (threadIdx.x == 0) ctr->bbox_min[a] = s;
-        __syncthreads();
-        s = RL(tmp.l).Reduce(mx[a], MaxOp());
-        if (threadIdx.x == 0) ctr->bbox_max[a] = s;
-        __syncthreads();
-    }
-    errs = __reduce_or_sync(0xffffffffu, (unsigned)errs);
-    __shared__ int s_err[kThreads / 32];
-    if ((threadIdx.x & 31) == 0) s_err[threadIdx.x >> 5] = errs;
-    __syncthreads();
-    if (threadIdx.x != 0) return;
-    for (int w = 1; w < kThreads / 32; ++w) errs |= s_err[w];
-    if (errs & 1) ctr->err_budget = 1;
-    if (errs & 2) ctr->err_pack = 1;
-    if (errs & 8) ctr->err_rows = 1;
-    int ab = ctr->err_budget | ctr->err_pack | ctr->err_rows;
-    if (ctr->rows > ctr->p.rcap) {
+// Decide, once per frame on the device, whether the frame may mutate the map
+// -- the reference's checks before any allocation (_core.pyx:661-712,
+// :386-387) plus the dense row capacity.  Run by one thread of the last walk
+// CTA, when every CTA's tallies are in the frame counters.  The host reports
+// the reason after the frame.
+__device__ void gate_body(FrameCtr* ctr) {
+    volatile FrameCtr* c = ctr;
+    int ab = c->err_budget | c->err_pack | c->err_rows;
+    const unsigned long long rows = c->rows;
+    if (rows > c->p.rcap) {
         ctr->err_cap = 1;
         ab = 1;
     }
-    if (ctr->rows) {
+    if (rows) {
         for (int a = 0; a < 3; ++a) {
-            long long lo = ctr->bbox_min[a], hi = ctr->bbox_max[a];
+            const long long lo = c->bbox_min[a], hi = c->bbox_max[a];
             if (hi - lo >= (1LL << kPackBits)) ab = 1;
             if (llabs(lo) >= kCoordLimit || llabs(hi) >= kCoordLimit) ab = 1;
         }
