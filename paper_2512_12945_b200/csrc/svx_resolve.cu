@@ -39,8 +39,7 @@ __global__ void __launch_bounds__(kResolveThreads) k_resolve(
     const unsigned long long* __restrict__ rowkey, const int* __restrict__ rowray,
     const double* __restrict__ rowd, const int* __restrict__ rowlab, rt::ResolveArgs ra) {
     grid_dep_wait();
-    using Scan = cub::BlockScan<int, kResolveThreads>;
-    __shared__ typename Scan::TempStorage scan_tmp;
+    __shared__ int s_warp[kResolveThreads / 32];
     __shared__ unsigned long long s_base;
     __shared__ unsigned s_tcount;
     FrameCtr* ctr = ra.ctr;
@@ -74,7 +73,7 @@ __global__ void __launch_bounds__(kResolveThreads) k_resolve(
             rsl.label = rowlab[t];
             rsl.d = rowd[t];
         }
-        rt::resolve_step<kResolveThreads>(ra, valid, key, rsl, t, scan_tmp, s_base, s_tcount);
+        rt::resolve_step<kResolveThreads>(ra, valid, key, rsl, t, s_warp, s_base, s_tcount);
         __syncthreads();
     }
     if (ra.slots && threadIdx.x == 0) {   // this CTA's touched region

@@ -101,6 +101,27 @@ __device__ int leaf_find_or_insert(int4* table, long long mask, int a, int b, in
     }
 }
 
+// CTA-wide exclusive rank of a predicate (warp ballots + one shared-memory
+// round); every thread gets the total.  s_warp holds kThreads/32 counts and
+// must not be rewritten before every thread has passed the next barrier.
+template <int kThreads>
+__device__ __forceinline__ int cta_rank(bool pred, int& total, int* s_warp) {
+    constexpr int kWarps = kThreads / 32;
+    const unsigned b = __ballot_sync(0xffffffffu, pred);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) s_warp[w] = __popc(b);
+    __syncthreads();
+    int off = 0, tot = 0;
+#pragma unroll
+    for (int i = 0; i < kWarps; ++i) {
+        const int c = s_warp[i];
+        off += i < w ? c : 0;
+        tot += c;
+    }
+    total = tot;
+    return off + __popc(b & ((1u << lane) - 1u));
+}
+
 struct ResolveArgs {
     int4* table;
     int4* bcoord;
@@ -136,9 +157,8 @@ template <int kThreads>
 __device__ __forceinline__ void resolve_step(const ResolveArgs& ra, bool valid,
                                              unsigned long long key, const RowSlot& rsl,
                                              long long t,
-                                             typename cub::BlockScan<int, kThreads>::TempStorage& scan_tmp,
-                                             unsigned long long& s_base, unsigned& s_tcount) {
-    using Scan = cub::BlockScan<int, kThreads>;
+                                             int* s_warp, unsigned long long& s_base,
+                                             unsigned& s_tcount) {
     const KeyPack& kp = ra.kp;
     const long long hmask = ra.hmask, bcap = ra.bcap, vcap = ra.vcap, nblocks0 = ra.nblocks0;
     const int frame = ra.frame;
@@ -189,10 +209,14 @@ __device__ __forceinline__ void resolve_step(const ResolveArgs& ra, bool valid,
             // lost the race for this slot: look at it again
         }
     }
-    int rank, cnt;
-    Scan(scan_tmp).ExclusiveSum(lstate == 1 ? 1 : 0, rank, cnt);
-    if (threadIdx.x == 0 && cnt) s_base = atomicAdd(&ctr->nblocks, (unsigned long long)cnt);
-    __syncthreads();
+    int rank = 0, cnt = 0;
+    // leaf claims are rare: the rank/publish round only runs when this step has any
+    const bool lclaims = __syncthreads_or(lstate == 1);
+    if (lclaims) {
+        rank = cta_rank<kThreads>(lstate == 1, cnt, s_warp);
+        if (threadIdx.x == 0) s_base = atomicAdd(&ctr->nblocks, (unsigned long long)cnt);
+        __syncthreads();
+    }
     if (lstate == 1) {
         const long long nid = (long long)s_base + rank;
         if (nid >= bcap) {
@@ -204,7 +228,7 @@ __device__ __forceinline__ void resolve_step(const ResolveArgs& ra, bool valid,
             id = (int)nid;
         }
     }
-    __syncthreads();
+    if (lclaims) __syncthreads();   // this step's claims are published before anyone waits
     if (lstate == 2) {   // another CTA is publishing this slot (maybe another key)
         volatile int* vw = &table[lpos].w;
         int v = *vw;
@@ -245,9 +269,12 @@ __device__ __forceinline__ void resolve_step(const ResolveArgs& ra, bool valid,
             }
         }
     }
-    Scan(scan_tmp).ExclusiveSum(vstate == 1 ? 1 : 0, rank, cnt);
-    if (threadIdx.x == 0 && cnt) s_base = atomicAdd(&ctr->nvox, (unsigned long long)cnt);
-    __syncthreads();
+    const bool vclaims = __syncthreads_or(vstate == 1);
+    if (vclaims) {
+        rank = cta_rank<kThreads>(vstate == 1, cnt, s_warp);
+        if (threadIdx.x == 0) s_base = atomicAdd(&ctr->nvox, (unsigned long long)cnt);
+        __syncthreads();
+    }
     bool created = false;
     if (vstate == 1) {
         const long long nv = (long long)s_base + rank;
@@ -263,7 +290,7 @@ __device__ __forceinline__ void resolve_step(const ResolveArgs& ra, bool valid,
             created = true;
         }
     }
-    __syncthreads();
+    if (vclaims) __syncthreads();
     if (vstate == 2) {
         volatile unsigned* vsp = reinterpret_cast<volatile unsigned*>(sp);   // low half
         const int pending = slots ? -1 : -2;
@@ -287,7 +314,7 @@ __device__ __forceinline__ void resolve_step(const ResolveArgs& ra, bool valid,
         cbase = c & ~kNewBit;
         first = cbase == 0u;
     }
-    Scan(scan_tmp).ExclusiveSum(first ? 1 : 0, rank, cnt);
+    rank = cta_rank<kThreads>(first, cnt, s_warp);
     if (slots) {
         if (first) {
             TouchEntry te;
