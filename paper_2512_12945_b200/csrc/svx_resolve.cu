@@ -66,12 +66,13 @@ __global__ void __launch_bounds__(kResolveThreads) k_resolve(
     for (long long tile = blockIdx.x; tile * kResolveThreads < total; tile += gridDim.x) {
         const long long t = tile * kResolveThreads + threadIdx.x;
         const bool valid = t < total;
-        const unsigned long long key = valid ? rowkey[t] : kKeyEmpty;
+        // row arrays are dead after this read: evict-first
+        const unsigned long long key = valid ? __ldcs(rowkey + t) : kKeyEmpty;
         RowSlot rsl{0, 0, 0.0};
         if (valid && ra.slots) {
-            rsl.point = rowray[t];
-            rsl.label = rowlab[t];
-            rsl.d = rowd[t];
+            rsl.point = __ldcs(rowray + t);
+            rsl.label = __ldcs(rowlab + t);
+            rsl.d = __ldcs(rowd + t);
         }
         rt::resolve_step<kResolveThreads>(ra, valid, key, rsl, t, s_warp, s_base, s_tcount);
         __syncthreads();
@@ -273,6 +274,11 @@ rt::ResolveArgs resolve_args(svx_map* m) {
     ra.vslot = ptr<RowSlot>(m->vslot);
     ra.rowvid = ptr<int>(m->rowvid);
     ra.ctr = ptr<FrameCtr>(m->ctr);
+    ra.vt = ptr<const char>(m->vt);
+    ra.vt_bytes = (int)(2 * tsdf_elem(m));
+    ra.counts = m->cfg.sem_kind == SVX_SEM_CLOSED ? ptr<const char>(m->s0) : nullptr;
+    ra.count_bytes = (int)sem_elem(m);
+    ra.ncounts = m->cfg.sem_kind == SVX_SEM_CLOSED ? m->payload_d : 0;
     return ra;
 }
 

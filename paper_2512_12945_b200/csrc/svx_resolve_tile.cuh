@@ -138,6 +138,13 @@ struct ResolveArgs {
     KeyPack kp;
     long long hmask, bcap, vcap, nblocks0;
     long long region;            // slot mode: touched entries per CTA region
+    // slot mode: the first toucher prefetches the voxel's TSDF pair and its
+    // own label's count into L2 for the update kernel (no registers held)
+    const char* vt;
+    int vt_bytes;                // bytes per voxel in vt
+    const char* counts;
+    int count_bytes;             // bytes per count
+    int ncounts;                 // counts per voxel (C), 0 = none
     int frame;
     bool slots;
 };
@@ -317,6 +324,14 @@ __device__ __forceinline__ void resolve_step(const ResolveArgs& ra, bool valid,
     rank = cta_rank<kThreads>(first, cnt, s_warp);
     if (slots) {
         if (first) {
+            if (vid >= 0) {
+                const char* pv = ra.vt + (long long)vid * ra.vt_bytes;
+                asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(pv));
+                if (ra.ncounts && rsl.label >= 1) {
+                    const char* pc = ra.counts + ((long long)vid * ra.ncounts + (rsl.label - 1)) * ra.count_bytes;
+                    asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(pc));
+                }
+            }
             TouchEntry te;
             te.vid = vid >= 0 ? ((unsigned)vid | (created ? kNewBit : 0u)) : 0xFFFFFFFFu;
             te.bidx = (unsigned)(sp - bslot);

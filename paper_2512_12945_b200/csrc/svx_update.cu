@@ -274,7 +274,7 @@ __device__ __forceinline__ void fold_row(const UpdateArgs& a, double d, int lab,
 }
 
 __device__ __forceinline__ RowSlot ld_slot16(const RowSlot* p) {
-    const int4 v = *reinterpret_cast<const int4*>(p);
+    const int4 v = __ldcs(reinterpret_cast<const int4*>(p));   // dead after this frame: evict-first
     RowSlot r;
     r.point = v.x;
     r.label = v.y;
@@ -302,7 +302,10 @@ __global__ void __launch_bounds__(256, 4) k_update_slots(UpdateArgs a, const Tou
     const unsigned cnt = rcount[blockIdx.x];
     const TouchEntry* te = tent + (long long)blockIdx.x * region;
     for (unsigned e = threadIdx.x; e < cnt; e += blockDim.x) {
-        const TouchEntry en = te[e];
+        const unsigned long long raw = __ldcs(reinterpret_cast<const unsigned long long*>(te + e));
+        TouchEntry en;
+        en.vid = (unsigned)raw;
+        en.bidx = (unsigned)(raw >> 32);
         const int vid = (int)(en.vid & ~kNewBit);
         const unsigned c = (unsigned)(bslot[en.bidx] >> 32) | (en.vid & kNewBit);
         P2 st = reinterpret_cast<const P2*>(vt)[vid];
