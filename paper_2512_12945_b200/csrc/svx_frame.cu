@@ -289,7 +289,7 @@ static svx_status run_frame(svx_map* m, int pts_f64, int feats_f64, cudaStream_t
     // the graph was captured on the map's own stream; it runs on the caller's
     if (g_trace_host) g_t_launch0 = now_us();
     SVX_CUDA(cudaGraphLaunch(gexec, s));
-    count_launch(gm ? 3 : 6);
+    count_launch(gm ? 4 : 6);
     SVX_CUDA(cudaEventRecord(m->ev1, s));
     if (g_trace_host) g_t_launch1 = now_us();
     SVX_CUDA(cudaEventSynchronize(m->ev1));
@@ -388,7 +388,6 @@ svx_status recover_slots(svx_map* m, int64_t nblocks0, cudaStream_t s) {
 // rows per voxel), open-set and carving maps use segments.
 int choose_slots(const svx_map* m) {
     if (m->cfg.sem_kind == SVX_SEM_OPEN || m->cfg.space_carving || m->maxrows <= 0) return 0;
-    if (m->frame_n >= (1LL << 27)) return 0;   // slot sort keys pack the point index in 27 bits
     if (m->mode_pref == SVX_UPDATE_SEGMENTS) return 0;
     if (m->mode_pref == SVX_UPDATE_SLOTS) return m->frame_retry_segments ? 0 : 1;
     if (m->slot_hold > 0) return 0;
@@ -454,7 +453,6 @@ svx_status integrate_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n
                              &feats));
     }
     init_row_space(m, n);
-    m->frame_n = n;
     KeyPack kp = default_key_pack(m, pp);
     FrameCtr* hc = m->h_ctr;
     // counts before this frame (stamps, report); m->nblocks / m->nvox stay the

@@ -227,7 +227,6 @@ struct svx_map {
     int64_t last_rows = 0, last_touched = 0;   // previous frame's rows and touched voxels
     int frame_slots = 0;    // mode of the attempt being run
     int frame_retry_segments = 0;   // this frame overflowed its slots: re-run with segments
-    int64_t frame_n = 0;            // points of the frame being integrated
     int64_t frames = 0;
     unsigned seq = 0;   // frame launches so far (attempts included)
     // per-frame scratch

@@ -107,6 +107,7 @@ struct UpdateArgs {
     const double4* ray;
     int* longlist;
     int* hugelist;
+    TouchEntry* hugelist2;   // slot mode: voxels of 5..16 rows
     unsigned* bitmap;     // kHugeWarps * bm_words
     long long bm_words;
     double h, trunc;
@@ -281,40 +282,8 @@ __device__ __forceinline__ RowSlot ld_slot16(const RowSlot* p) {
     return r;
 }
 
-template <int N, class TC>
-__device__ __forceinline__ void sorted_fold(const UpdateArgs& a, const RowSlot* sl, unsigned k,
-                                            TC* crow, bool closed, RowAcc& acc) {
-    unsigned key[N];
-#pragma unroll
-    for (int j = 0; j < N; ++j)
-        key[j] = (unsigned)j < k ? (((unsigned)sl[j * kSlotStride].point << 4) | (unsigned)j) : 0xFFFFFFFFu;
-#pragma unroll
-    for (int kk = 2; kk <= N; kk <<= 1) {
-#pragma unroll
-        for (int jj = kk >> 1; jj > 0; jj >>= 1) {
-#pragma unroll
-            for (int i = 0; i < N; ++i) {
-                const int l = i ^ jj;
-                if (l > i) {
-                    const unsigned x = key[i], y = key[l];
-                    const bool up = (i & kk) == 0;
-                    key[i] = up ? min(x, y) : max(x, y);
-                    key[l] = up ? max(x, y) : min(x, y);
-                }
-            }
-        }
-    }
-#pragma unroll
-    for (int j = 0; j < N; ++j) {
-        if ((unsigned)j < k) {
-            const RowSlot r = ld_slot16(sl + (int)(key[j] & 15u) * kSlotStride);
-            fold_row<TC>(a, r.d, r.label, crow, closed, acc);
-        }
-    }
-}
-
 template <class TD, class TC>
-__device__ __forceinline__ void k_update_slots_body(UpdateArgs a, const TouchEntry* __restrict__ tent,
+__global__ void __launch_bounds__(256, 4) k_update_slots(UpdateArgs a, const TouchEntry* __restrict__ tent,
                                                       const unsigned* __restrict__ rcount,
                                                       unsigned long long* __restrict__ bslot,
                                                       const RowSlot* __restrict__ vslot, TD* vt,
@@ -342,14 +311,43 @@ __device__ __forceinline__ void k_update_slots_body(UpdateArgs a, const TouchEnt
         P2 st = reinterpret_cast<const P2*>(vt)[vid];
         const RowSlot* sl = vslot + (long long)vid * kSlots * kSlotStride;
         const unsigned k = c & ~kNewBit;
+        if (k > 8u) {   // 9..16 rows (rare): one warp per voxel in k_update_slots_long
+            a.hugelist2[warp_ticket(&ctr->n_long)] = en;
+            continue;
+        }
         TC* crow = counts + (long long)vid * a.C;
         RowAcc acc;
         if (k > 4u) {
-            // 5..16 rows: sort (point << 4 | slot) keys in registers (points
-            // < 2^27 in slot mode), then fold the rows in that order (their
-            // slots were just read: L1/L2 hits)
-            if (k <= 8u) sorted_fold<8, TC>(a, sl, k, crow, closed, acc);
-            else sorted_fold<16, TC>(a, sl, k, crow, closed, acc);
+            // 5..8 rows: sort (point, slot) keys in registers, then fold the rows
+            // in that order (their slots were just read: L1/L2 hits)
+            unsigned long long key[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                key[j] = (unsigned)j < k ? (((unsigned long long)(unsigned)sl[j * kSlotStride].point << 3) | (unsigned)j)
+                                         : ~0ULL;
+#pragma unroll
+            for (int kk = 2; kk <= 8; kk <<= 1) {
+#pragma unroll
+                for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const int l = i ^ jj;
+                        if (l > i) {
+                            const unsigned long long x = key[i], y = key[l];
+                            const bool up = (i & kk) == 0;
+                            key[i] = up ? (x < y ? x : y) : (x > y ? x : y);
+                            key[l] = up ? (x > y ? x : y) : (x < y ? x : y);
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                if ((unsigned)j < k) {
+                    const RowSlot r = ld_slot16(sl + (int)(key[j] & 7u) * kSlotStride);
+                    fold_row<TC>(a, r.d, r.label, crow, closed, acc);
+                }
+            }
         } else {
         // rows in registers; only slots that exist are read (no partial-sector reads)
         RowSlot q0 = ld_slot16(sl), q1, q2, q3;
@@ -395,14 +393,84 @@ __device__ __forceinline__ void k_update_slots_body(UpdateArgs a, const TouchEnt
     }
 }
 
-// The slot-mode frame's last kernel: its last CTA publishes the counters.
+// Slot-mode voxels of 9..16 rows: one warp per voxel; lanes own rows, a
+// shuffle bitonic sort on (point, lane) orders them, the sums run in that
+// order through shuffles.
 template <class TD, class TC>
-__global__ void __launch_bounds__(256, 4) k_update_slots(UpdateArgs a, const TouchEntry* __restrict__ tent,
-                                                         const unsigned* __restrict__ rcount,
-                                                         unsigned long long* __restrict__ bslot,
-                                                         const RowSlot* __restrict__ vslot, TD* vt,
-                                                         TC* counts) {
-    k_update_slots_body<TD, TC>(a, tent, rcount, bslot, vslot, vt, counts);
+__device__ __forceinline__ void k_update_slots_long_body(UpdateArgs a,
+                                                           unsigned long long* __restrict__ bslot,
+                                                           const RowSlot* __restrict__ vslot, TD* vt,
+                                                           TC* counts) {
+    grid_dep_wait();
+    FrameCtr* ctr = a.ctr;
+    KSpan _ks(ctr, kSpanUpdateB);
+    __shared__ FrameCtr s_ctr_;
+    snapshot_ctr(ctr, s_ctr_);
+    const FrameCtr* cv = &s_ctr_;
+    if (cv->abort | cv->err_cap | cv->err_slots) return;
+    const bool closed = a.sem_kind == SVX_SEM_CLOSED;
+    const int lane = threadIdx.x & 31;
+    using P2 = typename Pair<TD>::type;
+    const long long L = (long long)cv->n_long;
+    for (long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < L;
+         w += ((long long)gridDim.x * blockDim.x) >> 5) {
+        const TouchEntry en = a.hugelist2[w];
+        const int vid = (int)(en.vid & ~kNewBit);
+        const unsigned k = (unsigned)(bslot[en.bidx] >> 32);
+        RowSlot r{0x7fffffff, 0, 0.0};
+        if ((unsigned)lane < k) r = ld_slot16(vslot + ((long long)vid * kSlots + lane) * kSlotStride);
+        unsigned long long key = ((unsigned long long)(unsigned)r.point << 32) | (unsigned)lane;
+#pragma unroll
+        for (int kk = 2; kk <= 32; kk <<= 1) {
+#pragma unroll
+            for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+                const unsigned long long o = __shfl_xor_sync(0xffffffffu, key, jj);
+                const bool up = (lane & kk) == 0;
+                const bool lower = (lane & jj) == 0;
+                key = (lower == up) ? (key < o ? key : o) : (key > o ? key : o);
+            }
+        }
+        const int src = (int)(key & 31u);   // lane holding the lane-th smallest row
+        const double d = __shfl_sync(0xffffffffu, r.d, src);
+        const int lab = __shfl_sync(0xffffffffu, r.label, src);
+        const double w_row = (a.wfn == 1) ? (d >= 0.0 ? 1.0 : (a.trunc + d) / a.trunc) : 1.0;
+        RowAcc acc;
+        for (unsigned q = 0; q < k; ++q) {
+            const double wq = __shfl_sync(0xffffffffu, w_row, q);
+            const double dq = __shfl_sync(0xffffffffu, d, q);
+            acc.sw += wq;
+            acc.swd += wq * dq;
+            acc.mind = dq < acc.mind ? dq : acc.mind;
+            acc.maxd = dq > acc.maxd ? dq : acc.maxd;
+        }
+        TC* crow = counts + (long long)vid * a.C;
+        if (closed && !a.last_wins && (unsigned)lane < k) atomicAdd(&crow[lab - 1], (TC)1);
+        const int last = __shfl_sync(0xffffffffu, lab, k - 1);
+        if (lane == 0) {
+            P2 st = reinterpret_cast<const P2*>(vt)[vid];
+            if (en.vid & kNewBit) {
+                st.x = (TD)a.trunc;
+                st.y = (TD)0;
+            }
+            const double w_old = (double)st.y, d_old = (double)st.x;
+            const double w_new = w_old + acc.sw;
+            double d_new = w_new > 0.0 ? (w_old * d_old + acc.swd) / w_new : d_old;
+            if ((acc.mind == acc.maxd) && (w_old == 0.0 || equals_stored<TD>(st.x, acc.mind)))
+                d_new = acc.mind;
+            P2 out;
+            out.x = (TD)d_new;
+            out.y = (TD)w_new;
+            reinterpret_cast<P2*>(vt)[vid] = out;
+            bslot[en.bidx] = (unsigned long long)(unsigned)vid;
+        }
+        if (closed && a.last_wins)
+            for (int t = lane; t < a.C; t += 32) crow[t] = (TC)(t == last - 1 ? 1 : 0);
+    }
+}
+
+template <class TD, class TC>
+__global__ void __launch_bounds__(256) k_update_slots_long(UpdateArgs a, unsigned long long* __restrict__ bslot, const RowSlot* __restrict__ vslot, TD* vt, TC* counts) {
+    k_update_slots_long_body(a, bslot, vslot, vt, counts);
     frame_epilogue(a.ctr, a.ctr->p.epilogue, a.ctr->p.mirror);
 }
 
@@ -806,6 +874,7 @@ UpdateArgs make_args(svx_map* m) {
     a.ray = ptr<double4>(m->ray);
     a.longlist = ptr<int>(m->longlist);
     a.hugelist = ptr<int>(m->longlist) + m->ucap;
+    a.hugelist2 = ptr<TouchEntry>(m->longlist);
     a.bitmap = ptr<unsigned>(m->bitmap);
     a.bm_words = (m->npts_cap + 31) / 32 + 1;
     a.h = m->cfg.voxel_size;
@@ -869,6 +938,10 @@ template <class TD, class TC>
 svx_status slots_t(svx_map* m, cudaStream_t s) {
     SVX_CUDA(launch_pdl(k_update_slots<TD, TC>, kPersistentBlocks, 256, 0, s, make_args(m),
                         ptr<TouchEntry>(m->tlist), ptr<unsigned>(m->rcount),
+                        ptr<unsigned long long>(m->bslot), ptr<RowSlot>(m->vslot), ptr<TD>(m->vt),
+                        ptr<TC>(m->s0)));
+    SVX_LAUNCHED();
+    SVX_CUDA(launch_pdl(k_update_slots_long<TD, TC>, 148 * 2, 256, 0, s, make_args(m),
                         ptr<unsigned long long>(m->bslot), ptr<RowSlot>(m->vslot), ptr<TD>(m->vt),
                         ptr<TC>(m->s0)));
     SVX_LAUNCHED();
