@@ -151,22 +151,32 @@ def frame_bytes(used, touched, kind, C=0, D=0):
     return used * (12 + P) + 2 * touched * S
 
 
-def stage_bytes(stage, rep, kind, C, D, tsdf_elem):
-    """Algorithmic bytes one launch of a stage must move (DESIGN.md table)."""
+def stage_bytes(stage, rep, kind, C, D, tsdf_elem, slots=False):
+    """Algorithmic bytes one launch of a stage must move.
+    Voxel state is counted at the SURVEY 8(d) fp32 model (S = 8 + 4C closed,
+    8 + 8D open), read + write; hash probes, claims and frame scratch beyond
+    the rows and slots are overhead, not counted."""
     n, used, R, U = rep.points_in, rep.points_used, rep.band_hits, rep.touched_voxels
     P = 4 if kind == "closed" else (4 * D if kind == "open" else 0)
-    S = 2 * tsdf_elem + (4 * C if kind == "closed" else (8 * D if kind == "open" else 0))
+    S = 8 + (4 * C if kind == "closed" else (8 * D if kind == "open" else 0))
+    if slots:   # slot mode: rows {key 8, point 4, d 8, label 4}, slots {point, label, d} 16 B
+        return {
+            "walk": n * (12 + P) + R * 24,
+            "resolve": R * 24 + R * 16 + U * 8,
+            "update": 2 * U * S + R * 16 + U * 8,
+            "update_b": 0, "seg": 0, "scatter": 0,
+        }[stage]
     return {
         # read points (+labels/features), write the ray table and one 8-byte key per row
         "walk": n * (12 + P) + used * 32 + R * 8,
         # per row: key in, voxel id out, one count; per voxel: leaf lookup, slot, key
         "resolve": R * (8 + 4 + 4) + U * (16 + 4 + 8 + 4),
+        "seg": U * 8,
         # per row: voxel id + count in; single-row voxels also ray + label + state
         "scatter": R * (4 + 4 + 4) + U * (32 + 2 * S),
         # multi-row voxels: rows, rays, labels and state (upper bound: all voxels)
         "update": 2 * U * S + R * (4 + 32 + (4 if kind == "closed" else 0)),
         "update_b": 0,
-        "seg": U * 8,
     }[stage]
 
 
@@ -328,7 +338,9 @@ def run_ours(args):
     stages = list(_lib.STAGES)
     mean_stage = {s: statistics.mean(h[s] for h in stage_hist) for s in stages}
     dom = max(_lib.KERNEL_STAGES, key=lambda s: mean_stage[s])
-    dom_bytes = statistics.mean(stage_bytes(dom, r, kind, C, D, tsdf_elem) for r in prof_reps)
+    slot_frames = m.engine_stats().get("frames_slot_mode", 0) if not sharded else 0
+    slots = slot_frames > 0
+    dom_bytes = statistics.mean(stage_bytes(dom, r, kind, C, D, tsdf_elem, slots) for r in prof_reps)
     peak, peak_src = measured_peak()
     achieved = dom_bytes / (mean_stage[dom] / 1e3) / 1e9 if mean_stage[dom] > 0 else 0.0
     fb = frame_bytes(used / K, touched_all / K, kind, C, D)   # mean frame, global counts
@@ -417,7 +429,9 @@ def run_ours(args):
             "roofline": ({"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                           "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                           "peak_source": peak_src,
-                          "bytes_per_launch": dom_bytes, "ms_per_launch": mean_stage[dom]}
+                          "bytes_per_launch": dom_bytes, "ms_per_launch": mean_stage[dom],
+                          "timing": "kernel span inside the frame graph (%globaltimer, FrameParams.kspan)",
+                          "update_mode": "slots" if slots else "segments"}
                          if not sharded else
                          {"bound": "hbm", "kernel": "whole frame (per-rank peak x ranks)",
                           "achieved": frame_gbs, "peak": peak * world, "unit": "GB/s",
