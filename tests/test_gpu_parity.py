@@ -224,6 +224,32 @@ def test_update_modes_vs_oracle(mode, cfg, variant):
         assert np.array_equal(m.label_map()[1], om.label_map())
 
 
+@pytest.mark.parametrize("mode", ["slots", "segments"])
+def test_pinned_host_inputs_match_device_inputs(mode):
+    """Pinned host arrays are read in place by the walk in slot mode (no
+    staging copy); the map must equal the one built from device tensors."""
+    import torch
+
+    from paper_2512_12945_b200 import Mapper, scenes
+
+    wl = scenes.workload(2, device="cuda")
+    a = Mapper(**wl.mapper_kwargs)
+    b = Mapper(**wl.mapper_kwargs)
+    a.set_update_mode(mode)
+    b.set_update_mode(mode)
+    for i in range(3):
+        f = wl.make_frame(i)
+        pts = torch.empty(f.points.shape, dtype=f.points.dtype, pin_memory=True)
+        pts.copy_(f.points)
+        lab = torch.empty(f.labels.shape, dtype=f.labels.dtype, pin_memory=True)
+        lab.copy_(f.labels)
+        ra = a.integrate(pts, f.pose, labels=lab)
+        rb = b.integrate(f.points, f.pose, labels=f.labels)
+        assert np.array_equal(report_rows([ra]), report_rows([rb]))
+    assert a.grids[0].content_hash() == b.grids[0].content_hash()
+    assert a.grids[1].content_hash() == b.grids[1].content_hash()
+
+
 def test_update_mode_argument():
     from paper_2512_12945_b200 import Mapper
 
