@@ -63,21 +63,6 @@ svx_status stage_in(const void* p, size_t bytes, DevBuf& stage, cudaStream_t s, 
     return SVX_OK;
 }
 
-// Pinned host memory the device can read directly (UVA mapping).
-static bool host_mapped(const void* p, const void** dev) {
-    if (!p) return false;
-    cudaPointerAttributes a;
-    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
-        cudaGetLastError();
-        return false;
-    }
-    if (a.type == cudaMemoryTypeHost && a.devicePointer) {
-        *dev = a.devicePointer;
-        return true;
-    }
-    return false;
-}
-
 size_t tsdf_elem(const svx_map* m) { return m->cfg.tsdf_dtype == SVX_F64 ? 8 : 4; }
 
 size_t sem_elem(const svx_map* m) {
@@ -460,30 +445,14 @@ svx_status integrate_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n
     const void* pts = pts_in;
     const void* feats = kind == SVX_SEM_OPEN ? feats_in : nullptr;
     const void* labv = kind == SVX_SEM_CLOSED ? (const void*)labels_in : nullptr;
-    init_row_space(m, n);
-    // Slot-mode frames read points and labels exactly once, in the walk: from
-    // pinned host arrays the walk reads them in place (the transfer overlaps
-    // the band walk) instead of staging them with copies first.
-    bool zero_copy = false;
-    if (!device_inputs && kind != SVX_SEM_OPEN && choose_slots(m)) {
-        const void *dp = nullptr, *dl = nullptr;
-        if (host_mapped(pts_in, &dp) && (kind != SVX_SEM_CLOSED || host_mapped(labels_in, &dl))) {
-            pts = dp;
-            if (kind == SVX_SEM_CLOSED) labv = dl;
-            zero_copy = true;
-        }
-    }
-    auto stage_all = [&]() -> svx_status {
-        pts = pts_in;
-        labv = kind == SVX_SEM_CLOSED ? (const void*)labels_in : nullptr;
+    if (!device_inputs) {
         SVX_TRY(stage_in(pts_in, (size_t)n * 3 * (pts_f64 ? 8 : 4), m->in_pts, s, &pts));
         if (kind == SVX_SEM_CLOSED) SVX_TRY(stage_in(labels_in, (size_t)n * 4, m->in_lab, s, &labv));
         if (kind == SVX_SEM_OPEN)
             SVX_TRY(stage_in(feats_in, (size_t)n * m->payload_d * (feats_f64 ? 8 : 4), m->in_feat, s,
                              &feats));
-        return SVX_OK;
-    };
-    if (!device_inputs && !zero_copy) SVX_TRY(stage_all());
+    }
+    init_row_space(m, n);
     KeyPack kp = default_key_pack(m, pp);
     FrameCtr* hc = m->h_ctr;
     // counts before this frame (stamps, report); m->nblocks / m->nvox stay the
@@ -495,10 +464,6 @@ svx_status integrate_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n
         SVX_TRY(reserve_frame(m, n, s));
         SVX_TRY(reserve_pools(m, s));
         m->frame_slots = choose_slots(m);
-        if (zero_copy && !m->frame_slots) {   // re-run in segment mode: labels are gathered later
-            SVX_TRY(stage_all());
-            zero_copy = false;
-        }
         reset_ctr(m);
         FrameParams& p = hc->p;
         p.pts = pts;

@@ -82,6 +82,23 @@ def main():
         m.integrate(f.points, f.pose, labels=f.labels)
         spans.append(m.stage_times())
     m.set_profiling(False)
+    # pinned host inputs (the e2e path): spans and wall
+    hp = []
+    for f in frames[5:]:
+        pt = torch.empty(f.points.shape, dtype=f.points.dtype, pin_memory=True)
+        pt.copy_(f.points)
+        lb = torch.empty(f.labels.shape, dtype=f.labels.dtype, pin_memory=True)
+        lb.copy_(f.labels)
+        hp.append((pt.numpy(), lb.numpy()))
+    m.set_profiling(True)
+    hspans, hwall = [], []
+    for f, (pt, lb) in zip(frames[5:], hp):
+        t0 = time.perf_counter()
+        m.integrate(pt, f.pose, labels=lb)
+        hwall.append((time.perf_counter() - t0) * 1e3)
+        hspans.append(m.stage_times())
+    print("pinned host inputs: wall %.4f ms; kernel spans (median us): " % med(hwall) + ", ".join(
+        f"{k} {1e3 * med([sp[k] for sp in hspans]):.1f}" for k in _lib.STAGES))
     print("kernel spans (median us): " + ", ".join(
         f"{k} {1e3 * med([sp[k] for sp in spans]):.1f}" for k in _lib.STAGES))
     print(f"config {args.config} mode {args.mode}: per frame (median ms) "
