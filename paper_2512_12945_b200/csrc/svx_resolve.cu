@@ -40,8 +40,6 @@ __global__ void __launch_bounds__(kResolveThreads) k_resolve(
     const double* __restrict__ rowd, const int* __restrict__ rowlab, rt::ResolveArgs ra) {
     grid_dep_wait();
     __shared__ int s_warp[kResolveThreads / 32];
-    __shared__ int4 s_leaf[rt::kLeafCache];
-    for (int i = threadIdx.x; i < rt::kLeafCache; i += blockDim.x) s_leaf[i] = make_int4(0, 0, 0, -1);
     __shared__ unsigned long long s_base;
     __shared__ unsigned s_tcount;
     FrameCtr* ctr = ra.ctr;
@@ -65,11 +63,7 @@ __global__ void __launch_bounds__(kResolveThreads) k_resolve(
     ra.slots = fp.slots != 0;
     ra.region = fp.region;
     __syncthreads();
-    // each CTA takes a contiguous run of tiles (consecutive rays: leaf cache hits)
-    const long long ntiles = (total + kResolveThreads - 1) / kResolveThreads;
-    const long long per = (ntiles + gridDim.x - 1) / gridDim.x;
-    const long long tile_end = min(ntiles, (long long)(blockIdx.x + 1) * per);
-    for (long long tile = (long long)blockIdx.x * per; tile < tile_end; ++tile) {
+    for (long long tile = blockIdx.x; tile * kResolveThreads < total; tile += gridDim.x) {
         const long long t = tile * kResolveThreads + threadIdx.x;
         const bool valid = t < total;
         // row arrays are dead after this read: evict-first
@@ -80,7 +74,7 @@ __global__ void __launch_bounds__(kResolveThreads) k_resolve(
             rsl.label = __ldcs(rowlab + t);
             rsl.d = __ldcs(rowd + t);
         }
-        rt::resolve_step<kResolveThreads>(ra, valid, key, rsl, t, s_warp, s_base, s_tcount, s_leaf);
+        rt::resolve_step<kResolveThreads>(ra, valid, key, rsl, t, s_warp, s_base, s_tcount);
         __syncthreads();
     }
     if (ra.slots && threadIdx.x == 0) {   // this CTA's touched region

@@ -101,8 +101,6 @@ __device__ int leaf_find_or_insert(int4* table, long long mask, int a, int b, in
     }
 }
 
-constexpr int kLeafCache = 512;   // entries of the per-CTA leaf cache (8 KB shared memory)
-
 // CTA-wide exclusive rank of a predicate (warp ballots + one shared-memory
 // round); every thread gets the total.  s_warp holds kThreads/32 counts and
 // must not be rewritten before every thread has passed the next barrier.
@@ -167,7 +165,7 @@ __device__ __forceinline__ void resolve_step(const ResolveArgs& ra, bool valid,
                                              unsigned long long key, const RowSlot& rsl,
                                              long long t,
                                              int* s_warp, unsigned long long& s_base,
-                                             unsigned& s_tcount, int4* s_leaf) {
+                                             unsigned& s_tcount) {
     const KeyPack& kp = ra.kp;
     const long long hmask = ra.hmask, bcap = ra.bcap, vcap = ra.vcap, nblocks0 = ra.nblocks0;
     const int frame = ra.frame;
@@ -203,20 +201,8 @@ __device__ __forceinline__ void resolve_step(const ResolveArgs& ra, bool valid,
     // ---- leaves: find, or claim an empty slot; ids for the tile's claims
     int id = -1, lstate = 0;   // 1 = claimed here, 2 = another CTA's claim
     long long lpos = 0;
-    // per-CTA leaf cache (consecutive steps of a CTA cover consecutive rays,
-    // which mostly land in the leaves the previous step resolved)
-    const unsigned long long lh = is_ll ? block_hash(la, lb, lc) : 0ULL;
-    const int cslot = (int)((lh >> 40) & (kLeafCache - 1));
-    bool cached = false;
     if (is_ll) {
-        const int4 ce = s_leaf[cslot];
-        if (ce.w >= 0 && ce.x == la && ce.y == lb && ce.z == lc) {
-            id = ce.w;
-            cached = true;
-        }
-    }
-    if (is_ll && !cached) {
-        lpos = (long long)(lh & (unsigned long long)hmask);
+        lpos = (long long)(block_hash(la, lb, lc) & (unsigned long long)hmask);
         while (true) {
             const int4 sv = __ldcg(table + lpos);
             if (sv.w >= 0) {
@@ -261,7 +247,6 @@ __device__ __forceinline__ void resolve_step(const ResolveArgs& ra, bool valid,
         if (v >= 0 && sv.x == la && sv.y == lb && sv.z == lc) id = v;
         else id = leaf_find_or_insert(table, hmask, la, lb, lc, frame, bcap, bcoord, ctr);
     }
-    if (is_ll && !cached && id >= 0) s_leaf[cslot] = make_int4(la, lb, lc, id);   // read next step
     id = __shfl_sync(full, id, lleader);
 
     // ---- voxels: find, or claim an inactive slot; ids for the tile's claims
