@@ -267,20 +267,17 @@ static svx_status run_frame(svx_map* m, int pts_f64, int feats_f64, cudaStream_t
         m->graph[gm] = g;
         m->walk_node[gm] = root;
         m->walk_nargs[gm] = m->first_nargs;
+        const int na = m->first_nargs;
+        if (na < 1 || na > 16) return fail(SVX_E_INTERNAL, "frame graph: bad first-kernel arity");
+        SVX_CUDA(cudaGraphKernelNodeGetParams(root, &m->walk_kp[gm]));
+        for (int i = 0; i < na - 1; ++i) m->walk_args[gm][i] = m->walk_kp[gm].kernelParams[i];
+        m->walk_args[gm][na - 1] = &m->h_ctr->p;   // this frame's FrameParams, read at SetParams
+        m->walk_kp[gm].kernelParams = m->walk_args[gm];
+        m->walk_kp[gm].extra = nullptr;
         m->gsig[gm] = sig;
     }
-    {   // this frame's parameters into the first kernel's FrameParams argument
-        cudaKernelNodeParams kp;
-        SVX_CUDA(cudaGraphKernelNodeGetParams(m->walk_node[gm], &kp));
-        void* args[16];
-        const int na = m->walk_nargs[gm];
-        if (na < 1 || na > 16) return fail(SVX_E_INTERNAL, "frame graph: bad first-kernel arity");
-        for (int i = 0; i < na - 1; ++i) args[i] = kp.kernelParams[i];
-        args[na - 1] = &m->h_ctr->p;
-        kp.kernelParams = args;
-        kp.extra = nullptr;
-        SVX_CUDA(cudaGraphExecKernelNodeSetParams(gexec, m->walk_node[gm], &kp));
-    }
+    // this frame's parameters into the first kernel's FrameParams argument
+    SVX_CUDA(cudaGraphExecKernelNodeSetParams(gexec, m->walk_node[gm], &m->walk_kp[gm]));
     if (m->prof) {
         const size_t n = (size_t)kSpanKernels * 2 * kSpanMaxCtas * sizeof(unsigned long long);
         SVX_CUDA(cudaMemsetAsync(m->kspan.p, 0, n, s));

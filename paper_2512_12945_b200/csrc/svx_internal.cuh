@@ -243,6 +243,8 @@ struct svx_map {
     cudaGraph_t graph[2] = {};       // kept: its first-kernel node is updated per frame
     cudaGraphNode_t walk_node[2] = {};
     int walk_nargs[2] = {};          // parameters of that kernel (FrameParams is the last)
+    cudaKernelNodeParams walk_kp[2] = {};   // its captured launch parameters
+    void* walk_args[2][16] = {};            // its argument pointers (graph-owned storage)
     int first_nargs = 0;             // set by launch_march for the kernel it launched first
     unsigned long long gsig[2] = {};
     svx::DevBuf cubtmp;
