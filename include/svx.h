@@ -53,6 +53,13 @@ enum { SVX_F32 = 0, SVX_F64 = 1 };
  * device pointer (skips the per-call pointer-attribute queries).  Without it
  * the library detects host arrays and stages them itself. */
 #define SVX_DEVICE_INPUTS 0x100
+/* OR-ed into points_dtype of svx_integrate: the library checks the pose
+ * itself (finite, bottom row exactly [0 0 0 1], rotation rows orthonormal
+ * within 0.5e-4, det > 0 -- the fast acceptance test of fusion.py:31-77) and
+ * returns SVX_POSE_NEEDS_HOST, doing nothing, when the pose needs the host's
+ * full validation (validate_rotation's polar fix or its error messages). */
+#define SVX_POSE_CHECK 0x200
+#define SVX_POSE_NEEDS_HOST 8
 
 /*
  * Map construction parameters.  Mirrors the union of FusionConfig,

@@ -126,6 +126,8 @@ _SIGNATURES = {
 }
 
 DEVICE_INPUTS = 0x100   # svx.h SVX_DEVICE_INPUTS
+POSE_CHECK = 0x200      # svx.h SVX_POSE_CHECK
+POSE_NEEDS_HOST = 8     # svx.h SVX_POSE_NEEDS_HOST
 
 STAGES = ("walk", "resolve", "seg", "scatter", "update", "update_b", "frame")
 KERNEL_STAGES = STAGES[:-1]

@@ -20,6 +20,9 @@
 #include <cub/cub.cuh>
 #include <string>
 
+#include <cmath>
+#include <algorithm>
+
 #include "svx_internal.cuh"
 
 namespace svx {
@@ -105,6 +108,24 @@ svx_status out_finish(OutStage& o, cudaStream_t s) {
 
 void out_release(OutStage* o, int n) {
     for (int i = 0; i < n; ++i) release(o[i].buf);
+}
+
+// The fast acceptance test of the frame pose (fusion.py:31-77, mapper.py
+// _check_pose): anything else goes back to the host's full validation.
+bool pose_fast_ok(const double* f) {
+    for (int i = 0; i < 16; ++i)
+        if (!std::isfinite(f[i])) return false;
+    if (f[12] != 0.0 || f[13] != 0.0 || f[14] != 0.0 || f[15] != 1.0) return false;
+    const double a0 = f[0], a1 = f[1], a2 = f[2], b0 = f[4], b1 = f[5], b2 = f[6];
+    const double c0 = f[8], c1 = f[9], c2 = f[10];
+    double err = fabs(a0 * a0 + a1 * a1 + a2 * a2 - 1.0);
+    err = std::max(err, fabs(b0 * b0 + b1 * b1 + b2 * b2 - 1.0));
+    err = std::max(err, fabs(c0 * c0 + c1 * c1 + c2 * c2 - 1.0));
+    err = std::max(err, fabs(a0 * b0 + a1 * b1 + a2 * b2));
+    err = std::max(err, fabs(a0 * c0 + a1 * c1 + a2 * c2));
+    err = std::max(err, fabs(b0 * c0 + b1 * c1 + b2 * c2));
+    const double det = a0 * (b1 * c2 - b2 * c1) - a1 * (b0 * c2 - b2 * c0) + a2 * (b0 * c1 - b1 * c0);
+    return err <= 0.5e-4 && det > 0.0;
 }
 
 svx_status set_device(const svx_map* m) {
@@ -205,6 +226,7 @@ svx_status svx_integrate(svx_map* m, const void* points, int32_t points_dtype, i
                          const double pose[16], const int32_t* labels, const void* feats,
                          int32_t feats_dtype, void* stream, svx_report* report) {
     if (!m || !pose || (n > 0 && !points)) return fail(SVX_E_INPUT, "null argument");
+    if ((points_dtype & SVX_POSE_CHECK) && !pose_fast_ok(pose)) return (svx_status)SVX_POSE_NEEDS_HOST;
     SVX_TRY(set_device(m));
     PoseParams pp;
     for (int r = 0; r < 3; ++r) {

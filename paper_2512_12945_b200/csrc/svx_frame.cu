@@ -226,7 +226,24 @@ static svx_status collect_stage_times(svx_map* m) {
 
 // Run one frame attempt: replay (or capture, on the map's own stream) the
 // frame graph on the caller's stream.
+static const bool g_no_graph = getenv("SVX_NO_GRAPH") != nullptr;   // experiment: eager launches
+
 static svx_status run_frame(svx_map* m, int pts_f64, int feats_f64, cudaStream_t s) {
+    if (g_no_graph) {
+        if (m->prof) {
+            const size_t n = (size_t)kSpanKernels * 2 * kSpanMaxCtas * sizeof(unsigned long long);
+            SVX_CUDA(cudaMemsetAsync(m->kspan.p, 0, n, s));
+        }
+        SVX_TRY(clean_ctr(m, s));
+        if (g_trace_host) g_t_launch0 = now_us();
+        SVX_TRY(enqueue_frame(m, pts_f64, feats_f64, s));
+        SVX_CUDA(cudaEventRecord(m->ev1, s));
+        if (g_trace_host) g_t_launch1 = now_us();
+        SVX_CUDA(cudaEventSynchronize(m->ev1));
+        if (g_trace_host) g_t_synced = now_us();
+        if (m->prof) SVX_TRY(collect_stage_times(m));
+        return SVX_OK;
+    }
     const unsigned long long sig = graph_signature(m, pts_f64, feats_f64);
     const int gm = m->frame_slots ? 1 : 0;
     cudaGraphExec_t& gexec = m->gexec[gm];

@@ -137,6 +137,21 @@ def _check_pose(pose, frame_id):
     return fixed
 
 
+_TORCH = []
+
+
+def _torch_mod():
+    """torch if it is already imported (CUDA tensors imply it), else None."""
+    if not _TORCH:
+        import sys
+
+        t = sys.modules.get("torch")
+        if t is None:
+            return None
+        _TORCH.append(t)
+    return _TORCH[0]
+
+
 def _is_torch(x) -> bool:
     return type(x).__module__.startswith("torch")
 
@@ -382,10 +397,58 @@ class Mapper:
         sensor-to-world pose, with integer ``labels`` (closed-set) or float
         ``features`` (open-set).  Same contract as bindings/__init__.py:131-142
         and integrate_frame (fusion.py:200-293)."""
+        if features is None and self._open is None:
+            rep = self._integrate_fast(points, pose, labels)
+            if rep is not None:
+                return rep
         pts = self._points_arg(points)
         pose = _check_pose(pose, self._frames)
         lab, feat = self._payload_args(int(pts.shape[0]), labels, features, self._frames)
         return self._run(lib.svx_integrate, pts, pose.reshape(-1), lab, feat)
+
+    def _integrate_fast(self, points, pose, labels):
+        """The common call -- contiguous CUDA tensors on the map's GPU (f32/f64
+        points, int32 labels for closed-set maps) and a C-contiguous float64
+        4x4 pose -- with the pose's fast acceptance test done by the library
+        (SVX_POSE_CHECK).  Returns None when the call needs the general path
+        (any other argument form, or a pose that needs full validation), so
+        checks and error messages stay those of the general path."""
+        torch = _torch_mod()
+        if torch is None or type(points) is not torch.Tensor or not points.is_cuda:
+            return None
+        dt = points.dtype
+        if (dt is not torch.float32 and dt is not torch.float64) or points.dim() != 2 \
+                or points.shape[1] != 3 or not points.is_contiguous() \
+                or points.get_device() != self._device:
+            return None
+        n = points.shape[0]
+        lab_ptr = None
+        if self._closed is not None:
+            if type(labels) is not torch.Tensor or labels.dtype is not torch.int32 \
+                    or labels.dim() != 1 or labels.shape[0] != n or not labels.is_contiguous() \
+                    or labels.get_device() != self._device:
+                return None
+            lab_ptr = labels.data_ptr() if n else None
+        elif labels is not None:
+            return None
+        if type(pose) is not np.ndarray or pose.dtype != np.float64 or pose.shape != (4, 4) \
+                or not pose.flags.c_contiguous:
+            return None
+        code = (SVX_F64 if dt is torch.float64 else SVX_F32) | _lib.DEVICE_INPUTS | _lib.POSE_CHECK
+        stream = ctypes.c_void_p(torch._C._cuda_getCurrentRawStream(self._device))
+        st = lib.svx_integrate(self._handle, points.data_ptr() if n else None, code, n,
+                               pose.ctypes.data, lab_ptr, None, SVX_F32, stream, self._rep_ref)
+        if st == _lib.POSE_NEEDS_HOST:
+            return None
+        check(st)
+        self._frames += 1
+        rep = self._rep
+        return IntegrationReport(
+            points_in=rep.points_in, points_used=rep.points_used,
+            skipped_nonfinite=rep.skipped_nonfinite, skipped_range=rep.skipped_range,
+            skipped_degenerate=rep.skipped_degenerate, skipped_bad_label=rep.skipped_bad_label,
+            band_hits=rep.band_hits, touched_voxels=rep.touched_voxels,
+            kernel_ms=rep.kernel_ms, new_blocks=rep.new_blocks, new_voxels=rep.new_voxels)
 
     def integrate_world(self, points_world, origin, labels=None, features=None):
         """Fuse world-frame points observed from ``origin``: the reference's

@@ -250,6 +250,33 @@ def test_pinned_host_inputs_match_device_inputs(mode):
     assert a.grids[1].content_hash() == b.grids[1].content_hash()
 
 
+def test_cuda_fast_path_pose_fallbacks():
+    """CUDA-tensor calls take the library-side pose check; poses outside its
+    fast acceptance set (polar fix needed, non-finite, bad bottom row) must
+    behave exactly like the general path."""
+    import torch
+
+    from paper_2512_12945_b200 import Mapper
+    from paper_2512_12945_b200.errors import UserInputError
+
+    rng = np.random.default_rng(5)
+    pts = rng.normal(size=(4000, 3)).astype(np.float32) * 3.0
+    lab = rng.integers(1, 5, 4000).astype(np.int32)
+    tp, tl = torch.from_numpy(pts).cuda(), torch.from_numpy(lab).cuda()
+    kw = dict(voxel_size=0.1, truncation=0.3, num_classes=4, max_range=20.0)
+    pose = np.eye(4)
+    pose[:3, :3] += 4e-4 * rng.normal(size=(3, 3))   # needs validate_rotation's polar fix
+    pose[:3, 3] = [0.5, -0.2, 0.1]
+    a, b = Mapper(**kw), Mapper(**kw)
+    ra = a.integrate(tp, pose, labels=tl)            # fast path -> host fallback
+    rb = b.integrate(pts, pose, labels=lab)          # general path
+    assert ra.touched_voxels == rb.touched_voxels and ra.band_hits == rb.band_hits
+    assert a.grids[0].content_hash() == b.grids[0].content_hash()
+    for bad in (np.full((4, 4), np.nan), np.diag([1.0, 1.0, 1.0, 2.0])):
+        with pytest.raises(UserInputError):
+            a.integrate(tp, bad, labels=tl)
+
+
 def test_update_mode_argument():
     from paper_2512_12945_b200 import Mapper
 
