@@ -241,6 +241,143 @@ __global__ void k_classify(int64_t count, int D, int k, const int* __restrict__ 
     }
 }
 
+// classify_means (gaussian.py:132-155) on the FP64 tensor cores: one fused
+// kernel computes S = M . E^T with mma.sync.m8n8k4.f64 (DMMA; B200 has no
+// f64 kind of tcgen05) and applies the cosine normalisation, softmax, argmax
+// and the label rules in the epilogue, straight from the accumulator
+// fragments.  f64 end to end: the reference scores in f64 (means @ emb.T)
+// and softmax(S / tau) with tau = 0.01 turns any score error e into a
+// relative error e / tau, so a reduced-precision product cannot be used
+// (DESIGN.md section 8).
+//
+// Tiling: a CTA = 4 warps; a warp owns MT m-tiles of 8 voxels and all NT
+// n-tiles of 8 queries (k <= 8 NT), accumulators in registers (2 f64 per
+// thread per tile).  The queries stream through shared memory in chunks of
+// kDc dimensions; each thread feeds its A fragment (voxel row r = lane / 4,
+// dim d0 + lane % 4) straight from global (f32 -> f64) and accumulates the
+// row's squared norm on the way.
+constexpr int kDc = 16;              // dims per shared-memory chunk
+constexpr int kClsWarps = 4;
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                 : "+d"(c[0]), "+d"(c[1])
+                 : "d"(a), "d"(b));
+}
+
+template <int NT, int MT, class TS, class TD>
+__global__ void __launch_bounds__(32 * kClsWarps) k_classify_dmma(
+    int64_t count, int D, int k, const int* __restrict__ act_vid, const TS* __restrict__ mean,
+    const TD* __restrict__ vw, const double* __restrict__ emb, const double* __restrict__ en,
+    double tau, double tp, int32_t* __restrict__ labels, double* __restrict__ best,
+    double* __restrict__ sims_out) {
+    __shared__ double s_e[NT * 8][kDc + 1];   // +1: no bank conflicts on the B fragment reads
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int qr = lane >> 2, qc = lane & 3;   // fragment row / column group
+    const int64_t row0 = ((int64_t)blockIdx.x * kClsWarps + warp) * (8 * MT);
+    const TS* rp[MT];
+    int64_t ri[MT];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+        ri[mt] = row0 + mt * 8 + qr;
+        rp[mt] = ri[mt] < count ? mean + (int64_t)act_vid[ri[mt]] * D : nullptr;
+    }
+    double acc[MT][NT][2];
+    double nn[MT];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+        nn[mt] = 0.0;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+    }
+    for (int d0 = 0; d0 < D; d0 += kDc) {
+        __syncthreads();
+        for (int t = threadIdx.x; t < NT * 8 * kDc; t += blockDim.x) {
+            const int j = t / kDc, c = t % kDc;
+            s_e[j][c] = (j < k && d0 + c < D) ? emb[(int64_t)j * D + d0 + c] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < kDc; kk += 4) {
+            const int d = d0 + kk + qc;
+            double a[MT];
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) {
+                a[mt] = (rp[mt] && d < D) ? (double)rp[mt][d] : 0.0;
+                nn[mt] += a[mt] * a[mt];
+            }
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+                const double b = s_e[nt * 8 + qr][kk + qc];
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) dmma(acc[mt][nt], a[mt], b);
+            }
+        }
+    }
+    // epilogue: row qr of each m-tile lives in the 4 lanes of quad qr
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+        double n2 = nn[mt];
+        n2 += __shfl_xor_sync(0xffffffffu, n2, 1);
+        n2 += __shfl_xor_sync(0xffffffffu, n2, 2);
+        const double mn = sqrt(n2);
+        const bool live = ri[mt] < count;
+        const int vid = live ? act_vid[ri[mt]] : 0;
+        const double wgt = live ? (double)vw[2 * (int64_t)vid + 1] : 0.0;   // {d, w} pairs
+        const bool ok = live && mn != 0.0 && wgt > 0.0;
+        // e_j = (cos_j) / tau, as the reference computes it
+        double lmax = -INFINITY;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int j = nt * 8 + qc * 2 + h;
+                if (j < k) {
+                    const double sj = mn == 0.0 ? NAN : acc[mt][nt][h] / (mn * en[j]);
+                    if (sims_out && live) sims_out[ri[mt] * k + j] = sj;
+                    const double ej = sj / tau;
+                    acc[mt][nt][h] = ej;
+                    lmax = ej > lmax ? ej : lmax;
+                }
+            }
+        }
+        lmax = fmax(lmax, __shfl_xor_sync(0xffffffffu, lmax, 1));
+        lmax = fmax(lmax, __shfl_xor_sync(0xffffffffu, lmax, 2));
+        double den = 0.0, emax = -1.0;
+        int arg = 0x7fffffff;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int j = nt * 8 + qc * 2 + h;
+                if (j < k) {
+                    const double ej = exp(acc[mt][nt][h] - lmax);
+                    den += ej;
+                    if (ej > emax) { emax = ej; arg = j; }
+                }
+            }
+        }
+        // quad reduction; first index attaining the max (np.argmax)
+#pragma unroll
+        for (int o = 1; o <= 2; o <<= 1) {
+            den += __shfl_xor_sync(0xffffffffu, den, o);
+            const double oe = __shfl_xor_sync(0xffffffffu, emax, o);
+            const int oa = __shfl_xor_sync(0xffffffffu, arg, o);
+            if (oe > emax || (oe == emax && oa < arg)) { emax = oe; arg = oa; }
+        }
+        if (live && qc == 0) {
+            if (!ok) {
+                labels[ri[mt]] = 0;
+                best[ri[mt]] = 0.0;
+            } else {
+                const double top = emax / den;
+                labels[ri[mt]] = top < tp ? 0 : arg + 1;
+                best[ri[mt]] = top;
+            }
+        }
+    }
+}
+
 template <class TC>
 __global__ void k_label_map(int64_t count, int C, int mode, const int* __restrict__ act_vid,
                             const TC* __restrict__ counts, int32_t* __restrict__ labels) {
@@ -450,10 +587,30 @@ svx_status launch_cosine(svx_map* m, int64_t count, const double* q, double qn, 
     return SVX_OK;
 }
 
+template <int NT, int MT, class TS, class TD>
+static svx_status classify_dmma_t(svx_map* m, int64_t count, const double* emb, const double* en,
+                                  int k, double tau, double tp, int32_t* labels, double* best,
+                                  double* sims, cudaStream_t s) {
+    const int64_t rows_per_cta = (int64_t)kClsWarps * 8 * MT;
+    k_classify_dmma<NT, MT, TS, TD><<<(unsigned)((count + rows_per_cta - 1) / rows_per_cta),
+                                      32 * kClsWarps, 0, s>>>(
+        count, m->payload_d, k, ptr<int>(m->act_vid), ptr<TS>(m->s0), ptr<TD>(m->vt), emb, en,
+        tau, tp, labels, best, sims);
+    SVX_LAUNCHED();
+    return SVX_OK;
+}
+
 template <class TS, class TD>
 static svx_status classify_t(svx_map* m, int64_t count, const double* emb, const double* en, int k,
                              double tau, double tp, int32_t* labels, double* best, double* sims,
                              cudaStream_t s) {
+    // FP64 tensor cores (DMMA) for up to 128 queries; the warp-per-voxel
+    // CUDA-core kernel beyond
+    if (k <= 8) return classify_dmma_t<1, 4, TS, TD>(m, count, emb, en, k, tau, tp, labels, best, sims, s);
+    if (k <= 16) return classify_dmma_t<2, 4, TS, TD>(m, count, emb, en, k, tau, tp, labels, best, sims, s);
+    if (k <= 32) return classify_dmma_t<4, 4, TS, TD>(m, count, emb, en, k, tau, tp, labels, best, sims, s);
+    if (k <= 64) return classify_dmma_t<8, 2, TS, TD>(m, count, emb, en, k, tau, tp, labels, best, sims, s);
+    if (k <= 128) return classify_dmma_t<16, 1, TS, TD>(m, count, emb, en, k, tau, tp, labels, best, sims, s);
     const int T = 256;
     k_classify<TS, TD><<<grid_for(count * 32, T), T, 0, s>>>(
         count, m->payload_d, k, ptr<int>(m->act_vid), ptr<TS>(m->s0), ptr<TD>(m->vt), emb, en,

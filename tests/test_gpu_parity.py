@@ -279,6 +279,38 @@ def test_cuda_fast_path_pose_fallbacks():
             a.integrate(tp, bad, labels=tl)
 
 
+@pytest.mark.parametrize("k", [5, 32, 100, 160])
+def test_classify_fp64_tensor_core_vs_oracle(k):
+    """classify_means on the FP64 tensor cores (k <= 128) and the CUDA-core
+    kernel (k > 128) against the oracle's sequential f64 scoring: labels
+    exact, best and similarities within 1e-12 (only the summation order of
+    the dot products differs)."""
+    from paper_2512_12945_b200 import Mapper, scenes
+    from oracle.oracle import OracleMap
+
+    wl = scenes.workload(3, device="cuda")
+    kw = dict(wl.mapper_kwargs)
+    kw["feature_dim"] = 96                     # keeps the oracle fast; not a multiple of 16
+    m = Mapper(**kw)
+    om = OracleMap(**kw)
+    for i in range(2):
+        f = wl.make_frame(i * 5)
+        feats = f.features[:, :96].contiguous()
+        m.integrate_world(f.points_world, f.origin, features=feats)
+        om.integrate_world(f.points_world.cpu().numpy(), f.origin, features=feats.cpu().numpy())
+    rng = np.random.default_rng(k)
+    emb = rng.normal(size=(k, 96))
+    emb /= np.linalg.norm(emb, axis=1, keepdims=True)
+    lab, best, sims = m.classify(emb, return_sims=True)
+    olab, obest = om.classify(emb)
+    assert lab.shape[0] > 1000
+    assert np.array_equal(lab, olab)
+    np.testing.assert_allclose(best, obest, rtol=1e-12, atol=1e-300)
+    # similarities of the first query against the single-query cosine path
+    _, s0 = m.query(emb[0])
+    np.testing.assert_allclose(sims[:, 0], s0, rtol=1e-12, equal_nan=True)
+
+
 def test_update_mode_argument():
     from paper_2512_12945_b200 import Mapper
 
