@@ -308,7 +308,7 @@ def test_classify_fp64_tensor_core_vs_oracle(k):
     np.testing.assert_allclose(best, obest, rtol=1e-12, atol=1e-300)
     # similarities of the first query against the single-query cosine path
     _, s0 = m.query(emb[0])
-    np.testing.assert_allclose(sims[:, 0], s0, rtol=1e-12, equal_nan=True)
+    np.testing.assert_allclose(sims[:, 0], s0, rtol=1e-12, atol=1e-14, equal_nan=True)
 
 
 def test_update_mode_argument():
