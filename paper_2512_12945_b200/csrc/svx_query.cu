@@ -290,25 +290,7 @@ __global__ void __launch_bounds__(32 * kClsWarps) k_classify_dmma(
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
     }
-    // A values of the next chunk are loaded while the current one multiplies
-    TS an[kDc / 4][MT];
-#pragma unroll
-    for (int q = 0; q < kDc / 4; ++q)
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt) {
-            const int d = q * 4 + qc;
-            an[q][mt] = (rp[mt] && d < D) ? rp[mt][d] : (TS)0;
-        }
     for (int d0 = 0; d0 < D; d0 += kDc) {
-        TS ac[kDc / 4][MT];
-#pragma unroll
-        for (int q = 0; q < kDc / 4; ++q)
-#pragma unroll
-            for (int mt = 0; mt < MT; ++mt) {
-                ac[q][mt] = an[q][mt];
-                const int d = d0 + kDc + q * 4 + qc;
-                an[q][mt] = (rp[mt] && d < D) ? rp[mt][d] : (TS)0;
-            }
         __syncthreads();
         for (int t = threadIdx.x; t < NT * 8 * kDc; t += blockDim.x) {
             const int j = t / kDc, c = t % kDc;
@@ -317,10 +299,11 @@ __global__ void __launch_bounds__(32 * kClsWarps) k_classify_dmma(
         __syncthreads();
 #pragma unroll
         for (int kk = 0; kk < kDc; kk += 4) {
+            const int d = d0 + kk + qc;
             double a[MT];
 #pragma unroll
             for (int mt = 0; mt < MT; ++mt) {
-                a[mt] = (double)ac[kk / 4][mt];
+                a[mt] = (rp[mt] && d < D) ? (double)rp[mt][d] : 0.0;
                 nn[mt] += a[mt] * a[mt];
             }
 #pragma unroll
