@@ -41,13 +41,12 @@ __global__ void __launch_bounds__(kResolveThreads) k_resolve(
     grid_dep_wait();
     __shared__ int s_warp[kResolveThreads / 32];
     __shared__ unsigned long long s_base;
-    __shared__ unsigned s_tcount;
     FrameCtr* ctr = ra.ctr;
     KSpan _ks(ctr, kSpanResolve);
     __shared__ FrameCtr s_ctr_;
     snapshot_ctr(ctr, s_ctr_);
     const FrameCtr* cv = &s_ctr_;
-    if (threadIdx.x == 0) s_tcount = 0u;
+    unsigned tcount = 0u;   // this CTA's touched entries (same value in every thread)
     if (cv->abort) {
         if (threadIdx.x == 0) ra.rcount[blockIdx.x] = 0u;
         return;
@@ -74,12 +73,13 @@ __global__ void __launch_bounds__(kResolveThreads) k_resolve(
             rsl.label = __ldcs(rowlab + t);
             rsl.d = __ldcs(rowd + t);
         }
-        rt::resolve_step<kResolveThreads>(ra, valid, key, rsl, t, s_warp, s_base, s_tcount);
-        __syncthreads();
+        // (no barrier between steps: every shared value a step writes is
+        // written after a barrier the previous step's readers have passed)
+        rt::resolve_step<kResolveThreads>(ra, valid, key, rsl, t, s_warp, s_base, tcount);
     }
     if (ra.slots && threadIdx.x == 0) {   // this CTA's touched region
-        ra.rcount[blockIdx.x] = s_tcount;
-        if (s_tcount) atomicAdd(&ctr->n_touched, (unsigned long long)s_tcount);
+        ra.rcount[blockIdx.x] = tcount;
+        if (tcount) atomicAdd(&ctr->n_touched, (unsigned long long)tcount);
     }
 }
 

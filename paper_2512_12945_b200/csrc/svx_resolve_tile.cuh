@@ -165,7 +165,7 @@ __device__ __forceinline__ void resolve_step(const ResolveArgs& ra, bool valid,
                                              unsigned long long key, const RowSlot& rsl,
                                              long long t,
                                              int* s_warp, unsigned long long& s_base,
-                                             unsigned& s_tcount) {
+                                             unsigned& tcount) {
     const KeyPack& kp = ra.kp;
     const long long hmask = ra.hmask, bcap = ra.bcap, vcap = ra.vcap, nblocks0 = ra.nblocks0;
     const int frame = ra.frame;
@@ -335,12 +335,11 @@ __device__ __forceinline__ void resolve_step(const ResolveArgs& ra, bool valid,
             TouchEntry te;
             te.vid = vid >= 0 ? ((unsigned)vid | (created ? kNewBit : 0u)) : 0xFFFFFFFFu;
             te.bidx = (unsigned)(sp - bslot);
-            const long long pos = (long long)s_tcount + rank;
+            const long long pos = (long long)tcount + rank;
             if (pos < ra.region) ra.tent[(long long)blockIdx.x * ra.region + pos] = te;
             else atomicOr(&ctr->err_cap, 1);   // region sized from the row capacity: cannot happen
         }
-        __syncthreads();   // every thread has read s_tcount
-        if (threadIdx.x == 0) s_tcount += cnt;
+        tcount += (unsigned)cnt;   // every thread keeps the same running count
     } else {
         if (threadIdx.x == 0 && cnt) s_base = atomicAdd(&ctr->n_touched, (unsigned long long)cnt);
         __syncthreads();
