@@ -12,7 +12,7 @@ import os
 
 from .errors import STATUS_CLASSES, SemvoxError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsvx.so")
+LIB_PATH = os.environ.get("SVX_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsvx.so")
 
 SVX_F32, SVX_F64 = 0, 1
 SEM_NONE, SEM_CLOSED, SEM_OPEN = 0, 1, 2
