@@ -461,7 +461,10 @@ inline long long slot_region(unsigned long long rows_cap) {
     const long long tiles = (long long)((rows_cap + kResolveTile - 1) / kResolveTile);
     return ((tiles + kPersistentBlocks - 1) / kPersistentBlocks) * kResolveTile;
 }
-constexpr int kMarchBlocks = 148 * 4;        // march CTAs (one partial-counter record each)
+#ifndef SVX_MARCH_BLOCKS
+#define SVX_MARCH_BLOCKS (148 * 4)
+#endif
+constexpr int kMarchBlocks = SVX_MARCH_BLOCKS;   // march CTAs
 
 // TSDF state of one voxel, {d, w} interleaved so an update touches one sector.
 template <class T> struct Pair;

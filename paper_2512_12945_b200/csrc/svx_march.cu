@@ -273,13 +273,19 @@ __device__ __forceinline__ void finish_walk(const Tally& t, MarchPartial*, Frame
 // keys are staged in shared memory; a block scan packs the tile's rows and
 // one atomic per tile reserves their place in the dense row arrays, which
 // are then written coalesced (rowkey, rowray).
-constexpr int kTileRays = 128;
+#ifndef SVX_TILE_RAYS
+#define SVX_TILE_RAYS 128
+#endif
+#ifndef SVX_WALK_MINB
+#define SVX_WALK_MINB 4
+#endif
+constexpr int kTileRays = SVX_TILE_RAYS;
 
 // Slot mode also writes each row's clamped distance d (row_distances_weights,
 // _pycore.py:384-396, the same expression K5 would evaluate) and its point's
 // label, so the slot update needs no gathers.
 template <class P, class Fe>
-__global__ void __launch_bounds__(kTileRays, 4) k_walk(MarchParams mp, int sem_kind, int num_classes,
+__global__ void __launch_bounds__(kTileRays, SVX_WALK_MINB) k_walk(MarchParams mp, int sem_kind, int num_classes,
                                                     int D, double4* __restrict__ ray,
                                                     int* __restrict__ rcnt,
                                                     unsigned long long* __restrict__ rowkey,

@@ -283,7 +283,10 @@ __device__ __forceinline__ RowSlot ld_slot16(const RowSlot* p) {
 }
 
 template <class TD, class TC>
-__global__ void __launch_bounds__(256, 4) k_update_slots(UpdateArgs a, const TouchEntry* __restrict__ tent,
+#ifndef SVX_UPD_MINB
+#define SVX_UPD_MINB 4
+#endif
+__global__ void __launch_bounds__(256, SVX_UPD_MINB) k_update_slots(UpdateArgs a, const TouchEntry* __restrict__ tent,
                                                       const unsigned* __restrict__ rcount,
                                                       unsigned long long* __restrict__ bslot,
                                                       const RowSlot* __restrict__ vslot, TD* vt,
