@@ -284,7 +284,7 @@ __device__ __forceinline__ RowSlot ld_slot16(const RowSlot* p) {
 
 template <class TD, class TC>
 #ifndef SVX_UPD_MINB
-#define SVX_UPD_MINB 4
+#define SVX_UPD_MINB 3
 #endif
 __global__ void __launch_bounds__(256, SVX_UPD_MINB) k_update_slots(UpdateArgs a, const TouchEntry* __restrict__ tent,
                                                       const unsigned* __restrict__ rcount,
