@@ -303,7 +303,7 @@ static svx_status run_frame(svx_map* m, int pts_f64, int feats_f64, cudaStream_t
     // the graph was captured on the map's own stream; it runs on the caller's
     if (g_trace_host) g_t_launch0 = now_us();
     SVX_CUDA(cudaGraphLaunch(gexec, s));
-    count_launch(gm ? 4 : 6);
+    count_launch(gm ? (SVX_INLINE_LONG ? 3 : 4) : 6);
     SVX_CUDA(cudaEventRecord(m->ev1, s));
     if (g_trace_host) g_t_launch1 = now_us();
     SVX_CUDA(cudaEventSynchronize(m->ev1));

@@ -46,6 +46,11 @@ constexpr int kShortMax = 16;   // segments up to this many rows: thread-per-vox
 // A voxel with more rows stops the attempt before any payload changes; the
 // frame re-runs in segment mode.
 constexpr int kSlots = 16;
+// 1: slot-mode voxels of 9..16 rows sorted in-thread by the slot update;
+// 0 (measured faster): a warp per such voxel in k_update_slots_long.
+#ifndef SVX_INLINE_LONG
+#define SVX_INLINE_LONG 0
+#endif
 // RowSlot spacing in vslot (2 = one 32-byte sector per row; measured: no gain).
 constexpr int kSlotStride = 1;
 

@@ -279,6 +279,9 @@ __device__ __forceinline__ void finish_walk(const Tally& t, MarchPartial*, Frame
 #ifndef SVX_WALK_MINB
 #define SVX_WALK_MINB 4
 #endif
+#ifndef SVX_WALK_PREFETCH
+#define SVX_WALK_PREFETCH 0   // measured: +1.3 us walk, no resolve gain
+#endif
 constexpr int kTileRays = SVX_TILE_RAYS;
 
 // Slot mode also writes each row's clamped distance d (row_distances_weights,
@@ -294,6 +297,7 @@ __global__ void __launch_bounds__(kTileRays, SVX_WALK_MINB) k_walk(MarchParams m
                                                     int* __restrict__ rowlab,
                                                     MarchPartial* __restrict__ partials,
                                                     FrameCtr* __restrict__ ctr,
+                                                    const int4* __restrict__ htab,
                                                     const __grid_constant__ FrameParams fpk) {
     grid_dep_wait();
     __shared__ FrameCtr s_ctr_;
@@ -324,6 +328,7 @@ __global__ void __launch_bounds__(kTileRays, SVX_WALK_MINB) k_walk(MarchParams m
             if (prepare_ray<P, Fe>(i, fp, mp.max_range, sem_kind, num_classes, D, t, r)) {
                 long long f0 = 0, f1 = 0, f2 = 0, l0 = 0, l1 = 0, l2 = 0;
                 int nk = 0;
+                int pl0 = INT_MIN, pl1 = INT_MIN, pl2 = INT_MIN;   // last prefetched leaf
                 long long emitted = dda_walk(ox, oy, oz, r.x, r.y, r.z, r.w, mp,
                     [&](long long ci, long long cj, long long ck) {
                         if (!row_kept(ci, cj, ck, ox, oy, oz, r, mp)) return;
@@ -342,6 +347,19 @@ __global__ void __launch_bounds__(kTileRays, SVX_WALK_MINB) k_walk(MarchParams m
                         if (((ox_ | oy_ | oz_) & ~kPackMask) != 0) t.errs |= 2;
                         else key = pack_key(ox_, oy_, oz_);
                         rk[rows++] = key;
+#if SVX_WALK_PREFETCH
+                        // warm the leaf hash slot K2 will probe for this row (the walk
+                        // is compute bound; its DRAM is idle)
+                        {
+                            const int la = (int)(ci >> kLeafLog2), lb = (int)(cj >> kLeafLog2),
+                                      lc = (int)(ck >> kLeafLog2);
+                            if (la != pl0 || lb != pl1 || lc != pl2) {
+                                pl0 = la; pl1 = lb; pl2 = lc;
+                                const int4* hs = htab + (block_hash(la, lb, lc) & (unsigned long long)fp.hmask);
+                                asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(hs));
+                            }
+                        }
+#endif
                     });
                 if (emitted < 0) {
                     t.errs |= 1;
@@ -520,8 +538,8 @@ svx_status march_t(svx_map* m, cudaStream_t s) {
         SVX_CUDA(launch_pdl(k_walk<P, Fe>, kMarchBlocks, kTileRays, smem, s, 
             mp, m->cfg.sem_kind, m->cfg.num_classes, m->payload_d, ptr<double4>(m->ray),
             ptr<int>(m->rcnt), ptr<unsigned long long>(m->rowkey), ptr<int>(m->rowray),
-            ptr<double>(m->rowd), ptr<int>(m->rowlab), parts, dc, m->h_ctr->p));
-        m->first_nargs = 13;
+            ptr<double>(m->rowd), ptr<int>(m->rowlab), parts, dc, ptr<int4>(m->hash), m->h_ctr->p));
+        m->first_nargs = 14;
         SVX_LAUNCHED();
         return SVX_OK;
     }

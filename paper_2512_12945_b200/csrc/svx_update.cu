@@ -282,11 +282,46 @@ __device__ __forceinline__ RowSlot ld_slot16(const RowSlot* p) {
     return r;
 }
 
-template <class TD, class TC>
+// 9..16 rows in-thread: 16 (point << 4 | slot) keys through a bitonic
+// network in registers, then the rows in that order.
+template <class TC>
+__device__ __forceinline__ void sorted_fold16(const UpdateArgs& a, const RowSlot* sl, unsigned k,
+                                              TC* crow, bool closed, RowAcc& acc) {
+    unsigned long long key[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+        key[j] = (unsigned)j < k ? (((unsigned long long)(unsigned)sl[j * kSlotStride].point << 4) | (unsigned)j)
+                                 : ~0ULL;
+#pragma unroll
+    for (int kk = 2; kk <= 16; kk <<= 1) {
+#pragma unroll
+        for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const int l = i ^ jj;
+                if (l > i) {
+                    const unsigned long long x = key[i], y = key[l];
+                    const bool up = (i & kk) == 0;
+                    key[i] = up ? (x < y ? x : y) : (x > y ? x : y);
+                    key[l] = up ? (x > y ? x : y) : (x < y ? x : y);
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        if ((unsigned)j < k) {
+            const RowSlot r = ld_slot16(sl + (int)(key[j] & 15u) * kSlotStride);
+            fold_row<TC>(a, r.d, r.label, crow, closed, acc);
+        }
+    }
+}
+
 #ifndef SVX_UPD_MINB
 #define SVX_UPD_MINB 3
 #endif
-__global__ void __launch_bounds__(256, SVX_UPD_MINB) k_update_slots(UpdateArgs a, const TouchEntry* __restrict__ tent,
+template <class TD, class TC, bool kInlineLong>
+__device__ __forceinline__ void k_update_slots_body(UpdateArgs a, const TouchEntry* __restrict__ tent,
                                                       const unsigned* __restrict__ rcount,
                                                       unsigned long long* __restrict__ bslot,
                                                       const RowSlot* __restrict__ vslot, TD* vt,
@@ -314,13 +349,15 @@ __global__ void __launch_bounds__(256, SVX_UPD_MINB) k_update_slots(UpdateArgs a
         P2 st = reinterpret_cast<const P2*>(vt)[vid];
         const RowSlot* sl = vslot + (long long)vid * kSlots * kSlotStride;
         const unsigned k = c & ~kNewBit;
-        if (k > 8u) {   // 9..16 rows (rare): one warp per voxel in k_update_slots_long
+        if (!kInlineLong && k > 8u) {   // 9..16 rows (rare): one warp per voxel in k_update_slots_long
             a.hugelist2[warp_ticket(&ctr->n_long)] = en;
             continue;
         }
         TC* crow = counts + (long long)vid * a.C;
         RowAcc acc;
-        if (k > 4u) {
+        if (kInlineLong && k > 8u) {
+            sorted_fold16<TC>(a, sl, k, crow, closed, acc);
+        } else if (k > 4u) {
             // 5..8 rows: sort (point, slot) keys in registers, then fold the rows
             // in that order (their slots were just read: L1/L2 hits)
             unsigned long long key[8];
@@ -394,6 +431,16 @@ __global__ void __launch_bounds__(256, SVX_UPD_MINB) k_update_slots(UpdateArgs a
             for (int t = 0; t < a.C; ++t) crow[t] = (TC)(t == acc.last - 1 ? 1 : 0);
         bslot[en.bidx] = (unsigned long long)(unsigned)vid;   // frame count back to 0
     }
+}
+
+template <class TD, class TC, bool kInlineLong>
+__global__ void __launch_bounds__(256, SVX_UPD_MINB) k_update_slots(UpdateArgs a, const TouchEntry* __restrict__ tent,
+                                                                  const unsigned* __restrict__ rcount,
+                                                                  unsigned long long* __restrict__ bslot,
+                                                                  const RowSlot* __restrict__ vslot, TD* vt,
+                                                                  TC* counts) {
+    k_update_slots_body<TD, TC, kInlineLong>(a, tent, rcount, bslot, vslot, vt, counts);
+    if (kInlineLong) frame_epilogue(a.ctr, a.ctr->p.epilogue, a.ctr->p.mirror);
 }
 
 // Slot-mode voxels of 9..16 rows: one warp per voxel; lanes own rows, a
@@ -939,15 +986,18 @@ svx_status open_b(svx_map* m, cudaStream_t s) {
 
 template <class TD, class TC>
 svx_status slots_t(svx_map* m, cudaStream_t s) {
-    SVX_CUDA(launch_pdl(k_update_slots<TD, TC>, kPersistentBlocks, 256, 0, s, make_args(m),
+    constexpr bool inl = SVX_INLINE_LONG != 0;
+    SVX_CUDA(launch_pdl(k_update_slots<TD, TC, inl>, kPersistentBlocks, 256, 0, s, make_args(m),
                         ptr<TouchEntry>(m->tlist), ptr<unsigned>(m->rcount),
                         ptr<unsigned long long>(m->bslot), ptr<RowSlot>(m->vslot), ptr<TD>(m->vt),
                         ptr<TC>(m->s0)));
     SVX_LAUNCHED();
-    SVX_CUDA(launch_pdl(k_update_slots_long<TD, TC>, 148 * 2, 256, 0, s, make_args(m),
-                        ptr<unsigned long long>(m->bslot), ptr<RowSlot>(m->vslot), ptr<TD>(m->vt),
-                        ptr<TC>(m->s0)));
-    SVX_LAUNCHED();
+    if (!inl) {   // voxels of 9..16 rows; this kernel publishes the frame counters
+        SVX_CUDA(launch_pdl(k_update_slots_long<TD, TC>, 148 * 2, 256, 0, s, make_args(m),
+                            ptr<unsigned long long>(m->bslot), ptr<RowSlot>(m->vslot), ptr<TD>(m->vt),
+                            ptr<TC>(m->s0)));
+        SVX_LAUNCHED();
+    }
     return SVX_OK;
 }
 
