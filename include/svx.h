@@ -155,6 +155,29 @@ svx_status svx_integrate_world(svx_map* map, const void* points_world, int32_t p
                                const void* feats, int32_t feats_dtype, void* stream,
                                svx_report* report);
 
+/* ---- depth frames ---------------------------------------
+ * Replaces ingest.project_depth (ingest.py:285-322) followed by integrate on
+ * the returned Frame: pixel (u, v) of the raster, sampled every `stride`
+ * pixels from (0, 0), with depth d > 0 and finite maps to the sensor-frame
+ * point (((u - cx) * d) / fx, ((v - cy) * d) / fy, d) * depth_scale, in f64;
+ * the payload raster gives the point's label (int32, (H, W)) or features
+ * ((H, W, D), SVX_F32 | SVX_F64).  Invalid pixels are not points (they do not
+ * count in points_in or any skip counter), exactly as project_depth drops them.
+ * depth_dtype: SVX_F32, SVX_F64 or SVX_U16.  Camera validation follows
+ * CameraConfig.validate (config.py:126-134) -> SVX_E_CONFIG. */
+enum { SVX_U16 = 2 };
+typedef struct {
+    double fx, fy, cx, cy;
+    double depth_scale;
+    int32_t width, height;
+    int32_t stride;
+    int32_t pad;
+} svx_camera;
+svx_status svx_integrate_depth(svx_map* map, const void* depth, int32_t depth_dtype,
+                               const svx_camera* camera, const double pose[16],
+                               const int32_t* labels, const void* feats, int32_t feats_dtype,
+                               void* stream, svx_report* report);
+
 /* ---- sharded integration (no reference counterpart) -----------
  * A map sharded over G ranks (one GPU each): rank r holds the leaves with
  * svx_leaf_owner(leaf, G) == r.  Each frame is split into G contiguous point

@@ -217,3 +217,30 @@ def raycast_band(origin, endpoint, voxel_size, truncation, space_carving=False):
     if n < 0:
         raise OracleError(6, "ray band exceeds step budget")
     return out[:n].copy()
+
+
+def project_depth(depth, payload, camera):
+    """Depth raster -> sensor-frame points + payload, restating
+    ingest.project_depth (ingest.py:285-322): pixels sampled every `stride`
+    from (0, 0) in row-major order; d > 0 and finite only; point
+    ((u - cx) * d / fx, (v - cy) * d / fy, d) * depth_scale in f64; integer
+    payloads give int32 labels, float payloads (n, l) f64 features.
+    `camera` is a mapping with the CameraConfig fields."""
+    s = int(camera.get("stride", 1))
+    d = np.asarray(depth)[::s, ::s].astype(np.float64)
+    us = np.arange(0, camera["width"], s, dtype=np.float64)
+    vs = np.arange(0, camera["height"], s, dtype=np.float64)
+    uu, vv = np.meshgrid(us, vs)
+    with np.errstate(invalid="ignore"):
+        ok = (d > 0) & np.isfinite(d)
+    d, uu, vv = d[ok], uu[ok], vv[ok]
+    pts = np.stack([(uu - camera["cx"]) * d / camera["fx"],
+                    (vv - camera["cy"]) * d / camera["fy"],
+                    d], axis=1) * camera.get("depth_scale", 1.0)
+    pay = np.asarray(payload)[::s, ::s]
+    if np.issubdtype(pay.dtype, np.floating):
+        feats = pay[ok].astype(np.float64)
+        if feats.ndim == 1:
+            feats = feats[:, None]
+        return pts, None, feats
+    return pts, pay[ok].astype(np.int32), None

@@ -56,6 +56,19 @@ class SvxReport(ctypes.Structure):
     ]
 
 
+class SvxCamera(ctypes.Structure):
+    _fields_ = [
+        ("fx", ctypes.c_double), ("fy", ctypes.c_double),
+        ("cx", ctypes.c_double), ("cy", ctypes.c_double),
+        ("depth_scale", ctypes.c_double),
+        ("width", ctypes.c_int32), ("height", ctypes.c_int32),
+        ("stride", ctypes.c_int32), ("pad", ctypes.c_int32),
+    ]
+
+
+SVX_U16 = 2
+
+
 class SvxStats(ctypes.Structure):
     _fields_ = [
         ("leaf_count", ctypes.c_int64),
@@ -105,6 +118,8 @@ _SIGNATURES = {
     # pose / origin as a raw address (a numpy array's .ctypes.data)
     "svx_integrate": [_P, _P, _I32, _I64, _P, _P, _P, _I32, _P, ctypes.POINTER(SvxReport)],
     "svx_integrate_world": [_P, _P, _I32, _I64, _P, _P, _P, _I32, _P,
+                            ctypes.POINTER(SvxReport)],
+    "svx_integrate_depth": [_P, _P, _I32, ctypes.POINTER(SvxCamera), _P, _P, _P, _I32, _P,
                             ctypes.POINTER(SvxReport)],
     "svx_stats_get": [_P, ctypes.POINTER(SvxStats)],
     "svx_active_count": [_P, ctypes.POINTER(_I64)],

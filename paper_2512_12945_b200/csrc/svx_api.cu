@@ -201,7 +201,7 @@ svx_status svx_destroy(svx_map* m) {
     cudaSetDevice(m->cfg.device);
     DevBuf* bufs[] = {&m->hash, &m->bcoord, &m->bkey, &m->bmask, &m->bslot, &m->vt,
                       &m->s0, &m->s1, &m->vrec, &m->vslot, &m->in_pts,
-                      &m->in_lab, &m->in_feat, &m->ray, &m->rcnt, &m->roff, &m->rowkey,
+                      &m->in_lab, &m->in_feat, &m->dp_depth, &m->dp_lab_in, &m->dp_feat_in, &m->dp_pts, &m->dp_lab, &m->dp_feat, &m->ray, &m->rcnt, &m->roff, &m->rowkey,
                       &m->rowvid, &m->rowray, &m->rowd, &m->rowlab, &m->partials, &m->tlist, &m->mlist,
                       &m->longlist, &m->srid, &m->bitmap, &m->rcount, &m->cubtmp, &m->ctr, &m->ord0,
                       &m->ord1, &m->ordk0, &m->ordk1, &m->ordf0, &m->ordf1, &m->act_cnt,
@@ -237,6 +237,22 @@ svx_status svx_integrate(svx_map* m, const void* points, int32_t points_dtype, i
     const int dev = (points_dtype & SVX_DEVICE_INPUTS) ? 1 : 0;
     return integrate_impl(m, points, (points_dtype & 0xff) == SVX_F64, n, pp, labels, feats,
                           (feats_dtype & 0xff) == SVX_F64, (cudaStream_t)stream, report, dev);
+}
+
+svx_status svx_integrate_depth(svx_map* m, const void* depth, int32_t depth_dtype,
+                               const svx_camera* camera, const double pose[16],
+                               const int32_t* labels, const void* feats, int32_t feats_dtype,
+                               void* stream, svx_report* report) {
+    if (!m || !depth || !camera || !pose) return fail(SVX_E_INPUT, "null argument");
+    SVX_TRY(set_device(m));
+    PoseParams pp;
+    for (int r = 0; r < 3; ++r) {
+        for (int c = 0; c < 3; ++c) pp.R[3 * r + c] = pose[4 * r + c];
+        pp.t[r] = pose[4 * r + 3];
+    }
+    pp.sensor = 1;
+    return integrate_depth_impl(m, depth, depth_dtype & 0xff, *camera, pp, labels, feats,
+                                (feats_dtype & 0xff) == SVX_F64, (cudaStream_t)stream, report);
 }
 
 svx_status svx_integrate_world(svx_map* m, const void* points_world, int32_t points_dtype,

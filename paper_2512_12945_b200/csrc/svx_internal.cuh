@@ -236,6 +236,7 @@ struct svx_map {
     unsigned seq = 0;   // frame launches so far (attempts included)
     // per-frame scratch
     svx::DevBuf in_pts, in_lab, in_feat;
+    svx::DevBuf dp_depth, dp_lab_in, dp_feat_in, dp_pts, dp_lab, dp_feat;   // depth frames
     svx::DevBuf ray, rcnt, roff, rowkey, rowvid, rowray, rowd, rowlab, partials;
     svx::DevBuf tlist, mlist, longlist, srid, bitmap, rcount;
     uint64_t ucap = 0, rcap = 0;
@@ -563,6 +564,11 @@ __host__ __device__ inline int leaf_owner(long long a, long long b, long long c,
 svx_status build_active_list(svx_map* m, int64_t* count, cudaStream_t s);
 svx_status launch_leaf_stamps(svx_map* m, int32_t* frame, uint64_t* key, int32_t* count,
                               cudaStream_t s);
+
+// depth frames (svx_depth.cu)
+svx_status integrate_depth_impl(svx_map* m, const void* depth, int depth_dtype, const svx_camera& cam,
+                                const PoseParams& pp, const int32_t* labels, const void* feats,
+                                int feats_f64, cudaStream_t s, svx_report* rep);
 
 // sharded integration (svx_shard.cu)
 svx_status shard_march(svx_map* m, const void* pts, int pts_f64, int64_t n, const PoseParams& pp,

@@ -168,6 +168,10 @@ class _Arg:
             if kind == "int32":
                 t = x if x.dtype == torch.int32 else x.to(torch.int32)
                 self.code = None
+            elif kind == "depth" and x.dtype in (torch.float32, torch.float64, torch.uint16):
+                t = x
+                self.code = {torch.float32: SVX_F32, torch.float64: SVX_F64,
+                             torch.uint16: _lib.SVX_U16}[x.dtype]
             elif x.dtype in (torch.float32, torch.float64):
                 t = x
                 self.code = SVX_F64 if x.dtype == torch.float64 else SVX_F32
@@ -190,6 +194,13 @@ class _Arg:
         if kind == "int32":
             a = np.ascontiguousarray(x, np.int32)
             self.code = None
+        elif kind == "depth":
+            a = np.asarray(x)
+            if a.dtype not in (np.float32, np.float64, np.uint16):
+                a = a.astype(np.float64)
+            a = np.ascontiguousarray(a)
+            self.code = {np.dtype(np.float32): SVX_F32, np.dtype(np.float64): SVX_F64,
+                         np.dtype(np.uint16): _lib.SVX_U16}[a.dtype]
         else:
             a = np.asarray(x)
             if a.dtype not in (np.float32, np.float64):
@@ -202,6 +213,33 @@ class _Arg:
 
     def finite_host(self):
         return None if self.cuda else self.keep
+
+
+def _camera_arg(camera):
+    """CameraConfig fields (config.py:114-134) -> SvxCamera, validated with
+    the reference's messages."""
+    get = (lambda k, dflt: camera.get(k, dflt)) if isinstance(camera, dict) else \
+        (lambda k, dflt: getattr(camera, k, dflt))
+    c = _lib.SvxCamera()
+    c.fx, c.fy = float(get("fx", 0.0)), float(get("fy", 0.0))
+    c.cx, c.cy = float(get("cx", 0.0)), float(get("cy", 0.0))
+    c.depth_scale = float(get("depth_scale", 1.0))
+    c.width, c.height, c.stride = int(get("width", 0)), int(get("height", 0)), int(get("stride", 1))
+    if c.fx <= 0 or c.fy <= 0:
+        raise ConfigError("fx and fy must be positive")
+    if c.width < 1 or c.height < 1:
+        raise ConfigError("raster dimensions must be positive")
+    if c.depth_scale <= 0:
+        raise ConfigError("depth_scale must be positive")
+    if c.stride < 1:
+        raise ConfigError("stride must be >= 1")
+    return c
+
+
+def _is_float_raster(x) -> bool:
+    if _is_torch(x):
+        return x.dtype.is_floating_point
+    return np.issubdtype(np.asarray(x).dtype, np.floating)
 
 
 def _stream_for(args):
@@ -443,6 +481,57 @@ class Mapper:
         check(st)
         self._frames += 1
         rep = self._rep
+        return IntegrationReport(
+            points_in=rep.points_in, points_used=rep.points_used,
+            skipped_nonfinite=rep.skipped_nonfinite, skipped_range=rep.skipped_range,
+            skipped_degenerate=rep.skipped_degenerate, skipped_bad_label=rep.skipped_bad_label,
+            band_hits=rep.band_hits, touched_voxels=rep.touched_voxels,
+            kernel_ms=rep.kernel_ms, new_blocks=rep.new_blocks, new_voxels=rep.new_voxels)
+
+    def integrate_depth(self, depth, payload, camera, pose=None):
+        """Back-project a depth raster on the GPU and fuse it: the
+        reference's ``ingest.project_depth(depth, payload, intr, pose)``
+        (ingest.py:285-322) followed by ``integrate`` on the returned Frame.
+        ``camera`` has the CameraConfig fields (fx, fy, cx, cy, width, height,
+        depth_scale, stride; an object or a mapping); ``payload`` is an
+        integer (H, W) label raster or a float (H, W[, l]) feature raster.
+        Rasters may be numpy arrays or CUDA tensors."""
+        cam = _camera_arg(camera)
+        d = _Arg(depth, "depth")
+        if tuple(d.shape) != (cam.height, cam.width):
+            raise ConfigError(f"depth raster {tuple(d.shape)} does not match camera "
+                              f"({cam.height}, {cam.width})")
+        pshape = tuple(payload.shape)
+        if pshape[:2] != tuple(d.shape):
+            raise ConfigError(f"payload raster {pshape[:2]} does not match depth {tuple(d.shape)}")
+        is_float = _is_float_raster(payload)
+        lab = feat = None
+        if is_float:
+            feat = _Arg(payload, "float")
+            dim = 1 if len(pshape) == 2 else pshape[2]
+            if self._closed is not None:
+                raise PayloadMismatchError("closed-set grid requires per-point labels")
+            if self._open is not None and dim != self._open.feature_dim:
+                raise PayloadMismatchError(
+                    f"feature dim {dim} != grid dim {self._open.feature_dim}")
+        else:
+            lab = _Arg(payload, "int32")
+            if self._open is not None:
+                raise PayloadMismatchError("open-set grid requires per-point features")
+        if self._closed is None:
+            lab = None
+        if self._open is None:
+            feat = None
+        pose = np.eye(4) if pose is None else pose
+        pose = _check_pose(pose, self._frames)
+        rep = self._rep
+        stream, _ = _stream_for((d, lab, feat))
+        vec = np.ascontiguousarray(pose.reshape(-1), np.float64)
+        check(lib.svx_integrate_depth(
+            self._handle, d.ptr, d.code, ctypes.byref(cam), vec.ctypes.data,
+            lab.ptr if lab is not None else None, feat.ptr if feat is not None else None,
+            feat.code if feat is not None else SVX_F32, stream, self._rep_ref))
+        self._frames += 1
         return IntegrationReport(
             points_in=rep.points_in, points_used=rep.points_used,
             skipped_nonfinite=rep.skipped_nonfinite, skipped_range=rep.skipped_range,

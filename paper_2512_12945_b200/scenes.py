@@ -292,6 +292,8 @@ class FrameData:
     labels: torch.Tensor | None
     features: torch.Tensor | None
     truth: torch.Tensor
+    depth: torch.Tensor | None = None    # depth cameras: (H, W) f32 z-depth, NaN = no return
+    camera: dict | None = None           # CameraConfig fields of that raster
 
     @property
     def origin(self):
@@ -379,7 +381,11 @@ def _camera_workload(name, scene, width, height, f, n_frames, radius, height_m, 
             labels = closed_labels(truth, num_classes, 0.5, 0.7, wrong_frac, gen, device)
         else:
             feats = open_features(truth, centres, 0.05, gen, device)
-        return FrameData(ps, pose, pw, labels, feats, truth)
+        depth_raster = depth.to(torch.float32).reshape(height, width)
+        depth_raster[~torch.isfinite(t).reshape(height, width)] = float("nan")
+        camera = dict(fx=float(f), fy=float(f), cx=width / 2.0, cy=height / 2.0, width=width,
+                      height=height, depth_scale=1.0, stride=1)
+        return FrameData(ps, pose, pw, labels, feats, truth, depth_raster, camera)
 
     queries = None
     if n_queries:

@@ -214,8 +214,80 @@ def plane_frames(seed, n, frames, labels_k=0, feat_dim=0, with_bad=True):
     return out
 
 
+def depth_scenario(name, mapper_kw, camera, frames):
+    """The reference's depth path: ingest.project_depth (ingest.py:285-322)
+    then Mapper.integrate on the Frame (identity rotations: exact BLAS).
+    frames: list of (depth raster, payload raster, pose)."""
+    from semvox.config import CameraConfig
+    from semvox.ingest import project_depth
+
+    intr = CameraConfig(**camera)
+    m = sb.Mapper(**mapper_kw)
+    reps = []
+    out = {"mode": np.array("depth"), "camera": np.array(repr(camera))}
+    for i, (depth, payload, pose) in enumerate(frames):
+        fr = project_depth(depth, payload, intr, pose=pose, frame_id=i)
+        out[f"depth_{i}"] = depth
+        out[f"payload_{i}"] = payload
+        out[f"pose_{i}"] = pose
+        out[f"ref_points_{i}"] = fr.points
+        reps.append(m.integrate(fr.points, pose, labels=fr.labels, features=fr.features))
+    tsdf, sem = m.grids
+    kind = "closed" if mapper_kw.get("num_classes") else ("open" if mapper_kw.get("feature_dim") else None)
+    out["reports"] = _reports_array(reps)
+    out["n_frames"] = np.array(len(frames))
+    out["mapper_kw"] = np.array(repr(mapper_kw))
+    _dump_state(out, tsdf, sem, kind)
+    np.savez_compressed(os.path.join(HERE, name + ".npz"), **out)
+    print(name, "frames", len(frames), "active", out["coords"].shape[0])
+
+
+def depth_frames(seed, H, W, frames, labels_k=0, feat_dim=0, dtype=np.float32, scale=1.0):
+    """A tilted wall seen by a camera translating along x (identity
+    rotation), with zero, negative and non-finite depth pixels."""
+    rng = np.random.default_rng(seed)
+    out = []
+    vv, uu = np.meshgrid(np.arange(H), np.arange(W), indexing="ij")
+    for i in range(frames):
+        z = 1.5 + 0.4 * uu / W + 0.2 * vv / H + rng.normal(0, 0.005, (H, W))
+        raw = z / scale
+        if np.issubdtype(dtype, np.integer):
+            raw = np.round(raw).astype(dtype)
+            raw[rng.random((H, W)) < 0.03] = 0
+        else:
+            raw = raw.astype(dtype)
+            raw[rng.random((H, W)) < 0.03] = 0.0
+            raw[rng.random((H, W)) < 0.02] = np.nan
+            raw[rng.random((H, W)) < 0.01] = -1.0
+        if labels_k:
+            pay = rng.integers(0, labels_k + 1, (H, W)).astype(np.int64)
+        else:
+            pay = rng.normal(size=(H, W, feat_dim)).astype(np.float32)
+        pose = np.eye(4)
+        pose[:3, 3] = [0.05 * i, 0.0, 0.0]
+        out.append((raw, pay, pose))
+    return out
+
+
+def main_depth():
+    # -- depth frames (project_depth + integrate) ---------------------------------
+    cam = dict(fx=50.0, fy=52.0, cx=31.5, cy=23.0, width=64, height=48, depth_scale=1.0, stride=1)
+    depth_scenario("depth_closed_f32", dict(voxel_size=0.05, truncation=0.15, num_classes=5),
+                   cam, depth_frames(11, 48, 64, 3, labels_k=5))
+    cam2 = dict(cam, stride=2, depth_scale=0.001)
+    depth_scenario("depth_closed_u16_stride2", dict(voxel_size=0.05, truncation=0.15, num_classes=5),
+                   cam2, depth_frames(12, 48, 64, 2, labels_k=5, dtype=np.uint16, scale=0.001))
+    depth_scenario("depth_open_f32_stride2", dict(voxel_size=0.05, truncation=0.15, feature_dim=4),
+                   dict(cam, stride=2), depth_frames(13, 48, 64, 2, feat_dim=4))
+
+
 def main():
     from paper_2512_12945_b200 import scenes
+
+    if "depth" in sys.argv[1:]:   # only the depth scenarios
+        main_depth()
+        return
+    main_depth()
 
     # -- API level ------------------------------------------------------------
     api_scenario("api_closed_plane", plane_frames(0, 600, 4, labels_k=4),

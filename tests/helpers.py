@@ -22,8 +22,15 @@ RTOL = 1e-5
 
 
 def golden_names():
+    """Point-cloud fixtures (api_* / seam_*); depth_* fixtures: depth_names()."""
     return sorted(os.path.splitext(os.path.basename(p))[0]
-                  for p in glob.glob(os.path.join(GOLDEN, "*.npz")))
+                  for p in glob.glob(os.path.join(GOLDEN, "*.npz"))
+                  if not os.path.basename(p).startswith("depth_"))
+
+
+def depth_names():
+    return sorted(os.path.splitext(os.path.basename(p))[0]
+                  for p in glob.glob(os.path.join(GOLDEN, "depth_*.npz")))
 
 
 def load_golden(name):
