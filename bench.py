@@ -51,6 +51,9 @@ def parse_args():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--depth", action="store_true",
+                    help="camera configs (1, 3, 5): feed depth rasters through integrate_depth "
+                         "(back-projection on the GPU) instead of point clouds")
     ap.add_argument("--tsdf-dtype", default="float64")
     ap.add_argument("--cpu-frames", type=int, default=0, help="oracle sample frames (0=auto)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -275,6 +278,13 @@ def run_ours(args):
             pts, lab, feat = host
         else:
             pts, lab, feat = f.points, f.labels, f.features
+        if args.depth:   # pts = depth raster, lab/feat = payload raster
+            pay = lab if kind == "closed" else feat
+            if host is None:
+                h, w = f.camera["height"], f.camera["width"]
+                pts = f.depth
+                pay = f.labels.reshape(h, w) if kind == "closed" else f.features.reshape(h, w, -1)
+            return m.integrate_depth(pts, pay, f.camera, pose=f.pose)
         extra = {"reduce_report": False} if sharded else {}
         return m.integrate(pts, f.pose, labels=lab if kind == "closed" else None,
                            features=feat if kind == "open" else None, **extra)
@@ -352,15 +362,19 @@ def run_ours(args):
     if not args.no_e2e:
         host = []
         for f in frames:
-            pts = torch.empty(f.points.shape, dtype=f.points.dtype, pin_memory=True)
-            pts.copy_(f.points)
+            src_pts = f.depth if args.depth else f.points
+            pts = torch.empty(src_pts.shape, dtype=src_pts.dtype, pin_memory=True)
+            pts.copy_(src_pts)
             lab = feat = None
             if f.labels is not None:
-                lab = torch.empty(f.labels.shape, dtype=f.labels.dtype, pin_memory=True)
-                lab.copy_(f.labels)
+                src = f.labels.reshape(f.depth.shape) if args.depth else f.labels
+                lab = torch.empty(src.shape, dtype=src.dtype, pin_memory=True)
+                lab.copy_(src)
             if f.features is not None:
-                feat = torch.empty(f.features.shape, dtype=f.features.dtype, pin_memory=True)
-                feat.copy_(f.features)
+                src = (f.features.reshape(f.depth.shape[0], f.depth.shape[1], -1) if args.depth
+                       else f.features)
+                feat = torch.empty(src.shape, dtype=src.dtype, pin_memory=True)
+                feat.copy_(src)
             host.append((pts.numpy(), lab.numpy() if lab is not None else None,
                          feat.numpy() if feat is not None else None))
         m2 = new_map()
@@ -417,7 +431,10 @@ def run_ours(args):
                 "num_classes": C or None, "feature_dim": D or None,
                 "tsdf_dtype": args.tsdf_dtype,
                 "api": ("ShardedMapper.integrate -> svx_shard_{march,plan,pack,apply} + NCCL "
-                        "all-to-all" if sharded else "Mapper.integrate -> svx_integrate"),
+                        "all-to-all" if sharded else
+                        ("Mapper.integrate_depth -> svx_integrate_depth (depth rasters, "
+                         "back-projection on the GPU)" if args.depth else
+                         "Mapper.integrate -> svx_integrate")),
                 "parallelism": f"leaf-shard{world}" if sharded else "single",
                 "l2": "flushed between steps (256 MiB write + 256 MiB read, outside step events)",
                 "frames_timed": f"{W}..{W + K - 1}",
