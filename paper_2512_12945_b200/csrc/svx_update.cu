@@ -941,7 +941,10 @@ UpdateArgs make_args(svx_map* m) {
 }
 
 constexpr int kShortBlocks = 148 * 8;
-constexpr int kLongBlocks = 148 * 4;
+#ifndef SVX_LONG_BLOCKS
+#define SVX_LONG_BLOCKS (148 * 4)
+#endif
+constexpr int kLongBlocks = SVX_LONG_BLOCKS;
 
 template <class TD, class TC>
 svx_status scatter_t(svx_map* m, cudaStream_t s) {

@@ -311,6 +311,30 @@ def test_classify_fp64_tensor_core_vs_oracle(k):
     np.testing.assert_allclose(sims[:, 0], s0, rtol=1e-12, atol=1e-14, equal_nan=True)
 
 
+@pytest.mark.parametrize("mode", ["slots", "segments"])
+def test_capacity_retries_vs_oracle(mode):
+    """Tiny initial pools: frames run out of leaves and voxels mid-flight, are
+    cleaned up, grown and re-run (recover_capacity / k_cleanup(_slots));
+    the map must still equal the oracle's bit for bit."""
+    from paper_2512_12945_b200 import Mapper, scenes
+    from oracle.oracle import OracleMap
+
+    wl = scenes.workload(2, device="cuda")
+    m = Mapper(**wl.mapper_kwargs, reserve_voxels=64, reserve_blocks=4)
+    m.set_update_mode(mode)
+    om = OracleMap(**wl.mapper_kwargs)
+    for i in range(3):
+        f = wl.make_frame(i * 7)
+        r1 = m.integrate(f.points, f.pose, labels=f.labels)
+        r2 = om.integrate(f.points.cpu().numpy(), f.pose, labels=f.labels.cpu().numpy())
+        assert np.array_equal(report_rows([r1]), report_rows([r2]))
+    c, d, w, s0, _ = m._export()
+    oc, od, ow, os0, _ = om.export()
+    assert np.array_equal(c, oc)
+    assert np.array_equal(d, od) and np.array_equal(w, ow)
+    assert np.array_equal(s0, os0)
+
+
 def test_update_mode_argument():
     from paper_2512_12945_b200 import Mapper
 
