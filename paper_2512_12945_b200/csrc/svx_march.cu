@@ -204,13 +204,44 @@ __device__ __forceinline__ void publish_tally(const Tally& t, FrameCtr* ctr) {
     }
 }
 
+// Open-set validation (features all finite), warp-cooperative: the warp
+// checks its lanes' feature rows one after another with coalesced loads
+// (a per-thread loop over D would read 32 rows with stride D).  Called by
+// all 32 lanes; `has` = this lane has a point to check.
+template <class Fe>
+__device__ __forceinline__ bool warp_feats_finite(const Fe* __restrict__ feats, int D, long long i,
+                                                  bool has) {
+    const int lane = threadIdx.x & 31;
+    bool mine = true;
+    unsigned todo = __ballot_sync(0xffffffffu, has);
+    while (todo) {
+        const int src = __ffs(todo) - 1;
+        todo &= todo - 1;
+        const long long pi = __shfl_sync(0xffffffffu, i, src);
+        const Fe* f = feats + pi * D;
+        bool ok = true;
+        if (sizeof(Fe) == 4 && (D & 3) == 0) {
+            const float4* f4 = reinterpret_cast<const float4*>(f);
+            for (int c = lane; c < (D >> 2); c += 32) {
+                const float4 v = __ldg(f4 + c);
+                ok = ok && isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w);
+            }
+        } else {
+            for (int c = lane; c < D; c += 32) ok = ok && isfinite((double)f[c]);
+        }
+        ok = __all_sync(0xffffffffu, ok);
+        if (lane == src) mine = ok;
+    }
+    return mine;
+}
+
 // Shared front half of the march for one point: validation masks
 // (integrate_frame, fusion.py:228-256) and ray setup (fusion.py:262-263).
 // Returns true when the point is kept; r = (u, t_surf).
 template <class P, class Fe>
 __device__ __forceinline__ bool prepare_ray(long long i, const FrameParams& fp, double max_range,
                                             int sem_kind, int num_classes, int D, Tally& t,
-                                            double4& r) {
+                                            double4& r, bool feats_ok = true) {
     double x, y, z;
     load_point((const P*)fp.pts, i, x, y, z);
     const PoseParams& pp = fp.pp;
@@ -238,9 +269,7 @@ __device__ __forceinline__ bool prepare_ray(long long i, const FrameParams& fp, 
         t.bad_label += keep && !good;
         keep = keep && good;
     } else if (sem_kind == SVX_SEM_OPEN) {
-        bool good = true;
-        const Fe* f = (const Fe*)fp.feats + i * D;
-        for (int c = 0; c < D; ++c) good = good && isfinite((double)f[c]);
+        const bool good = feats_ok;   // warp_feats_finite, evaluated by the caller
         t.bad_label += keep && !good;
         keep = keep && good;
     }
@@ -323,9 +352,11 @@ __global__ void __launch_bounds__(kTileRays, SVX_WALK_MINB) k_walk(MarchParams m
         const long long i = tile * kTileRays + threadIdx.x;
         int rows = 0;
         unsigned long long* rk = s_keys + (size_t)threadIdx.x * maxrows;
+        const bool fok = sem_kind != SVX_SEM_OPEN ||
+                         warp_feats_finite<Fe>((const Fe*)fp.feats, D, i, i < n);
         if (i < n) {
             double4 r;
-            if (prepare_ray<P, Fe>(i, fp, mp.max_range, sem_kind, num_classes, D, t, r)) {
+            if (prepare_ray<P, Fe>(i, fp, mp.max_range, sem_kind, num_classes, D, t, r, fok)) {
                 long long f0 = 0, f1 = 0, f2 = 0, l0 = 0, l1 = 0, l2 = 0;
                 int nk = 0;
                 int pl0 = INT_MIN, pl1 = INT_MIN, pl2 = INT_MIN;   // last prefetched leaf
@@ -442,15 +473,20 @@ __global__ void __launch_bounds__(kMarchThreads) k_walk_count(MarchParams mp, in
     const long long n = fp.n;
     const double ox = fp.pp.t[0], oy = fp.pp.t[1], oz = fp.pp.t[2];
     Tally t;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < npts_cap;
-         i += (long long)gridDim.x * blockDim.x) {
+    // warp-uniform trip count (warp_feats_finite needs every lane)
+    for (long long i0 = (long long)blockIdx.x * blockDim.x; i0 < npts_cap;
+         i0 += (long long)gridDim.x * blockDim.x) {
+        const long long i = i0 + threadIdx.x;
+        const bool fok = sem_kind != SVX_SEM_OPEN ||
+                         warp_feats_finite<Fe>((const Fe*)fp.feats, D, i, i < n);
+        if (i >= npts_cap) continue;
         if (i >= n) {
             rcnt[i] = 0;
             continue;
         }
         double4 r;
         int rows = 0;
-        if (prepare_ray<P, Fe>(i, fp, mp.max_range, sem_kind, num_classes, D, t, r)) {
+        if (prepare_ray<P, Fe>(i, fp, mp.max_range, sem_kind, num_classes, D, t, r, fok)) {
             long long emitted = dda_walk(ox, oy, oz, r.x, r.y, r.z, r.w, mp,
                 [&](long long ci, long long cj, long long ck) {
                     if (!row_kept(ci, cj, ck, ox, oy, oz, r, mp)) return;

@@ -760,7 +760,33 @@ template <class Fe>
 __device__ __forceinline__ void open_chunk(const Fe* __restrict__ feats, int D, int base,
                                            const int* buf, int cnt, double* sz, double* sz2) {
     const int lane = threadIdx.x & 31;
-    for (int j = 0; j < cnt; ++j) {
+    // 4 rows' values in flight at once, then folded in row order (the sums
+    // stay the sequential point-ordered ones)
+    int j = 0;
+    for (; j + 4 <= cnt; j += 4) {
+        Fe v[4][kOpenPer];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const Fe* f = feats + (long long)buf[j + u] * D + base;
+#pragma unroll
+            for (int q = 0; q < kOpenPer; ++q) {
+                const int cc = lane + 32 * q;
+                v[u][q] = base + cc < D ? f[cc] : (Fe)0;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+#pragma unroll
+            for (int q = 0; q < kOpenPer; ++q) {
+                if (base + lane + 32 * q < D) {
+                    const double zv = (double)v[u][q];
+                    sz[q] += zv;
+                    sz2[q] += zv * zv;
+                }
+            }
+        }
+    }
+    for (; j < cnt; ++j) {
         const Fe* f = feats + (long long)buf[j] * D + base;
 #pragma unroll
         for (int q = 0; q < kOpenPer; ++q) {
