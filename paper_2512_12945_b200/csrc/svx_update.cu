@@ -760,32 +760,7 @@ template <class Fe>
 __device__ __forceinline__ void open_chunk(const Fe* __restrict__ feats, int D, int base,
                                            const int* buf, int cnt, double* sz, double* sz2) {
     const int lane = threadIdx.x & 31;
-    // 4 rows' values in flight at once, then folded in row order (the sums
-    // stay the sequential point-ordered ones)
     int j = 0;
-    for (; j + 4 <= cnt; j += 4) {
-        Fe v[4][kOpenPer];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const Fe* f = feats + (long long)buf[j + u] * D + base;
-#pragma unroll
-            for (int q = 0; q < kOpenPer; ++q) {
-                const int cc = lane + 32 * q;
-                v[u][q] = base + cc < D ? f[cc] : (Fe)0;
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-#pragma unroll
-            for (int q = 0; q < kOpenPer; ++q) {
-                if (base + lane + 32 * q < D) {
-                    const double zv = (double)v[u][q];
-                    sz[q] += zv;
-                    sz2[q] += zv * zv;
-                }
-            }
-        }
-    }
     for (; j < cnt; ++j) {
         const Fe* f = feats + (long long)buf[j] * D + base;
 #pragma unroll
@@ -889,33 +864,170 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) k_update_open(UpdateArgs a,
     }
 }
 
+// K5 open, voxels of more than 1024 rows (a depth camera close to a
+// surface funnels most of its rays into a few voxels): one CTA per voxel.
+// The voxel's point indices go into a bitmap (per-CTA global scratch), are
+// extracted in ascending chunks of up to kHugeChunk into shared memory with
+// each row's d and w, and then: thread 0 folds the TSDF sums in order while
+// every thread folds the feature sums of its own dimensions in order (the
+// dims are independent, so a voxel's D sums run in parallel; the rows'
+// features are read coalesced, 4 rows in flight).  Sums are the sequential
+// point-ordered fp64 sums of the warp path.
+constexpr int kHugeThreads = 256;
+constexpr int kHugeChunk = 2048;         // rows per shared-memory chunk (64 bitmap words)
+constexpr int kHugeCtas = kHugeWarps;    // CTAs sharing the bitmap scratch
+constexpr int kHugeDims = 3;             // dims per thread and pass (768 per pass)
+
 template <class TD, class TS, class Fe>
-__device__ __forceinline__ void k_update_open_huge_body(UpdateArgs a, TD* vt,
-                                                                        TS* mean, TS* beta) {
+__device__ __forceinline__ void k_update_open_huge_body(UpdateArgs a, TD* vt, TS* mean, TS* beta) {
     grid_dep_wait();
-    __shared__ int sbuf[kWarpsPerCta][kSmemMax];
+    __shared__ int s_id[kHugeChunk];
+    __shared__ double s_d[kHugeChunk];
+    __shared__ double s_w[kHugeChunk];
+    __shared__ int s_wcnt[kHugeThreads / 32];
+    __shared__ int s_min, s_max, s_cnt;
+    __shared__ double s_wold;
     FrameCtr* ctr = a.ctr;
     KSpan _ks(ctr, kSpanUpdateB);
     __shared__ FrameCtr s_ctr_;
     snapshot_ctr(ctr, s_ctr_);
     const FrameCtr* cv = &s_ctr_;
     if (cv->abort | cv->err_cap) return;
-    const int wib = threadIdx.x >> 5;
-    const long long gw = (long long)blockIdx.x * kWarpsPerCta + wib;
-    unsigned* bm = a.bitmap + gw * a.bm_words;
+    const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
+    unsigned* bm = a.bitmap + (long long)blockIdx.x * a.bm_words;
     const long long Hn = (long long)cv->n_huge;
     const KeyPack kp = cv->p.kp;
     const PoseParams pp = cv->p.pp;
     const Fe* feats = (const Fe*)cv->p.feats;
-    for (long long t = gw; t < Hn; t += (long long)gridDim.x * kWarpsPerCta) {
+    const int D = a.D;
+    for (long long t = blockIdx.x; t < Hn; t += gridDim.x) {
         const int vid = a.mlist[a.hugelist[t]];
-        open_voxel<TD, TS, Fe>(a, kp, pp, vt, mean, beta, feats, vid, a.rec[vid].cnt, sbuf[wib], bm,
-                               true);
+        const unsigned c = a.rec[vid].cnt;
+        const unsigned k = c & ~kNewBit;
+        const bool isnew = (c & kNewBit) != 0u;
+        const unsigned seg = a.rec[vid].seg;
+        // ---- point-index bitmap of the voxel's rows
+        if (tid == 0) { s_min = 0x7fffffff; s_max = -1; }
+        __syncthreads();
+        int mn = 0x7fffffff, mx = -1;
+        for (unsigned j = tid; j < k; j += kHugeThreads) {
+            const int v = a.srid[seg + j];
+            mn = min(mn, v);
+            mx = max(mx, v);
+        }
+        mn = __reduce_min_sync(0xffffffffu, (unsigned)mn) ;
+        mx = (int)__reduce_max_sync(0xffffffffu, (unsigned)(mx + 1)) - 1;
+        if (lane == 0) { atomicMin(&s_min, mn); atomicMax(&s_max, mx); }
+        __syncthreads();
+        const int minr = s_min;
+        const long long nwords = ((long long)(s_max - minr) >> 5) + 1;
+        for (long long w = tid; w < nwords; w += kHugeThreads) bm[w] = 0u;
+        __syncthreads();
+        for (unsigned j = tid; j < k; j += kHugeThreads) {
+            const int v = a.srid[seg + j] - minr;
+            atomicOr(&bm[v >> 5], 1u << (v & 31));
+        }
+        __threadfence_block();
+        __syncthreads();
+        const Center cc = center_of(a.rec[vid].key, kp, a.h, pp);
+        TsdfAcc acc{0.0, 0.0, INFINITY, -INFINITY, 0};
+        // dims in passes of kHugeDims * kHugeThreads (one pass for D <= 768)
+        for (int dbase = 0; dbase < D; dbase += kHugeDims * kHugeThreads) {
+        const bool first_pass = dbase == 0;
+        double sz[kHugeDims], sz2[kHugeDims];
+#pragma unroll
+        for (int q = 0; q < kHugeDims; ++q) { sz[q] = 0.0; sz2[q] = 0.0; }
+        // ---- ascending chunks of 64 words (<= 2048 rows)
+        for (long long w0 = 0; w0 < nwords; w0 += kHugeChunk / 32) {
+            // 64 words: one per thread of the first two warps
+            unsigned bits = 0u;
+            const long long w = w0 + tid;
+            if (tid < kHugeChunk / 32 && w < nwords) bits = __ldcg(bm + w);
+            int cntw = __popc(bits);
+            int incl = cntw;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            if (lane == 31) s_wcnt[wib] = incl;
+            __syncthreads();
+            int pos = incl - cntw + (wib == 1 ? s_wcnt[0] : 0);
+            if (tid == 0) s_cnt = s_wcnt[0] + s_wcnt[1];
+            while (bits) {
+                const int bpos = __ffs(bits) - 1;
+                bits &= bits - 1;
+                s_id[pos++] = minr + (int)(w * 32 + bpos);
+            }
+            __syncthreads();
+            const int cnt = s_cnt;
+            if (first_pass) {
+                for (int j = tid; j < cnt; j += kHugeThreads) {
+                    double d, wr;
+                    row_dw(cc.x, cc.y, cc.z, a.ray[s_id[j]], a.trunc, a.wfn, d, wr);
+                    s_d[j] = d;
+                    s_w[j] = wr;
+                }
+            }
+            __syncthreads();
+            if (tid == 0 && first_pass) {
+                for (int j = 0; j < cnt; ++j) {
+                    const double wq = s_w[j], dq = s_d[j];
+                    acc.sw += wq;
+                    acc.swd += wq * dq;
+                    acc.mind = dq < acc.mind ? dq : acc.mind;
+                    acc.maxd = dq > acc.maxd ? dq : acc.maxd;
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < kHugeDims; ++q) {
+                const int col = dbase + tid + q * kHugeThreads;
+                if (col >= D) continue;
+                int j = 0;
+                for (; j + 4 <= cnt; j += 4) {
+                    const double z0 = (double)feats[(long long)s_id[j] * D + col];
+                    const double z1 = (double)feats[(long long)s_id[j + 1] * D + col];
+                    const double z2 = (double)feats[(long long)s_id[j + 2] * D + col];
+                    const double z3 = (double)feats[(long long)s_id[j + 3] * D + col];
+                    sz[q] += z0; sz2[q] += z0 * z0;
+                    sz[q] += z1; sz2[q] += z1 * z1;
+                    sz[q] += z2; sz2[q] += z2 * z2;
+                    sz[q] += z3; sz2[q] += z3 * z3;
+                }
+                for (; j < cnt; ++j) {
+                    const double z = (double)feats[(long long)s_id[j] * D + col];
+                    sz[q] += z;
+                    sz2[q] += z * z;
+                }
+            }
+            __syncthreads();
+        }
+        if (first_pass) {
+            if (tid == 0) s_wold = apply_tsdf<TD>(vt, vid, isnew, a.trunc, acc.sw, acc.swd, acc.mind, acc.maxd);
+            __syncthreads();
+        }
+        // NIG batch update with lambda from the pre-frame weight (_pycore.py:438)
+        const double w_old = s_wold;
+        const double nobs = (double)k;
+        const double lam = fmax(w_old, a.lambda_floor);
+        const double lam_post = lam + nobs;
+        const double coef = lam * nobs / lam_post;
+        const double b_bg = (double)(TS)a.prior_beta;
+        TS* mrow = mean + (long long)vid * D;
+        TS* brow = beta + (long long)vid * D;
+#pragma unroll
+        for (int q = 0; q < kHugeDims; ++q) {
+            const int col = dbase + tid + q * kHugeThreads;
+            if (col < D) nig_apply<TS>(mrow, brow, col, isnew, sz[q], sz2[q], lam, lam_post, coef, nobs, b_bg);
+        }
+        }   // dim passes
+        if (tid == 0) clear_voxel_frame(a, vid);
+        __syncthreads();
     }
 }
 
 template <class TD, class TS, class Fe>
-__global__ void __launch_bounds__(32 * kWarpsPerCta) k_update_open_huge(UpdateArgs a, TD* vt, TS* mean, TS* beta) {
+__global__ void __launch_bounds__(kHugeThreads, 1) k_update_open_huge(UpdateArgs a, TD* vt, TS* mean, TS* beta) {
     k_update_open_huge_body<TD, TS, Fe>(a, vt, mean, beta);
     frame_epilogue(a.ctr, a.ctr->p.epilogue, a.ctr->p.mirror);
 }
@@ -1007,7 +1119,7 @@ svx_status open_a(svx_map* m, cudaStream_t s) {
 
 template <class TD, class TS, class Fe>
 svx_status open_b(svx_map* m, cudaStream_t s) {
-    SVX_CUDA(launch_pdl(k_update_open_huge<TD, TS, Fe>, kHugeWarps / kWarpsPerCta, 32 * kWarpsPerCta, 0, s, 
+    SVX_CUDA(launch_pdl(k_update_open_huge<TD, TS, Fe>, kHugeCtas, kHugeThreads, 0, s, 
         make_args(m), ptr<TD>(m->vt), ptr<TS>(m->s0), ptr<TS>(m->s1)));
     SVX_LAUNCHED();
     return SVX_OK;
