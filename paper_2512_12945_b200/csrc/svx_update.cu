@@ -129,7 +129,12 @@ __device__ __forceinline__ void clear_voxel_frame(const UpdateArgs& a, int vid) 
 // sum, _core.pyx:793-795), so closed/geometry maps update it right here;
 // rows of other voxels go to their voxel's segment.
 template <class TD, class TC>
-__global__ void __launch_bounds__(256) k_scatter(UpdateArgs a, const int* __restrict__ rcnt,
+#if defined(SVX_SCATTER_MINB)
+#define SVX_LB_SCATTER __launch_bounds__(256, SVX_SCATTER_MINB)
+#else
+#define SVX_LB_SCATTER __launch_bounds__(256)
+#endif
+__global__ void SVX_LB_SCATTER k_scatter(UpdateArgs a, const int* __restrict__ rcnt,
                                                  const int* __restrict__ rowray,
                                                  const unsigned long long* __restrict__ rowkey,
                                                  const int* __restrict__ rowvid,
@@ -185,7 +190,12 @@ __global__ void __launch_bounds__(256) k_scatter(UpdateArgs a, const int* __rest
 // ---- K5 short: one thread per multi-row voxel (closed / geometry) ----------------
 
 template <class TD, class TC>
-__global__ void __launch_bounds__(256) k_update_short(UpdateArgs a, TD* vt, TC* counts) {
+#if defined(SVX_SHORT_MINB)
+#define SVX_LB_SHORT __launch_bounds__(256, SVX_SHORT_MINB)
+#else
+#define SVX_LB_SHORT __launch_bounds__(256)
+#endif
+__global__ void SVX_LB_SHORT k_update_short(UpdateArgs a, TD* vt, TC* counts) {
     grid_dep_wait();
     FrameCtr* ctr = a.ctr;
     KSpan _ks(ctr, kSpanUpdate);
@@ -727,7 +737,10 @@ __device__ __forceinline__ void k_update_long_body(UpdateArgs a, TD* vt,
 }
 
 template <class TD, class TC>
-__global__ void __launch_bounds__(32 * kWarpsPerCta) k_update_long(UpdateArgs a, TD* vt, TC* counts) {
+#ifndef SVX_LONGK_MINB
+#define SVX_LONGK_MINB 4
+#endif
+__global__ void __launch_bounds__(32 * kWarpsPerCta, SVX_LONGK_MINB) k_update_long(UpdateArgs a, TD* vt, TC* counts) {
     k_update_long_body(a, vt, counts);
     frame_epilogue(a.ctr, a.ctr->p.epilogue, a.ctr->p.mirror);
 }
