@@ -27,7 +27,7 @@ namespace {
 
 constexpr int kSmemMax = 1024;                   // rows per warp buffer (4 KB)
 constexpr int kWarpsPerCta = 8;
-constexpr int kHugeWarps = 128;                  // warps that share the bitmap scratch
+constexpr int kHugeWarps = 296;                  // bitmap scratch slots (huge segments)
 
 // counter += 1 for every converged lane, one atomic per warp; returns this
 // lane's ticket.
@@ -889,7 +889,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) k_update_open(UpdateArgs a,
 constexpr int kHugeThreads = 256;
 constexpr int kHugeChunk = 2048;         // rows per shared-memory chunk (64 bitmap words)
 constexpr int kHugeCtas = kHugeWarps;    // CTAs sharing the bitmap scratch
-constexpr int kHugeDims = 3;             // dims per thread and pass (768 per pass)
+constexpr int kHugeDims = 4;             // dims per feature thread and pass
+constexpr int kHugeFeatThreads = kHugeThreads - 32;   // warp 0 folds the TSDF sums
 
 template <class TD, class TS, class Fe>
 __device__ __forceinline__ void k_update_open_huge_body(UpdateArgs a, TD* vt, TS* mean, TS* beta) {
@@ -944,8 +945,9 @@ __device__ __forceinline__ void k_update_open_huge_body(UpdateArgs a, TD* vt, TS
         __syncthreads();
         const Center cc = center_of(a.rec[vid].key, kp, a.h, pp);
         TsdfAcc acc{0.0, 0.0, INFINITY, -INFINITY, 0};
-        // dims in passes of kHugeDims * kHugeThreads (one pass for D <= 768)
-        for (int dbase = 0; dbase < D; dbase += kHugeDims * kHugeThreads) {
+        // dims in passes of kHugeDims * kHugeFeatThreads (one pass for D <= 896);
+        // warp 0 folds the TSDF sums (thread 0), warps 1.. the feature sums
+        for (int dbase = 0; dbase < D; dbase += kHugeDims * kHugeFeatThreads) {
         const bool first_pass = dbase == 0;
         double sz[kHugeDims], sz2[kHugeDims];
 #pragma unroll
@@ -983,7 +985,7 @@ __device__ __forceinline__ void k_update_open_huge_body(UpdateArgs a, TD* vt, TS
                 }
             }
             __syncthreads();
-            if (tid == 0 && first_pass) {
+            if (tid == 0 && first_pass) {   // independent chains: one dependent add per row each
                 for (int j = 0; j < cnt; ++j) {
                     const double wq = s_w[j], dq = s_d[j];
                     acc.sw += wq;
@@ -994,8 +996,8 @@ __device__ __forceinline__ void k_update_open_huge_body(UpdateArgs a, TD* vt, TS
             }
 #pragma unroll
             for (int q = 0; q < kHugeDims; ++q) {
-                const int col = dbase + tid + q * kHugeThreads;
-                if (col >= D) continue;
+                const int col = dbase + (tid - 32) + q * kHugeFeatThreads;
+                if (tid < 32 || col >= D) continue;
                 int j = 0;
                 for (; j + 4 <= cnt; j += 4) {
                     const double z0 = (double)feats[(long long)s_id[j] * D + col];
@@ -1030,8 +1032,8 @@ __device__ __forceinline__ void k_update_open_huge_body(UpdateArgs a, TD* vt, TS
         TS* brow = beta + (long long)vid * D;
 #pragma unroll
         for (int q = 0; q < kHugeDims; ++q) {
-            const int col = dbase + tid + q * kHugeThreads;
-            if (col < D) nig_apply<TS>(mrow, brow, col, isnew, sz[q], sz2[q], lam, lam_post, coef, nobs, b_bg);
+            const int col = dbase + (tid - 32) + q * kHugeFeatThreads;
+            if (tid >= 32 && col < D) nig_apply<TS>(mrow, brow, col, isnew, sz[q], sz2[q], lam, lam_post, coef, nobs, b_bg);
         }
         }   // dim passes
         if (tid == 0) clear_voxel_frame(a, vid);
