@@ -748,6 +748,11 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, SVX_LONGK_MINB) k_update_lo
 // ---- K5 open set: one warp per voxel, lanes own feature dimensions ------------
 
 constexpr int kOpenPer = 8;   // dims per lane per pass (256 dims per pass)
+// open-set voxels with more rows than this go to the CTA-per-voxel kernel
+#ifndef SVX_OPEN_CTA_MIN
+#define SVX_OPEN_CTA_MIN 256   // measured best of 64 / 256 / 1024 on cfg3 and cfg5
+#endif
+constexpr int kOpenCtaMin = SVX_OPEN_CTA_MIN;
 
 template <class TS>
 __device__ __forceinline__ void nig_apply(TS* mrow, TS* brow, int c, bool isnew, double sz,
@@ -869,7 +874,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) k_update_open(UpdateArgs a,
          e += (long long)gridDim.x * kWarpsPerCta) {
         const int vid = a.mlist[e];
         const unsigned c = a.rec[vid].cnt;
-        if ((c & ~kNewBit) > (unsigned)kSmemMax) {
+        if ((c & ~kNewBit) > (unsigned)kOpenCtaMin) {   // one CTA per voxel (k_update_open_huge)
             if (lane == 0) a.hugelist[atomicAdd(&ctr->n_huge, 1ULL)] = (int)e;
             continue;
         }
