@@ -155,6 +155,20 @@ svx_status svx_integrate_world(svx_map* map, const void* points_world, int32_t p
                                const void* feats, int32_t feats_dtype, void* stream,
                                svx_report* report);
 
+/* ---- snapshots ------------------------------------------
+ * Load a map state into an EMPTY map: leaves in the snapshot's order become
+ * leaf ids 0..nl-1 (the reference's allocation order, grid.py:372-426
+ * read_grid_block), voxels in (leaf, slot) order become voxel ids 0..nv-1.
+ *   leaf_coords (nl, 3) int32 leaf coordinates (voxel >> 3)
+ *   voxel_leaf  (nv,) int32 leaf index of each voxel, non-decreasing
+ *   voxel_slot  (nv,) int32 slot (x&7)<<6 | (y&7)<<3 | (z&7), ascending within a leaf
+ *   d, w        (nv,) f64 TSDF; sem0 / sem1 (nv, C|D) in the map's storage dtype (or NULL)
+ * Host or device arrays.  The file format itself is written and parsed on the
+ * host (paper_2512_12945_b200/snapshot.py). */
+svx_status svx_import(svx_map* map, int64_t nl, const int32_t* leaf_coords, int64_t nv,
+                      const int32_t* voxel_leaf, const int32_t* voxel_slot, const double* d,
+                      const double* w, const void* sem0, const void* sem1, void* stream);
+
 /* ---- depth frames ---------------------------------------
  * Replaces ingest.project_depth (ingest.py:285-322) followed by integrate on
  * the returned Frame: pixel (u, v) of the raster, sampled every `stride`

@@ -129,6 +129,7 @@ _SIGNATURES = {
     "svx_classify": [_P, _P, _I32, _D, _D, _I64, _P, _P, _P, _P],
     "svx_label_map": [_P, _I32, _I64, _P, _P],
     "svx_set_profiling": [_P, _I32],
+    "svx_import": [_P, _I64, _P, _I64, _P, _P, _P, _P, _P, _P, _P],
     "svx_set_update_mode": [_P, _I32],
     "svx_reserve": [_P, _I64, _I64],
     "svx_shard_march": [_P, _P, _I32, _I64, ctypes.POINTER(_D), ctypes.POINTER(_D), _P, _P, _I32,

@@ -239,6 +239,16 @@ svx_status svx_integrate(svx_map* m, const void* points, int32_t points_dtype, i
                           (feats_dtype & 0xff) == SVX_F64, (cudaStream_t)stream, report, dev);
 }
 
+svx_status svx_import(svx_map* m, int64_t nl, const int32_t* leaf_coords, int64_t nv,
+                      const int32_t* voxel_leaf, const int32_t* voxel_slot, const double* d,
+                      const double* w, const void* sem0, const void* sem1, void* stream) {
+    if (!m || (nv > 0 && (!leaf_coords || !voxel_leaf || !voxel_slot || !d || !w)))
+        return fail(SVX_E_INPUT, "null argument");
+    SVX_TRY(set_device(m));
+    return import_impl(m, nl, leaf_coords, nv, voxel_leaf, voxel_slot, d, w, sem0, sem1,
+                       (cudaStream_t)stream);
+}
+
 svx_status svx_integrate_depth(svx_map* m, const void* depth, int32_t depth_dtype,
                                const svx_camera* camera, const double pose[16],
                                const int32_t* labels, const void* feats, int32_t feats_dtype,

@@ -565,6 +565,11 @@ svx_status build_active_list(svx_map* m, int64_t* count, cudaStream_t s);
 svx_status launch_leaf_stamps(svx_map* m, int32_t* frame, uint64_t* key, int32_t* count,
                               cudaStream_t s);
 
+// snapshots (svx_import.cu)
+svx_status import_impl(svx_map* m, int64_t nl, const int32_t* leaf_coords, int64_t nv,
+                       const int32_t* voxel_leaf, const int32_t* voxel_slot, const double* d,
+                       const double* w, const void* sem0, const void* sem1, cudaStream_t s);
+
 // depth frames (svx_depth.cu)
 svx_status integrate_depth_impl(svx_map* m, const void* depth, int depth_dtype, const svx_camera& cam,
                                 const PoseParams& pp, const int32_t* labels, const void* feats,

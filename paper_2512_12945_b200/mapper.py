@@ -24,7 +24,9 @@ import numpy as np
 from . import _lib
 from ._lib import SEM_CLOSED, SEM_NONE, SEM_OPEN, SVX_F32, SVX_F64, check, lib
 from .config import ClosedSetConfig, EngineConfig, FusionConfig, OpenSetConfig
-from .errors import ConfigError, OutOfRangeError, PayloadMismatchError, UserInputError
+from . import snapshot
+from .errors import (ConfigError, FormatError, OutOfRangeError, PayloadMismatchError,
+                     UserInputError)
 
 KIND_TSDF, KIND_CLOSED, KIND_OPEN = 0, 1, 2   # grid.py:26-28
 KIND_NAMES = {KIND_TSDF: "tsdf", KIND_CLOSED: "closed", KIND_OPEN: "open"}
@@ -648,8 +650,68 @@ class Mapper:
             report["semantic_active_voxels"] = self._sem_view.memory_stats().active_voxels
         return report
 
-    def save(self, path):
-        raise NotImplementedError(".slvg snapshot export is not part of this build (SURVEY §8(f)-2)")
+    def save(self, path) -> None:
+        """Write the map as a ``.slvg`` snapshot (bindings/__init__.py:183-187):
+        the TSDF grid block, then the semantic one; byte-identical to the
+        reference's file for the same map (snapshot.py)."""
+        coords, d, w, sem0, sem1 = self._export()
+        views = [v for v in (self._tsdf_view, self._sem_view) if v is not None]
+        with open(path, "wb") as fh:
+            for v in views:
+                snapshot.write_block(fh, v.kind, v.voxel_size, _params_block(v.payload), coords,
+                                     v._fields(d, w, sem0, sem1))
+
+    @classmethod
+    def from_snapshot(cls, path, config=None, /, **overrides):
+        """A Mapper whose map is the snapshot's, ready to integrate further
+        frames (engine extension; the reference only reads snapshots back as
+        grids, grid.py:358-407).  Voxel size, truncation and the semantic
+        payload parameters come from the file; the remaining configuration
+        (max_range, weight_fn, space_carving, engine keys) from `config` /
+        keyword arguments, which must not contradict the file."""
+        blocks = snapshot.read_blocks(path)
+        tsdf, sem = _split_blocks(blocks)
+        merged = dict(config or {})
+        merged.update(overrides)
+        from_file = {"voxel_size": tsdf.voxel_size, "truncation": tsdf.params[0]}
+        if sem is not None and sem.kind == KIND_CLOSED:
+            c, alpha, mode, code = sem.params
+            from_file.update(num_classes=c, prior_alpha=alpha,
+                             fusion="bayes" if mode == 0 else "last_wins",
+                             count_dtype=_CODE_NAMES[code])
+        elif sem is not None:
+            dim, beta, floor, conf, temp, code = sem.params
+            from_file.update(feature_dim=dim, prior_beta=beta, lambda_floor=floor,
+                             confidence_threshold=conf, temperature=temp,
+                             state_dtype=_CODE_NAMES[code])
+        for k, v in from_file.items():
+            if k in merged and merged[k] != v and not (
+                    isinstance(v, str) and np.dtype(merged[k]) == np.dtype(v)):
+                raise ConfigError(f"{k}={merged[k]!r} contradicts the snapshot's {v!r}")
+            merged[k] = v
+        if sem is None and (merged.get("num_classes") or merged.get("feature_dim")):
+            raise ConfigError("the snapshot holds geometry only")
+        m = cls(merged)
+        m._import_blocks(tsdf, sem)
+        return m
+
+    def _import_blocks(self, tsdf, sem):
+        n = tsdf.active_count
+        sem0 = sem1 = None
+        if sem is not None:
+            sem0 = np.ascontiguousarray(sem.fields[0])
+            sem1 = np.ascontiguousarray(sem.fields[1]) if sem.kind == KIND_OPEN else None
+        lc = np.ascontiguousarray(tsdf.leaf_coords, np.int32)
+        vl = np.ascontiguousarray(tsdf.voxel_leaf, np.int32)
+        vs = np.ascontiguousarray(tsdf.voxel_slot, np.int32)
+        d = np.ascontiguousarray(tsdf.fields[0], np.float64)
+        w = np.ascontiguousarray(tsdf.fields[1], np.float64)
+
+        def p(a):
+            return a.ctypes.data if (a is not None and a.size) else None
+
+        check(lib.svx_import(self._handle, lc.shape[0], p(lc), n, p(vl), p(vs), p(d), p(w),
+                             p(sem0), p(sem1), None))
 
     def extract(self, *args, **kwargs):
         raise NotImplementedError("mesh extraction is not part of this build (SURVEY §8(f)-3)")
@@ -768,6 +830,44 @@ class GridView:
         """Order-independent digest with the reference's layout (grid.py:204-215)."""
         coords, vals = self.active_values()
         return content_hash_of(coords, vals, self.payload, self.voxel_size)
+
+
+_CODE_NAMES = {0: "float32", 1: "float64"}
+
+
+def _split_blocks(blocks):
+    """(tsdf, semantic) blocks of a snapshot (load_grid,
+    bindings/__init__.py:189-201: the first of each kind), checked to share
+    one active set: the engine keeps TSDF and semantic payloads of a voxel in
+    one record, as every Mapper-written snapshot has them."""
+    tsdf = sem = None
+    for b in blocks:
+        if b.kind == KIND_TSDF and tsdf is None:
+            tsdf = b
+        elif b.kind != KIND_TSDF and sem is None:
+            sem = b
+    if tsdf is None:
+        raise FormatError("snapshot holds no TSDF grid block")
+    if sem is not None:
+        if sem.voxel_size != tsdf.voxel_size:
+            raise FormatError("TSDF and semantic blocks disagree on the voxel size")
+        if not (np.array_equal(sem.leaf_coords, tsdf.leaf_coords)
+                and np.array_equal(sem.voxel_leaf, tsdf.voxel_leaf)
+                and np.array_equal(sem.voxel_slot, tsdf.voxel_slot)):
+            raise FormatError("semantic block's active set differs from the TSDF block's")
+    return tsdf, sem
+
+
+def load_grid(path, backend=None, **engine):
+    """Read a snapshot written by Mapper.save (bindings/__init__.py:189-201).
+
+    Returns (tsdf, semantic) grid views over a device map holding the
+    snapshot (semantic None for geometry only); the views keep that map
+    alive.  `engine` takes EngineConfig keys (device, tsdf_dtype, ...)."""
+    if backend not in (None, "auto", "cuda"):
+        raise ConfigError(f"unknown backend {backend!r} (expected auto or cuda)")
+    m = Mapper.from_snapshot(path, **engine)
+    return m.grids
 
 
 def content_hash_of(coords, vals, payload, voxel_size: float) -> str:

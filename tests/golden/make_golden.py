@@ -281,11 +281,49 @@ def main_depth():
                    dict(cam, stride=2), depth_frames(13, 48, 64, 2, feat_dim=4))
 
 
+def main_snapshot():
+    # -- .slvg snapshots written by the reference's Mapper.save -------------------
+    # Re-runs the api_* fixtures' own inputs through the reference Mapper and
+    # saves its snapshot (bindings/__init__.py:183-187), so the engine's
+    # Mapper.save output can be compared byte for byte.
+    for name in ("api_closed_plane", "api_open_plane", "api_geometry_carving_dropoff",
+                 "api_closed_lastwins_dropoff"):
+        g = np.load(os.path.join(HERE, name + ".npz"))
+        kw = eval(str(g["mapper_kw"]))  # noqa: S307 -- our own repr() of a dict literal
+        m = sb.Mapper(**kw)
+        for i in range(int(g["n_frames"])):
+            m.integrate(g[f"points_{i}"], g[f"pose_{i}"],
+                        labels=g[f"labels_{i}"] if f"labels_{i}" in g else None,
+                        features=g[f"features_{i}"] if f"features_{i}" in g else None)
+        tsdf, sem = m.grids
+        assert tsdf.content_hash() == str(g["tsdf_hash"])
+        _save_gz(m, "snap_" + name[4:])
+    _save_gz(sb.Mapper(voxel_size=0.1, truncation=0.2), "snap_empty")
+
+
+def _save_gz(mapper, stem):
+    import gzip
+    import tempfile
+
+    with tempfile.TemporaryDirectory() as td:
+        tmp = os.path.join(td, "map.slvg")
+        mapper.save(tmp)
+        with open(tmp, "rb") as fh:
+            raw = fh.read()
+    path = os.path.join(HERE, stem + ".slvg.gz")
+    with gzip.GzipFile(path, "wb", mtime=0) as fh:
+        fh.write(raw)
+    print(path, len(raw), "bytes,", os.path.getsize(path), "compressed")
+
+
 def main():
     from paper_2512_12945_b200 import scenes
 
     if "depth" in sys.argv[1:]:   # only the depth scenarios
         main_depth()
+        return
+    if "snapshot" in sys.argv[1:]:
+        main_snapshot()
         return
     main_depth()
 
@@ -330,6 +368,7 @@ def main():
         f = wl.make_frame(i)
         fr.append((f.points_world.numpy(), f.origin, f.labels.numpy(), None))
     seam_scenario("seam_closed_city_small", fr, wl.mapper_kwargs)
+    main_snapshot()
 
 
 if __name__ == "__main__":
