@@ -15,12 +15,13 @@ from .errors import (
     SemvoxError,
     UserInputError,
 )
-from .mapper import GridView, IntegrationReport, Mapper, load_grid, validate_rotation
+from .mapper import (GridView, IntegrationReport, Mapper, grids_equal, load_grid,
+                     validate_rotation)
 
 __version__ = "0.1.0"
 
 __all__ = [
-    "Mapper", "load_grid", "GridView", "IntegrationReport", "validate_rotation",
+    "Mapper", "load_grid", "grids_equal", "GridView", "IntegrationReport", "validate_rotation",
     "FusionConfig", "ClosedSetConfig", "OpenSetConfig", "EngineConfig",
     "SemvoxError", "UserInputError", "ConfigError", "PayloadMismatchError",
     "FormatError", "OutOfRangeError",

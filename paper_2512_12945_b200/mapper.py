@@ -870,6 +870,28 @@ def load_grid(path, backend=None, **engine):
     return m.grids
 
 
+def grids_equal(a, b, exact=True, rtol=0.0, atol=0.0) -> bool:
+    """grid.py:428-447 over any two grids with ``kind``, ``voxel_size`` and
+    ``active_values()`` (engine views, or the reference's SparseGrid)."""
+    if a.kind != b.kind or a.voxel_size != b.voxel_size:
+        return False
+    ca, va = a.active_values()
+    cb, vb = b.active_values()
+    if ca.shape != cb.shape:
+        return False
+    oa = np.lexsort((ca[:, 2], ca[:, 1], ca[:, 0]))
+    ob = np.lexsort((cb[:, 2], cb[:, 1], cb[:, 0]))
+    if not np.array_equal(ca[oa], cb[ob]):
+        return False
+    for fa, fb in zip(va, vb):
+        if exact:
+            if not np.array_equal(fa[oa], fb[ob]):
+                return False
+        elif not np.allclose(fa[oa], fb[ob], rtol=rtol, atol=atol):
+            return False
+    return True
+
+
 def content_hash_of(coords, vals, payload, voxel_size: float) -> str:
     """content_hash (grid.py:204-215) of active coords + field arrays."""
     order = np.lexsort((coords[:, 2], coords[:, 1], coords[:, 0]))

@@ -289,3 +289,33 @@ def test_resume_full_size(config, tmp_path):
     m.save(str(qa))
     m2.save(str(qb))
     assert qa.read_bytes() == qb.read_bytes()
+
+
+def test_missing_and_empty_files(tmp_path):
+    """test_bindings.py TestSnapshots: empty file -> FormatError, missing -> OSError
+    (both raised before any device work)."""
+    from paper_2512_12945_b200 import FormatError, load_grid
+
+    bad = tmp_path / "empty.slvg"
+    bad.write_bytes(b"")
+    with pytest.raises(FormatError):
+        load_grid(bad)
+    with pytest.raises(OSError):
+        load_grid(tmp_path / "nope.slvg")
+
+
+@pytest.mark.gpu
+def test_grids_equal_and_path_objects(tmp_path):
+    from paper_2512_12945_b200 import grids_equal, load_grid
+
+    g = load_golden("api_closed_plane")
+    m = mapper_for(g)
+    replay_mapper(g, m)
+    snap = tmp_path / "run.slvg"
+    m.save(snap)                                  # pathlib paths, like the reference
+    tsdf, sem = load_grid(snap)
+    assert grids_equal(tsdf, m.grids[0]) and grids_equal(sem, m.grids[1])
+    assert not grids_equal(tsdf, sem)
+    m2 = mapper_for(g)
+    replay_mapper(dict(g, n_frames=1), m2)
+    assert not grids_equal(tsdf, m2.grids[0])
