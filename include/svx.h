@@ -169,6 +169,24 @@ svx_status svx_import(svx_map* map, int64_t nl, const int32_t* leaf_coords, int6
                       const int32_t* voxel_leaf, const int32_t* voxel_slot, const double* d,
                       const double* w, const void* sem0, const void* sem1, void* stream);
 
+/* ---- surface extraction ---------------------------------
+ * Mapper.extract = extract_mesh (mesh.py:419-545) on the device map.
+ * svx_extract_mesh triangulates the D = 0 level set over voxels with weight
+ * >= min_weight and keeps the mesh on the device; *n_vertices / *n_triangles
+ * get its size.  emb (k, D) f64: open-set vertex labels by classify_means
+ * (temperature, confidence_threshold); NULL = the dominant feature axis
+ * (voxel_labels, mesh.py:392-416).  Fails with SVX_E_RANGE when the kept
+ * voxels span more than 2^20 voxels on an axis (mesh.py:461-466).
+ * svx_mesh_read copies the last mesh out (host or device pointers, any may be
+ * NULL): vertices (nv,3) f64, triangles (nt,3) int32, labels (nv,) int32,
+ * colors (nv,3) u8 = palette row of the label (palette_colors,
+ * mesh.py:382-389; palette (npal,3) u8, npal >= 2). */
+svx_status svx_extract_mesh(svx_map* map, double min_weight, const double* emb, int32_t k,
+                            double temperature, double confidence_threshold, int64_t* n_vertices,
+                            int64_t* n_triangles, void* stream);
+svx_status svx_mesh_read(svx_map* map, double* vertices, int32_t* triangles, int32_t* labels,
+                         uint8_t* colors, const uint8_t* palette, int32_t npal, void* stream);
+
 /* ---- depth frames ---------------------------------------
  * Replaces ingest.project_depth (ingest.py:285-322) followed by integrate on
  * the returned Frame: pixel (u, v) of the raster, sampled every `stride`

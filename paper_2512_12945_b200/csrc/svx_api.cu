@@ -205,7 +205,12 @@ svx_status svx_destroy(svx_map* m) {
                       &m->rowvid, &m->rowray, &m->rowd, &m->rowlab, &m->partials, &m->tlist, &m->mlist,
                       &m->longlist, &m->srid, &m->bitmap, &m->rcount, &m->cubtmp, &m->ctr, &m->ord0,
                       &m->ord1, &m->ordk0, &m->ordk1, &m->ordf0, &m->ordf1, &m->act_cnt,
-                      &m->act_off, &m->act_vid, &m->act_coord, &m->q_buf, &m->out_buf};
+                      &m->act_off, &m->act_vid, &m->act_coord, &m->q_buf, &m->out_buf,
+                      &m->mesh_ctr, &m->mesh_k0, &m->mesh_k1, &m->mesh_i0, &m->mesh_i1,
+                      &m->mesh_rec, &m->mesh_meta, &m->mesh_vmask, &m->mesh_cnt, &m->mesh_off,
+                      &m->mesh_toff, &m->mesh_vk, &m->mesh_vv, &m->mesh_vidx, &m->mesh_v,
+                      &m->mesh_l, &m->mesh_t, &m->mesh_col, &m->mesh_vlab, &m->mesh_cls_l,
+                      &m->mesh_cls_b, &m->mesh_pal};
     for (DevBuf* b : bufs) release(*b);
     if (m->h_ctr) cudaFreeHost(m->h_ctr);
     if (m->h_kspan) cudaFreeHost(m->h_kspan);
@@ -446,14 +451,9 @@ svx_status svx_query_cosine(svx_map* m, const double* query, int64_t capacity, d
     return SVX_OK;
 }
 
-svx_status svx_classify(svx_map* m, const double* emb, int32_t k, double temperature,
-                        double confidence_threshold, int64_t capacity, int32_t* labels,
-                        double* best, double* sims, void* stream) {
-    if (!m || !emb || !labels || !best || k < 1) return fail(SVX_E_INPUT, "null argument");
-    if (m->cfg.sem_kind != SVX_SEM_OPEN)
-        return fail(SVX_E_PAYLOAD, "classification needs an open-set map");
-    SVX_TRY(set_device(m));
-    cudaStream_t s = (cudaStream_t)stream;
+// classify_means' query block in device memory (m->q_buf): emb (k, D) then
+// the k row norms (gaussian.py:132-155).
+static svx_status upload_queries(svx_map* m, const double* emb, int k, cudaStream_t s) {
     const int D = m->payload_d;
     const size_t eb = (size_t)8 * D * k;
     double* he = new double[(size_t)D * k + k];
@@ -476,6 +476,69 @@ svx_status svx_classify(svx_map* m, const double* emb, int32_t k, double tempera
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     delete[] he;
     if (e != cudaSuccess) return fail(SVX_E_CUDA, cudaGetErrorString(e));
+    return SVX_OK;
+}
+
+svx_status svx_extract_mesh(svx_map* m, double min_weight, const double* emb, int32_t k,
+                            double temperature, double confidence_threshold, int64_t* n_vertices,
+                            int64_t* n_triangles, void* stream) {
+    if (!m || !n_vertices || !n_triangles || (emb && k < 1)) return fail(SVX_E_INPUT, "null argument");
+    SVX_TRY(set_device(m));
+    cudaStream_t s = (cudaStream_t)stream;
+    const int* vlab = nullptr;
+    if (emb && m->cfg.sem_kind == SVX_SEM_OPEN) {
+        // open-set vertex labels: classify_means of every active voxel, by voxel id
+        SVX_TRY(upload_queries(m, emb, k, s));
+        int64_t count = 0;
+        SVX_TRY(build_active_list(m, &count, s));
+        SVX_TRY(ensure(m->mesh_cls_l, 4 * std::max<int64_t>(count, 1), s));
+        SVX_TRY(ensure(m->mesh_cls_b, 8 * std::max<int64_t>(count, 1), s));
+        SVX_TRY(ensure(m->mesh_vlab, 4 * std::max<int64_t>(m->nvox, 1), s));
+        const double* q = ptr<double>(m->q_buf);
+        SVX_TRY(launch_classify(m, count, q, q + (size_t)m->payload_d * k, k, temperature,
+                                confidence_threshold, ptr<int32_t>(m->mesh_cls_l),
+                                ptr<double>(m->mesh_cls_b), nullptr, s));
+        SVX_TRY(scatter_active_labels(m, count, ptr<int>(m->mesh_cls_l), ptr<int>(m->mesh_vlab), s));
+        vlab = ptr<int>(m->mesh_vlab);
+    }
+    SVX_TRY(mesh_impl(m, min_weight, vlab, s));
+    *n_vertices = m->mesh_nv;
+    *n_triangles = m->mesh_nt;
+    return SVX_OK;
+}
+
+svx_status svx_mesh_read(svx_map* m, double* vertices, int32_t* triangles, int32_t* labels,
+                         uint8_t* colors, const uint8_t* palette, int32_t npal, void* stream) {
+    if (!m || (colors && (!palette || npal < 2))) return fail(SVX_E_INPUT, "null argument");
+    SVX_TRY(set_device(m));
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t nv = m->mesh_nv, nt = m->mesh_nt;
+    if (vertices && nv) SVX_CUDA(cudaMemcpyAsync(vertices, m->mesh_v.p, 24 * nv, cudaMemcpyDefault, s));
+    if (triangles && nt) SVX_CUDA(cudaMemcpyAsync(triangles, m->mesh_t.p, 12 * nt, cudaMemcpyDefault, s));
+    if (labels && nv) SVX_CUDA(cudaMemcpyAsync(labels, m->mesh_l.p, 4 * nv, cudaMemcpyDefault, s));
+    if (colors && nv) {
+        SVX_TRY(ensure(m->mesh_pal, 3 * (size_t)npal, s));
+        SVX_CUDA(cudaMemcpyAsync(m->mesh_pal.p, palette, 3 * (size_t)npal, cudaMemcpyDefault, s));
+        SVX_TRY(ensure(m->mesh_col, 3 * nv, s));
+        SVX_TRY(mesh_colors(m, ptr<unsigned char>(m->mesh_pal), npal, ptr<unsigned char>(m->mesh_col), s));
+        SVX_CUDA(cudaMemcpyAsync(colors, m->mesh_col.p, 3 * nv, cudaMemcpyDefault, s));
+    }
+    SVX_CUDA(cudaStreamSynchronize(s));
+    return SVX_OK;
+}
+
+svx_status svx_classify(svx_map* m, const double* emb, int32_t k, double temperature,
+                        double confidence_threshold, int64_t capacity, int32_t* labels,
+                        double* best, double* sims, void* stream) {
+    if (!m || !emb || !labels || !best || k < 1) return fail(SVX_E_INPUT, "null argument");
+    if (m->cfg.sem_kind != SVX_SEM_OPEN)
+        return fail(SVX_E_PAYLOAD, "classification needs an open-set map");
+    SVX_TRY(set_device(m));
+    cudaStream_t s = (cudaStream_t)stream;
+    SVX_TRY(upload_queries(m, emb, k, s));
+    const int D = m->payload_d;
+    svx_status st = SVX_OK;
+    cudaError_t e = cudaSuccess;
     int64_t count = 0;
     SVX_TRY(build_active_list(m, &count, s));
     if (capacity < count) return fail(SVX_E_INPUT, "output capacity smaller than active count");

@@ -263,6 +263,11 @@ struct svx_map {
     int64_t ord_nblocks = -1;
     int* leaf_order = nullptr;
     svx::DevBuf act_cnt, act_off, act_vid, act_coord, q_buf, out_buf;
+    // surface extraction (svx_mesh.cu)
+    svx::DevBuf mesh_ctr, mesh_k0, mesh_k1, mesh_i0, mesh_i1, mesh_rec, mesh_meta, mesh_vmask,
+        mesh_cnt, mesh_off, mesh_toff, mesh_vk, mesh_vv, mesh_vidx, mesh_v, mesh_l, mesh_t, mesh_col,
+        mesh_vlab, mesh_cls_l, mesh_cls_b, mesh_pal;
+    int64_t mesh_nv = 0, mesh_nt = 0;
     int64_t act_valid_frames = -1;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_in = nullptr;
     // optional per-kernel timing (svx_set_profiling; FrameCtr.kspan)
@@ -564,6 +569,16 @@ __host__ __device__ inline int leaf_owner(long long a, long long b, long long c,
 svx_status build_active_list(svx_map* m, int64_t* count, cudaStream_t s);
 svx_status launch_leaf_stamps(svx_map* m, int32_t* frame, uint64_t* key, int32_t* count,
                               cudaStream_t s);
+
+// surface extraction (svx_mesh.cu)
+svx_status mesh_impl(svx_map* m, double min_weight, const int* vlab, cudaStream_t s);
+svx_status mesh_colors(svx_map* m, const unsigned char* pal, int npal, unsigned char* colors,
+                       cudaStream_t s);
+svx_status scatter_active_labels(svx_map* m, int64_t count, const int* labels, int* vlab,
+                                 cudaStream_t s);
+svx_status launch_classify(svx_map* m, int64_t count, const double* emb, const double* en, int k,
+                           double tau, double tp, int32_t* labels, double* best, double* sims,
+                           cudaStream_t s);
 
 // snapshots (svx_import.cu)
 svx_status import_impl(svx_map* m, int64_t nl, const int32_t* leaf_coords, int64_t nv,

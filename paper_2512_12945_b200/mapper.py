@@ -24,7 +24,7 @@ import numpy as np
 from . import _lib
 from ._lib import SEM_CLOSED, SEM_NONE, SEM_OPEN, SVX_F32, SVX_F64, check, lib
 from .config import ClosedSetConfig, EngineConfig, FusionConfig, OpenSetConfig
-from . import snapshot
+from . import snapshot, surface
 from .errors import (ConfigError, FormatError, OutOfRangeError, PayloadMismatchError,
                      UserInputError)
 
@@ -713,8 +713,49 @@ class Mapper:
         check(lib.svx_import(self._handle, lc.shape[0], p(lc), n, p(vl), p(vs), p(d), p(w),
                              p(sem0), p(sem1), None))
 
-    def extract(self, *args, **kwargs):
-        raise NotImplementedError("mesh extraction is not part of this build (SURVEY §8(f)-3)")
+    def extract(self, min_weight: float = 0.5, embeddings=None, palette=None):
+        """Triangulate the current zero level set (bindings/__init__.py:144-151 ->
+        extract_mesh, mesh.py:419-545) on the GPU: a SemanticMesh with
+        vertices, triangles, per-vertex labels and colours, byte-identical to
+        the reference's for the same map.  ``embeddings`` (k, D) labels
+        open-set vertices by classify_means; otherwise closed-set maps use
+        the count argmax and open-set maps the dominant feature axis."""
+        emb = None
+        k = 0
+        if embeddings is not None and self._open is not None:
+            emb = np.ascontiguousarray(embeddings, np.float64)
+            if emb.ndim != 2 or emb.shape[1] != self._open.feature_dim:
+                raise PayloadMismatchError(
+                    f"embeddings shape {emb.shape} incompatible with feature dim "
+                    f"{self._open.feature_dim}")
+            k = emb.shape[0]
+        tau = self._open.temperature if self._open is not None else 0.0
+        tp = self._open.confidence_threshold if self._open is not None else 0.0
+        nv, nt = ctypes.c_int64(), ctypes.c_int64()
+        check(lib.svx_extract_mesh(self._handle, float(min_weight),
+                                   emb.ctypes.data if emb is not None else None, k, tau, tp,
+                                   ctypes.byref(nv), ctypes.byref(nt), None))
+        nv, nt = int(nv.value), int(nt.value)
+        if nt == 0:
+            return surface.SemanticMesh.empty()
+        if palette is None:
+            if self._closed is not None:
+                size = self._closed.num_classes
+            elif self._open is not None:
+                size = k if emb is not None else self._open.feature_dim
+            else:
+                size = 1
+            palette = surface.default_palette(size)
+        palette = surface.check_palette(palette)
+        mesh = surface.SemanticMesh(vertices=np.empty((nv, 3), np.float64),
+                                    triangles=np.empty((nt, 3), np.int32),
+                                    labels=np.empty(nv, np.int32),
+                                    colors=np.empty((nv, 3), np.uint8))
+        check(lib.svx_mesh_read(self._handle, mesh.vertices.ctypes.data,
+                                mesh.triangles.ctypes.data, mesh.labels.ctypes.data,
+                                mesh.colors.ctypes.data, palette.ctypes.data, palette.shape[0],
+                                None))
+        return mesh
 
     # -- bulk export -----------------------------------------------------------
 

@@ -301,6 +301,114 @@ def main_snapshot():
     _save_gz(sb.Mapper(voxel_size=0.1, truncation=0.2), "snap_empty")
 
 
+def _mesh_out(out, prefix, mesh):
+    out[prefix + "vertices"] = mesh.vertices
+    out[prefix + "triangles"] = mesh.triangles
+    out[prefix + "labels"] = mesh.labels
+    out[prefix + "colors"] = mesh.colors
+
+
+def _band_grid(cfg_kw, sdf, span, sem=None, seed=0, permute=False, weight=1.0):
+    """A reference grid pair filled directly (no integration): every voxel
+    whose centre is within the truncation of sdf's zero set."""
+    from semvox import ClosedSetConfig, FusionConfig, OpenSetConfig, make_grids
+
+    cfg = FusionConfig(**cfg_kw)
+    kw = {}
+    if sem and sem[0] == "closed":
+        kw["closed"] = ClosedSetConfig(num_classes=sem[1])
+    elif sem:
+        kw["open_set"] = OpenSetConfig(feature_dim=sem[1])
+    tsdf, sg = make_grids(cfg, **kw)
+    g = np.stack(np.meshgrid(*[np.arange(-span, span + 1)] * 3, indexing="ij"), -1).reshape(-1, 3)
+    d = sdf((g + 0.5) * cfg.voxel_size)
+    keep = np.abs(d) <= cfg.truncation
+    coords, d = g[keep], d[keep]
+    rng = np.random.default_rng(seed)
+    if permute:
+        p = rng.permutation(len(d))
+        coords, d = coords[p], d[p]
+    w = np.where(rng.random(len(d)) < 0.1, 0.3, weight)      # some voxels below min_weight
+    tsdf.set_many(coords, [d, w])
+    if sg is not None and sem[0] == "closed":
+        counts = rng.integers(0, 3, (len(d), sem[1])).astype(np.float32)
+        counts[rng.random(len(d)) < 0.1] = 0.0                # some voxels without counts
+        sg.set_many(coords, [counts])
+    elif sg is not None:
+        mean = rng.normal(size=(len(d), sem[1])).astype(np.float32)
+        mean[rng.random(len(d)) < 0.05] = 0.0
+        sg.set_many(coords, [mean, np.ones_like(mean)])
+    return tsdf, sg
+
+
+def main_mesh():
+    # -- surface extraction (extract_mesh, mesh.py:419-545) -------------------------
+    from semvox import extract_mesh, save_grids
+
+    # maps integrated by the api_* fixtures
+    for name, variants in (("api_closed_plane", [dict()]),
+                           ("api_open_plane", [dict(), dict(emb=True)]),
+                           ("api_geometry_carving_dropoff", [dict(), dict(min_weight=0.0),
+                                                             dict(min_weight=2.0)])):
+        g = np.load(os.path.join(HERE, name + ".npz"))
+        kw = eval(str(g["mapper_kw"]))  # noqa: S307 -- our own repr() of a dict literal
+        m = sb.Mapper(**kw)
+        for i in range(int(g["n_frames"])):
+            m.integrate(g[f"points_{i}"], g[f"pose_{i}"],
+                        labels=g[f"labels_{i}"] if f"labels_{i}" in g else None,
+                        features=g[f"features_{i}"] if f"features_{i}" in g else None)
+        out = {}
+        for j, v in enumerate(variants):
+            emb = g["queries"] if v.get("emb") else None
+            mesh = m.extract(min_weight=v.get("min_weight", 0.5), embeddings=emb)
+            _mesh_out(out, f"v{j}_", mesh)
+            out[f"v{j}_min_weight"] = np.array(v.get("min_weight", 0.5))
+            out[f"v{j}_emb"] = np.array(bool(v.get("emb")))
+            print(name, j, mesh.n_vertices, mesh.n_triangles)
+        out["n_variants"] = np.array(len(variants))
+        np.savez_compressed(os.path.join(HERE, "mesh_" + name[4:] + ".npz"), **out)
+
+    # grids filled directly, loaded through their snapshots
+    cfg = dict(voxel_size=0.05, truncation=0.15)
+    c = np.array([0.013, -0.004, 0.021])
+    sphere = lambda p: np.linalg.norm(p - c, axis=-1) - 0.5              # noqa: E731
+    # a level set through voxel centres: corners exactly on it collapse edges
+    lattice = lambda p: p[:, 2] - 0.025 - 0.0 * p[:, 0]                   # noqa: E731
+    wavy = lambda p: p[:, 2] - 0.1 * np.sin(7.0 * p[:, 0]) * np.cos(5.0 * p[:, 1])  # noqa: E731
+    scenes = [("sphere_closed", sphere, 14, ("closed", 4), {}),
+              ("sphere_open", sphere, 14, ("open", 5), {}),
+              ("lattice_plane", lattice, 10, None, {}),
+              ("wavy_closed_permuted", wavy, 12, ("closed", 3), dict(permute=True))]
+    import tempfile
+
+    for stem, sdf, span, sem, extra in scenes:
+        tsdf, sg = _band_grid(cfg, sdf, span, sem, seed=len(stem), **extra)
+        with tempfile.TemporaryDirectory() as td:
+            tmp = os.path.join(td, "g.slvg")
+            save_grids(tmp, [x for x in (tsdf, sg) if x is not None])
+            with open(tmp, "rb") as fh:
+                raw = fh.read()
+        import gzip
+
+        with gzip.GzipFile(os.path.join(HERE, f"meshsnap_{stem}.slvg.gz"), "wb", mtime=0) as fh:
+            fh.write(raw)
+        out = {}
+        variants = [dict(), dict(min_weight=0.1)]
+        if sem and sem[0] == "open":
+            q = np.random.default_rng(9).normal(size=(3, sem[1]))
+            out["queries"] = q
+            variants.append(dict(emb=True))
+        for j, v in enumerate(variants):
+            mesh = extract_mesh(tsdf, sg, min_weight=v.get("min_weight", 0.5),
+                                embeddings=out["queries"] if v.get("emb") else None)
+            _mesh_out(out, f"v{j}_", mesh)
+            out[f"v{j}_min_weight"] = np.array(v.get("min_weight", 0.5))
+            out[f"v{j}_emb"] = np.array(bool(v.get("emb")))
+            print(stem, j, mesh.n_vertices, mesh.n_triangles, len(raw))
+        out["n_variants"] = np.array(len(variants))
+        np.savez_compressed(os.path.join(HERE, f"mesh_{stem}.npz"), **out)
+
+
 def _save_gz(mapper, stem):
     import gzip
     import tempfile
@@ -324,6 +432,9 @@ def main():
         return
     if "snapshot" in sys.argv[1:]:
         main_snapshot()
+        return
+    if "mesh" in sys.argv[1:]:
+        main_mesh()
         return
     main_depth()
 
@@ -369,6 +480,7 @@ def main():
         fr.append((f.points_world.numpy(), f.origin, f.labels.numpy(), None))
     seam_scenario("seam_closed_city_small", fr, wl.mapper_kwargs)
     main_snapshot()
+    main_mesh()
 
 
 if __name__ == "__main__":
