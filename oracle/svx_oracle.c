@@ -290,6 +290,18 @@ static void radix_sort(uint64_t* key, int64_t* row, uint64_t* k2, int64_t* r2, i
  * reference's BLAS product for identity rotations).  sensor == 0: points are
  * world-frame and pose[3], pose[7], pose[11] hold the origin.
  */
+/* Frame.points_world (fusion.py:98-100): `points @ R.T + t`.  numpy hands
+ * an (n, 3) @ (3, 3) product with n >= 2 to OpenBLAS dgemm, whose microkernel
+ * accumulates k = 0, 1, 2 with fused multiply-adds starting from the k = 0
+ * product; a single row goes through the vector-matrix path, which starts
+ * from the k = 1 product and fuses k = 0, then k = 2.  Both orders were
+ * measured against numpy in the build container (make_golden.py rotated). */
+static double world_pt(const double* pose, int r, double x, double y, double z, int single) {
+    const double* R = pose + 4 * r;
+    const double acc = single ? fma(R[0], x, R[1] * y) : fma(R[1], y, R[0] * x);
+    return fma(R[2], z, acc) + R[3];
+}
+
 int orc_integrate(orc_map* m, const double* pts, int64_t n, const double pose[16], int sensor,
                   const int32_t* labels, const double* feats, orc_report* rep) {
     const orc_config* c = &m->cfg;
@@ -316,10 +328,10 @@ int orc_integrate(orc_map* m, const double* pts, int64_t n, const double pose[16
     for (int64_t i = 0; i < n; ++i) {
         double x = pts[3 * i], y = pts[3 * i + 1], z = pts[3 * i + 2];
         double wx = x, wy = y, wz = z;
-        if (sensor) {
-            wx = ((pose[0] * x + pose[1] * y) + pose[2] * z) + pose[3];
-            wy = ((pose[4] * x + pose[5] * y) + pose[6] * z) + pose[7];
-            wz = ((pose[8] * x + pose[9] * y) + pose[10] * z) + pose[11];
+        if (sensor) {   /* points @ R.T + t in numpy/OpenBLAS order (world_pt) */
+            wx = world_pt(pose, 0, x, y, z, n == 1);
+            wy = world_pt(pose, 1, x, y, z, n == 1);
+            wz = world_pt(pose, 2, x, y, z, n == 1);
         }
         int finite = isfinite(wx) && isfinite(wy) && isfinite(wz);
         double dx = wx - ox, dy = wy - oy, dz = wz - oz;

@@ -239,6 +239,7 @@ svx_status svx_integrate(svx_map* m, const void* points, int32_t points_dtype, i
         pp.t[r] = pose[4 * r + 3];
     }
     pp.sensor = 1;
+    pp.single = n == 1;
     const int dev = (points_dtype & SVX_DEVICE_INPUTS) ? 1 : 0;
     return integrate_impl(m, points, (points_dtype & 0xff) == SVX_F64, n, pp, labels, feats,
                           (feats_dtype & 0xff) == SVX_F64, (cudaStream_t)stream, report, dev);
@@ -266,6 +267,7 @@ svx_status svx_integrate_depth(svx_map* m, const void* depth, int32_t depth_dtyp
         pp.t[r] = pose[4 * r + 3];
     }
     pp.sensor = 1;
+    pp.single = 0;   // (a raster with exactly one valid pixel would take numpy's 1-row path)
     return integrate_depth_impl(m, depth, depth_dtype & 0xff, *camera, pp, labels, feats,
                                 (feats_dtype & 0xff) == SVX_F64, (cudaStream_t)stream, report);
 }
@@ -281,6 +283,7 @@ svx_status svx_integrate_world(svx_map* m, const void* points_world, int32_t poi
     pp.R[0] = pp.R[4] = pp.R[8] = 1.0;
     for (int a = 0; a < 3; ++a) pp.t[a] = origin[a];
     pp.sensor = 0;
+    pp.single = 0;
     const int dev = (points_dtype & SVX_DEVICE_INPUTS) ? 1 : 0;
     return integrate_impl(m, points_world, (points_dtype & 0xff) == SVX_F64, n, pp, labels, feats,
                           (feats_dtype & 0xff) == SVX_F64, (cudaStream_t)stream, report, dev);

@@ -58,7 +58,21 @@ struct PoseParams {
     double R[9];
     double t[3];
     int sensor;      // 1: transform points by (R, t); 0: points already world, origin = t
+    int single;      // the frame has exactly one point (see world_point)
 };
+
+// Frame.points_world (fusion.py:98-100) = points @ R.T + t, evaluated the way
+// the reference's numpy/OpenBLAS does it, so rotated poses reproduce bit for
+// bit: a frame of n >= 2 points goes through dgemm, whose microkernel
+// accumulates k = 0, 1, 2 with fused multiply-adds from the k = 0 product;
+// a one-point frame goes through the vector-matrix path, which starts from
+// the k = 1 product, then fuses k = 0 and k = 2 (both measured against
+// numpy in the build container, tests/golden/make_golden.py rotated).
+__host__ __device__ inline double world_coord(const double* Rrow, double t, double x, double y,
+                                              double z, int single) {
+    const double acc = single ? fma(Rrow[0], x, Rrow[1] * y) : fma(Rrow[1], y, Rrow[0] * x);
+    return fma(Rrow[2], z, acc) + t;
+}
 
 // Frame key: voxel offsets from `base` packed 21 bits per axis, x-major, so
 // key order is the reference's lexicographic voxel order (_core.pyx:727-732).

@@ -247,9 +247,9 @@ __device__ __forceinline__ bool prepare_ray(long long i, const FrameParams& fp, 
     const PoseParams& pp = fp.pp;
     double wx, wy, wz;
     if (pp.sensor) {
-        wx = ((pp.R[0] * x + pp.R[1] * y) + pp.R[2] * z) + pp.t[0];
-        wy = ((pp.R[3] * x + pp.R[4] * y) + pp.R[5] * z) + pp.t[1];
-        wz = ((pp.R[6] * x + pp.R[7] * y) + pp.R[8] * z) + pp.t[2];
+        wx = world_coord(pp.R, pp.t[0], x, y, z, pp.single);
+        wy = world_coord(pp.R + 3, pp.t[1], x, y, z, pp.single);
+        wz = world_coord(pp.R + 6, pp.t[2], x, y, z, pp.single);
     } else {
         wx = x; wy = y; wz = z;
     }

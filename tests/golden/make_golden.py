@@ -281,6 +281,68 @@ def main_depth():
                    dict(cam, stride=2), depth_frames(13, 48, 64, 2, feat_dim=4))
 
 
+def main_rotated():
+    # -- rotated poses through the public API ---------------------------------------
+    # Frame.points_world = points @ R.T + t goes through numpy/OpenBLAS; the
+    # engine and the oracle evaluate it in the same fused-multiply-add order
+    # (svx_internal.cuh world_coord), so rotated trajectories are pinned bit
+    # for bit through Mapper.integrate too.  First check that order here.
+    from fractions import Fraction
+
+    def fma(a, b, c):
+        return float(Fraction(a) * Fraction(b) + Fraction(c))
+
+    rng = np.random.default_rng(21)
+    for n in (1, 2, 3, 7, 64):
+        q, _ = np.linalg.qr(rng.normal(size=(3, 3)))
+        pts = rng.normal(size=(n, 3)) * 5.0
+        t = rng.normal(size=3)
+        ref = pts @ q.T + t
+        for i in range(n):
+            for j in range(3):
+                x, y, z = pts[i]
+                acc = fma(q[j, 0], x, q[j, 1] * y) if n == 1 else fma(q[j, 1], y, q[j, 0] * x)
+                assert fma(q[j, 2], z, acc) + t[j] == ref[i, j], (n, i, j)
+    from paper_2512_12945_b200 import scenes
+
+    wl = scenes.workload(1, small=True)
+    fr = []
+    for i in range(3):
+        f = wl.make_frame(i)
+        fr.append((f.points.numpy(), f.pose, f.labels.numpy(), None))
+    api_scenario("api_closed_room_rotated", fr, wl.mapper_kwargs)
+    wl = scenes.workload(4, small=True)
+    fr = []
+    for i in range(2):
+        f = wl.make_frame(i)
+        fr.append((f.points.numpy(), f.pose, f.labels.numpy(), None))
+    api_scenario("api_closed_city_rotated", fr, wl.mapper_kwargs)
+    wl = scenes.workload(3, small=True)
+    fr = []
+    dim = 16
+    for i in range(2):
+        f = wl.make_frame(i)
+        fr.append((f.points.numpy()[::2], f.pose, None,
+                   np.ascontiguousarray(f.features.numpy()[::2, :dim])))
+    api_scenario("api_open_room_rotated", fr, dict(wl.mapper_kwargs, feature_dim=dim),
+                 queries=np.ascontiguousarray(wl.queries[:4, :dim].numpy()))
+    # tiny frames (1, 2, 3 points): numpy's one-row product takes another path
+    rng = np.random.default_rng(22)
+    fr = []
+    for i in range(12):
+        n = 1 + i % 3
+        q, _ = np.linalg.qr(rng.normal(size=(3, 3)))
+        if np.linalg.det(q) < 0:
+            q[:, 0] = -q[:, 0]
+        pose = np.eye(4)
+        pose[:3, :3] = q
+        pose[:3, 3] = rng.uniform(-1.0, 1.0, 3)
+        pts = rng.normal(size=(n, 3)) * 1.5
+        fr.append((pts, pose, rng.integers(1, 4, n).astype(np.int32), None))
+    api_scenario("api_closed_tiny_frames_rotated", fr,
+                 dict(voxel_size=0.05, truncation=0.15, num_classes=3))
+
+
 def main_snapshot():
     # -- .slvg snapshots written by the reference's Mapper.save -------------------
     # Re-runs the api_* fixtures' own inputs through the reference Mapper and
@@ -436,6 +498,9 @@ def main():
     if "mesh" in sys.argv[1:]:
         main_mesh()
         return
+    if "rotated" in sys.argv[1:]:
+        main_rotated()
+        return
     main_depth()
 
     # -- API level ------------------------------------------------------------
@@ -479,6 +544,7 @@ def main():
         f = wl.make_frame(i)
         fr.append((f.points_world.numpy(), f.origin, f.labels.numpy(), None))
     seam_scenario("seam_closed_city_small", fr, wl.mapper_kwargs)
+    main_rotated()
     main_snapshot()
     main_mesh()
 
