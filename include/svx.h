@@ -187,6 +187,38 @@ svx_status svx_extract_mesh(svx_map* map, double min_weight, const double* emb, 
 svx_status svx_mesh_read(svx_map* map, double* vertices, int32_t* triangles, int32_t* labels,
                          uint8_t* colors, const uint8_t* palette, int32_t npal, void* stream);
 
+/* ---- rendering ------------------------------------------
+ * render (render.py:214-272) = ray-march of the device map from a pinhole
+ * camera (RenderCamera, render.py:33-85: x right, y down, z forward; pose =
+ * camera-to-world 4x4 row-major with a validated rotation).  Outputs, row-major
+ * pixels, background 0:
+ *   SVX_RENDER_DEPTH    (H, W) f64 distance along the ray
+ *   SVX_RENDER_SEMANTIC (H, W, 3) u8 palette colour of the nearest voxel's label
+ *                       (palette (npal,3) u8, npal >= 2; emb (k, D) f64 labels
+ *                       open-set maps by classify_means, NULL = dominant axis)
+ *   SVX_RENDER_NORMAL   (H, W, 3) f64 unit outward normal (central differences)
+ * `out` may be a host or device pointer. */
+#define SVX_RENDER_DEPTH 0
+#define SVX_RENDER_SEMANTIC 1
+#define SVX_RENDER_NORMAL 2
+
+typedef struct svx_render_camera {
+    double pose[16];
+    double fx, fy, cx, cy;
+    int32_t width, height;
+    double near_plane, far_plane;
+} svx_render_camera;
+
+svx_status svx_render(svx_map* map, const svx_render_camera* camera, int32_t mode,
+                      const double* emb, int32_t k, double temperature,
+                      double confidence_threshold, const uint8_t* palette, int32_t npal, void* out,
+                      void* stream);
+
+/* sample_distance (render.py:88-113): trilinear D at n world points (n,3) f64;
+ * valid[i] = 0 and vals[i] = NaN where a surrounding voxel centre is inactive. */
+svx_status svx_sample_distance(svx_map* map, const double* points, int64_t n, double* vals,
+                               uint8_t* valid, void* stream);
+
 /* ---- depth frames ---------------------------------------
  * Replaces ingest.project_depth (ingest.py:285-322) followed by integrate on
  * the returned Frame: pixel (u, v) of the raster, sampled every `stride`

@@ -18,10 +18,14 @@ from .errors import (
 from .mapper import (GridView, IntegrationReport, Mapper, grids_equal, load_grid,
                      validate_rotation)
 
+from .render import RenderCamera, render, sample_distance
+from .surface import SemanticMesh, default_palette, palette_colors
+
 __version__ = "0.1.0"
 
 __all__ = [
-    "Mapper", "load_grid", "grids_equal", "GridView", "IntegrationReport", "validate_rotation",
+    "Mapper", "load_grid", "grids_equal", "RenderCamera", "render", "sample_distance",
+    "SemanticMesh", "default_palette", "palette_colors", "GridView", "IntegrationReport", "validate_rotation",
     "FusionConfig", "ClosedSetConfig", "OpenSetConfig", "EngineConfig",
     "SemvoxError", "UserInputError", "ConfigError", "PayloadMismatchError",
     "FormatError", "OutOfRangeError",

@@ -132,6 +132,8 @@ _SIGNATURES = {
     "svx_extract_mesh": [_P, ctypes.c_double, _P, _I32, ctypes.c_double, ctypes.c_double, _P, _P,
                          _P],
     "svx_mesh_read": [_P, _P, _P, _P, _P, _P, _I32, _P],
+    "svx_render": [_P, _P, _I32, _P, _I32, ctypes.c_double, ctypes.c_double, _P, _I32, _P, _P],
+    "svx_sample_distance": [_P, _P, _I64, _P, _P, _P],
     "svx_import": [_P, _I64, _P, _I64, _P, _P, _P, _P, _P, _P, _P],
     "svx_set_update_mode": [_P, _I32],
     "svx_reserve": [_P, _I64, _I64],

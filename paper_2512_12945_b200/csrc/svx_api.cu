@@ -482,6 +482,88 @@ static svx_status upload_queries(svx_map* m, const double* emb, int k, cudaStrea
     return SVX_OK;
 }
 
+// classify_means of every active voxel (TSDF weight as the observation
+// weight), stored by voxel id: the open-set labels of mesh vertices and
+// rendered pixels (voxel_labels, mesh.py:392-416).
+static svx_status voxel_class_labels(svx_map* m, const double* emb, int k, double temperature,
+                                     double confidence_threshold, cudaStream_t s, const int** out) {
+    SVX_TRY(upload_queries(m, emb, k, s));
+    int64_t count = 0;
+    SVX_TRY(build_active_list(m, &count, s));
+    SVX_TRY(ensure(m->mesh_cls_l, 4 * std::max<int64_t>(count, 1), s));
+    SVX_TRY(ensure(m->mesh_cls_b, 8 * std::max<int64_t>(count, 1), s));
+    SVX_TRY(ensure(m->mesh_vlab, 4 * std::max<int64_t>(m->nvox, 1), s));
+    const double* q = ptr<double>(m->q_buf);
+    SVX_TRY(launch_classify(m, count, q, q + (size_t)m->payload_d * k, k, temperature,
+                            confidence_threshold, ptr<int32_t>(m->mesh_cls_l),
+                            ptr<double>(m->mesh_cls_b), nullptr, s));
+    SVX_TRY(scatter_active_labels(m, count, ptr<int>(m->mesh_cls_l), ptr<int>(m->mesh_vlab), s));
+    *out = ptr<int>(m->mesh_vlab);
+    return SVX_OK;
+}
+
+svx_status svx_render(svx_map* m, const svx_render_camera* cam, int32_t mode, const double* emb,
+                      int32_t k, double temperature, double confidence_threshold,
+                      const uint8_t* palette, int32_t npal, void* out, void* stream) {
+    if (!m || !cam || !out || (emb && k < 1)) return fail(SVX_E_INPUT, "null argument");
+    if (mode != SVX_RENDER_DEPTH && mode != SVX_RENDER_SEMANTIC && mode != SVX_RENDER_NORMAL)
+        return fail(SVX_E_CONFIG, "render mode must be depth, semantic or normal");
+    if (mode == SVX_RENDER_SEMANTIC && m->cfg.sem_kind == SVX_SEM_NONE)
+        return fail(SVX_E_CONFIG, "semantic mode needs a semantic grid");
+    if (mode == SVX_RENDER_SEMANTIC && (!palette || npal < 2))
+        return fail(SVX_E_INPUT, "semantic mode needs a palette of >= 2 rows");
+    if (cam->width <= 0 || cam->height <= 0) return fail(SVX_E_CONFIG, "image dimensions must be positive");
+    if (!(cam->near_plane > 0.0) || !(cam->far_plane > cam->near_plane))
+        return fail(SVX_E_CONFIG, "near/far planes must satisfy 0 < near < far");
+    SVX_TRY(set_device(m));
+    cudaStream_t s = (cudaStream_t)stream;
+    const int* vlab = nullptr;
+    if (mode == SVX_RENDER_SEMANTIC && emb && m->cfg.sem_kind == SVX_SEM_OPEN)
+        SVX_TRY(voxel_class_labels(m, emb, k, temperature, confidence_threshold, s, &vlab));
+    const unsigned char* pal = nullptr;
+    if (mode == SVX_RENDER_SEMANTIC) {
+        SVX_TRY(ensure(m->mesh_pal, 3 * (size_t)npal, s));
+        SVX_CUDA(cudaMemcpyAsync(m->mesh_pal.p, palette, 3 * (size_t)npal, cudaMemcpyDefault, s));
+        pal = ptr<unsigned char>(m->mesh_pal);
+    }
+    const int64_t npx = (int64_t)cam->width * cam->height;
+    const size_t bytes = (size_t)npx * (mode == SVX_RENDER_DEPTH ? 8 : mode == SVX_RENDER_NORMAL ? 24 : 3);
+    OutStage o;
+    void* dout = nullptr;
+    svx_status st = out_prepare(o, out, bytes, s, &dout);
+    if (!st) st = render_impl(m, *cam, mode, vlab, pal, npal, dout, s);
+    if (!st) st = out_finish(o, s);
+    cudaError_t e = cudaStreamSynchronize(s);
+    out_release(&o, 1);
+    if (st) return st;
+    if (e != cudaSuccess) return fail(SVX_E_CUDA, std::string("render: ") + cudaGetErrorString(e));
+    return SVX_OK;
+}
+
+svx_status svx_sample_distance(svx_map* m, const double* points, int64_t n, double* vals,
+                               uint8_t* valid, void* stream) {
+    if (!m || (n > 0 && (!points || !vals || !valid))) return fail(SVX_E_INPUT, "null argument");
+    SVX_TRY(set_device(m));
+    cudaStream_t s = (cudaStream_t)stream;
+    DevBuf stage;
+    const void* dp = nullptr;
+    SVX_TRY(stage_in(points, 24 * (size_t)n, stage, s, &dp));
+    OutStage o[2];
+    void *dv, *dk;
+    svx_status st = SVX_OK;
+    if (!(st = out_prepare(o[0], vals, 8 * (size_t)n, s, &dv)) &&
+        !(st = out_prepare(o[1], valid, (size_t)n, s, &dk)) &&
+        !(st = sample_impl(m, n, (const double*)dp, (double*)dv, (unsigned char*)dk, s))) {
+        for (int i = 0; i < 2 && st == SVX_OK; ++i) st = out_finish(o[i], s);
+    }
+    cudaError_t e = cudaStreamSynchronize(s);
+    out_release(o, 2);
+    release(stage);
+    if (st) return st;
+    if (e != cudaSuccess) return fail(SVX_E_CUDA, std::string("sample: ") + cudaGetErrorString(e));
+    return SVX_OK;
+}
+
 svx_status svx_extract_mesh(svx_map* m, double min_weight, const double* emb, int32_t k,
                             double temperature, double confidence_threshold, int64_t* n_vertices,
                             int64_t* n_triangles, void* stream) {
@@ -489,21 +571,8 @@ svx_status svx_extract_mesh(svx_map* m, double min_weight, const double* emb, in
     SVX_TRY(set_device(m));
     cudaStream_t s = (cudaStream_t)stream;
     const int* vlab = nullptr;
-    if (emb && m->cfg.sem_kind == SVX_SEM_OPEN) {
-        // open-set vertex labels: classify_means of every active voxel, by voxel id
-        SVX_TRY(upload_queries(m, emb, k, s));
-        int64_t count = 0;
-        SVX_TRY(build_active_list(m, &count, s));
-        SVX_TRY(ensure(m->mesh_cls_l, 4 * std::max<int64_t>(count, 1), s));
-        SVX_TRY(ensure(m->mesh_cls_b, 8 * std::max<int64_t>(count, 1), s));
-        SVX_TRY(ensure(m->mesh_vlab, 4 * std::max<int64_t>(m->nvox, 1), s));
-        const double* q = ptr<double>(m->q_buf);
-        SVX_TRY(launch_classify(m, count, q, q + (size_t)m->payload_d * k, k, temperature,
-                                confidence_threshold, ptr<int32_t>(m->mesh_cls_l),
-                                ptr<double>(m->mesh_cls_b), nullptr, s));
-        SVX_TRY(scatter_active_labels(m, count, ptr<int>(m->mesh_cls_l), ptr<int>(m->mesh_vlab), s));
-        vlab = ptr<int>(m->mesh_vlab);
-    }
+    if (emb && m->cfg.sem_kind == SVX_SEM_OPEN)
+        SVX_TRY(voxel_class_labels(m, emb, k, temperature, confidence_threshold, s, &vlab));
     SVX_TRY(mesh_impl(m, min_weight, vlab, s));
     *n_vertices = m->mesh_nv;
     *n_triangles = m->mesh_nt;

@@ -584,6 +584,12 @@ svx_status build_active_list(svx_map* m, int64_t* count, cudaStream_t s);
 svx_status launch_leaf_stamps(svx_map* m, int32_t* frame, uint64_t* key, int32_t* count,
                               cudaStream_t s);
 
+// rendering (svx_render.cu)
+svx_status render_impl(svx_map* m, const svx_render_camera& cam, int mode, const int* vlab,
+                       const unsigned char* pal, int npal, void* out, cudaStream_t s);
+svx_status sample_impl(svx_map* m, int64_t n, const double* pts, double* vals, unsigned char* valid,
+                       cudaStream_t s);
+
 // surface extraction (svx_mesh.cu)
 svx_status mesh_impl(svx_map* m, double min_weight, const int* vlab, cudaStream_t s);
 svx_status mesh_colors(svx_map* m, const unsigned char* pal, int npal, unsigned char* colors,

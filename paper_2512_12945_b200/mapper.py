@@ -661,6 +661,14 @@ class Mapper:
                 snapshot.write_block(fh, v.kind, v.voxel_size, _params_block(v.payload), coords,
                                      v._fields(d, w, sem0, sem1))
 
+    def render(self, camera, mode: str = "depth", embeddings=None, palette=None):
+        """render (render.py:214-272) of this map from `camera` (a RenderCamera),
+        ray-marched on the GPU; see paper_2512_12945_b200.render.render."""
+        from .render import render
+
+        return render(self._tsdf_view, self._sem_view, camera, mode=mode, embeddings=embeddings,
+                      palette=palette)
+
     @classmethod
     def from_snapshot(cls, path, config=None, /, **overrides):
         """A Mapper whose map is the snapshot's, ready to integrate further

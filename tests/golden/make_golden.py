@@ -471,6 +471,64 @@ def main_mesh():
         np.savez_compressed(os.path.join(HERE, f"mesh_{stem}.npz"), **out)
 
 
+def main_render():
+    # -- ray-march rendering (render.py:214-272) -------------------------------------
+    import gzip
+
+    from semvox import RenderCamera, load_grids, render
+
+    from cameras import RENDER_CAMERAS
+
+    def cam(name):
+        pose, w, h, f, near, far = RENDER_CAMERAS[name]
+        return RenderCamera(pose=pose.copy(), fx=f, fy=f * 1.05, cx=w / 2.0 - 0.3,
+                            cy=h / 2.0 + 0.2, width=w, height=h, near=near, far=far)
+
+    def shoot(out, tsdf, sem, cams, emb=None):
+        for c in cams:
+            out[f"{c}_depth"] = render(tsdf, sem, cam(c), mode="depth")
+            out[f"{c}_normal"] = render(tsdf, sem, cam(c), mode="normal")
+            if sem is not None:
+                out[f"{c}_semantic"] = render(tsdf, sem, cam(c), mode="semantic")
+                if emb is not None:
+                    out[f"{c}_semantic_emb"] = render(tsdf, sem, cam(c), mode="semantic",
+                                                      embeddings=emb)
+            print("render", c, int((out[f"{c}_depth"] > 0).sum()), "hits")
+        out["cameras"] = np.array(list(cams))
+
+    # grids from the mesh snapshots
+    for stem, cams in (("sphere_closed", ["front", "oblique"]),
+                       ("sphere_open", ["front"]),
+                       ("lattice_plane", ["down", "down_far_cut", "down_near_skip"])):
+        with gzip.open(os.path.join(HERE, f"meshsnap_{stem}.slvg.gz"), "rb") as fh:
+            raw = fh.read()
+        import tempfile
+
+        with tempfile.TemporaryDirectory() as td:
+            p = os.path.join(td, "g.slvg")
+            with open(p, "wb") as fh:
+                fh.write(raw)
+            grids = load_grids(p)
+        tsdf, sem = grids[0], (grids[1] if len(grids) > 1 else None)
+        out = {}
+        emb = None
+        if stem == "sphere_open":
+            emb = np.random.default_rng(9).normal(size=(3, 5))
+            out["queries"] = emb
+        shoot(out, tsdf, sem, cams, emb)
+        np.savez_compressed(os.path.join(HERE, f"render_{stem}.npz"), **out)
+    # an integrated map (api_closed_plane) seen from above
+    g = np.load(os.path.join(HERE, "api_closed_plane.npz"))
+    kw = eval(str(g["mapper_kw"]))  # noqa: S307 -- our own repr() of a dict literal
+    m = sb.Mapper(**kw)
+    for i in range(int(g["n_frames"])):
+        m.integrate(g[f"points_{i}"], g[f"pose_{i}"], labels=g[f"labels_{i}"])
+    tsdf, sem = m.grids
+    out = {}
+    shoot(out, tsdf, sem, ["down", "oblique"])
+    np.savez_compressed(os.path.join(HERE, "render_closed_plane.npz"), **out)
+
+
 def _save_gz(mapper, stem):
     import gzip
     import tempfile
@@ -500,6 +558,9 @@ def main():
         return
     if "rotated" in sys.argv[1:]:
         main_rotated()
+        return
+    if "render" in sys.argv[1:]:
+        main_render()
         return
     main_depth()
 
@@ -547,6 +608,7 @@ def main():
     main_rotated()
     main_snapshot()
     main_mesh()
+    main_render()
 
 
 if __name__ == "__main__":
