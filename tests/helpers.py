@@ -25,7 +25,7 @@ def golden_names():
     """Point-cloud fixtures (api_* / seam_*); depth_* fixtures: depth_names()."""
     return sorted(os.path.splitext(os.path.basename(p))[0]
                   for p in glob.glob(os.path.join(GOLDEN, "*.npz"))
-                  if not os.path.basename(p).startswith(("depth_", "mesh_")))
+                  if os.path.basename(p).startswith(("api_", "seam_")))
 
 
 def depth_names():
