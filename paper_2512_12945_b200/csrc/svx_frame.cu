@@ -48,6 +48,19 @@ bool is_device_ptr(const void* p) {
     return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
+// Device address of page-locked host memory (mapped under UVA), else null.
+static const void* pinned_device_ptr(const void* p) {
+    if (!p) return nullptr;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
+}
+
+static const bool g_no_zero_copy = getenv("SVX_NO_ZERO_COPY") != nullptr;   // A/B switch
+
 svx_status stage_in(const void* p, size_t bytes, DevBuf& stage, cudaStream_t s, const void** out) {
     if (!p || bytes == 0) {
         *out = p;
@@ -459,13 +472,31 @@ svx_status integrate_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n
     const void* pts = pts_in;
     const void* feats = kind == SVX_SEM_OPEN ? feats_in : nullptr;
     const void* labv = kind == SVX_SEM_CLOSED ? (const void*)labels_in : nullptr;
-    if (!device_inputs) {
+    // Pinned host points/labels of closed-set and geometry frames are read
+    // in place by the walk (zero-copy over the host link) when the frame
+    // runs in slot mode: the walk is their only reader there, so the
+    // transfer overlaps the band walk instead of preceding it.  Segment-mode
+    // frames read labels again by point index and get a device copy.
+    const void* zc_pts = nullptr;
+    const void* zc_lab = nullptr;
+    if (!device_inputs && kind != SVX_SEM_OPEN && !g_no_zero_copy) {
+        zc_pts = pinned_device_ptr(pts_in);
+        if (zc_pts && kind == SVX_SEM_CLOSED) {
+            zc_lab = pinned_device_ptr(labels_in);
+            if (!zc_lab) zc_pts = nullptr;
+        }
+    }
+    bool staged = device_inputs != 0;
+    auto stage_all = [&]() -> svx_status {
         SVX_TRY(stage_in(pts_in, (size_t)n * 3 * (pts_f64 ? 8 : 4), m->in_pts, s, &pts));
         if (kind == SVX_SEM_CLOSED) SVX_TRY(stage_in(labels_in, (size_t)n * 4, m->in_lab, s, &labv));
         if (kind == SVX_SEM_OPEN)
             SVX_TRY(stage_in(feats_in, (size_t)n * m->payload_d * (feats_f64 ? 8 : 4), m->in_feat, s,
                              &feats));
-    }
+        staged = true;
+        return SVX_OK;
+    };
+    if (!staged && !zc_pts) SVX_TRY(stage_all());
     init_row_space(m, n);
     KeyPack kp = default_key_pack(m, pp);
     FrameCtr* hc = m->h_ctr;
@@ -478,10 +509,11 @@ svx_status integrate_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n
         SVX_TRY(reserve_frame(m, n, s));
         SVX_TRY(reserve_pools(m, s));
         m->frame_slots = choose_slots(m);
+        if (!staged && !m->frame_slots) SVX_TRY(stage_all());
         reset_ctr(m);
         FrameParams& p = hc->p;
-        p.pts = pts;
-        p.labels = (const int32_t*)labv;
+        p.pts = staged ? pts : zc_pts;
+        p.labels = (const int32_t*)(staged ? labv : zc_lab);
         p.feats = feats;
         p.n = n;
         p.pp = pp;

@@ -241,7 +241,8 @@ __device__ __forceinline__ bool warp_feats_finite(const Fe* __restrict__ feats, 
 template <class P, class Fe>
 __device__ __forceinline__ bool prepare_ray(long long i, const FrameParams& fp, double max_range,
                                             int sem_kind, int num_classes, int D, Tally& t,
-                                            double4& r, bool feats_ok = true) {
+                                            double4& r, bool feats_ok = true,
+                                            int* lab_out = nullptr) {
     double x, y, z;
     load_point((const P*)fp.pts, i, x, y, z);
     const PoseParams& pp = fp.pp;
@@ -264,7 +265,8 @@ __device__ __forceinline__ bool prepare_ray(long long i, const FrameParams& fp, 
     t.degenerate += degenerate;
     t.range += finite && !degenerate && !in_range;
     if (sem_kind == SVX_SEM_CLOSED) {
-        int lab = fp.labels[i];
+        const int lab = fp.labels[i];   // read once: may be zero-copy host memory
+        if (lab_out) *lab_out = lab;
         bool good = lab >= 1 && lab <= num_classes;
         t.bad_label += keep && !good;
         keep = keep && good;
@@ -354,9 +356,11 @@ __global__ void __launch_bounds__(kTileRays, SVX_WALK_MINB) k_walk(MarchParams m
         unsigned long long* rk = s_keys + (size_t)threadIdx.x * maxrows;
         const bool fok = sem_kind != SVX_SEM_OPEN ||
                          warp_feats_finite<Fe>((const Fe*)fp.feats, D, i, i < n);
+        int lab_i = 0;
         if (i < n) {
             double4 r;
-            if (prepare_ray<P, Fe>(i, fp, mp.max_range, sem_kind, num_classes, D, t, r, fok)) {
+            if (prepare_ray<P, Fe>(i, fp, mp.max_range, sem_kind, num_classes, D, t, r, fok,
+                                   &lab_i)) {
                 long long f0 = 0, f1 = 0, f2 = 0, l0 = 0, l1 = 0, l2 = 0;
                 int nk = 0;
                 int pl0 = INT_MIN, pl1 = INT_MIN, pl2 = INT_MIN;   // last prefetched leaf
@@ -409,7 +413,7 @@ __global__ void __launch_bounds__(kTileRays, SVX_WALK_MINB) k_walk(MarchParams m
             rcnt[i] = rows;
             if (slots) {
                 s_ray[threadIdx.x] = r;
-                s_lab[threadIdx.x] = sem_kind == SVX_SEM_CLOSED ? fp.labels[i] : 0;
+                s_lab[threadIdx.x] = lab_i;
             }
         }
         int off, total;

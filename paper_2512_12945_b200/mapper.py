@@ -447,12 +447,15 @@ class Mapper:
         return self._run(lib.svx_integrate, pts, pose.reshape(-1), lab, feat)
 
     def _integrate_fast(self, points, pose, labels):
-        """The common call -- contiguous CUDA tensors on the map's GPU (f32/f64
-        points, int32 labels for closed-set maps) and a C-contiguous float64
-        4x4 pose -- with the pose's fast acceptance test done by the library
-        (SVX_POSE_CHECK).  Returns None when the call needs the general path
-        (any other argument form, or a pose that needs full validation), so
-        checks and error messages stay those of the general path."""
+        """The common call -- contiguous CUDA tensors on the map's GPU or
+        contiguous numpy arrays (f32/f64 points, int32 labels for closed-set
+        maps) and a C-contiguous float64 4x4 pose -- with the pose's fast
+        acceptance test done by the library (SVX_POSE_CHECK).  Returns None
+        when the call needs the general path (any other argument form, or a
+        pose that needs full validation), so checks and error messages stay
+        those of the general path."""
+        if type(points) is np.ndarray:
+            return self._integrate_fast_host(points, pose, labels)
         torch = _torch_mod()
         if torch is None or type(points) is not torch.Tensor or not points.is_cuda:
             return None
@@ -478,6 +481,40 @@ class Mapper:
         stream = ctypes.c_void_p(torch._C._cuda_getCurrentRawStream(self._device))
         st = lib.svx_integrate(self._handle, points.data_ptr() if n else None, code, n,
                                pose.ctypes.data, lab_ptr, None, SVX_F32, stream, self._rep_ref)
+        if st == _lib.POSE_NEEDS_HOST:
+            return None
+        check(st)
+        self._frames += 1
+        rep = self._rep
+        return IntegrationReport(
+            points_in=rep.points_in, points_used=rep.points_used,
+            skipped_nonfinite=rep.skipped_nonfinite, skipped_range=rep.skipped_range,
+            skipped_degenerate=rep.skipped_degenerate, skipped_bad_label=rep.skipped_bad_label,
+            band_hits=rep.band_hits, touched_voxels=rep.touched_voxels,
+            kernel_ms=rep.kernel_ms, new_blocks=rep.new_blocks, new_voxels=rep.new_voxels)
+
+    def _integrate_fast_host(self, points, pose, labels):
+        """_integrate_fast for host numpy arrays: the library copies them to
+        the GPU on the default stream (pinned memory goes by DMA)."""
+        dt = points.dtype
+        if (dt != np.float32 and dt != np.float64) or points.ndim != 2 or points.shape[1] != 3 \
+                or not points.flags.c_contiguous:
+            return None
+        n = points.shape[0]
+        lab_ptr = None
+        if self._closed is not None:
+            if type(labels) is not np.ndarray or labels.dtype != np.int32 or labels.ndim != 1 \
+                    or labels.shape[0] != n or not labels.flags.c_contiguous:
+                return None
+            lab_ptr = labels.ctypes.data if n else None
+        elif labels is not None:
+            return None
+        if type(pose) is not np.ndarray or pose.dtype != np.float64 or pose.shape != (4, 4) \
+                or not pose.flags.c_contiguous:
+            return None
+        code = (SVX_F64 if dt == np.float64 else SVX_F32) | _lib.POSE_CHECK
+        st = lib.svx_integrate(self._handle, points.ctypes.data if n else None, code, n,
+                               pose.ctypes.data, lab_ptr, None, SVX_F32, None, self._rep_ref)
         if st == _lib.POSE_NEEDS_HOST:
             return None
         check(st)

@@ -66,11 +66,25 @@ def replay_oracle(g, om):
     return reps
 
 
-def replay_mapper(g, mapper, device_inputs=False):
-    """Feed a fixture through the engine's Mapper (host numpy arrays, or CUDA
-    tensors when device_inputs)."""
+def _pinned(a):
+    """A copy of numpy array `a` in page-locked host memory (numpy view)."""
+    import torch
+
+    if a is None:
+        return None
+    t = torch.empty(a.shape, dtype=torch.from_numpy(np.ascontiguousarray(a)).dtype,
+                    pin_memory=True)
+    t.copy_(torch.from_numpy(np.ascontiguousarray(a)))
+    return t.numpy()
+
+
+def replay_mapper(g, mapper, device_inputs=False, pinned=False):
+    """Feed a fixture through the engine's Mapper (host numpy arrays -- pageable,
+    or page-locked when pinned -- or CUDA tensors when device_inputs)."""
     reps = []
     for pts, pose, origin, lab, feat in frames_of(g):
+        if pinned:
+            pts, lab, feat = _pinned(pts), _pinned(lab), _pinned(feat)
         if device_inputs:
             import torch
 

@@ -57,6 +57,22 @@ def test_engine_matches_reference_fixture(name, device_inputs):
         np.testing.assert_allclose(best, g["classify_best"], rtol=1e-12)
 
 
+@pytest.mark.parametrize("mode", ["auto", "slots", "segments"])
+@pytest.mark.parametrize("name", [n for n in NAMES if "open" not in n])
+def test_pinned_host_inputs(name, mode):
+    """Page-locked host arrays: slot-mode frames read them in place
+    (zero-copy walk), segment-mode frames copy them first; same bits."""
+    g = load_golden(name)
+    m = mapper_for(g)
+    m.set_update_mode(mode)
+    reps = replay_mapper(g, m, pinned=True)
+    assert np.array_equal(report_rows(reps), g["reports"])
+    tsdf, sem = m.grids
+    assert tsdf.content_hash() == str(g["tsdf_hash"])
+    if sem is not None:
+        assert sem.content_hash() == str(g["sem_hash"])
+
+
 @pytest.mark.parametrize("name", NAMES)
 def test_compact_tsdf_vs_oracle_and_reference(name):
     g = load_golden(name)
@@ -269,14 +285,25 @@ def test_cuda_fast_path_pose_fallbacks():
     pose[:3, 3] = [0.5, -0.2, 0.1]
     r = pose[:3, :3]
     assert 1e-4 < np.abs(r @ r.T - np.eye(3)).max() <= 1e-3
-    a, b = Mapper(**kw), Mapper(**kw)
-    ra = a.integrate(tp, pose, labels=tl)            # fast path -> host fallback
-    rb = b.integrate(pts, pose, labels=lab)          # general path
-    assert ra.touched_voxels == rb.touched_voxels and ra.band_hits == rb.band_hits
-    assert a.grids[0].content_hash() == b.grids[0].content_hash()
+    a, b, c = Mapper(**kw), Mapper(**kw), Mapper(**kw)
+    ra = a.integrate(tp, pose, labels=tl)            # CUDA fast path -> host fallback
+    rb = b.integrate(pts, pose, labels=lab)          # numpy fast path -> host fallback
+    rc = c.integrate(pts, pose, labels=lab.astype(np.int64))   # general path
+    for r in (ra, rb):
+        assert r.touched_voxels == rc.touched_voxels and r.band_hits == rc.band_hits
+    assert a.grids[0].content_hash() == c.grids[0].content_hash()
+    assert b.grids[0].content_hash() == c.grids[0].content_hash()
+    # a pose inside the fast acceptance set: all three paths agree too
+    good = np.eye(4)
+    good[:3, 3] = [0.1, 0.2, -0.3]
+    ra, rb, rc = (a.integrate(tp, good, labels=tl), b.integrate(pts, good, labels=lab),
+                  c.integrate(pts.astype(np.float64).tolist(), good, labels=lab.tolist()))
+    assert a.grids[0].content_hash() == c.grids[0].content_hash() == b.grids[0].content_hash()
     for bad in (np.full((4, 4), np.nan), np.diag([1.0, 1.0, 1.0, 2.0])):
         with pytest.raises(UserInputError):
             a.integrate(tp, bad, labels=tl)
+        with pytest.raises(UserInputError):
+            b.integrate(pts, bad, labels=lab)
 
 
 @pytest.mark.parametrize("k", [5, 32, 100, 160])
