@@ -292,6 +292,23 @@ __device__ __forceinline__ RowSlot ld_slot16(const RowSlot* p) {
     return r;
 }
 
+// The first two slots of a voxel share one 32-byte sector: loaded together,
+// issued before the voxel's row count is known (asm volatile keeps the load
+// where it is written, next to the count and TSDF loads it overlaps).
+__device__ __forceinline__ void ld_slot_pair(const RowSlot* p, RowSlot& a, RowSlot& b) {
+    int x0, y0, z0, w0, x1, y1, z1, w1;
+    asm volatile("ld.global.cs.v4.s32 {%0, %1, %2, %3}, [%8];\n\t"
+                 "ld.global.cs.v4.s32 {%4, %5, %6, %7}, [%8+16];"
+                 : "=r"(x0), "=r"(y0), "=r"(z0), "=r"(w0), "=r"(x1), "=r"(y1), "=r"(z1), "=r"(w1)
+                 : "l"(p));
+    a.point = x0;
+    a.label = y0;
+    a.d = __hiloint2double(w0, z0);
+    b.point = x1;
+    b.label = y1;
+    b.d = __hiloint2double(w1, z1);
+}
+
 // 9..16 rows in-thread: 16 (point << 4 | slot) keys through a bitonic
 // network in registers, then the rows in that order.
 template <class TC>
@@ -330,6 +347,9 @@ __device__ __forceinline__ void sorted_fold16(const UpdateArgs& a, const RowSlot
 #ifndef SVX_UPD_MINB
 #define SVX_UPD_MINB 3
 #endif
+#ifndef SVX_SLOT_PAIR
+#define SVX_SLOT_PAIR 1
+#endif
 template <class TD, class TC, bool kInlineLong>
 __device__ __forceinline__ void k_update_slots_body(UpdateArgs a, const TouchEntry* __restrict__ tent,
                                                       const unsigned* __restrict__ rcount,
@@ -358,6 +378,10 @@ __device__ __forceinline__ void k_update_slots_body(UpdateArgs a, const TouchEnt
         const unsigned c = (unsigned)(bslot[en.bidx] >> 32) | (en.vid & kNewBit);
         P2 st = reinterpret_cast<const P2*>(vt)[vid];
         const RowSlot* sl = vslot + (long long)vid * kSlots * kSlotStride;
+#if SVX_SLOT_PAIR
+        RowSlot p0, p1;
+        ld_slot_pair(sl, p0, p1);   // overlaps the count load: most voxels have 1-2 rows
+#endif
         const unsigned k = c & ~kNewBit;
         if (!kInlineLong && k > 8u) {   // 9..16 rows (rare): one warp per voxel in k_update_slots_long
             a.hugelist2[warp_ticket(&ctr->n_long)] = en;
@@ -400,9 +424,15 @@ __device__ __forceinline__ void k_update_slots_body(UpdateArgs a, const TouchEnt
             }
         } else {
         // rows in registers; only slots that exist are read (no partial-sector reads)
+#if SVX_SLOT_PAIR
+        RowSlot q0 = p0, q1 = p1, q2, q3;
+        q2.point = q3.point = 0x7fffffff;
+        if (k <= 1u) q1.point = 0x7fffffff;
+#else
         RowSlot q0 = ld_slot16(sl), q1, q2, q3;
         q1.point = q2.point = q3.point = 0x7fffffff;
         if (k > 1u) q1 = ld_slot16(sl + 1 * kSlotStride);
+#endif
         if (k > 2u) q2 = ld_slot16(sl + 2 * kSlotStride);
         if (k > 3u) q3 = ld_slot16(sl + 3 * kSlotStride);
         // 4-element sorting network on the point index (5 compare-exchanges)
