@@ -203,7 +203,7 @@ svx_status svx_destroy(svx_map* m) {
                       &m->s0, &m->s1, &m->vrec, &m->vslot, &m->in_pts,
                       &m->in_lab, &m->in_feat, &m->dp_depth, &m->dp_lab_in, &m->dp_feat_in, &m->dp_pts, &m->dp_lab, &m->dp_feat, &m->ray, &m->rcnt, &m->roff, &m->rowkey,
                       &m->rowvid, &m->rowray, &m->rowd, &m->rowlab, &m->partials, &m->tlist, &m->mlist,
-                      &m->longlist, &m->srid, &m->bitmap, &m->rcount, &m->cubtmp, &m->ctr, &m->ord0,
+                      &m->longlist, &m->hinfo, &m->srid, &m->bitmap, &m->rcount, &m->cubtmp, &m->ctr, &m->ord0,
                       &m->ord1, &m->ordk0, &m->ordk1, &m->ordf0, &m->ordf1, &m->act_cnt,
                       &m->act_off, &m->act_vid, &m->act_coord, &m->q_buf, &m->out_buf,
                       &m->mesh_ctr, &m->mesh_k0, &m->mesh_k1, &m->mesh_i0, &m->mesh_i1,

@@ -23,6 +23,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "svx_internal.cuh"
 
@@ -147,6 +148,8 @@ svx_status reserve_frame(svx_map* m, int64_t n, cudaStream_t s) {
     SVX_TRY(ensure(m->longlist, 2 * sizeof(int) * rows, s));   // long list, then huge list
     SVX_TRY(ensure(m->srid, sizeof(int) * rows, s));
     SVX_TRY(ensure(m->bitmap, (size_t)4 * huge_warps() * ((m->npts_cap + 31) / 32 + 1), s));
+    if (m->cfg.sem_kind == SVX_SEM_OPEN)   // huge voxels have > 256 rows each
+        SVX_TRY(ensure(m->hinfo, huge_info_bytes() * (size_t)(rows / 256 + 2), s));
     SVX_TRY(ensure(m->rowray, sizeof(int) * rows, s));
     if (m->cfg.sem_kind != SVX_SEM_OPEN && !m->cfg.space_carving) {   // slot mode row payload
         SVX_TRY(ensure(m->rowd, sizeof(double) * rows, s));
@@ -167,7 +170,7 @@ static unsigned long long graph_signature(const svx_map* m, int pts_f64, int fea
                           m->srid.p,   m->bitmap.p, m->cubtmp.p,  m->hash.p,   m->bcoord.p,
                           m->bkey.p,   m->bmask.p,  m->bslot.p,   m->vt.p,     m->s0.p,
                           m->s1.p,     m->vrec.p,   m->vslot.p,   m->rowd.p,   m->rowlab.p,
-                          m->ctr.p};
+                          m->ctr.p,    m->hinfo.p};
     unsigned long long h = 1469598103934665603ULL;
     auto mix = [&](unsigned long long v) {
         h ^= v;
@@ -305,6 +308,16 @@ static svx_status run_frame(svx_map* m, int pts_f64, int feats_f64, cudaStream_t
         m->walk_kp[gm].kernelParams = m->walk_args[gm];
         m->walk_kp[gm].extra = nullptr;
         m->gsig[gm] = sig;
+        size_t nn = 0;
+        cudaGraphGetNodes(g, nullptr, &nn);
+        std::vector<cudaGraphNode_t> nodes(nn);
+        int nk = 0;
+        if (nn && cudaGraphGetNodes(g, nodes.data(), &nn) == cudaSuccess)
+            for (cudaGraphNode_t nd : nodes) {
+                cudaGraphNodeType t;
+                if (cudaGraphNodeGetType(nd, &t) == cudaSuccess && t == cudaGraphNodeTypeKernel) ++nk;
+            }
+        m->graph_kernels[gm] = nk;
     }
     // this frame's parameters into the first kernel's FrameParams argument
     SVX_CUDA(cudaGraphExecKernelNodeSetParams(gexec, m->walk_node[gm], &m->walk_kp[gm]));
@@ -316,7 +329,7 @@ static svx_status run_frame(svx_map* m, int pts_f64, int feats_f64, cudaStream_t
     // the graph was captured on the map's own stream; it runs on the caller's
     if (g_trace_host) g_t_launch0 = now_us();
     SVX_CUDA(cudaGraphLaunch(gexec, s));
-    count_launch(gm ? (SVX_INLINE_LONG ? 3 : 4) : 6);
+    count_launch(m->graph_kernels[gm]);   // the frame graph's kernel nodes
     SVX_CUDA(cudaEventRecord(m->ev1, s));
     if (g_trace_host) g_t_launch1 = now_us();
     SVX_CUDA(cudaEventSynchronize(m->ev1));

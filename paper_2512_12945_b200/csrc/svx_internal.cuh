@@ -252,7 +252,7 @@ struct svx_map {
     svx::DevBuf in_pts, in_lab, in_feat;
     svx::DevBuf dp_depth, dp_lab_in, dp_feat_in, dp_pts, dp_lab, dp_feat;   // depth frames
     svx::DevBuf ray, rcnt, roff, rowkey, rowvid, rowray, rowd, rowlab, partials;
-    svx::DevBuf tlist, mlist, longlist, srid, bitmap, rcount;
+    svx::DevBuf tlist, mlist, longlist, srid, bitmap, rcount, hinfo;
     uint64_t ucap = 0, rcap = 0;
     int64_t new_leaves_cap = 0;   // leaf-pool headroom kept for one frame
     int maxrows = -1;      // row slots per ray; 0 = dense rows
@@ -267,6 +267,7 @@ struct svx_map {
     void* walk_args[2][16] = {};            // its argument pointers (graph-owned storage)
     int first_nargs = 0;             // set by launch_march for the kernel it launched first
     unsigned long long gsig[2] = {};
+    int graph_kernels[2] = {0, 0};   // kernel nodes of each frame graph (launch accounting)
     svx::DevBuf cubtmp;
     svx::DevBuf ctr;      // FrameCtr
     svx::FrameCtr* h_ctr = nullptr;  // pinned, mapped mirror (host side)
@@ -561,6 +562,7 @@ svx_status launch_update_slots(svx_map* m, cudaStream_t s);
 svx_status launch_rehash(svx_map* m, int4* new_table, int64_t new_cap, cudaStream_t s);
 svx_status launch_fill_u64(unsigned long long* p, int64_t n, unsigned long long v, cudaStream_t s);
 int huge_warps();
+size_t huge_info_bytes();
 
 // frame driver pieces shared by svx_integrate and the sharded calls (svx_frame.cu)
 void init_row_space(svx_map* m, int64_t n);

@@ -20,6 +20,9 @@
 
 #include <algorithm>
 
+#include <cub/block/block_scan.cuh>
+#include <cuda_pipeline.h>
+
 #include "svx_internal.cuh"
 
 namespace svx {
@@ -912,6 +915,40 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) k_update_open(UpdateArgs a,
     }
 }
 
+// K5 open, voxels of more than kOpenCtaMin rows (a depth camera close to a
+// surface funnels most of its rays into a few voxels).  Every dimension's
+// two sums and the TSDF sums are sequential over the voxel's rows in point
+// order (the reference's order), so one voxel's work cannot be split by
+// rows -- but its dimensions are independent, so it is split by them:
+//   k_huge_prep   one CTA per huge voxel: stash (vid, count, segment, the
+//                 pre-frame weight) and sort the voxel's row ids in place
+//                 (point-index bitmap in per-CTA scratch, CTA-wide scan);
+//   k_huge_items  work items (voxel, 32-dimension slice) plus one TSDF item
+//                 per voxel, over persistent CTAs (one per SM): a slice's
+//                 feature columns stream through a 4-stage shared-memory ring
+//                 with cp.async gathers issued by all 256 threads (~96 KB in
+//                 flight per SM), while one warp folds them (lane = dimension)
+//                 -- so a voxel of N rows runs on ceil(D / 32) + 1 SMs at
+//                 once, each bound by its fp64 add chain, not by the few
+//                 bytes one thread can keep in flight.
+constexpr int kHugeThreads = 256;
+constexpr int kHugeCtas = kHugeWarps;    // prep CTAs sharing the bitmap scratch
+constexpr int kHugeSlice = 32;           // dimensions per feature item
+constexpr int kHugeStages = 4;
+constexpr int kHugeStageBytes = 32768;
+constexpr int kHugeItemCtas = 148;       // one per SM (128 KB of shared memory each)
+// Voxels of up to kGiantRows rows: one CTA each (k_update_open_huge, all
+// dimensions); bigger ones: dimension slices over many SMs (k_huge_items).
+constexpr int kGiantRows = 8192;
+
+struct HugeInfo {
+    int vid;
+    unsigned cnt;      // frame count with the new-voxel bit
+    unsigned seg;
+    unsigned pad;
+    double w_old;      // pre-frame TSDF weight (lambda of the NIG update)
+};
+
 // K5 open, voxels of more than 1024 rows (a depth camera close to a
 // surface funnels most of its rays into a few voxels): one CTA per voxel.
 // The voxel's point indices go into a bitmap (per-CTA global scratch), are
@@ -921,9 +958,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) k_update_open(UpdateArgs a,
 // dims are independent, so a voxel's D sums run in parallel; the rows'
 // features are read coalesced, 4 rows in flight).  Sums are the sequential
 // point-ordered fp64 sums of the warp path.
-constexpr int kHugeThreads = 256;
 constexpr int kHugeChunk = 2048;         // rows per shared-memory chunk (64 bitmap words)
-constexpr int kHugeCtas = kHugeWarps;    // CTAs sharing the bitmap scratch
 constexpr int kHugeDims = 4;             // dims per feature thread and pass
 constexpr int kHugeFeatThreads = kHugeThreads - 32;   // warp 0 folds the TSDF sums
 
@@ -953,6 +988,7 @@ __device__ __forceinline__ void k_update_open_huge_body(UpdateArgs a, TD* vt, TS
         const int vid = a.mlist[a.hugelist[t]];
         const unsigned c = a.rec[vid].cnt;
         const unsigned k = c & ~kNewBit;
+        if (k > (unsigned)kGiantRows) continue;   // dimension-sliced kernels (k_huge_items)
         const bool isnew = (c & kNewBit) != 0u;
         const unsigned seg = a.rec[vid].seg;
         // ---- point-index bitmap of the voxel's rows
@@ -1079,7 +1115,257 @@ __device__ __forceinline__ void k_update_open_huge_body(UpdateArgs a, TD* vt, TS
 template <class TD, class TS, class Fe>
 __global__ void __launch_bounds__(kHugeThreads, 1) k_update_open_huge(UpdateArgs a, TD* vt, TS* mean, TS* beta) {
     k_update_open_huge_body<TD, TS, Fe>(a, vt, mean, beta);
-    frame_epilogue(a.ctr, a.ctr->p.epilogue, a.ctr->p.mirror);
+}
+
+template <class TD>
+__global__ void __launch_bounds__(kHugeThreads) k_huge_prep(UpdateArgs a, const TD* vt,
+                                                             HugeInfo* hinfo, int* srid) {
+    grid_dep_wait();
+    using Scan = cub::BlockScan<int, kHugeThreads>;
+    __shared__ typename Scan::TempStorage scan_tmp;
+    __shared__ int s_min, s_max;
+    FrameCtr* ctr = a.ctr;
+    __shared__ FrameCtr s_ctr_;
+    snapshot_ctr(ctr, s_ctr_);
+    const FrameCtr* cv = &s_ctr_;
+    if (cv->abort | cv->err_cap) return;
+    const int tid = threadIdx.x, lane = tid & 31;
+    unsigned* bm = a.bitmap + (long long)blockIdx.x * a.bm_words;
+    const long long Hn = (long long)cv->n_huge;
+    for (long long t = blockIdx.x; t < Hn; t += gridDim.x) {
+        const int vid = a.mlist[a.hugelist[t]];
+        const unsigned c = a.rec[vid].cnt;
+        const unsigned k = c & ~kNewBit;
+        const unsigned seg = a.rec[vid].seg;
+        if (k <= (unsigned)kGiantRows) {   // k_update_open_huge's voxel: no items
+            if (tid == 0) hinfo[t].cnt = 0u;
+            continue;
+        }
+        if (tid == 0) {
+            HugeInfo hi;
+            hi.vid = vid;
+            hi.cnt = c;
+            hi.seg = seg;
+            hi.pad = 0u;
+            hi.w_old = (c & kNewBit) ? 0.0 : (double)vt[2 * (long long)vid + 1];
+            hinfo[t] = hi;
+            s_min = 0x7fffffff;
+            s_max = -1;
+        }
+        __syncthreads();
+        int mn = 0x7fffffff, mx = -1;
+        for (unsigned j = tid; j < k; j += kHugeThreads) {
+            const int v = srid[seg + j];
+            mn = min(mn, v);
+            mx = max(mx, v);
+        }
+        mn = (int)__reduce_min_sync(0xffffffffu, (unsigned)mn);
+        mx = (int)__reduce_max_sync(0xffffffffu, (unsigned)(mx + 1)) - 1;
+        if (lane == 0) {
+            atomicMin(&s_min, mn);
+            atomicMax(&s_max, mx);
+        }
+        __syncthreads();
+        const int minr = s_min;
+        const long long nwords = ((long long)(s_max - minr) >> 5) + 1;
+        for (long long w = tid; w < nwords; w += kHugeThreads) bm[w] = 0u;
+        __syncthreads();
+        for (unsigned j = tid; j < k; j += kHugeThreads) {
+            const int v = srid[seg + j] - minr;
+            atomicOr(&bm[v >> 5], 1u << (v & 31));
+        }
+        __threadfence_block();
+        __syncthreads();
+        // ascending ids back into the segment
+        int base = 0;
+        for (long long w0 = 0; w0 < nwords; w0 += kHugeThreads) {
+            const long long w = w0 + tid;
+            unsigned bits = w < nwords ? __ldcg(bm + w) : 0u;
+            int off, total;
+            Scan(scan_tmp).ExclusiveSum(__popc(bits), off, total);
+            int pos = base + off;
+            while (bits) {
+                const int b = __ffs(bits) - 1;
+                bits &= bits - 1;
+                srid[seg + pos++] = minr + (int)(w * 32 + b);
+            }
+            base += total;
+            __syncthreads();
+        }
+    }
+}
+
+template <class TD, class TS, class Fe>
+__global__ void __launch_bounds__(kHugeThreads, 1) k_huge_items(UpdateArgs a, TD* vt, TS* mean, TS* beta,
+                                                                const HugeInfo* __restrict__ hinfo) {
+    extern __shared__ __align__(16) unsigned char hsm[];
+    grid_dep_wait();
+    FrameCtr* ctr = a.ctr;
+    {
+    KSpan _ks(ctr, kSpanUpdateB);
+    __shared__ FrameCtr s_ctr_;
+    __shared__ double s_red[4][kHugeThreads / 32];
+    snapshot_ctr(ctr, s_ctr_);
+    const FrameCtr* cv = &s_ctr_;
+    if (!(cv->abort | cv->err_cap)) {
+    const int tid = threadIdx.x, wib = tid >> 5, lane = tid & 31;
+    const int D = a.D;
+    const int S = (D + kHugeSlice - 1) / kHugeSlice;
+    const long long Hn = (long long)cv->n_huge;
+    const KeyPack kp = cv->p.kp;
+    const PoseParams pp = cv->p.pp;
+    const Fe* feats = (const Fe*)cv->p.feats;
+    // items: per giant voxel S feature slices and one TSDF item
+    const long long items = Hn * (S + 1);
+    for (long long it = blockIdx.x; it < items; it += gridDim.x) {
+        const long long t = it / (S + 1);
+        const int sl = (int)(it % (S + 1));
+        const HugeInfo hi = hinfo[t];
+        const int vid = hi.vid;
+        const unsigned k = hi.cnt & ~kNewBit;
+        const bool isnew = (hi.cnt & kNewBit) != 0u;
+        const int* ids = a.srid + hi.seg;
+        if (k == 0u) continue;   // not a giant voxel (k_update_open_huge)
+        if (sl == S) {
+            // ---- TSDF item: w and w*d of 1024 rows at a time in parallel; thread 0
+            // folds the two sums in order (loads batched ahead of the adds), min/max
+            // by reduction (order-free)
+            double* s_w = reinterpret_cast<double*>(hsm);
+            double* s_p = s_w + 1024;
+            const Center cc = center_of(a.rec[vid].key, kp, a.h, pp);
+            double sw = 0.0, swd = 0.0, mind = INFINITY, maxd = -INFINITY;
+            for (unsigned j0 = 0; j0 < k; j0 += 1024) {
+                const unsigned n = min(1024u, k - j0);
+                for (unsigned q = tid; q < n; q += kHugeThreads) {
+                    double d, wr;
+                    row_dw(cc.x, cc.y, cc.z, a.ray[ids[j0 + q]], a.trunc, a.wfn, d, wr);
+                    s_w[q] = wr;
+                    s_p[q] = wr * d;
+                    mind = d < mind ? d : mind;
+                    maxd = d > maxd ? d : maxd;
+                }
+                __syncthreads();
+                if (tid == 0) {
+                    unsigned q = 0;
+                    for (; q + 8 <= n; q += 8) {
+                        double wv[8], pv[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            wv[u] = s_w[q + u];
+                            pv[u] = s_p[q + u];
+                        }
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            sw += wv[u];
+                            swd += pv[u];
+                        }
+                    }
+                    for (; q < n; ++q) {
+                        sw += s_w[q];
+                        swd += s_p[q];
+                    }
+                }
+                __syncthreads();
+            }
+            for (int o = 16; o; o >>= 1) {
+                mind = fmin(mind, __shfl_xor_sync(0xffffffffu, mind, o));
+                maxd = fmax(maxd, __shfl_xor_sync(0xffffffffu, maxd, o));
+            }
+            if (lane == 0) {
+                s_red[0][wib] = mind;
+                s_red[1][wib] = maxd;
+            }
+            __syncthreads();
+            if (tid == 0) {
+                for (int w = 1; w < kHugeThreads / 32; ++w) {
+                    mind = fmin(mind, s_red[0][w]);
+                    maxd = fmax(maxd, s_red[1][w]);
+                }
+                apply_tsdf<TD>(vt, vid, isnew, a.trunc, sw, swd, mind, maxd);
+                clear_voxel_frame(a, vid);
+            }
+            __syncthreads();
+            continue;
+        }
+        // ---- feature item: the 32 dimensions of slice sl
+        const int G = 1;
+        const int col0 = sl * kHugeSlice;
+        const int ncols = min(G * kHugeSlice, D - col0);
+        const int W = G * kHugeSlice;                                  // row stride in the stage
+        const int SR = kHugeStageBytes / (W * (int)sizeof(Fe));        // rows per stage
+        const int nst = (int)((k + SR - 1) / SR);
+        // every stage holds exactly kEpt elements per thread: the row ids of a
+        // thread's elements are loaded together first (independent loads), then
+        // its gathers are issued
+        constexpr int kEpt = kHugeStageBytes / (int)sizeof(Fe) / kHugeThreads;
+        auto issue = [&](int st) {
+            if (st < nst) {
+                Fe* buf = reinterpret_cast<Fe*>(hsm + (st % kHugeStages) * kHugeStageBytes);
+                int idv[kEpt];
+#pragma unroll
+                for (int i = 0; i < kEpt; ++i) {
+                    const int e = tid + i * kHugeThreads;
+                    const unsigned j = (unsigned)(st * SR + e / W);
+                    idv[i] = j < k ? __ldg(ids + j) : 0;
+                }
+#pragma unroll
+                for (int i = 0; i < kEpt; ++i) {
+                    const int e = tid + i * kHugeThreads;
+                    const int r = e / W, c = e - r * W;
+                    const unsigned j = (unsigned)(st * SR + r);
+                    if (j < k && c < ncols)
+                        __pipeline_memcpy_async(buf + e, feats + (long long)idv[i] * D + col0 + c,
+                                                sizeof(Fe));
+                }
+            }
+            __pipeline_commit();
+        };
+        for (int st = 0; st < kHugeStages - 1; ++st) issue(st);
+        const int mycol = wib * kHugeSlice + lane;                     // this thread's dimension
+        const bool folds = wib < G && mycol < ncols;
+        double sz = 0.0, sz2 = 0.0;
+        for (int st = 0; st < nst; ++st) {
+            issue(st + kHugeStages - 1);   // into the buffer the previous iteration consumed
+            __pipeline_wait_prior(kHugeStages - 1);
+            __syncthreads();
+            if (folds) {
+                const Fe* buf = reinterpret_cast<const Fe*>(hsm + (st % kHugeStages) * kHugeStageBytes);
+                const int n = min(SR, (int)(k - (unsigned)(st * SR)));
+                int r = 0;
+                for (; r + 8 <= n; r += 8) {
+                    double z[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) z[u] = (double)buf[(r + u) * W + mycol];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        sz += z[u];
+                        sz2 += z[u] * z[u];
+                    }
+                }
+                for (; r < n; ++r) {
+                    const double z = (double)buf[r * W + mycol];
+                    sz += z;
+                    sz2 += z * z;
+                }
+            }
+            __syncthreads();
+        }
+        __pipeline_wait_prior(0);
+        if (folds) {
+            // NIG batch update with lambda from the pre-frame weight (_pycore.py:438)
+            const double nobs = (double)k;
+            const double lam = fmax(hi.w_old, a.lambda_floor);
+            const double lam_post = lam + nobs;
+            const double coef = lam * nobs / lam_post;
+            const double b_bg = (double)(TS)a.prior_beta;
+            nig_apply<TS>(mean + (long long)vid * D, beta + (long long)vid * D, col0 + mycol, isnew, sz,
+                          sz2, lam, lam_post, coef, nobs, b_bg);
+        }
+        __syncthreads();
+    }
+    }
+    }
+    frame_epilogue(ctr, ctr->p.epilogue, ctr->p.mirror);
 }
 
 __global__ void k_rehash(int64_t nblocks, const int4* __restrict__ bcoord, int4* table,
@@ -1169,8 +1455,17 @@ svx_status open_a(svx_map* m, cudaStream_t s) {
 
 template <class TD, class TS, class Fe>
 svx_status open_b(svx_map* m, cudaStream_t s) {
-    SVX_CUDA(launch_pdl(k_update_open_huge<TD, TS, Fe>, kHugeCtas, kHugeThreads, 0, s, 
-        make_args(m), ptr<TD>(m->vt), ptr<TS>(m->s0), ptr<TS>(m->s1)));
+    SVX_CUDA(launch_pdl(k_update_open_huge<TD, TS, Fe>, kHugeCtas, kHugeThreads, 0, s, make_args(m),
+                        ptr<TD>(m->vt), ptr<TS>(m->s0), ptr<TS>(m->s1)));
+    SVX_LAUNCHED();
+    SVX_CUDA(launch_pdl(k_huge_prep<TD>, kHugeCtas, kHugeThreads, 0, s, make_args(m), ptr<TD>(m->vt),
+                        ptr<HugeInfo>(m->hinfo), ptr<int>(m->srid)));
+    SVX_LAUNCHED();
+    const int smem = kHugeStages * kHugeStageBytes;
+    SVX_CUDA(cudaFuncSetAttribute(k_huge_items<TD, TS, Fe>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  smem));
+    SVX_CUDA(launch_pdl(k_huge_items<TD, TS, Fe>, kHugeItemCtas, kHugeThreads, smem, s, make_args(m),
+                        ptr<TD>(m->vt), ptr<TS>(m->s0), ptr<TS>(m->s1), ptr<HugeInfo>(m->hinfo)));
     SVX_LAUNCHED();
     return SVX_OK;
 }
@@ -1248,5 +1543,6 @@ svx_status launch_fill_u64(unsigned long long* p, int64_t n, unsigned long long 
 }
 
 int huge_warps() { return kHugeWarps; }
+size_t huge_info_bytes() { return sizeof(HugeInfo); }
 
 }  // namespace svx
