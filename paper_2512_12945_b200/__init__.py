@@ -19,13 +19,13 @@ from .mapper import (GridView, IntegrationReport, Mapper, grids_equal, load_grid
                      validate_rotation)
 
 from .render import RenderCamera, render, sample_distance
-from .surface import SemanticMesh, default_palette, palette_colors
+from .surface import SemanticMesh, default_palette, palette_colors, read_ply, write_ply
 
 __version__ = "0.1.0"
 
 __all__ = [
     "Mapper", "load_grid", "grids_equal", "RenderCamera", "render", "sample_distance",
-    "SemanticMesh", "default_palette", "palette_colors", "GridView", "IntegrationReport", "validate_rotation",
+    "SemanticMesh", "default_palette", "palette_colors", "write_ply", "read_ply", "GridView", "IntegrationReport", "validate_rotation",
     "FusionConfig", "ClosedSetConfig", "OpenSetConfig", "EngineConfig",
     "SemvoxError", "UserInputError", "ConfigError", "PayloadMismatchError",
     "FormatError", "OutOfRangeError",

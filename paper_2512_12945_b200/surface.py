@@ -75,6 +75,64 @@ def check_palette(palette) -> np.ndarray:
     return palette
 
 
+def write_ply(mesh: SemanticMesh, path) -> None:
+    """ASCII PLY with per-vertex colour and class label, the reference's
+    layout (mesh.py:580-600): byte-identical files for identical meshes."""
+    mesh.validate()
+    with open(path, "w", encoding="ascii") as fh:
+        fh.write("ply\nformat ascii 1.0\n")
+        fh.write("element vertex %d\n" % mesh.n_vertices)
+        fh.write("property float x\nproperty float y\nproperty float z\n")
+        fh.write("property uchar red\nproperty uchar green\nproperty uchar blue\n")
+        fh.write("property int label\n")
+        fh.write("element face %d\n" % mesh.n_triangles)
+        fh.write("property list uchar int vertex_indices\nend_header\n")
+        rows = np.column_stack([mesh.vertices, mesh.colors.astype(np.float64),
+                                mesh.labels.astype(np.float64)])
+        np.savetxt(fh, rows, fmt=["%.9g"] * 3 + ["%d"] * 4)
+        np.savetxt(fh, mesh.triangles, fmt="3 %d %d %d")
+
+
+def read_ply(path) -> SemanticMesh:
+    """Read meshes written by write_ply (mesh.py:603-650): ASCII, fixed layout."""
+    with open(path, "r", encoding="ascii") as fh:
+        if fh.readline().strip() != "ply":
+            raise SemvoxError("%s: not a PLY file" % path)
+        n_vert = n_face = -1
+        while True:
+            line = fh.readline()
+            if not line:
+                raise SemvoxError("%s: unterminated PLY header" % path)
+            parts = line.split()
+            if parts[:2] in (["format", "binary_little_endian"], ["format", "binary_big_endian"]):
+                raise SemvoxError("%s: only ASCII PLY is supported" % path)
+            if parts[:2] == ["element", "vertex"]:
+                n_vert = int(parts[2])
+            elif parts[:2] == ["element", "face"]:
+                n_face = int(parts[2])
+            elif parts[:1] == ["end_header"]:
+                break
+        if n_vert < 0 or n_face < 0:
+            raise SemvoxError("%s: missing vertex/face elements" % path)
+        verts = np.zeros((n_vert, 3), np.float64)
+        labels = np.zeros(n_vert, np.int32)
+        colors = np.zeros((n_vert, 3), np.uint8)
+        for i in range(n_vert):
+            f = fh.readline().split()
+            verts[i] = [float(f[0]), float(f[1]), float(f[2])]
+            colors[i] = [int(f[3]), int(f[4]), int(f[5])]
+            labels[i] = int(f[6])
+        tri = np.zeros((n_face, 3), np.int32)
+        for i in range(n_face):
+            f = fh.readline().split()
+            if int(f[0]) != 3:
+                raise SemvoxError("%s: face %d is not a triangle" % (path, i))
+            tri[i] = [int(f[1]), int(f[2]), int(f[3])]
+    mesh = SemanticMesh(vertices=verts, triangles=tri, labels=labels, colors=colors)
+    mesh.validate()
+    return mesh
+
+
 def palette_colors(labels, palette) -> np.ndarray:
     """Host restatement of the device colour lookup (label 0 -> row 0,
     others wrap over rows 1..), for callers colouring their own labels."""

@@ -466,6 +466,13 @@ def main_mesh():
             _mesh_out(out, f"v{j}_", mesh)
             out[f"v{j}_min_weight"] = np.array(v.get("min_weight", 0.5))
             out[f"v{j}_emb"] = np.array(bool(v.get("emb")))
+            if j == 0:   # the reference's PLY text of this mesh (write_ply, mesh.py:580-600)
+                from semvox import write_ply
+
+                with tempfile.TemporaryDirectory() as td2:
+                    pp = os.path.join(td2, "m.ply")
+                    write_ply(mesh, pp)
+                    out["ply_v0"] = np.frombuffer(open(pp, "rb").read(), np.uint8)
             print(stem, j, mesh.n_vertices, mesh.n_triangles, len(raw))
         out["n_variants"] = np.array(len(variants))
         np.savez_compressed(os.path.join(HERE, f"mesh_{stem}.npz"), **out)
