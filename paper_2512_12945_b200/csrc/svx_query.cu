@@ -11,6 +11,8 @@
 
 #include <cub/cub.cuh>
 
+#include <cuda_pipeline.h>
+
 #include "svx_internal.cuh"
 
 namespace svx {
@@ -257,6 +259,7 @@ __global__ void k_classify(int64_t count, int D, int k, const int* __restrict__ 
 // dim d0 + lane % 4) straight from global (f32 -> f64) and accumulates the
 // row's squared norm on the way.
 constexpr int kDc = 16;              // dims per shared-memory chunk
+
 constexpr int kClsWarps = 4;
 
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
@@ -265,23 +268,15 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
                  : "d"(a), "d"(b));
 }
 
-template <int NT, int MT, class TS, class TD>
+template <int NT, int MT, bool kStaged, class TS, class TD>
 __global__ void __launch_bounds__(32 * kClsWarps) k_classify_dmma(
     int64_t count, int D, int k, const int* __restrict__ act_vid, const TS* __restrict__ mean,
     const TD* __restrict__ vw, const double* __restrict__ emb, const double* __restrict__ en,
     double tau, double tp, int32_t* __restrict__ labels, double* __restrict__ best,
     double* __restrict__ sims_out) {
-    __shared__ double s_e[NT * 8][kDc + 1];   // +1: no bank conflicts on the B fragment reads
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int qr = lane >> 2, qc = lane & 3;   // fragment row / column group
-    const int64_t row0 = ((int64_t)blockIdx.x * kClsWarps + warp) * (8 * MT);
-    const TS* rp[MT];
     int64_t ri[MT];
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt) {
-        ri[mt] = row0 + mt * 8 + qr;
-        rp[mt] = ri[mt] < count ? mean + (int64_t)act_vid[ri[mt]] * D : nullptr;
-    }
     double acc[MT][NT][2];
     double nn[MT];
 #pragma unroll
@@ -289,6 +284,76 @@ __global__ void __launch_bounds__(32 * kClsWarps) k_classify_dmma(
         nn[mt] = 0.0;
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+    }
+    if constexpr (kStaged) {
+    // both operands stream through a 2-stage shared-memory ring (cp.async):
+    // the next chunk's voxel means and queries are in flight while this
+    // chunk's DMMAs run
+    constexpr int RA = kClsWarps * 8 * MT;   // voxel rows per CTA
+    __shared__ TS s_a[2][RA][kDc + 1];
+    __shared__ double s_b[2][NT * 8][kDc + 1];
+    __shared__ int s_vid[RA];
+    const int64_t cta0 = (int64_t)blockIdx.x * RA;
+    for (int r = threadIdx.x; r < RA; r += blockDim.x)
+        s_vid[r] = cta0 + r < count ? act_vid[cta0 + r] : -1;
+    __syncthreads();
+    const int64_t row0 = cta0 + warp * (8 * MT);
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) ri[mt] = row0 + mt * 8 + qr;
+    const int nch = (D + kDc - 1) / kDc;
+    auto issue = [&](int ch) {
+        if (ch < nch) {
+            const int st = ch & 1, d0 = ch * kDc;
+            for (int t = threadIdx.x; t < RA * kDc; t += blockDim.x) {
+                const int r = t / kDc, c = t % kDc;
+                const int vid = s_vid[r];
+                if (vid >= 0 && d0 + c < D)
+                    __pipeline_memcpy_async(&s_a[st][r][c], mean + (int64_t)vid * D + d0 + c, sizeof(TS));
+                else
+                    s_a[st][r][c] = (TS)0;
+            }
+            for (int t = threadIdx.x; t < NT * 8 * kDc; t += blockDim.x) {
+                const int j = t / kDc, c = t % kDc;
+                if (j < k && d0 + c < D)
+                    __pipeline_memcpy_async(&s_b[st][j][c], emb + (int64_t)j * D + d0 + c, sizeof(double));
+                else
+                    s_b[st][j][c] = 0.0;
+            }
+        }
+        __pipeline_commit();
+    };
+    issue(0);
+    for (int ch = 0; ch < nch; ++ch) {
+        issue(ch + 1);   // into the buffer the previous iteration consumed
+        __pipeline_wait_prior(1);
+        __syncthreads();
+        const int st = ch & 1;
+#pragma unroll
+        for (int kk = 0; kk < kDc; kk += 4) {
+            double a[MT];
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) {
+                a[mt] = (double)s_a[st][warp * 8 * MT + mt * 8 + qr][kk + qc];
+                nn[mt] += a[mt] * a[mt];
+            }
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+                const double b = s_b[st][nt * 8 + qr][kk + qc];
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) dmma(acc[mt][nt], a[mt], b);
+            }
+        }
+        __syncthreads();
+    }
+    __pipeline_wait_prior(0);
+    } else {
+    __shared__ double s_e[NT * 8][kDc + 1];   // +1: no bank conflicts on the B fragment reads
+    const int64_t row0 = ((int64_t)blockIdx.x * kClsWarps + warp) * (8 * MT);
+    const TS* rp[MT];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+        ri[mt] = row0 + mt * 8 + qr;
+        rp[mt] = ri[mt] < count ? mean + (int64_t)act_vid[ri[mt]] * D : nullptr;
     }
     for (int d0 = 0; d0 < D; d0 += kDc) {
         __syncthreads();
@@ -313,6 +378,7 @@ __global__ void __launch_bounds__(32 * kClsWarps) k_classify_dmma(
                 for (int mt = 0; mt < MT; ++mt) dmma(acc[mt][nt], a[mt], b);
             }
         }
+    }
     }
     // epilogue: row qr of each m-tile lives in the 4 lanes of quad qr
 #pragma unroll
@@ -587,12 +653,12 @@ svx_status launch_cosine(svx_map* m, int64_t count, const double* q, double qn, 
     return SVX_OK;
 }
 
-template <int NT, int MT, class TS, class TD>
+template <int NT, int MT, bool kStaged, class TS, class TD>
 static svx_status classify_dmma_t(svx_map* m, int64_t count, const double* emb, const double* en,
                                   int k, double tau, double tp, int32_t* labels, double* best,
                                   double* sims, cudaStream_t s) {
     const int64_t rows_per_cta = (int64_t)kClsWarps * 8 * MT;
-    k_classify_dmma<NT, MT, TS, TD><<<(unsigned)((count + rows_per_cta - 1) / rows_per_cta),
+    k_classify_dmma<NT, MT, kStaged, TS, TD><<<(unsigned)((count + rows_per_cta - 1) / rows_per_cta),
                                       32 * kClsWarps, 0, s>>>(
         count, m->payload_d, k, ptr<int>(m->act_vid), ptr<TS>(m->s0), ptr<TD>(m->vt), emb, en,
         tau, tp, labels, best, sims);
@@ -606,11 +672,18 @@ static svx_status classify_t(svx_map* m, int64_t count, const double* emb, const
                              cudaStream_t s) {
     // FP64 tensor cores (DMMA) for up to 128 queries; the warp-per-voxel
     // CUDA-core kernel beyond
-    if (k <= 8) return classify_dmma_t<1, 4, TS, TD>(m, count, emb, en, k, tau, tp, labels, best, sims, s);
-    if (k <= 16) return classify_dmma_t<2, 4, TS, TD>(m, count, emb, en, k, tau, tp, labels, best, sims, s);
-    if (k <= 32) return classify_dmma_t<4, 4, TS, TD>(m, count, emb, en, k, tau, tp, labels, best, sims, s);
-    if (k <= 64) return classify_dmma_t<8, 2, TS, TD>(m, count, emb, en, k, tau, tp, labels, best, sims, s);
-    if (k <= 128) return classify_dmma_t<16, 1, TS, TD>(m, count, emb, en, k, tau, tp, labels, best, sims, s);
+    // up to 64 queries: operands straight from global/L2 (measured best); 65..128:
+    // both operands through a cp.async ring, two m-tiles per warp for f32 means
+    // (cfg5, D = 768, k = 128: 29 % -> 49 % of the FP64 tensor peak)
+    if (k <= 8) return classify_dmma_t<1, 4, false, TS, TD>(m, count, emb, en, k, tau, tp, labels, best, sims, s);
+    if (k <= 16) return classify_dmma_t<2, 4, false, TS, TD>(m, count, emb, en, k, tau, tp, labels, best, sims, s);
+    if (k <= 32) return classify_dmma_t<4, 4, false, TS, TD>(m, count, emb, en, k, tau, tp, labels, best, sims, s);
+    if (k <= 64) return classify_dmma_t<8, 2, false, TS, TD>(m, count, emb, en, k, tau, tp, labels, best, sims, s);
+    if (k <= 128) {
+        if constexpr (sizeof(TS) == 4)
+            return classify_dmma_t<16, 2, true, TS, TD>(m, count, emb, en, k, tau, tp, labels, best, sims, s);
+        return classify_dmma_t<16, 1, true, TS, TD>(m, count, emb, en, k, tau, tp, labels, best, sims, s);
+    }
     const int T = 256;
     k_classify<TS, TD><<<grid_for(count * 32, T), T, 0, s>>>(
         count, m->payload_d, k, ptr<int>(m->act_vid), ptr<TS>(m->s0), ptr<TD>(m->vt), emb, en,
