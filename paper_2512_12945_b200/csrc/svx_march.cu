@@ -284,11 +284,25 @@ __device__ __forceinline__ bool prepare_ray(long long i, const FrameParams& fp, 
 }
 
 __device__ void gate_body(FrameCtr* ctr);
+#ifndef SVX_WALK_FENCE1
+#define SVX_WALK_FENCE1 1
+#endif
 
 // Every CTA of a walk adds its tallies; the last one to finish runs the gate.
 template <int kThreads>
 __device__ __forceinline__ void finish_walk(const Tally& t, MarchPartial*, FrameCtr* ctr) {
     publish_tally<kThreads>(t, ctr);
+#if SVX_WALK_FENCE1
+    // thread 0 published this CTA's tallies: it alone fences before counting
+    // the CTA done (the rows reach the next kernel through the kernel boundary)
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(&ctr->walk_done, 1u) == gridDim.x - 1) {
+            __threadfence();
+            gate_body(ctr);
+        }
+    }
+#else
     __shared__ bool s_last;
     __threadfence();
     __syncthreads();
@@ -298,6 +312,7 @@ __device__ __forceinline__ void finish_walk(const Tally& t, MarchPartial*, Frame
         __threadfence();
         gate_body(ctr);
     }
+#endif
 }
 
 // K1 (bounded bands): compute-only walk over 128-ray tiles.  Each ray's row
