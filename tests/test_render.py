@@ -212,3 +212,39 @@ def test_render_full_size_map_vs_oracle():
         if mode == "depth":
             assert (img > 0).sum() > 300
         assert np.array_equal(img, want), mode
+
+
+@pytest.mark.gpu
+def test_compact_f32_map_queries_vs_oracle(tmp_path):
+    """The compact layout (tsdf_dtype float32): marching cubes and rendering
+    read the stored f32 pair as f64, exactly like the oracle run on the
+    exported state; a snapshot of it stores f64 and loads back unchanged."""
+    from oracle import mesh as om
+    from oracle import render as orc
+    from oracle.render import VoxelState
+    from paper_2512_12945_b200 import Mapper, RenderCamera
+
+    g = load_golden("api_closed_plane")
+    kw = dict(g["mapper_kw"], tsdf_dtype="float32")
+    m = Mapper(**kw)
+    replay_mapper(g, m)
+    coords, d, w, s0, _ = m._export()
+    mesh = m.extract()
+    want = om.extract(coords, d, w, kw["voxel_size"], 0.5, "closed", s0,
+                      palette_size=kw["num_classes"])
+    assert mesh.n_triangles > 100
+    for a, b in zip((mesh.vertices, mesh.triangles, mesh.labels, mesh.colors), want):
+        assert np.array_equal(a, b)
+    st = VoxelState(coords, d, w, kw["voxel_size"], kw["truncation"], "closed", s0)
+    cam = RenderCamera(**cam_args("down"))
+    for mode in ("depth", "semantic"):
+        img = m.render(cam, mode=mode)
+        ref = orc.render(st, cam.pose, cam.fx, cam.fy, cam.cx, cam.cy, cam.width, cam.height,
+                         cam.near, cam.far, mode=mode, palette_size=kw["num_classes"])
+        assert np.array_equal(img, ref), mode
+    p = tmp_path / "f32.slvg"
+    m.save(p)
+    m2 = Mapper.from_snapshot(p, tsdf_dtype="float32")
+    c2, d2, w2, s2, _ = m2._export()
+    assert np.array_equal(c2, coords) and np.array_equal(d2, d) and np.array_equal(w2, w)
+    assert np.array_equal(s2, s0)
