@@ -16,6 +16,10 @@
 
 #include "svx_internal.cuh"
 
+#ifndef SVX_RESOLVE_PREFETCH
+#define SVX_RESOLVE_PREFETCH 1
+#endif
+
 namespace svx {
 namespace rt {
 
@@ -324,7 +328,7 @@ __device__ __forceinline__ void resolve_step(const ResolveArgs& ra, bool valid,
     rank = cta_rank<kThreads>(first, cnt, s_warp);
     if (slots) {
         if (first) {
-            if (vid >= 0) {
+            if (SVX_RESOLVE_PREFETCH && vid >= 0) {
                 const char* pv = ra.vt + (long long)vid * ra.vt_bytes;
                 asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(pv));
                 if (ra.ncounts && rsl.label >= 1) {
