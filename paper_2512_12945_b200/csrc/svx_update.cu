@@ -781,6 +781,9 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, SVX_LONGK_MINB) k_update_lo
 // ---- K5 open set: one warp per voxel, lanes own feature dimensions ------------
 
 constexpr int kOpenPer = 8;   // dims per lane per pass (256 dims per pass)
+#ifndef SVX_OPEN_RING
+#define SVX_OPEN_RING 1
+#endif
 // open-set voxels with more rows than this go to the CTA-per-voxel kernel
 #ifndef SVX_OPEN_CTA_MIN
 #define SVX_OPEN_CTA_MIN 256   // measured best of 64 / 256 / 1024 on cfg3 and cfg5
@@ -826,11 +829,73 @@ __device__ __forceinline__ void open_chunk(const Fe* __restrict__ feats, int D, 
     }
 }
 
+// open_chunk with the rows' feature slices streamed through this lane's
+// part of a shared-memory ring by cp.async: kOpenRingR rows per group,
+// kOpenRingS groups in flight.  Every lane reads back only what it copied
+// itself, so the ring needs no warp synchronisation; the sums are the same
+// in-order sums as open_chunk.
+#ifndef SVX_OPEN_RING_R
+#define SVX_OPEN_RING_R 2
+#endif
+#ifndef SVX_OPEN_RING_S
+#define SVX_OPEN_RING_S 2
+#endif
+constexpr int kOpenRingR = SVX_OPEN_RING_R;
+constexpr int kOpenRingS = SVX_OPEN_RING_S;
+constexpr int kOpenPass = 32 * kOpenPer;   // dims per pass
+
+template <class Fe>
+__device__ __forceinline__ void open_chunk_ring(const Fe* __restrict__ feats, int D, int base,
+                                                const int* buf, int cnt, double* sz, double* sz2,
+                                                Fe* ring) {
+    const int lane = threadIdx.x & 31;
+    const int ng = (cnt + kOpenRingR - 1) / kOpenRingR;
+    auto issue = [&](int g) {
+        if (g < ng) {
+            Fe* dst = ring + (g % kOpenRingS) * kOpenRingR * kOpenPass;
+#pragma unroll
+            for (int r = 0; r < kOpenRingR; ++r) {
+                const int j = g * kOpenRingR + r;
+                if (j < cnt) {
+                    const Fe* src = feats + (long long)buf[j] * D + base;
+#pragma unroll
+                    for (int q = 0; q < kOpenPer; ++q) {
+                        const int cc = lane + 32 * q;
+                        if (base + cc < D)
+                            __pipeline_memcpy_async(dst + r * kOpenPass + cc, src + cc, sizeof(Fe));
+                    }
+                }
+            }
+        }
+        __pipeline_commit();
+    };
+#pragma unroll
+    for (int g = 0; g < kOpenRingS - 1; ++g) issue(g);
+    for (int g = 0; g < ng; ++g) {
+        issue(g + kOpenRingS - 1);
+        __pipeline_wait_prior(kOpenRingS - 1);
+        const Fe* src = ring + (g % kOpenRingS) * kOpenRingR * kOpenPass;
+        const int n = min(kOpenRingR, cnt - g * kOpenRingR);
+        for (int r = 0; r < n; ++r) {
+#pragma unroll
+            for (int q = 0; q < kOpenPer; ++q) {
+                const int cc = lane + 32 * q;
+                if (base + cc < D) {
+                    const double zv = (double)src[r * kOpenPass + cc];
+                    sz[q] += zv;
+                    sz2[q] += zv * zv;
+                }
+            }
+        }
+    }
+    __pipeline_wait_prior(0);
+}
+
 template <class TD, class TS, class Fe>
 __device__ __forceinline__ void open_voxel(const UpdateArgs& a, const KeyPack& kp,
                                            const PoseParams& pp, TD* vt, TS* mean, TS* beta,
                                            const Fe* feats, int vid, unsigned c, int* buf,
-                                           unsigned* bm, bool huge) {
+                                           unsigned* bm, bool huge, Fe* ring = nullptr) {
     const int lane = threadIdx.x & 31;
     const unsigned k = c & ~kNewBit;
     const bool isnew = (c & kNewBit) != 0u;
@@ -871,6 +936,8 @@ __device__ __forceinline__ void open_voxel(const UpdateArgs& a, const KeyPack& k
                 open_chunk<Fe>(feats, a.D, base, buf, cnt, sz, sz2);
                 __syncwarp();
             }
+        } else if (ring) {
+            open_chunk_ring<Fe>(feats, a.D, base, buf, (int)k, sz, sz2, ring);
         } else {
             open_chunk<Fe>(feats, a.D, base, buf, (int)k, sz, sz2);
         }
@@ -892,6 +959,9 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) k_update_open(UpdateArgs a,
                                                                    TS* beta) {
     grid_dep_wait();
     __shared__ int sbuf[kWarpsPerCta][kSmemMax];
+#if SVX_OPEN_RING
+    extern __shared__ __align__(16) unsigned char oring[];
+#endif
     FrameCtr* ctr = a.ctr;
     KSpan _ks(ctr, kSpanUpdate);
     __shared__ FrameCtr s_ctr_;
@@ -911,7 +981,12 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) k_update_open(UpdateArgs a,
             if (lane == 0) a.hugelist[atomicAdd(&ctr->n_huge, 1ULL)] = (int)e;
             continue;
         }
+#if SVX_OPEN_RING
+        Fe* ring = reinterpret_cast<Fe*>(oring) + (size_t)wib * kOpenRingS * kOpenRingR * kOpenPass;
+        open_voxel<TD, TS, Fe>(a, kp, pp, vt, mean, beta, feats, vid, c, sbuf[wib], nullptr, false, ring);
+#else
         open_voxel<TD, TS, Fe>(a, kp, pp, vt, mean, beta, feats, vid, c, sbuf[wib], nullptr, false);
+#endif
     }
 }
 
@@ -940,6 +1015,13 @@ constexpr int kHugeItemCtas = 148;       // one per SM (128 KB of shared memory 
 // Voxels of up to kGiantRows rows: one CTA each (k_update_open_huge, all
 // dimensions); bigger ones: dimension slices over many SMs (k_huge_items).
 constexpr int kGiantRows = 8192;
+#ifndef SVX_HUGE_RING
+#define SVX_HUGE_RING 1
+#endif
+#ifndef SVX_HUGE_RING_R
+#define SVX_HUGE_RING_R 8
+#endif
+constexpr int kHugeRingR = SVX_HUGE_RING_R;   // rows per ring group (k_update_open_huge)
 
 struct HugeInfo {
     int vid;
@@ -968,6 +1050,10 @@ __device__ __forceinline__ void k_update_open_huge_body(UpdateArgs a, TD* vt, TS
     __shared__ int s_id[kHugeChunk];
     __shared__ double s_d[kHugeChunk];
     __shared__ double s_w[kHugeChunk];
+#if SVX_HUGE_RING
+    extern __shared__ __align__(16) unsigned char hring_raw[];
+    Fe* hring = reinterpret_cast<Fe*>(hring_raw);
+#endif
     __shared__ int s_wcnt[kHugeThreads / 32];
     __shared__ int s_min, s_max, s_cnt;
     __shared__ double s_wold;
@@ -1065,6 +1151,54 @@ __device__ __forceinline__ void k_update_open_huge_body(UpdateArgs a, TD* vt, TS
                     acc.maxd = dq > acc.maxd ? dq : acc.maxd;
                 }
             }
+#if SVX_HUGE_RING
+            // rows stream through this thread's slots of a shared-memory ring
+            // (cp.async, kHugeRingR rows x kHugeDims dims per group, two groups
+            // in flight); slot-major layout, so a warp's slots are consecutive
+            if (tid >= 32) {
+                const int ng = (cnt + kHugeRingR - 1) / kHugeRingR;
+                auto slot_of_ring = [&](int g, int r, int q) {
+                    return hring + ((size_t)(((g & 1) * kHugeRingR + r) * kHugeDims + q) * kHugeThreads + tid);
+                };
+                auto issue = [&](int g) {
+                    if (g < ng) {
+#pragma unroll
+                        for (int r = 0; r < kHugeRingR; ++r) {
+                            const int j = g * kHugeRingR + r;
+                            if (j < cnt) {
+                                const long long rowb = (long long)s_id[j] * D;
+#pragma unroll
+                                for (int q = 0; q < kHugeDims; ++q) {
+                                    const int col = dbase + (tid - 32) + q * kHugeFeatThreads;
+                                    if (col < D)
+                                        __pipeline_memcpy_async(slot_of_ring(g, r, q), feats + rowb + col,
+                                                                sizeof(Fe));
+                                }
+                            }
+                        }
+                    }
+                    __pipeline_commit();
+                };
+                issue(0);
+                for (int g = 0; g < ng; ++g) {
+                    issue(g + 1);
+                    __pipeline_wait_prior(1);
+                    const int n = min(kHugeRingR, cnt - g * kHugeRingR);
+                    for (int r = 0; r < n; ++r) {
+#pragma unroll
+                        for (int q = 0; q < kHugeDims; ++q) {
+                            const int col = dbase + (tid - 32) + q * kHugeFeatThreads;
+                            if (col < D) {
+                                const double z = (double)*slot_of_ring(g, r, q);
+                                sz[q] += z;
+                                sz2[q] += z * z;
+                            }
+                        }
+                    }
+                }
+                __pipeline_wait_prior(0);
+            }
+#else
 #pragma unroll
             for (int q = 0; q < kHugeDims; ++q) {
                 const int col = dbase + (tid - 32) + q * kHugeFeatThreads;
@@ -1086,6 +1220,7 @@ __device__ __forceinline__ void k_update_open_huge_body(UpdateArgs a, TD* vt, TS
                     sz2[q] += z * z;
                 }
             }
+#endif
             __syncthreads();
         }
         if (first_pass) {
@@ -1447,7 +1582,11 @@ svx_status closed_b(svx_map* m, cudaStream_t s) {
 
 template <class TD, class TS, class Fe>
 svx_status open_a(svx_map* m, cudaStream_t s) {
-    SVX_CUDA(launch_pdl(k_update_open<TD, TS, Fe>, kLongBlocks, 32 * kWarpsPerCta, 0, s, 
+    const int ring = SVX_OPEN_RING ? kWarpsPerCta * kOpenRingS * kOpenRingR * kOpenPass * (int)sizeof(Fe) : 0;
+    if (ring > 0)
+        SVX_CUDA(cudaFuncSetAttribute(k_update_open<TD, TS, Fe>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      ring));
+    SVX_CUDA(launch_pdl(k_update_open<TD, TS, Fe>, kLongBlocks, 32 * kWarpsPerCta, ring, s, 
         make_args(m), ptr<TD>(m->vt), ptr<TS>(m->s0), ptr<TS>(m->s1)));
     SVX_LAUNCHED();
     return SVX_OK;
@@ -1455,7 +1594,11 @@ svx_status open_a(svx_map* m, cudaStream_t s) {
 
 template <class TD, class TS, class Fe>
 svx_status open_b(svx_map* m, cudaStream_t s) {
-    SVX_CUDA(launch_pdl(k_update_open_huge<TD, TS, Fe>, kHugeCtas, kHugeThreads, 0, s, make_args(m),
+    const int hsmem = SVX_HUGE_RING ? 2 * kHugeRingR * kHugeDims * kHugeThreads * (int)sizeof(Fe) : 0;
+    if (hsmem > 0)
+        SVX_CUDA(cudaFuncSetAttribute(k_update_open_huge<TD, TS, Fe>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, hsmem));
+    SVX_CUDA(launch_pdl(k_update_open_huge<TD, TS, Fe>, kHugeCtas, kHugeThreads, hsmem, s, make_args(m),
                         ptr<TD>(m->vt), ptr<TS>(m->s0), ptr<TS>(m->s1)));
     SVX_LAUNCHED();
     SVX_CUDA(launch_pdl(k_huge_prep<TD>, kHugeCtas, kHugeThreads, 0, s, make_args(m), ptr<TD>(m->vt),
