@@ -395,14 +395,19 @@ void reset_ctr(svx_map* m) {
 // and the caller runs the frame again.
 svx_status recover_capacity(svx_map* m, int64_t nblocks0, cudaStream_t s) {
     FrameCtr* hc = m->h_ctr;
+    // the attempt's allocation counters kept counting past the pools: they
+    // are the frame's demand (voxels of leaves that could not be created are
+    // not in it yet, so a second retry can still be needed)
+    const int64_t want_b = (int64_t)hc->nblocks, want_v = (int64_t)hc->nvox;
     SVX_TRY(launch_cleanup(m, s));
     SVX_CUDA(cudaStreamSynchronize(s));
-    m->nblocks = (int64_t)std::min<unsigned long long>(hc->nblocks, (unsigned long long)m->bcap);
-    m->nvox = (int64_t)std::min<unsigned long long>(hc->nvox, (unsigned long long)m->vcap);
+    m->nblocks = std::min<int64_t>(want_b, m->bcap);
+    m->nvox = std::min<int64_t>(want_v, m->vcap);
     m->ord_nblocks = std::min<int64_t>(m->ord_nblocks, nblocks0);
     m->ctr_clean = false;   // live counts may have been clamped to the pools
-    m->new_leaves_cap = std::max<int64_t>(2 * m->new_leaves_cap, m->bcap);
-    SVX_TRY(reserve_voxels(m, 2 * m->vcap, s));
+    m->new_leaves_cap = std::max<int64_t>(m->new_leaves_cap, 2 * (want_b - nblocks0) + 4096);
+    if (want_b >= m->bcap) SVX_TRY(reserve_blocks(m, want_b + want_b / 2 + 4096, s));
+    if (want_v >= m->vcap) SVX_TRY(reserve_voxels(m, want_v + want_v / 2 + 65536, s));
     return SVX_OK;
 }
 

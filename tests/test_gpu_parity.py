@@ -360,6 +360,12 @@ def test_capacity_retries_vs_oracle(mode):
     assert np.array_equal(c, oc)
     assert np.array_equal(d, od) and np.array_equal(w, ow)
     assert np.array_equal(s0, os0)
+    # retries grow the pools to the frame's measured demand, not by repeated
+    # doubling (a city frame once asked for 49 GB of slots this way)
+    st = m.engine_stats()
+    rows = 64 * 1024 * 24 + 4096
+    assert st["block_capacity"] <= 8 * st["leaf_count"] + 65536
+    assert st["voxel_capacity"] <= 4 * (st["active_voxels"] + rows) + 65536
 
 
 def test_update_mode_argument():
