@@ -168,6 +168,10 @@ def read_block(buf: memoryview, pos: int):
         raise FormatError(f"unknown dtype code {params[-1]}")
     (nl,) = struct.unpack_from("<Q", buf, pos)
     pos += 8
+    if nl > (len(buf) - pos) // (12 + 8 * MASK_WORDS):
+        raise FormatError(f"leaf count {nl} exceeds the rest of the file")
+    if kind != KIND_TSDF and not 1 <= params[0] <= (1 << 20):
+        raise FormatError(f"payload width {params[0]} out of range")
     block = GridBlock(kind, voxel_size, params, None, None, None, [])
     dt = block.dtype()
     width = block.width()

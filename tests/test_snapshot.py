@@ -319,3 +319,59 @@ def test_grids_equal_and_path_objects(tmp_path):
     m2 = mapper_for(g)
     replay_mapper(dict(g, n_frames=1), m2)
     assert not grids_equal(tsdf, m2.grids[0])
+
+
+def test_parser_rejects_corruption_cleanly():
+    """Truncations and byte flips of a reference snapshot either parse or
+    raise FormatError -- never another exception (the parser validates every
+    length and count before using it)."""
+    from paper_2512_12945_b200 import FormatError, snapshot
+
+    raw = snap_bytes("closed_plane")
+    rng = np.random.default_rng(11)
+    cuts = sorted(set(rng.integers(0, len(raw), 60).tolist()) | {1, 3, 4, 8, 20, 40})
+    for cut in cuts:
+        try:
+            snapshot.parse(raw[:cut])
+        except FormatError:
+            pass
+    for _ in range(150):
+        b = bytearray(raw)
+        for pos in rng.integers(0, 200, 3):      # header, parameters, first leaves
+            b[pos] = int(rng.integers(0, 256))
+        try:
+            snapshot.parse(bytes(b))
+        except FormatError:
+            pass
+
+
+@pytest.mark.gpu
+def test_device_import_rejects_bad_arrays():
+    """svx_import validates what it is given (C-ABI callers need not come
+    through the parser): a repeated slot, a leaf index out of range or a
+    repeated leaf fails with FormatError and leaves the map empty and usable."""
+    from types import SimpleNamespace
+
+    from paper_2512_12945_b200 import FormatError, Mapper
+
+    g = load_golden("api_closed_plane")
+
+    def block(lc, vl, vs):
+        n = len(vs)
+        return SimpleNamespace(leaf_coords=np.array(lc, np.int32).reshape(-1, 3),
+                               voxel_leaf=np.array(vl, np.int32), voxel_slot=np.array(vs, np.int32),
+                               active_count=n, fields=[np.zeros(n), np.ones(n)])
+
+    bad = [block([[0, 0, 0]], [0, 0], [5, 5]),                   # repeated slot
+           block([[0, 0, 0]], [0, 1], [5, 6]),                   # leaf index out of range
+           block([[0, 0, 0], [0, 0, 0]], [0, 1], [5, 6]),        # repeated leaf
+           block([[1 << 28, 0, 0]], [0], [5])]                   # beyond +/-2^30 voxels
+    for b in bad:
+        m = Mapper(**{k: v for k, v in g["mapper_kw"].items() if k != "num_classes"})
+        with pytest.raises(FormatError):
+            m._import_blocks(b, None)
+        assert m.active_count() == 0
+        replay_mapper(dict(g, labels_0=None, labels_1=None, labels_2=None, labels_3=None), m)
+        ref = Mapper(**{k: v for k, v in g["mapper_kw"].items() if k != "num_classes"})
+        replay_mapper(dict(g, labels_0=None, labels_1=None, labels_2=None, labels_3=None), ref)
+        assert m.grids[0].content_hash() == ref.grids[0].content_hash()
