@@ -35,7 +35,10 @@ struct RenderArgs {
     const unsigned long long* bslot;
     const TD* vt;
     double h, trunc;
+    int* err;   // set when a ray exceeds kMarchMaxSteps (absurd far planes)
 };
+
+constexpr long long kMarchMaxSteps = 1LL << 22;   // 2^22 half-voxel steps or leaf jumps per ray
 
 __device__ __forceinline__ long long floor_ll(double v) { return (long long)floor(v); }
 
@@ -94,7 +97,12 @@ __device__ bool march(const RenderArgs<TD>& a, const Ray& r, double near, double
     bool prev_ok = false;
     double t0 = 0.0, d0 = 0.0, t1 = 0.0, d1 = 0.0;
     bool hit = false;
+    long long steps = 0;
     while (true) {
+        if (++steps > kMarchMaxSteps) {   // a guard, not the reference's semantics
+            if (a.err) atomicOr(a.err, 1);
+            return false;
+        }
         double p[3];
         ray_point(r, t, p);
         const long long vx = floor_ll(p[0] / h), vy = floor_ll(p[1] / h), vz = floor_ll(p[2] / h);
@@ -271,7 +279,7 @@ __global__ void k_sample_points(RenderArgs<TD> a, int64_t n, const double* __res
 template <class TD>
 RenderArgs<TD> render_args(svx_map* m) {
     return RenderArgs<TD>{ptr<int4>(m->hash), m->hcap - 1, ptr<unsigned long long>(m->bslot),
-                          ptr<TD>(m->vt), m->cfg.voxel_size, m->cfg.truncation};
+                          ptr<TD>(m->vt), m->cfg.voxel_size, m->cfg.truncation, nullptr};
 }
 
 template <class TD, class TS>
@@ -294,9 +302,18 @@ svx_status render_t(svx_map* m, const svx_render_camera& cam, int mode, const in
     const int64_t npx = (int64_t)cam.width * cam.height;
     const int T = 128;
     const int G = (int)std::min<int64_t>((npx + T - 1) / T, 148 * 16);
-    k_render<TD, TS><<<G, T, 0, s>>>(render_args<TD>(m), c, mode, m->cfg.sem_kind, m->payload_d,
-                                     ptr<TS>(m->s0), vlab, pal, npal, out);
+    RenderArgs<TD> ra = render_args<TD>(m);
+    SVX_CUDA(cudaMallocAsync(&ra.err, sizeof(int), s));
+    SVX_CUDA(cudaMemsetAsync(ra.err, 0, sizeof(int), s));
+    k_render<TD, TS><<<G, T, 0, s>>>(ra, c, mode, m->cfg.sem_kind, m->payload_d, ptr<TS>(m->s0), vlab, pal,
+                                     npal, out);
     SVX_LAUNCHED();
+    int herr = 0;
+    cudaError_t e = cudaMemcpyAsync(&herr, ra.err, sizeof(int), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaFreeAsync(ra.err, s);
+    if (e != cudaSuccess) return fail(SVX_E_CUDA, std::string("render: ") + cudaGetErrorString(e));
+    if (herr) return fail(SVX_E_INPUT, "render: a ray exceeded 2^22 march steps (far plane too far)");
     return SVX_OK;
 }
 

@@ -248,3 +248,16 @@ def test_compact_f32_map_queries_vs_oracle(tmp_path):
     c2, d2, w2, s2, _ = m2._export()
     assert np.array_equal(c2, coords) and np.array_equal(d2, d) and np.array_equal(w2, w)
     assert np.array_equal(s2, s0)
+
+
+@pytest.mark.gpu
+def test_absurd_far_plane_is_an_error_not_a_hang():
+    from paper_2512_12945_b200 import Mapper, RenderCamera, UserInputError
+
+    m = Mapper(voxel_size=0.05, truncation=0.15)
+    cam = RenderCamera(pose=np.eye(4), fx=8.0, fy=8.0, cx=4.0, cy=3.0, width=8, height=6,
+                       near=0.05, far=1e12)
+    with pytest.raises(UserInputError, match="march steps"):
+        m.render(cam)
+    cam.far = 50.0
+    assert not m.render(cam).any()
