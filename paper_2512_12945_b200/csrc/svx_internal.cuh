@@ -149,6 +149,10 @@ struct FrameCtr {
     int err_slots;                  // slot mode: a voxel got more than kSlots rows (re-run in segment mode)
     unsigned epi_done;              // CTAs of the last kernel finished (frame_epilogue)
     unsigned pad_;
+    unsigned long long work_long;   // K5 long / open: next listed voxel to take (dynamic scheduling)
+    unsigned long long work_open;
+    unsigned long long work_huge;   // K5h: next huge voxel; K5g: next (voxel, slice) item
+    unsigned long long work_items;
 };
 
 // Per-voxel frame record (indexed by voxel id; cnt and cur are zero between

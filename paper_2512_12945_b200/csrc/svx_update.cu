@@ -30,6 +30,9 @@ namespace {
 
 constexpr int kSmemMax = 1024;                   // rows per warp buffer (4 KB)
 constexpr int kWarpsPerCta = 8;
+#ifndef SVX_DYN_LONG
+#define SVX_DYN_LONG 1   // K5 long / open: warps take voxels from a frame counter
+#endif
 constexpr int kHugeWarps = 296;                  // bitmap scratch slots (huge segments)
 
 // counter += 1 for every converged lane, one atomic per warp; returns this
@@ -729,7 +732,16 @@ __device__ __forceinline__ void k_update_long_body(UpdateArgs a, TD* vt,
     const long long gw = (long long)blockIdx.x * kWarpsPerCta + wib;
     const long long nwarps = (long long)gridDim.x * kWarpsPerCta;
     const long long L = (long long)cv->n_long;
+#if SVX_DYN_LONG
+    // voxels cost from 17 to 1024 rows: warps take the next one from a frame
+    // counter instead of a fixed stride, so no warp idles while others work
+    for (long long t = 0;;) {
+        if (lane == 0) t = (long long)atomicAdd(&ctr->work_long, 1ULL);
+        t = __shfl_sync(0xffffffffu, t, 0);
+        if (t >= L) break;
+#else
     for (long long t = gw; t < L; t += nwarps) {
+#endif
         const int vid = a.mlist[a.longlist[t]];
         const unsigned c = a.rec[vid].cnt;
         const unsigned k = c & ~kNewBit;
@@ -973,8 +985,15 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) k_update_open(UpdateArgs a,
     const KeyPack kp = cv->p.kp;
     const PoseParams pp = cv->p.pp;
     const Fe* feats = (const Fe*)cv->p.feats;
+#if SVX_DYN_LONG
+    for (long long e = 0;;) {
+        if (lane == 0) e = (long long)atomicAdd(&ctr->work_open, 1ULL);
+        e = __shfl_sync(0xffffffffu, e, 0);
+        if (e >= L) break;
+#else
     for (long long e = (long long)blockIdx.x * kWarpsPerCta + wib; e < L;
          e += (long long)gridDim.x * kWarpsPerCta) {
+#endif
         const int vid = a.mlist[e];
         const unsigned c = a.rec[vid].cnt;
         if ((c & ~kNewBit) > (unsigned)kOpenCtaMin) {   // one CTA per voxel (k_update_open_huge)
@@ -1070,7 +1089,17 @@ __device__ __forceinline__ void k_update_open_huge_body(UpdateArgs a, TD* vt, TS
     const PoseParams pp = cv->p.pp;
     const Fe* feats = (const Fe*)cv->p.feats;
     const int D = a.D;
+#if SVX_DYN_LONG
+    __shared__ long long s_next;
+    for (;;) {
+        __syncthreads();   // every thread has read the previous ticket
+        if (tid == 0) s_next = (long long)atomicAdd(&ctr->work_huge, 1ULL);
+        __syncthreads();
+        const long long t = s_next;
+        if (t >= Hn) break;
+#else
     for (long long t = blockIdx.x; t < Hn; t += gridDim.x) {
+#endif
         const int vid = a.mlist[a.hugelist[t]];
         const unsigned c = a.rec[vid].cnt;
         const unsigned k = c & ~kNewBit;
@@ -1352,7 +1381,17 @@ __global__ void __launch_bounds__(kHugeThreads, 1) k_huge_items(UpdateArgs a, TD
     const Fe* feats = (const Fe*)cv->p.feats;
     // items: per giant voxel S feature slices and one TSDF item
     const long long items = Hn * (S + 1);
+#if SVX_DYN_LONG
+    __shared__ long long s_next;
+    for (;;) {
+        __syncthreads();   // every thread has read the previous ticket
+        if (tid == 0) s_next = (long long)atomicAdd(&ctr->work_items, 1ULL);
+        __syncthreads();
+        const long long it = s_next;
+        if (it >= items) break;
+#else
     for (long long it = blockIdx.x; it < items; it += gridDim.x) {
+#endif
         const long long t = it / (S + 1);
         const int sl = (int)(it % (S + 1));
         const HugeInfo hi = hinfo[t];
