@@ -430,9 +430,12 @@ def _lidar_workload(name, scene, rows, cols, fov, max_range, n_frames, step, hei
     return Workload(name, n_frames, rows * cols, mapper_kwargs, make_frame)
 
 
-def workload(cfg: int, device="cpu", seed=None, scale_frames=None, small=False) -> Workload:
+def workload(cfg: int, device="cpu", seed=None, scale_frames=None, small=False,
+             dim=None) -> Workload:
     """BASELINE.json configs[cfg-1] (1-based cfg).  `small` shrinks sensors
-    for CPU tests (same geometry and value distributions)."""
+    for CPU tests (same geometry and value distributions); `dim` overrides the
+    open-set embedding dimension (small sensors with the BASELINE D = 512 /
+    768 for reference-generated fixtures)."""
     if cfg == 1:
         s = 1 if seed is None else seed
         scene = room_scene(s, device=device)
@@ -452,7 +455,7 @@ def workload(cfg: int, device="cpu", seed=None, scale_frames=None, small=False) 
         s = 3 if seed is None else seed
         scene = room_scene(s, size=(8.0, 8.0, 3.0), n_boxes=8, n_spheres=4, device=device)
         w, h, f = (64, 48, 52.5) if small else (640, 480, 525.0)
-        dim = 32 if small else 512
+        dim = dim or (32 if small else 512)
         return _camera_workload("cfg3_open_room_640x480_D512", scene, w, h, f, 50, 2.0, 1.2, 0.01,
                                 s, dict(voxel_size=0.04, truncation=0.12, max_range=15.0,
                                         feature_dim=dim), "open", device, dim=dim, n_queries=32)
@@ -468,7 +471,7 @@ def workload(cfg: int, device="cpu", seed=None, scale_frames=None, small=False) 
         s = 5 if seed is None else seed
         scene = floor_scene(s, device=device)
         w, h, f = (64, 36, 45.0) if small else (1280, 720, 900.0)
-        dim = 32 if small else 768
+        dim = dim or (32 if small else 768)
         return _camera_workload("cfg5_open_floor_1280x720_D768", scene, w, h, f, 300, 6.0, 1.4,
                                 0.01, s, dict(voxel_size=0.03, truncation=0.09, max_range=30.0,
                                               feature_dim=dim), "open", device, dim=dim,

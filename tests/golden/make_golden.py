@@ -55,7 +55,13 @@ def _reports_array(reps):
                      for r in reps], np.int64)
 
 
-def _dump_state(out, tsdf, sem, sem_kind, queries=None, tau=0.01, tp=0.1):
+def _sha(a):
+    import hashlib
+
+    return np.array(hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest())
+
+
+def _dump_state(out, tsdf, sem, sem_kind, queries=None, tau=0.01, tp=0.1, digest=False):
     coords, (d, w) = tsdf.active_values()
     out["coords"] = np.asarray(coords, np.int64)
     out["d"] = d
@@ -71,7 +77,11 @@ def _dump_state(out, tsdf, sem, sem_kind, queries=None, tau=0.01, tp=0.1):
         out["label_map"] = label_map(sem)[1].astype(np.int32)
         out["grid_labels"] = grid_labels(sem)[1]
     else:
-        out["mean"], out["beta"] = svals
+        if digest:   # large D: SHA-256 of the exact arrays + the first rows for diagnostics
+            out["mean_sha256"], out["beta_sha256"] = _sha(svals[0]), _sha(svals[1])
+            out["mean_head"], out["beta_head"] = svals[0][:32], svals[1][:32]
+        else:
+            out["mean"], out["beta"] = svals
         if queries is not None:
             out["queries"] = queries
             out["cosine_q0"] = cosine_to_embeddings(svals[0], queries[:1])[:, 0]
@@ -80,8 +90,13 @@ def _dump_state(out, tsdf, sem, sem_kind, queries=None, tau=0.01, tp=0.1):
             out["classify_best"] = best
 
 
-def api_scenario(name, frames, mapper_kw, queries=None):
-    """frames: list of (points_sensor, pose, labels|None, feats|None)."""
+def api_scenario(name, frames, mapper_kw, queries=None, feat_store=None):
+    """frames: list of (points_sensor, pose, labels|None, feats|None).
+    feat_store: None (features stored as given), "f16" (the features are
+    exactly float16-representable and stored as float16), or ("basis", B,
+    idx_list) (each frame's features are rows B[idx]; only B and idx are
+    stored) -- keeps the large-D fixtures small; the loader rebuilds the
+    exact float32 inputs (tests/helpers.py load_golden)."""
     m = sb.Mapper(**mapper_kw)
     reps = []
     for pts, pose, lab, feat in frames:
@@ -95,10 +110,20 @@ def api_scenario(name, frames, mapper_kw, queries=None):
         if lab is not None:
             out[f"labels_{i}"] = lab
         if feat is not None:
-            out[f"features_{i}"] = feat
+            if feat_store == "f16":
+                f16 = feat.astype(np.float16)
+                assert np.array_equal(f16.astype(feat.dtype), feat)
+                out[f"features16_{i}"] = f16
+            elif isinstance(feat_store, tuple):
+                basis, idxs = feat_store[1], feat_store[2]
+                assert np.array_equal(basis[idxs[i]], feat)
+                out["featbasis"] = basis
+                out[f"featidx_{i}"] = idxs[i]
+            else:
+                out[f"features_{i}"] = feat
     out["n_frames"] = np.array(len(frames))
     out["mapper_kw"] = np.array(repr(mapper_kw))
-    _dump_state(out, tsdf, sem, kind, queries)
+    _dump_state(out, tsdf, sem, kind, queries, digest=feat_store is not None)
     np.savez_compressed(os.path.join(HERE, name + ".npz"), **out)
     print(name, "frames", len(frames), "active", out["coords"].shape[0])
 
@@ -180,7 +205,7 @@ def seam_scenario(name, frames, mapper_kw, queries=None):
     out["reports"] = _reports_array(reps)
     out["n_frames"] = np.array(len(frames))
     out["mapper_kw"] = np.array(repr(mapper_kw))
-    _dump_state(out, tsdf, sem, kind, queries)
+    _dump_state(out, tsdf, sem, kind, queries, digest=feat_store is not None)
     np.savez_compressed(os.path.join(HERE, name + ".npz"), **out)
     print(name, "frames", len(frames), "active", out["coords"].shape[0])
 
@@ -551,8 +576,49 @@ def _save_gz(mapper, stem):
     print(path, len(raw), "bytes,", os.path.getsize(path), "compressed")
 
 
+def main_bigdim():
+    """Open-set fixtures at the BASELINE embedding dims (cfg3 D = 512 with its
+    32 queries, cfg5 D = 768 with its 128 queries) and a close wall at D = 768
+    whose band voxels collect > 8192 rows each (the engine's dimension-sliced
+    huge-voxel path, 24 slices of 32 dims)."""
+    from paper_2512_12945_b200 import scenes
+
+    for cfg, stem, step in ((3, "api_open_room_d512", 6), (5, "api_open_floor_d768", 6)):
+        wl = scenes.workload(cfg, small=True, dim=512 if cfg == 3 else 768)
+        fr = []
+        for i in range(2):
+            f = wl.make_frame(i * 3)
+            feats = f.features.numpy()[::step].astype(np.float16).astype(np.float32)
+            fr.append((np.ascontiguousarray(f.points.numpy()[::step]), f.pose, None,
+                       np.ascontiguousarray(feats)))
+        api_scenario(stem, fr, wl.mapper_kwargs, queries=np.ascontiguousarray(wl.queries.numpy()),
+                     feat_store="f16")
+    rng = np.random.default_rng(768)
+    D = 768
+    basis = rng.normal(size=(8, D)).astype(np.float32)
+    fr, idxs = [], []
+    for f in range(2):
+        n = 9000 + 1500 * f
+        pts = np.column_stack([1.0 + rng.normal(0.0, 0.002, n), rng.uniform(-0.012, 0.012, n),
+                               rng.uniform(-0.012, 0.012, n)])
+        pose = np.eye(4)
+        pose[:3, 3] = [0.015 + 0.002 * f, 0.015, 0.015]
+        idx = rng.integers(0, 8, n).astype(np.uint8)
+        idxs.append(idx)
+        fr.append((pts, pose, None, basis[idx]))
+    q = rng.normal(size=(128, D))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    api_scenario("api_open_wall_d768", fr, dict(voxel_size=0.03, truncation=0.09, feature_dim=D,
+                                                max_range=5.0),
+                 queries=q, feat_store=("basis", basis, idxs))
+
+
 def main():
     from paper_2512_12945_b200 import scenes
+
+    if "bigdim" in sys.argv[1:]:
+        main_bigdim()
+        return
 
     if "depth" in sys.argv[1:]:   # only the depth scenarios
         main_depth()
@@ -613,6 +679,7 @@ def main():
         fr.append((f.points_world.numpy(), f.origin, f.labels.numpy(), None))
     seam_scenario("seam_closed_city_small", fr, wl.mapper_kwargs)
     main_rotated()
+    main_bigdim()
     main_snapshot()
     main_mesh()
     main_render()

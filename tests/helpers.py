@@ -39,6 +39,11 @@ def load_golden(name):
     g["mapper_kw"] = ast.literal_eval(str(g["mapper_kw"]))
     g["mode"] = str(g["mode"])
     g["n_frames"] = int(g["n_frames"])
+    for i in range(g["n_frames"]):   # compact feature storage (make_golden.api_scenario)
+        if f"features16_{i}" in g:
+            g[f"features_{i}"] = g.pop(f"features16_{i}").astype(np.float32)
+        elif f"featidx_{i}" in g:
+            g[f"features_{i}"] = g["featbasis"][g.pop(f"featidx_{i}")]
     return g
 
 
@@ -104,6 +109,18 @@ def report_rows(reps):
         get = (lambda k: getattr(r, k))
         out.append([int(get(k)) for k in REPORT_KEYS])
     return np.array(out, np.int64)
+
+
+def open_state_matches(g, mean, beta):
+    """Open-set state vs a fixture: exact arrays, or (large-D fixtures) the
+    SHA-256 of the exact float32 arrays in active order."""
+    import hashlib
+
+    if "mean" in g:
+        return np.array_equal(mean, g["mean"]) and np.array_equal(beta, g["beta"])
+    sha = lambda a: hashlib.sha256(np.ascontiguousarray(a, np.float32).tobytes()).hexdigest()
+    ok_head = (np.array_equal(mean[:32], g["mean_head"]) and np.array_equal(beta[:32], g["beta_head"]))
+    return ok_head and sha(mean) == str(g["mean_sha256"]) and sha(beta) == str(g["beta_sha256"])
 
 
 def assert_close_rel(a, b, rtol=RTOL, atol=0.0, what=""):

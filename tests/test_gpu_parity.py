@@ -11,8 +11,8 @@ against the oracle's fp32 mode and within tolerance of the reference.
 import numpy as np
 import pytest
 
-from helpers import (RTOL, assert_close_rel, golden_names, load_golden, oracle_for,
-                     replay_mapper, replay_oracle, report_rows)
+from helpers import (RTOL, assert_close_rel, golden_names, load_golden, open_state_matches,
+                     oracle_for, replay_mapper, replay_oracle, report_rows)
 
 pytestmark = pytest.mark.gpu
 NAMES = golden_names()
@@ -46,7 +46,7 @@ def test_engine_matches_reference_fixture(name, device_inputs):
             assert np.array_equal(m.label_map()[1], g["label_map"])
             assert np.array_equal(m.label_map(zero_if_empty=True)[1], g["grid_labels"])
         else:
-            assert np.array_equal(vals[0], g["mean"]) and np.array_equal(vals[1], g["beta"])
+            assert open_state_matches(g, vals[0], vals[1])
     if "queries" in g:
         q = g["queries"]
         qc, sims = m.query(q[0])
@@ -92,6 +92,8 @@ def test_compact_tsdf_vs_oracle_and_reference(name):
     if "mean" in g:
         assert_close_rel(s0, g["mean"], atol=1e-7, what="mean")
         assert_close_rel(s1, g["beta"], what="beta")
+    elif "mean_sha256" in g:   # large-D fixture: exact vs the fp32-TSDF oracle
+        assert np.array_equal(s0, os0) and np.array_equal(s1, os1)
 
 
 def test_probe_and_background():
@@ -164,29 +166,34 @@ def test_random_world_frames_vs_oracle(carving, wfn):
     assert np.array_equal(s0, os0)
 
 
+# Frames per config: cfg3 frame 6 faces a wall at close range (about 200
+# band voxels collecting ~10^4 rows each), which takes the open-set update's
+# dimension-sliced giant-voxel kernels (k_huge_prep / k_huge_items, 16 slices
+# of 32 dims at D = 512); the other frames take the per-voxel kernels.
+WORKLOAD_FRAMES = {1: (0, 3), 2: (0, 3), 3: (0, 6), 4: (0, 3), 5: (0, 3)}
+
+
 @pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
 def test_workload_frames_vs_oracle(cfg):
-    """Full-resolution BASELINE frames (2 per config; open-set dims cut to 64
-    to keep the oracle fast) through integrate_world, bit-exact vs the oracle."""
+    """Full-resolution BASELINE frames at the BASELINE dims (C = 20/40,
+    D = 512/768) through integrate_world, bit-exact vs the oracle; for the
+    open-set configs also classify_means against the config's own queries
+    (cfg3: k = 32 at D = 512; cfg5: k = 128 at D = 768): labels exact, best
+    within 1e-12 relative (only the dot products' summation order differs)."""
     from paper_2512_12945_b200 import Mapper, scenes
     from oracle.oracle import OracleMap
 
     wl = scenes.workload(cfg, device="cuda")
     kw = dict(wl.mapper_kwargs)
-    dim = None
-    if "feature_dim" in kw:
-        dim = 64
-        kw["feature_dim"] = dim
     m = Mapper(**kw)
     om = OracleMap(**kw)
-    for i in range(2):
-        f = wl.make_frame(i * 3)
+    for i in WORKLOAD_FRAMES[cfg]:
+        f = wl.make_frame(i)
         pw = f.points_world
-        feats = f.features[:, :dim].contiguous() if dim else None
-        r1 = m.integrate_world(pw, f.origin, labels=f.labels, features=feats)
+        r1 = m.integrate_world(pw, f.origin, labels=f.labels, features=f.features)
         r2 = om.integrate_world(pw.cpu().numpy(), f.origin,
                                 labels=f.labels.cpu().numpy() if f.labels is not None else None,
-                                features=feats.cpu().numpy() if feats is not None else None)
+                                features=f.features.cpu().numpy() if f.features is not None else None)
         assert np.array_equal(report_rows([r1]), report_rows([r2]))
     c, d, w, s0, s1 = m._export()
     oc, od, ow, os0, os1 = om.export()
@@ -195,6 +202,14 @@ def test_workload_frames_vs_oracle(cfg):
     assert np.array_equal(s0, os0)
     if s1 is not None:
         assert np.array_equal(s1, os1)
+    if wl.queries is not None:
+        q = wl.queries.cpu().numpy()
+        assert q.shape == ((32, 512) if cfg == 3 else (128, 768))
+        lab, best = m.classify(q)
+        olab, obest = om.classify(q)
+        assert lab.shape[0] == c.shape[0] > 100000
+        assert np.array_equal(lab, olab)
+        np.testing.assert_allclose(best, obest, rtol=1e-12, atol=1e-300)
 
 
 @pytest.mark.parametrize("variant", ["bayes", "last_wins_dropoff", "geometry"])
@@ -488,21 +503,21 @@ class TestErrors:
 
 
 @pytest.mark.parametrize("feat_dtype", ["float32", "float64"])
-@pytest.mark.parametrize("D", [40, 96])
+@pytest.mark.parametrize("D", [40, 96, 512, 768])
 def test_open_huge_voxels_vs_oracle(D, feat_dtype):
     """Open-set voxels with thousands of rows (every ray of a frame crosses
     the same few band voxels, like a depth camera facing a close wall): the
     dimension-sliced huge-voxel kernels (k_huge_prep / k_huge_items) against
     the oracle's sequential point-ordered sums, bit for bit; D not a
-    multiple of the 32-dimension slice, f32 and f64 features."""
+    multiple of the 32-dimension slice, the BASELINE D = 512 / 768 (16 / 24
+    slices), f32 and f64 features."""
     from oracle.oracle import OracleMap
     from paper_2512_12945_b200 import Mapper
 
     rng = np.random.default_rng(D)
     kw = dict(voxel_size=0.05, truncation=0.15, feature_dim=D, max_range=5.0)
     m, om = Mapper(**kw), OracleMap(**kw)
-    for f in range(3):
-        n = 6000 + 2000 * f
+    for f, n in enumerate((6000, 8000, 10000, 30000)):
         pts = np.column_stack([1.0 + rng.normal(0.0, 0.003, n), rng.uniform(-0.03, 0.03, n),
                                rng.uniform(-0.03, 0.03, n)])
         origin = np.array([0.01 * f, 0.005 * f, -0.004 * f])
@@ -510,6 +525,10 @@ def test_open_huge_voxels_vs_oracle(D, feat_dtype):
         r1 = m.integrate_world(pts + origin, origin, features=feats)
         r2 = om.integrate_world(pts + origin, origin, features=feats)
         assert r1.touched_voxels == r2.touched_voxels and r1.band_hits == r2.band_hits
+        if n == 30000:   # this frame alone gives some voxels > 8192 rows (giant path)
+            one = OracleMap(voxel_size=0.05, truncation=0.15, max_range=5.0)
+            one.integrate_world(pts + origin, origin)
+            assert one.export()[2].max() > 8192
     assert m.engine_stats()["active_voxels"] < 200    # few voxels, thousands of rows each
     c1, d1, w1, m1, b1 = m._export()
     c2, d2, w2, m2, b2 = om.export()
