@@ -177,8 +177,10 @@ def stage_bytes(stage, rep, kind, C, D, tsdf_elem, slots=False):
         "seg": U * 8,
         # per row: voxel id + count in; single-row voxels also ray + label + state
         "scatter": R * (4 + 4 + 4) + U * (32 + 2 * S),
-        # multi-row voxels: rows, rays, labels and state (upper bound: all voxels)
-        "update": 2 * U * S + R * (4 + 32 + (4 if kind == "closed" else 0)),
+        # multi-row voxels: rows, rays, labels or feature rows, and state
+        # (upper bound: all voxels); open-set: each row reads its point's
+        # feature vector (4D bytes) once
+        "update": 2 * U * S + R * (4 + 32 + (4 if kind == "closed" else 0)) + R * (4 * D if kind == "open" else 0),
         "update_b": 0,
     }[stage]
 
@@ -204,12 +206,45 @@ def ncu_traffic(stage):
 
 # -- workloads -----------------------------------------------------------------------
 
-def make_frames(cfg, count, device, start=0):
-    from paper_2512_12945_b200 import scenes
+def load_scenes():
+    """paper_2512_12945_b200/scenes.py as a standalone module: it needs only
+    numpy and torch, and importing it this way does not import the package
+    (whose __init__ loads libsvx.so) -- the reference arm must not map the
+    engine's library."""
+    import importlib.util
 
+    name = "_svx_bench_scenes"
+    if name in sys.modules:
+        return sys.modules[name]
+    path = os.path.join(REPO, "paper_2512_12945_b200", "scenes.py")
+    spec = importlib.util.spec_from_file_location(name, path)
+    mod = importlib.util.module_from_spec(spec)
+    sys.modules[name] = mod
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def make_frames(cfg, count, device, start=0):
+    scenes = load_scenes()
     wl = scenes.workload(cfg, device=device)
     frames = [wl.make_frame((start + i) % wl.n_frames) for i in range(count)]
     return wl, frames
+
+
+def config_dict(args, wl, world):
+    """The workload description, identical in both arms (the driver compares
+    them); how each arm runs it goes in top-level keys."""
+    kw = wl.mapper_kwargs
+    return {
+        "workload": wl.name, "points_per_frame": wl.points_per_frame,
+        "voxel_size": kw["voxel_size"], "truncation": kw["truncation"],
+        "max_range": kw.get("max_range"),
+        "num_classes": kw.get("num_classes") or None, "feature_dim": kw.get("feature_dim") or None,
+        "tsdf_dtype": args.tsdf_dtype,
+        "input": "depth rasters" if args.depth else "point clouds",
+        "parallelism": f"leaf-shard{world}" if world > 1 else "single",
+        "frames_timed": f"{args.warmup}..{args.warmup + args.steps - 1}",
+    }
 
 
 def sem_kind_of(kw):
@@ -355,7 +390,6 @@ def run_ours(args):
         # segment mode: the byte model covers both update kernels together
         # (K5 short/long or open, then K5b long / huge), so they are timed together
         dom, dom_ms = "update", mean_stage["update"] + mean_stage["update_b"]
-        traffic_key = None   # (ncu_traffic.json holds the slot-mode kernels)
     dom_bytes = statistics.mean(stage_bytes(dom, r, kind, C, D, tsdf_elem, slots) for r in prof_reps)
     peak, peak_src = measured_peak()
     achieved = dom_bytes / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else 0.0
@@ -390,7 +424,7 @@ def run_ours(args):
         m2.reserve(st["active_voxels"] + 2 * per_frame * K,
                    st["leaf_count"] * (1 + 2 * K // max(W, 1)))
         dstream = torch.cuda.default_stream()
-        e_ms, e_used, h2d = 0.0, 0, 0
+        e_ms, e_used, h2d, d2h = 0.0, 0, 0, 0
         if world > 1:
             torch.distributed.barrier()
         torch.cuda.synchronize()
@@ -401,16 +435,18 @@ def run_ours(args):
             b = torch.cuda.Event(enable_timing=True)
             a.record(dstream)
             r = integrate(m2, frames[W + i], host[W + i])
+            e_used += r.points_used   # the frame's report, read back from the device
             b.record(dstream)
             b.synchronize()
             e_ms += a.elapsed_time(b)
-            e_used += r.points_used
-            h2d += sum(x.nbytes for x in host[W + i] if x is not None)
+            io = m2.engine_stats() if not sharded else None   # bytes the library moved
+            h2d += io["last_h2d_bytes"] if io else sum(x.nbytes for x in host[W + i] if x is not None)
+            d2h += io["last_d2h_bytes"] if io else 0
         te = torch.tensor([e_ms], dtype=torch.float64, device=dev)
         if world > 1:
             torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
         e2e = {"value": e_used / (float(te.item()) / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": int(h2d // K), "d2h_bytes_per_step": 136,
+               "h2d_bytes_per_step": int(h2d // K), "d2h_bytes_per_step": int(d2h // K),
                "ms_per_step": float(te.item()) / K}
         del m2
 
@@ -431,20 +467,13 @@ def run_ours(args):
             "warmup": W, "ms_per_step": total_ms_max / K, "higher_is_better": True,
             "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {
-                "workload": wl.name, "points_per_frame": wl.points_per_frame,
-                "voxel_size": kw["voxel_size"], "truncation": kw["truncation"],
-                "num_classes": C or None, "feature_dim": D or None,
-                "tsdf_dtype": args.tsdf_dtype,
-                "api": ("ShardedMapper.integrate -> svx_shard_{march,plan,pack,apply} + NCCL "
-                        "all-to-all" if sharded else
-                        ("Mapper.integrate_depth -> svx_integrate_depth (depth rasters, "
-                         "back-projection on the GPU)" if args.depth else
-                         "Mapper.integrate -> svx_integrate")),
-                "parallelism": f"leaf-shard{world}" if sharded else "single",
-                "l2": "flushed between steps (256 MiB write + 256 MiB read, outside step events)",
-                "frames_timed": f"{W}..{W + K - 1}",
-            },
+            "config": config_dict(args, wl, world),
+            "api": ("ShardedMapper.integrate -> svx_shard_{march,plan,pack,apply} + NCCL "
+                    "all-to-all" if sharded else
+                    ("Mapper.integrate_depth -> svx_integrate_depth (depth rasters, "
+                     "back-projection on the GPU)" if args.depth else
+                     "Mapper.integrate -> svx_integrate")),
+            "l2": "flushed between steps (256 MiB write + 256 MiB read, outside step events)",
             "ms_per_frame_p50": statistics.median(step_ms),
             "points_used_per_frame": used / K,
             "touched_voxels_per_frame": touched_all / K,
@@ -469,6 +498,11 @@ def run_ours(args):
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }
+        if sharded:
+            import torch.distributed as dist
+
+            line["nccl"] = {"backend": dist.get_backend(), "world_size": dist.get_world_size(),
+                            "version": ".".join(map(str, torch.cuda.nccl.version()))}
         print(json.dumps(line))
     if world > 1:
         torch.distributed.destroy_process_group()
@@ -490,6 +524,62 @@ def load_reference():
     return None, False
 
 
+def _ref_frame_inputs(semvox, args, f, kind, i):
+    """One frame as the reference's own API takes it: a semvox.Frame from the
+    sensor points (or, with --depth, semvox.ingest.project_depth of the depth
+    raster, ingest.py:285-322)."""
+    import numpy as np
+
+    if args.depth:
+        from semvox.config import CameraConfig
+        from semvox.ingest import project_depth
+
+        cam = CameraConfig(**{k: f.camera[k] for k in ("fx", "fy", "cx", "cy", "width", "height",
+                                                        "depth_scale", "stride")})
+        h, w = f.camera["height"], f.camera["width"]
+        pay = (f.labels.cpu().numpy().reshape(h, w) if kind == "closed"
+               else f.features.cpu().numpy().reshape(h, w, -1))
+        return lambda: project_depth(f.depth.cpu().numpy(), pay, cam, pose=f.pose, frame_id=i)
+    pts = f.points.cpu().numpy()
+    lab = f.labels.cpu().numpy() if kind == "closed" else None
+    feat = f.features.cpu().numpy() if kind == "open" else None
+    return lambda: semvox.Frame(points=pts, pose=f.pose, labels=lab, features=feat, frame_id=i)
+
+
+def _ref_run(semvox, native, kw, kind, args, frames, threads, stages=None):
+    """integrate_frame (evalbench.py:409-413) per frame on fresh grids; wall
+    time per frame (Frame construction + integrate_frame, as the reference's
+    own benchmark times it).  `stages`: collect the backend's stage timers."""
+    fusion = semvox.FusionConfig(voxel_size=kw["voxel_size"], truncation=kw["truncation"],
+                                 max_range=kw["max_range"])
+    closed = semvox.ClosedSetConfig(num_classes=kw["num_classes"]) if kind == "closed" else None
+    open_set = semvox.OpenSetConfig(feature_dim=kw["feature_dim"]) if kind == "open" else None
+    tsdf, sem = semvox.make_grids(fusion, closed=closed, open_set=open_set,
+                                  backend="native" if native else "python")
+    be = tsdf.backend
+    orig = be.integrate_points
+    if stages is not None:
+        # pass-through wrapper: keeps the t_*_ms timers integrate_points
+        # returns (_core.pyx:705-857), which IntegrationReport drops
+        def traced(*a, **k):
+            out = orig(*a, **k)
+            stages.append({n: out[n] for n in out if n.startswith("t_")})
+            return out
+
+        be.integrate_points = traced
+    times, used = [], []
+    try:
+        for i, f in enumerate(frames):
+            mk = _ref_frame_inputs(semvox, args, f, kind, i)
+            t0 = time.perf_counter()
+            r = semvox.integrate_frame(tsdf, sem, mk(), fusion, threads=threads)
+            times.append(time.perf_counter() - t0)
+            used.append(r.points_used)
+    finally:
+        be.integrate_points = orig
+    return times, used
+
+
 def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
@@ -503,25 +593,29 @@ def run_reference(args):
     kind = sem_kind_of(kw)
     threads = host_threads()
     semvox, native = load_reference()
-    used, secs = 0, 0.0
+    extra = {}
     if semvox is not None:
-        fusion = semvox.FusionConfig(voxel_size=kw["voxel_size"], truncation=kw["truncation"],
-                                     max_range=kw["max_range"])
-        closed = semvox.ClosedSetConfig(num_classes=kw["num_classes"]) if kind == "closed" else None
-        open_set = semvox.OpenSetConfig(feature_dim=kw["feature_dim"]) if kind == "open" else None
-        tsdf, sem = semvox.make_grids(fusion, closed=closed, open_set=open_set,
-                                      backend="native" if native else "python")
-        for i, f in enumerate(frames):
-            pts = f.points.cpu().numpy()
-            lab = f.labels.cpu().numpy() if kind == "closed" else None
-            feat = f.features.cpu().numpy() if kind == "open" else None
-            t0 = time.perf_counter()
-            fr = semvox.Frame(points=pts, pose=f.pose, labels=lab, features=feat, frame_id=i)
-            r = semvox.integrate_frame(tsdf, sem, fr, fusion, threads=threads)
-            dt = time.perf_counter() - t0
-            if i >= W:
-                secs += dt
-                used += r.points_used
+        stages = []
+        times, used_l = _ref_run(semvox, native, kw, kind, args, frames, threads, stages)
+        secs, used = sum(times[W:]), sum(used_l[W:])
+        # single-thread number and the allocation split
+        n1 = min(len(frames), W + K, 6 if kind == "closed" else 2)
+        t1, u1 = _ref_run(semvox, native, kw, kind, args, frames[:n1], 1)
+        steady1 = t1[1:] if n1 > 1 else t1
+        st_mean = {k: statistics.mean(s[k] for s in stages[W:] if k in s)
+                   for k in (stages[W] if len(stages) > W else {})}
+        extra = {
+            "ms_per_frame_first": times[0] * 1e3,
+            "ms_per_frame_steady": secs * 1e3 / K,
+            "allocation_note": "frame 0 allocates the map's first leaves (allocation-heavy); "
+                               "timed frames are steady state (warm-up frames allocate first)",
+            "stage_ms": {k: round(v, 3) for k, v in st_mean.items()},
+            "stage_ms_source": "integrate_points' own t_*_ms timers (_core.pyx:705-857), "
+                               "mean over the timed frames",
+            "threads_1": {"value": sum(u1[1:] if n1 > 1 else u1) / sum(steady1), "unit": UNIT,
+                          "ms_per_frame": statistics.mean(steady1) * 1e3,
+                          "sample": f"frames 1..{n1 - 1} after frame 0, threads=1"},
+        }
         what = (f"semvox (reference) {'native Cython/C++ OpenMP' if native else 'numpy'} backend "
                 f"from baseline/_ref, integrate_frame per frame, threads={threads}, {cpu_model()}")
         kind_s = "reference"
@@ -529,6 +623,7 @@ def run_reference(args):
         from oracle.oracle import OracleMap
 
         om = OracleMap(**kw, threads=threads)
+        used, secs = 0, 0.0
         for i, f in enumerate(frames):
             t0 = time.perf_counter()
             r = om.integrate(f.points.cpu().numpy(), f.pose,
@@ -542,21 +637,56 @@ def run_reference(args):
         kind_s = "port"
     value = used / secs
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
-        "ms_per_step": secs * 1e3 / K, "higher_is_better": True, "scaling": "weak",
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": max(world, args.gpus),
+        "steps": K, "warmup": W,
+        "ms_per_step": secs * 1e3 / K, "higher_is_better": True,
+        "scaling": "strong" if max(world, args.gpus) > 1 else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-        "config": {"workload": wl.name, "points_per_frame": wl.points_per_frame,
-                   "voxel_size": kw["voxel_size"], "truncation": kw["truncation"],
-                   "frames_timed": f"{W}..{W + K - 1}"},
+        "config": config_dict(args, wl, max(world, args.gpus)),
+        "api": "semvox.Frame + semvox.integrate_frame (reference CPU path)",
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind_s,
                          "sample": what},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    line.update(extra)
     print(json.dumps(line))
+
+
+def spawn_ranks(args):
+    """`bench.py --gpus N` without a torchrun environment: launch N ranks
+    (one process per GPU, NCCL) through torch.distributed.run and pass their
+    output through; rank 0 prints the JSON line.  Fails loudly when fewer
+    than N GPUs are visible (ranks never share a GPU)."""
+    import socket
+    import subprocess
+
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, "
+                         f"found {have}; not running (would otherwise report n_gpus=1)\n")
+        sys.exit(2)
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
 
 
 def main():
     args = parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        if args.impl == "reference":   # rank 0 alone runs the reference
+            run_reference(args)
+            return
+        spawn_ranks(args)
+    world = dist_env()[0]
+    if args.impl == "ours" and world != max(args.gpus, 1):
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}\n")
+        sys.exit(2)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -119,6 +119,9 @@ typedef struct {
     int64_t block_capacity;
     int64_t frames_slot_mode;     /* frames finished in slot mode (svx_set_update_mode) */
     int64_t slot_overflow_reruns; /* slot-mode attempts re-run in segment mode */
+    int64_t async_reruns;         /* asynchronous frames re-run after an overflow */
+    int64_t last_h2d_bytes;       /* host -> device bytes of the last frame's inputs */
+    int64_t last_d2h_bytes;       /* device -> host bytes of the last frame's report */
 } svx_stats;
 
 typedef struct svx_map svx_map;
@@ -146,6 +149,30 @@ svx_status svx_reserve(svx_map* map, int64_t voxels, int64_t blocks);
 svx_status svx_integrate(svx_map* map, const void* points, int32_t points_dtype, int64_t n,
                          const double pose[16], const int32_t* labels, const void* feats,
                          int32_t feats_dtype, void* stream, svx_report* report);
+
+/* Asynchronous integrate_frame (fusion.py:200-293) for closed-set and
+ * geometry maps: enqueues the frame on `stream` and returns at once with a
+ * ticket; svx_report_wait(ticket) gives its IntegrationReport.  Same inputs,
+ * results and errors as svx_integrate -- a frame goes asynchronous only when
+ * none of the reference's frame errors (step budget, 2^21 extent, +/-2^30
+ * range, _core.pyx:661-712) can occur for it, which a finite max_range and
+ * bounded bands (no space carving) decide from the configuration and the
+ * origin; otherwise the frame runs synchronously and its report is held for
+ * the ticket the same way.  Host input arrays have been read when the call
+ * returns; device inputs are copied on the device by the frame itself (a
+ * frame stopped by a pool or slot overflow is re-run from that copy).  Every
+ * other entry point first finishes the frames in flight, so it sees the map
+ * after all of them.  At most svx_set_async frames (default 2, max 4)
+ * are in flight (svx_set_async); the last 64 reports are held. */
+svx_status svx_integrate_async(svx_map* map, const void* points, int32_t points_dtype, int64_t n,
+                               const double pose[16], const int32_t* labels, void* stream,
+                               uint64_t* ticket);
+svx_status svx_report_wait(svx_map* map, uint64_t ticket, svx_report* report);
+/* depth: frames in flight (0 = every frame synchronous, at most 4).
+ * leaf_headroom: leaf-pool room kept per frame in flight (0 = automatic:
+ * twice the most leaves a recent frame created, at least 4096); a frame that
+ * still runs out is re-run as described above. */
+svx_status svx_set_async(svx_map* map, int32_t depth, int64_t leaf_headroom);
 
 /* Same, for points already in the world frame with the sensor origin given:
  * the reference's backend seam (fusion.py:229-263 -> integrate_points), where

@@ -81,6 +81,9 @@ class SvxStats(ctypes.Structure):
         ("block_capacity", ctypes.c_int64),
         ("frames_slot_mode", ctypes.c_int64),
         ("slot_overflow_reruns", ctypes.c_int64),
+        ("async_reruns", ctypes.c_int64),
+        ("last_h2d_bytes", ctypes.c_int64),
+        ("last_d2h_bytes", ctypes.c_int64),
     ]
 
 
@@ -119,6 +122,9 @@ _SIGNATURES = {
     "svx_integrate": [_P, _P, _I32, _I64, _P, _P, _P, _I32, _P, ctypes.POINTER(SvxReport)],
     "svx_integrate_world": [_P, _P, _I32, _I64, _P, _P, _P, _I32, _P,
                             ctypes.POINTER(SvxReport)],
+    "svx_integrate_async": [_P, _P, _I32, _I64, _P, _P, _P, ctypes.POINTER(ctypes.c_uint64)],
+    "svx_report_wait": [_P, ctypes.c_uint64, ctypes.POINTER(SvxReport)],
+    "svx_set_async": [_P, _I32, _I64],
     "svx_integrate_depth": [_P, _P, _I32, ctypes.POINTER(SvxCamera), _P, _P, _P, _I32, _P,
                             ctypes.POINTER(SvxReport)],
     "svx_stats_get": [_P, ctypes.POINTER(SvxStats)],

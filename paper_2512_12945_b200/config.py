@@ -112,12 +112,20 @@ class EngineConfig:
     tsdf_dtype: "float64" keeps the reference's TSDF layout (grid.py:45-47) and
     makes d/w bit-identical to it; "float32" stores d/w in fp32 (update math
     stays fp64) and halves TSDF traffic.
+    async_frames: how many closed-set / geometry frames ``Mapper.integrate``
+    may leave in flight on the GPU (0-4; 0 = every call waits for its frame).
+    Reports are read when first used; every other call sees the map after
+    all submitted frames (svx_integrate_async, include/svx.h).
+    async_leaf_headroom: leaf-pool room kept per frame in flight (0 =
+    automatic); a frame that runs out anyway is re-run (svx_set_async).
     """
 
     tsdf_dtype: str = "float64"
     device: int = 0
     reserve_voxels: int = 0
     reserve_blocks: int = 0
+    async_frames: int = 2
+    async_leaf_headroom: int = 0
 
     def validate(self) -> None:
         if str(np.dtype(self.tsdf_dtype)) not in TSDF_DTYPES:
@@ -126,3 +134,7 @@ class EngineConfig:
             raise ConfigError(f"device must be >= 0, got {self.device}")
         if int(self.reserve_voxels) < 0 or int(self.reserve_blocks) < 0:
             raise ConfigError("reserve_voxels / reserve_blocks must be >= 0")
+        if not 0 <= int(self.async_frames) <= 4:
+            raise ConfigError(f"async_frames must be in [0, 4], got {self.async_frames}")
+        if int(self.async_leaf_headroom) < 0:
+            raise ConfigError("async_leaf_headroom must be >= 0")

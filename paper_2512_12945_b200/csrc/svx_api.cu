@@ -177,6 +177,8 @@ svx_status svx_create(const svx_config* cfg, svx_map** out) {
         return bail(fail(SVX_E_CUDA, "pinned mapped allocation failed"));
     }
     memset(m->h_ctr, 0, sizeof(FrameCtr));
+    m->h_ctr0 = m->h_ctr;
+    m->d_hctr0 = m->d_hctr;
     if ((st = ensure(m->ctr, sizeof(FrameCtr), s)) != SVX_OK) return bail(st);
     if (cudaEventCreate(&m->ev0) != cudaSuccess || cudaEventCreate(&m->ev1) != cudaSuccess ||
         cudaEventCreateWithFlags(&m->ev_in, cudaEventDisableTiming) != cudaSuccess ||
@@ -199,6 +201,12 @@ svx_status svx_create(const svx_config* cfg, svx_map** out) {
 svx_status svx_destroy(svx_map* m) {
     if (!m) return SVX_OK;
     cudaSetDevice(m->cfg.device);
+    for (int i = 0; i < m->aq_count; ++i) {   // frames in flight finish first
+        const AsyncFrame& f = m->aq[(m->aq_head + i) % kAsyncSlots];
+        if (f.e1) cudaEventSynchronize(f.e1);
+    }
+    m->aq_count = 0;
+    release_async(m);
     DevBuf* bufs[] = {&m->hash, &m->bcoord, &m->bkey, &m->bmask, &m->bslot, &m->vt,
                       &m->s0, &m->s1, &m->vrec, &m->vslot, &m->in_pts,
                       &m->in_lab, &m->in_feat, &m->dp_depth, &m->dp_lab_in, &m->dp_feat_in, &m->dp_pts, &m->dp_lab, &m->dp_feat, &m->ray, &m->rcnt, &m->roff, &m->rowkey,
@@ -212,7 +220,7 @@ svx_status svx_destroy(svx_map* m) {
                       &m->mesh_l, &m->mesh_t, &m->mesh_col, &m->mesh_vlab, &m->mesh_cls_l,
                       &m->mesh_cls_b, &m->mesh_pal};
     for (DevBuf* b : bufs) release(*b);
-    if (m->h_ctr) cudaFreeHost(m->h_ctr);
+    if (m->h_ctr0) cudaFreeHost(m->h_ctr0);
     if (m->h_kspan) cudaFreeHost(m->h_kspan);
     release(m->kspan);
     if (m->ev0) cudaEventDestroy(m->ev0);
@@ -233,6 +241,7 @@ svx_status svx_integrate(svx_map* m, const void* points, int32_t points_dtype, i
     if (!m || !pose || (n > 0 && !points)) return fail(SVX_E_INPUT, "null argument");
     if ((points_dtype & SVX_POSE_CHECK) && !pose_fast_ok(pose)) return (svx_status)SVX_POSE_NEEDS_HOST;
     SVX_TRY(set_device(m));
+    SVX_TRY(drain(m));
     PoseParams pp;
     for (int r = 0; r < 3; ++r) {
         for (int c = 0; c < 3; ++c) pp.R[3 * r + c] = pose[4 * r + c];
@@ -245,12 +254,48 @@ svx_status svx_integrate(svx_map* m, const void* points, int32_t points_dtype, i
                           (feats_dtype & 0xff) == SVX_F64, (cudaStream_t)stream, report, dev);
 }
 
+svx_status svx_integrate_async(svx_map* m, const void* points, int32_t points_dtype, int64_t n,
+                               const double pose[16], const int32_t* labels, void* stream,
+                               uint64_t* ticket) {
+    if (!m || !pose || !ticket || (n > 0 && !points)) return fail(SVX_E_INPUT, "null argument");
+    if (m->cfg.sem_kind == SVX_SEM_OPEN)
+        return fail(SVX_E_PAYLOAD, "open-set grid requires per-point features (use svx_integrate)");
+    if ((points_dtype & SVX_POSE_CHECK) && !pose_fast_ok(pose)) return (svx_status)SVX_POSE_NEEDS_HOST;
+    SVX_TRY(set_device(m));
+    PoseParams pp;
+    for (int r = 0; r < 3; ++r) {
+        for (int c = 0; c < 3; ++c) pp.R[3 * r + c] = pose[4 * r + c];
+        pp.t[r] = pose[4 * r + 3];
+    }
+    pp.sensor = 1;
+    pp.single = n == 1;
+    const int dev = (points_dtype & SVX_DEVICE_INPUTS) ? 1 : 0;
+    return integrate_async_impl(m, points, (points_dtype & 0xff) == SVX_F64, n, pp, labels,
+                                (cudaStream_t)stream, dev, ticket);
+}
+
+svx_status svx_report_wait(svx_map* m, uint64_t ticket, svx_report* report) {
+    if (!m) return fail(SVX_E_INPUT, "null argument");
+    SVX_TRY(set_device(m));
+    return report_wait(m, ticket, report);
+}
+
+svx_status svx_set_async(svx_map* m, int32_t depth, int64_t leaf_headroom) {
+    if (!m || depth < 0 || leaf_headroom < 0) return fail(SVX_E_INPUT, "invalid asynchronous settings");
+    SVX_TRY(set_device(m));
+    SVX_TRY(drain(m));
+    m->async_depth = std::min<int32_t>(depth, kAsyncSlots);
+    m->async_leaf_headroom = leaf_headroom;
+    return SVX_OK;
+}
+
 svx_status svx_import(svx_map* m, int64_t nl, const int32_t* leaf_coords, int64_t nv,
                       const int32_t* voxel_leaf, const int32_t* voxel_slot, const double* d,
                       const double* w, const void* sem0, const void* sem1, void* stream) {
     if (!m || (nv > 0 && (!leaf_coords || !voxel_leaf || !voxel_slot || !d || !w)))
         return fail(SVX_E_INPUT, "null argument");
     SVX_TRY(set_device(m));
+    SVX_TRY(drain(m));
     return import_impl(m, nl, leaf_coords, nv, voxel_leaf, voxel_slot, d, w, sem0, sem1,
                        (cudaStream_t)stream);
 }
@@ -261,6 +306,7 @@ svx_status svx_integrate_depth(svx_map* m, const void* depth, int32_t depth_dtyp
                                void* stream, svx_report* report) {
     if (!m || !depth || !camera || !pose) return fail(SVX_E_INPUT, "null argument");
     SVX_TRY(set_device(m));
+    SVX_TRY(drain(m));
     PoseParams pp;
     for (int r = 0; r < 3; ++r) {
         for (int c = 0; c < 3; ++c) pp.R[3 * r + c] = pose[4 * r + c];
@@ -278,6 +324,7 @@ svx_status svx_integrate_world(svx_map* m, const void* points_world, int32_t poi
                                svx_report* report) {
     if (!m || !origin || (n > 0 && !points_world)) return fail(SVX_E_INPUT, "null argument");
     SVX_TRY(set_device(m));
+    SVX_TRY(drain(m));
     PoseParams pp;
     memset(&pp, 0, sizeof(pp));
     pp.R[0] = pp.R[4] = pp.R[8] = 1.0;
@@ -292,6 +339,7 @@ svx_status svx_integrate_world(svx_map* m, const void* points_world, int32_t poi
 svx_status svx_reserve(svx_map* m, int64_t voxels, int64_t blocks) {
     if (!m || voxels < 0 || blocks < 0) return fail(SVX_E_INPUT, "invalid reserve arguments");
     SVX_TRY(set_device(m));
+    SVX_TRY(drain(m));
     cudaStream_t s = 0;
     SVX_TRY(reserve_blocks(m, std::max<int64_t>(blocks, m->nblocks), s));
     SVX_TRY(reserve_voxels(m, std::max<int64_t>(voxels, m->nvox), s));
@@ -302,6 +350,7 @@ svx_status svx_reserve(svx_map* m, int64_t voxels, int64_t blocks) {
 svx_status svx_set_profiling(svx_map* m, int32_t enable) {
     if (!m) return fail(SVX_E_INPUT, "null argument");
     SVX_TRY(set_device(m));
+    SVX_TRY(drain(m));
     if (enable && !m->h_kspan) {
         const size_t n = (size_t)kSpanKernels * 2 * kSpanMaxCtas * sizeof(unsigned long long);
         SVX_TRY(ensure(m->kspan, n, 0));
@@ -326,6 +375,8 @@ int32_t svx_stage_times(svx_map* m, double* ms, int32_t n) {
 
 svx_status svx_stats_get(svx_map* m, svx_stats* out) {
     if (!m || !out) return fail(SVX_E_INPUT, "null argument");
+    SVX_TRY(set_device(m));
+    SVX_TRY(drain(m));
     const int64_t te = (int64_t)tsdf_elem(m), se = (int64_t)sem_elem(m);
     int64_t per_vox = 2 * te + se * m->payload_d * (m->cfg.sem_kind == SVX_SEM_OPEN ? 2 : 1);
     out->leaf_count = m->nblocks;
@@ -339,11 +390,16 @@ svx_status svx_stats_get(svx_map* m, svx_stats* out) {
     out->block_capacity = m->bcap;
     out->frames_slot_mode = m->n_slot_frames;
     out->slot_overflow_reruns = m->n_slot_reruns;
+    out->async_reruns = m->n_async_reruns;
+    out->last_h2d_bytes = m->io_h2d;
+    out->last_d2h_bytes = m->io_d2h;
     return SVX_OK;
 }
 
 svx_status svx_active_count(svx_map* m, int64_t* count) {
     if (!m || !count) return fail(SVX_E_INPUT, "null argument");
+    SVX_TRY(set_device(m));
+    SVX_TRY(drain(m));
     *count = m->nvox;
     return SVX_OK;
 }
@@ -352,6 +408,7 @@ svx_status svx_export_active(svx_map* m, int64_t capacity, int64_t* coords, void
                              void* sem0, void* sem1, void* stream) {
     if (!m) return fail(SVX_E_INPUT, "null argument");
     SVX_TRY(set_device(m));
+    SVX_TRY(drain(m));
     cudaStream_t s = (cudaStream_t)stream;
     int64_t count = 0;
     SVX_TRY(build_active_list(m, &count, s));
@@ -382,6 +439,7 @@ svx_status svx_probe(svx_map* m, const int64_t* coords, int64_t cnt, void* d, vo
                      void* sem1, uint8_t* active, void* stream) {
     if (!m || (cnt > 0 && !coords)) return fail(SVX_E_INPUT, "null argument");
     SVX_TRY(set_device(m));
+    SVX_TRY(drain(m));
     cudaStream_t s = (cudaStream_t)stream;
     if (cnt == 0) return SVX_OK;
     DevBuf cstage;
@@ -417,6 +475,7 @@ svx_status svx_query_cosine(svx_map* m, const double* query, int64_t capacity, d
     if (m->cfg.sem_kind != SVX_SEM_OPEN)
         return fail(SVX_E_PAYLOAD, "embedding query needs an open-set map");
     SVX_TRY(set_device(m));
+    SVX_TRY(drain(m));
     cudaStream_t s = (cudaStream_t)stream;
     const int D = m->payload_d;
     // query norm on the host (D doubles)
@@ -516,6 +575,7 @@ svx_status svx_render(svx_map* m, const svx_render_camera* cam, int32_t mode, co
     if (!(cam->near_plane > 0.0) || !(cam->far_plane > cam->near_plane))
         return fail(SVX_E_CONFIG, "near/far planes must satisfy 0 < near < far");
     SVX_TRY(set_device(m));
+    SVX_TRY(drain(m));
     cudaStream_t s = (cudaStream_t)stream;
     const int* vlab = nullptr;
     if (mode == SVX_RENDER_SEMANTIC && emb && m->cfg.sem_kind == SVX_SEM_OPEN)
@@ -544,6 +604,7 @@ svx_status svx_sample_distance(svx_map* m, const double* points, int64_t n, doub
                                uint8_t* valid, void* stream) {
     if (!m || (n > 0 && (!points || !vals || !valid))) return fail(SVX_E_INPUT, "null argument");
     SVX_TRY(set_device(m));
+    SVX_TRY(drain(m));
     cudaStream_t s = (cudaStream_t)stream;
     DevBuf stage;
     const void* dp = nullptr;
@@ -569,6 +630,7 @@ svx_status svx_extract_mesh(svx_map* m, double min_weight, const double* emb, in
                             int64_t* n_triangles, void* stream) {
     if (!m || !n_vertices || !n_triangles || (emb && k < 1)) return fail(SVX_E_INPUT, "null argument");
     SVX_TRY(set_device(m));
+    SVX_TRY(drain(m));
     cudaStream_t s = (cudaStream_t)stream;
     const int* vlab = nullptr;
     if (emb && m->cfg.sem_kind == SVX_SEM_OPEN)
@@ -583,6 +645,7 @@ svx_status svx_mesh_read(svx_map* m, double* vertices, int32_t* triangles, int32
                          uint8_t* colors, const uint8_t* palette, int32_t npal, void* stream) {
     if (!m || (colors && (!palette || npal < 2))) return fail(SVX_E_INPUT, "null argument");
     SVX_TRY(set_device(m));
+    SVX_TRY(drain(m));
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t nv = m->mesh_nv, nt = m->mesh_nt;
     if (vertices && nv) SVX_CUDA(cudaMemcpyAsync(vertices, m->mesh_v.p, 24 * nv, cudaMemcpyDefault, s));
@@ -606,6 +669,7 @@ svx_status svx_classify(svx_map* m, const double* emb, int32_t k, double tempera
     if (m->cfg.sem_kind != SVX_SEM_OPEN)
         return fail(SVX_E_PAYLOAD, "classification needs an open-set map");
     SVX_TRY(set_device(m));
+    SVX_TRY(drain(m));
     cudaStream_t s = (cudaStream_t)stream;
     SVX_TRY(upload_queries(m, emb, k, s));
     const int D = m->payload_d;
@@ -639,6 +703,7 @@ svx_status svx_label_map(svx_map* m, int32_t mode, int64_t capacity, int32_t* la
     if (m->cfg.sem_kind != SVX_SEM_CLOSED)
         return fail(SVX_E_PAYLOAD, "label map needs a closed-set map");
     SVX_TRY(set_device(m));
+    SVX_TRY(drain(m));
     cudaStream_t s = (cudaStream_t)stream;
     int64_t count = 0;
     SVX_TRY(build_active_list(m, &count, s));
@@ -671,6 +736,7 @@ svx_status svx_shard_march(svx_map* m, const void* points, int32_t points_dtype,
     if (!m || !local || (!pose && !origin) || (n > 0 && !points))
         return fail(SVX_E_INPUT, "null argument");
     SVX_TRY(set_device(m));
+    SVX_TRY(drain(m));
     PoseParams pp;
     memset(&pp, 0, sizeof(pp));
     if (pose) {
@@ -692,6 +758,7 @@ svx_status svx_shard_plan(svx_map* m, const svx_shard_summary* global, int32_t r
                           int32_t nranks, int64_t* send_bytes, int32_t* remarch) {
     if (!m || !global || !send_bytes || !remarch) return fail(SVX_E_INPUT, "null argument");
     SVX_TRY(set_device(m));
+    SVX_TRY(drain(m));
     int rm = 0;
     svx_status st = shard_plan(m, global, rank, nranks, send_bytes, &rm, (cudaStream_t)0);
     *remarch = rm;
@@ -701,6 +768,7 @@ svx_status svx_shard_plan(svx_map* m, const svx_shard_summary* global, int32_t r
 svx_status svx_shard_pack(svx_map* m, void* send, int64_t capacity, void* stream) {
     if (!m) return fail(SVX_E_INPUT, "null argument");
     SVX_TRY(set_device(m));
+    SVX_TRY(drain(m));
     return shard_pack(m, send, capacity, (cudaStream_t)stream);
 }
 
@@ -708,6 +776,7 @@ svx_status svx_shard_apply(svx_map* m, const void* recv, const int64_t* recv_byt
                            void* stream, svx_report* report) {
     if (!m || !recv_bytes) return fail(SVX_E_INPUT, "null argument");
     SVX_TRY(set_device(m));
+    SVX_TRY(drain(m));
     return shard_apply(m, recv, recv_bytes, nranks, (cudaStream_t)stream, report);
 }
 
@@ -715,6 +784,7 @@ svx_status svx_export_leaf_stamps(svx_map* m, int64_t capacity, int32_t* frame, 
                                   int32_t* count, int64_t* nleaves, void* stream) {
     if (!m || !nleaves) return fail(SVX_E_INPUT, "null argument");
     SVX_TRY(set_device(m));
+    SVX_TRY(drain(m));
     cudaStream_t s = (cudaStream_t)stream;
     int64_t vox = 0;
     SVX_TRY(build_active_list(m, &vox, s));

@@ -19,6 +19,8 @@
 #include <math.h>
 #include <string.h>
 
+#include <cmath>
+
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
@@ -159,6 +161,7 @@ svx_status reserve_frame(svx_map* m, int64_t n, cudaStream_t s) {
         SVX_TRY(ensure(m->roff, sizeof(long long) * m->npts_cap, s));
         SVX_TRY(ensure(m->cubtmp, scan_temp_bytes(m->npts_cap), s));
     }
+    m->rcap_sized = m->rcap;
     return SVX_OK;
 }
 
@@ -240,11 +243,14 @@ static svx_status collect_stage_times(svx_map* m) {
     return SVX_OK;
 }
 
-// Run one frame attempt: replay (or capture, on the map's own stream) the
-// frame graph on the caller's stream.
+// Launch one frame attempt: replay (or capture, on the map's own stream) the
+// frame graph on the caller's stream; ev_end is recorded after it.  The
+// frame's parameters are read from m->h_ctr->p (the mirror the attempt
+// uses).
 static const bool g_no_graph = getenv("SVX_NO_GRAPH") != nullptr;   // experiment: eager launches
 
-static svx_status run_frame(svx_map* m, int pts_f64, int feats_f64, cudaStream_t s) {
+static svx_status launch_frame(svx_map* m, int pts_f64, int feats_f64, cudaStream_t s,
+                               cudaEvent_t ev_end) {
     if (g_no_graph) {
         if (m->prof) {
             const size_t n = (size_t)kSpanKernels * 2 * kSpanMaxCtas * sizeof(unsigned long long);
@@ -253,11 +259,8 @@ static svx_status run_frame(svx_map* m, int pts_f64, int feats_f64, cudaStream_t
         SVX_TRY(clean_ctr(m, s));
         if (g_trace_host) g_t_launch0 = now_us();
         SVX_TRY(enqueue_frame(m, pts_f64, feats_f64, s));
-        SVX_CUDA(cudaEventRecord(m->ev1, s));
+        SVX_CUDA(cudaEventRecord(ev_end, s));
         if (g_trace_host) g_t_launch1 = now_us();
-        SVX_CUDA(cudaEventSynchronize(m->ev1));
-        if (g_trace_host) g_t_synced = now_us();
-        if (m->prof) SVX_TRY(collect_stage_times(m));
         return SVX_OK;
     }
     const unsigned long long sig = graph_signature(m, pts_f64, feats_f64);
@@ -304,7 +307,6 @@ static svx_status run_frame(svx_map* m, int pts_f64, int feats_f64, cudaStream_t
         if (na < 1 || na > 16) return fail(SVX_E_INTERNAL, "frame graph: bad first-kernel arity");
         SVX_CUDA(cudaGraphKernelNodeGetParams(root, &m->walk_kp[gm]));
         for (int i = 0; i < na - 1; ++i) m->walk_args[gm][i] = m->walk_kp[gm].kernelParams[i];
-        m->walk_args[gm][na - 1] = &m->h_ctr->p;   // this frame's FrameParams, read at SetParams
         m->walk_kp[gm].kernelParams = m->walk_args[gm];
         m->walk_kp[gm].extra = nullptr;
         m->gsig[gm] = sig;
@@ -319,7 +321,10 @@ static svx_status run_frame(svx_map* m, int pts_f64, int feats_f64, cudaStream_t
             }
         m->graph_kernels[gm] = nk;
     }
-    // this frame's parameters into the first kernel's FrameParams argument
+    // this frame's parameters (in the attempt's mirror) into the first kernel's
+    // FrameParams argument; an instantiated graph copies them at this call, so
+    // launches already queued keep theirs
+    m->walk_args[gm][m->walk_nargs[gm] - 1] = &m->h_ctr->p;
     SVX_CUDA(cudaGraphExecKernelNodeSetParams(gexec, m->walk_node[gm], &m->walk_kp[gm]));
     if (m->prof) {
         const size_t n = (size_t)kSpanKernels * 2 * kSpanMaxCtas * sizeof(unsigned long long);
@@ -330,8 +335,14 @@ static svx_status run_frame(svx_map* m, int pts_f64, int feats_f64, cudaStream_t
     if (g_trace_host) g_t_launch0 = now_us();
     SVX_CUDA(cudaGraphLaunch(gexec, s));
     count_launch(m->graph_kernels[gm]);   // the frame graph's kernel nodes
-    SVX_CUDA(cudaEventRecord(m->ev1, s));
+    SVX_CUDA(cudaEventRecord(ev_end, s));
     if (g_trace_host) g_t_launch1 = now_us();
+    return SVX_OK;
+}
+
+// Run one frame attempt and wait for it (synchronous frames).
+static svx_status run_frame(svx_map* m, int pts_f64, int feats_f64, cudaStream_t s) {
+    SVX_TRY(launch_frame(m, pts_f64, feats_f64, s, m->ev1));
     SVX_CUDA(cudaEventSynchronize(m->ev1));
     if (g_trace_host) g_t_synced = now_us();
     if (m->prof) SVX_TRY(collect_stage_times(m));
@@ -364,7 +375,7 @@ svx_status reserve_pools(svx_map* m, cudaStream_t s) {
 }
 
 // Zeroed counters with the live pool counts; FrameParams are filled by the caller.
-void reset_ctr(svx_map* m) {
+void reset_ctr(svx_map* m, int64_t stamp) {
     FrameCtr* hc = m->h_ctr;
     memset(hc, 0, sizeof(FrameCtr));
     for (int a = 0; a < 3; ++a) {
@@ -379,7 +390,7 @@ void reset_ctr(svx_map* m) {
     p.hmask = m->hcap - 1;
     p.bcap = m->bcap;
     p.vcap = m->vcap;
-    p.frame = (int)m->frames;
+    p.frame = (int)stamp;
     p.maxrows = m->maxrows;
     p.inline_singles = inline_singles(m);
     p.slots = m->frame_slots;
@@ -448,7 +459,6 @@ void finish_frame(svx_map* m, int64_t nblocks0, int64_t nvox0, svx_report& r) {
     m->new_leaves_cap = std::max<int64_t>(m->new_leaves_cap, 2 * r.new_blocks + 1024);
     m->nblocks = (int64_t)hc->nblocks;
     m->nvox = (int64_t)hc->nvox;
-    m->frames++;
     m->n_slot_frames += m->frame_slots;
     m->last_rows = (int64_t)hc->rows;
     m->last_touched = (int64_t)hc->n_touched;
@@ -468,8 +478,11 @@ KeyPack default_key_pack(const svx_map* m, const PoseParams& pp) {
 
 svx_status integrate_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n,
                           const PoseParams& pp, const int32_t* labels_in, const void* feats_in,
-                          int feats_f64, cudaStream_t s, svx_report* rep, int device_inputs) {
+                          int feats_f64, cudaStream_t s, svx_report* rep, int device_inputs,
+                          const FrameOpts* opt) {
     const double t_enter = g_trace_host ? now_us() : 0.0;
+    const bool rerun = opt && opt->stamp >= 0;
+    const int64_t stamp = rerun ? opt->stamp : m->frames;
     svx_report r;
     memset(&r, 0, sizeof(r));
     r.points_in = n;
@@ -482,10 +495,12 @@ svx_status integrate_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n
     if (n < 0) return fail(SVX_E_INPUT, "negative point count");
     if (n >= (int64_t)INT_MAX) return fail(SVX_E_INPUT, "point count exceeds 2^31-1");
     if (n == 0) {
-        m->frames++;
+        if (!rerun) m->frames++;
         if (rep) *rep = r;
         return SVX_OK;
     }
+    m->h_ctr = m->h_ctr0;   // synchronous frames use the map's own mirror
+    m->d_hctr = m->d_hctr0;
     SVX_CUDA(cudaEventRecord(m->ev0, s));
     const void* pts = pts_in;
     const void* feats = kind == SVX_SEM_OPEN ? feats_in : nullptr;
@@ -515,20 +530,31 @@ svx_status integrate_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n
         return SVX_OK;
     };
     if (!staged && !zc_pts) SVX_TRY(stage_all());
+    if (!device_inputs && !rerun) {   // host-link bytes: inputs in (copied or read in place)
+        const bool host_p = zc_pts || (pts != pts_in);
+        m->io_h2d = host_p ? (int64_t)n * 3 * (pts_f64 ? 8 : 4) : 0;
+        if (kind == SVX_SEM_CLOSED && (zc_lab || labv != (const void*)labels_in)) m->io_h2d += n * 4;
+        if (kind == SVX_SEM_OPEN && feats != feats_in)
+            m->io_h2d += (int64_t)n * m->payload_d * (feats_f64 ? 8 : 4);
+    } else if (!rerun) {
+        m->io_h2d = 0;
+    }
+    m->io_d2h = (int64_t)sizeof(FrameCtr);   // the counter mirror the last kernel writes
     init_row_space(m, n);
     KeyPack kp = default_key_pack(m, pp);
     FrameCtr* hc = m->h_ctr;
     // counts before this frame (stamps, report); m->nblocks / m->nvox stay the
     // live counts, including what a capacity-aborted attempt allocated
-    const int64_t nblocks0 = m->nblocks, nvox0 = m->nvox;
-    m->frame_retry_segments = 0;
+    const int64_t nblocks0 = opt && opt->nblocks0 >= 0 ? opt->nblocks0 : m->nblocks;
+    const int64_t nvox0 = opt && opt->nvox0 >= 0 ? opt->nvox0 : m->nvox;
+    m->frame_retry_segments = opt ? opt->force_segments : 0;
     for (int attempt = 0;; ++attempt) {
         if (attempt >= 8) return fail(SVX_E_INTERNAL, "frame scratch could not be sized");
         SVX_TRY(reserve_frame(m, n, s));
         SVX_TRY(reserve_pools(m, s));
         m->frame_slots = choose_slots(m);
         if (!staged && !m->frame_slots) SVX_TRY(stage_all());
-        reset_ctr(m);
+        reset_ctr(m, stamp);
         FrameParams& p = hc->p;
         p.pts = staged ? pts : zc_pts;
         p.labels = (const int32_t*)(staged ? labv : zc_lab);
@@ -537,8 +563,12 @@ svx_status integrate_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n
         p.pp = pp;
         p.kp = kp;
         p.nblocks0 = nblocks0;
+        p.nvox0 = nvox0;
 
         SVX_TRY(run_frame(m, pts_f64, feats_f64, s));
+        // a frame that ends needing the host leaves the device counters
+        // poisoned for queued frames: clear them before the next attempt
+        if (hc->abort | hc->err_cap | hc->err_slots) m->ctr_clean = false;
 
         // the reference's pre-allocation checks, in its order (_core.pyx:661-712, :386-387)
         if (hc->err_budget)
@@ -587,6 +617,7 @@ svx_status integrate_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n
     r.band_hits = (int64_t)hc->band_hits;
     r.kernel_ms = ms;
     finish_frame(m, nblocks0, nvox0, r);
+    if (!rerun) m->frames++;
     if (rep) *rep = r;
     if (g_trace_host) {
         const double t_exit = now_us();
@@ -594,6 +625,264 @@ svx_status integrate_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n
                 g_t_launch0 - t_enter, g_t_launch1 - g_t_launch0, g_t_synced - g_t_launch1,
                 t_exit - g_t_synced, t_exit - t_enter, 1e3 * ms);
     }
+    return SVX_OK;
+}
+
+// ---- asynchronous frames ---------------------------------------------------
+//
+// svx_integrate_async enqueues a frame and returns a ticket; the report is
+// read later (svx_report_wait) and every other entry point first finishes
+// the frames in flight (drain).  A frame goes asynchronous only when nothing
+// it can meet needs the host before it mutates the map:
+//   - the reference's frame errors cannot occur: with a finite max_range
+//     every band lies within max_range + truncation of the sensor, so the
+//     step budget, the 2^21 extent / key window and the +/-2^30 range checks
+//     (_core.pyx:661-712, :386-387) are decided by the configuration and the
+//     origin alone;
+//   - bounded bands (no space carving): at most maxrows rows per point, so
+//     the row buffers are sized for the worst case;
+//   - closed-set or geometry payloads (open-set frames take milliseconds,
+//     where one host round trip does not matter).
+// What remains data-dependent -- a pool or slot overflow -- stops the frame
+// on the device before any payload change (as for synchronous frames), and
+// the frames queued behind it find the device counters poisoned and do
+// nothing but keep their own copy of their inputs.  When the host finishes
+// the failed frame it recovers as the synchronous path does and re-runs it,
+// then the frames behind it, from those copies.
+
+static bool async_eligible(const svx_map* m, int64_t n, const PoseParams& pp) {
+    const svx_config& c = m->cfg;
+    if (m->async_depth < 1 || m->prof || g_no_graph || n <= 0 || n >= (int64_t)INT_MAX) return false;
+    if (c.sem_kind == SVX_SEM_OPEN || c.space_carving) return false;
+    const double h = c.voxel_size;
+    const double bound = 3.0 * (2.0 * c.truncation / h + 1.0) + 3.0;
+    if (bound > 32.0) return false;   // dense rows (init_row_space)
+    const double reach = (c.max_range + c.truncation) / h + 4.0;   // voxels from the sensor
+    if (!std::isfinite(reach) || reach >= (double)(1LL << (kPackBits - 1))) return false;
+    for (int a = 0; a < 3; ++a) {
+        const double o = pp.t[a] / h;
+        if (!std::isfinite(o) || fabs(o) + reach >= (double)kCoordLimit) return false;
+    }
+    return true;
+}
+
+static void store_report(svx_map* m, uint64_t ticket, const svx_report& r) {
+    const int i = (int)(ticket % kDoneReports);
+    m->done_rep[i] = r;
+    m->done_tag[i] = ticket;
+}
+
+static svx_status ensure_async_slot(svx_map* m, AsyncFrame& f) {
+    if (f.h) return SVX_OK;
+    if (cudaHostAlloc((void**)&f.h, sizeof(FrameCtr), cudaHostAllocMapped) != cudaSuccess ||
+        cudaHostGetDevicePointer((void**)&f.d, f.h, 0) != cudaSuccess ||
+        cudaEventCreate(&f.e0) != cudaSuccess || cudaEventCreate(&f.e1) != cudaSuccess ||
+        cudaEventCreateWithFlags(&f.ecopy, cudaEventDisableTiming) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(SVX_E_CUDA, "asynchronous frame slot allocation failed");
+    }
+    memset(f.h, 0, sizeof(FrameCtr));
+    return SVX_OK;
+}
+
+void release_async(svx_map* m) {
+    for (AsyncFrame& f : m->aq) {
+        if (f.h) cudaFreeHost(f.h);
+        if (f.e0) cudaEventDestroy(f.e0);
+        if (f.e1) cudaEventDestroy(f.e1);
+        if (f.ecopy) cudaEventDestroy(f.ecopy);
+        release(f.pts);
+        release(f.lab);
+        f = AsyncFrame();
+    }
+    if (m->cstream) cudaStreamDestroy(m->cstream);
+    m->cstream = nullptr;
+}
+
+// Re-run asynchronous frame f synchronously from its own input copy.
+static svx_status rerun_async(svx_map* m, const AsyncFrame& f, const FrameOpts& o, svx_report* r) {
+    return integrate_impl(m, f.pts.p, f.pts_f64, f.n, f.pp,
+                          m->cfg.sem_kind == SVX_SEM_CLOSED ? ptr<int32_t>(f.lab) : nullptr,
+                          nullptr, 0, f.stream, r, 1, &o);
+}
+
+// Finish the oldest frame in flight: wait for it and take its report, or --
+// when it stopped needing the host -- recover and re-run it and every frame
+// queued behind it (those did nothing; see above).
+static svx_status finalize_oldest(svx_map* m) {
+    AsyncFrame& f = m->aq[m->aq_head];
+    SVX_CUDA(cudaEventSynchronize(f.e1));
+    FrameCtr* hc = f.h;
+    if (!(hc->abort | hc->err_cap | hc->err_slots)) {
+        svx_report r;
+        memset(&r, 0, sizeof(r));
+        float ms = 0.f;
+        SVX_CUDA(cudaEventElapsedTime(&ms, f.e0, f.e1));
+        r.points_in = f.n;
+        r.skipped_nonfinite = (int64_t)hc->nonfinite;
+        r.skipped_range = (int64_t)hc->range;
+        r.skipped_degenerate = (int64_t)hc->degenerate;
+        r.skipped_bad_label = (int64_t)hc->bad_label;
+        r.points_used = (int64_t)hc->used;
+        r.band_hits = (int64_t)hc->band_hits;
+        r.kernel_ms = ms;
+        m->h_ctr = hc;
+        m->frame_slots = f.slots;
+        finish_frame(m, hc->p.nblocks0, hc->p.nvox0, r);
+        m->h_ctr = m->h_ctr0;
+        store_report(m, f.ticket, r);
+        m->aq_head = (m->aq_head + 1) % kAsyncSlots;
+        m->aq_count--;
+        return SVX_OK;
+    }
+    // recovery: everything queued behind f is a no-op; let it finish
+    const int last = (m->aq_head + m->aq_count - 1) % kAsyncSlots;
+    SVX_CUDA(cudaEventSynchronize(m->aq[last].e1));
+    const int64_t nblocks0 = hc->p.nblocks0, nvox0 = hc->p.nvox0;
+    cudaStream_t s = f.stream;
+    m->h_ctr = hc;
+    m->d_hctr = f.d;
+    m->frame_slots = f.slots;
+    FrameOpts o;
+    o.stamp = f.frame;
+    o.nblocks0 = nblocks0;
+    o.nvox0 = nvox0;
+    svx_status st = SVX_OK;
+    if (hc->abort) {   // gate abort: nothing changed (the row buffer only; cannot recur)
+        if (hc->err_cap) m->rcap = std::max<uint64_t>(2 * m->rcap, hc->rows + hc->rows / 2 + 4096);
+    } else if (hc->err_cap) {
+        st = recover_capacity(m, nblocks0, s);
+    } else {
+        st = recover_slots(m, nblocks0, s);
+        o.force_segments = 1;
+    }
+    m->ctr_clean = false;   // clears the poison
+    m->n_async_reruns++;
+    m->h_ctr = m->h_ctr0;
+    m->d_hctr = m->d_hctr0;
+    // re-run f, then the frames behind it, in order (the ring empties even on error)
+    const int cnt = m->aq_count;
+    const int head = m->aq_head;
+    m->aq_count = 0;
+    m->aq_head = (head + cnt) % kAsyncSlots;
+    for (int i = 0; i < cnt && st == SVX_OK; ++i) {
+        const AsyncFrame& g = m->aq[(head + i) % kAsyncSlots];
+        FrameOpts go;
+        go.stamp = g.frame;
+        svx_report r;
+        st = rerun_async(m, g, i == 0 ? o : go, &r);
+        if (st == SVX_OK) store_report(m, g.ticket, r);
+    }
+    return st;
+}
+
+svx_status drain(svx_map* m) {
+    while (m->aq_count > 0) SVX_TRY(finalize_oldest(m));
+    return SVX_OK;
+}
+
+svx_status report_wait(svx_map* m, uint64_t ticket, svx_report* out) {
+    if (ticket == 0 || ticket >= m->ticket_next) return fail(SVX_E_INPUT, "unknown frame ticket");
+    while (m->aq_count > 0 && m->aq[m->aq_head].ticket <= ticket) SVX_TRY(finalize_oldest(m));
+    const int i = (int)(ticket % kDoneReports);
+    if (m->done_tag[i] != ticket) return fail(SVX_E_INPUT, "frame report no longer held (read it sooner)");
+    if (out) *out = m->done_rep[i];
+    return SVX_OK;
+}
+
+svx_status integrate_async_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n,
+                                const PoseParams& pp, const int32_t* labels_in, cudaStream_t s,
+                                int device_inputs, uint64_t* ticket) {
+    const int kind = m->cfg.sem_kind;
+    if (kind == SVX_SEM_CLOSED && !labels_in && n > 0)
+        return fail(SVX_E_PAYLOAD, "closed-set grid requires per-point labels");
+    if (!async_eligible(m, n, pp)) {   // synchronous frame, report kept the same way
+        SVX_TRY(drain(m));
+        svx_report r;
+        SVX_TRY(integrate_impl(m, pts_in, pts_f64, n, pp, labels_in, nullptr, 0, s, &r, device_inputs));
+        const uint64_t t = m->ticket_next++;
+        store_report(m, t, r);
+        *ticket = t;
+        return SVX_OK;
+    }
+    if (m->aq_count >= std::min(m->async_depth, kAsyncSlots)) SVX_TRY(finalize_oldest(m));
+    init_row_space(m, n);
+    // worst-case rows (finish_frame may have lowered rcap to 1.5x the last
+    // frame's rows: asynchronous frames always take the bound), and pool
+    // headroom for every frame in flight; growing anything first finishes
+    // the frames in flight
+    const uint64_t rows_bound = (uint64_t)n * (uint64_t)m->maxrows + 4096;
+    const int64_t vneed_per = (int64_t)rows_bound;
+    const int64_t bneed_per = m->async_leaf_headroom > 0 ? m->async_leaf_headroom
+                                                         : std::max<int64_t>(m->new_leaves_cap, 4096);
+    const int depth = std::min(m->async_depth, kAsyncSlots);
+    const int q = m->aq_count + 1;
+    const bool grow = n > m->npts_cap || rows_bound > m->rcap_sized ||
+                      m->nvox + q * vneed_per > m->vcap || m->nblocks + q * bneed_per > m->bcap;
+    if (grow) {
+        SVX_TRY(drain(m));
+        m->rcap = std::max<uint64_t>(m->rcap, rows_bound);
+        SVX_TRY(reserve_frame(m, n, s));
+        SVX_TRY(reserve_voxels(m, m->nvox + depth * vneed_per, s));
+        SVX_TRY(reserve_blocks(m, m->nblocks + depth * bneed_per, s));
+    }
+    m->rcap = m->rcap_sized;   // the row space the scratch buffers were sized for (>= the bound)
+    const int slot = (m->aq_head + m->aq_count) % kAsyncSlots;
+    AsyncFrame& f = m->aq[slot];
+    SVX_TRY(ensure_async_slot(m, f));
+    const size_t pbytes = (size_t)n * 3 * (pts_f64 ? 8 : 4);
+    SVX_TRY(ensure(f.pts, pbytes, s));
+    if (kind == SVX_SEM_CLOSED) SVX_TRY(ensure(f.lab, (size_t)n * 4, s));
+    const bool dev = device_inputs || is_device_ptr(pts_in);
+    const void* pts = pts_in;
+    const int32_t* lab = kind == SVX_SEM_CLOSED ? labels_in : nullptr;
+    if (!dev) {
+        // host inputs: copied into the frame's own buffers on the copy stream
+        // (overlapping the frames in flight); on return the caller's arrays
+        // have been read
+        if (!m->cstream) SVX_CUDA(cudaStreamCreateWithFlags(&m->cstream, cudaStreamNonBlocking));
+        SVX_CUDA(cudaMemcpyAsync(f.pts.p, pts_in, pbytes, cudaMemcpyHostToDevice, m->cstream));
+        if (lab) SVX_CUDA(cudaMemcpyAsync(f.lab.p, lab, (size_t)n * 4, cudaMemcpyHostToDevice, m->cstream));
+        SVX_CUDA(cudaEventRecord(f.ecopy, m->cstream));
+        SVX_CUDA(cudaStreamWaitEvent(s, f.ecopy, 0));
+        pts = f.pts.p;
+        lab = lab ? ptr<int32_t>(f.lab) : nullptr;
+    }
+    m->h_ctr = f.h;
+    m->d_hctr = f.d;
+    m->frame_retry_segments = 0;
+    m->frame_slots = choose_slots(m);
+    reset_ctr(m, m->frames);
+    FrameParams& p = f.h->p;
+    p.pts = pts;
+    p.labels = lab;
+    p.feats = nullptr;
+    p.n = n;
+    p.pp = pp;
+    p.kp = default_key_pack(m, pp);
+    p.nblocks0 = -1;   // taken on the device at the frame's start
+    p.nvox0 = -1;
+    p.stage_pts = dev ? f.pts.p : nullptr;
+    p.stage_lab = dev && kind == SVX_SEM_CLOSED ? ptr<int32_t>(f.lab) : nullptr;
+    f.ticket = m->ticket_next;
+    f.frame = m->frames;
+    f.n = n;
+    f.pts_f64 = pts_f64;
+    f.slots = m->frame_slots;
+    f.pp = pp;
+    f.stream = s;
+    svx_status st = SVX_OK;
+    if (cudaEventRecord(f.e0, s) != cudaSuccess) st = fail(SVX_E_CUDA, "event record failed");
+    if (st == SVX_OK) st = launch_frame(m, pts_f64, 0, s, f.e1);
+    m->h_ctr = m->h_ctr0;
+    m->d_hctr = m->d_hctr0;
+    if (st != SVX_OK) return st;
+    if (!dev) SVX_CUDA(cudaEventSynchronize(f.ecopy));
+    m->io_h2d = dev ? 0 : (int64_t)pbytes + (kind == SVX_SEM_CLOSED ? n * 4 : 0);
+    m->io_d2h = (int64_t)sizeof(FrameCtr);
+    m->aq_count++;
+    m->frames++;
+    *ticket = m->ticket_next++;
     return SVX_OK;
 }
 

@@ -92,7 +92,9 @@ struct FrameParams {
     unsigned long long ucap;   // touched voxels the per-frame lists hold
     unsigned long long rcap;   // rows the dense row arrays / segment buffer hold
     long long hmask;           // leaf hash capacity - 1
-    long long nblocks0;        // leaves before this frame (ids >= it are new)
+    long long nblocks0;        // leaves before this frame (ids >= it are new); < 0: the
+                               // first kernel takes it (and nvox0) from the live counters
+    long long nvox0;           // voxels before this frame (report only)
     long long bcap;            // leaf pool capacity
     long long vcap;            // voxel pool capacity
     int frame;                 // creation stamp for new leaves
@@ -104,6 +106,10 @@ struct FrameParams {
     void* mirror;              // graph frames: device address of the mapped host FrameCtr
     int epilogue;              // 1: the frame's last kernel publishes + resets the counters
     unsigned seq;              // launch sequence number (epoch of the segment-scan status)
+    // asynchronous frames with device inputs: the walk copies the frame's
+    // points / labels here first (the frame's own copy, for a re-run)
+    void* stage_pts;
+    int32_t* stage_lab;
 };
 
 // Kernels with recorded spans in profiling mode (svx_stage_times order).
@@ -153,6 +159,11 @@ struct FrameCtr {
     unsigned long long work_open;
     unsigned long long work_huge;   // K5h: next huge voxel; K5g: next (voxel, slice) item
     unsigned long long work_items;
+    // Persistent (kept by the epilogue's reset, like nblocks / nvox): set when a
+    // frame ends needing the host (pool overflow, slot overflow, gate abort).
+    // Asynchronous frames queued behind it see it and do nothing but stage
+    // their inputs; the host clears it after recovering (clean_ctr).
+    unsigned long long poison;
 };
 
 // Per-voxel frame record (indexed by voxel id; cnt and cur are zero between
@@ -235,6 +246,24 @@ __host__ __device__ inline void unpack_key(unsigned long long key, const KeyPack
 
 }  // namespace svx
 
+namespace svx {
+constexpr int kAsyncSlots = 4;     // most frames in flight (svx_set_async_depth)
+constexpr int kDoneReports = 64;   // finished asynchronous reports kept for svx_report_wait
+// One asynchronous frame in flight: its counter mirror, events and its own
+// copy of its inputs (a frame that must be re-run is re-run from it).
+struct AsyncFrame {
+    FrameCtr* h = nullptr;        // mapped pinned counter mirror (host address)
+    FrameCtr* d = nullptr;        // its device address
+    cudaEvent_t e0 = nullptr, e1 = nullptr, ecopy = nullptr;
+    DevBuf pts, lab;              // staged inputs
+    uint64_t ticket = 0;
+    int64_t frame = 0, n = 0;     // creation stamp, points
+    int pts_f64 = 0, slots = 0;
+    PoseParams pp{};
+    cudaStream_t stream = nullptr;
+};
+}  // namespace svx
+
 struct svx_map {
     svx_config cfg;
     int payload_d = 0;     // C (closed) or D (open)
@@ -244,7 +273,8 @@ struct svx_map {
     svx::DevBuf vt, s0, s1;                  int64_t vcap = 0, nvox = 0;  // vt: {d, w} per voxel
     svx::DevBuf vrec;                        // per-voxel frame records (svx::VoxFrame)
     svx::DevBuf vslot;                       // slot mode: kSlots RowSlots per voxel
-    int64_t n_slot_frames = 0, n_slot_reruns = 0;
+    int64_t n_slot_frames = 0, n_slot_reruns = 0, n_async_reruns = 0;
+    int64_t io_h2d = 0, io_d2h = 0;   // host-link bytes of the last frame (inputs in, report out)
     int mode_pref = 0;      // SVX_UPDATE_AUTO / SEGMENTS / SLOTS
     int slot_hold = 0;      // frames to stay in segment mode after a slot overflow
     int64_t last_rows = 0, last_touched = 0;   // previous frame's rows and touched voxels
@@ -252,12 +282,23 @@ struct svx_map {
     int frame_retry_segments = 0;   // this frame overflowed its slots: re-run with segments
     int64_t frames = 0;
     unsigned seq = 0;   // frame launches so far (attempts included)
+    // asynchronous frames (svx_integrate_async): ring of frames in flight,
+    // finished in order; their reports are kept for svx_report_wait
+    svx::AsyncFrame aq[svx::kAsyncSlots];
+    int aq_head = 0, aq_count = 0;
+    int async_depth = 2;
+    int64_t async_leaf_headroom = 0;   // leaves kept free per frame in flight (0 = automatic)
+    uint64_t ticket_next = 1;
+    svx_report done_rep[svx::kDoneReports] = {};
+    uint64_t done_tag[svx::kDoneReports] = {};
+    cudaStream_t cstream = nullptr;   // host-input copies of asynchronous frames
     // per-frame scratch
     svx::DevBuf in_pts, in_lab, in_feat;
     svx::DevBuf dp_depth, dp_lab_in, dp_feat_in, dp_pts, dp_lab, dp_feat;   // depth frames
     svx::DevBuf ray, rcnt, roff, rowkey, rowvid, rowray, rowd, rowlab, partials;
     svx::DevBuf tlist, mlist, longlist, srid, bitmap, rcount, hinfo;
     uint64_t ucap = 0, rcap = 0;
+    uint64_t rcap_sized = 0;      // rcap the frame scratch was last sized for (reserve_frame)
     int64_t new_leaves_cap = 0;   // leaf-pool headroom kept for one frame
     int maxrows = -1;      // row slots per ray; 0 = dense rows
     int64_t npts_cap = 0;  // points the per-ray scratch holds
@@ -274,8 +315,10 @@ struct svx_map {
     int graph_kernels[2] = {0, 0};   // kernel nodes of each frame graph (launch accounting)
     svx::DevBuf cubtmp;
     svx::DevBuf ctr;      // FrameCtr
-    svx::FrameCtr* h_ctr = nullptr;  // pinned, mapped mirror (host side)
+    svx::FrameCtr* h_ctr = nullptr;  // pinned, mapped mirror of the frame being run (host side)
     svx::FrameCtr* d_hctr = nullptr; // its device address
+    svx::FrameCtr* h_ctr0 = nullptr; // the mirror of synchronous frames (h_ctr points at it,
+    svx::FrameCtr* d_hctr0 = nullptr;//   or at an asynchronous frame's own mirror)
     bool ctr_clean = false;          // device FrameCtr is in the reset state
     // query scratch
     svx::DevBuf ord0, ord1, ordk0, ordk1, ordf0, ordf1;  // leaf order (by creation stamp)
@@ -397,6 +440,11 @@ __device__ __forceinline__ void load_frame_params(FrameCtr* ctr, FrameCtr& s, co
     static_assert(sizeof(FrameParams) % 8 == 0, "FrameParams must be a whole number of words");
     for (int i = threadIdx.x; i < (int)(sizeof(FrameParams) / 8); i += blockDim.x) dst[i] = src[i];
     __syncthreads();
+    if (threadIdx.x == 0 && s.p.nblocks0 < 0) {   // asynchronous frame: pool counts at its start
+        s.p.nblocks0 = (long long)s.nblocks;
+        s.p.nvox0 = (long long)s.nvox;
+    }
+    __syncthreads();
     if (blockIdx.x == 0) {
         unsigned long long* g = reinterpret_cast<unsigned long long*>(&ctr->p);
         for (int i = threadIdx.x; i < (int)(sizeof(FrameParams) / 8); i += blockDim.x) g[i] = dst[i];
@@ -414,9 +462,10 @@ __device__ __forceinline__ void reset_ctr_device(FrameCtr* ctr) {
     const int first = (int)(offsetof(FrameCtr, nonfinite) / 8);
     const int total = (int)(sizeof(FrameCtr) / 8);
     const int keep0 = (int)(offsetof(FrameCtr, nblocks) / 8), keep1 = (int)(offsetof(FrameCtr, nvox) / 8);
+    const int keep2 = (int)(offsetof(FrameCtr, poison) / 8);
     const int bb0 = (int)(offsetof(FrameCtr, bbox_min) / 8), bb1 = (int)(offsetof(FrameCtr, bbox_max) / 8);
     for (int i = first + (int)threadIdx.x; i < total; i += blockDim.x) {
-        if (i == keep0 || i == keep1) continue;
+        if (i == keep0 || i == keep1 || i == keep2) continue;
         unsigned long long v = 0ULL;
         if (i >= bb0 && i < bb0 + 3) v = (unsigned long long)LLONG_MAX;
         if (i >= bb1 && i < bb1 + 3) v = (unsigned long long)LLONG_MIN;
@@ -441,6 +490,7 @@ __device__ __forceinline__ void frame_epilogue(FrameCtr* ctr, int epi, void* mir
     unsigned long long* dst = reinterpret_cast<unsigned long long*>(mirror);
     for (int i = threadIdx.x; i < (int)(sizeof(FrameCtr) / 8); i += blockDim.x) dst[i] = __ldcg(src + i);
     __syncthreads();
+    if (threadIdx.x == 0 && (ctr->err_cap | ctr->err_slots | ctr->abort)) ctr->poison = 1ULL;
     reset_ctr_device(ctr);
     __threadfence_system();
 }
@@ -540,9 +590,25 @@ size_t tsdf_elem(const svx_map* m);
 size_t sem_elem(const svx_map* m);
 svx_status reserve_voxels(svx_map* m, int64_t need, cudaStream_t s);
 svx_status reserve_blocks(svx_map* m, int64_t need, cudaStream_t s);
+// Options of a frame run by integrate_impl for an asynchronous frame being
+// re-run: its creation stamp and the pool counts at its first attempt.
+struct FrameOpts {
+    int64_t stamp = -1;          // < 0: a new frame (m->frames, then counted)
+    int64_t nblocks0 = -1, nvox0 = -1;
+    int force_segments = 0;
+};
 svx_status integrate_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n,
                           const PoseParams& pp, const int32_t* labels_in, const void* feats_in,
-                          int feats_f64, cudaStream_t s, svx_report* rep, int device_inputs = 0);
+                          int feats_f64, cudaStream_t s, svx_report* rep, int device_inputs = 0,
+                          const FrameOpts* opt = nullptr);
+svx_status integrate_async_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n,
+                                const PoseParams& pp, const int32_t* labels_in, cudaStream_t s,
+                                int device_inputs, uint64_t* ticket);
+svx_status report_wait(svx_map* m, uint64_t ticket, svx_report* out);
+// Finish every asynchronous frame in flight (every other entry point calls
+// it first, so the map it reads is the map after all submitted frames).
+svx_status drain(svx_map* m);
+void release_async(svx_map* m);
 
 // ---- launchers implemented in the .cu files ---------------------------------
 // svx_march.cu: K1 walk (+ dense-row scan) and the gate
@@ -572,7 +638,7 @@ size_t huge_info_bytes();
 void init_row_space(svx_map* m, int64_t n);
 svx_status reserve_frame(svx_map* m, int64_t n, cudaStream_t s);
 svx_status reserve_pools(svx_map* m, cudaStream_t s);
-void reset_ctr(svx_map* m);
+void reset_ctr(svx_map* m, int64_t stamp);
 svx_status recover_capacity(svx_map* m, int64_t nblocks0, cudaStream_t s);
 svx_status recover_slots(svx_map* m, int64_t nblocks0, cudaStream_t s);
 svx_status clean_ctr(svx_map* m, cudaStream_t s);

@@ -315,6 +315,21 @@ __device__ __forceinline__ void finish_walk(const Tally& t, MarchPartial*, Frame
 #endif
 }
 
+// Asynchronous frames with device inputs: the frame's own copy of its
+// points / labels (a frame that has to be re-run after a pool or slot
+// overflow is re-run from it, whatever the caller did to its buffers since).
+template <class P>
+__device__ __forceinline__ void stage_inputs(const FrameParams& fp, int sem_kind) {
+    const long long n = fp.n;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    const long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const P* src = (const P*)fp.pts;
+    P* dst = (P*)fp.stage_pts;
+    for (long long e = t0; e < 3 * n; e += stride) dst[e] = src[e];
+    if (sem_kind == SVX_SEM_CLOSED)
+        for (long long e = t0; e < n; e += stride) fp.stage_lab[e] = fp.labels[e];
+}
+
 // K1 (bounded bands): compute-only walk over 128-ray tiles.  Each ray's row
 // keys are staged in shared memory; a block scan packs the tile's rows and
 // one atomic per tile reserves their place in the dense row arrays, which
@@ -364,7 +379,9 @@ __global__ void __launch_bounds__(kTileRays, SVX_WALK_MINB) k_walk(MarchParams m
     unsigned char* s_own = reinterpret_cast<unsigned char*>(s_keys + (size_t)kTileRays * maxrows);
     const double ox = fp.pp.t[0], oy = fp.pp.t[1], oz = fp.pp.t[2];
     Tally t;
-    const long long tiles = (n + kTileRays - 1) / kTileRays;
+    if (fp.stage_pts) stage_inputs<P>(fp, sem_kind);
+    // queued behind a frame that needs the host: stage only (the gate aborts)
+    const long long tiles = s_ctr_.poison ? 0 : (n + kTileRays - 1) / kTileRays;
     for (long long tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
         const long long i = tile * kTileRays + threadIdx.x;
         int rows = 0;
@@ -567,7 +584,7 @@ __global__ void __launch_bounds__(kMarchThreads) k_walk_write(MarchParams mp,
 // the reason after the frame.
 __device__ void gate_body(FrameCtr* ctr) {
     volatile FrameCtr* c = ctr;
-    int ab = c->err_budget | c->err_pack | c->err_rows;
+    int ab = c->err_budget | c->err_pack | c->err_rows | (c->poison ? 1 : 0);
     const unsigned long long rows = c->rows;
     if (rows > c->p.rcap) {
         ctr->err_cap = 1;

@@ -48,7 +48,8 @@ __global__ void __launch_bounds__(kResolveThreads, 6) k_resolve(
     const FrameCtr* cv = &s_ctr_;
     unsigned tcount = 0u;   // this CTA's touched entries (same value in every thread)
     if (cv->abort) {
-        if (threadIdx.x == 0) ra.rcount[blockIdx.x] = 0u;
+        // (a poisoned frame keeps the failed frame's touched regions for its cleanup)
+        if (threadIdx.x == 0 && !cv->poison) ra.rcount[blockIdx.x] = 0u;
         return;
     }
     const FrameParams& fp = cv->p;

@@ -291,7 +291,7 @@ svx_status shard_march(svx_map* m, const void* pts_in, int pts_f64, int64_t n, c
     m->shard_feat = nullptr;
     FrameCtr* hc = m->h_ctr;
     if (n == 0) {
-        reset_ctr(m);
+        reset_ctr(m, m->frames);
         fill_summary(m, out);
         m->shard_phase = 1;
         return SVX_OK;
@@ -309,7 +309,7 @@ svx_status shard_march(svx_map* m, const void* pts_in, int pts_f64, int64_t n, c
         if (attempt >= 8) return fail(SVX_E_INTERNAL, "frame scratch could not be sized");
         SVX_TRY(reserve_frame(m, n, s));
         m->frame_slots = 0;   // shard rows travel without d / labels; owners use segments
-        reset_ctr(m);
+        reset_ctr(m, m->frames);
         FrameParams& p = hc->p;
         p.pts = pts;
         p.labels = (const int32_t*)labv;
@@ -500,8 +500,9 @@ svx_status shard_apply(svx_map* m, const void* recv, const int64_t* recv_bytes, 
     const int64_t nblocks0 = m->nblocks, nvox0 = m->nvox;
     FrameCtr* hc = m->h_ctr;
     if (R == 0) {   // nothing owned here this frame
-        reset_ctr(m);
+        reset_ctr(m, m->frames);
         finish_frame(m, nblocks0, nvox0, r);
+        m->frames++;
         m->shard_phase = 0;
         if (rep) *rep = r;
         return SVX_OK;
@@ -539,7 +540,7 @@ svx_status shard_apply(svx_map* m, const void* recv, const int64_t* recv_bytes, 
     for (int attempt = 0;; ++attempt) {
         if (attempt >= 8) return fail(SVX_E_INTERNAL, "frame scratch could not be sized");
         SVX_TRY(reserve_pools(m, s));
-        reset_ctr(m);
+        reset_ctr(m, m->frames);
         FrameParams& p = hc->p;
         p.pts = nullptr;
         p.labels = m->cfg.sem_kind == SVX_SEM_CLOSED ? ptr<int32_t>(m->in_lab) : nullptr;
@@ -573,6 +574,7 @@ svx_status shard_apply(svx_map* m, const void* recv, const int64_t* recv_bytes, 
     SVX_CUDA(cudaEventElapsedTime(&ms, m->ev0, m->ev1));
     r.kernel_ms = ms;
     finish_frame(m, nblocks0, nvox0, r);
+    m->frames++;
     m->shard_phase = 0;
     if (rep) *rep = r;
     return SVX_OK;

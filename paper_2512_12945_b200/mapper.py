@@ -12,6 +12,7 @@ current stream).
 
 from __future__ import annotations
 
+import collections
 import ctypes
 import dataclasses
 import hashlib
@@ -61,7 +62,40 @@ class IntegrationReport:
     new_voxels: int = 0
 
     def as_dict(self):
-        return dict(self.__dict__)
+        return {f.name: getattr(self, f.name) for f in dataclasses.fields(IntegrationReport)}
+
+
+_REPORT_FIELDS = frozenset(f.name for f in dataclasses.fields(IntegrationReport))
+_RESOLVE_AFTER = 32   # pending reports older than this many frames are fetched (64 are held)
+
+
+class _PendingReport(IntegrationReport):
+    """The report of a frame still in flight (svx_integrate_async): its
+    fields are fetched with svx_report_wait on first access, so reading one
+    waits for that frame (and only for the frames before it)."""
+
+    def __init__(self, mapper, ticket):
+        object.__setattr__(self, "_mapper", mapper)
+        object.__setattr__(self, "_ticket", ticket)
+
+    def __getattribute__(self, name):
+        if name in _REPORT_FIELDS and object.__getattribute__(self, "_mapper") is not None:
+            object.__getattribute__(self, "_resolve")()
+        return object.__getattribute__(self, name)
+
+    def _resolve(self):
+        m = object.__getattribute__(self, "_mapper")
+        if m is None:
+            return
+        rep = _lib.SvxReport()
+        check(lib.svx_report_wait(m._handle, object.__getattribute__(self, "_ticket"),
+                                  ctypes.byref(rep)))
+        for f in ("points_in", "points_used", "skipped_nonfinite", "skipped_range",
+                  "skipped_degenerate", "skipped_bad_label", "band_hits", "touched_voxels",
+                  "kernel_ms", "new_blocks", "new_voxels"):
+            object.__setattr__(self, f, getattr(rep, f))
+        object.__setattr__(self, "prep_ms", 0.0)
+        object.__setattr__(self, "_mapper", None)
 
 
 @dataclass
@@ -350,6 +384,13 @@ class Mapper:
         self._handle = h
         self._rep = _lib.SvxReport()
         self._rep_ref = ctypes.byref(self._rep)
+        # asynchronous frames (closed-set / geometry maps): Mapper.integrate's
+        # fast paths submit the frame and return a report read on first use
+        self._async = int(self._engine.async_frames) if open_set is None else 0
+        check(lib.svx_set_async(h, self._async, int(self._engine.async_leaf_headroom)))
+        self._pending = collections.deque()
+        self._ticket = ctypes.c_uint64()
+        self._ticket_ref = ctypes.byref(self._ticket)
         self._tsdf_view = GridView(self, KIND_TSDF)
         self._sem_view = None
         if closed is not None:
@@ -479,6 +520,8 @@ class Mapper:
             return None
         code = (SVX_F64 if dt is torch.float64 else SVX_F32) | _lib.DEVICE_INPUTS | _lib.POSE_CHECK
         stream = ctypes.c_void_p(torch._C._cuda_getCurrentRawStream(self._device))
+        if self._async:
+            return self._submit(points.data_ptr() if n else None, code, n, pose, lab_ptr, stream)
         st = lib.svx_integrate(self._handle, points.data_ptr() if n else None, code, n,
                                pose.ctypes.data, lab_ptr, None, SVX_F32, stream, self._rep_ref)
         if st == _lib.POSE_NEEDS_HOST:
@@ -492,6 +535,22 @@ class Mapper:
             skipped_degenerate=rep.skipped_degenerate, skipped_bad_label=rep.skipped_bad_label,
             band_hits=rep.band_hits, touched_voxels=rep.touched_voxels,
             kernel_ms=rep.kernel_ms, new_blocks=rep.new_blocks, new_voxels=rep.new_voxels)
+
+    def _submit(self, pts_ptr, code, n, pose, lab_ptr, stream):
+        """svx_integrate_async: the frame is queued; its report is fetched on
+        first use (or here, once it is _RESOLVE_AFTER frames old)."""
+        st = lib.svx_integrate_async(self._handle, pts_ptr, code, n, pose.ctypes.data, lab_ptr,
+                                     stream, self._ticket_ref)
+        if st == _lib.POSE_NEEDS_HOST:
+            return None
+        check(st)
+        self._frames += 1
+        rep = _PendingReport(self, self._ticket.value)
+        pend = self._pending
+        pend.append(rep)
+        while len(pend) > _RESOLVE_AFTER:
+            pend.popleft()._resolve()
+        return rep
 
     def _integrate_fast_host(self, points, pose, labels):
         """_integrate_fast for host numpy arrays: the library copies them to
@@ -513,6 +572,8 @@ class Mapper:
                 or not pose.flags.c_contiguous:
             return None
         code = (SVX_F64 if dt == np.float64 else SVX_F32) | _lib.POSE_CHECK
+        if self._async:
+            return self._submit(points.ctypes.data if n else None, code, n, pose, lab_ptr, None)
         st = lib.svx_integrate(self._handle, points.ctypes.data if n else None, code, n,
                                pose.ctypes.data, lab_ptr, None, SVX_F32, None, self._rep_ref)
         if st == _lib.POSE_NEEDS_HOST:
