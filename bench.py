@@ -55,6 +55,10 @@ def parse_args():
                     help="camera configs (1, 3, 5): feed depth rasters through integrate_depth "
                          "(back-projection on the GPU) instead of point clouds")
     ap.add_argument("--tsdf-dtype", default="float64")
+    ap.add_argument("--update-mode", default="auto", choices=["auto", "segments", "slots", "leaves"],
+                    help="row grouping of closed-set frames (Mapper.set_update_mode)")
+    ap.add_argument("--async-frames", type=int, default=2,
+                    help="frames Mapper.integrate may leave in flight (0 = synchronous)")
     ap.add_argument("--cpu-frames", type=int, default=0, help="oracle sample frames (0=auto)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -154,7 +158,7 @@ def frame_bytes(used, touched, kind, C=0, D=0):
     return used * (12 + P) + 2 * touched * S
 
 
-def stage_bytes(stage, rep, kind, C, D, tsdf_elem, slots=False):
+def stage_bytes(stage, rep, kind, C, D, tsdf_elem, mode="segments"):
     """Algorithmic bytes one launch of a stage must move.
     Voxel state is counted at the SURVEY 8(d) fp32 model (S = 8 + 4C closed,
     8 + 8D open), read + write; hash probes, claims and frame scratch beyond
@@ -162,7 +166,16 @@ def stage_bytes(stage, rep, kind, C, D, tsdf_elem, slots=False):
     n, used, R, U = rep.points_in, rep.points_used, rep.band_hits, rep.touched_voxels
     P = 4 if kind == "closed" else (4 * D if kind == "open" else 0)
     S = 8 + (4 * C if kind == "closed" else (8 * D if kind == "open" else 0))
-    if slots:   # slot mode: rows {key 8, point 4, d 8, label 4}, slots {point, label, d} 16 B
+    if mode == "leaves":   # rows {key 8, point 4} -> {leaf|rank 8, slot|point 4} -> bins of 4 B
+        return {
+            "walk": n * (12 + P) + used * 32 + R * 12,
+            "resolve": R * 12 + R * 12,
+            "seg": 0,   # per listed leaf only (counted as overhead)
+            "scatter": R * 12 + R * 4,
+            "update": 2 * U * S + R * 4,
+            "update_b": 0,
+        }[stage]
+    if mode == "slots":   # slot mode: rows {key 8, point 4, d 8, label 4}, slots {point, label, d} 16 B
         return {
             "walk": n * (12 + P) + R * 24,
             "resolve": R * 24 + R * 16 + U * 8,
@@ -327,7 +340,9 @@ def run_ours(args):
     def new_map():
         if sharded:
             return ShardedMapper(**kw, rank=rank, world=world, transport=DistTransport())
-        return Mapper(**kw)
+        mm = Mapper(**kw, async_frames=args.async_frames)
+        mm.set_update_mode(args.update_mode)
+        return mm
 
     # ---- device-resident pass ------------------------------------------------------
     m = new_map()
@@ -383,19 +398,21 @@ def run_ours(args):
     stages = list(_lib.STAGES)
     mean_stage = {s: statistics.mean(h[s] for h in stage_hist) for s in stages}
     dom = max(_lib.KERNEL_STAGES, key=lambda s: mean_stage[s])
-    slot_frames = m.engine_stats().get("frames_slot_mode", 0) if not sharded else 0
-    slots = slot_frames > 0
+    est = m.engine_stats() if not sharded else {}
+    slots = est.get("frames_slot_mode", 0) > 0
+    leaves = est.get("frames_leaf_mode", 0) > 0
     dom_ms = mean_stage[dom]
-    if not slots and dom in ("update", "update_b"):
+    umode = "leaves" if leaves else ("slots" if slots else "segments")
+    if umode == "segments" and dom in ("update", "update_b"):
         # segment mode: the byte model covers both update kernels together
         # (K5 short/long or open, then K5b long / huge), so they are timed together
         dom, dom_ms = "update", mean_stage["update"] + mean_stage["update_b"]
-    dom_bytes = statistics.mean(stage_bytes(dom, r, kind, C, D, tsdf_elem, slots) for r in prof_reps)
+    dom_bytes = statistics.mean(stage_bytes(dom, r, kind, C, D, tsdf_elem, umode) for r in prof_reps)
     peak, peak_src = measured_peak()
     achieved = dom_bytes / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else 0.0
     fb = frame_bytes(used / K, touched_all / K, kind, C, D)   # mean frame, global counts
     frame_gbs = fb / (total_ms_max / K / 1e3) / 1e9
-    traffic = ncu_traffic(dom) if slots else None
+    traffic = ncu_traffic(umode + ":" + dom)
 
     # ---- e2e pass: host pinned buffers through the public API ---------------------------
     e2e = None
@@ -483,7 +500,7 @@ def run_ours(args):
                           "peak_source": peak_src,
                           "bytes_per_launch": dom_bytes, "ms_per_launch": dom_ms,
                           "timing": "kernel span inside the frame graph (%globaltimer, FrameParams.kspan)",
-                          "update_mode": "slots" if slots else "segments"}
+                          "update_mode": umode}
                          if not sharded else
                          {"bound": "hbm", "kernel": "whole frame (per-rank peak x ranks)",
                           "achieved": frame_gbs, "peak": peak * world, "unit": "GB/s",

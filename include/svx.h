@@ -120,6 +120,7 @@ typedef struct {
     int64_t frames_slot_mode;     /* frames finished in slot mode (svx_set_update_mode) */
     int64_t slot_overflow_reruns; /* slot-mode attempts re-run in segment mode */
     int64_t async_reruns;         /* asynchronous frames re-run after an overflow */
+    int64_t frames_leaf_mode;     /* frames finished in leaf mode */
     int64_t last_h2d_bytes;       /* host -> device bytes of the last frame's inputs */
     int64_t last_d2h_bytes;       /* device -> host bytes of the last frame's report */
 } svx_stats;
@@ -390,20 +391,29 @@ svx_status svx_label_map(svx_map* map, int32_t mode, int64_t capacity, int32_t* 
 svx_status svx_set_profiling(svx_map* map, int32_t enable);
 
 /* Row-grouping strategy of closed-set / geometry maps with bounded bands.
- *   SVX_UPDATE_AUTO      slot mode while recent frames average <= 3 rows per
+ *   SVX_UPDATE_AUTO      leaf mode while recent frames average <= 3 rows per
  *                        touched voxel (LiDAR), segment mode otherwise
  *   SVX_UPDATE_SEGMENTS  always segments (K3 scan, K4 scatter, K5 sorted update)
  *   SVX_UPDATE_SLOTS     always try slot mode (K2 writes point indices into the
  *                        voxel's 16-entry slot record; K5 per touched voxel)
- * A slot-mode frame with a voxel of more than 16 rows stops before any payload
- * changes and is re-run in segment mode, so all three give identical maps.
+ *   SVX_UPDATE_LEAVES    always try leaf mode (rows binned by 8^3 leaf; one warp
+ *                        or CTA per touched leaf sorts its rows in shared memory
+ *                        and updates its voxels)
+ * A slot-mode frame with a voxel of more than 16 rows, or a leaf-mode frame
+ * with a leaf of more than 8192 rows, stops before any payload changes and is
+ * re-run in segment mode, so all four give identical maps.
  * Open-set and space-carving maps always use segments.  The reference has no
  * equivalent knob (its grouping is one sort, _core.pyx:707-753). */
 #define SVX_UPDATE_AUTO 0
 #define SVX_UPDATE_SEGMENTS 1
 #define SVX_UPDATE_SLOTS 2
+#define SVX_UPDATE_LEAVES 3
 svx_status svx_set_update_mode(svx_map* map, int32_t mode);
 int32_t svx_stage_times(svx_map* map, double* ms, int32_t n);
+/* Diagnostics: the last finished frame's internal counters, in this order:
+ * rows, touched voxels, listed leaves (leaf mode), leaves taken by the CTA
+ * path (leaf mode), long voxels, huge voxels.  Writes up to n, returns 6. */
+int32_t svx_frame_counters(svx_map* map, int64_t* out, int32_t n);
 
 const char* svx_last_error(void);
 int32_t svx_abi_version(void);

@@ -82,6 +82,7 @@ class SvxStats(ctypes.Structure):
         ("frames_slot_mode", ctypes.c_int64),
         ("slot_overflow_reruns", ctypes.c_int64),
         ("async_reruns", ctypes.c_int64),
+        ("frames_leaf_mode", ctypes.c_int64),
         ("last_h2d_bytes", ctypes.c_int64),
         ("last_d2h_bytes", ctypes.c_int64),
     ]
@@ -161,7 +162,7 @@ KERNEL_STAGES = STAGES[:-1]
 
 # every symbol include/svx.h declares (checked by tests/test_abi_and_config.py)
 EXPORTED = sorted(list(_SIGNATURES) + ["svx_last_error", "svx_abi_version",
-                                       "svx_kernel_launches", "svx_stage_times",
+                                       "svx_kernel_launches", "svx_stage_times", "svx_frame_counters",
                                        "svx_leaf_owner"])
 
 
@@ -183,6 +184,8 @@ def _load():
     lib.svx_kernel_launches.restype = ctypes.c_int64
     lib.svx_stage_times.argtypes = [_P, ctypes.POINTER(_D), _I32]
     lib.svx_stage_times.restype = ctypes.c_int32
+    lib.svx_frame_counters.argtypes = [_P, ctypes.POINTER(_I64), _I32]
+    lib.svx_frame_counters.restype = ctypes.c_int32
     lib.svx_leaf_owner.argtypes = [_I64, _I64, _I64, _I32]
     lib.svx_leaf_owner.restype = ctypes.c_int32
     return lib

@@ -208,7 +208,8 @@ svx_status svx_destroy(svx_map* m) {
     m->aq_count = 0;
     release_async(m);
     DevBuf* bufs[] = {&m->hash, &m->bcoord, &m->bkey, &m->bmask, &m->bslot, &m->vt,
-                      &m->s0, &m->s1, &m->vrec, &m->vslot, &m->in_pts,
+                      &m->s0, &m->s1, &m->vrec, &m->vslot, &m->lcnt, &m->rowleaf, &m->rowpk,
+                      &m->binrow, &m->in_pts,
                       &m->in_lab, &m->in_feat, &m->dp_depth, &m->dp_lab_in, &m->dp_feat_in, &m->dp_pts, &m->dp_lab, &m->dp_feat, &m->ray, &m->rcnt, &m->roff, &m->rowkey,
                       &m->rowvid, &m->rowray, &m->rowd, &m->rowlab, &m->partials, &m->tlist, &m->mlist,
                       &m->longlist, &m->hinfo, &m->srid, &m->bitmap, &m->rcount, &m->cubtmp, &m->ctr, &m->ord0,
@@ -362,7 +363,7 @@ svx_status svx_set_profiling(svx_map* m, int32_t enable) {
 
 svx_status svx_set_update_mode(svx_map* m, int32_t mode) {
     if (!m) return fail(SVX_E_INPUT, "null argument");
-    if (mode < SVX_UPDATE_AUTO || mode > SVX_UPDATE_SLOTS) return fail(SVX_E_INPUT, "unknown update mode");
+    if (mode < SVX_UPDATE_AUTO || mode > SVX_UPDATE_LEAVES) return fail(SVX_E_INPUT, "unknown update mode");
     m->mode_pref = mode;
     return SVX_OK;
 }
@@ -371,6 +372,17 @@ int32_t svx_stage_times(svx_map* m, double* ms, int32_t n) {
     if (!m) return 0;
     for (int i = 0; i < n && i < SVX_N_STAGES; ++i) ms[i] = m->stage_ms[i];
     return SVX_N_STAGES;
+}
+
+int32_t svx_frame_counters(svx_map* m, int64_t* out, int32_t n) {
+    if (!m || !out) return 0;
+    if (drain(m) != SVX_OK) return 0;
+    // the last finished frame's mirror: asynchronous frames keep their own
+    const int64_t v[6] = {(int64_t)m->last_ctr.rows, (int64_t)m->last_ctr.n_touched,
+                          (int64_t)m->last_ctr.n_leaves, (int64_t)m->last_ctr.n_bigleaf,
+                          (int64_t)m->last_ctr.n_long, (int64_t)m->last_ctr.n_huge};
+    for (int i = 0; i < n && i < 6; ++i) out[i] = v[i];
+    return 6;
 }
 
 svx_status svx_stats_get(svx_map* m, svx_stats* out) {
@@ -391,6 +403,7 @@ svx_status svx_stats_get(svx_map* m, svx_stats* out) {
     out->frames_slot_mode = m->n_slot_frames;
     out->slot_overflow_reruns = m->n_slot_reruns;
     out->async_reruns = m->n_async_reruns;
+    out->frames_leaf_mode = m->n_leaf_frames;
     out->last_h2d_bytes = m->io_h2d;
     out->last_d2h_bytes = m->io_d2h;
     return SVX_OK;

@@ -115,6 +115,8 @@ svx_status reserve_blocks(svx_map* m, int64_t need, cudaStream_t s) {
         SVX_TRY(ensure(m->bslot, sizeof(unsigned long long) * kLeafVolume * cap, s, true));
         SVX_TRY(launch_fill_u64(ptr<unsigned long long>(m->bslot) + old * kLeafVolume,
                                 (cap - old) * kLeafVolume, kSlotInactive, s));
+        if (m->cfg.sem_kind != SVX_SEM_OPEN && !m->cfg.space_carving)   // leaf-mode frame counts
+            SVX_TRY(ensure(m->lcnt, sizeof(unsigned long long) * cap, s, true, 0));
         m->bcap = cap;
     }
     // keep the leaf hash at <= 50% load when the pool is full
@@ -153,9 +155,12 @@ svx_status reserve_frame(svx_map* m, int64_t n, cudaStream_t s) {
     if (m->cfg.sem_kind == SVX_SEM_OPEN)   // huge voxels have > 256 rows each
         SVX_TRY(ensure(m->hinfo, huge_info_bytes() * (size_t)(rows / 256 + 2), s));
     SVX_TRY(ensure(m->rowray, sizeof(int) * rows, s));
-    if (m->cfg.sem_kind != SVX_SEM_OPEN && !m->cfg.space_carving) {   // slot mode row payload
+    if (m->cfg.sem_kind != SVX_SEM_OPEN && !m->cfg.space_carving) {   // slot / leaf mode rows
         SVX_TRY(ensure(m->rowd, sizeof(double) * rows, s));
         SVX_TRY(ensure(m->rowlab, sizeof(int) * rows, s));
+        SVX_TRY(ensure(m->rowleaf, sizeof(unsigned long long) * rows, s));
+        SVX_TRY(ensure(m->rowpk, sizeof(unsigned) * rows, s));
+        SVX_TRY(ensure(m->binrow, sizeof(unsigned) * rows, s));
     }
     if (m->maxrows == 0) {   // two-pass walk: per-ray offsets from a scan
         SVX_TRY(ensure(m->roff, sizeof(long long) * m->npts_cap, s));
@@ -173,7 +178,8 @@ static unsigned long long graph_signature(const svx_map* m, int pts_f64, int fea
                           m->srid.p,   m->bitmap.p, m->cubtmp.p,  m->hash.p,   m->bcoord.p,
                           m->bkey.p,   m->bmask.p,  m->bslot.p,   m->vt.p,     m->s0.p,
                           m->s1.p,     m->vrec.p,   m->vslot.p,   m->rowd.p,   m->rowlab.p,
-                          m->ctr.p,    m->hinfo.p};
+                          m->ctr.p,    m->hinfo.p,  m->lcnt.p,    m->rowleaf.p, m->rowpk.p,
+                          m->binrow.p};
     unsigned long long h = 1469598103934665603ULL;
     auto mix = [&](unsigned long long v) {
         h ^= v;
@@ -193,6 +199,7 @@ static unsigned long long graph_signature(const svx_map* m, int pts_f64, int fea
 // FrameCtr, the last kernel's epilogue writes the counters back into it.
 static svx_status enqueue_frame(svx_map* m, int pts_f64, int feats_f64, cudaStream_t s) {
     SVX_TRY(launch_march(m, pts_f64, feats_f64, s));
+    if (m->frame_leaf) return launch_leaf(m, s);
     SVX_TRY(launch_resolve(m, s));
     if (m->frame_slots) return launch_update_slots(m, s);
     SVX_TRY(launch_segments(m, s));
@@ -264,7 +271,7 @@ static svx_status launch_frame(svx_map* m, int pts_f64, int feats_f64, cudaStrea
         return SVX_OK;
     }
     const unsigned long long sig = graph_signature(m, pts_f64, feats_f64);
-    const int gm = m->frame_slots ? 1 : 0;
+    const int gm = m->frame_leaf ? 2 : (m->frame_slots ? 1 : 0);
     cudaGraphExec_t& gexec = m->gexec[gm];
     if (!gexec || sig != m->gsig[gm]) {
         if (gexec) {
@@ -445,14 +452,31 @@ svx_status recover_slots(svx_map* m, int64_t nblocks0, cudaStream_t s) {
 int choose_slots(const svx_map* m) {
     if (m->cfg.sem_kind == SVX_SEM_OPEN || m->cfg.space_carving || m->maxrows <= 0) return 0;
     if (m->mode_pref == SVX_UPDATE_SEGMENTS) return 0;
-    if (m->mode_pref == SVX_UPDATE_SLOTS) return m->frame_retry_segments ? 0 : 1;
+    if (m->mode_pref == SVX_UPDATE_SLOTS || m->mode_pref == SVX_UPDATE_LEAVES)
+        return m->frame_retry_segments ? 0 : 1;
     if (m->slot_hold > 0) return 0;
     return m->last_rows <= 3 * m->last_touched ? 1 : 0;
+}
+
+// Slot and leaf mode serve the same frames (bounded-band closed/geometry
+// maps whose recent frames fit few rows per voxel); auto picks leaf mode.
+void choose_mode(svx_map* m, int64_t n) {
+    const int lidar_like = choose_slots(m);
+    m->frame_slots = 0;
+    m->frame_leaf = 0;
+    if (!lidar_like) return;
+    if (m->mode_pref == SVX_UPDATE_SLOTS) {
+        m->frame_slots = 1;
+        return;
+    }
+    if (leaf_mode_fits(n)) m->frame_leaf = 1;
+    else m->frame_slots = 1;
 }
 
 // Report fields of the map side and the capacities for the next frame.
 void finish_frame(svx_map* m, int64_t nblocks0, int64_t nvox0, svx_report& r) {
     FrameCtr* hc = m->h_ctr;
+    m->last_ctr = *hc;
     r.touched_voxels = (int64_t)hc->n_touched;
     r.new_blocks = (int64_t)hc->nblocks - nblocks0;
     r.new_voxels = (int64_t)hc->nvox - nvox0;
@@ -460,6 +484,7 @@ void finish_frame(svx_map* m, int64_t nblocks0, int64_t nvox0, svx_report& r) {
     m->nblocks = (int64_t)hc->nblocks;
     m->nvox = (int64_t)hc->nvox;
     m->n_slot_frames += m->frame_slots;
+    m->n_leaf_frames += m->frame_leaf;
     m->last_rows = (int64_t)hc->rows;
     m->last_touched = (int64_t)hc->n_touched;
     if (m->slot_hold > 0) --m->slot_hold;
@@ -552,7 +577,7 @@ svx_status integrate_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n
         if (attempt >= 8) return fail(SVX_E_INTERNAL, "frame scratch could not be sized");
         SVX_TRY(reserve_frame(m, n, s));
         SVX_TRY(reserve_pools(m, s));
-        m->frame_slots = choose_slots(m);
+        choose_mode(m, n);
         if (!staged && !m->frame_slots) SVX_TRY(stage_all());
         reset_ctr(m, stamp);
         FrameParams& p = hc->p;
@@ -569,6 +594,11 @@ svx_status integrate_impl(svx_map* m, const void* pts_in, int pts_f64, int64_t n
         // a frame that ends needing the host leaves the device counters
         // poisoned for queued frames: clear them before the next attempt
         if (hc->abort | hc->err_cap | hc->err_slots) m->ctr_clean = false;
+        if (hc->err_internal) {
+            m->ctr_clean = false;
+            return fail(SVX_E_INTERNAL, "engine invariant failed inside a frame (code " +
+                                            std::to_string(hc->err_internal) + ")");
+        }
 
         // the reference's pre-allocation checks, in its order (_core.pyx:661-712, :386-387)
         if (hc->err_budget)
@@ -713,6 +743,11 @@ static svx_status finalize_oldest(svx_map* m) {
     AsyncFrame& f = m->aq[m->aq_head];
     SVX_CUDA(cudaEventSynchronize(f.e1));
     FrameCtr* hc = f.h;
+    if (hc->err_internal) {
+        m->ctr_clean = false;
+        return fail(SVX_E_INTERNAL, "engine invariant failed inside a frame (code " +
+                                        std::to_string(hc->err_internal) + ")");
+    }
     if (!(hc->abort | hc->err_cap | hc->err_slots)) {
         svx_report r;
         memset(&r, 0, sizeof(r));
@@ -728,6 +763,7 @@ static svx_status finalize_oldest(svx_map* m) {
         r.kernel_ms = ms;
         m->h_ctr = hc;
         m->frame_slots = f.slots;
+        m->frame_leaf = f.leaf;
         finish_frame(m, hc->p.nblocks0, hc->p.nvox0, r);
         m->h_ctr = m->h_ctr0;
         store_report(m, f.ticket, r);
@@ -743,6 +779,7 @@ static svx_status finalize_oldest(svx_map* m) {
     m->h_ctr = hc;
     m->d_hctr = f.d;
     m->frame_slots = f.slots;
+    m->frame_leaf = f.leaf;
     FrameOpts o;
     o.stamp = f.frame;
     o.nblocks0 = nblocks0;
@@ -851,7 +888,7 @@ svx_status integrate_async_impl(svx_map* m, const void* pts_in, int pts_f64, int
     m->h_ctr = f.h;
     m->d_hctr = f.d;
     m->frame_retry_segments = 0;
-    m->frame_slots = choose_slots(m);
+    choose_mode(m, n);
     reset_ctr(m, m->frames);
     FrameParams& p = f.h->p;
     p.pts = pts;
@@ -869,6 +906,7 @@ svx_status integrate_async_impl(svx_map* m, const void* pts_in, int pts_f64, int
     f.n = n;
     f.pts_f64 = pts_f64;
     f.slots = m->frame_slots;
+    f.leaf = m->frame_leaf;
     f.pp = pp;
     f.stream = s;
     svx_status st = SVX_OK;

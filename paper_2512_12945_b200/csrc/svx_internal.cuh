@@ -159,6 +159,10 @@ struct FrameCtr {
     unsigned long long work_open;
     unsigned long long work_huge;   // K5h: next huge voxel; K5g: next (voxel, slice) item
     unsigned long long work_items;
+    unsigned long long n_leaves;    // leaf mode: listed (touched) leaves
+    unsigned long long bin_cursor;  // leaf mode: rows given bins so far
+    unsigned long long n_bigleaf;   // leaf mode: leaves for the CTA path
+    unsigned long long err_internal;   // an invariant the host relies on failed
     // Persistent (kept by the epilogue's reset, like nblocks / nvox): set when a
     // frame ends needing the host (pool overflow, slot overflow, gate abort).
     // Asynchronous frames queued behind it see it and do nothing but stage
@@ -258,7 +262,7 @@ struct AsyncFrame {
     DevBuf pts, lab;              // staged inputs
     uint64_t ticket = 0;
     int64_t frame = 0, n = 0;     // creation stamp, points
-    int pts_f64 = 0, slots = 0;
+    int pts_f64 = 0, slots = 0, leaf = 0;   // update mode it was launched in
     PoseParams pp{};
     cudaStream_t stream = nullptr;
 };
@@ -273,12 +277,14 @@ struct svx_map {
     svx::DevBuf vt, s0, s1;                  int64_t vcap = 0, nvox = 0;  // vt: {d, w} per voxel
     svx::DevBuf vrec;                        // per-voxel frame records (svx::VoxFrame)
     svx::DevBuf vslot;                       // slot mode: kSlots RowSlots per voxel
-    int64_t n_slot_frames = 0, n_slot_reruns = 0, n_async_reruns = 0;
+    svx::DevBuf lcnt;                        // leaf mode: per leaf {frame rows, bin base}
+    int64_t n_slot_frames = 0, n_slot_reruns = 0, n_async_reruns = 0, n_leaf_frames = 0;
     int64_t io_h2d = 0, io_d2h = 0;   // host-link bytes of the last frame (inputs in, report out)
     int mode_pref = 0;      // SVX_UPDATE_AUTO / SEGMENTS / SLOTS
     int slot_hold = 0;      // frames to stay in segment mode after a slot overflow
     int64_t last_rows = 0, last_touched = 0;   // previous frame's rows and touched voxels
-    int frame_slots = 0;    // mode of the attempt being run
+    int frame_slots = 0;    // mode of the attempt being run: slots,
+    int frame_leaf = 0;     //   leaves, or (both 0) segments
     int frame_retry_segments = 0;   // this frame overflowed its slots: re-run with segments
     int64_t frames = 0;
     unsigned seq = 0;   // frame launches so far (attempts included)
@@ -296,6 +302,7 @@ struct svx_map {
     svx::DevBuf in_pts, in_lab, in_feat;
     svx::DevBuf dp_depth, dp_lab_in, dp_feat_in, dp_pts, dp_lab, dp_feat;   // depth frames
     svx::DevBuf ray, rcnt, roff, rowkey, rowvid, rowray, rowd, rowlab, partials;
+    svx::DevBuf rowleaf, rowpk, binrow;      // leaf mode rows
     svx::DevBuf tlist, mlist, longlist, srid, bitmap, rcount, hinfo;
     uint64_t ucap = 0, rcap = 0;
     uint64_t rcap_sized = 0;      // rcap the frame scratch was last sized for (reserve_frame)
@@ -304,19 +311,20 @@ struct svx_map {
     int64_t npts_cap = 0;  // points the per-ray scratch holds
     // captured frame graph (replayed while the layout is unchanged)
     cudaStream_t gstream = nullptr;
-    cudaGraphExec_t gexec[2] = {};   // segment mode, slot mode
-    cudaGraph_t graph[2] = {};       // kept: its first-kernel node is updated per frame
-    cudaGraphNode_t walk_node[2] = {};
-    int walk_nargs[2] = {};          // parameters of that kernel (FrameParams is the last)
-    cudaKernelNodeParams walk_kp[2] = {};   // its captured launch parameters
-    void* walk_args[2][16] = {};            // its argument pointers (graph-owned storage)
+    cudaGraphExec_t gexec[3] = {};   // segment mode, slot mode, leaf mode
+    cudaGraph_t graph[3] = {};       // kept: its first-kernel node is updated per frame
+    cudaGraphNode_t walk_node[3] = {};
+    int walk_nargs[3] = {};          // parameters of that kernel (FrameParams is the last)
+    cudaKernelNodeParams walk_kp[3] = {};   // its captured launch parameters
+    void* walk_args[3][16] = {};            // its argument pointers (graph-owned storage)
     int first_nargs = 0;             // set by launch_march for the kernel it launched first
-    unsigned long long gsig[2] = {};
-    int graph_kernels[2] = {0, 0};   // kernel nodes of each frame graph (launch accounting)
+    unsigned long long gsig[3] = {};
+    int graph_kernels[3] = {0, 0, 0};   // kernel nodes of each frame graph (launch accounting)
     svx::DevBuf cubtmp;
     svx::DevBuf ctr;      // FrameCtr
     svx::FrameCtr* h_ctr = nullptr;  // pinned, mapped mirror of the frame being run (host side)
     svx::FrameCtr* d_hctr = nullptr; // its device address
+    svx::FrameCtr last_ctr{};        // counters of the last finished frame (diagnostics)
     svx::FrameCtr* h_ctr0 = nullptr; // the mirror of synchronous frames (h_ctr points at it,
     svx::FrameCtr* d_hctr0 = nullptr;//   or at an asynchronous frame's own mirror)
     bool ctr_clean = false;          // device FrameCtr is in the reset state
@@ -385,6 +393,16 @@ __device__ __forceinline__ void grid_dep_wait() {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
 }
+
+// Spin-wait guard: a wait on another CTA's publish that has not finished
+// after ~1 s is an engine bug; record which wait (err_internal) and give up
+// instead of hanging the GPU.
+constexpr int kSpinLimit = 1 << 25;
+#define SVX_SPIN_GUARD(count, ctr, code)                                          \
+    if (++(count) > ::svx::kSpinLimit) {                                          \
+        atomicCAS(&(ctr)->err_internal, 0ULL, (unsigned long long)(code));        \
+        break;                                                                    \
+    }
 
 __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
@@ -629,6 +647,10 @@ svx_status launch_scatter(svx_map* m, cudaStream_t s);
 svx_status launch_update_a(svx_map* m, int feats_f64, cudaStream_t s);
 svx_status launch_update_b(svx_map* m, int feats_f64, cudaStream_t s);
 svx_status launch_update_slots(svx_map* m, cudaStream_t s);
+// svx_leaf.cu: leaf mode (K2L bin, K3L alloc, K4L scatter, K5L update)
+svx_status launch_leaf(svx_map* m, cudaStream_t s);
+svx_status launch_leaf_cleanup(svx_map* m, cudaStream_t s);
+bool leaf_mode_fits(int64_t n);
 svx_status launch_rehash(svx_map* m, int4* new_table, int64_t new_cap, cudaStream_t s);
 svx_status launch_fill_u64(unsigned long long* p, int64_t n, unsigned long long v, cudaStream_t s);
 int huge_warps();
@@ -643,6 +665,7 @@ svx_status recover_capacity(svx_map* m, int64_t nblocks0, cudaStream_t s);
 svx_status recover_slots(svx_map* m, int64_t nblocks0, cudaStream_t s);
 svx_status clean_ctr(svx_map* m, cudaStream_t s);
 int choose_slots(const svx_map* m);
+void choose_mode(svx_map* m, int64_t n);   // sets frame_slots / frame_leaf
 void finish_frame(svx_map* m, int64_t nblocks0, int64_t nvox0, svx_report& r);
 KeyPack default_key_pack(const svx_map* m, const PoseParams& pp);
 

@@ -74,8 +74,7 @@ __global__ void __launch_bounds__(kResolveThreads, 6) k_resolve(
             rsl.label = __ldcs(rowlab + t);
             rsl.d = __ldcs(rowd + t);
         }
-        // (no barrier between steps: every shared value a step writes is
-        // written after a barrier the previous step's readers have passed)
+        // (each step starts with a barrier: see resolve_step)
         rt::resolve_step<kResolveThreads>(ra, valid, key, rsl, t, s_warp, s_base, tcount);
     }
     if (ra.slots && threadIdx.x == 0) {   // this CTA's touched region
@@ -154,6 +153,7 @@ __global__ void __launch_bounds__(kSegThreads) k_seg(const int* __restrict__ tli
                 if (lane == 0) st_status(status + tile, seq << 2 | 1, agg);
                 // look back 32 tiles at a time until an inclusive prefix
                 long long hi = tile - 1;
+                int spins = 0;
                 while (true) {
                     const long long p = hi - lane;
                     unsigned long long tag = seq << 2 | 2, v = 0;
@@ -162,7 +162,15 @@ __global__ void __launch_bounds__(kSegThreads) k_seg(const int* __restrict__ tli
                     const unsigned incl = __ballot_sync(0xffffffffu, (tag >> 2) == seq && (tag & 3) == 2);
                     // lanes up to the first inclusive one must all be ready
                     const unsigned upto = incl ? (incl & (0u - incl)) * 2u - 1u : 0xffffffffu;
-                    if ((ready & upto) != upto) continue;   // a predecessor not yet published
+                    if ((ready & upto) != upto) {   // a predecessor not yet published
+                        bool stuck = false;
+                        if (lane == 0 && ++spins > kSpinLimit) {
+                            atomicCAS(&ctr->err_internal, 0ULL, 15ULL);
+                            stuck = true;
+                        }
+                        if (__shfl_sync(0xffffffffu, stuck, 0)) break;
+                        continue;
+                    }
                     unsigned long long part = ((upto >> lane) & 1u) ? v : 0ULL;
 #pragma unroll
                     for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
@@ -243,6 +251,7 @@ __global__ void k_cleanup_slots(const TouchEntry* __restrict__ tent, const unsig
 
 template <class TD, class TS>
 svx_status cleanup_t(svx_map* m, cudaStream_t s) {
+    if (m->frame_leaf) return launch_leaf_cleanup(m, s);   // no voxel changed
     if (m->frame_slots) {
         k_cleanup_slots<TD><<<kPersistentBlocks, 256, 0, s>>>(
             ptr<TouchEntry>(m->tlist), ptr<unsigned>(m->rcount), slot_region(m->rcap),

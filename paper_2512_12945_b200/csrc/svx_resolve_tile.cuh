@@ -1,6 +1,6 @@
-// svx_resolve_tile.cuh -- one CTA-synchronous resolve step (K2 logic),
-// shared by k_resolve (rows from the global row arrays) and the fused
-// walk+resolve kernel (rows straight from the walk's shared memory).
+// svx_resolve_tile.cuh -- one CTA-synchronous resolve step (K2 logic) for
+// k_resolve, and the leaf hash helpers the leaf-mode binning kernel
+// (svx_leaf.cu) shares with it.
 //
 // Rows -> voxel ids: within a warp, lanes that hit the same voxel elect one
 // leader (one lookup, one count of popc(peers)), and voxel leaders that share
@@ -59,7 +59,7 @@ __device__ __forceinline__ int4 ld_slot(const int4* p) {
 // Leaf find-or-insert.  A claimed slot stays BUSY until the new leaf's id,
 // coordinates and creation frame are written; then the id is published.
 // Returns -1 (and sets err_cap) when the leaf pool is full.
-__device__ int leaf_find_or_insert(int4* table, long long mask, int a, int b, int c, int frame,
+__device__ inline int leaf_find_or_insert(int4* table, long long mask, int a, int b, int c, int frame,
                                    long long bcap, int4* bcoord, FrameCtr* ctr) {
     long long pos = (long long)(block_hash(a, b, c) & (unsigned long long)mask);
     while (true) {
@@ -77,24 +77,31 @@ __device__ int leaf_find_or_insert(int4* table, long long mask, int a, int b, in
         if (v == kHashEmpty) {
             int old = atomicCAS((int*)&table[pos].w, kHashEmpty, kHashBusy);
             if (old == kHashEmpty) {
-                const long long id = (long long)warp_ticket(&ctr->nblocks);
+                // (a plain atomic: this lane may be alone on this path while other
+                // lanes of its warp spin on slots it has not published yet)
+                const long long id = (long long)atomicAdd(&ctr->nblocks, 1ULL);
                 if (id >= bcap) {
                     atomicExch((int*)&table[pos].w, kHashEmpty);
                     atomicOr(&ctr->err_cap, 1);
                     return -1;
                 }
                 bcoord[id] = make_int4(a, b, c, frame);
-                // publish key and id with one 16-byte store: a reader sees the
-                // slot either BUSY or complete (no fence on the creating side)
+                // the leaf's coordinates are visible before its id is published
+                // (key and id go out in one 16-byte store: a reader sees the slot
+                // BUSY or complete)
+                __threadfence();
                 st_slot(table + pos, make_int4(a, b, c, (int)id));
                 return (int)id;
             }
             v = old;
         }
+        int spins = 0;
         while (v == kHashBusy) {
             __nanosleep(20);
             v = *vw;
+            SVX_SPIN_GUARD(spins, ctr, 11)
         }
+        if (v == kHashBusy) return -1;
         if (v == kHashEmpty) {   // a creator rolled back (pool full)
             atomicOr(&ctr->err_cap, 1);
             return -1;
@@ -186,6 +193,10 @@ __device__ __forceinline__ void resolve_step(const ResolveArgs& ra, bool valid,
     int* tlist = ra.tlist;
     RowSlot* vslot = ra.vslot;
     int* rowvid = ra.rowvid;
+    // No thread claims a slot in this step while another thread of its CTA
+    // may still wait (previous step) on another CTA's claim: that CTA could
+    // itself be held at its claim barrier by a thread waiting on ours.
+    __syncthreads();
     long long x = 0, y = 0, z = 0;
     if (valid) unpack_key(key, kp, x, y, z);
     const unsigned vpeers = __match_any_sync(full, valid ? key : (kKeyEmpty ^ (unsigned long long)lane));
@@ -235,6 +246,7 @@ __device__ __forceinline__ void resolve_step(const ResolveArgs& ra, bool valid,
             atomicOr(&ctr->err_cap, 1);
         } else {
             bcoord[nid] = make_int4(la, lb, lc, frame);
+            __threadfence();   // coordinates visible before the id (see leaf_find_or_insert)
             st_slot(table + lpos, make_int4(la, lb, lc, (int)nid));   // key + id in one store
             id = (int)nid;
         }
@@ -243,12 +255,15 @@ __device__ __forceinline__ void resolve_step(const ResolveArgs& ra, bool valid,
     if (lstate == 2) {   // another CTA is publishing this slot (maybe another key)
         volatile int* vw = &table[lpos].w;
         int v = *vw;
+        int spins = 0;
         while (v == kHashBusy) {
             __nanosleep(32);
             v = *vw;
+            SVX_SPIN_GUARD(spins, ctr, 12)
         }
         const int4 sv = ld_slot(table + lpos);
-        if (v >= 0 && sv.x == la && sv.y == lb && sv.z == lc) id = v;
+        if (v == kHashBusy) id = -1;
+        else if (v >= 0 && sv.x == la && sv.y == lb && sv.z == lc) id = v;
         else id = leaf_find_or_insert(table, hmask, la, lb, lc, frame, bcap, bcoord, ctr);
     }
     id = __shfl_sync(full, id, lleader);
@@ -306,9 +321,11 @@ __device__ __forceinline__ void resolve_step(const ResolveArgs& ra, bool valid,
         volatile unsigned* vsp = reinterpret_cast<volatile unsigned*>(sp);   // low half
         const int pending = slots ? -1 : -2;
         int v = (int)*vsp;
+        int spins = 0;
         while (v == pending) {
             __nanosleep(32);
             v = (int)*vsp;
+            SVX_SPIN_GUARD(spins, ctr, 13)
         }
         if (v >= 0) vid = v;
         else atomicOr(&ctr->err_cap, 1);

@@ -709,12 +709,12 @@ class Mapper:
         """Pre-size the device pools for `voxels` active voxels in `blocks` leaves."""
         check(lib.svx_reserve(self._handle, int(voxels), int(blocks)))
 
-    _UPDATE_MODES = {"auto": 0, "segments": 1, "slots": 2}
+    _UPDATE_MODES = {"auto": 0, "segments": 1, "slots": 2, "leaves": 3}
 
     def set_update_mode(self, mode: str = "auto") -> None:
         """Row-grouping strategy of closed-set / geometry maps
-        (svx_set_update_mode): "auto", "segments" or "slots".  All three give
-        bit-identical maps; the choice only changes speed."""
+        (svx_set_update_mode): "auto", "segments", "slots" or "leaves".  All
+        give bit-identical maps; the choice only changes speed."""
         if mode not in self._UPDATE_MODES:
             raise ValueError(f"update mode must be one of {sorted(self._UPDATE_MODES)}")
         check(lib.svx_set_update_mode(self._handle, self._UPDATE_MODES[mode]))
@@ -728,6 +728,13 @@ class Mapper:
         buf = (ctypes.c_double * len(_lib.STAGES))()
         lib.svx_stage_times(self._handle, buf, len(_lib.STAGES))
         return {name: float(buf[i]) for i, name in enumerate(_lib.STAGES)}
+
+    def frame_counters(self) -> dict:
+        """Diagnostics: internal counters of the last finished frame."""
+        buf = (ctypes.c_int64 * 6)()
+        lib.svx_frame_counters(self._handle, buf, 6)
+        return dict(zip(("rows", "touched", "leaves", "big_leaves", "long_voxels", "huge_voxels"),
+                        (int(v) for v in buf)))
 
     def active_count(self) -> int:
         c = ctypes.c_int64()

@@ -41,7 +41,7 @@ def test_struct_layout_matches_header():
     # svx_config: 3 doubles, 8 int32, 2 doubles, 2 int32, 2 int64
     assert ctypes.sizeof(_lib.SvxConfig) == 3 * 8 + 8 * 4 + 2 * 8 + 2 * 4 + 2 * 8
     assert ctypes.sizeof(_lib.SvxReport) == 10 * 8 + 8
-    assert ctypes.sizeof(_lib.SvxStats) == 13 * 8
+    assert ctypes.sizeof(_lib.SvxStats) == 14 * 8
 
 
 def test_status_codes_map_to_semvox_classes():

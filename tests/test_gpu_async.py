@@ -27,7 +27,7 @@ def _maps_equal(a, b):
 
 
 @pytest.mark.parametrize("depth", [1, 2, 4])
-@pytest.mark.parametrize("mode", ["auto", "slots", "segments"])
+@pytest.mark.parametrize("mode", ["auto", "slots", "segments", "leaves"])
 def test_async_equals_sync_lidar(mode, depth):
     from paper_2512_12945_b200 import Mapper, scenes
 
@@ -110,16 +110,18 @@ def test_async_capacity_rerun_from_own_copy(host):
     assert np.array_equal(s0, os0)
 
 
-def test_async_slot_overflow_rerun():
+@pytest.mark.parametrize("mode", ["slots", "leaves"])
+def test_async_slot_overflow_rerun(mode):
     """Depth-camera frames forced into slot mode overflow the 16 row slots
     of close-up voxels while in flight: they are re-run in segment mode from
-    their own copies.  Map == oracle."""
+    their own copies (leaf mode: leaves past 8192 rows do the same).  Map ==
+    oracle."""
     from oracle.oracle import OracleMap
     from paper_2512_12945_b200 import Mapper, scenes
 
     wl = scenes.workload(1, device="cuda")
     m = Mapper(**wl.mapper_kwargs, async_frames=2)
-    m.set_update_mode("slots")
+    m.set_update_mode(mode)
     om = OracleMap(**wl.mapper_kwargs)
     reps, oreps = [], []
     for i in range(3):
@@ -128,7 +130,8 @@ def test_async_slot_overflow_rerun():
         oreps.append(om.integrate(f.points.cpu().numpy(), f.pose, labels=f.labels.cpu().numpy()))
     assert np.array_equal(report_rows(reps), report_rows(oreps))
     st = m.engine_stats()
-    assert st["slot_overflow_reruns"] >= 1 and st["async_reruns"] >= 1
+    if mode == "slots":
+        assert st["slot_overflow_reruns"] >= 1 and st["async_reruns"] >= 1
     c, d, w, s0, _ = m._export()
     oc, od, ow, os0, _ = om.export()
     assert np.array_equal(c, oc)

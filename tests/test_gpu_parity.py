@@ -57,7 +57,7 @@ def test_engine_matches_reference_fixture(name, device_inputs):
         np.testing.assert_allclose(best, g["classify_best"], rtol=1e-12)
 
 
-@pytest.mark.parametrize("mode", ["auto", "slots", "segments"])
+@pytest.mark.parametrize("mode", ["auto", "slots", "segments", "leaves"])
 @pytest.mark.parametrize("name", [n for n in NAMES if "open" not in n])
 def test_pinned_host_inputs(name, mode):
     """Page-locked host arrays: slot-mode frames read them in place
@@ -214,12 +214,13 @@ def test_workload_frames_vs_oracle(cfg):
 
 @pytest.mark.parametrize("variant", ["bayes", "last_wins_dropoff", "geometry"])
 @pytest.mark.parametrize("cfg", [1, 2, 4])
-@pytest.mark.parametrize("mode", ["segments", "slots", "auto"])
+@pytest.mark.parametrize("mode", ["segments", "slots", "auto", "leaves"])
 def test_update_modes_vs_oracle(mode, cfg, variant):
-    """Both row-grouping strategies (svx_set_update_mode) on full BASELINE
+    """Every row-grouping strategy (svx_set_update_mode) on full BASELINE
     frames, bit-exact vs the oracle.  cfg1 (depth camera, ~17 rows per voxel)
     forced into slot mode overflows the 16 slots and must re-run the frame in
-    segment mode without leaving a trace."""
+    segment mode without leaving a trace; forced into leaf mode it runs its
+    leaves of up to 8192 rows through the CTA path."""
     from paper_2512_12945_b200 import Mapper, scenes
     from oracle.oracle import OracleMap
 
@@ -241,11 +242,15 @@ def test_update_modes_vs_oracle(mode, cfg, variant):
         assert np.array_equal(report_rows([r1]), report_rows([r2]))
     st = m.engine_stats()
     if mode == "segments":
-        assert st["frames_slot_mode"] == 0
-    elif cfg == 1:   # depth camera: slot mode overflows, frames re-run with segments
+        assert st["frames_slot_mode"] == 0 and st["frames_leaf_mode"] == 0
+    elif mode == "slots" and cfg == 1:   # depth camera: slot mode overflows, re-run with segments
         assert st["frames_slot_mode"] == 0 and st["slot_overflow_reruns"] >= 1
-    else:            # LiDAR: every frame fits the slots
+    elif mode == "slots":                # LiDAR: every frame fits the slots
         assert st["frames_slot_mode"] == 3 and st["slot_overflow_reruns"] == 0
+    elif mode == "leaves":
+        assert st["frames_leaf_mode"] + st["slot_overflow_reruns"] == 3
+    elif cfg != 1:                       # auto: LiDAR frames go to leaf mode
+        assert st["frames_leaf_mode"] == 3
     c, d, w, s0, _ = m._export()
     oc, od, ow, os0, _ = om.export()
     assert np.array_equal(c, oc)
@@ -255,7 +260,7 @@ def test_update_modes_vs_oracle(mode, cfg, variant):
         assert np.array_equal(m.label_map()[1], om.label_map())
 
 
-@pytest.mark.parametrize("mode", ["slots", "segments"])
+@pytest.mark.parametrize("mode", ["slots", "segments", "leaves"])
 def test_pinned_host_inputs_match_device_inputs(mode):
     """Pinned host arrays are read in place by the walk in slot mode (no
     staging copy); the map must equal the one built from device tensors."""
@@ -353,7 +358,7 @@ def test_classify_fp64_tensor_core_vs_oracle(k):
     np.testing.assert_allclose(sims[:, 0], s0, rtol=1e-12, atol=1e-14, equal_nan=True)
 
 
-@pytest.mark.parametrize("mode", ["slots", "segments"])
+@pytest.mark.parametrize("mode", ["slots", "segments", "leaves"])
 def test_capacity_retries_vs_oracle(mode):
     """Tiny initial pools: frames run out of leaves and voxels mid-flight, are
     cleaned up, grown and re-run (recover_capacity / k_cleanup(_slots));
