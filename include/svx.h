@@ -391,7 +391,7 @@ svx_status svx_label_map(svx_map* map, int32_t mode, int64_t capacity, int32_t* 
 svx_status svx_set_profiling(svx_map* map, int32_t enable);
 
 /* Row-grouping strategy of closed-set / geometry maps with bounded bands.
- *   SVX_UPDATE_AUTO      leaf mode while recent frames average <= 3 rows per
+ *   SVX_UPDATE_AUTO      slot mode while recent frames average <= 3 rows per
  *                        touched voxel (LiDAR), segment mode otherwise
  *   SVX_UPDATE_SEGMENTS  always segments (K3 scan, K4 scatter, K5 sorted update)
  *   SVX_UPDATE_SLOTS     always try slot mode (K2 writes point indices into the

@@ -459,17 +459,14 @@ int choose_slots(const svx_map* m) {
 }
 
 // Slot and leaf mode serve the same frames (bounded-band closed/geometry
-// maps whose recent frames fit few rows per voxel); auto picks leaf mode.
+// maps whose recent frames fit few rows per voxel); auto picks slot mode
+// (measured faster on cfg2: frame span 79 vs 130 us).
 void choose_mode(svx_map* m, int64_t n) {
     const int lidar_like = choose_slots(m);
     m->frame_slots = 0;
     m->frame_leaf = 0;
     if (!lidar_like) return;
-    if (m->mode_pref == SVX_UPDATE_SLOTS) {
-        m->frame_slots = 1;
-        return;
-    }
-    if (leaf_mode_fits(n)) m->frame_leaf = 1;
+    if (m->mode_pref == SVX_UPDATE_LEAVES && leaf_mode_fits(n)) m->frame_leaf = 1;
     else m->frame_slots = 1;
 }
 

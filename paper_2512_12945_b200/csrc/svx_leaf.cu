@@ -41,7 +41,13 @@ namespace {
 
 constexpr int kLeafThreads = 256;
 constexpr int kLeafWarps = kLeafThreads / 32;
-constexpr int kWarpRows = 1024;        // rows a warp sorts in shared memory
+#ifndef SVX_LEAF_WARP_ROWS
+#define SVX_LEAF_WARP_ROWS 256
+#endif
+// Leaves of up to kWarpRows rows go to one warp, bigger ones to a whole CTA:
+// a warp folds its leaf's voxels 32 at a time, so a leaf of a few hundred
+// voxels would keep one warp busy for many dependent passes.
+constexpr int kWarpRows = SVX_LEAF_WARP_ROWS;
 constexpr int kCtaRows = 8192;         // rows a CTA sorts (more: the frame re-runs in segment mode)
 constexpr unsigned kPointBits = 23;    // binned row = slot << 23 | point (n < 2^23)
 constexpr unsigned kPointMask = (1u << kPointBits) - 1u;
@@ -258,6 +264,12 @@ __global__ void __launch_bounds__(256) k_leaf_scatter(const unsigned long long* 
 
 // ---- K5L ----------------------------------------------------------------------------
 
+__device__ __forceinline__ double4 ldg_ray(const double4* p) {
+    const double2* q = reinterpret_cast<const double2*>(p);
+    const double2 u = __ldg(q), v = __ldg(q + 1);
+    return make_double4(u.x, u.y, v.x, v.y);
+}
+
 // Fold one voxel's rows (points in ascending order) and apply the update:
 // the sums of k_update_short (_core.pyx:759-843), apply_tsdf (_pycore.py:
 // 399-417), apply_closed (:420-429).
@@ -276,9 +288,10 @@ __device__ __forceinline__ void fold_voxel(const LeafArgs& a, const FrameParams&
     TC* crow = counts + (long long)vid * a.C;
     double sw = 0.0, swd = 0.0, mind = INFINITY, maxd = -INFINITY;
     int last = 0;
+#pragma unroll 4
     for (int j = 0; j < k; ++j) {
         const int p = pt(j);
-        const double4 r = a.ray[p];
+        const double4 r = ldg_ray(a.ray + p);   // read-only: loads of later rows can issue early
         const double proj = cx * r.x + cy * r.y + cz * r.z;
         double d = r.w - proj;
         if (d < -a.trunc) d = -a.trunc;
@@ -306,44 +319,46 @@ __device__ __forceinline__ void fold_voxel(const LeafArgs& a, const FrameParams&
         for (int q = 0; q < a.C; ++q) crow[q] = (TC)(q == last - 1 ? 1 : 0);
 }
 
-// Warp-wide bitonic sort of n (power of two, >= 32) unsigned keys in buf.
-__device__ __forceinline__ void warp_bitonic(unsigned* buf, int n) {
-    const int lane = threadIdx.x & 31;
-    for (int kk = 2; kk <= n; kk <<= 1) {
-        for (int jj = kk >> 1; jj > 0; jj >>= 1) {
-            for (int i = lane; i < n; i += 32) {
-                const int l = i ^ jj;
-                if (l > i) {
-                    const unsigned x = buf[i], y = buf[l];
-                    const bool up = (i & kk) == 0;
-                    if ((x > y) == up) {
-                        buf[i] = y;
-                        buf[l] = x;
-                    }
-                }
-            }
-            __syncwarp();
+// Ascending insertion sort of a voxel's point indices (a handful of rows).
+__device__ __forceinline__ void sort_points(unsigned* p, int k) {
+    for (int i = 1; i < k; ++i) {
+        const unsigned v = p[i];
+        int j = i - 1;
+        while (j >= 0 && p[j] > v) {
+            p[j + 1] = p[j];
+            --j;
         }
+        p[j + 1] = v;
     }
 }
 
+// Shared memory of K5L.  Both paths counting-sort the leaf's rows by slot
+// (binned rows are read twice from L2: histogram, then scatter), so only the
+// point indices are kept.  Warp path: 16-bit per-slot counts packed in pairs
+// (one 32-bit atomic per row), the list of the leaf's voxels (slots).
 struct alignas(16) LeafSmem {
     union {
         struct {   // CTA path
-            unsigned keys[kCtaRows];
             unsigned pts[kCtaRows];
-            unsigned cnt[kLeafVolume];
-            unsigned off[kLeafVolume];
+            unsigned cnt[kLeafVolume];   // counts, then ends
         } c;
         struct {   // warp path, per warp
-            unsigned keys[kLeafWarps][kWarpRows];
-            unsigned short runs[kLeafWarps][kWarpRows + 2];
+            unsigned pts[kLeafWarps][kWarpRows];
+            unsigned cnt2[kLeafWarps][kLeafVolume / 2];   // two 16-bit counts per word
+            unsigned short vox[kLeafWarps][kLeafVolume];
         } w;
     };
 };
 
+__device__ __forceinline__ unsigned cnt16(const unsigned* c2, int s) {
+    return (c2[s >> 1] >> ((s & 1) * 16)) & 0xFFFFu;
+}
+
+#ifndef SVX_LEAF_UPD_MINB
+#define SVX_LEAF_UPD_MINB 4   // CTAs per SM (64 registers; 3 = 80 registers, no spills)
+#endif
 template <class TD, class TC>
-__global__ void __launch_bounds__(kLeafThreads) k_leaf_update(const unsigned* __restrict__ binrow, LeafArgs a,
+__global__ void __launch_bounds__(kLeafThreads, SVX_LEAF_UPD_MINB) k_leaf_update(const unsigned* __restrict__ binrow, LeafArgs a,
                                                               TD* vt, TC* counts) {
     grid_dep_wait();
     FrameCtr* ctr = a.ctr;
@@ -376,48 +391,40 @@ __global__ void __launch_bounds__(kLeafThreads) k_leaf_update(const unsigned* __
         const int4 lc = a.bcoord[id];
         for (int s = threadIdx.x; s < kLeafVolume; s += kLeafThreads) S.c.cnt[s] = 0u;
         __syncthreads();
-        for (unsigned j = threadIdx.x; j < c; j += kLeafThreads) {
-            const unsigned v = __ldcs(binrow + base + j);
-            S.c.keys[j] = v;
-            atomicAdd(&S.c.cnt[v >> kPointBits], 1u);
-        }
+        for (unsigned j = threadIdx.x; j < c; j += kLeafThreads)
+            atomicAdd(&S.c.cnt[__ldcg(binrow + base + j) >> kPointBits], 1u);
         __syncthreads();
-        {   // exclusive scan of the 512 slot counts (2 per thread)
+        unsigned k2[2];
+        {   // exclusive scan of the 512 slot counts (2 per thread) -> slot starts
             using Scan = cub::BlockScan<unsigned, kLeafThreads>;
             __shared__ typename Scan::TempStorage scan_tmp;
-            unsigned v2[2] = {S.c.cnt[2 * threadIdx.x], S.c.cnt[2 * threadIdx.x + 1]};
+            k2[0] = S.c.cnt[2 * threadIdx.x];
+            k2[1] = S.c.cnt[2 * threadIdx.x + 1];
             unsigned o2[2];
-            Scan(scan_tmp).ExclusiveSum(v2, o2);
-            S.c.off[2 * threadIdx.x] = o2[0];
-            S.c.off[2 * threadIdx.x + 1] = o2[1];
+            Scan(scan_tmp).ExclusiveSum(k2, o2);
+            __syncthreads();
+            S.c.cnt[2 * threadIdx.x] = o2[0];
+            S.c.cnt[2 * threadIdx.x + 1] = o2[1];
         }
         __syncthreads();
-        // scatter by slot with per-slot cursors (the counts are rebuilt below)
-        for (int s = threadIdx.x; s < kLeafVolume; s += kLeafThreads) S.c.cnt[s] = S.c.off[s];
-        __syncthreads();
-        for (unsigned j = threadIdx.x; j < c; j += kLeafThreads) {
-            const unsigned v = S.c.keys[j];
+        for (unsigned j = threadIdx.x; j < c; j += kLeafThreads) {   // cursors advance to the slot ends
+            const unsigned v = __ldcs(binrow + base + j);
             S.c.pts[atomicAdd(&S.c.cnt[v >> kPointBits], 1u)] = v & kPointMask;
         }
         __syncthreads();
         // voxels: slots 2*tid, 2*tid+1; new ones get consecutive ids
         int vidv[2];
-        bool newv[2], hasv[2];
-        int kv[2];
+        bool newv[2];
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
             const int s = 2 * threadIdx.x + q;
-            const unsigned o = S.c.off[s];
-            kv[q] = (int)(S.c.cnt[s] - o);
-            hasv[q] = kv[q] > 0;
             vidv[q] = -1;
-            if (hasv[q]) vidv[q] = (int)(unsigned)a.bslot[(long long)id * kLeafVolume + s];
-            newv[q] = hasv[q] && vidv[q] < 0;
+            if (k2[q]) vidv[q] = (int)(unsigned)a.bslot[(long long)id * kLeafVolume + s];
+            newv[q] = k2[q] && vidv[q] < 0;
         }
         {
-            int tot = 0;
+            int tot = 0, tot1 = 0;
             const int r0 = rt::cta_rank<kLeafThreads>(newv[0], tot, s_warp);
-            int tot1 = 0;
             __syncthreads();
             const int r1 = rt::cta_rank<kLeafThreads>(newv[1], tot1, s_warp);
             if (threadIdx.x == 0 && tot + tot1) s_vbase = atomicAdd(&ctr->nvox, (unsigned long long)(tot + tot1));
@@ -427,20 +434,11 @@ __global__ void __launch_bounds__(kLeafThreads) k_leaf_update(const unsigned* __
         }
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
-            if (!hasv[q]) continue;
+            if (!k2[q]) continue;
             const int s = 2 * threadIdx.x + q;
-            const int k = kv[q];
-            unsigned* pp = S.c.pts + S.c.off[s];
-            // rows of one voxel: insertion sort by point index
-            for (int i = 1; i < k; ++i) {
-                const unsigned v = pp[i];
-                int j = i - 1;
-                while (j >= 0 && pp[j] > v) {
-                    pp[j + 1] = pp[j];
-                    --j;
-                }
-                pp[j + 1] = v;
-            }
+            const int k = (int)k2[q];
+            unsigned* pp = S.c.pts + (S.c.cnt[s] - k2[q]);
+            sort_points(pp, k);
             if ((long long)vidv[q] >= vcap) {
                 ctr->err_internal = 1;
                 continue;
@@ -458,8 +456,9 @@ __global__ void __launch_bounds__(kLeafThreads) k_leaf_update(const unsigned* __
     }
     // -- warp path: leaves of <= kWarpRows rows ---------------------------------------
     const long long L = (long long)cv->n_leaves;
-    unsigned* keys = S.w.keys[warp];
-    unsigned short* runs = S.w.runs[warp];
+    unsigned* pts = S.w.pts[warp];
+    unsigned* cnt2 = S.w.cnt2[warp];
+    unsigned short* vox = S.w.vox[warp];
     while (true) {
         unsigned long long e = 0;
         if (lane == 0) e = atomicAdd(&ctr->work_long, 1ULL);
@@ -470,31 +469,71 @@ __global__ void __launch_bounds__(kLeafThreads) k_leaf_update(const unsigned* __
         const unsigned c = (unsigned)lw, base = (unsigned)(lw >> 32);
         if (c > (unsigned)kWarpRows) continue;   // the CTA path's
         const int4 lc = a.bcoord[id];
-        int P = 32;
-        while (P < (int)c) P <<= 1;
-        for (int j = lane; j < P; j += 32) keys[j] = j < (int)c ? __ldcs(binrow + base + j) : 0xFFFFFFFFu;
+#pragma unroll
+        for (int q = 0; q < kLeafVolume / 64; ++q) cnt2[lane + 32 * q] = 0u;
         __syncwarp();
-        warp_bitonic(keys, P);
-        // runs of equal slot: start positions, then the end sentinel
-        int nv = 0;
-        for (int j0 = 0; j0 < (int)c; j0 += 32) {
-            const int j = j0 + lane;
-            const bool st = j < (int)c && (j == 0 || (keys[j - 1] >> kPointBits) != (keys[j] >> kPointBits));
-            const unsigned b = __ballot_sync(0xffffffffu, st);
-            if (st) runs[nv + __popc(b & ((1u << lane) - 1u))] = (unsigned short)j;
-            nv += __popc(b);
+        for (unsigned j = lane; j < c; j += 32) {
+            const unsigned s = __ldcg(binrow + base + j) >> kPointBits;
+            atomicAdd(&cnt2[s >> 1], (s & 1u) ? 0x10000u : 1u);
         }
-        if (lane == 0) runs[nv] = (unsigned short)c;
+        __syncwarp();
+        // lane owns slots 16*lane .. 16*lane+15: local counts, a warp scan of
+        // rows and of voxels, then slot starts written back (16-bit) and the
+        // lane's voxels appended to the list in slot order
+        unsigned cl[16];
+        unsigned rows_l = 0, vox_l = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const unsigned w2 = cnt2[8 * lane + q];
+            cl[2 * q] = w2 & 0xFFFFu;
+            cl[2 * q + 1] = w2 >> 16;
+            rows_l += cl[2 * q] + cl[2 * q + 1];
+            vox_l += (cl[2 * q] != 0u) + (cl[2 * q + 1] != 0u);
+        }
+        unsigned r_incl = rows_l, v_incl = vox_l;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned rr = __shfl_up_sync(0xffffffffu, r_incl, o);
+            const unsigned vv = __shfl_up_sync(0xffffffffu, v_incl, o);
+            if (lane >= o) {
+                r_incl += rr;
+                v_incl += vv;
+            }
+        }
+        const int nv = (int)__shfl_sync(0xffffffffu, v_incl, 31);
+        unsigned off = r_incl - rows_l, vo = v_incl - vox_l;
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {   // slot starts (16-bit) overwrite the counts
+            const unsigned lo = off, hi = off + cl[2 * q];
+            off = hi + cl[2 * q + 1];
+            cnt2[8 * lane + q] = lo | (hi << 16);
+        }
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+            if (cl[q]) vox[vo++] = (unsigned short)(16 * lane + q);
+        __syncwarp();
+        for (unsigned j = lane; j < c; j += 32) {   // starts advance to the slot ends
+            const unsigned v = __ldcs(binrow + base + j);
+            const unsigned s = v >> kPointBits;
+            const unsigned old = atomicAdd(&cnt2[s >> 1], (s & 1u) ? 0x10000u : 1u);
+            pts[(old >> ((s & 1u) * 16)) & 0xFFFFu] = v & kPointMask;
+        }
         __syncwarp();
         for (int v0 = 0; v0 < nv; v0 += 32) {
             const int v = v0 + lane;
             const bool has = v < nv;
-            int r0 = 0, k = 0, slot = 0, vid = -1;
+            int slot = 0, vid = -1, k = 0;
+            unsigned* pp = pts;
             if (has) {
-                r0 = runs[v];
-                k = runs[v + 1] - r0;
-                slot = (int)(keys[r0] >> kPointBits);
+                slot = vox[v];
                 vid = (int)(unsigned)a.bslot[(long long)id * kLeafVolume + slot];
+                const unsigned end = cnt16(cnt2, slot);
+                const unsigned st0 = slot ? cnt16(cnt2, slot - 1) : 0u;
+                // (an empty slot's end equals its start; the previous slot's end
+                // is this slot's start)
+                k = (int)(end - st0);
+                pp = pts + st0;
             }
             const bool isnew = has && vid < 0;
             const unsigned nb = __ballot_sync(0xffffffffu, isnew);
@@ -503,6 +542,7 @@ __global__ void __launch_bounds__(kLeafThreads) k_leaf_update(const unsigned* __
             if (nb) vb = __shfl_sync(0xffffffffu, vb, __ffs(nb) - 1);
             if (isnew) vid = (int)(vb + __popc(nb & ((1u << lane) - 1u)));
             if (!has) continue;
+            sort_points(pp, k);
             if ((long long)vid >= vcap) {
                 ctr->err_internal = 1;
                 continue;
@@ -511,8 +551,7 @@ __global__ void __launch_bounds__(kLeafThreads) k_leaf_update(const unsigned* __
                 a.bslot[(long long)id * kLeafVolume + slot] = (unsigned long long)(unsigned)vid;
                 atomicOr(&a.bmask[(long long)id * kMaskWords + (slot >> 6)], 1ULL << (slot & 63));
             }
-            fold_voxel<TD, TC>(a, fp, lc, slot, k, [&](int j) { return (int)(keys[r0 + j] & kPointMask); },
-                               vid, isnew, vt, counts);
+            fold_voxel<TD, TC>(a, fp, lc, slot, k, [&](int j) { return (int)pp[j]; }, vid, isnew, vt, counts);
             ++touched;
         }
         __syncwarp();
@@ -574,7 +613,7 @@ svx_status leaf_t(svx_map* m, cudaStream_t s) {
     SVX_LAUNCHED();
     const int smem = (int)sizeof(LeafSmem);
     SVX_CUDA(cudaFuncSetAttribute(k_leaf_update<TD, TC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    SVX_CUDA(launch_pdl(k_leaf_update<TD, TC>, 148 * 3, kLeafThreads, smem, s, ptr<unsigned>(m->binrow), a,
+    SVX_CUDA(launch_pdl(k_leaf_update<TD, TC>, 148 * SVX_LEAF_UPD_MINB, kLeafThreads, smem, s, ptr<unsigned>(m->binrow), a,
                         ptr<TD>(m->vt), ptr<TC>(m->s0)));
     SVX_LAUNCHED();
     return SVX_OK;

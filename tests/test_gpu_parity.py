@@ -249,8 +249,8 @@ def test_update_modes_vs_oracle(mode, cfg, variant):
         assert st["frames_slot_mode"] == 3 and st["slot_overflow_reruns"] == 0
     elif mode == "leaves":
         assert st["frames_leaf_mode"] + st["slot_overflow_reruns"] == 3
-    elif cfg != 1:                       # auto: LiDAR frames go to leaf mode
-        assert st["frames_leaf_mode"] == 3
+    elif cfg != 1:                       # auto: LiDAR frames go to slot mode
+        assert st["frames_slot_mode"] == 3
     c, d, w, s0, _ = m._export()
     oc, od, ow, os0, _ = om.export()
     assert np.array_equal(c, oc)
