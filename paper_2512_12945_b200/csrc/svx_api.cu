@@ -227,8 +227,9 @@ svx_status svx_destroy(svx_map* m) {
     if (m->ev0) cudaEventDestroy(m->ev0);
     if (m->ev1) cudaEventDestroy(m->ev1);
     if (m->ev_in) cudaEventDestroy(m->ev_in);
-    for (cudaGraphExec_t g : m->gexec)
-        if (g) cudaGraphExecDestroy(g);
+    for (auto& per_mode : m->gexec)
+        for (cudaGraphExec_t g : per_mode)
+            if (g) cudaGraphExecDestroy(g);
     for (cudaGraph_t g : m->graph)
         if (g) cudaGraphDestroy(g);
     if (m->gstream) cudaStreamDestroy(m->gstream);

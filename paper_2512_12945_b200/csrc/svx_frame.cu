@@ -272,12 +272,13 @@ static svx_status launch_frame(svx_map* m, int pts_f64, int feats_f64, cudaStrea
     }
     const unsigned long long sig = graph_signature(m, pts_f64, feats_f64);
     const int gm = m->frame_leaf ? 2 : (m->frame_slots ? 1 : 0);
-    cudaGraphExec_t& gexec = m->gexec[gm];
-    if (!gexec || sig != m->gsig[gm]) {
-        if (gexec) {
-            cudaGraphExecDestroy(gexec);
-            gexec = nullptr;
-        }
+    cudaGraphExec_t& gexec = m->gexec[gm][m->exec_slot];
+    if (!m->graph[gm] || sig != m->gsig[gm]) {
+        for (cudaGraphExec_t& g : m->gexec[gm])
+            if (g) {
+                cudaGraphExecDestroy(g);
+                g = nullptr;
+            }
         if (m->graph[gm]) {
             cudaGraphDestroy(m->graph[gm]);
             m->graph[gm] = nullptr;
@@ -301,12 +302,6 @@ static svx_status launch_frame(svx_map* m, int pts_f64, int feats_f64, cudaStrea
             cudaGraphDestroy(g);
             return fail(SVX_E_INTERNAL, "frame graph: expected one root kernel node");
         }
-        e = cudaGraphInstantiate(&gexec, g, 0);
-        if (e != cudaSuccess) {
-            cudaGraphDestroy(g);
-            gexec = nullptr;
-            return fail(SVX_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
-        }
         m->graph[gm] = g;
         m->walk_node[gm] = root;
         m->walk_nargs[gm] = m->first_nargs;
@@ -327,6 +322,13 @@ static svx_status launch_frame(svx_map* m, int pts_f64, int feats_f64, cudaStrea
                 if (cudaGraphNodeGetType(nd, &t) == cudaSuccess && t == cudaGraphNodeTypeKernel) ++nk;
             }
         m->graph_kernels[gm] = nk;
+    }
+    if (!gexec) {
+        cudaError_t e = cudaGraphInstantiate(&gexec, m->graph[gm], 0);
+        if (e != cudaSuccess) {
+            gexec = nullptr;
+            return fail(SVX_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+        }
     }
     // this frame's parameters (in the attempt's mirror) into the first kernel's
     // FrameParams argument; an instantiated graph copies them at this call, so
@@ -349,6 +351,7 @@ static svx_status launch_frame(svx_map* m, int pts_f64, int feats_f64, cudaStrea
 
 // Run one frame attempt and wait for it (synchronous frames).
 static svx_status run_frame(svx_map* m, int pts_f64, int feats_f64, cudaStream_t s) {
+    m->exec_slot = kAsyncSlots;
     SVX_TRY(launch_frame(m, pts_f64, feats_f64, s, m->ev1));
     SVX_CUDA(cudaEventSynchronize(m->ev1));
     if (g_trace_host) g_t_synced = now_us();
@@ -839,7 +842,9 @@ svx_status integrate_async_impl(svx_map* m, const void* pts_in, int pts_f64, int
         *ticket = t;
         return SVX_OK;
     }
+    const double ta0 = g_trace_host ? now_us() : 0.0;
     if (m->aq_count >= std::min(m->async_depth, kAsyncSlots)) SVX_TRY(finalize_oldest(m));
+    const double ta1 = g_trace_host ? now_us() : 0.0;
     init_row_space(m, n);
     // worst-case rows (finish_frame may have lowered rcap to 1.5x the last
     // frame's rows: asynchronous frames always take the bound), and pool
@@ -908,6 +913,7 @@ svx_status integrate_async_impl(svx_map* m, const void* pts_in, int pts_f64, int
     f.stream = s;
     svx_status st = SVX_OK;
     if (cudaEventRecord(f.e0, s) != cudaSuccess) st = fail(SVX_E_CUDA, "event record failed");
+    m->exec_slot = slot;
     if (st == SVX_OK) st = launch_frame(m, pts_f64, 0, s, f.e1);
     m->h_ctr = m->h_ctr0;
     m->d_hctr = m->d_hctr0;
@@ -918,6 +924,11 @@ svx_status integrate_async_impl(svx_map* m, const void* pts_in, int pts_f64, int
     m->aq_count++;
     m->frames++;
     *ticket = m->ticket_next++;
+    if (g_trace_host) {
+        const double ta2 = now_us();
+        fprintf(stderr, "svx async us: finalize %.1f grow %d launch %.1f total %.1f in flight %d\n", ta1 - ta0,
+                grow ? 1 : 0, ta2 - ta1, ta2 - ta0, m->aq_count);
+    }
     return SVX_OK;
 }
 
