@@ -903,11 +903,160 @@ __device__ __forceinline__ void open_chunk_ring(const Fe* __restrict__ feats, in
     __pipeline_wait_prior(0);
 }
 
+// ---- 1-D TMA (cp.async.bulk) feature ring ---------------------------------------
+// Each row's slice of kOpenPass feature columns is one contiguous block of
+// global memory, so lane 0 moves it into the warp's shared-memory ring with
+// one bulk copy (the TMA engine; completion counted in bytes on the slot's
+// mbarrier) instead of 8 four-byte cp.async per lane.  kOpenBulkRing rows
+// are in flight per warp.  Used when the slice bytes are a multiple of 16
+// and the feature array is 16-byte aligned (every BASELINE open-set config).
+#ifndef SVX_OPEN_BULK
+#define SVX_OPEN_BULK 1
+#endif
+#ifndef SVX_OPEN_BULK_RING
+#define SVX_OPEN_BULK_RING 4
+#endif
+constexpr int kOpenBulkRing = SVX_OPEN_BULK_RING;
+
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_fence_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+// lane 0: expect `bytes` on bar, then one bulk copy global -> shared completing on it
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes,
+                                          unsigned long long* bar) {
+    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d),
+        "l"(src), "r"(bytes), "r"(b)
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(b),
+        "r"(parity)
+        : "memory");
+}
+
+// Warp state of the bulk ring: kOpenBulkRing slots of kOpenPass features,
+// one mbarrier per slot and the slots' phase bits (warp-uniform).
+template <class Fe>
+struct BulkRing {
+    Fe* slot;                   // kOpenBulkRing * kOpenPass
+    unsigned long long* bar;    // kOpenBulkRing
+    unsigned phase;             // bit s = parity of slot s's next completion
+};
+
+// open_chunk over a ring of bulk copies: row j of this pass sits in slot
+// j % kOpenBulkRing; the sums are the same in-order sums as open_chunk.
+template <class Fe>
+__device__ __forceinline__ void open_chunk_bulk(const Fe* __restrict__ feats, int D, int base,
+                                                const int* buf, int cnt, double* sz, double* sz2,
+                                                BulkRing<Fe>& R) {
+    const int lane = threadIdx.x & 31;
+    const int nd = min(kOpenPass, D - base);
+    const unsigned bytes = (unsigned)(nd * (int)sizeof(Fe));
+    if (lane == 0) {
+        const int pre = min(kOpenBulkRing, cnt);
+        // (slots were last read by this warp's previous pass; every lane passed
+        // the __syncwarp after its reads)
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        for (int j = 0; j < pre; ++j)
+            bulk_load(R.slot + j * kOpenPass, feats + (long long)buf[j] * D + base, bytes, R.bar + j);
+    }
+    for (int j = 0; j < cnt; ++j) {
+        const int sl = j % kOpenBulkRing;
+        mbar_wait(R.bar + sl, (R.phase >> sl) & 1u);
+        R.phase ^= 1u << sl;
+        const Fe* src = R.slot + sl * kOpenPass;
+#pragma unroll
+        for (int q = 0; q < kOpenPer; ++q) {
+            const int cc = lane + 32 * q;
+            if (cc < nd) {
+                const double zv = (double)src[cc];
+                sz[q] += zv;
+                sz2[q] += zv * zv;
+            }
+        }
+        __syncwarp();
+        if (lane == 0 && j + kOpenBulkRing < cnt) {
+            // the slot's generic reads are done: order them before the async write
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            bulk_load(R.slot + sl * kOpenPass, feats + (long long)buf[j + kOpenBulkRing] * D + base, bytes,
+                      R.bar + sl);
+        }
+    }
+}
+
+// Full passes (kOpenPass columns): lane owns the 8 contiguous columns
+// base + 8 lane .. +7, read from the ring with two 16-byte shared loads (f32)
+// and no per-column bounds checks; same per-column in-order sums.
+template <class Fe>
+__device__ __forceinline__ void load8(const Fe* p, double* v) {
+    if constexpr (sizeof(Fe) == 4) {
+        const float4 a = reinterpret_cast<const float4*>(p)[0], b = reinterpret_cast<const float4*>(p)[1];
+        v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+        v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const double2 a = reinterpret_cast<const double2*>(p)[q];
+            v[2 * q] = a.x;
+            v[2 * q + 1] = a.y;
+        }
+    }
+}
+
+template <class Fe>
+__device__ __forceinline__ void open_chunk_bulk_vec(const Fe* __restrict__ feats, int D, int base,
+                                                    const int* buf, int cnt, double* sz, double* sz2,
+                                                    BulkRing<Fe>& R) {
+    const int lane = threadIdx.x & 31;
+    constexpr unsigned bytes = (unsigned)(kOpenPass * sizeof(Fe));
+    if (lane == 0) {
+        const int pre = min(kOpenBulkRing, cnt);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        for (int j = 0; j < pre; ++j)
+            bulk_load(R.slot + j * kOpenPass, feats + (long long)buf[j] * D + base, bytes, R.bar + j);
+    }
+    for (int j = 0; j < cnt; ++j) {
+        const int sl = j % kOpenBulkRing;
+        mbar_wait(R.bar + sl, (R.phase >> sl) & 1u);
+        R.phase ^= 1u << sl;
+        double v[kOpenPer];
+        load8<Fe>(R.slot + sl * kOpenPass + kOpenPer * lane, v);
+#pragma unroll
+        for (int q = 0; q < kOpenPer; ++q) {
+            sz[q] += v[q];
+            sz2[q] += v[q] * v[q];
+        }
+        __syncwarp();
+        if (lane == 0 && j + kOpenBulkRing < cnt) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            bulk_load(R.slot + sl * kOpenPass, feats + (long long)buf[j + kOpenBulkRing] * D + base, bytes,
+                      R.bar + sl);
+        }
+    }
+}
+
 template <class TD, class TS, class Fe>
 __device__ __forceinline__ void open_voxel(const UpdateArgs& a, const KeyPack& kp,
                                            const PoseParams& pp, TD* vt, TS* mean, TS* beta,
                                            const Fe* feats, int vid, unsigned c, int* buf,
-                                           unsigned* bm, bool huge, Fe* ring = nullptr) {
+                                           unsigned* bm, bool huge, Fe* ring = nullptr,
+                                           BulkRing<Fe>* bulk = nullptr) {
     const int lane = threadIdx.x & 31;
     const unsigned k = c & ~kNewBit;
     const bool isnew = (c & kNewBit) != 0u;
@@ -948,6 +1097,15 @@ __device__ __forceinline__ void open_voxel(const UpdateArgs& a, const KeyPack& k
                 open_chunk<Fe>(feats, a.D, base, buf, cnt, sz, sz2);
                 __syncwarp();
             }
+        } else if (bulk && base + kOpenPass <= a.D) {   // full pass, contiguous columns per lane
+            open_chunk_bulk_vec<Fe>(feats, a.D, base, buf, (int)k, sz, sz2, *bulk);
+#pragma unroll
+            for (int q = 0; q < kOpenPer; ++q)
+                nig_apply<TS>(mrow, brow, base + kOpenPer * lane + q, isnew, sz[q], sz2[q], lam, lam_post,
+                              coef, nobs, b_bg);
+            continue;
+        } else if (bulk) {
+            open_chunk_bulk<Fe>(feats, a.D, base, buf, (int)k, sz, sz2, *bulk);
         } else if (ring) {
             open_chunk_ring<Fe>(feats, a.D, base, buf, (int)k, sz, sz2, ring);
         } else {
@@ -971,8 +1129,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) k_update_open(UpdateArgs a,
                                                                    TS* beta) {
     grid_dep_wait();
     __shared__ int sbuf[kWarpsPerCta][kSmemMax];
-#if SVX_OPEN_RING
-    extern __shared__ __align__(16) unsigned char oring[];
+#if SVX_OPEN_RING || SVX_OPEN_BULK
+    extern __shared__ __align__(128) unsigned char oring[];
 #endif
     FrameCtr* ctr = a.ctr;
     KSpan _ks(ctr, kSpanUpdate);
@@ -985,6 +1143,20 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) k_update_open(UpdateArgs a,
     const KeyPack kp = cv->p.kp;
     const PoseParams pp = cv->p.pp;
     const Fe* feats = (const Fe*)cv->p.feats;
+#if SVX_OPEN_BULK
+    // bulk ring (dynamic shared memory after the cp.async ring's space)
+    __shared__ __align__(8) unsigned long long s_bar[kWarpsPerCta][kOpenBulkRing];
+    const bool use_bulk = ((a.D * (int)sizeof(Fe)) % 16) == 0 && (((uintptr_t)feats) & 15) == 0;
+    BulkRing<Fe> bulk;
+    bulk.slot = reinterpret_cast<Fe*>(oring) + (size_t)wib * kOpenBulkRing * kOpenPass;
+    bulk.bar = s_bar[wib];
+    bulk.phase = 0u;
+    if (use_bulk && lane == 0) {
+        for (int q = 0; q < kOpenBulkRing; ++q) mbar_init(bulk.bar + q, 1u);
+        mbar_fence_init();
+    }
+    __syncwarp();
+#endif
 #if SVX_DYN_LONG
     for (long long e = 0;;) {
         if (lane == 0) e = (long long)atomicAdd(&ctr->work_open, 1ULL);
@@ -1000,6 +1172,13 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) k_update_open(UpdateArgs a,
             if (lane == 0) a.hugelist[atomicAdd(&ctr->n_huge, 1ULL)] = (int)e;
             continue;
         }
+#if SVX_OPEN_BULK
+        if (use_bulk) {
+            open_voxel<TD, TS, Fe>(a, kp, pp, vt, mean, beta, feats, vid, c, sbuf[wib], nullptr, false,
+                                   nullptr, &bulk);
+            continue;
+        }
+#endif
 #if SVX_OPEN_RING
         Fe* ring = reinterpret_cast<Fe*>(oring) + (size_t)wib * kOpenRingS * kOpenRingR * kOpenPass;
         open_voxel<TD, TS, Fe>(a, kp, pp, vt, mean, beta, feats, vid, c, sbuf[wib], nullptr, false, ring);
@@ -1621,7 +1800,8 @@ svx_status closed_b(svx_map* m, cudaStream_t s) {
 
 template <class TD, class TS, class Fe>
 svx_status open_a(svx_map* m, cudaStream_t s) {
-    const int ring = SVX_OPEN_RING ? kWarpsPerCta * kOpenRingS * kOpenRingR * kOpenPass * (int)sizeof(Fe) : 0;
+    int ring = SVX_OPEN_RING ? kWarpsPerCta * kOpenRingS * kOpenRingR * kOpenPass * (int)sizeof(Fe) : 0;
+    if (SVX_OPEN_BULK) ring = std::max(ring, kWarpsPerCta * kOpenBulkRing * kOpenPass * (int)sizeof(Fe));
     if (ring > 0)
         SVX_CUDA(cudaFuncSetAttribute(k_update_open<TD, TS, Fe>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       ring));
