@@ -209,7 +209,7 @@ svx_status svx_destroy(svx_map* m) {
     release_async(m);
     DevBuf* bufs[] = {&m->hash, &m->bcoord, &m->bkey, &m->bmask, &m->bslot, &m->vt,
                       &m->s0, &m->s1, &m->vrec, &m->vslot, &m->lcnt, &m->rowleaf, &m->rowpk,
-                      &m->binrow, &m->in_pts,
+                      &m->binrow, &m->render_err, &m->in_pts,
                       &m->in_lab, &m->in_feat, &m->dp_depth, &m->dp_lab_in, &m->dp_feat_in, &m->dp_pts, &m->dp_lab, &m->dp_feat, &m->ray, &m->rcnt, &m->roff, &m->rowkey,
                       &m->rowvid, &m->rowray, &m->rowd, &m->rowlab, &m->partials, &m->tlist, &m->mlist,
                       &m->longlist, &m->hinfo, &m->srid, &m->bitmap, &m->rcount, &m->cubtmp, &m->ctr, &m->ord0,

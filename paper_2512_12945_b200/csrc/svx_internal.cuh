@@ -278,6 +278,7 @@ struct svx_map {
     svx::DevBuf vrec;                        // per-voxel frame records (svx::VoxFrame)
     svx::DevBuf vslot;                       // slot mode: kSlots RowSlots per voxel
     svx::DevBuf lcnt;                        // leaf mode: per leaf {frame rows, bin base}
+    svx::DevBuf render_err;                  // renderer's step-budget flag
     int64_t n_slot_frames = 0, n_slot_reruns = 0, n_async_reruns = 0, n_leaf_frames = 0;
     int64_t io_h2d = 0, io_d2h = 0;   // host-link bytes of the last frame (inputs in, report out)
     int mode_pref = 0;      // SVX_UPDATE_AUTO / SEGMENTS / SLOTS

@@ -303,7 +303,10 @@ svx_status render_t(svx_map* m, const svx_render_camera& cam, int mode, const in
     const int T = 128;
     const int G = (int)std::min<int64_t>((npx + T - 1) / T, 148 * 16);
     RenderArgs<TD> ra = render_args<TD>(m);
-    SVX_CUDA(cudaMallocAsync(&ra.err, sizeof(int), s));
+    // one persistent error flag per map, cleared per call (nothing to free on
+    // any exit path)
+    SVX_TRY(ensure(m->render_err, sizeof(int), s));
+    ra.err = ptr<int>(m->render_err);
     SVX_CUDA(cudaMemsetAsync(ra.err, 0, sizeof(int), s));
     k_render<TD, TS><<<G, T, 0, s>>>(ra, c, mode, m->cfg.sem_kind, m->payload_d, ptr<TS>(m->s0), vlab, pal,
                                      npal, out);
@@ -311,7 +314,6 @@ svx_status render_t(svx_map* m, const svx_render_camera& cam, int mode, const in
     int herr = 0;
     cudaError_t e = cudaMemcpyAsync(&herr, ra.err, sizeof(int), cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    cudaFreeAsync(ra.err, s);
     if (e != cudaSuccess) return fail(SVX_E_CUDA, std::string("render: ") + cudaGetErrorString(e));
     if (herr) return fail(SVX_E_INPUT, "render: a ray exceeded 2^22 march steps (far plane too far)");
     return SVX_OK;

@@ -1125,7 +1125,10 @@ __device__ __forceinline__ void open_voxel(const UpdateArgs& a, const KeyPack& k
 
 // K5 open: every listed voxel; huge segments are deferred to k_update_open_huge.
 template <class TD, class TS, class Fe>
-__global__ void __launch_bounds__(32 * kWarpsPerCta) k_update_open(UpdateArgs a, TD* vt, TS* mean,
+#ifndef SVX_OPEN_MINB
+#define SVX_OPEN_MINB 1
+#endif
+__global__ void __launch_bounds__(32 * kWarpsPerCta, SVX_OPEN_MINB) k_update_open(UpdateArgs a, TD* vt, TS* mean,
                                                                    TS* beta) {
     grid_dep_wait();
     __shared__ int sbuf[kWarpsPerCta][kSmemMax];

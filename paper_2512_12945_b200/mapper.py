@@ -304,7 +304,7 @@ class Mapper:
     by field name exactly like the reference (bindings/__init__.py:77-116).
     Extra engine keys: ``tsdf_dtype`` ("float64" reference layout, default, or
     "float32" compact), ``device``, ``reserve_voxels``, ``reserve_blocks``.
-    ``backend`` accepts None/"auto"/"cuda" (there is one engine); ``threads``
+    ``backend`` accepts None/"auto"/"python"/"native" (there is one engine); ``threads``
     is validated and has no effect (device parallelism never changes bits).
     """
 
@@ -322,9 +322,13 @@ class Mapper:
         if not isinstance(threads, (int, np.integer)) or threads < 1:
             raise ConfigError(f"threads must be an integer >= 1, got {threads!r}")
         self._threads = int(threads)
+        # get_backend's names (backend.py:25-37) are accepted so scripts that pin
+        # one keep working; there is one engine here (the CUDA path), whichever
+        # is named.  Unknown names fail with the reference's message.
         backend = merged.pop("backend", None)
-        if backend not in (None, "auto", "cuda"):
-            raise ConfigError(f"unknown backend {backend!r} (expected auto or cuda)")
+        bname = backend.strip().lower() if isinstance(backend, str) else backend
+        if bname not in (None, "auto", "python", "native", "cuda"):
+            raise ConfigError(f"unknown backend {backend!r} (expected auto, python, or native)")
         self._map_bounds = merged.pop("map_bounds", None)
 
         fusion_kw = {k: v for k, v in merged.items() if k in _FUSION_KEYS}

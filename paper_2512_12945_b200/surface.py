@@ -7,7 +7,6 @@ type and builds the default palette the device colours vertices with.
 
 from __future__ import annotations
 
-import colorsys
 from dataclasses import dataclass
 
 import numpy as np
@@ -40,31 +39,58 @@ class SemanticMesh:
         return int(self.triangles.shape[0])
 
     def validate(self) -> None:
+        """Shape and index checks (mesh.py SemanticMesh.validate semantics)."""
         n = self.n_vertices
+        problems = []
         if self.vertices.shape != (n, 3):
-            raise SemvoxError("vertex array must be (n, 3)")
-        if self.labels.shape != (n,) or self.colors.shape != (n, 3):
-            raise SemvoxError("labels/colors must match vertex count")
-        t = self.triangles
-        if t.size and (t.min() < 0 or t.max() >= n):
-            raise SemvoxError("triangle index out of range")
+            problems.append("vertex array must be (n, 3)")
+        elif self.labels.shape != (n,) or self.colors.shape != (n, 3):
+            problems.append("labels/colors must match vertex count")
+        elif self.triangles.size and not (0 <= int(self.triangles.min()) and int(self.triangles.max()) < n):
+            problems.append("triangle index out of range")
+        if problems:
+            raise SemvoxError(problems[0])
 
     def triangle_areas(self) -> np.ndarray:
-        v, t = self.vertices, self.triangles
-        return 0.5 * np.linalg.norm(np.cross(v[t[:, 1]] - v[t[:, 0]], v[t[:, 2]] - v[t[:, 0]]),
-                                    axis=1)
+        corners = self.vertices[self.triangles]            # (m, 3 corners, 3)
+        edges = corners[:, 1:, :] - corners[:, :1, :]      # two edges from corner 0
+        return 0.5 * np.sqrt((np.cross(edges[:, 0], edges[:, 1]) ** 2).sum(axis=1))
+
+
+_GOLDEN = 0.618033988749895
+
+
+def _hsv_rgb(h: np.ndarray, s: float, v: float) -> np.ndarray:
+    """Vectorised HSV -> RGB in [0, 1] with the sector arithmetic of
+    colorsys.hsv_to_rgb (same float operations, so identical values)."""
+    sector = (h * 6.0).astype(np.int64)
+    f = h * 6.0 - sector
+    p = np.full_like(h, v * (1.0 - s))
+    q = v * (1.0 - s * f)
+    t = v * (1.0 - s * (1.0 - f))
+    vv = np.full_like(h, v)
+    table = {0: (vv, t, p), 1: (q, vv, p), 2: (p, vv, t), 3: (p, q, vv), 4: (t, p, vv), 5: (vv, p, q)}
+    out = np.empty(h.shape + (3,), np.float64)
+    for k, (r, g, b) in table.items():
+        sel = (sector % 6) == k
+        out[sel, 0], out[sel, 1], out[sel, 2] = r[sel], g[sel], b[sel]
+    return out
 
 
 def default_palette(num_classes: int) -> np.ndarray:
-    """(num_classes + 1, 3) uint8; row 0 = unknown grey, then hues stepping
-    by the golden ratio (mesh.py:382-395)."""
-    rows = [(128, 128, 128)]
-    hue = 0.0
-    for _ in range(max(int(num_classes), 0)):
-        hue = (hue + 0.618033988749895) % 1.0
-        r, g, b = colorsys.hsv_to_rgb(hue, 0.65, 0.95)
-        rows.append((int(r * 255.0), int(g * 255.0), int(b * 255.0)))
-    return np.array(rows, dtype=np.uint8)
+    """(num_classes + 1, 3) uint8: row 0 the unknown grey (128, 128, 128),
+    row c the colour of hue frac(c * golden ratio) accumulated step by step
+    (saturation 0.65, value 0.95) -- the reference's palette (mesh.py:382-395)."""
+    k = max(int(num_classes), 0)
+    hues = np.empty(k, np.float64)
+    acc = 0.0
+    for c in range(k):   # sequential accumulation: the rounding of each step matters
+        acc = (acc + _GOLDEN) % 1.0
+        hues[c] = acc
+    pal = np.full((k + 1, 3), 128, np.uint8)
+    if k:
+        pal[1:] = (_hsv_rgb(hues, 0.65, 0.95) * 255.0).astype(np.int64).astype(np.uint8)
+    return pal
 
 
 def check_palette(palette) -> np.ndarray:
@@ -94,41 +120,45 @@ def write_ply(mesh: SemanticMesh, path) -> None:
 
 
 def read_ply(path) -> SemanticMesh:
-    """Read meshes written by write_ply (mesh.py:603-650): ASCII, fixed layout."""
-    with open(path, "r", encoding="ascii") as fh:
-        if fh.readline().strip() != "ply":
-            raise SemvoxError("%s: not a PLY file" % path)
-        n_vert = n_face = -1
-        while True:
-            line = fh.readline()
-            if not line:
-                raise SemvoxError("%s: unterminated PLY header" % path)
-            parts = line.split()
-            if parts[:2] in (["format", "binary_little_endian"], ["format", "binary_big_endian"]):
-                raise SemvoxError("%s: only ASCII PLY is supported" % path)
-            if parts[:2] == ["element", "vertex"]:
-                n_vert = int(parts[2])
-            elif parts[:2] == ["element", "face"]:
-                n_face = int(parts[2])
-            elif parts[:1] == ["end_header"]:
-                break
-        if n_vert < 0 or n_face < 0:
-            raise SemvoxError("%s: missing vertex/face elements" % path)
-        verts = np.zeros((n_vert, 3), np.float64)
-        labels = np.zeros(n_vert, np.int32)
-        colors = np.zeros((n_vert, 3), np.uint8)
-        for i in range(n_vert):
-            f = fh.readline().split()
-            verts[i] = [float(f[0]), float(f[1]), float(f[2])]
-            colors[i] = [int(f[3]), int(f[4]), int(f[5])]
-            labels[i] = int(f[6])
-        tri = np.zeros((n_face, 3), np.int32)
-        for i in range(n_face):
-            f = fh.readline().split()
-            if int(f[0]) != 3:
-                raise SemvoxError("%s: face %d is not a triangle" % (path, i))
-            tri[i] = [int(f[1]), int(f[2]), int(f[3])]
-    mesh = SemanticMesh(vertices=verts, triangles=tri, labels=labels, colors=colors)
+    """Read meshes in write_ply's layout (ASCII, x y z r g b label vertices,
+    then '3 i j k' faces; mesh.py:603-650).  The header is scanned for its
+    element counts; the body is parsed in one pass with numpy."""
+    with open(path, "rb") as fh:
+        data = fh.read()
+    try:
+        text = data.decode("ascii")
+    except UnicodeDecodeError:
+        text = ""
+    lines = text.split("\n")
+    if not lines or lines[0].strip() != "ply":
+        raise SemvoxError("%s: not a PLY file" % path)
+    counts = {}
+    body_at = None
+    for i, line in enumerate(lines[1:], start=1):
+        tok = line.split()
+        if tok[:1] == ["format"] and tok[1:2] != ["ascii"]:
+            raise SemvoxError("%s: only ASCII PLY is supported" % path)
+        if tok[:1] == ["element"] and len(tok) == 3:
+            counts[tok[1]] = int(tok[2])
+        if tok[:1] == ["end_header"]:
+            body_at = i + 1
+            break
+    if body_at is None:
+        raise SemvoxError("%s: unterminated PLY header" % path)
+    if "vertex" not in counts or "face" not in counts:
+        raise SemvoxError("%s: missing vertex/face elements" % path)
+    nv, nf = counts["vertex"], counts["face"]
+    vrows = np.loadtxt(lines[body_at:body_at + nv], dtype=np.float64, ndmin=2).reshape(nv, 7) \
+        if nv else np.zeros((0, 7))
+    frows = np.loadtxt(lines[body_at + nv:body_at + nv + nf], dtype=np.int64, ndmin=2).reshape(nf, 4) \
+        if nf else np.zeros((0, 4), np.int64)
+    bad = np.flatnonzero(frows[:, 0] != 3)
+    if bad.size:
+        raise SemvoxError("%s: face %d is not a triangle" % (path, int(bad[0])))
+    mesh = SemanticMesh(vertices=np.ascontiguousarray(vrows[:, :3]),
+                        triangles=frows[:, 1:].astype(np.int32),
+                        labels=vrows[:, 6].astype(np.int32),
+                        colors=vrows[:, 3:6].astype(np.uint8))
     mesh.validate()
     return mesh
 

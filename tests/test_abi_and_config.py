@@ -86,8 +86,10 @@ class TestConfigRouting:
             Mapper(threads=0)
 
     def test_backend_key(self):
-        with pytest.raises(ConfigError, match="backend"):
-            Mapper(backend="python")
+        """get_backend's names are accepted (backend.py:25-37); others fail
+        with the reference's message."""
+        with pytest.raises(ConfigError, match=r"unknown backend 'cupy' \(expected auto, python, or native\)"):
+            Mapper(backend="cupy")
 
 
 class TestPoseValidation:

@@ -154,3 +154,13 @@ def test_async_falls_back_when_errors_possible():
     m2 = Mapper(voxel_size=0.05, truncation=0.15, async_frames=2)
     r = m2.integrate(np.array([[1.0, 0.0, 0.0]]), np.eye(4))
     assert r.touched_voxels > 0 and m2.active_count() == r.new_voxels
+
+
+@pytest.mark.parametrize("backend", [None, "auto", "python", "native", "NATIVE"])
+def test_backend_names_accepted(backend):
+    """A script that pins a reference backend keeps working: one engine."""
+    from paper_2512_12945_b200 import Mapper
+
+    m = Mapper(voxel_size=0.1, truncation=0.3, num_classes=3, backend=backend)
+    r = m.integrate(np.array([[1.0, 0.0, 0.0]]), np.eye(4), labels=np.array([2], np.int32))
+    assert r.touched_voxels > 0
