@@ -351,7 +351,6 @@ static svx_status launch_frame(svx_map* m, int pts_f64, int feats_f64, cudaStrea
 
 // Run one frame attempt and wait for it (synchronous frames).
 static svx_status run_frame(svx_map* m, int pts_f64, int feats_f64, cudaStream_t s) {
-    m->exec_slot = kAsyncSlots;
     SVX_TRY(launch_frame(m, pts_f64, feats_f64, s, m->ev1));
     SVX_CUDA(cudaEventSynchronize(m->ev1));
     if (g_trace_host) g_t_synced = now_us();
@@ -851,7 +850,13 @@ svx_status integrate_async_impl(svx_map* m, const void* pts_in, int pts_f64, int
     // headroom for every frame in flight; growing anything first finishes
     // the frames in flight
     const uint64_t rows_bound = (uint64_t)n * (uint64_t)m->maxrows + 4096;
-    const int64_t vneed_per = (int64_t)rows_bound;
+    // voxel headroom per frame in flight: every row could open a voxel, but
+    // sizing the pools for n * maxrows new voxels per frame costs gigabytes on
+    // large frames; like the synchronous path, take 1.5x the last frame's rows
+    // and let the rare overflow stop the frame and be re-run (recovery above)
+    const int64_t vneed_per = m->last_rows > 0
+                                  ? std::min<int64_t>((int64_t)rows_bound, m->last_rows + m->last_rows / 2 + 65536)
+                                  : (int64_t)rows_bound;
     const int64_t bneed_per = m->async_leaf_headroom > 0 ? m->async_leaf_headroom
                                                          : std::max<int64_t>(m->new_leaves_cap, 4096);
     const int depth = std::min(m->async_depth, kAsyncSlots);
@@ -913,7 +918,6 @@ svx_status integrate_async_impl(svx_map* m, const void* pts_in, int pts_f64, int
     f.stream = s;
     svx_status st = SVX_OK;
     if (cudaEventRecord(f.e0, s) != cudaSuccess) st = fail(SVX_E_CUDA, "event record failed");
-    m->exec_slot = slot;
     if (st == SVX_OK) st = launch_frame(m, pts_f64, 0, s, f.e1);
     m->h_ctr = m->h_ctr0;
     m->d_hctr = m->d_hctr0;

@@ -312,11 +312,11 @@ struct svx_map {
     int64_t npts_cap = 0;  // points the per-ray scratch holds
     // captured frame graph (replayed while the layout is unchanged)
     cudaStream_t gstream = nullptr;
-    // per mode (segments, slots, leaves) one captured graph, instantiated once
-    // per asynchronous ring slot (+ one for synchronous frames): a frame in
-    // flight never shares its executable graph with the frame being launched
-    cudaGraphExec_t gexec[3][svx::kAsyncSlots + 1] = {};
-    int exec_slot = svx::kAsyncSlots;   // which instance the next launch uses
+    // per mode (segments, slots, leaves) one captured graph and one executable
+    // instance; updating the instance's first-kernel parameters does not touch
+    // launches already queued, so frames in flight share it
+    cudaGraphExec_t gexec[3][1] = {};
+    int exec_slot = 0;
     cudaGraph_t graph[3] = {};       // kept: its first-kernel node is updated per frame
     cudaGraphNode_t walk_node[3] = {};
     int walk_nargs[3] = {};          // parameters of that kernel (FrameParams is the last)

@@ -86,8 +86,9 @@ def pipeline(config=2, frames=30, mode="auto", async_frames=2, flush=False, rese
 
 if __name__ == "__main__":
     if "--pipeline" in sys.argv:
+        cfg = int(os.environ.get("DIAG_CONFIG", "2"))
         for af in ([int(a) for a in sys.argv[sys.argv.index("--pipeline") + 1].split(",")]
                    if len(sys.argv) > sys.argv.index("--pipeline") + 1 else (0, 1, 2, 3, 4)):
-            pipeline(mode="slots", async_frames=af, reserve=True)
+            pipeline(config=cfg, mode="auto", async_frames=af, reserve=True)
     else:
         main()
