@@ -368,6 +368,12 @@ svx_status svx_classify(svx_map* map, const double* emb, int32_t k, double tempe
                         double confidence_threshold, int64_t capacity, int32_t* labels,
                         double* best, double* sims, void* stream);
 
+/* Score path of svx_classify: 0 = auto (the exact int8 split GEMM on the
+ * tcgen05 tensor cores for more than 64 queries with f32 means, the FP64 DMMA
+ * kernel otherwise), 1 = DMMA, 2 = tcgen05 (f32 means; else DMMA).  All give
+ * labels equal to the reference's and scores within f64 rounding of it. */
+svx_status svx_set_score_path(svx_map* map, int32_t path);
+
 /* Closed-set readout over active voxels: mode 0 = dirichlet.label_map
  * (argmax+1, ties to lowest, dirichlet.py:81-88); mode 1 = evalbench.grid_labels
  * (0 when all counts are zero, evalbench.py:30-55). */

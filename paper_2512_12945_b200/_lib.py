@@ -143,6 +143,7 @@ _SIGNATURES = {
     "svx_sample_distance": [_P, _P, _I64, _P, _P, _P],
     "svx_import": [_P, _I64, _P, _I64, _P, _P, _P, _P, _P, _P, _P],
     "svx_set_update_mode": [_P, _I32],
+    "svx_set_score_path": [_P, _I32],
     "svx_reserve": [_P, _I64, _I64],
     "svx_shard_march": [_P, _P, _I32, _I64, ctypes.POINTER(_D), ctypes.POINTER(_D), _P, _P, _I32,
                         ctypes.POINTER(_I64), _P, ctypes.POINTER(SvxShardSummary)],

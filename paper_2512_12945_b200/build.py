@@ -22,7 +22,7 @@ BUILD = os.path.join(os.path.dirname(PKG), "build", "svx")
 
 SOURCES = [
     "svx_api.cu", "svx_frame.cu", "svx_march.cu", "svx_resolve.cu", "svx_update.cu", "svx_leaf.cu",
-    "svx_query.cu", "svx_shard.cu", "svx_depth.cu", "svx_import.cu",
+    "svx_query.cu", "svx_score.cu", "svx_shard.cu", "svx_depth.cu", "svx_import.cu",
     "svx_mesh.cu", "svx_render.cu",
 ]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

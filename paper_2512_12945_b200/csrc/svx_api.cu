@@ -209,7 +209,7 @@ svx_status svx_destroy(svx_map* m) {
     release_async(m);
     DevBuf* bufs[] = {&m->hash, &m->bcoord, &m->bkey, &m->bmask, &m->bslot, &m->vt,
                       &m->s0, &m->s1, &m->vrec, &m->vslot, &m->lcnt, &m->rowleaf, &m->rowpk,
-                      &m->binrow, &m->render_err, &m->in_pts,
+                      &m->binrow, &m->render_err, &m->sc_q, &m->sc_o, &m->in_pts,
                       &m->in_lab, &m->in_feat, &m->dp_depth, &m->dp_lab_in, &m->dp_feat_in, &m->dp_pts, &m->dp_lab, &m->dp_feat, &m->ray, &m->rcnt, &m->roff, &m->rowkey,
                       &m->rowvid, &m->rowray, &m->rowd, &m->rowlab, &m->partials, &m->tlist, &m->mlist,
                       &m->longlist, &m->hinfo, &m->srid, &m->bitmap, &m->rcount, &m->cubtmp, &m->ctr, &m->ord0,
@@ -359,6 +359,13 @@ svx_status svx_set_profiling(svx_map* m, int32_t enable) {
         SVX_CUDA(cudaMallocHost((void**)&m->h_kspan, n));
     }
     m->prof = enable != 0;
+    return SVX_OK;
+}
+
+svx_status svx_set_score_path(svx_map* m, int32_t path) {
+    if (!m) return fail(SVX_E_INPUT, "null argument");
+    if (path < 0 || path > 2) return fail(SVX_E_INPUT, "unknown score path");
+    m->score_path = path;
     return SVX_OK;
 }
 

@@ -279,6 +279,8 @@ struct svx_map {
     svx::DevBuf vslot;                       // slot mode: kSlots RowSlots per voxel
     svx::DevBuf lcnt;                        // leaf mode: per leaf {frame rows, bin base}
     svx::DevBuf render_err;                  // renderer's step-budget flag
+    svx::DevBuf sc_q, sc_o;                  // tcgen05 scoring scratch (svx_score.cu)
+    int score_path = 0;                      // classify: 0 auto, 1 DMMA, 2 tcgen05 (svx_set_score_path)
     int64_t n_slot_frames = 0, n_slot_reruns = 0, n_async_reruns = 0, n_leaf_frames = 0;
     int64_t io_h2d = 0, io_d2h = 0;   // host-link bytes of the last frame (inputs in, report out)
     int mode_pref = 0;      // SVX_UPDATE_AUTO / SEGMENTS / SLOTS
@@ -729,5 +731,9 @@ svx_status launch_classify(svx_map* m, int64_t count, const double* emb, const d
                            double tau, double tp, int32_t* labels, double* best, double* sims,
                            cudaStream_t s);
 svx_status launch_label_map(svx_map* m, int64_t count, int mode, int32_t* labels, cudaStream_t s);
+// svx_score.cu: classify_means scores as an int8 split GEMM on tcgen05
+svx_status classify_tc(svx_map* m, int64_t count, const int* act_vid, const double* emb, const double* en,
+                       int k, double tau, double tp, int32_t* labels, double* best, double* sims,
+                       cudaStream_t s);
 
 }  // namespace svx

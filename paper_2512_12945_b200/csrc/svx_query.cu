@@ -666,10 +666,23 @@ static svx_status classify_dmma_t(svx_map* m, int64_t count, const double* emb, 
     return SVX_OK;
 }
 
+// SVX_SCORE_TC=0: keep classify on the FP64 DMMA kernel; SVX_SCORE_TC=1: the
+// tcgen05 kernel for every k (A/B switches and the tests of both paths)
+static const bool g_score_tc = !(getenv("SVX_SCORE_TC") && getenv("SVX_SCORE_TC")[0] == '0');
+static const bool g_score_tc_force = getenv("SVX_SCORE_TC") && getenv("SVX_SCORE_TC")[0] == '1';
+
 template <class TS, class TD>
 static svx_status classify_t(svx_map* m, int64_t count, const double* emb, const double* en, int k,
                              double tau, double tp, int32_t* labels, double* best, double* sims,
                              cudaStream_t s) {
+    // f32 means and more than 64 queries: the exact int8 split GEMM on
+    // tcgen05 (svx_score.cu; cfg5, D = 768, k = 128: 9.4 ms vs 13.1 ms on the
+    // DMMA kernel).  Up to 64 queries the DMMA kernel is faster (cfg3, k = 32:
+    // 0.88 vs 1.26 ms): its tiles are issue-bound at N <= 32
+    if constexpr (sizeof(TS) == 4)
+        if (m->payload_d <= 1024 && m->score_path != 1 &&
+            (m->score_path == 2 || g_score_tc_force || (g_score_tc && k > 64)))
+            return classify_tc(m, count, ptr<int>(m->act_vid), emb, en, k, tau, tp, labels, best, sims, s);
     // FP64 tensor cores (DMMA) for up to 128 queries; the warp-per-voxel
     // CUDA-core kernel beyond
     // up to 64 queries: operands straight from global/L2 (measured best); 65..128:

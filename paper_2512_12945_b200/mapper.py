@@ -723,6 +723,16 @@ class Mapper:
             raise ValueError(f"update mode must be one of {sorted(self._UPDATE_MODES)}")
         check(lib.svx_set_update_mode(self._handle, self._UPDATE_MODES[mode]))
 
+    _SCORE_PATHS = {"auto": 0, "dmma": 1, "tcgen05": 2}
+
+    def set_score_path(self, path: str = "auto") -> None:
+        """classify's kernel (svx_set_score_path): "auto", "dmma" (FP64 tensor
+        cores) or "tcgen05" (exact int8 split GEMM on the 5th-gen tensor
+        cores).  Same labels; scores within f64 rounding."""
+        if path not in self._SCORE_PATHS:
+            raise ValueError(f"score path must be one of {sorted(self._SCORE_PATHS)}")
+        check(lib.svx_set_score_path(self._handle, self._SCORE_PATHS[path]))
+
     def set_profiling(self, enable: bool = True) -> None:
         """Record per-stage device times of each integrate (svx_set_profiling)."""
         check(lib.svx_set_profiling(self._handle, int(bool(enable))))

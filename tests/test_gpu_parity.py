@@ -205,11 +205,13 @@ def test_workload_frames_vs_oracle(cfg):
     if wl.queries is not None:
         q = wl.queries.cpu().numpy()
         assert q.shape == ((32, 512) if cfg == 3 else (128, 768))
-        lab, best = m.classify(q)
         olab, obest = om.classify(q)
-        assert lab.shape[0] == c.shape[0] > 100000
-        assert np.array_equal(lab, olab)
-        np.testing.assert_allclose(best, obest, rtol=1e-12, atol=1e-300)
+        for path in ("dmma", "tcgen05"):   # FP64 DMMA and the int8 split GEMM on tcgen05
+            m.set_score_path(path)
+            lab, best = m.classify(q)
+            assert lab.shape[0] == c.shape[0] > 100000
+            assert np.array_equal(lab, olab), path
+            np.testing.assert_allclose(best, obest, rtol=1e-12, atol=1e-300, err_msg=path)
 
 
 @pytest.mark.parametrize("variant", ["bayes", "last_wins_dropoff", "geometry"])
@@ -326,12 +328,13 @@ def test_cuda_fast_path_pose_fallbacks():
             b.integrate(pts, bad, labels=lab)
 
 
+@pytest.mark.parametrize("path", ["dmma", "tcgen05"])
 @pytest.mark.parametrize("k", [5, 32, 100, 160])
-def test_classify_fp64_tensor_core_vs_oracle(k):
-    """classify_means on the FP64 tensor cores (k <= 128) and the CUDA-core
-    kernel (k > 128) against the oracle's sequential f64 scoring: labels
-    exact, best and similarities within 1e-12 (only the summation order of
-    the dot products differs)."""
+def test_classify_fp64_tensor_core_vs_oracle(k, path):
+    """classify_means on the FP64 tensor cores (DMMA, k <= 128; the CUDA-core
+    kernel beyond) and on the tcgen05 int8 split GEMM (any k) against the
+    oracle's sequential f64 scoring: labels exact, best and similarities
+    within 1e-12 (only the rounding of the dot products differs)."""
     from paper_2512_12945_b200 import Mapper, scenes
     from oracle.oracle import OracleMap
 
@@ -339,6 +342,7 @@ def test_classify_fp64_tensor_core_vs_oracle(k):
     kw = dict(wl.mapper_kwargs)
     kw["feature_dim"] = 96                     # keeps the oracle fast; not a multiple of 16
     m = Mapper(**kw)
+    m.set_score_path(path)
     om = OracleMap(**kw)
     for i in range(2):
         f = wl.make_frame(i * 5)

@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--frames", type=int, default=4)
     ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--path", default="auto", choices=["auto", "dmma", "tcgen05"])
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -40,6 +41,7 @@ def main():
     D = kw["feature_dim"]
     k = 32 if args.config == 3 else 128
     m = Mapper(**kw)
+    m.set_score_path(args.path)
     for i in range(args.frames):
         f = wl.make_frame(i * max(1, wl.n_frames // args.frames))
         m.integrate_world(f.points_world, f.origin, features=f.features)
@@ -76,8 +78,10 @@ def main():
         "value": V / t, "gflops_f64": flops / t / 1e9,
         "frac_of_fp64_tensor_peak": flops / t / 1e12 / FP64_TENSOR_PEAK_TFLOPS,
         "peak_source": "nominal B200 FP64 tensor core 40 TFLOP/s",
-        "path": "mma.sync.m8n8k4.f64 (DMMA) fused GEMM + softmax epilogue" if k <= 128
-                else "CUDA-core f64",
+        "path": ("tcgen05.mma.kind::i8 exact split GEMM (7 byte planes per operand, 34 plane pairs, "
+                 "int32 TMEM accumulators) + softmax kernel"
+                 if (args.path == "tcgen05" or (args.path == "auto" and k > 64))
+                 else "mma.sync.m8n8k4.f64 (DMMA) fused GEMM + softmax epilogue"),
         "timing": "CUDA events around svx_classify (includes the active-list build)",
     }))
 
