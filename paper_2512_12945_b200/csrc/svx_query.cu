@@ -680,7 +680,7 @@ static svx_status classify_t(svx_map* m, int64_t count, const double* emb, const
     // DMMA kernel).  Up to 64 queries the DMMA kernel is faster (cfg3, k = 32:
     // 0.88 vs 1.26 ms): its tiles are issue-bound at N <= 32
     if constexpr (sizeof(TS) == 4)
-        if (m->payload_d <= 1024 && m->score_path != 1 &&
+        if (m->payload_d <= 1024 && k <= 4096 && m->score_path != 1 &&
             (m->score_path == 2 || g_score_tc_force || (g_score_tc && k > 64)))
             return classify_tc(m, count, ptr<int>(m->act_vid), emb, en, k, tau, tp, labels, best, sims, s);
     // FP64 tensor cores (DMMA) for up to 128 queries; the warp-per-voxel

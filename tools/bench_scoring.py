@@ -5,9 +5,10 @@
 Builds an open-set map from the BASELINE depth-camera workload (cfg3: D=512,
 32 queries; cfg5: D=768, 128 queries), then times svx_classify with device
 output buffers (CUDA events around the call, which includes the active-list
-build).  Prints one JSON line: voxels scored per second, f64 GFLOP/s of the
-scoring GEMM (2*V*D*k) and its fraction of the B200's nominal FP64 tensor-core
-peak (40 TFLOP/s; the DMMA path), and the kernel's span.
+build).  Prints one JSON line: voxels scored per second, the f64-equivalent
+GFLOP/s of the scoring GEMM (2*V*D*k), and against measured peaks: the DMMA
+path's fraction of the FP64 tensor rate, the tcgen05 path's int8 TOP/s (34
+plane-pair GEMMs) against the dense int8 rate and the N=64 shared-memory rate.
 """
 
 from __future__ import annotations
@@ -21,7 +22,10 @@ import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
-FP64_TENSOR_PEAK_TFLOPS = 40.0   # B200 nominal FP64 / FP64 tensor core
+# measured on this pool's B200 by tools/tc_peaks.py (profiles/r02_tensor_peaks_measured.json)
+FP64_TENSOR_PEAK_TFLOPS = 37.17   # mma.sync.m8n8k4.f64
+I8_DENSE_PEAK_TOPS = 4494.9       # tcgen05 kind::i8, M=128 N=256 (tensor-bound)
+I8_SS_N64_TOPS = 2893.9           # the scoring kernel's shape: N=64, both operands in smem (48 cycles/MMA)
 
 
 def main():
@@ -72,19 +76,33 @@ def main():
         ms.append(a.elapsed_time(b))
     t = statistics.median(ms) / 1e3
     flops = 2.0 * V * D * k
-    print(json.dumps({
+    tc = args.path == "tcgen05" or (args.path == "auto" and k > 64)
+    out = {
         "metric": "open-set voxels scored/sec", "config": f"cfg{args.config}",
         "voxels": V, "feature_dim": D, "queries": k, "ms": t * 1e3,
-        "value": V / t, "gflops_f64": flops / t / 1e9,
-        "frac_of_fp64_tensor_peak": flops / t / 1e12 / FP64_TENSOR_PEAK_TFLOPS,
-        "peak_source": "nominal B200 FP64 tensor core 40 TFLOP/s",
-        "path": ("tcgen05.mma.kind::i8 exact split GEMM (7 byte planes per operand, 34 plane pairs, "
-                 "int32 TMEM accumulators) + softmax kernel"
-                 if (args.path == "tcgen05" or (args.path == "auto" and k > 64))
-                 else "mma.sync.m8n8k4.f64 (DMMA) fused GEMM + softmax epilogue"),
+        "value": V / t, "gflops_f64_equiv": flops / t / 1e9,
         "timing": "CUDA events around svx_classify (includes the active-list build)",
-    }))
-
+    }
+    if tc:
+        tn = 32 if k <= 32 else 64
+        kp = -(-k // tn) * tn
+        dp = max(2, -(-D // 64)) * 64
+        i8 = 34 * 2.0 * (-(-V // 128) * 128) * kp * dp   # 34 byte-plane pair GEMMs
+        out.update({
+            "path": "tcgen05.mma.kind::i8 exact split GEMM (7 byte planes per operand, 34 plane pairs, "
+                    "int32 TMEM accumulators)" + (" + fused softmax" if k <= 32 else " + softmax kernel"),
+            "int8_tops": i8 / t / 1e12,
+            "frac_of_i8_dense_peak": i8 / t / 1e12 / I8_DENSE_PEAK_TOPS,
+            "frac_of_i8_ss_n64_rate": i8 / t / 1e12 / I8_SS_N64_TOPS,
+            "peak_source": "measured, profiles/r02_tensor_peaks_measured.json (whole call incl. prep and softmax)",
+        })
+    else:
+        out.update({
+            "path": "mma.sync.m8n8k4.f64 (DMMA) fused GEMM + softmax epilogue",
+            "frac_of_fp64_tensor_peak": flops / t / 1e12 / FP64_TENSOR_PEAK_TFLOPS,
+            "peak_source": "measured DMMA 37.17 TFLOP/s, profiles/r02_tensor_peaks_measured.json",
+        })
+    print(json.dumps(out))
 
 if __name__ == "__main__":
     main()
