@@ -330,6 +330,57 @@ svx_status svx_shard_pack(svx_map* map, void* send, int64_t capacity, void* stre
 svx_status svx_shard_apply(svx_map* map, const void* recv, const int64_t* recv_bytes,
                            int32_t nranks, void* stream, svx_report* report);
 
+/* Device-planned frames: the same four phases with every size and check kept
+ * on the device, so a frame takes exactly one host synchronisation (after
+ * its last collective) instead of one per phase.  The caller's transport
+ * runs, on the same stream and without reading anything back:
+ *
+ *   svx_shard_march_async   march the slice; write the local summary vector
+ *                           (SVX_SHARD_SUMMARY_WORDS int64, device memory)
+ *   -- all-reduce: words [0, SVX_SHARD_SUM_WORDS) summed, the rest max
+ *   svx_shard_plan_async    the frame checks on the global summary into the
+ *                           device abort vector (SVX_SHARD_ABORT_WORDS int64);
+ *                           bucket the rows by owner into sections of a fixed
+ *                           capacity `cap` bytes per destination
+ *   svx_shard_pack_async    write the sections (send: nranks * cap bytes)
+ *   -- all-reduce (max) of the abort vector; all-to-all of equal cap-byte
+ *      blocks (no size exchange)
+ *   svx_shard_apply_async   K2-K5 on the received sections, or nothing when
+ *                           the frame is aborted; writes 4 report words
+ *                           (touched, new leaves, new voxels, redo flag)
+ *   -- optional all-reduce (sum) of the report words
+ *   -- the one host synchronisation: read back summary, abort, report
+ *   svx_shard_finish        raise the frame's error (same messages as
+ *                           svx_shard_plan, on every rank), or *action:
+ *                           0 done; 1 redo the frame on every rank (key
+ *                           rebase to the summary's bbox minimum, larger
+ *                           scratch, or *need bytes of section capacity);
+ *                           2 redo this rank's apply (scratch / pools grown;
+ *                           nothing was changed); 3 done here, but another
+ *                           rank redoes its apply: repeat the report sum.
+ * A frame aborted on the device changes no map: the checks run before any
+ * rank's K2. */
+#define SVX_SHARD_SUM_WORDS 10
+#define SVX_SHARD_SUMMARY_WORDS 18
+#define SVX_SHARD_ABORT_WORDS 8
+svx_status svx_shard_march_async(svx_map* map, const void* points, int32_t points_dtype, int64_t n,
+                                 const double pose[16], const double origin[3], const int32_t* labels,
+                                 const void* feats, int32_t feats_dtype, const int64_t key_base[3],
+                                 void* stream, int64_t* summary);
+svx_status svx_shard_plan_async(svx_map* map, const int64_t* global_summary, int32_t rank,
+                                int32_t nranks, int64_t cap, void* stream, int64_t* abort_words);
+svx_status svx_shard_pack_async(svx_map* map, void* send, int64_t cap, void* stream,
+                                const int64_t* abort_words);
+/* frame_points: the whole frame's point count (bounds the received points). */
+svx_status svx_shard_apply_async(svx_map* map, const void* recv, int64_t cap, int32_t nranks,
+                                 const int64_t* abort_words, int64_t frame_points, void* stream,
+                                 int64_t* report_words);
+/* Host copies of the reduced summary / abort words and (NULL when the caller
+ * did not sum them) the summed report words. */
+svx_status svx_shard_finish(svx_map* map, const int64_t* summary, const int64_t* abort_words,
+                            const int64_t* report_sum, svx_report* report, int32_t* action,
+                            int64_t* need);
+
 /* Per leaf, in this map's active (leaf) order: creation frame, the leaf's
  * smallest packed key in that frame, and its active voxel count.  Sorting
  * the concatenated shards' leaves by (frame, key) gives the global order. */

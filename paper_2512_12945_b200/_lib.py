@@ -152,7 +152,18 @@ _SIGNATURES = {
     "svx_shard_pack": [_P, _P, _I64, _P],
     "svx_shard_apply": [_P, _P, ctypes.POINTER(_I64), _I32, _P, ctypes.POINTER(SvxReport)],
     "svx_export_leaf_stamps": [_P, _I64, _P, _P, _P, ctypes.POINTER(_I64), _P],
+    "svx_shard_march_async": [_P, _P, _I32, _I64, ctypes.POINTER(_D), ctypes.POINTER(_D), _P, _P, _I32,
+                              ctypes.POINTER(_I64), _P, _P],
+    "svx_shard_plan_async": [_P, _P, _I32, _I32, _I64, _P, _P],
+    "svx_shard_pack_async": [_P, _P, _I64, _P, _P],
+    "svx_shard_apply_async": [_P, _P, _I64, _I32, _P, _I64, _P, _P],
+    "svx_shard_finish": [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64), ctypes.POINTER(_I64),
+                         ctypes.POINTER(SvxReport), ctypes.POINTER(_I32), ctypes.POINTER(_I64)],
 }
+
+SHARD_SUM_WORDS = 10        # svx.h SVX_SHARD_SUM_WORDS
+SHARD_SUMMARY_WORDS = 18    # svx.h SVX_SHARD_SUMMARY_WORDS
+SHARD_ABORT_WORDS = 8       # svx.h SVX_SHARD_ABORT_WORDS
 
 DEVICE_INPUTS = 0x100   # svx.h SVX_DEVICE_INPUTS
 POSE_CHECK = 0x200      # svx.h SVX_POSE_CHECK

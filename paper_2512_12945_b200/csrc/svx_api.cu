@@ -223,6 +223,7 @@ svx_status svx_destroy(svx_map* m) {
     for (DevBuf* b : bufs) release(*b);
     if (m->h_ctr0) cudaFreeHost(m->h_ctr0);
     if (m->h_kspan) cudaFreeHost(m->h_kspan);
+    if (m->sh_hlocal) cudaFreeHost(m->sh_hlocal);
     release(m->kspan);
     if (m->ev0) cudaEventDestroy(m->ev0);
     if (m->ev1) cudaEventDestroy(m->ev1);
@@ -799,6 +800,63 @@ svx_status svx_shard_apply(svx_map* m, const void* recv, const int64_t* recv_byt
     SVX_TRY(set_device(m));
     SVX_TRY(drain(m));
     return shard_apply(m, recv, recv_bytes, nranks, (cudaStream_t)stream, report);
+}
+
+static PoseParams shard_pose(const double pose[16], const double origin[3]) {
+    PoseParams pp;
+    memset(&pp, 0, sizeof(pp));
+    if (pose) {
+        for (int r = 0; r < 3; ++r) {
+            for (int c = 0; c < 3; ++c) pp.R[3 * r + c] = pose[4 * r + c];
+            pp.t[r] = pose[4 * r + 3];
+        }
+        pp.sensor = 1;
+    } else {
+        pp.R[0] = pp.R[4] = pp.R[8] = 1.0;
+        for (int a = 0; a < 3; ++a) pp.t[a] = origin[a];
+        pp.sensor = 0;
+    }
+    return pp;
+}
+
+svx_status svx_shard_march_async(svx_map* m, const void* points, int32_t points_dtype, int64_t n,
+                                 const double pose[16], const double origin[3], const int32_t* labels,
+                                 const void* feats, int32_t feats_dtype, const int64_t key_base[3],
+                                 void* stream, int64_t* summary) {
+    if (!m || !summary || (!pose && !origin) || (n > 0 && !points)) return fail(SVX_E_INPUT, "null argument");
+    SVX_TRY(set_device(m));
+    SVX_TRY(drain(m));
+    return shard_march_async(m, points, points_dtype == SVX_F64, n, shard_pose(pose, origin), labels, feats,
+                             feats_dtype == SVX_F64, key_base, (cudaStream_t)stream, summary);
+}
+
+svx_status svx_shard_plan_async(svx_map* m, const int64_t* global_summary, int32_t rank, int32_t nranks,
+                                int64_t cap, void* stream, int64_t* abort_words) {
+    if (!m || !global_summary || !abort_words) return fail(SVX_E_INPUT, "null argument");
+    SVX_TRY(set_device(m));
+    return shard_plan_async(m, global_summary, rank, nranks, cap, (cudaStream_t)stream, abort_words);
+}
+
+svx_status svx_shard_pack_async(svx_map* m, void* send, int64_t cap, void* stream, const int64_t* abort_words) {
+    if (!m || !abort_words) return fail(SVX_E_INPUT, "null argument");
+    SVX_TRY(set_device(m));
+    return shard_pack_async(m, send, cap, (cudaStream_t)stream, abort_words);
+}
+
+svx_status svx_shard_apply_async(svx_map* m, const void* recv, int64_t cap, int32_t nranks,
+                                 const int64_t* abort_words, int64_t frame_points, void* stream,
+                                 int64_t* report_words) {
+    if (!m || !abort_words || !report_words) return fail(SVX_E_INPUT, "null argument");
+    SVX_TRY(set_device(m));
+    return shard_apply_async(m, recv, cap, nranks, abort_words, frame_points, (cudaStream_t)stream,
+                             report_words);
+}
+
+svx_status svx_shard_finish(svx_map* m, const int64_t* summary, const int64_t* abort_words,
+                            const int64_t* report_sum, svx_report* report, int32_t* action, int64_t* need) {
+    if (!m || !summary || !abort_words || !action || !need) return fail(SVX_E_INPUT, "null argument");
+    SVX_TRY(set_device(m));
+    return shard_finish(m, summary, abort_words, report_sum, report, action, need);
 }
 
 svx_status svx_export_leaf_stamps(svx_map* m, int64_t capacity, int32_t* frame, uint64_t* key,

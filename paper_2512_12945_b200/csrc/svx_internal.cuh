@@ -366,6 +366,13 @@ struct svx_map {
     svx::DevBuf sh_mask, sh_pos, sh_tiles, sh_meta;
     int64_t sh_npts[SVX_MAX_SHARDS] = {}, sh_nrows[SVX_MAX_SHARDS] = {};
     int64_t sh_bytes[SVX_MAX_SHARDS] = {};
+    // device-planned frames (svx_shard_*_async)
+    int shard_async = 0;
+    int64_t sh_cap = 0;
+    int64_t sh_nblocks0 = 0, sh_nvox0 = 0;
+    int64_t sh_last_rows = 0;           // rows of the last frame (global march / local apply, larger)
+    svx::DevBuf sh_ao;                  // ApplyOffsets + local flags
+    long long* sh_hlocal = nullptr;     // pinned copy of the local flags
 };
 
 namespace svx {
@@ -721,6 +728,16 @@ svx_status shard_plan(svx_map* m, const svx_shard_summary* global, int rank, int
 svx_status shard_pack(svx_map* m, void* send, int64_t capacity, cudaStream_t s);
 svx_status shard_apply(svx_map* m, const void* recv, const int64_t* recv_bytes, int nranks,
                        cudaStream_t s, svx_report* rep);
+svx_status shard_march_async(svx_map* m, const void* pts, int pts_f64, int64_t n, const PoseParams& pp,
+                             const int32_t* labels, const void* feats, int feats_f64,
+                             const int64_t* key_base, cudaStream_t s, int64_t* summary);
+svx_status shard_plan_async(svx_map* m, const int64_t* gsum, int rank, int G, int64_t cap, cudaStream_t s,
+                            int64_t* abort);
+svx_status shard_pack_async(svx_map* m, void* send, int64_t cap, cudaStream_t s, const int64_t* abort);
+svx_status shard_apply_async(svx_map* m, const void* recv, int64_t cap, int G, const int64_t* abort,
+                             int64_t frame_points, cudaStream_t s, int64_t* rep_words);
+svx_status shard_finish(svx_map* m, const int64_t* g, const int64_t* abort, const int64_t* rsum,
+                        svx_report* rep, int32_t* action, int64_t* need);
 svx_status launch_export(svx_map* m, int64_t count, int64_t* coords, void* d, void* w, void* sem0,
                          void* sem1, cudaStream_t s);
 svx_status launch_probe(svx_map* m, const int64_t* coords, int64_t cnt, void* d, void* w,

@@ -72,10 +72,21 @@ struct ShardMeta {
 
 // Rows -> owning rank (kept in rowvid, unused until apply); the point's
 // owner mask; per-owner row counts (one atomic per CTA and owner).
+// Frame-level abort of a device-planned frame (svx_shard_*_async): any of the
+// global checks, or (for the local pack) a section over its capacity.
+__device__ __forceinline__ bool shard_aborted(const long long* abort, bool local) {
+    if (!abort) return false;
+    bool a = false;
+    for (int i = 0; i < 5; ++i) a |= abort[i] != 0;
+    return a || (local && abort[5] != 0);
+}
+
 __global__ void __launch_bounds__(kPlanThreads) k_shard_rows(
     long long R, int G, KeyPack kp, const unsigned long long* __restrict__ rowkey,
     const int* __restrict__ rowray, int* __restrict__ rowown, unsigned* __restrict__ ptmask,
-    ShardMeta* meta) {
+    ShardMeta* meta, const FrameCtr* ctr, const long long* abort) {
+    if (R < 0) R = (long long)ctr->rows;   // device-planned frames: the march's count
+    if (shard_aborted(abort, false)) return;
     __shared__ unsigned s_cnt[SVX_MAX_SHARDS];
     if (threadIdx.x < SVX_MAX_SHARDS) s_cnt[threadIdx.x] = 0;
     __syncthreads();
@@ -114,7 +125,7 @@ __global__ void __launch_bounds__(kPlanThreads) k_shard_tiles(long long n, int G
 // One warp: per owner, exclusive scan of the tile counts (in place), then
 // section sizes and offsets in rank order.
 __global__ void k_shard_plan(long long ntiles, int G, long long pay, long long* __restrict__ tiles,
-                             ShardMeta* meta) {
+                             ShardMeta* meta, long long cap, long long* abort) {
     const int o = threadIdx.x;
     if (o < G) {
         long long acc = 0;
@@ -128,12 +139,17 @@ __global__ void k_shard_plan(long long ntiles, int G, long long pay, long long* 
     }
     __syncwarp();
     if (o == 0) {
-        long long off = 0;
+        long long off = 0, big = 0;
         for (int q = 0; q < G; ++q) {
             const SectionLayout L = section_layout(meta->npts[q], meta->nrows[q], pay);
             meta->size[q] = L.size;
-            meta->off[q] = off;
+            meta->off[q] = cap > 0 ? q * cap : off;   // fixed-capacity sections (device-planned frames)
             off += L.size;
+            big = L.size > big ? L.size : big;
+        }
+        if (cap > 0 && abort) {
+            abort[6] = big;                  // the capacity this frame needs
+            if (big > cap) abort[5] = 1;     // pack skips; the frame is redone with a larger capacity
         }
     }
 }
@@ -143,7 +159,8 @@ __global__ void k_shard_plan(long long ntiles, int G, long long pay, long long* 
 __global__ void __launch_bounds__(kPlanThreads) k_shard_pack_points(
     long long n, int G, const unsigned* __restrict__ ptmask, const long long* __restrict__ tiles,
     const double4* __restrict__ ray, const int32_t* __restrict__ labels, int* __restrict__ ptpos,
-    const ShardMeta* __restrict__ meta, char* __restrict__ send, long long pay) {
+    const ShardMeta* __restrict__ meta, char* __restrict__ send, long long pay, const long long* abort) {
+    if (shard_aborted(abort, true)) return;
     using Scan = cub::BlockScan<int, kPlanThreads>;
     __shared__ typename Scan::TempStorage tmp;
     const long long i = (long long)blockIdx.x * kPlanThreads + threadIdx.x;
@@ -167,7 +184,8 @@ __global__ void __launch_bounds__(kPlanThreads) k_shard_pack_points(
 __global__ void k_shard_pack_feats(long long n, int G, const unsigned* __restrict__ ptmask,
                                    const int* __restrict__ ptpos, const char* __restrict__ feats,
                                    const ShardMeta* __restrict__ meta, char* __restrict__ send,
-                                   long long pay) {
+                                   long long pay, const long long* abort) {
+    if (shard_aborted(abort, true)) return;
     const int lane = threadIdx.x & 31;
     const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
     const long long words = pay / 4;
@@ -190,7 +208,9 @@ __global__ void k_shard_pack_feats(long long n, int G, const unsigned* __restric
 __global__ void __launch_bounds__(kPlanThreads) k_shard_pack_rows(
     long long R, long long n, int G, const unsigned long long* __restrict__ rowkey,
     const int* __restrict__ rowray, const int* __restrict__ rowown, const int* __restrict__ ptpos,
-    ShardMeta* meta, char* __restrict__ send, long long pay) {
+    ShardMeta* meta, char* __restrict__ send, long long pay, const FrameCtr* ctr, const long long* abort) {
+    if (R < 0) R = (long long)ctr->rows;
+    if (shard_aborted(abort, true)) return;
     __shared__ unsigned s_cnt[SVX_MAX_SHARDS];
     __shared__ unsigned long long s_base[SVX_MAX_SHARDS];
     if (blockIdx.x == 0 && threadIdx.x < G) {
@@ -265,6 +285,166 @@ void fill_summary(const svx_map* m, svx_shard_summary* out) {
     out->err_pack = hc->err_pack;
 }
 
+// ---- device-planned frames (svx_shard_*_async): one host sync per frame ----
+//
+// Summary vector (int64, SVX_SHARD_SUMMARY_WORDS): kSumWords counters summed
+// over ranks, then kMaxWords maxima (bbox_max, -bbox_min, and the slices'
+// scratch overflows: err_rows, err_cap).
+enum {
+    kSumPoints, kSumNonfinite, kSumRange, kSumDegenerate, kSumBadLabel, kSumUsed, kSumBandHits, kSumRows,
+    kSumErrBudget, kSumErrPack, kSumWords
+};
+constexpr int kMaxWords = 8;
+constexpr int kMaxErrRows = kSumWords + 6, kMaxErrCap = kSumWords + 7;
+static_assert(kSumWords == SVX_SHARD_SUM_WORDS && kSumWords + kMaxWords == SVX_SHARD_SUMMARY_WORDS,
+              "summary layout");
+
+__global__ void k_shard_summary(const FrameCtr* __restrict__ c, long long n, long long* __restrict__ v) {
+    v[kSumPoints] = n;
+    v[kSumNonfinite] = (long long)c->nonfinite;
+    v[kSumRange] = (long long)c->range;
+    v[kSumDegenerate] = (long long)c->degenerate;
+    v[kSumBadLabel] = (long long)c->bad_label;
+    v[kSumUsed] = (long long)c->used;
+    v[kSumBandHits] = (long long)c->band_hits;
+    v[kSumRows] = (long long)c->rows;
+    v[kSumErrBudget] = c->err_budget ? 1 : 0;
+    v[kSumErrPack] = c->err_pack ? 1 : 0;
+    for (int a = 0; a < 3; ++a) {
+        v[kSumWords + a] = c->rows ? c->bbox_max[a] : LLONG_MIN;
+        v[kSumWords + 3 + a] = c->rows ? -c->bbox_min[a] : LLONG_MIN;
+    }
+    v[kMaxErrRows] = c->err_rows ? 1 : 0;   // this slice's scratch was too small
+    v[kMaxErrCap] = c->err_cap ? 1 : 0;
+}
+
+// The reference's pre-allocation checks (_core.pyx:661-712, :386-387) on the
+// global summary, in shard_plan's order; every rank computes the same flags.
+//   abort[0] step budget  [1] extent  [2] coordinate range  [3] key window
+//   (re-march with the frame's minimum as key base)  [4] a slice's scratch
+//   overflowed  [5] a section over its capacity (this rank)  [6] largest
+//   section  [7] unused
+__global__ void k_shard_checks(const long long* __restrict__ g, long long* __restrict__ abort) {
+    for (int i = 0; i < SVX_SHARD_ABORT_WORDS; ++i) abort[i] = 0;
+    if (g[kMaxErrRows] | g[kMaxErrCap]) {
+        abort[4] = 1;
+        return;
+    }
+    if (g[kSumErrBudget]) {
+        abort[0] = 1;
+        return;
+    }
+    if (g[kSumRows]) {
+        bool extent = false, range = false;
+        for (int a = 0; a < 3; ++a) {
+            const long long hi = g[kSumWords + a], lo = -g[kSumWords + 3 + a];
+            if (hi - lo >= (1LL << kPackBits)) extent = true;
+            if (llabs(lo) >= kCoordLimit || llabs(hi) >= kCoordLimit) range = true;
+        }
+        if (extent) {
+            abort[1] = 1;
+            return;
+        }
+        if (range) {
+            abort[2] = 1;
+            return;
+        }
+    }
+    if (g[kSumErrPack]) abort[3] = 1;
+}
+
+// Received sections (fixed capacity each, rank order): validate the headers,
+// concatenation offsets and totals; the frame's row count goes to the
+// counters K2-K5 read, or the frame is dropped before any mutation (a global
+// abort, a corrupt section, or this rank's scratch too small: local[0] = 1).
+struct ApplyOffsets {
+    long long pt_off[SVX_MAX_SHARDS + 1];
+    long long row_off[SVX_MAX_SHARDS + 1];
+    unsigned npts[SVX_MAX_SHARDS], nrows[SVX_MAX_SHARDS];
+    int live;
+};
+
+__global__ void k_shard_apply_prep(const char* __restrict__ recv, long long cap, int G, long long pay,
+                                   const long long* __restrict__ abort, long long pcap, long long rcap,
+                                   FrameCtr* __restrict__ ctr, ApplyOffsets* __restrict__ ao,
+                                   long long* __restrict__ local) {
+    local[0] = local[1] = local[2] = 0;
+    ao->live = 0;
+    bool drop = shard_aborted(abort, false) || abort[5] != 0;
+    long long P = 0, R = 0;
+    ao->pt_off[0] = ao->row_off[0] = 0;
+    if (!drop) {
+        for (int q = 0; q < G; ++q) {
+            const SectionHeader hd = *reinterpret_cast<const SectionHeader*>(recv + q * cap);
+            if (hd.magic != kSectionMagic || (long long)hd.pay != pay ||
+                section_layout(hd.npts, hd.nrows, pay).size > cap) {
+                local[2] = 1;   // corrupt exchange
+                drop = true;
+                break;
+            }
+            ao->npts[q] = hd.npts;
+            ao->nrows[q] = hd.nrows;
+            P += hd.npts;
+            R += hd.nrows;
+            ao->pt_off[q + 1] = P;
+            ao->row_off[q + 1] = R;
+        }
+    }
+    if (!drop && (P > pcap || R > rcap)) {
+        local[0] = 1;   // grow and re-run this rank's apply
+        local[1] = R;
+        drop = true;
+    }
+    if (drop) {
+        ctr->abort = 1;
+        ctr->rows = ctr->rows_alloc = 0;
+        return;
+    }
+    ao->live = 1;
+    ctr->rows = ctr->rows_alloc = (unsigned long long)R;
+}
+
+// Sections -> the frame's point and row arrays (block y = source rank).
+__global__ void k_shard_apply_copy(const char* __restrict__ recv, long long cap, long long pay,
+                                   const ApplyOffsets* __restrict__ ao, double4* __restrict__ ray,
+                                   char* __restrict__ payload, unsigned long long* __restrict__ rowkey,
+                                   int* __restrict__ rowray) {
+    if (!ao->live) return;
+    const int q = blockIdx.y;
+    const long long np = ao->npts[q], nr = ao->nrows[q];
+    const SectionLayout L = section_layout(np, nr, pay);
+    const char* sec = recv + q * cap;
+    const long long p0 = ao->pt_off[q], r0 = ao->row_off[q];
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    const long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const double4* rs = reinterpret_cast<const double4*>(sec + L.rays);
+    for (long long i = t0; i < np; i += stride) ray[p0 + i] = rs[i];
+    if (pay) {
+        const long long words = np * pay / 4;   // payload rows are whole 4-byte words
+        const unsigned* src = reinterpret_cast<const unsigned*>(sec + L.pay);
+        unsigned* dst = reinterpret_cast<unsigned*>(payload + p0 * pay);
+        for (long long i = t0; i < words; i += stride) dst[i] = src[i];
+    }
+    const unsigned long long* ks = reinterpret_cast<const unsigned long long*>(sec + L.keys);
+    const int* ps = reinterpret_cast<const int*>(sec + L.pts);
+    for (long long i = t0; i < nr; i += stride) {
+        rowkey[r0 + i] = ks[i];
+        rowray[r0 + i] = ps[i] + (int)p0;
+    }
+}
+
+// Per-rank report words for the summed report: touched voxels, new leaves,
+// new voxels, and 1 when this rank must re-run its apply (scratch or pool
+// capacity; nothing was changed).
+__global__ void k_shard_apply_report(const FrameCtr* __restrict__ c, long long nblocks0, long long nvox0,
+                                     const long long* __restrict__ local, long long* __restrict__ rep) {
+    const bool redo = local[0] != 0 || c->err_cap != 0;
+    rep[0] = redo ? 0 : (long long)c->n_touched;
+    rep[1] = redo ? 0 : (long long)c->nblocks - nblocks0;
+    rep[2] = redo ? 0 : (long long)c->nvox - nvox0;
+    rep[3] = redo ? 1 : 0;
+}
+
 }  // namespace
 
 svx_status shard_march(svx_map* m, const void* pts_in, int pts_f64, int64_t n, const PoseParams& pp,
@@ -278,6 +458,7 @@ svx_status shard_march(svx_map* m, const void* pts_in, int pts_f64, int64_t n, c
     if (n < 0) return fail(SVX_E_INPUT, "negative point count");
     if (n >= (int64_t)INT_MAX) return fail(SVX_E_INPUT, "point count exceeds 2^31-1");
     m->shard_phase = 0;
+    m->shard_async = 0;
     m->shard_n = n;
     m->shard_rows = 0;
     m->shard_pts_f64 = pts_f64;
@@ -392,7 +573,7 @@ svx_status shard_plan(svx_map* m, const svx_shard_summary* g, int rank, int G, i
     if (R > 0) {
         k_shard_rows<<<grid_of(R, kPlanThreads, kPersistentBlocks * 2), kPlanThreads, 0, s>>>(
             R, G, m->shard_kp, ptr<unsigned long long>(m->rowkey), ptr<int>(m->rowray),
-            ptr<int>(m->rowvid), ptr<unsigned>(m->sh_mask), meta);
+            ptr<int>(m->rowvid), ptr<unsigned>(m->sh_mask), meta, ptr<FrameCtr>(m->ctr), nullptr);
         SVX_LAUNCHED();
     }
     if (n > 0) {
@@ -402,7 +583,7 @@ svx_status shard_plan(svx_map* m, const svx_shard_summary* g, int rank, int G, i
     } else {
         SVX_CUDA(cudaMemsetAsync(m->sh_tiles.p, 0, sizeof(long long) * ntiles * G, s));
     }
-    k_shard_plan<<<1, 32, 0, s>>>(ntiles, G, pay, ptr<long long>(m->sh_tiles), meta);
+    k_shard_plan<<<1, 32, 0, s>>>(ntiles, G, pay, ptr<long long>(m->sh_tiles), meta, 0, nullptr);
     SVX_LAUNCHED();
     ShardMeta hm;
     SVX_CUDA(cudaMemcpyAsync(&hm, meta, sizeof(ShardMeta), cudaMemcpyDeviceToHost, s));
@@ -433,18 +614,18 @@ svx_status shard_pack(svx_map* m, void* send, int64_t capacity, cudaStream_t s) 
         k_shard_pack_points<<<(int)ntiles, kPlanThreads, 0, s>>>(
             n, G, ptr<unsigned>(m->sh_mask), ptr<long long>(m->sh_tiles), ptr<double4>(m->ray),
             m->cfg.sem_kind == SVX_SEM_CLOSED ? (const int32_t*)m->shard_lab : nullptr,
-            ptr<int>(m->sh_pos), meta, (char*)send, pay);
+            ptr<int>(m->sh_pos), meta, (char*)send, pay, nullptr);
         SVX_LAUNCHED();
         if (m->cfg.sem_kind == SVX_SEM_OPEN) {
             k_shard_pack_feats<<<grid_of(n * 32, 256, kPersistentBlocks * 2), 256, 0, s>>>(
                 n, G, ptr<unsigned>(m->sh_mask), ptr<int>(m->sh_pos), (const char*)m->shard_feat,
-                meta, (char*)send, pay);
+                meta, (char*)send, pay, nullptr);
             SVX_LAUNCHED();
         }
     }
     k_shard_pack_rows<<<grid_of(R, kPlanThreads, kPersistentBlocks * 2), kPlanThreads, 0, s>>>(
         R, n, G, ptr<unsigned long long>(m->rowkey), ptr<int>(m->rowray), ptr<int>(m->rowvid),
-        ptr<int>(m->sh_pos), meta, (char*)send, pay);
+        ptr<int>(m->sh_pos), meta, (char*)send, pay, ptr<FrameCtr>(m->ctr), nullptr);
     SVX_LAUNCHED();
     m->shard_phase = 3;
     return SVX_OK;
@@ -576,6 +757,269 @@ svx_status shard_apply(svx_map* m, const void* recv, const int64_t* recv_bytes, 
     finish_frame(m, nblocks0, nvox0, r);
     m->frames++;
     m->shard_phase = 0;
+    if (rep) *rep = r;
+    return SVX_OK;
+}
+
+// ---- device-planned frames --------------------------------------------------
+
+svx_status shard_march_async(svx_map* m, const void* pts_in, int pts_f64, int64_t n, const PoseParams& pp,
+                             const int32_t* labels_in, const void* feats_in, int feats_f64,
+                             const int64_t* key_base, cudaStream_t s, int64_t* summary) {
+    const int kind = m->cfg.sem_kind;
+    if (kind == SVX_SEM_CLOSED && !labels_in && n > 0)
+        return fail(SVX_E_PAYLOAD, "closed-set grid requires per-point labels");
+    if (kind == SVX_SEM_OPEN && !feats_in && n > 0)
+        return fail(SVX_E_PAYLOAD, "open-set grid requires per-point features");
+    if (n < 0) return fail(SVX_E_INPUT, "negative point count");
+    if (n >= (int64_t)INT_MAX) return fail(SVX_E_INPUT, "point count exceeds 2^31-1");
+    if (!is_device_ptr(summary)) return fail(SVX_E_INPUT, "shard summary must be device memory");
+    m->shard_phase = 0;
+    m->shard_n = n;
+    m->shard_rows = -1;   // on the device
+    m->shard_pts_f64 = pts_f64;
+    m->shard_feats_f64 = feats_f64;
+    m->shard_pp = pp;
+    KeyPack kp = default_key_pack(m, pp);
+    if (key_base)
+        for (int a = 0; a < 3; ++a) kp.base[a] = key_base[a];
+    m->shard_kp = kp;
+    m->shard_lab = nullptr;
+    m->shard_feat = nullptr;
+    FrameCtr* hc = m->h_ctr;
+    FrameCtr* dc = ptr<FrameCtr>(m->ctr);
+    const void* pts = nullptr;
+    const void* feats = nullptr;
+    const void* labv = nullptr;
+    if (n > 0) {
+        SVX_TRY(stage_in(pts_in, (size_t)n * 3 * (pts_f64 ? 8 : 4), m->in_pts, s, &pts));
+        if (kind == SVX_SEM_CLOSED) SVX_TRY(stage_in(labels_in, (size_t)n * 4, m->in_lab, s, &labv));
+        if (kind == SVX_SEM_OPEN)
+            SVX_TRY(stage_in(feats_in, (size_t)n * m->payload_d * (feats_f64 ? 8 : 4), m->in_feat, s,
+                             &feats));
+        init_row_space(m, n);
+        // the slice's rows are at most the frame's (last frame + half); an
+        // overflow is caught on the device and the frame redone
+        m->rcap = std::max<uint64_t>(m->rcap, (uint64_t)(m->sh_last_rows + m->sh_last_rows / 2 + 4096));
+        SVX_TRY(reserve_frame(m, n, s));
+    }
+    m->frame_slots = 0;
+    reset_ctr(m, m->frames);
+    FrameParams& p = hc->p;
+    p.pts = pts;
+    p.labels = (const int32_t*)labv;
+    p.feats = feats;
+    p.n = n;
+    p.pp = pp;
+    p.kp = kp;
+    p.nblocks0 = m->nblocks;
+    hc->p.epilogue = 0;
+    m->ctr_clean = false;
+    SVX_CUDA(cudaMemcpyAsync(dc, hc, sizeof(FrameCtr), cudaMemcpyHostToDevice, s));
+    if (n > 0) SVX_TRY(launch_march(m, pts_f64, feats_f64, s));
+    k_shard_summary<<<1, 1, 0, s>>>(dc, n, (long long*)summary);
+    SVX_LAUNCHED();
+    m->shard_lab = labv;
+    m->shard_feat = feats;
+    m->shard_async = 1;
+    m->shard_phase = 1;
+    return SVX_OK;
+}
+
+svx_status shard_plan_async(svx_map* m, const int64_t* gsum, int rank, int G, int64_t cap, cudaStream_t s,
+                            int64_t* abort) {
+    if (m->shard_phase != 1 || !m->shard_async) return fail(SVX_E_INPUT, "svx_shard_plan_async: no marched frame");
+    if (G < 1 || G > SVX_MAX_SHARDS || rank < 0 || rank >= G)
+        return fail(SVX_E_INPUT, "invalid shard rank / count");
+    if (cap < 64 || (cap & 15)) return fail(SVX_E_INPUT, "shard section capacity must be a multiple of 16 >= 64");
+    if (!is_device_ptr(gsum) || !is_device_ptr(abort))
+        return fail(SVX_E_INPUT, "shard summary / abort words must be device memory");
+    m->shard_g = G;
+    m->shard_rank = rank;
+    m->sh_cap = cap;
+    const long long n = m->shard_n;
+    const long long pay = payload_bytes(m, m->shard_feats_f64);
+    const long long ntiles = std::max<long long>(1, (n + kPlanThreads - 1) / kPlanThreads);
+    SVX_TRY(ensure(m->sh_meta, sizeof(ShardMeta), s));
+    SVX_TRY(ensure(m->sh_mask, sizeof(unsigned) * std::max<long long>(n, 1), s));
+    SVX_TRY(ensure(m->sh_pos, sizeof(int) * std::max<long long>(n, 1) * G, s));
+    SVX_TRY(ensure(m->sh_tiles, sizeof(long long) * ntiles * G, s));
+    ShardMeta* meta = ptr<ShardMeta>(m->sh_meta);
+    long long* ab = (long long*)abort;
+    SVX_CUDA(cudaMemsetAsync(meta, 0, sizeof(ShardMeta), s));
+    k_shard_checks<<<1, 1, 0, s>>>((const long long*)gsum, ab);
+    SVX_LAUNCHED();
+    if (n > 0) {
+        SVX_CUDA(cudaMemsetAsync(m->sh_mask.p, 0, sizeof(unsigned) * n, s));
+        k_shard_rows<<<kPersistentBlocks * 2, kPlanThreads, 0, s>>>(
+            -1, G, m->shard_kp, ptr<unsigned long long>(m->rowkey), ptr<int>(m->rowray),
+            ptr<int>(m->rowvid), ptr<unsigned>(m->sh_mask), meta, ptr<FrameCtr>(m->ctr), ab);
+        SVX_LAUNCHED();
+        k_shard_tiles<<<(int)ntiles, kPlanThreads, 0, s>>>(n, G, ptr<unsigned>(m->sh_mask),
+                                                           ptr<long long>(m->sh_tiles));
+        SVX_LAUNCHED();
+    } else {
+        SVX_CUDA(cudaMemsetAsync(m->sh_tiles.p, 0, sizeof(long long) * ntiles * G, s));
+    }
+    k_shard_plan<<<1, 32, 0, s>>>(ntiles, G, pay, ptr<long long>(m->sh_tiles), meta, cap, ab);
+    SVX_LAUNCHED();
+    m->shard_phase = 2;
+    return SVX_OK;
+}
+
+svx_status shard_pack_async(svx_map* m, void* send, int64_t cap, cudaStream_t s, const int64_t* abort) {
+    if (m->shard_phase != 2 || !m->shard_async) return fail(SVX_E_INPUT, "svx_shard_pack_async: no planned frame");
+    if (cap != m->sh_cap) return fail(SVX_E_INPUT, "svx_shard_pack_async: capacity differs from plan");
+    if (!send || ((uintptr_t)send & 15) != 0 || !is_device_ptr(send))
+        return fail(SVX_E_INPUT, "shard send buffer must be 16-byte aligned device memory");
+    const int G = m->shard_g;
+    const long long n = m->shard_n;
+    const long long pay = payload_bytes(m, m->shard_feats_f64);
+    ShardMeta* meta = ptr<ShardMeta>(m->sh_meta);
+    const long long* ab = (const long long*)abort;
+    if (n > 0) {
+        const long long ntiles = (n + kPlanThreads - 1) / kPlanThreads;
+        k_shard_pack_points<<<(int)ntiles, kPlanThreads, 0, s>>>(
+            n, G, ptr<unsigned>(m->sh_mask), ptr<long long>(m->sh_tiles), ptr<double4>(m->ray),
+            m->cfg.sem_kind == SVX_SEM_CLOSED ? (const int32_t*)m->shard_lab : nullptr,
+            ptr<int>(m->sh_pos), meta, (char*)send, pay, ab);
+        SVX_LAUNCHED();
+        if (m->cfg.sem_kind == SVX_SEM_OPEN) {
+            k_shard_pack_feats<<<grid_of(n * 32, 256, kPersistentBlocks * 2), 256, 0, s>>>(
+                n, G, ptr<unsigned>(m->sh_mask), ptr<int>(m->sh_pos), (const char*)m->shard_feat,
+                meta, (char*)send, pay, ab);
+            SVX_LAUNCHED();
+        }
+    }
+    k_shard_pack_rows<<<kPersistentBlocks * 2, kPlanThreads, 0, s>>>(
+        -1, n, G, ptr<unsigned long long>(m->rowkey), ptr<int>(m->rowray), ptr<int>(m->rowvid),
+        ptr<int>(m->sh_pos), meta, (char*)send, pay, ptr<FrameCtr>(m->ctr), ab);
+    SVX_LAUNCHED();
+    m->shard_phase = 3;
+    return SVX_OK;
+}
+
+svx_status shard_apply_async(svx_map* m, const void* recv, int64_t cap, int G, const int64_t* abort,
+                             int64_t frame_points, cudaStream_t s, int64_t* rep_words) {
+    if ((m->shard_phase != 3 && m->shard_phase != 5) || !m->shard_async)
+        return fail(SVX_E_INPUT, "svx_shard_apply_async: no packed frame");
+    if (G != m->shard_g || cap != m->sh_cap) return fail(SVX_E_INPUT, "svx_shard_apply_async: plan mismatch");
+    if (!recv || ((uintptr_t)recv & 15) != 0 || !is_device_ptr(recv) || !is_device_ptr(rep_words))
+        return fail(SVX_E_INPUT, "shard receive buffer / report words must be device memory");
+    if (frame_points < 0) return fail(SVX_E_INPUT, "negative frame point count");
+    if (!m->sh_hlocal) SVX_CUDA(cudaMallocHost((void**)&m->sh_hlocal, 4 * sizeof(long long)));
+    const long long pay = payload_bytes(m, m->shard_feats_f64);
+    if (m->shard_phase == 3) {   // (a re-run keeps the frame's starting counts: the
+        m->sh_nblocks0 = m->nblocks;   //  failed attempt's leaves stay allocated)
+        m->sh_nvox0 = m->nvox;
+    }
+    const int64_t nblocks0 = m->sh_nblocks0, nvox0 = m->sh_nvox0;
+    const int64_t P = std::max<int64_t>(frame_points, 1);   // a point reaches a rank at most once
+    init_row_space(m, P);
+    m->rcap = std::max<uint64_t>(m->rcap, (uint64_t)(m->sh_last_rows + m->sh_last_rows / 2 + 4096));
+    SVX_TRY(reserve_frame(m, P, s));
+    if (pay) {
+        DevBuf& pb = m->cfg.sem_kind == SVX_SEM_OPEN ? m->in_feat : m->in_lab;
+        SVX_TRY(ensure(pb, (size_t)(P * pay), s));
+    }
+    SVX_TRY(reserve_pools(m, s));
+    SVX_TRY(ensure(m->sh_ao, sizeof(ApplyOffsets) + 4 * sizeof(long long), s));
+    ApplyOffsets* ao = ptr<ApplyOffsets>(m->sh_ao);
+    long long* local = reinterpret_cast<long long*>(ptr<char>(m->sh_ao) + sizeof(ApplyOffsets));
+    FrameCtr* hc = m->h_ctr;
+    FrameCtr* dc = ptr<FrameCtr>(m->ctr);
+    reset_ctr(m, m->frames);
+    FrameParams& p = hc->p;
+    p.pts = nullptr;
+    p.labels = m->cfg.sem_kind == SVX_SEM_CLOSED ? ptr<int32_t>(m->in_lab) : nullptr;
+    p.feats = m->cfg.sem_kind == SVX_SEM_OPEN ? m->in_feat.p : nullptr;
+    p.n = P;
+    p.pp = m->shard_pp;
+    p.kp = m->shard_kp;
+    p.nblocks0 = nblocks0;
+    p.slots = 0;   // shard sections always take the segment path
+    hc->p.epilogue = 0;
+    m->ctr_clean = false;
+    SVX_CUDA(cudaMemcpyAsync(dc, hc, sizeof(FrameCtr), cudaMemcpyHostToDevice, s));
+    SVX_CUDA(cudaEventRecord(m->ev0, s));
+    k_shard_apply_prep<<<1, 1, 0, s>>>((const char*)recv, cap, G, pay, (const long long*)abort,
+                                       (long long)m->npts_cap, (long long)m->rcap, dc, ao, local);
+    SVX_LAUNCHED();
+    char* payload = pay ? (char*)(m->cfg.sem_kind == SVX_SEM_OPEN ? m->in_feat.p : m->in_lab.p) : nullptr;
+    k_shard_apply_copy<<<dim3(std::max(1, kPersistentBlocks / std::max(1, G)), G), 256, 0, s>>>(
+        (const char*)recv, cap, pay, ao, ptr<double4>(m->ray), payload, ptr<unsigned long long>(m->rowkey),
+        ptr<int>(m->rowray));
+    SVX_LAUNCHED();
+    const int feats_f64 = m->shard_feats_f64;
+    SVX_TRY(launch_resolve(m, s));
+    SVX_TRY(launch_segments(m, s));
+    SVX_TRY(launch_scatter(m, s));
+    SVX_TRY(launch_update_a(m, feats_f64, s));
+    SVX_TRY(launch_update_b(m, feats_f64, s));
+    k_shard_apply_report<<<1, 1, 0, s>>>(dc, nblocks0, nvox0, local, (long long*)rep_words);
+    SVX_LAUNCHED();
+    SVX_CUDA(cudaMemcpyAsync(hc, dc, sizeof(FrameCtr), cudaMemcpyDeviceToHost, s));
+    SVX_CUDA(cudaMemcpyAsync(m->sh_hlocal, local, 3 * sizeof(long long), cudaMemcpyDeviceToHost, s));
+    SVX_CUDA(cudaEventRecord(m->ev1, s));
+    m->shard_phase = 4;
+    return SVX_OK;
+}
+
+svx_status shard_finish(svx_map* m, const int64_t* g, const int64_t* abort, const int64_t* rsum,
+                        svx_report* rep, int32_t* action, int64_t* need) {
+    if (m->shard_phase != 4 || !m->shard_async) return fail(SVX_E_INPUT, "svx_shard_finish: no applied frame");
+    SVX_CUDA(cudaEventSynchronize(m->ev1));   // (the caller has synchronised; cheap)
+    *action = 0;
+    *need = 0;
+    FrameCtr* hc = m->h_ctr;
+    const long long* loc = m->sh_hlocal;
+    if (abort[4]) {   // a slice's scratch overflowed: larger row space, then redo everywhere
+        if (g[kMaxErrRows]) m->maxrows = 0;
+        m->rcap = std::max<uint64_t>(2 * m->rcap, (uint64_t)g[kSumRows] + (uint64_t)g[kSumRows] / 2 + 4096);
+        m->shard_phase = 0;
+        *action = 1;
+        return SVX_OK;
+    }
+    m->shard_phase = 0;
+    if (abort[0]) return fail(SVX_E_INTERNAL, "ray band exceeds step budget; shrink max_range or grow voxels");
+    if (abort[1])
+        return fail(SVX_E_INTERNAL, "frame voxel extent exceeds 2^21 per axis; shrink max_range or grow voxels");
+    if (abort[2]) return fail(SVX_E_RANGE, "voxel coordinate beyond +/-2^30 addressable range");
+    if (abort[3] || abort[5]) {   // key rebase / larger sections: redo the frame everywhere
+        *need = abort[5] ? abort[6] : 0;
+        *action = 1;
+        return SVX_OK;
+    }
+    if (loc[2]) return fail(SVX_E_INTERNAL, "corrupt shard exchange: section header mismatch");
+    const int64_t nblocks0 = m->sh_nblocks0, nvox0 = m->sh_nvox0;
+    if (loc[0] || hc->err_cap) {   // this rank's scratch or pools: grow, redo its apply
+        if (hc->err_cap) SVX_TRY(recover_capacity(m, nblocks0, 0));
+        if (loc[0]) m->rcap = std::max<uint64_t>(m->rcap, (uint64_t)loc[1] + (uint64_t)loc[1] / 2 + 4096);
+        m->shard_phase = 5;   // packed sections still in the receive buffer
+        *action = 2;
+        return SVX_OK;
+    }
+    svx_report r;
+    memset(&r, 0, sizeof(r));
+    r.points_in = g[kSumPoints];
+    r.skipped_nonfinite = g[kSumNonfinite];
+    r.skipped_range = g[kSumRange];
+    r.skipped_degenerate = g[kSumDegenerate];
+    r.skipped_bad_label = g[kSumBadLabel];
+    r.points_used = g[kSumUsed];
+    r.band_hits = g[kSumBandHits];
+    float ms = 0.f;
+    SVX_CUDA(cudaEventElapsedTime(&ms, m->ev0, m->ev1));
+    r.kernel_ms = ms;
+    finish_frame(m, nblocks0, nvox0, r);
+    m->sh_last_rows = std::max<int64_t>((int64_t)g[kSumRows], (int64_t)hc->rows);
+    m->frames++;
+    if (rsum) {
+        r.touched_voxels = rsum[0];
+        r.new_blocks = rsum[1];
+        r.new_voxels = rsum[2];
+        if (rsum[3] > 0) *action = 3;
+    }
     if (rep) *rep = r;
     return SVX_OK;
 }

@@ -19,6 +19,13 @@ Two drivers share the per-rank phases:
 * ``integrate_loopback`` -- all G shards in one process (one GPU), the
   exchange done by device copies; used by the single-GPU parity tests.
 
+Each driver runs a frame in one of two plans.  The host plan reads every
+phase's result back (summaries, section sizes, headers, report: about seven
+host synchronisations per frame).  The device plan (``device_plan=True``, the
+default with NCCL) keeps sizes and checks on the device: fixed-capacity
+sections, all-to-all of equal blocks, abort words reduced on the device, and
+one host synchronisation after the last collective (``svx_shard_*_async``).
+
 Queries gather per-shard results and merge them into the reference's global
 active order with the leaf stamps (creation frame, smallest packed key).
 """
@@ -30,7 +37,8 @@ import ctypes
 import numpy as np
 
 from . import _lib
-from ._lib import MAX_SHARDS, SVX_F32, SvxShardSummary, check, lib
+from ._lib import (MAX_SHARDS, SHARD_ABORT_WORDS, SHARD_SUM_WORDS, SHARD_SUMMARY_WORDS, SVX_F32,
+                   SvxShardSummary, check, lib)
 from .errors import UserInputError
 from .mapper import IntegrationReport, Mapper, _check_pose, content_hash_of
 
@@ -126,6 +134,27 @@ class DistTransport:
                                group=self.group)
         return recv, recv_sizes
 
+    # -- device-plan collectives (device tensors in, in place; gloo stages through host) --
+
+    def all_reduce(self, tensor, op: str):
+        dist = self._dist
+        rop = dist.ReduceOp.SUM if op == "sum" else dist.ReduceOp.MAX
+        if self.device.type == "cuda":
+            dist.all_reduce(tensor, op=rop, group=self.group)
+        else:
+            t = tensor.cpu()
+            dist.all_reduce(t, op=rop, group=self.group)
+            tensor.copy_(t)
+
+    def all_to_all_equal(self, recv, send):
+        """Equal-size blocks: send[q*cap:(q+1)*cap] to rank q, in rank order."""
+        if self.device.type == "cuda":
+            self._dist.all_to_all_single(recv, send, group=self.group)
+        else:
+            r = recv.new_empty(recv.shape, device="cpu")
+            self._dist.all_to_all_single(r, send.cpu(), group=self.group)
+            recv.copy_(r)
+
     def gather_objects(self, obj, dst: int = 0):
         out = [None] * self.world if self.rank == dst else None
         self._dist.gather_object(obj, out, dst=dst, group=self.group)
@@ -150,6 +179,10 @@ class ShardedMapper(Mapper):
         super().__init__(config, **overrides)
         self.rank, self.world = int(rank), int(world)
         self.transport = transport
+        self.device_plan = None      # None: device plan when the transport is on CUDA
+        self._cap = 0                # device plan: section capacity per destination (bytes)
+        self._bufs = {}
+        self.host_syncs = 0          # device plan: host synchronisations of the last frame
 
     # -- per-rank phases (shared by both drivers) ----------------------------
 
@@ -194,6 +227,125 @@ class ShardedMapper(Mapper):
         self._frames += 1
         return rep
 
+    # -- device-plan phases (one host synchronisation per frame) ---------------
+
+    def _buf(self, name, nbytes, device):
+        import torch
+
+        b = self._bufs.get(name)
+        if b is None or b.numel() < nbytes:
+            b = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=device)
+            self._bufs[name] = b
+        return b[:nbytes]
+
+    def _initial_cap(self, n_frame):
+        pay = 0
+        if self._c.sem_kind == _lib.SEM_CLOSED:
+            pay = 4
+        elif self._c.sem_kind == _lib.SEM_OPEN:
+            pay = 8 * int(self._c.feature_dim)
+        # a slice's points and ~8 rows each, twice over for an uneven split
+        per = -(-int(n_frame) // self.world)
+        cap = 2 * per * (32 + pay + 8 * 12) + 65536
+        return (cap + 15) // 16 * 16
+
+    def _march_async(self, pts, vec, sensor, lab, feat, key_base, summary):
+        v = np.ascontiguousarray(vec, np.float64)
+        vp = v.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+        kb = None
+        if key_base is not None:
+            kba = np.ascontiguousarray(key_base, np.int64)
+            kb = kba.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
+        n = int(pts.shape[0])
+        check(lib.svx_shard_march_async(self._handle, pts.ptr, pts.code, n, vp if sensor else None,
+                                        None if sensor else vp,
+                                        lab.ptr if lab is not None else None,
+                                        feat.ptr if feat is not None else None,
+                                        feat.code if feat is not None else SVX_F32, kb,
+                                        self._stream_handle(), ctypes.c_void_p(summary.data_ptr())))
+
+    def _plan_async(self, gsum, cap, abort):
+        check(lib.svx_shard_plan_async(self._handle, ctypes.c_void_p(gsum.data_ptr()), self.rank, self.world,
+                                       int(cap), self._stream_handle(), ctypes.c_void_p(abort.data_ptr())))
+
+    def _pack_async(self, send, cap, abort):
+        check(lib.svx_shard_pack_async(self._handle, ctypes.c_void_p(send.data_ptr()), int(cap),
+                                       self._stream_handle(), ctypes.c_void_p(abort.data_ptr())))
+
+    def _apply_async(self, recv, cap, abort, n_frame, rep):
+        check(lib.svx_shard_apply_async(self._handle, ctypes.c_void_p(recv.data_ptr()), int(cap), self.world,
+                                        ctypes.c_void_p(abort.data_ptr()), int(n_frame),
+                                        self._stream_handle(), ctypes.c_void_p(rep.data_ptr())))
+
+    def _finish(self, summary, abort, rep_sum):
+        """After the frame's host synchronisation: (action, need, SvxReport)."""
+        sm = np.ascontiguousarray(summary, np.int64)
+        ab = np.ascontiguousarray(abort, np.int64)
+        rs = None if rep_sum is None else np.ascontiguousarray(rep_sum, np.int64)
+        P = ctypes.POINTER(ctypes.c_int64)
+        rep = _lib.SvxReport()
+        action, need = ctypes.c_int32(), ctypes.c_int64()
+        check(lib.svx_shard_finish(self._handle, sm.ctypes.data_as(P), ab.ctypes.data_as(P),
+                                   rs.ctypes.data_as(P) if rs is not None else None, ctypes.byref(rep),
+                                   ctypes.byref(action), ctypes.byref(need)))
+        if action.value == 0 or action.value == 3:
+            self._frames += 1
+        return action.value, int(need.value), rep
+
+    def _redo_setup(self, host, need):
+        """Frame-level redo (action 1): larger sections or the rebased key window."""
+        if need:
+            self._cap = (need + need // 4 + 15) // 16 * 16
+        ab = host[SHARD_SUMMARY_WORDS:SHARD_SUMMARY_WORDS + SHARD_ABORT_WORDS]
+        if ab[3]:   # key window: the frame's minimum as key base
+            return [-int(host[SHARD_SUM_WORDS + 3 + a]) for a in range(3)]
+        return None
+
+    def _integrate_dev(self, pts, vec, sensor, lab, feat, n_frame):
+        import torch
+
+        t = self.transport
+        device = torch.device("cuda", torch.cuda.current_device())
+        G, S, A = self.world, SHARD_SUMMARY_WORDS, SHARD_ABORT_WORDS
+        if self._cap == 0:
+            self._cap = self._initial_cap(n_frame)
+        key_base = None
+        self.host_syncs = 0
+        while True:
+            cap = self._cap
+            words = torch.empty(S + A + 4, dtype=torch.int64, device=device)
+            summ, abort, rep = words[:S], words[S:S + A], words[S + A:]
+            self._march_async(pts, vec, sensor, lab, feat, key_base, summ)
+            t.all_reduce(summ[:SHARD_SUM_WORDS], "sum")
+            t.all_reduce(summ[SHARD_SUM_WORDS:], "max")
+            self._plan_async(summ, cap, abort)
+            send = self._buf("send", G * cap, device)
+            self._pack_async(send, cap, abort)
+            t.all_reduce(abort, "max")
+            recv = self._buf("recv", G * cap, device)
+            t.all_to_all_equal(recv, send)
+            self._apply_async(recv, cap, abort, n_frame, rep)
+            mine = rep.clone()
+            t.all_reduce(rep, "sum")
+            host = words.cpu().numpy()      # the frame's one host synchronisation
+            self.host_syncs += 1
+            action, need, r = self._finish(host[:S], host[S:S + A], host[S + A:])
+            while action in (2, 3):          # a rank re-runs its apply (scratch or pools grown)
+                if action == 2:
+                    self._apply_async(recv, cap, abort, n_frame, mine)
+                rs = mine.clone()
+                t.all_reduce(rs, "sum")
+                hr = rs.cpu().numpy()
+                self.host_syncs += 1
+                if action == 2:
+                    action, need, r = self._finish(host[:S], host[S:S + A], hr)
+                else:
+                    r.touched_voxels, r.new_blocks, r.new_voxels = int(hr[0]), int(hr[1]), int(hr[2])
+                    action = 3 if hr[3] > 0 else 0
+            if action == 0:
+                return r
+            key_base = self._redo_setup(host, need)
+
     def _stream_handle(self):
         """All four calls of a frame run on the current torch stream of the
         map's device."""
@@ -210,12 +362,15 @@ class ShardedMapper(Mapper):
 
     # -- distributed driver --------------------------------------------------
 
-    def _integrate_dist(self, pts, vec, sensor, lab, feat, reduce_report):
+    def _integrate_dist(self, pts, vec, sensor, lab, feat, reduce_report, n_frame=None):
         import torch
 
         t = self.transport
         if t is None:
             raise UserInputError("ShardedMapper.integrate needs a transport (DistTransport)")
+        dev_plan = self.device_plan if self.device_plan is not None else t.device.type == "cuda"
+        if dev_plan:
+            return _report(self._integrate_dev(pts, vec, sensor, lab, feat, n_frame))
         device = torch.device("cuda", torch.cuda.current_device())
         key_base = None
         while True:
@@ -240,16 +395,18 @@ class ShardedMapper(Mapper):
         into the sharded map; see Mapper.integrate.  ``reduce_report`` sums
         touched/new counts over ranks (one small all-reduce)."""
         pose = _check_pose(pose, self._frames)
+        n_frame = int(self._points_arg(points).shape[0])
         pts, lab, feat = self._slice_inputs(points, labels, features)
-        return self._integrate_dist(pts, pose.reshape(-1), True, lab, feat, reduce_report)
+        return self._integrate_dist(pts, pose.reshape(-1), True, lab, feat, reduce_report, n_frame)
 
     def integrate_world(self, points_world, origin, labels=None, features=None,
                         reduce_report=True):
         o = np.asarray(origin, np.float64).reshape(-1)
         if o.shape != (3,) or not np.isfinite(o).all():
             raise UserInputError("origin must be a finite 3-vector")
+        n_frame = int(self._points_arg(points_world).shape[0])
         pts, lab, feat = self._slice_inputs(points_world, labels, features)
-        return self._integrate_dist(pts, o, False, lab, feat, reduce_report)
+        return self._integrate_dist(pts, o, False, lab, feat, reduce_report, n_frame)
 
     # -- shard-local readouts and the merged global view -----------------------
 
@@ -350,10 +507,12 @@ def merge_by_stamps(parts):
     return tuple(c[order] if c is not None else None for c in cat[:-2])
 
 
-def integrate_loopback(shards, points, pose=None, origin=None, labels=None, features=None):
+def integrate_loopback(shards, points, pose=None, origin=None, labels=None, features=None,
+                       device_plan=False):
     """Integrate one frame into G in-process shards (one GPU): the same phases
     as the distributed driver, with the summary reduction and the all-to-all
-    done in-process.  Returns the frame's IntegrationReport."""
+    done in-process.  Returns the frame's IntegrationReport.  ``device_plan``
+    runs the one-synchronisation plan (svx_shard_*_async)."""
     import torch
 
     G = len(shards)
@@ -364,6 +523,9 @@ def integrate_loopback(shards, points, pose=None, origin=None, labels=None, feat
     vec = (_check_pose(pose, shards[0]._frames).reshape(-1) if sensor
            else np.asarray(origin, np.float64).reshape(-1))
     inputs = [s._slice_inputs(points, labels, features) for s in shards]
+    if device_plan:
+        n_frame = int(shards[0]._points_arg(points).shape[0])
+        return _report(_loopback_dev(shards, inputs, vec, sensor, n_frame, device))
     key_base = None
     while True:
         locals_ = [s._march(inp[0], vec, sensor, inp[1], inp[2], key_base)
@@ -386,6 +548,65 @@ def integrate_loopback(shards, points, pose=None, origin=None, labels=None, feat
         reps.append(s._apply(recv, sizes, device))
     sums = np.sum([[r.touched_voxels, r.new_blocks, r.new_voxels] for r in reps], axis=0)
     return _report(reps[0], sums)
+
+
+def _loopback_dev(shards, inputs, vec, sensor, n_frame, device):
+    """integrate_loopback's device plan: the G shards' phases in lock step,
+    the collectives as device reductions and block copies, one host
+    synchronisation per frame (plus one per rare apply re-run)."""
+    import torch
+
+    G, S, A, SW = len(shards), SHARD_SUMMARY_WORDS, SHARD_ABORT_WORDS, SHARD_SUM_WORDS
+    for s in shards:
+        if s._cap == 0:
+            s._cap = s._initial_cap(n_frame)
+    key_base = None
+    syncs = 0
+    while True:
+        cap = max(s._cap for s in shards)
+        words = torch.empty((G, S + A + 4), dtype=torch.int64, device=device)
+        for s, inp, w in zip(shards, inputs, words):
+            s._march_async(inp[0], vec, sensor, inp[1], inp[2], key_base, w[:S])
+        words[:, :SW] = words[:, :SW].sum(0)
+        words[:, SW:S] = words[:, SW:S].max(0).values
+        sends = []
+        for s, w in zip(shards, words):
+            s._plan_async(w[:S], cap, w[S:S + A])
+            send = s._buf("send", G * cap, device)
+            s._pack_async(send, cap, w[S:S + A])
+            sends.append(send)
+        words[:, S:S + A] = words[:, S:S + A].max(0).values
+        for q, (s, w) in enumerate(zip(shards, words)):
+            recv = s._buf("recv", G * cap, device)
+            for src in range(G):
+                recv[src * cap:(src + 1) * cap].copy_(sends[src][q * cap:(q + 1) * cap])
+            s._apply_async(recv, cap, w[S:S + A], n_frame, w[S + A:])
+        mine = words[:, S + A:].clone()
+        words[:, S + A:] = words[:, S + A:].sum(0)
+        host = words.cpu().numpy()           # the frame's one host synchronisation
+        syncs += 1
+        res = [s._finish(h[:S], h[S:S + A], h[S + A:]) for s, h in zip(shards, host)]
+        while any(a in (2, 3) for a, _, _ in res):
+            for i, (s, (a, _, _)) in enumerate(zip(shards, res)):
+                if a == 2:
+                    s._apply_async(s._bufs["recv"][:G * cap], cap, words[i, S:S + A], n_frame, mine[i])
+            hr = mine.sum(0).cpu().numpy()
+            syncs += 1
+            new = []
+            for s, h, (a, need, r) in zip(shards, host, res):
+                if a == 2:
+                    new.append(s._finish(h[:S], h[S:S + A], hr))
+                else:
+                    r.touched_voxels, r.new_blocks, r.new_voxels = int(hr[0]), int(hr[1]), int(hr[2])
+                    new.append((3 if hr[3] > 0 else 0, need, r))
+            res = new
+        for s in shards:
+            s.host_syncs = syncs
+        if all(a == 0 for a, _, _ in res):
+            return res[0][2]
+        need = max(n for _, n, _ in res)
+        kb = [s._redo_setup(host[0], need) for s in shards]
+        key_base = kb[0]
 
 
 def merged_content_hash(export, view) -> str:

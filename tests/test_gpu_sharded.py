@@ -81,7 +81,8 @@ def _assert_owned(shards):
 
 @pytest.mark.parametrize("G", [1, 2, 3, 4])
 @pytest.mark.parametrize("case", sorted(CASES))
-def test_loopback_shards_equal_single_gpu(case, G):
+@pytest.mark.parametrize("plan", [False, True], ids=["host_plan", "device_plan"])
+def test_loopback_shards_equal_single_gpu(case, G, plan):
     from paper_2512_12945_b200 import Mapper
     from paper_2512_12945_b200.sharded import integrate_loopback
 
@@ -92,7 +93,7 @@ def test_loopback_shards_equal_single_gpu(case, G):
     for pts, origin in _frames(11, 2500, 3):
         lab, feat = _payload(kw, rng, pts.shape[0])
         r1 = single.integrate_world(pts, origin, labels=lab, features=feat)
-        r2 = integrate_loopback(shards, pts, origin=origin, labels=lab, features=feat)
+        r2 = integrate_loopback(shards, pts, origin=origin, labels=lab, features=feat, device_plan=plan)
         assert np.array_equal(report_rows([r1]), report_rows([r2]))
         assert (r1.new_blocks, r1.new_voxels) == (r2.new_blocks, r2.new_voxels)
     _assert_union_equals(single, shards)
@@ -100,7 +101,8 @@ def test_loopback_shards_equal_single_gpu(case, G):
     assert sum(s.active_count() for s in shards) == single.active_count()
 
 
-def test_loopback_workload_vs_oracle():
+@pytest.mark.parametrize("plan", [False, True], ids=["host_plan", "device_plan"])
+def test_loopback_workload_vs_oracle(plan):
     """Full cfg2 LiDAR frames (65,536 points, sensor pose) on 4 shards,
     bit-exact against the oracle."""
     from oracle.oracle import OracleMap
@@ -113,7 +115,7 @@ def test_loopback_workload_vs_oracle():
     om = OracleMap(**kw)
     for i in range(2):
         f = wl.make_frame(i * 3)
-        r1 = integrate_loopback(shards, f.points_world, origin=f.origin, labels=f.labels)
+        r1 = integrate_loopback(shards, f.points_world, origin=f.origin, labels=f.labels, device_plan=plan)
         r2 = om.integrate_world(f.points_world.cpu().numpy(), f.origin,
                                 labels=f.labels.cpu().numpy())
         assert np.array_equal(report_rows([r1]), report_rows([r2]))
@@ -125,7 +127,8 @@ def test_loopback_workload_vs_oracle():
     _assert_owned(shards)
 
 
-def test_loopback_sensor_pose_and_device_inputs():
+@pytest.mark.parametrize("plan", [False, True], ids=["host_plan", "device_plan"])
+def test_loopback_sensor_pose_and_device_inputs(plan):
     """Mapper.integrate semantics (sensor points + pose) with CUDA inputs."""
     import torch
 
@@ -142,12 +145,13 @@ def test_loopback_sensor_pose_and_device_inputs():
         pts = torch.as_tensor(rng.normal(size=(4000, 3)) * 2.0, dtype=torch.float32).cuda()
         lab = torch.as_tensor(rng.integers(1, 5, 4000), dtype=torch.int32).cuda()
         r1 = single.integrate(pts, pose, labels=lab)
-        r2 = integrate_loopback(shards, pts, pose=pose, labels=lab)
+        r2 = integrate_loopback(shards, pts, pose=pose, labels=lab, device_plan=plan)
         assert np.array_equal(report_rows([r1]), report_rows([r2]))
     _assert_union_equals(single, shards)
 
 
-def test_global_queries_merge_in_active_order():
+@pytest.mark.parametrize("plan", [False, True], ids=["host_plan", "device_plan"])
+def test_global_queries_merge_in_active_order(plan):
     from paper_2512_12945_b200 import Mapper
     from paper_2512_12945_b200.sharded import integrate_loopback, merge_by_stamps
 
@@ -158,7 +162,7 @@ def test_global_queries_merge_in_active_order():
     for pts, origin in _frames(2, 2000, 2):
         _, feat = _payload(kw, rng, pts.shape[0])
         single.integrate_world(pts, origin, features=feat)
-        integrate_loopback(shards, pts, origin=origin, features=feat)
+        integrate_loopback(shards, pts, origin=origin, features=feat, device_plan=plan)
     q = rng.normal(size=kw["feature_dim"])
     c1, s1 = single.query(q)
     c2, s2 = merge_by_stamps([s.local_query(q) for s in shards])
@@ -172,14 +176,41 @@ def test_global_queries_merge_in_active_order():
     for pts, origin in _frames(4, 2000, 2):
         lab, _ = _payload(kwc, rng, pts.shape[0])
         single.integrate_world(pts, origin, labels=lab)
-        integrate_loopback(shards, pts, origin=origin, labels=lab)
+        integrate_loopback(shards, pts, origin=origin, labels=lab, device_plan=plan)
     for zero in (False, True):
         c1, l1 = single.label_map(zero)
         c2, l2 = merge_by_stamps([s.local_label_map(zero) for s in shards])
         assert np.array_equal(c1, c2) and np.array_equal(l1, l2)
 
 
-def test_key_window_rebase_is_global():
+def test_device_plan_one_sync_and_capacity_redo():
+    """The device plan takes one host synchronisation per frame; sections
+    over their capacity abort the frame on every shard before any change and
+    it is redone with the capacity the device reported."""
+    from paper_2512_12945_b200 import Mapper
+    from paper_2512_12945_b200.sharded import integrate_loopback
+
+    kw = CASES["closed"]
+    single = Mapper(**kw)
+    shards = _shards(3, **kw)
+    rng = np.random.default_rng(5)
+    for i, (pts, origin) in enumerate(_frames(13, 3000, 4)):
+        lab, _ = _payload(kw, rng, pts.shape[0])
+        if i == 2:
+            for s in shards:
+                s._cap = 1024   # far below one section
+        r1 = single.integrate_world(pts, origin, labels=lab)
+        r2 = integrate_loopback(shards, pts, origin=origin, labels=lab, device_plan=True)
+        assert np.array_equal(report_rows([r1]), report_rows([r2]))
+        assert shards[0].host_syncs == (2 if i == 2 else 1)
+        if i == 2:
+            assert shards[0]._cap > 1024
+    _assert_union_equals(single, shards)
+    assert all(s.stats()["frames_integrated"] == 4 for s in shards)
+
+
+@pytest.mark.parametrize("plan", [False, True], ids=["host_plan", "device_plan"])
+def test_key_window_rebase_is_global(plan):
     """Rows beyond the default packed-key window (2^20 voxels from the
     sensor) make every rank re-march with the frame's minimum as key base."""
     from oracle.oracle import OracleMap
@@ -193,14 +224,15 @@ def test_key_window_rebase_is_global():
     pts = np.array([[0.5, 0.0, 0.0], [0.6, 0.1, 0.0], [1100.0, 0.2, 0.0], [1100.4, 0.1, 0.3]])
     lab = np.array([1, 2, 3, 1], np.int32)
     r1 = single.integrate_world(pts, (0.0, 0.0, 0.0), labels=lab)
-    r2 = integrate_loopback(shards, pts, origin=(0.0, 0.0, 0.0), labels=lab)
+    r2 = integrate_loopback(shards, pts, origin=(0.0, 0.0, 0.0), labels=lab, device_plan=plan)
     r3 = om.integrate_world(pts, (0.0, 0.0, 0.0), labels=lab)
     assert np.array_equal(report_rows([r1]), report_rows([r2]))
     assert np.array_equal(report_rows([r2]), report_rows([r3]))
     _assert_union_equals(single, shards)
 
 
-def test_frame_errors_fail_on_every_shard_before_mutation():
+@pytest.mark.parametrize("plan", [False, True], ids=["host_plan", "device_plan"])
+def test_frame_errors_fail_on_every_shard_before_mutation(plan):
     from paper_2512_12945_b200 import SemvoxError
     from paper_2512_12945_b200.sharded import integrate_loopback
 
@@ -208,18 +240,19 @@ def test_frame_errors_fail_on_every_shard_before_mutation():
     shards = _shards(2, voxel_size=1e-6, truncation=3e-6, max_range=50.0)
     pts = np.array([[3.0, 0.0, 0.0], [-3.0, 0.0, 0.0]])
     with pytest.raises(SemvoxError, match="2\\^21"):
-        integrate_loopback(shards, pts, origin=(0.0, 0.0, 0.0))
+        integrate_loopback(shards, pts, origin=(0.0, 0.0, 0.0), device_plan=plan)
     assert all(s.active_count() == 0 for s in shards)
     shards = _shards(3, voxel_size=1e-5, truncation=3e-5, space_carving=True, max_range=50.0)
     with pytest.raises(SemvoxError, match="step budget"):
-        integrate_loopback(shards, np.array([[12.0, 0.0, 0.0]] * 3), origin=(0.0, 0.0, 0.0))
+        integrate_loopback(shards, np.array([[12.0, 0.0, 0.0]] * 3), origin=(0.0, 0.0, 0.0), device_plan=plan)
     assert all(s.active_count() == 0 for s in shards)
     # the shards stay usable after a rejected frame
-    r = integrate_loopback(shards, np.array([[0.001, 0.0, 0.0]]), origin=(0.0, 0.0, 0.0))
+    r = integrate_loopback(shards, np.array([[0.001, 0.0, 0.0]]), origin=(0.0, 0.0, 0.0), device_plan=plan)
     assert r.points_used == 1 and sum(s.active_count() for s in shards) > 0
 
 
-def test_empty_and_tiny_frames():
+@pytest.mark.parametrize("plan", [False, True], ids=["host_plan", "device_plan"])
+def test_empty_and_tiny_frames(plan):
     from paper_2512_12945_b200 import Mapper
     from paper_2512_12945_b200.sharded import integrate_loopback
 
@@ -230,13 +263,13 @@ def test_empty_and_tiny_frames():
                      (np.array([[1.0, 0.5, 0.2], [0.3, -1.0, 0.4]]), np.array([1, 3], np.int32)),
                      (np.array([[np.nan, 0.0, 0.0]]), np.array([2], np.int32))]:
         r1 = single.integrate_world(pts, (0.0, 0.0, 0.0), labels=lab)
-        r2 = integrate_loopback(shards, pts, origin=(0.0, 0.0, 0.0), labels=lab)
+        r2 = integrate_loopback(shards, pts, origin=(0.0, 0.0, 0.0), labels=lab, device_plan=plan)
         assert np.array_equal(report_rows([r1]), report_rows([r2]))
     _assert_union_equals(single, shards)
     assert all(s.stats()["frames_integrated"] == 3 for s in shards)
 
 
-def _dist_worker(rank, world, port, kw, seed, out):
+def _dist_worker(rank, world, port, kw, seed, out, plan=False):
     import os
 
     import torch
@@ -250,6 +283,7 @@ def _dist_worker(rank, world, port, kw, seed, out):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         m = ShardedMapper(**kw, rank=rank, world=world, transport=DistTransport())
+        m.device_plan = plan
         rng = np.random.default_rng(seed)
         reps = []
         for pts, origin in _frames(seed, 3000, 3):
@@ -262,7 +296,8 @@ def _dist_worker(rank, world, port, kw, seed, out):
         dist.destroy_process_group()
 
 
-def test_dist_driver_two_processes_gloo():
+@pytest.mark.parametrize("plan", [False, True], ids=["host_plan", "device_plan"])
+def test_dist_driver_two_processes_gloo(plan):
     """ShardedMapper.integrate through DistTransport in two processes (gloo
     collectives; both ranks on cuda:0, kernels independent) == one Mapper."""
     import socket
@@ -278,7 +313,7 @@ def test_dist_driver_two_processes_gloo():
         port = s.getsockname()[1]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_dist_worker, args=(r, 2, port, kw, seed, q)) for r in range(2)]
+    procs = [ctx.Process(target=_dist_worker, args=(r, 2, port, kw, seed, q, plan)) for r in range(2)]
     for p in procs:
         p.start()
     res = dict((r[0], r[1:]) for r in (q.get(timeout=300) for _ in range(2)))
