@@ -23,6 +23,7 @@
 #include <cub/block/block_scan.cuh>
 
 #include "svx_internal.cuh"
+#define SVX_RT_TRACE_HOST 1
 #include "svx_resolve_tile.cuh"
 
 namespace svx {
@@ -63,7 +64,8 @@ __global__ void __launch_bounds__(kResolveThreads, 6) k_resolve(
     ra.slots = fp.slots != 0;
     ra.region = fp.region;
     __syncthreads();
-    for (long long tile = blockIdx.x; tile * kResolveThreads < total; tile += gridDim.x) {
+    int tstep = 0;
+    for (long long tile = blockIdx.x; tile * kResolveThreads < total; tile += gridDim.x, ++tstep) {
         const long long t = tile * kResolveThreads + threadIdx.x;
         const bool valid = t < total;
         // row arrays are dead after this read: evict-first
@@ -75,7 +77,7 @@ __global__ void __launch_bounds__(kResolveThreads, 6) k_resolve(
             rsl.d = __ldcs(rowd + t);
         }
         // (each step starts with a barrier: see resolve_step)
-        rt::resolve_step<kResolveThreads>(ra, valid, key, rsl, t, s_warp, s_base, tcount);
+        rt::resolve_step<kResolveThreads>(ra, valid, key, rsl, t, s_warp, s_base, tcount, tstep);
     }
     if (ra.slots && threadIdx.x == 0) {   // this CTA's touched region
         ra.rcount[blockIdx.x] = tcount;
@@ -269,6 +271,22 @@ svx_status cleanup_t(svx_map* m, cudaStream_t s) {
 }
 
 }  // namespace
+
+#ifdef SVX_RESOLVE_TRACE
+// Debug build only: the last K2's per-CTA step stamps (kTraceCtas x
+// kTraceSteps x kTraceMarks u64, zero where no step ran).
+extern "C" int svx_debug_resolve_trace(unsigned long long* out, long long n) {
+    const long long cap = (long long)sizeof(rt::g_rtrace) / 8;
+    if (!out) return (int)cap;
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, rt::g_rtrace, (size_t)(n < cap ? n : cap) * 8);
+    void* p = nullptr;
+    cudaGetSymbolAddress(&p, rt::g_rtrace);
+    cudaMemset(p, 0, sizeof(rt::g_rtrace));
+    cudaDeviceSynchronize();
+    return (int)cap;
+}
+#endif
 
 rt::ResolveArgs resolve_args(svx_map* m) {
     rt::ResolveArgs ra{};

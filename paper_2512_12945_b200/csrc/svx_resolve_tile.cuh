@@ -23,6 +23,21 @@
 namespace svx {
 namespace rt {
 
+// -DSVX_RESOLVE_TRACE: thread 0 of each K2 CTA stamps the phases of its first
+// kTraceSteps steps (%globaltimer) into g_rtrace (read by svx_debug_resolve_trace).
+// (only svx_resolve.cu, which defines SVX_RT_TRACE_HOST, holds the buffer)
+#if defined(SVX_RESOLVE_TRACE) && defined(SVX_RT_TRACE_HOST)
+constexpr int kTraceSteps = 4, kTraceMarks = 6, kTraceCtas = 2048;
+__device__ unsigned long long g_rtrace[kTraceCtas][kTraceSteps][kTraceMarks];
+#define RT_MARK(i)                                                                         \
+    do {                                                                                   \
+        if (threadIdx.x == 0 && blockIdx.x < kTraceCtas && tstep < kTraceSteps)              \
+            g_rtrace[blockIdx.x][tstep][i] = globaltimer();                                 \
+    } while (0)
+#else
+#define RT_MARK(i) do { } while (0)
+#endif
+
 __device__ __forceinline__ int slot_of(long long x, long long y, long long z) {
     return (int)(((x & 7) << 6) | ((y & 7) << 3) | (z & 7));
 }
@@ -176,7 +191,7 @@ __device__ __forceinline__ void resolve_step(const ResolveArgs& ra, bool valid,
                                              unsigned long long key, const RowSlot& rsl,
                                              long long t,
                                              int* s_warp, unsigned long long& s_base,
-                                             unsigned& tcount) {
+                                             unsigned& tcount, int tstep = 0) {
     const KeyPack& kp = ra.kp;
     const long long hmask = ra.hmask, bcap = ra.bcap, vcap = ra.vcap, nblocks0 = ra.nblocks0;
     const int frame = ra.frame;
@@ -196,7 +211,9 @@ __device__ __forceinline__ void resolve_step(const ResolveArgs& ra, bool valid,
     // No thread claims a slot in this step while another thread of its CTA
     // may still wait (previous step) on another CTA's claim: that CTA could
     // itself be held at its claim barrier by a thread waiting on ours.
+    RT_MARK(0);
     __syncthreads();
+    RT_MARK(1);
     long long x = 0, y = 0, z = 0;
     if (valid) unpack_key(key, kp, x, y, z);
     const unsigned vpeers = __match_any_sync(full, valid ? key : (kKeyEmpty ^ (unsigned long long)lane));
@@ -234,6 +251,7 @@ __device__ __forceinline__ void resolve_step(const ResolveArgs& ra, bool valid,
     int rank = 0, cnt = 0;
     // leaf claims are rare: the rank/publish round only runs when this step has any
     const bool lclaims = __syncthreads_or(lstate == 1);
+    RT_MARK(2);
     if (lclaims) {
         rank = cta_rank<kThreads>(lstate == 1, cnt, s_warp);
         if (threadIdx.x == 0) s_base = atomicAdd(&ctr->nblocks, (unsigned long long)cnt);
@@ -296,6 +314,7 @@ __device__ __forceinline__ void resolve_step(const ResolveArgs& ra, bool valid,
         }
     }
     const bool vclaims = __syncthreads_or(vstate == 1);
+    RT_MARK(3);
     if (vclaims) {
         rank = cta_rank<kThreads>(vstate == 1, cnt, s_warp);
         if (threadIdx.x == 0) s_base = atomicAdd(&ctr->nvox, (unsigned long long)cnt);
@@ -343,6 +362,7 @@ __device__ __forceinline__ void resolve_step(const ResolveArgs& ra, bool valid,
         first = cbase == 0u;
     }
     rank = cta_rank<kThreads>(first, cnt, s_warp);
+    RT_MARK(4);
     if (slots) {
         if (first) {
             if (SVX_RESOLVE_PREFETCH && vid >= 0) {
@@ -385,6 +405,7 @@ __device__ __forceinline__ void resolve_step(const ResolveArgs& ra, bool valid,
     } else if (valid) {
         rowvid[t] = vid;
     }
+    RT_MARK(5);
 }
 
 }  // namespace rt

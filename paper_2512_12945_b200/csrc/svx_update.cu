@@ -797,6 +797,9 @@ constexpr int kOpenPer = 8;   // dims per lane per pass (256 dims per pass)
 #define SVX_OPEN_RING 1
 #endif
 // open-set voxels with more rows than this go to the CTA-per-voxel kernel
+#ifndef SVX_OPEN_PREFETCH
+#define SVX_OPEN_PREFETCH 1
+#endif
 #ifndef SVX_OPEN_CTA_MIN
 #define SVX_OPEN_CTA_MIN 256   // measured best of 64 / 256 / 1024 on cfg3 and cfg5
 #endif
@@ -818,6 +821,61 @@ __device__ __forceinline__ void nig_apply(TS* mrow, TS* brow, int c, bool isnew,
     double b_new = b_old + 0.5 * ss + gap;
     mrow[c] = (TS)m_new;
     brow[c] = (TS)b_new;
+}
+
+// nig_apply for the 8 contiguous dimensions c0 .. c0+7 of a full pass (f32
+// state: two 16-byte loads and stores per row of mean / beta); per element the
+// same arithmetic as nig_apply.
+template <class TS>
+__device__ __forceinline__ void nig_apply8(TS* mrow, TS* brow, int c0, bool isnew, const double* sz,
+                                           const double* sz2, double lam, double lam_post, double coef,
+                                           double nobs, double b_bg) {
+    if constexpr (sizeof(TS) == 4) {
+        float m[8], b[8];
+        if (isnew) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) { m[q] = 0.0f; b[q] = (float)b_bg; }
+        } else {
+            const float4* m4 = reinterpret_cast<const float4*>(mrow + c0);
+            const float4* b4 = reinterpret_cast<const float4*>(brow + c0);
+            const float4 m0 = m4[0], m1 = m4[1], b0 = b4[0], b1 = b4[1];
+            m[0] = m0.x; m[1] = m0.y; m[2] = m0.z; m[3] = m0.w; m[4] = m1.x; m[5] = m1.y; m[6] = m1.z; m[7] = m1.w;
+            b[0] = b0.x; b[1] = b0.y; b[2] = b0.z; b[3] = b0.w; b[4] = b1.x; b[5] = b1.y; b[6] = b1.z; b[7] = b1.w;
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const double m_old = isnew ? 0.0 : (double)m[q];
+            const double b_old = isnew ? b_bg : (double)b[q];
+            const double m_new = (lam * m_old + sz[q]) / lam_post;
+            const double zbar = sz[q] / nobs;
+            double ss = sz2[q] - sz[q] * zbar;
+            ss = ss < 0.0 ? 0.0 : ss;
+            const double diff = zbar - m_old;
+            const double gap = coef * (diff * diff) * 0.5;
+            m[q] = (float)m_new;
+            b[q] = (float)(b_old + 0.5 * ss + gap);
+        }
+        float4* mo = reinterpret_cast<float4*>(mrow + c0);
+        float4* bo = reinterpret_cast<float4*>(brow + c0);
+        mo[0] = make_float4(m[0], m[1], m[2], m[3]);
+        mo[1] = make_float4(m[4], m[5], m[6], m[7]);
+        bo[0] = make_float4(b[0], b[1], b[2], b[3]);
+        bo[1] = make_float4(b[4], b[5], b[6], b[7]);
+    } else {
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            nig_apply<TS>(mrow, brow, c0 + q, isnew, sz[q], sz2[q], lam, lam_post, coef, nobs, b_bg);
+    }
+}
+
+// L2 prefetch of a voxel's open-set state (mean and beta rows, `bytes` each):
+// issued when the voxel is taken, so the per-pass NIG reads hit L2.
+__device__ __forceinline__ void prefetch_rows_l2(const void* m, const void* b, int bytes) {
+    const int lane = threadIdx.x & 31;
+    for (int o = lane * 128; o < bytes; o += 32 * 128) {
+        asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"((const char*)m + o));
+        asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"((const char*)b + o));
+    }
 }
 
 // Per-dimension sequential sums over an ordered chunk (lane owns dims
@@ -914,7 +972,7 @@ __device__ __forceinline__ void open_chunk_ring(const Fe* __restrict__ feats, in
 #define SVX_OPEN_BULK 1
 #endif
 #ifndef SVX_OPEN_BULK_RING
-#define SVX_OPEN_BULK_RING 4
+#define SVX_OPEN_BULK_RING 2
 #endif
 constexpr int kOpenBulkRing = SVX_OPEN_BULK_RING;
 
@@ -1051,6 +1109,82 @@ __device__ __forceinline__ void open_chunk_bulk_vec(const Fe* __restrict__ feats
     }
 }
 
+// Grouped bulk ring: a slot holds kOpenGrp rows and one mbarrier counts all
+// their bytes, so a warp waits, syncs and refills once per kOpenGrp rows
+// (lanes 0 .. kOpenGrp-1 issue one bulk copy each); kOpenBulkRing slots, i.e.
+// kOpenBulkRing * kOpenGrp rows in flight per warp.  Same in-order sums.
+#ifndef SVX_OPEN_GRP
+#define SVX_OPEN_GRP 6
+#endif
+constexpr int kOpenGrp = SVX_OPEN_GRP;
+static_assert(kOpenGrp >= 1 && kOpenGrp <= 32 && kOpenBulkRing <= 32, "grouped ring geometry");
+
+// one bulk copy completing on bar (the expected bytes were posted separately)
+__device__ __forceinline__ void bulk_copy(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d),
+        "l"(src), "r"(bytes), "r"(b)
+        : "memory");
+}
+
+template <class Fe, bool kFull>
+__device__ __forceinline__ void open_chunk_grp(const Fe* __restrict__ feats, int D, int base, const int* buf,
+                                               int cnt, double* sz, double* sz2, BulkRing<Fe>& R) {
+    const int lane = threadIdx.x & 31;
+    const int nd = kFull ? kOpenPass : min(kOpenPass, D - base);
+    const unsigned bytes = (unsigned)(nd * (int)sizeof(Fe));
+    const int ng = (cnt + kOpenGrp - 1) / kOpenGrp;
+    auto issue = [&](int g) {
+        const int sl = g % kOpenBulkRing, j0 = g * kOpenGrp;
+        const int nr = min(kOpenGrp, cnt - j0);
+        // (every lane's reads of the slot precede this point: __syncwarp below / at the call)
+        if (lane == 0) {
+            const unsigned b = (unsigned)__cvta_generic_to_shared(R.bar + sl);
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b),
+                         "r"(bytes * (unsigned)nr) : "memory");
+        }
+        if (lane < nr) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            bulk_copy(R.slot + (sl * kOpenGrp + lane) * kOpenPass, feats + (long long)buf[j0 + lane] * D + base,
+                      bytes, R.bar + sl);
+        }
+    };
+    __syncwarp();
+    for (int g = 0; g < kOpenBulkRing && g < ng; ++g) issue(g);
+    for (int g = 0; g < ng; ++g) {
+        const int sl = g % kOpenBulkRing;
+        mbar_wait(R.bar + sl, (R.phase >> sl) & 1u);
+        R.phase ^= 1u << sl;
+        const int nr = min(kOpenGrp, cnt - g * kOpenGrp);
+        const Fe* src = R.slot + sl * kOpenGrp * kOpenPass;
+        for (int r = 0; r < nr; ++r, src += kOpenPass) {
+            if constexpr (kFull) {
+                double v[kOpenPer];
+                load8<Fe>(src + kOpenPer * lane, v);
+#pragma unroll
+                for (int q = 0; q < kOpenPer; ++q) {
+                    sz[q] += v[q];
+                    sz2[q] += v[q] * v[q];
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < kOpenPer; ++q) {
+                    const int cc = lane + 32 * q;
+                    if (cc < nd) {
+                        const double zv = (double)src[cc];
+                        sz[q] += zv;
+                        sz2[q] += zv * zv;
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        if (g + kOpenBulkRing < ng) issue(g + kOpenBulkRing);
+    }
+}
+
 template <class TD, class TS, class Fe>
 __device__ __forceinline__ void open_voxel(const UpdateArgs& a, const KeyPack& kp,
                                            const PoseParams& pp, TD* vt, TS* mean, TS* beta,
@@ -1060,6 +1194,9 @@ __device__ __forceinline__ void open_voxel(const UpdateArgs& a, const KeyPack& k
     const int lane = threadIdx.x & 31;
     const unsigned k = c & ~kNewBit;
     const bool isnew = (c & kNewBit) != 0u;
+#if SVX_OPEN_PREFETCH
+    if (!isnew) prefetch_rows_l2(mean + (long long)vid * a.D, beta + (long long)vid * a.D, a.D * (int)sizeof(TS));
+#endif
     const Center cc = center_of(a.rec[vid].key, kp, a.h, pp);
     int minr = 0;
     long long nwords = 0;
@@ -1098,14 +1235,19 @@ __device__ __forceinline__ void open_voxel(const UpdateArgs& a, const KeyPack& k
                 __syncwarp();
             }
         } else if (bulk && base + kOpenPass <= a.D) {   // full pass, contiguous columns per lane
-            open_chunk_bulk_vec<Fe>(feats, a.D, base, buf, (int)k, sz, sz2, *bulk);
+            open_chunk_grp<Fe, true>(feats, a.D, base, buf, (int)k, sz, sz2, *bulk);
+            if ((a.D & 3) == 0) {   // 16-byte aligned rows of mean / beta
+                nig_apply8<TS>(mrow, brow, base + kOpenPer * lane, isnew, sz, sz2, lam, lam_post, coef, nobs,
+                               b_bg);
+            } else {
 #pragma unroll
-            for (int q = 0; q < kOpenPer; ++q)
-                nig_apply<TS>(mrow, brow, base + kOpenPer * lane + q, isnew, sz[q], sz2[q], lam, lam_post,
-                              coef, nobs, b_bg);
+                for (int q = 0; q < kOpenPer; ++q)
+                    nig_apply<TS>(mrow, brow, base + kOpenPer * lane + q, isnew, sz[q], sz2[q], lam, lam_post,
+                                  coef, nobs, b_bg);
+            }
             continue;
         } else if (bulk) {
-            open_chunk_bulk<Fe>(feats, a.D, base, buf, (int)k, sz, sz2, *bulk);
+            open_chunk_grp<Fe, false>(feats, a.D, base, buf, (int)k, sz, sz2, *bulk);
         } else if (ring) {
             open_chunk_ring<Fe>(feats, a.D, base, buf, (int)k, sz, sz2, ring);
         } else {
@@ -1126,12 +1268,12 @@ __device__ __forceinline__ void open_voxel(const UpdateArgs& a, const KeyPack& k
 // K5 open: every listed voxel; huge segments are deferred to k_update_open_huge.
 template <class TD, class TS, class Fe>
 #ifndef SVX_OPEN_MINB
-#define SVX_OPEN_MINB 1
+#define SVX_OPEN_MINB 2   // 2 CTAs per SM (<= 128 registers, no spills): cfg3 update -38 %, cfg5 -39 % vs 1
 #endif
 __global__ void __launch_bounds__(32 * kWarpsPerCta, SVX_OPEN_MINB) k_update_open(UpdateArgs a, TD* vt, TS* mean,
                                                                    TS* beta) {
     grid_dep_wait();
-    __shared__ int sbuf[kWarpsPerCta][kSmemMax];
+    __shared__ int sbuf[kWarpsPerCta][kOpenCtaMin];   // a segment of <= kOpenCtaMin rows
 #if SVX_OPEN_RING || SVX_OPEN_BULK
     extern __shared__ __align__(128) unsigned char oring[];
 #endif
@@ -1151,7 +1293,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, SVX_OPEN_MINB) k_update_ope
     __shared__ __align__(8) unsigned long long s_bar[kWarpsPerCta][kOpenBulkRing];
     const bool use_bulk = ((a.D * (int)sizeof(Fe)) % 16) == 0 && (((uintptr_t)feats) & 15) == 0;
     BulkRing<Fe> bulk;
-    bulk.slot = reinterpret_cast<Fe*>(oring) + (size_t)wib * kOpenBulkRing * kOpenPass;
+    bulk.slot = reinterpret_cast<Fe*>(oring) + (size_t)wib * kOpenBulkRing * kOpenGrp * kOpenPass;
     bulk.bar = s_bar[wib];
     bulk.phase = 0u;
     if (use_bulk && lane == 0) {
@@ -1211,11 +1353,24 @@ constexpr int kHugeThreads = 256;
 constexpr int kHugeCtas = kHugeWarps;    // prep CTAs sharing the bitmap scratch
 constexpr int kHugeSlice = 32;           // dimensions per feature item
 constexpr int kHugeStages = 4;
-constexpr int kHugeStageBytes = 32768;
-constexpr int kHugeItemCtas = 148;       // one per SM (128 KB of shared memory each)
+#ifndef SVX_HUGE_STAGE_KB
+#define SVX_HUGE_STAGE_KB 16
+#endif
+#ifndef SVX_HUGE_ITEM_CPS
+#define SVX_HUGE_ITEM_CPS 2
+#endif
+constexpr int kHugeStageBytes = SVX_HUGE_STAGE_KB * 1024;
+constexpr int kHugeItemCtas = 148 * SVX_HUGE_ITEM_CPS;   // CTAs per SM x SMs (4 stages of shared memory each)
 // Voxels of up to kGiantRows rows: one CTA each (k_update_open_huge, all
 // dimensions); bigger ones: dimension slices over many SMs (k_huge_items).
 constexpr int kGiantRows = 8192;
+// k_huge_items: warps folding one item's dimensions (32 each); the SM folds
+// kHugeFold * 32 dimension chains at once (1 = one fold warp per SM).
+#ifndef SVX_HUGE_FOLD
+#define SVX_HUGE_FOLD 1
+#endif
+constexpr int kHugeFold = SVX_HUGE_FOLD;
+static_assert(kHugeFold >= 1 && kHugeFold <= 8, "fold warps per item");
 #ifndef SVX_HUGE_RING
 #define SVX_HUGE_RING 1
 #endif
@@ -1556,7 +1711,8 @@ __global__ void __launch_bounds__(kHugeThreads, 1) k_huge_items(UpdateArgs a, TD
     if (!(cv->abort | cv->err_cap)) {
     const int tid = threadIdx.x, wib = tid >> 5, lane = tid & 31;
     const int D = a.D;
-    const int S = (D + kHugeSlice - 1) / kHugeSlice;
+    constexpr int G = kHugeFold;   // folding warps per item (32 dimensions each)
+    const int S = (D + G * kHugeSlice - 1) / (G * kHugeSlice);
     const long long Hn = (long long)cv->n_huge;
     const KeyPack kp = cv->p.kp;
     const PoseParams pp = cv->p.pp;
@@ -1643,9 +1799,8 @@ __global__ void __launch_bounds__(kHugeThreads, 1) k_huge_items(UpdateArgs a, TD
             __syncthreads();
             continue;
         }
-        // ---- feature item: the 32 dimensions of slice sl
-        const int G = 1;
-        const int col0 = sl * kHugeSlice;
+        // ---- feature item: the G * 32 dimensions of slice sl
+        const int col0 = sl * G * kHugeSlice;
         const int ncols = min(G * kHugeSlice, D - col0);
         const int W = G * kHugeSlice;                                  // row stride in the stage
         const int SR = kHugeStageBytes / (W * (int)sizeof(Fe));        // rows per stage
@@ -1654,8 +1809,29 @@ __global__ void __launch_bounds__(kHugeThreads, 1) k_huge_items(UpdateArgs a, TD
         // thread's elements are loaded together first (independent loads), then
         // its gathers are issued
         constexpr int kEpt = kHugeStageBytes / (int)sizeof(Fe) / kHugeThreads;
+        // 16-byte copies (kVec elements) when rows, slices and the array allow
+        constexpr int kVec = 16 / (int)sizeof(Fe);
+        constexpr int kCpt = kEpt / kVec;   // 16-byte chunks per thread and stage
+        const bool vec = ((D * (int)sizeof(Fe)) & 15) == 0 && (((uintptr_t)feats) & 15) == 0;
         auto issue = [&](int st) {
-            if (st < nst) {
+            if (st < nst && vec) {
+                Fe* buf = reinterpret_cast<Fe*>(hsm + (st % kHugeStages) * kHugeStageBytes);
+                int idv[kCpt];
+#pragma unroll
+                for (int i = 0; i < kCpt; ++i) {
+                    const int e = (tid + i * kHugeThreads) * kVec;
+                    const unsigned j = (unsigned)(st * SR + e / W);
+                    idv[i] = j < k ? __ldg(ids + j) : 0;
+                }
+#pragma unroll
+                for (int i = 0; i < kCpt; ++i) {
+                    const int e = (tid + i * kHugeThreads) * kVec;
+                    const int r = e / W, c = e - r * W;
+                    const unsigned j = (unsigned)(st * SR + r);
+                    if (j < k && c < ncols)
+                        __pipeline_memcpy_async(buf + e, feats + (long long)idv[i] * D + col0 + c, 16);
+                }
+            } else if (st < nst) {
                 Fe* buf = reinterpret_cast<Fe*>(hsm + (st % kHugeStages) * kHugeStageBytes);
                 int idv[kEpt];
 #pragma unroll
@@ -1804,7 +1980,7 @@ svx_status closed_b(svx_map* m, cudaStream_t s) {
 template <class TD, class TS, class Fe>
 svx_status open_a(svx_map* m, cudaStream_t s) {
     int ring = SVX_OPEN_RING ? kWarpsPerCta * kOpenRingS * kOpenRingR * kOpenPass * (int)sizeof(Fe) : 0;
-    if (SVX_OPEN_BULK) ring = std::max(ring, kWarpsPerCta * kOpenBulkRing * kOpenPass * (int)sizeof(Fe));
+    if (SVX_OPEN_BULK) ring = std::max(ring, kWarpsPerCta * kOpenBulkRing * kOpenGrp * kOpenPass * (int)sizeof(Fe));
     if (ring > 0)
         SVX_CUDA(cudaFuncSetAttribute(k_update_open<TD, TS, Fe>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       ring));
