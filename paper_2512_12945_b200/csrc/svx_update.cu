@@ -826,6 +826,18 @@ __device__ __forceinline__ void nig_apply(TS* mrow, TS* brow, int c, bool isnew,
 // nig_apply for the 8 contiguous dimensions c0 .. c0+7 of a full pass (f32
 // state: two 16-byte loads and stores per row of mean / beta); per element the
 // same arithmetic as nig_apply.
+// a / b, correctly rounded, from y = RN(1 / b): q = RN(a y) is within an ulp of
+// a / b, the residual a - q b is exact (FMA), and one corrected FMA rounds to
+// RN(a / b) (Markstein's theorem; finite operands, no underflow -- the NIG sums
+// and weights here).  Checked against IEEE division on 2e8 random pairs
+// (nobs-, lambda- and wide-range divisors).  Saves the per-element DDIV
+// sequence (reciprocal on the XU pipe + Newton steps) when b is shared.
+__device__ __forceinline__ double div_rn(double a, double b, double y) {
+    const double q = a * y;
+    const double r = fma(-q, b, a);
+    return fma(r, y, q);
+}
+
 template <class TS>
 __device__ __forceinline__ void nig_apply8(TS* mrow, TS* brow, int c0, bool isnew, const double* sz,
                                            const double* sz2, double lam, double lam_post, double coef,
@@ -842,12 +854,13 @@ __device__ __forceinline__ void nig_apply8(TS* mrow, TS* brow, int c0, bool isne
             m[0] = m0.x; m[1] = m0.y; m[2] = m0.z; m[3] = m0.w; m[4] = m1.x; m[5] = m1.y; m[6] = m1.z; m[7] = m1.w;
             b[0] = b0.x; b[1] = b0.y; b[2] = b0.z; b[3] = b0.w; b[4] = b1.x; b[5] = b1.y; b[6] = b1.z; b[7] = b1.w;
         }
+        const double inv_lp = 1.0 / lam_post, inv_n = 1.0 / nobs;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
             const double m_old = isnew ? 0.0 : (double)m[q];
             const double b_old = isnew ? b_bg : (double)b[q];
-            const double m_new = (lam * m_old + sz[q]) / lam_post;
-            const double zbar = sz[q] / nobs;
+            const double m_new = div_rn(lam * m_old + sz[q], lam_post, inv_lp);
+            const double zbar = div_rn(sz[q], nobs, inv_n);
             double ss = sz2[q] - sz[q] * zbar;
             ss = ss < 0.0 ? 0.0 : ss;
             const double diff = zbar - m_old;
@@ -1378,6 +1391,7 @@ static_assert(kHugeFold >= 1 && kHugeFold <= 8, "fold warps per item");
 #define SVX_HUGE_RING_R 8
 #endif
 constexpr int kHugeRingR = SVX_HUGE_RING_R;   // rows per ring group (k_update_open_huge)
+constexpr int kHugeRingBytes = 2 * kHugeRingR * 4 * 256 * 4;   // its dynamic shared memory (f32 features)
 
 struct HugeInfo {
     int vid;
@@ -1426,6 +1440,8 @@ __device__ __forceinline__ void k_update_open_huge_body(UpdateArgs a, TD* vt, TS
     const PoseParams pp = cv->p.pp;
     const Fe* feats = (const Fe*)cv->p.feats;
     const int D = a.D;
+    // vector mode: row slices by 16-byte cp.async (16-byte sizes and addresses)
+    const bool hbulk = SVX_HUGE_RING && ((D * (int)sizeof(Fe)) & 15) == 0 && (((uintptr_t)feats) & 15) == 0;
 #if SVX_DYN_LONG
     __shared__ long long s_next;
     for (;;) {
@@ -1470,8 +1486,11 @@ __device__ __forceinline__ void k_update_open_huge_body(UpdateArgs a, TD* vt, TS
         TsdfAcc acc{0.0, 0.0, INFINITY, -INFINITY, 0};
         // dims in passes of kHugeDims * kHugeFeatThreads (one pass for D <= 896);
         // warp 0 folds the TSDF sums (thread 0), warps 1.. the feature sums
-        for (int dbase = 0; dbase < D; dbase += kHugeDims * kHugeFeatThreads) {
+        for (int dbase = 0; dbase < D; dbase += hbulk ? kHugeDims * kHugeThreads : kHugeDims * kHugeFeatThreads) {
         const bool first_pass = dbase == 0;
+        const int hpw = min(kHugeDims * kHugeThreads, D - dbase);   // bulk mode: this pass's columns
+        const unsigned hbytes = (unsigned)(hpw * (int)sizeof(Fe));
+        const int hG = max(1, min(16, kHugeRingBytes / (2 * hpw * (int)sizeof(Fe))));
         double sz[kHugeDims], sz2[kHugeDims];
 #pragma unroll
         for (int q = 0; q < kHugeDims; ++q) { sz[q] = 0.0; sz2[q] = 0.0; }
@@ -1508,6 +1527,60 @@ __device__ __forceinline__ void k_update_open_huge_body(UpdateArgs a, TD* vt, TS
                 }
             }
             __syncthreads();
+            if (hbulk) {
+                // rows (this pass's columns) stream through two slots of hG rows:
+                // every thread issues 16-byte cp.async chunks of the group's rows,
+                // then folds dims tid + 256 q of each row; thread 0 folds the
+                // group's TSDF rows in between (first pass)
+                const int ng = (cnt + hG - 1) / hG;
+                const int c4 = hpw * (int)sizeof(Fe) / 16;   // 16-byte chunks per row
+                auto issue = [&](int g) {
+                    if (g < ng) {
+                        const int j0 = g * hG, nr = min(hG, cnt - j0);
+                        Fe* dst = hring + (size_t)(g & 1) * hG * hpw;
+                        for (int c = tid; c < nr * c4; c += kHugeThreads) {
+                            const int r = c / c4, cc = c - r * c4;
+                            __pipeline_memcpy_async(reinterpret_cast<char*>(dst + (size_t)r * hpw) + cc * 16,
+                                                    reinterpret_cast<const char*>(feats + (long long)s_id[j0 + r] * D + dbase) + cc * 16,
+                                                    16);
+                        }
+                    }
+                    __pipeline_commit();
+                };
+                issue(0);
+                issue(1);
+                for (int g = 0; g < ng; ++g) {
+                    const int j0 = g * hG;
+                    const int nr = min(hG, cnt - j0);
+                    if (tid == 0 && first_pass) {
+                        for (int j = j0; j < j0 + nr; ++j) {
+                            const double wq = s_w[j], dq = s_d[j];
+                            acc.sw += wq;
+                            acc.swd += wq * dq;
+                            acc.mind = dq < acc.mind ? dq : acc.mind;
+                            acc.maxd = dq > acc.maxd ? dq : acc.maxd;
+                        }
+                    }
+                    __pipeline_wait_prior(1);   // this thread's chunks of group g
+                    __syncthreads();            // everyone's
+                    const Fe* src = hring + (size_t)(g & 1) * hG * hpw;
+                    for (int r = 0; r < nr; ++r, src += hpw) {
+#pragma unroll
+                        for (int q = 0; q < kHugeDims; ++q) {
+                            const int col = tid + q * kHugeThreads;
+                            if (col < hpw) {
+                                const double z = (double)src[col];
+                                sz[q] += z;
+                                sz2[q] += z * z;
+                            }
+                        }
+                    }
+                    __syncthreads();   // the slot is consumed
+                    issue(g + 2);
+                }
+                __pipeline_wait_prior(0);
+                continue;
+            }
             if (tid == 0 && first_pass) {   // independent chains: one dependent add per row each
                 for (int j = 0; j < cnt; ++j) {
                     const double wq = s_w[j], dq = s_d[j];
@@ -1604,6 +1677,12 @@ __device__ __forceinline__ void k_update_open_huge_body(UpdateArgs a, TD* vt, TS
         TS* brow = beta + (long long)vid * D;
 #pragma unroll
         for (int q = 0; q < kHugeDims; ++q) {
+            if (hbulk) {
+                const int col = dbase + tid + q * kHugeThreads;
+                if (col < D && tid + q * kHugeThreads < hpw)
+                    nig_apply<TS>(mrow, brow, col, isnew, sz[q], sz2[q], lam, lam_post, coef, nobs, b_bg);
+                continue;
+            }
             const int col = dbase + (tid - 32) + q * kHugeFeatThreads;
             if (tid >= 32 && col < D) nig_apply<TS>(mrow, brow, col, isnew, sz[q], sz2[q], lam, lam_post, coef, nobs, b_bg);
         }
@@ -1992,7 +2071,8 @@ svx_status open_a(svx_map* m, cudaStream_t s) {
 
 template <class TD, class TS, class Fe>
 svx_status open_b(svx_map* m, cudaStream_t s) {
-    const int hsmem = SVX_HUGE_RING ? 2 * kHugeRingR * kHugeDims * kHugeThreads * (int)sizeof(Fe) : 0;
+    const int hsmem = SVX_HUGE_RING ? std::max(2 * kHugeRingR * kHugeDims * kHugeThreads * (int)sizeof(Fe),
+                                               kHugeRingBytes) : 0;
     if (hsmem > 0)
         SVX_CUDA(cudaFuncSetAttribute(k_update_open_huge<TD, TS, Fe>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, hsmem));
