@@ -1130,6 +1130,10 @@ __device__ __forceinline__ void open_chunk_bulk_vec(const Fe* __restrict__ feats
 #define SVX_OPEN_GRP 6
 #endif
 constexpr int kOpenGrp = SVX_OPEN_GRP;
+#ifndef SVX_OPEN_UNROLL
+#define SVX_OPEN_UNROLL 3
+#endif
+constexpr int kOpenUnroll = SVX_OPEN_UNROLL;   // rows of a group folded per loop iteration
 static_assert(kOpenGrp >= 1 && kOpenGrp <= 32 && kOpenBulkRing <= 32, "grouped ring geometry");
 
 // one bulk copy completing on bar (the expected bytes were posted separately)
@@ -1172,6 +1176,7 @@ __device__ __forceinline__ void open_chunk_grp(const Fe* __restrict__ feats, int
         R.phase ^= 1u << sl;
         const int nr = min(kOpenGrp, cnt - g * kOpenGrp);
         const Fe* src = R.slot + sl * kOpenGrp * kOpenPass;
+#pragma unroll (kOpenUnroll)
         for (int r = 0; r < nr; ++r, src += kOpenPass) {
             if constexpr (kFull) {
                 double v[kOpenPer];
@@ -1534,15 +1539,25 @@ __device__ __forceinline__ void k_update_open_huge_body(UpdateArgs a, TD* vt, TS
                 // group's TSDF rows in between (first pass)
                 const int ng = (cnt + hG - 1) / hG;
                 const int c4 = hpw * (int)sizeof(Fe) / 16;   // 16-byte chunks per row
+                // this thread's first chunk (row r0, chunk cc0) and its stride in
+                // (rows, chunks) per kHugeThreads chunks: no division per chunk
+                const int r0 = tid / c4, cc0 = tid - r0 * c4;
+                const int dq = kHugeThreads / c4, dc = kHugeThreads - dq * c4;
                 auto issue = [&](int g) {
                     if (g < ng) {
                         const int j0 = g * hG, nr = min(hG, cnt - j0);
                         Fe* dst = hring + (size_t)(g & 1) * hG * hpw;
-                        for (int c = tid; c < nr * c4; c += kHugeThreads) {
-                            const int r = c / c4, cc = c - r * c4;
+                        int r = r0, cc = cc0;
+                        while (r < nr) {
                             __pipeline_memcpy_async(reinterpret_cast<char*>(dst + (size_t)r * hpw) + cc * 16,
                                                     reinterpret_cast<const char*>(feats + (long long)s_id[j0 + r] * D + dbase) + cc * 16,
                                                     16);
+                            r += dq;
+                            cc += dc;
+                            if (cc >= c4) {
+                                cc -= c4;
+                                ++r;
+                            }
                         }
                     }
                     __pipeline_commit();
@@ -1564,6 +1579,7 @@ __device__ __forceinline__ void k_update_open_huge_body(UpdateArgs a, TD* vt, TS
                     __pipeline_wait_prior(1);   // this thread's chunks of group g
                     __syncthreads();            // everyone's
                     const Fe* src = hring + (size_t)(g & 1) * hG * hpw;
+#pragma unroll 2
                     for (int r = 0; r < nr; ++r, src += hpw) {
 #pragma unroll
                         for (int q = 0; q < kHugeDims; ++q) {
@@ -1693,7 +1709,7 @@ __device__ __forceinline__ void k_update_open_huge_body(UpdateArgs a, TD* vt, TS
 }
 
 template <class TD, class TS, class Fe>
-__global__ void __launch_bounds__(kHugeThreads, 1) k_update_open_huge(UpdateArgs a, TD* vt, TS* mean, TS* beta) {
+__global__ void __launch_bounds__(kHugeThreads, 2) k_update_open_huge(UpdateArgs a, TD* vt, TS* mean, TS* beta) {
     k_update_open_huge_body<TD, TS, Fe>(a, vt, mean, beta);
 }
 
@@ -2060,9 +2076,12 @@ template <class TD, class TS, class Fe>
 svx_status open_a(svx_map* m, cudaStream_t s) {
     int ring = SVX_OPEN_RING ? kWarpsPerCta * kOpenRingS * kOpenRingR * kOpenPass * (int)sizeof(Fe) : 0;
     if (SVX_OPEN_BULK) ring = std::max(ring, kWarpsPerCta * kOpenBulkRing * kOpenGrp * kOpenPass * (int)sizeof(Fe));
-    if (ring > 0)
+    if (ring > 0) {
         SVX_CUDA(cudaFuncSetAttribute(k_update_open<TD, TS, Fe>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       ring));
+        SVX_CUDA(cudaFuncSetAttribute(k_update_open<TD, TS, Fe>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                      100));
+    }
     SVX_CUDA(launch_pdl(k_update_open<TD, TS, Fe>, kLongBlocks, 32 * kWarpsPerCta, ring, s, 
         make_args(m), ptr<TD>(m->vt), ptr<TS>(m->s0), ptr<TS>(m->s1)));
     SVX_LAUNCHED();
@@ -2073,9 +2092,13 @@ template <class TD, class TS, class Fe>
 svx_status open_b(svx_map* m, cudaStream_t s) {
     const int hsmem = SVX_HUGE_RING ? std::max(2 * kHugeRingR * kHugeDims * kHugeThreads * (int)sizeof(Fe),
                                                kHugeRingBytes) : 0;
-    if (hsmem > 0)
+    if (hsmem > 0) {
         SVX_CUDA(cudaFuncSetAttribute(k_update_open_huge<TD, TS, Fe>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, hsmem));
+        // two CTAs per SM need the largest shared-memory carveout
+        SVX_CUDA(cudaFuncSetAttribute(k_update_open_huge<TD, TS, Fe>,
+                                      cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    }
     SVX_CUDA(launch_pdl(k_update_open_huge<TD, TS, Fe>, kHugeCtas, kHugeThreads, hsmem, s, make_args(m),
                         ptr<TD>(m->vt), ptr<TS>(m->s0), ptr<TS>(m->s1)));
     SVX_LAUNCHED();
@@ -2085,6 +2108,7 @@ svx_status open_b(svx_map* m, cudaStream_t s) {
     const int smem = kHugeStages * kHugeStageBytes;
     SVX_CUDA(cudaFuncSetAttribute(k_huge_items<TD, TS, Fe>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   smem));
+    SVX_CUDA(cudaFuncSetAttribute(k_huge_items<TD, TS, Fe>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     SVX_CUDA(launch_pdl(k_huge_items<TD, TS, Fe>, kHugeItemCtas, kHugeThreads, smem, s, make_args(m),
                         ptr<TD>(m->vt), ptr<TS>(m->s0), ptr<TS>(m->s1), ptr<HugeInfo>(m->hinfo)));
     SVX_LAUNCHED();
