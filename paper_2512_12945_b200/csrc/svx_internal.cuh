@@ -435,10 +435,15 @@ struct KSpan {
     __device__ __forceinline__ KSpan(const FrameCtr* snap, FrameCtr*, int k) : rec(snap->p.kspan) {
         start(k);
     }
-    __device__ __forceinline__ void start(int k) {
+    // end_only: a later kernel of the same stage (its CTAs' end times replace
+    // the first kernel's, whose start times stay): the stage spans both
+    __device__ __forceinline__ KSpan(FrameCtr* ctr, int k, bool end_only) : rec(ctr->p.kspan) {
+        start(k, end_only);
+    }
+    __device__ __forceinline__ void start(int k, bool end_only = false) {
         if (rec && threadIdx.x == 0 && blockIdx.x < kSpanMaxCtas) {
             rec += (size_t)k * 2 * kSpanMaxCtas + blockIdx.x;
-            rec[0] = globaltimer();
+            if (!end_only) rec[0] = globaltimer();
         } else {
             rec = nullptr;
         }

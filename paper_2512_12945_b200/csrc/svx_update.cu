@@ -1798,7 +1798,7 @@ __global__ void __launch_bounds__(kHugeThreads, 1) k_huge_items(UpdateArgs a, TD
     grid_dep_wait();
     FrameCtr* ctr = a.ctr;
     {
-    KSpan _ks(ctr, kSpanUpdateB);
+    KSpan _ks(ctr, kSpanUpdateB, true);   // update_b spans k_update_open_huge .. k_huge_items
     __shared__ FrameCtr s_ctr_;
     __shared__ double s_red[4][kHugeThreads / 32];
     snapshot_ctr(ctr, s_ctr_);
