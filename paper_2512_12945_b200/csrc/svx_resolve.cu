@@ -30,6 +30,9 @@ namespace svx {
 namespace {
 
 constexpr int kResolveThreads = kResolveTile;
+#ifndef SVX_ROW_DISCARD
+#define SVX_ROW_DISCARD 1
+#endif
 constexpr int kSegThreads = 256;
 constexpr int kSegTile = kSegThreads * 4;
 constexpr int kSegBlocks = 148 * 4;
@@ -78,6 +81,19 @@ __global__ void __launch_bounds__(kResolveThreads, 6) k_resolve(
         }
         // (each step starts with a barrier: see resolve_step)
         rt::resolve_step<kResolveThreads>(ra, valid, key, rsl, t, s_warp, s_base, tcount, tstep);
+#if SVX_ROW_DISCARD
+        // slot mode: the tile's rows are dead once every thread used them (the
+        // step's barriers): drop their 48 L2 lines without write-back
+        if (ra.slots && threadIdx.x < 48) {
+            const long long t0 = tile * kResolveThreads;
+            const int q = threadIdx.x;
+            const char* line = q < 16 ? (const char*)(rowkey + t0) + 128 * q
+                             : q < 32 ? (const char*)(rowd + t0) + 128 * (q - 16)
+                             : q < 40 ? (const char*)(rowray + t0) + 128 * (q - 32)
+                                      : (const char*)(rowlab + t0) + 128 * (q - 40);
+            asm volatile("discard.global.L2 [%0], 128;" ::"l"(line) : "memory");
+        }
+#endif
     }
     if (ra.slots && threadIdx.x == 0) {   // this CTA's touched region
         ra.rcount[blockIdx.x] = tcount;

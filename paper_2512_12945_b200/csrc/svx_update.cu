@@ -356,6 +356,9 @@ __device__ __forceinline__ void sorted_fold16(const UpdateArgs& a, const RowSlot
 #ifndef SVX_SLOT_PAIR
 #define SVX_SLOT_PAIR 1
 #endif
+#ifndef SVX_SLOT_DISCARD
+#define SVX_SLOT_DISCARD 1
+#endif
 template <class TD, class TC, bool kInlineLong>
 __device__ __forceinline__ void k_update_slots_body(UpdateArgs a, const TouchEntry* __restrict__ tent,
                                                       const unsigned* __restrict__ rcount,
@@ -476,6 +479,11 @@ __device__ __forceinline__ void k_update_slots_body(UpdateArgs a, const TouchEnt
         if (closed && a.last_wins)
             for (int t = 0; t < a.C; ++t) crow[t] = (TC)(t == acc.last - 1 ? 1 : 0);
         bslot[en.bidx] = (unsigned long long)(unsigned)vid;   // frame count back to 0
+#if SVX_SLOT_DISCARD
+        // the voxel's row slots are dead until K2 of a later frame rewrites them:
+        // drop their L2 lines without writing them back (k <= 8 here: one line)
+        asm volatile("discard.global.L2 [%0], 128;" ::"l"(sl) : "memory");
+#endif
     }
 }
 
