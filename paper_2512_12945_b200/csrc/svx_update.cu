@@ -1006,18 +1006,6 @@ __device__ __forceinline__ void mbar_fence_init() {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 
-// lane 0: expect `bytes` on bar, then one bulk copy global -> shared completing on it
-__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes,
-                                          unsigned long long* bar) {
-    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
-    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d),
-        "l"(src), "r"(bytes), "r"(b)
-        : "memory");
-}
-
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
     const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
     asm volatile(
@@ -1038,47 +1026,6 @@ struct BulkRing {
     unsigned phase;             // bit s = parity of slot s's next completion
 };
 
-// open_chunk over a ring of bulk copies: row j of this pass sits in slot
-// j % kOpenBulkRing; the sums are the same in-order sums as open_chunk.
-template <class Fe>
-__device__ __forceinline__ void open_chunk_bulk(const Fe* __restrict__ feats, int D, int base,
-                                                const int* buf, int cnt, double* sz, double* sz2,
-                                                BulkRing<Fe>& R) {
-    const int lane = threadIdx.x & 31;
-    const int nd = min(kOpenPass, D - base);
-    const unsigned bytes = (unsigned)(nd * (int)sizeof(Fe));
-    if (lane == 0) {
-        const int pre = min(kOpenBulkRing, cnt);
-        // (slots were last read by this warp's previous pass; every lane passed
-        // the __syncwarp after its reads)
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        for (int j = 0; j < pre; ++j)
-            bulk_load(R.slot + j * kOpenPass, feats + (long long)buf[j] * D + base, bytes, R.bar + j);
-    }
-    for (int j = 0; j < cnt; ++j) {
-        const int sl = j % kOpenBulkRing;
-        mbar_wait(R.bar + sl, (R.phase >> sl) & 1u);
-        R.phase ^= 1u << sl;
-        const Fe* src = R.slot + sl * kOpenPass;
-#pragma unroll
-        for (int q = 0; q < kOpenPer; ++q) {
-            const int cc = lane + 32 * q;
-            if (cc < nd) {
-                const double zv = (double)src[cc];
-                sz[q] += zv;
-                sz2[q] += zv * zv;
-            }
-        }
-        __syncwarp();
-        if (lane == 0 && j + kOpenBulkRing < cnt) {
-            // the slot's generic reads are done: order them before the async write
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            bulk_load(R.slot + sl * kOpenPass, feats + (long long)buf[j + kOpenBulkRing] * D + base, bytes,
-                      R.bar + sl);
-        }
-    }
-}
-
 // Full passes (kOpenPass columns): lane owns the 8 contiguous columns
 // base + 8 lane .. +7, read from the ring with two 16-byte shared loads (f32)
 // and no per-column bounds checks; same per-column in-order sums.
@@ -1094,38 +1041,6 @@ __device__ __forceinline__ void load8(const Fe* p, double* v) {
             const double2 a = reinterpret_cast<const double2*>(p)[q];
             v[2 * q] = a.x;
             v[2 * q + 1] = a.y;
-        }
-    }
-}
-
-template <class Fe>
-__device__ __forceinline__ void open_chunk_bulk_vec(const Fe* __restrict__ feats, int D, int base,
-                                                    const int* buf, int cnt, double* sz, double* sz2,
-                                                    BulkRing<Fe>& R) {
-    const int lane = threadIdx.x & 31;
-    constexpr unsigned bytes = (unsigned)(kOpenPass * sizeof(Fe));
-    if (lane == 0) {
-        const int pre = min(kOpenBulkRing, cnt);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        for (int j = 0; j < pre; ++j)
-            bulk_load(R.slot + j * kOpenPass, feats + (long long)buf[j] * D + base, bytes, R.bar + j);
-    }
-    for (int j = 0; j < cnt; ++j) {
-        const int sl = j % kOpenBulkRing;
-        mbar_wait(R.bar + sl, (R.phase >> sl) & 1u);
-        R.phase ^= 1u << sl;
-        double v[kOpenPer];
-        load8<Fe>(R.slot + sl * kOpenPass + kOpenPer * lane, v);
-#pragma unroll
-        for (int q = 0; q < kOpenPer; ++q) {
-            sz[q] += v[q];
-            sz2[q] += v[q] * v[q];
-        }
-        __syncwarp();
-        if (lane == 0 && j + kOpenBulkRing < cnt) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            bulk_load(R.slot + sl * kOpenPass, feats + (long long)buf[j + kOpenBulkRing] * D + base, bytes,
-                      R.bar + sl);
         }
     }
 }
@@ -1397,14 +1312,7 @@ constexpr int kGiantRows = 8192;
 #endif
 constexpr int kHugeFold = SVX_HUGE_FOLD;
 static_assert(kHugeFold >= 1 && kHugeFold <= 8, "fold warps per item");
-#ifndef SVX_HUGE_RING
-#define SVX_HUGE_RING 1
-#endif
-#ifndef SVX_HUGE_RING_R
-#define SVX_HUGE_RING_R 8
-#endif
-constexpr int kHugeRingR = SVX_HUGE_RING_R;   // rows per ring group (k_update_open_huge)
-constexpr int kHugeRingBytes = 2 * kHugeRingR * 4 * 256 * 4;   // its dynamic shared memory (f32 features)
+constexpr int kHugeRingBytes = 64 * 1024;   // k_update_open_huge: three row slots of dynamic shared memory
 
 struct HugeInfo {
     int vid;
@@ -1414,47 +1322,51 @@ struct HugeInfo {
     double w_old;      // pre-frame TSDF weight (lambda of the NIG update)
 };
 
-// K5 open, voxels of more than 1024 rows (a depth camera close to a
-// surface funnels most of its rays into a few voxels): one CTA per voxel.
-// The voxel's point indices go into a bitmap (per-CTA global scratch), are
-// extracted in ascending chunks of up to kHugeChunk into shared memory with
-// each row's d and w, and then: thread 0 folds the TSDF sums in order while
-// every thread folds the feature sums of its own dimensions in order (the
-// dims are independent, so a voxel's D sums run in parallel; the rows'
-// features are read coalesced, 4 rows in flight).  Sums are the sequential
-// point-ordered fp64 sums of the warp path.
-constexpr int kHugeChunk = 2048;         // rows per shared-memory chunk (64 bitmap words)
+// K5 open, voxels of kOpenCtaMin+1 .. kGiantRows rows (a depth camera close
+// to a surface funnels most of its rays into a few voxels): one CTA per voxel,
+// after k_huge_prep sorted its rows and applied its TSDF sums.  Row slices of
+// up to 1024 dimensions stream through three shared-memory slots by 16-byte
+// cp.async (a warp per row); every thread folds its own dimensions in row
+// order, so the voxel's D sums run in parallel and each is the sequential
+// point-ordered fp64 sum of the warp path.
 constexpr int kHugeDims = 4;             // dims per feature thread and pass
-constexpr int kHugeFeatThreads = kHugeThreads - 32;   // warp 0 folds the TSDF sums
+
+// Per-thread fold of dims tid + 256 q (q < NQ) over nr staged rows (row
+// stride hpw): sequential per-dimension Σz, Σz² in row order.
+template <int NQ, class Fe>
+__device__ __forceinline__ void fold_rows(const Fe* src, int nr, int hpw, int tid, double* sz, double* sz2) {
+#pragma unroll 2
+    for (int r = 0; r < nr; ++r, src += hpw) {
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            const int col = tid + q * kHugeThreads;
+            if (q < NQ - 1 || col < hpw) {
+                const double z = (double)src[col];
+                sz[q] += z;
+                sz2[q] += z * z;
+            }
+        }
+    }
+}
 
 template <class TD, class TS, class Fe>
-__device__ __forceinline__ void k_update_open_huge_body(UpdateArgs a, TD* vt, TS* mean, TS* beta) {
+__device__ __forceinline__ void k_update_open_huge_body(UpdateArgs a, TD* vt, TS* mean, TS* beta,
+                                                        const HugeInfo* __restrict__ hinfo) {
     grid_dep_wait();
-    __shared__ int s_id[kHugeChunk];
-    __shared__ double s_d[kHugeChunk];
-    __shared__ double s_w[kHugeChunk];
-#if SVX_HUGE_RING
     extern __shared__ __align__(16) unsigned char hring_raw[];
     Fe* hring = reinterpret_cast<Fe*>(hring_raw);
-#endif
-    __shared__ int s_wcnt[kHugeThreads / 32];
-    __shared__ int s_min, s_max, s_cnt;
-    __shared__ double s_wold;
     FrameCtr* ctr = a.ctr;
-    KSpan _ks(ctr, kSpanUpdateB);
+    KSpan _ks(ctr, kSpanUpdateB, true);   // update_b: k_huge_prep .. k_huge_items
     __shared__ FrameCtr s_ctr_;
     snapshot_ctr(ctr, s_ctr_);
     const FrameCtr* cv = &s_ctr_;
     if (cv->abort | cv->err_cap) return;
     const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
-    unsigned* bm = a.bitmap + (long long)blockIdx.x * a.bm_words;
     const long long Hn = (long long)cv->n_huge;
-    const KeyPack kp = cv->p.kp;
-    const PoseParams pp = cv->p.pp;
     const Fe* feats = (const Fe*)cv->p.feats;
     const int D = a.D;
     // vector mode: row slices by 16-byte cp.async (16-byte sizes and addresses)
-    const bool hbulk = SVX_HUGE_RING && ((D * (int)sizeof(Fe)) & 15) == 0 && (((uintptr_t)feats) & 15) == 0;
+    const bool hbulk = ((D * (int)sizeof(Fe)) & 15) == 0 && (((uintptr_t)feats) & 15) == 0;
 #if SVX_DYN_LONG
     __shared__ long long s_next;
     for (;;) {
@@ -1466,106 +1378,44 @@ __device__ __forceinline__ void k_update_open_huge_body(UpdateArgs a, TD* vt, TS
 #else
     for (long long t = blockIdx.x; t < Hn; t += gridDim.x) {
 #endif
-        const int vid = a.mlist[a.hugelist[t]];
-        const unsigned c = a.rec[vid].cnt;
-        const unsigned k = c & ~kNewBit;
-        if (k > (unsigned)kGiantRows) continue;   // dimension-sliced kernels (k_huge_items)
-        const bool isnew = (c & kNewBit) != 0u;
-        const unsigned seg = a.rec[vid].seg;
-        // ---- point-index bitmap of the voxel's rows
-        if (tid == 0) { s_min = 0x7fffffff; s_max = -1; }
-        __syncthreads();
-        int mn = 0x7fffffff, mx = -1;
-        for (unsigned j = tid; j < k; j += kHugeThreads) {
-            const int v = a.srid[seg + j];
-            mn = min(mn, v);
-            mx = max(mx, v);
-        }
-        mn = __reduce_min_sync(0xffffffffu, (unsigned)mn) ;
-        mx = (int)__reduce_max_sync(0xffffffffu, (unsigned)(mx + 1)) - 1;
-        if (lane == 0) { atomicMin(&s_min, mn); atomicMax(&s_max, mx); }
-        __syncthreads();
-        const int minr = s_min;
-        const long long nwords = ((long long)(s_max - minr) >> 5) + 1;
-        for (long long w = tid; w < nwords; w += kHugeThreads) bm[w] = 0u;
-        __syncthreads();
-        for (unsigned j = tid; j < k; j += kHugeThreads) {
-            const int v = a.srid[seg + j] - minr;
-            atomicOr(&bm[v >> 5], 1u << (v & 31));
-        }
-        __threadfence_block();
-        __syncthreads();
-        const Center cc = center_of(a.rec[vid].key, kp, a.h, pp);
-        TsdfAcc acc{0.0, 0.0, INFINITY, -INFINITY, 0};
-        // dims in passes of kHugeDims * kHugeFeatThreads (one pass for D <= 896);
-        // warp 0 folds the TSDF sums (thread 0), warps 1.. the feature sums
-        for (int dbase = 0; dbase < D; dbase += hbulk ? kHugeDims * kHugeThreads : kHugeDims * kHugeFeatThreads) {
-        const bool first_pass = dbase == 0;
-        const int hpw = min(kHugeDims * kHugeThreads, D - dbase);   // bulk mode: this pass's columns
-        const unsigned hbytes = (unsigned)(hpw * (int)sizeof(Fe));
-        const int hG = max(1, min(16, kHugeRingBytes / (2 * hpw * (int)sizeof(Fe))));
-        double sz[kHugeDims], sz2[kHugeDims];
+        const HugeInfo hi = hinfo[t];   // k_huge_prep: rows sorted, TSDF applied
+        const unsigned k = hi.cnt & ~kNewBit;
+        if (k > (unsigned)kGiantRows) continue;   // dimension-sliced kernel (k_huge_items)
+        const bool isnew = (hi.cnt & kNewBit) != 0u;
+        const int vid = hi.vid;
+        const int* ids = a.srid + hi.seg;
+        const int cnt = (int)k;
+        // NIG batch update with lambda from the pre-frame weight (_pycore.py:438)
+        const double nobs = (double)k;
+        const double lam = fmax(hi.w_old, a.lambda_floor);
+        const double lam_post = lam + nobs;
+        const double coef = lam * nobs / lam_post;
+        const double b_bg = (double)(TS)a.prior_beta;
+        TS* mrow = mean + (long long)vid * D;
+        TS* brow = beta + (long long)vid * D;
+        // dims in passes of kHugeDims * kHugeThreads (one pass for D <= 1024);
+        // thread tid owns dims dbase + tid + 256 q
+        for (int dbase = 0; dbase < D; dbase += kHugeDims * kHugeThreads) {
+            const int hpw = min(kHugeDims * kHugeThreads, D - dbase);   // this pass's columns
+            double sz[kHugeDims], sz2[kHugeDims];
 #pragma unroll
-        for (int q = 0; q < kHugeDims; ++q) { sz[q] = 0.0; sz2[q] = 0.0; }
-        // ---- ascending chunks of 64 words (<= 2048 rows)
-        for (long long w0 = 0; w0 < nwords; w0 += kHugeChunk / 32) {
-            // 64 words: one per thread of the first two warps
-            unsigned bits = 0u;
-            const long long w = w0 + tid;
-            if (tid < kHugeChunk / 32 && w < nwords) bits = __ldcg(bm + w);
-            int cntw = __popc(bits);
-            int incl = cntw;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int y = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += y;
-            }
-            if (lane == 31) s_wcnt[wib] = incl;
-            __syncthreads();
-            int pos = incl - cntw + (wib == 1 ? s_wcnt[0] : 0);
-            if (tid == 0) s_cnt = s_wcnt[0] + s_wcnt[1];
-            while (bits) {
-                const int bpos = __ffs(bits) - 1;
-                bits &= bits - 1;
-                s_id[pos++] = minr + (int)(w * 32 + bpos);
-            }
-            __syncthreads();
-            const int cnt = s_cnt;
-            if (first_pass) {
-                for (int j = tid; j < cnt; j += kHugeThreads) {
-                    double d, wr;
-                    row_dw(cc.x, cc.y, cc.z, a.ray[s_id[j]], a.trunc, a.wfn, d, wr);
-                    s_d[j] = d;
-                    s_w[j] = wr;
-                }
-            }
-            __syncthreads();
+            for (int q = 0; q < kHugeDims; ++q) { sz[q] = 0.0; sz2[q] = 0.0; }
             if (hbulk) {
-                // rows (this pass's columns) stream through two slots of hG rows:
-                // every thread issues 16-byte cp.async chunks of the group's rows,
-                // then folds dims tid + 256 q of each row; thread 0 folds the
-                // group's TSDF rows in between (first pass)
+                // rows stream through three slots of hG rows (one barrier per
+                // group): a warp copies a whole row slice with 16-byte cp.async
+                // per lane, then every thread folds its dims of each row in order
+                const int hG = max(1, min(16, kHugeRingBytes / (3 * hpw * (int)sizeof(Fe))));
                 const int ng = (cnt + hG - 1) / hG;
                 const int c4 = hpw * (int)sizeof(Fe) / 16;   // 16-byte chunks per row
-                // this thread's first chunk (row r0, chunk cc0) and its stride in
-                // (rows, chunks) per kHugeThreads chunks: no division per chunk
-                const int r0 = tid / c4, cc0 = tid - r0 * c4;
-                const int dq = kHugeThreads / c4, dc = kHugeThreads - dq * c4;
                 auto issue = [&](int g) {
                     if (g < ng) {
                         const int j0 = g * hG, nr = min(hG, cnt - j0);
-                        Fe* dst = hring + (size_t)(g & 1) * hG * hpw;
-                        int r = r0, cc = cc0;
-                        while (r < nr) {
-                            __pipeline_memcpy_async(reinterpret_cast<char*>(dst + (size_t)r * hpw) + cc * 16,
-                                                    reinterpret_cast<const char*>(feats + (long long)s_id[j0 + r] * D + dbase) + cc * 16,
-                                                    16);
-                            r += dq;
-                            cc += dc;
-                            if (cc >= c4) {
-                                cc -= c4;
-                                ++r;
-                            }
+                        Fe* dst = hring + (size_t)(g % 3) * hG * hpw;
+                        for (int r = wib; r < nr; r += kHugeThreads / 32) {
+                            const char* srow = reinterpret_cast<const char*>(feats + (long long)__ldg(ids + j0 + r) * D + dbase);
+                            char* drow = reinterpret_cast<char*>(dst + (size_t)r * hpw);
+                            for (int cc = lane; cc < c4; cc += 32)
+                                __pipeline_memcpy_async(drow + cc * 16, srow + cc * 16, 16);
                         }
                     }
                     __pipeline_commit();
@@ -1573,186 +1423,81 @@ __device__ __forceinline__ void k_update_open_huge_body(UpdateArgs a, TD* vt, TS
                 issue(0);
                 issue(1);
                 for (int g = 0; g < ng; ++g) {
-                    const int j0 = g * hG;
-                    const int nr = min(hG, cnt - j0);
-                    if (tid == 0 && first_pass) {
-                        for (int j = j0; j < j0 + nr; ++j) {
-                            const double wq = s_w[j], dq = s_d[j];
-                            acc.sw += wq;
-                            acc.swd += wq * dq;
-                            acc.mind = dq < acc.mind ? dq : acc.mind;
-                            acc.maxd = dq > acc.maxd ? dq : acc.maxd;
-                        }
-                    }
-                    __pipeline_wait_prior(1);   // this thread's chunks of group g
-                    __syncthreads();            // everyone's
-                    const Fe* src = hring + (size_t)(g & 1) * hG * hpw;
-#pragma unroll 2
-                    for (int r = 0; r < nr; ++r, src += hpw) {
-#pragma unroll
-                        for (int q = 0; q < kHugeDims; ++q) {
-                            const int col = tid + q * kHugeThreads;
-                            if (col < hpw) {
-                                const double z = (double)src[col];
-                                sz[q] += z;
-                                sz2[q] += z * z;
-                            }
-                        }
-                    }
-                    __syncthreads();   // the slot is consumed
-                    issue(g + 2);
-                }
-                __pipeline_wait_prior(0);
-                continue;
-            }
-            if (tid == 0 && first_pass) {   // independent chains: one dependent add per row each
-                for (int j = 0; j < cnt; ++j) {
-                    const double wq = s_w[j], dq = s_d[j];
-                    acc.sw += wq;
-                    acc.swd += wq * dq;
-                    acc.mind = dq < acc.mind ? dq : acc.mind;
-                    acc.maxd = dq > acc.maxd ? dq : acc.maxd;
-                }
-            }
-#if SVX_HUGE_RING
-            // rows stream through this thread's slots of a shared-memory ring
-            // (cp.async, kHugeRingR rows x kHugeDims dims per group, two groups
-            // in flight); slot-major layout, so a warp's slots are consecutive
-            if (tid >= 32) {
-                const int ng = (cnt + kHugeRingR - 1) / kHugeRingR;
-                auto slot_of_ring = [&](int g, int r, int q) {
-                    return hring + ((size_t)(((g & 1) * kHugeRingR + r) * kHugeDims + q) * kHugeThreads + tid);
-                };
-                auto issue = [&](int g) {
-                    if (g < ng) {
-#pragma unroll
-                        for (int r = 0; r < kHugeRingR; ++r) {
-                            const int j = g * kHugeRingR + r;
-                            if (j < cnt) {
-                                const long long rowb = (long long)s_id[j] * D;
-#pragma unroll
-                                for (int q = 0; q < kHugeDims; ++q) {
-                                    const int col = dbase + (tid - 32) + q * kHugeFeatThreads;
-                                    if (col < D)
-                                        __pipeline_memcpy_async(slot_of_ring(g, r, q), feats + rowb + col,
-                                                                sizeof(Fe));
-                                }
-                            }
-                        }
-                    }
-                    __pipeline_commit();
-                };
-                issue(0);
-                for (int g = 0; g < ng; ++g) {
-                    issue(g + 1);
-                    __pipeline_wait_prior(1);
-                    const int n = min(kHugeRingR, cnt - g * kHugeRingR);
-                    for (int r = 0; r < n; ++r) {
-#pragma unroll
-                        for (int q = 0; q < kHugeDims; ++q) {
-                            const int col = dbase + (tid - 32) + q * kHugeFeatThreads;
-                            if (col < D) {
-                                const double z = (double)*slot_of_ring(g, r, q);
-                                sz[q] += z;
-                                sz2[q] += z * z;
-                            }
-                        }
+                    const int nr = min(hG, cnt - g * hG);
+                    __pipeline_wait_prior(1);   // this thread's copies of group g
+                    __syncthreads();            // everyone's; everyone is done with group g - 1
+                    issue(g + 2);               // into group g - 1's slot
+                    const Fe* src = hring + (size_t)(g % 3) * hG * hpw;
+                    switch ((hpw + kHugeThreads - 1) / kHugeThreads) {
+                        case 1: fold_rows<1, Fe>(src, nr, hpw, tid, sz, sz2); break;
+                        case 2: fold_rows<2, Fe>(src, nr, hpw, tid, sz, sz2); break;
+                        case 3: fold_rows<3, Fe>(src, nr, hpw, tid, sz, sz2); break;
+                        default: fold_rows<4, Fe>(src, nr, hpw, tid, sz, sz2); break;
                     }
                 }
                 __pipeline_wait_prior(0);
+                __syncthreads();   // every fold done before the slots are reused
+            } else {
+                // unaligned rows: direct loads, same in-order sums
+#pragma unroll
+                for (int q = 0; q < kHugeDims; ++q) {
+                    const int col = dbase + tid + q * kHugeThreads;
+                    if (tid + q * kHugeThreads >= hpw) continue;
+                    for (int j = 0; j < cnt; ++j) {
+                        const double z = (double)feats[(long long)__ldg(ids + j) * D + col];
+                        sz[q] += z;
+                        sz2[q] += z * z;
+                    }
+                }
             }
-#else
 #pragma unroll
             for (int q = 0; q < kHugeDims; ++q) {
-                const int col = dbase + (tid - 32) + q * kHugeFeatThreads;
-                if (tid < 32 || col >= D) continue;
-                int j = 0;
-                for (; j + 4 <= cnt; j += 4) {
-                    const double z0 = (double)feats[(long long)s_id[j] * D + col];
-                    const double z1 = (double)feats[(long long)s_id[j + 1] * D + col];
-                    const double z2 = (double)feats[(long long)s_id[j + 2] * D + col];
-                    const double z3 = (double)feats[(long long)s_id[j + 3] * D + col];
-                    sz[q] += z0; sz2[q] += z0 * z0;
-                    sz[q] += z1; sz2[q] += z1 * z1;
-                    sz[q] += z2; sz2[q] += z2 * z2;
-                    sz[q] += z3; sz2[q] += z3 * z3;
-                }
-                for (; j < cnt; ++j) {
-                    const double z = (double)feats[(long long)s_id[j] * D + col];
-                    sz[q] += z;
-                    sz2[q] += z * z;
-                }
-            }
-#endif
-            __syncthreads();
-        }
-        if (first_pass) {
-            if (tid == 0) s_wold = apply_tsdf<TD>(vt, vid, isnew, a.trunc, acc.sw, acc.swd, acc.mind, acc.maxd);
-            __syncthreads();
-        }
-        // NIG batch update with lambda from the pre-frame weight (_pycore.py:438)
-        const double w_old = s_wold;
-        const double nobs = (double)k;
-        const double lam = fmax(w_old, a.lambda_floor);
-        const double lam_post = lam + nobs;
-        const double coef = lam * nobs / lam_post;
-        const double b_bg = (double)(TS)a.prior_beta;
-        TS* mrow = mean + (long long)vid * D;
-        TS* brow = beta + (long long)vid * D;
-#pragma unroll
-        for (int q = 0; q < kHugeDims; ++q) {
-            if (hbulk) {
                 const int col = dbase + tid + q * kHugeThreads;
-                if (col < D && tid + q * kHugeThreads < hpw)
+                if (tid + q * kHugeThreads < hpw)
                     nig_apply<TS>(mrow, brow, col, isnew, sz[q], sz2[q], lam, lam_post, coef, nobs, b_bg);
-                continue;
             }
-            const int col = dbase + (tid - 32) + q * kHugeFeatThreads;
-            if (tid >= 32 && col < D) nig_apply<TS>(mrow, brow, col, isnew, sz[q], sz2[q], lam, lam_post, coef, nobs, b_bg);
         }
-        }   // dim passes
-        if (tid == 0) clear_voxel_frame(a, vid);
-        __syncthreads();
     }
 }
 
 template <class TD, class TS, class Fe>
-__global__ void __launch_bounds__(kHugeThreads, 2) k_update_open_huge(UpdateArgs a, TD* vt, TS* mean, TS* beta) {
-    k_update_open_huge_body<TD, TS, Fe>(a, vt, mean, beta);
+__global__ void __launch_bounds__(kHugeThreads, 2) k_update_open_huge(UpdateArgs a, TD* vt, TS* mean, TS* beta,
+                                                                     const HugeInfo* __restrict__ hinfo) {
+    k_update_open_huge_body<TD, TS, Fe>(a, vt, mean, beta, hinfo);
 }
 
+// K5p: every huge voxel (> kOpenCtaMin rows), one CTA each: sort the voxel's
+// row ids in place (point-index bitmap in per-CTA scratch, CTA scan), fold
+// its TSDF sums in point order (d, w of 1024 rows at a time in parallel,
+// thread 0 adds them in order; min / max by reduction), apply apply_tsdf and
+// stash (id, count, segment, pre-frame weight) for the feature kernels.  The
+// feature sums then read the sorted segment directly, with no per-row TSDF
+// chain inside their CTA-wide steps.
 template <class TD>
-__global__ void __launch_bounds__(kHugeThreads) k_huge_prep(UpdateArgs a, const TD* vt,
-                                                             HugeInfo* hinfo, int* srid) {
+__global__ void __launch_bounds__(kHugeThreads) k_huge_prep(UpdateArgs a, TD* vt, HugeInfo* hinfo, int* srid) {
     grid_dep_wait();
     using Scan = cub::BlockScan<int, kHugeThreads>;
     __shared__ typename Scan::TempStorage scan_tmp;
     __shared__ int s_min, s_max;
+    __shared__ double s_w[1024], s_p[1024];
+    __shared__ double s_red[2][kHugeThreads / 32];
     FrameCtr* ctr = a.ctr;
+    KSpan _ks(ctr, kSpanUpdateB);   // update_b: this kernel .. k_huge_items (end-only spans)
     __shared__ FrameCtr s_ctr_;
     snapshot_ctr(ctr, s_ctr_);
     const FrameCtr* cv = &s_ctr_;
     if (cv->abort | cv->err_cap) return;
-    const int tid = threadIdx.x, lane = tid & 31;
+    const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
     unsigned* bm = a.bitmap + (long long)blockIdx.x * a.bm_words;
     const long long Hn = (long long)cv->n_huge;
+    const KeyPack kp = cv->p.kp;
+    const PoseParams pp = cv->p.pp;
     for (long long t = blockIdx.x; t < Hn; t += gridDim.x) {
         const int vid = a.mlist[a.hugelist[t]];
         const unsigned c = a.rec[vid].cnt;
         const unsigned k = c & ~kNewBit;
         const unsigned seg = a.rec[vid].seg;
-        if (k <= (unsigned)kGiantRows) {   // k_update_open_huge's voxel: no items
-            if (tid == 0) hinfo[t].cnt = 0u;
-            continue;
-        }
         if (tid == 0) {
-            HugeInfo hi;
-            hi.vid = vid;
-            hi.cnt = c;
-            hi.seg = seg;
-            hi.pad = 0u;
-            hi.w_old = (c & kNewBit) ? 0.0 : (double)vt[2 * (long long)vid + 1];
-            hinfo[t] = hi;
             s_min = 0x7fffffff;
             s_max = -1;
         }
@@ -1796,6 +1541,84 @@ __global__ void __launch_bounds__(kHugeThreads) k_huge_prep(UpdateArgs a, const 
             base += total;
             __syncthreads();
         }
+        __threadfence_block();
+        __syncthreads();
+        if (k > (unsigned)kGiantRows) {
+            // giant voxel: its TSDF item in k_huge_items runs beside the feature
+            // items (and clears the voxel's frame record)
+            if (tid == 0) {
+                HugeInfo hi;
+                hi.vid = vid;
+                hi.cnt = c;
+                hi.seg = seg;
+                hi.pad = 0u;
+                hi.w_old = (c & kNewBit) ? 0.0 : (double)vt[2 * (long long)vid + 1];
+                hinfo[t] = hi;
+            }
+            __syncthreads();
+            continue;
+        }
+        // TSDF sums in point order (_core.pyx:759-843)
+        const Center cc = center_of(a.rec[vid].key, kp, a.h, pp);
+        const int* ids = srid + seg;
+        double sw = 0.0, swd = 0.0, mind = INFINITY, maxd = -INFINITY;
+        for (unsigned j0 = 0; j0 < k; j0 += 1024) {
+            const unsigned n = min(1024u, k - j0);
+            for (unsigned q = tid; q < n; q += kHugeThreads) {
+                double d, wr;
+                row_dw(cc.x, cc.y, cc.z, a.ray[ids[j0 + q]], a.trunc, a.wfn, d, wr);
+                s_w[q] = wr;
+                s_p[q] = wr * d;
+                mind = d < mind ? d : mind;
+                maxd = d > maxd ? d : maxd;
+            }
+            __syncthreads();
+            if (tid == 0) {
+                unsigned q = 0;
+                for (; q + 8 <= n; q += 8) {
+                    double wv[8], pv[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        wv[u] = s_w[q + u];
+                        pv[u] = s_p[q + u];
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        sw += wv[u];
+                        swd += pv[u];
+                    }
+                }
+                for (; q < n; ++q) {
+                    sw += s_w[q];
+                    swd += s_p[q];
+                }
+            }
+            __syncthreads();
+        }
+        for (int o = 16; o; o >>= 1) {
+            mind = fmin(mind, __shfl_xor_sync(0xffffffffu, mind, o));
+            maxd = fmax(maxd, __shfl_xor_sync(0xffffffffu, maxd, o));
+        }
+        if (lane == 0) {
+            s_red[0][wib] = mind;
+            s_red[1][wib] = maxd;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            for (int w = 1; w < kHugeThreads / 32; ++w) {
+                mind = fmin(mind, s_red[0][w]);
+                maxd = fmax(maxd, s_red[1][w]);
+            }
+            HugeInfo hi;
+            hi.vid = vid;
+            hi.cnt = c;
+            hi.seg = seg;
+            hi.pad = 0u;
+            hi.w_old = apply_tsdf<TD>(vt, vid, (c & kNewBit) != 0u, a.trunc, sw, swd, mind, maxd);
+            hinfo[t] = hi;
+            clear_voxel_frame(a, vid);   // (the feature kernels read hinfo only)
+        }
+        __syncthreads();
     }
 }
 
@@ -1806,7 +1629,7 @@ __global__ void __launch_bounds__(kHugeThreads, 1) k_huge_items(UpdateArgs a, TD
     grid_dep_wait();
     FrameCtr* ctr = a.ctr;
     {
-    KSpan _ks(ctr, kSpanUpdateB, true);   // update_b spans k_update_open_huge .. k_huge_items
+    KSpan _ks(ctr, kSpanUpdateB, true);   // update_b spans k_huge_prep .. k_huge_items
     __shared__ FrameCtr s_ctr_;
     __shared__ double s_red[4][kHugeThreads / 32];
     snapshot_ctr(ctr, s_ctr_);
@@ -1840,7 +1663,7 @@ __global__ void __launch_bounds__(kHugeThreads, 1) k_huge_items(UpdateArgs a, TD
         const unsigned k = hi.cnt & ~kNewBit;
         const bool isnew = (hi.cnt & kNewBit) != 0u;
         const int* ids = a.srid + hi.seg;
-        if (k == 0u) continue;   // not a giant voxel (k_update_open_huge)
+        if (k <= (unsigned)kGiantRows) continue;   // k_update_open_huge's voxel (k_huge_prep applied its TSDF)
         if (sl == S) {
             // ---- TSDF item: w and w*d of 1024 rows at a time in parallel; thread 0
             // folds the two sums in order (loads batched ahead of the adds), min/max
@@ -2098,20 +1921,18 @@ svx_status open_a(svx_map* m, cudaStream_t s) {
 
 template <class TD, class TS, class Fe>
 svx_status open_b(svx_map* m, cudaStream_t s) {
-    const int hsmem = SVX_HUGE_RING ? std::max(2 * kHugeRingR * kHugeDims * kHugeThreads * (int)sizeof(Fe),
-                                               kHugeRingBytes) : 0;
-    if (hsmem > 0) {
-        SVX_CUDA(cudaFuncSetAttribute(k_update_open_huge<TD, TS, Fe>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, hsmem));
-        // two CTAs per SM need the largest shared-memory carveout
-        SVX_CUDA(cudaFuncSetAttribute(k_update_open_huge<TD, TS, Fe>,
-                                      cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    }
-    SVX_CUDA(launch_pdl(k_update_open_huge<TD, TS, Fe>, kHugeCtas, kHugeThreads, hsmem, s, make_args(m),
-                        ptr<TD>(m->vt), ptr<TS>(m->s0), ptr<TS>(m->s1)));
-    SVX_LAUNCHED();
+    // sort + TSDF of every huge voxel first, then their feature sums
     SVX_CUDA(launch_pdl(k_huge_prep<TD>, kHugeCtas, kHugeThreads, 0, s, make_args(m), ptr<TD>(m->vt),
                         ptr<HugeInfo>(m->hinfo), ptr<int>(m->srid)));
+    SVX_LAUNCHED();
+    const int hsmem = kHugeRingBytes;
+    SVX_CUDA(cudaFuncSetAttribute(k_update_open_huge<TD, TS, Fe>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  hsmem));
+    // two CTAs per SM need the largest shared-memory carveout
+    SVX_CUDA(cudaFuncSetAttribute(k_update_open_huge<TD, TS, Fe>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                  100));
+    SVX_CUDA(launch_pdl(k_update_open_huge<TD, TS, Fe>, kHugeCtas, kHugeThreads, hsmem, s, make_args(m),
+                        ptr<TD>(m->vt), ptr<TS>(m->s0), ptr<TS>(m->s1), ptr<HugeInfo>(m->hinfo)));
     SVX_LAUNCHED();
     const int smem = kHugeStages * kHugeStageBytes;
     SVX_CUDA(cudaFuncSetAttribute(k_huge_items<TD, TS, Fe>, cudaFuncAttributeMaxDynamicSharedMemorySize,
