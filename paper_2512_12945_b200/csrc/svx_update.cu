@@ -899,6 +899,16 @@ __device__ __forceinline__ void prefetch_rows_l2(const void* m, const void* b, i
     }
 }
 
+// Σz² term of the open-set sums: z is an f32 value widened to f64, so z·z is
+// exact in f64 (24-bit significands) and one fused multiply-add rounds exactly
+// like the reference's product-then-add (_pycore.py:432-446); f64 features keep
+// the two separate steps.
+template <class Fe>
+__device__ __forceinline__ double add_sq(double s, double z) {
+    if constexpr (sizeof(Fe) == 4) return fma(z, z, s);
+    else return s + z * z;
+}
+
 // Per-dimension sequential sums over an ordered chunk (lane owns dims
 // base + lane + 32 q).
 template <class Fe>
@@ -914,7 +924,7 @@ __device__ __forceinline__ void open_chunk(const Fe* __restrict__ feats, int D, 
             if (base + cc < D) {
                 const double zv = (double)f[cc];
                 sz[q] += zv;
-                sz2[q] += zv * zv;
+                sz2[q] = add_sq<Fe>(sz2[q], zv);
             }
         }
     }
@@ -974,7 +984,7 @@ __device__ __forceinline__ void open_chunk_ring(const Fe* __restrict__ feats, in
                 if (base + cc < D) {
                     const double zv = (double)src[r * kOpenPass + cc];
                     sz[q] += zv;
-                    sz2[q] += zv * zv;
+                    sz2[q] = add_sq<Fe>(sz2[q], zv);
                 }
             }
         }
@@ -1107,7 +1117,7 @@ __device__ __forceinline__ void open_chunk_grp(const Fe* __restrict__ feats, int
 #pragma unroll
                 for (int q = 0; q < kOpenPer; ++q) {
                     sz[q] += v[q];
-                    sz2[q] += v[q] * v[q];
+                    sz2[q] = add_sq<Fe>(sz2[q], v[q]);
                 }
             } else {
 #pragma unroll
@@ -1116,7 +1126,7 @@ __device__ __forceinline__ void open_chunk_grp(const Fe* __restrict__ feats, int
                     if (cc < nd) {
                         const double zv = (double)src[cc];
                         sz[q] += zv;
-                        sz2[q] += zv * zv;
+                        sz2[q] = add_sq<Fe>(sz2[q], zv);
                     }
                 }
             }
@@ -1343,7 +1353,7 @@ __device__ __forceinline__ void fold_rows(const Fe* src, int nr, int hpw, int ti
             if (q < NQ - 1 || col < hpw) {
                 const double z = (double)src[col];
                 sz[q] += z;
-                sz2[q] += z * z;
+                sz2[q] = add_sq<Fe>(sz2[q], z);
             }
         }
     }
@@ -1446,7 +1456,7 @@ __device__ __forceinline__ void k_update_open_huge_body(UpdateArgs a, TD* vt, TS
                     for (int j = 0; j < cnt; ++j) {
                         const double z = (double)feats[(long long)__ldg(ids + j) * D + col];
                         sz[q] += z;
-                        sz2[q] += z * z;
+                        sz2[q] = add_sq<Fe>(sz2[q], z);
                     }
                 }
             }
@@ -1797,13 +1807,13 @@ __global__ void __launch_bounds__(kHugeThreads, 1) k_huge_items(UpdateArgs a, TD
 #pragma unroll
                     for (int u = 0; u < 8; ++u) {
                         sz += z[u];
-                        sz2 += z[u] * z[u];
+                        sz2 = add_sq<Fe>(sz2, z[u]);
                     }
                 }
                 for (; r < n; ++r) {
                     const double z = (double)buf[r * W + mycol];
                     sz += z;
-                    sz2 += z * z;
+                    sz2 = add_sq<Fe>(sz2, z);
                 }
             }
             __syncthreads();
