@@ -190,10 +190,11 @@ def stage_bytes(stage, rep, kind, C, D, tsdf_elem, mode="segments"):
         "seg": U * 8,
         # per row: voxel id + count in; single-row voxels also ray + label + state
         "scatter": R * (4 + 4 + 4) + U * (32 + 2 * S),
-        # multi-row voxels: rows, rays, labels or feature rows, and state
-        # (upper bound: all voxels); open-set: each row reads its point's
-        # feature vector (4D bytes) once
-        "update": 2 * U * S + R * (4 + 32 + (4 if kind == "closed" else 0)) + R * (4 * D if kind == "open" else 0),
+        # multi-row voxels: rows, rays, labels, and state (upper bound: all
+        # voxels); open-set: the frame's feature array once (SURVEY 8(d):
+        # N_used * 4D) -- a row's re-read of its point's features (~9 per point)
+        # is the implementation's cost, not algorithmic bytes
+        "update": 2 * U * S + R * (4 + 32 + (4 if kind == "closed" else 0)) + (used * 4 * D if kind == "open" else 0),
         "update_b": 0,
     }[stage]
 

@@ -13,7 +13,7 @@ python -c "import __graft_entry__ as g; g.smoke()" > "$OUT/${TAG}_smoke.log" 2>&
 timeout 600 python bench.py > "$OUT/${TAG}_bench_cfg2.json" 2> "$OUT/${TAG}_bench_cfg2.err"
 timeout 900 python bench.py --impl reference --steps 5 --warmup 3 > "$OUT/${TAG}_bench_ref.json" 2> "$OUT/${TAG}_bench_ref.err"
 timeout 600 python bench.py --config 1 --depth --steps 15 --warmup 3 --no-cpu-baseline > "$OUT/${TAG}_bench_cfg1_depth.json" 2> "$OUT/${TAG}_bench_cfg1.err"
-timeout 600 python bench.py --config 4 --steps 15 --warmup 3 --no-cpu-baseline > "$OUT/${TAG}_bench_cfg4.json" 2> "$OUT/${TAG}_bench_cfg4.err"
+timeout 600 python bench.py --config 4 --no-cpu-baseline > "$OUT/${TAG}_bench_cfg4.json" 2> "$OUT/${TAG}_bench_cfg4.err"
 timeout 900 python bench.py --config 3 --depth --steps 15 --warmup 3 --no-cpu-baseline > "$OUT/${TAG}_bench_cfg3_depth.json" 2> "$OUT/${TAG}_bench_cfg3.err"
 timeout 900 python bench.py --config 5 --depth --steps 10 --warmup 3 --no-cpu-baseline > "$OUT/${TAG}_bench_cfg5_depth.json" 2> "$OUT/${TAG}_bench_cfg5.err"
 [ -n "${NO_NCU:-}" ] && exit 0
