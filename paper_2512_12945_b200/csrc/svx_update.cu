@@ -1322,7 +1322,13 @@ constexpr int kGiantRows = 8192;
 #endif
 constexpr int kHugeFold = SVX_HUGE_FOLD;
 static_assert(kHugeFold >= 1 && kHugeFold <= 8, "fold warps per item");
-constexpr int kHugeRingBytes = 64 * 1024;   // k_update_open_huge: three row slots of dynamic shared memory
+#ifndef SVX_HUGE_MINB
+#define SVX_HUGE_MINB 3   // k_update_open_huge CTAs per SM (<= 85 registers, no spills)
+#endif
+#ifndef SVX_HUGE_RING_KB
+#define SVX_HUGE_RING_KB 72
+#endif
+constexpr int kHugeRingBytes = SVX_HUGE_RING_KB * 1024;   // k_update_open_huge: three row slots of dynamic shared memory
 
 struct HugeInfo {
     int vid;
@@ -1471,7 +1477,7 @@ __device__ __forceinline__ void k_update_open_huge_body(UpdateArgs a, TD* vt, TS
 }
 
 template <class TD, class TS, class Fe>
-__global__ void __launch_bounds__(kHugeThreads, 2) k_update_open_huge(UpdateArgs a, TD* vt, TS* mean, TS* beta,
+__global__ void __launch_bounds__(kHugeThreads, SVX_HUGE_MINB) k_update_open_huge(UpdateArgs a, TD* vt, TS* mean, TS* beta,
                                                                      const HugeInfo* __restrict__ hinfo) {
     k_update_open_huge_body<TD, TS, Fe>(a, vt, mean, beta, hinfo);
 }
@@ -1941,7 +1947,7 @@ svx_status open_b(svx_map* m, cudaStream_t s) {
     // two CTAs per SM need the largest shared-memory carveout
     SVX_CUDA(cudaFuncSetAttribute(k_update_open_huge<TD, TS, Fe>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                   100));
-    SVX_CUDA(launch_pdl(k_update_open_huge<TD, TS, Fe>, kHugeCtas, kHugeThreads, hsmem, s, make_args(m),
+    SVX_CUDA(launch_pdl(k_update_open_huge<TD, TS, Fe>, 148 * SVX_HUGE_MINB, kHugeThreads, hsmem, s, make_args(m),
                         ptr<TD>(m->vt), ptr<TS>(m->s0), ptr<TS>(m->s1), ptr<HugeInfo>(m->hinfo)));
     SVX_LAUNCHED();
     const int smem = kHugeStages * kHugeStageBytes;
