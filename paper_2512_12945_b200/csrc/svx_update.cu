@@ -1308,7 +1308,7 @@ constexpr int kHugeStages = 4;
 #define SVX_HUGE_STAGE_KB 16
 #endif
 #ifndef SVX_HUGE_ITEM_CPS
-#define SVX_HUGE_ITEM_CPS 2
+#define SVX_HUGE_ITEM_CPS 3
 #endif
 constexpr int kHugeStageBytes = SVX_HUGE_STAGE_KB * 1024;
 constexpr int kHugeItemCtas = 148 * SVX_HUGE_ITEM_CPS;   // CTAs per SM x SMs (4 stages of shared memory each)
@@ -1639,7 +1639,7 @@ __global__ void __launch_bounds__(kHugeThreads) k_huge_prep(UpdateArgs a, TD* vt
 }
 
 template <class TD, class TS, class Fe>
-__global__ void __launch_bounds__(kHugeThreads, 1) k_huge_items(UpdateArgs a, TD* vt, TS* mean, TS* beta,
+__global__ void __launch_bounds__(kHugeThreads, SVX_HUGE_ITEM_CPS) k_huge_items(UpdateArgs a, TD* vt, TS* mean, TS* beta,
                                                                 const HugeInfo* __restrict__ hinfo) {
     extern __shared__ __align__(16) unsigned char hsm[];
     grid_dep_wait();
