@@ -571,7 +571,10 @@ inline int grid_for(int64_t n, int threads) {
 }
 
 constexpr int kPersistentBlocks = 148 * 8;   // grid-stride kernels over device-side counts
-constexpr int kResolveTile = 256;            // K2 rows per CTA step
+#ifndef SVX_RESOLVE_TILE
+#define SVX_RESOLVE_TILE 256
+#endif
+constexpr int kResolveTile = SVX_RESOLVE_TILE;   // K2 rows per CTA step
 // Slot mode: K2 CTA b lists its touched voxels in tent[b * region, ...); a CTA
 // handles at most ceil(tiles / grid) tiles of kResolveTile rows.
 inline long long slot_region(unsigned long long rows_cap) {

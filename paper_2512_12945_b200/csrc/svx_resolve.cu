@@ -39,7 +39,10 @@ constexpr int kSegBlocks = 148 * 4;
 
 // K2: rows -> voxel ids over CTA-synchronous tiles of 256 rows
 // (svx_resolve_tile.cuh).
-__global__ void __launch_bounds__(kResolveThreads, 6) k_resolve(
+#ifndef SVX_RESOLVE_MINB
+#define SVX_RESOLVE_MINB 6
+#endif
+__global__ void __launch_bounds__(kResolveThreads, SVX_RESOLVE_MINB) k_resolve(
     const unsigned long long* __restrict__ rowkey, const int* __restrict__ rowray,
     const double* __restrict__ rowd, const int* __restrict__ rowlab, rt::ResolveArgs ra) {
     grid_dep_wait();
