@@ -152,8 +152,8 @@ svx_status reserve_frame(svx_map* m, int64_t n, cudaStream_t s) {
     SVX_TRY(ensure(m->longlist, 2 * sizeof(int) * rows, s));   // long list, then huge list
     SVX_TRY(ensure(m->srid, sizeof(int) * rows, s));
     SVX_TRY(ensure(m->bitmap, (size_t)4 * huge_warps() * ((m->npts_cap + 31) / 32 + 1), s));
-    if (m->cfg.sem_kind == SVX_SEM_OPEN)   // huge voxels have > 256 rows each
-        SVX_TRY(ensure(m->hinfo, huge_info_bytes() * (size_t)(rows / 256 + 2), s));
+    if (m->cfg.sem_kind == SVX_SEM_OPEN)   // huge voxels have > open_cta_min() rows each
+        SVX_TRY(ensure(m->hinfo, huge_info_bytes() * (size_t)(rows / open_cta_min() + 2), s));
     SVX_TRY(ensure(m->rowray, sizeof(int) * rows, s));
     if (m->cfg.sem_kind != SVX_SEM_OPEN && !m->cfg.space_carving) {   // slot / leaf mode rows
         SVX_TRY(ensure(m->rowd, sizeof(double) * rows, s));

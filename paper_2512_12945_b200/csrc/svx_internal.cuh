@@ -677,6 +677,7 @@ svx_status launch_rehash(svx_map* m, int4* new_table, int64_t new_cap, cudaStrea
 svx_status launch_fill_u64(unsigned long long* p, int64_t n, unsigned long long v, cudaStream_t s);
 int huge_warps();
 size_t huge_info_bytes();
+int open_cta_min();   // open-set voxels above this many rows take the CTA kernels
 
 // frame driver pieces shared by svx_integrate and the sharded calls (svx_frame.cu)
 void init_row_space(svx_map* m, int64_t n);

@@ -812,6 +812,9 @@ constexpr int kOpenPer = 8;   // dims per lane per pass (256 dims per pass)
 #define SVX_OPEN_CTA_MIN 256   // measured best of 64 / 256 / 1024 on cfg3 and cfg5
 #endif
 constexpr int kOpenCtaMin = SVX_OPEN_CTA_MIN;
+// (k_update_open sorts a segment in a power-of-two shared buffer of kOpenCtaMin rows)
+static_assert((kOpenCtaMin & (kOpenCtaMin - 1)) == 0 && kOpenCtaMin >= 32 && kOpenCtaMin <= kSmemMax,
+              "kOpenCtaMin: a power of two in [32, kSmemMax]");
 
 template <class TS>
 __device__ __forceinline__ void nig_apply(TS* mrow, TS* brow, int c, bool isnew, double sz,
@@ -2034,5 +2037,6 @@ svx_status launch_fill_u64(unsigned long long* p, int64_t n, unsigned long long 
 
 int huge_warps() { return kHugeWarps; }
 size_t huge_info_bytes() { return sizeof(HugeInfo); }
+int open_cta_min() { return kOpenCtaMin; }
 
 }  // namespace svx
