@@ -12,6 +12,9 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <string.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <time.h>
 
 #include "svx_internal.cuh"
 
@@ -68,6 +71,13 @@ svx_status backproject_t(svx_map* m, const void* depth, const svx_camera& cam, i
 
 }  // namespace
 
+static const bool g_trace_depth = getenv("SVX_TRACE_HOST") != nullptr;
+static double depth_now_us() {
+    timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return ts.tv_sec * 1e6 + ts.tv_nsec * 1e-3;
+}
+
 svx_status integrate_depth_impl(svx_map* m, const void* depth, int depth_dtype, const svx_camera& cam,
                                 const PoseParams& pp, const int32_t* labels, const void* feats,
                                 int feats_f64, cudaStream_t s, svx_report* rep) {
@@ -80,6 +90,7 @@ svx_status integrate_depth_impl(svx_map* m, const void* depth, int depth_dtype, 
     const int kind = m->cfg.sem_kind;
     if (kind == SVX_SEM_CLOSED && !labels) return fail(SVX_E_PAYLOAD, "closed-set grid requires per-point labels");
     if (kind == SVX_SEM_OPEN && !feats) return fail(SVX_E_PAYLOAD, "open-set grid requires per-point features");
+    const double t0 = g_trace_depth ? depth_now_us() : 0.0;
     const int H = cam.height, W = cam.width, st = cam.stride;
     const int Hs = (H + st - 1) / st, Ws = (W + st - 1) / st;
     const long long npix = (long long)H * W, n = (long long)Hs * Ws;
@@ -120,11 +131,16 @@ svx_status integrate_depth_impl(svx_map* m, const void* depth, int depth_dtype, 
     svx_report r;
     const int32_t* lab_use = kind == SVX_SEM_CLOSED ? (st > 1 ? lab_out : lab_in) : nullptr;
     const void* feat_use = kind == SVX_SEM_OPEN ? (st > 1 ? feat_out : fd) : nullptr;
+    const double t1 = g_trace_depth ? depth_now_us() : 0.0;
     SVX_TRY(integrate_impl(m, pts, 1, n, pp, lab_use, feat_use, feats_f64, s, &r, 1));
+    const double t2 = g_trace_depth ? depth_now_us() : 0.0;
     unsigned long long inv = 0;
     SVX_CUDA(cudaMemcpyAsync(&inv, d_inv, sizeof(inv), cudaMemcpyDeviceToHost, s));
     SVX_CUDA(cudaStreamSynchronize(s));
     // invalid pixels are not points of the reference's Frame
+    if (g_trace_depth)
+        fprintf(stderr, "svx depth us: backproject %.1f integrate %.1f tail %.1f\n", t1 - t0, t2 - t1,
+                depth_now_us() - t2);
     r.points_in -= (int64_t)inv;
     r.skipped_nonfinite -= (int64_t)inv;
     if (rep) *rep = r;

@@ -801,6 +801,17 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, SVX_LONGK_MINB) k_update_lo
 // ---- K5 open set: one warp per voxel, lanes own feature dimensions ------------
 
 constexpr int kOpenPer = 8;   // dims per lane per pass (256 dims per pass)
+#ifndef SVX_OPEN_SPLIT
+#define SVX_OPEN_SPLIT 1
+#endif
+__device__ __forceinline__ int open_col(int lane, int q) {
+#if SVX_OPEN_SPLIT
+    return (q >> 2) * 128 + 4 * lane + (q & 3);
+#else
+    return 8 * lane + q;
+#endif
+}
+
 #ifndef SVX_OPEN_RING
 #define SVX_OPEN_RING 1
 #endif
@@ -834,7 +845,7 @@ __device__ __forceinline__ void nig_apply(TS* mrow, TS* brow, int c, bool isnew,
     brow[c] = (TS)b_new;
 }
 
-// nig_apply for the 8 contiguous dimensions c0 .. c0+7 of a full pass (f32
+// nig_apply for the 8 dimensions base + open_col(lane, 0..7) of a full pass (f32
 // state: two 16-byte loads and stores per row of mean / beta); per element the
 // same arithmetic as nig_apply.
 // a / b, correctly rounded, from y = RN(1 / b): q = RN(a y) is within an ulp of
@@ -850,7 +861,7 @@ __device__ __forceinline__ double div_rn(double a, double b, double y) {
 }
 
 template <class TS>
-__device__ __forceinline__ void nig_apply8(TS* mrow, TS* brow, int c0, bool isnew, const double* sz,
+__device__ __forceinline__ void nig_apply8(TS* mrow, TS* brow, int base, int lane, bool isnew, const double* sz,
                                            const double* sz2, double lam, double lam_post, double coef,
                                            double nobs, double b_bg) {
     if constexpr (sizeof(TS) == 4) {
@@ -859,9 +870,11 @@ __device__ __forceinline__ void nig_apply8(TS* mrow, TS* brow, int c0, bool isne
 #pragma unroll
             for (int q = 0; q < 8; ++q) { m[q] = 0.0f; b[q] = (float)b_bg; }
         } else {
-            const float4* m4 = reinterpret_cast<const float4*>(mrow + c0);
-            const float4* b4 = reinterpret_cast<const float4*>(brow + c0);
-            const float4 m0 = m4[0], m1 = m4[1], b0 = b4[0], b1 = b4[1];
+            const int c0 = base + open_col(lane, 0), c1 = base + open_col(lane, 4);
+            const float4 m0 = *reinterpret_cast<const float4*>(mrow + c0),
+                         m1 = *reinterpret_cast<const float4*>(mrow + c1),
+                         b0 = *reinterpret_cast<const float4*>(brow + c0),
+                         b1 = *reinterpret_cast<const float4*>(brow + c1);
             m[0] = m0.x; m[1] = m0.y; m[2] = m0.z; m[3] = m0.w; m[4] = m1.x; m[5] = m1.y; m[6] = m1.z; m[7] = m1.w;
             b[0] = b0.x; b[1] = b0.y; b[2] = b0.z; b[3] = b0.w; b[4] = b1.x; b[5] = b1.y; b[6] = b1.z; b[7] = b1.w;
         }
@@ -879,16 +892,16 @@ __device__ __forceinline__ void nig_apply8(TS* mrow, TS* brow, int c0, bool isne
             m[q] = (float)m_new;
             b[q] = (float)(b_old + 0.5 * ss + gap);
         }
-        float4* mo = reinterpret_cast<float4*>(mrow + c0);
-        float4* bo = reinterpret_cast<float4*>(brow + c0);
-        mo[0] = make_float4(m[0], m[1], m[2], m[3]);
-        mo[1] = make_float4(m[4], m[5], m[6], m[7]);
-        bo[0] = make_float4(b[0], b[1], b[2], b[3]);
-        bo[1] = make_float4(b[4], b[5], b[6], b[7]);
+        const int c0 = base + open_col(lane, 0), c1 = base + open_col(lane, 4);
+        *reinterpret_cast<float4*>(mrow + c0) = make_float4(m[0], m[1], m[2], m[3]);
+        *reinterpret_cast<float4*>(mrow + c1) = make_float4(m[4], m[5], m[6], m[7]);
+        *reinterpret_cast<float4*>(brow + c0) = make_float4(b[0], b[1], b[2], b[3]);
+        *reinterpret_cast<float4*>(brow + c1) = make_float4(b[4], b[5], b[6], b[7]);
     } else {
 #pragma unroll
         for (int q = 0; q < 8; ++q)
-            nig_apply<TS>(mrow, brow, c0 + q, isnew, sz[q], sz2[q], lam, lam_post, coef, nobs, b_bg);
+            nig_apply<TS>(mrow, brow, base + open_col(lane, q), isnew, sz[q], sz2[q], lam, lam_post, coef,
+                          nobs, b_bg);
     }
 }
 
@@ -1039,21 +1052,26 @@ struct BulkRing {
     unsigned phase;             // bit s = parity of slot s's next completion
 };
 
-// Full passes (kOpenPass columns): lane owns the 8 contiguous columns
-// base + 8 lane .. +7, read from the ring with two 16-byte shared loads (f32)
-// and no per-column bounds checks; same per-column in-order sums.
+// Full passes (kOpenPass columns): lane owns columns base + 4 lane .. +3 and
+// base + 128 + 4 lane .. +3 (SVX_OPEN_SPLIT; else the 8 contiguous columns
+// base + 8 lane .. +7), read from the ring with two 16-byte shared loads (f32)
+// and no per-column bounds checks; same per-column in-order sums.  The split
+// mapping makes each 16-byte load of a warp one contiguous 512-byte span
+// (4 shared wavefronts, no bank conflicts) and the mean / beta rows of the
+// NIG apply coalesced 512-byte accesses.
 template <class Fe>
-__device__ __forceinline__ void load8(const Fe* p, double* v) {
+__device__ __forceinline__ void load8(const Fe* row, int lane, double* v) {
     if constexpr (sizeof(Fe) == 4) {
-        const float4 a = reinterpret_cast<const float4*>(p)[0], b = reinterpret_cast<const float4*>(p)[1];
+        const float4 a = *reinterpret_cast<const float4*>(row + open_col(lane, 0)),
+                     b = *reinterpret_cast<const float4*>(row + open_col(lane, 4));
         v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
         v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
     } else {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const double2 a = reinterpret_cast<const double2*>(p)[q];
-            v[2 * q] = a.x;
-            v[2 * q + 1] = a.y;
+        for (int q = 0; q < 8; q += 2) {
+            const double2 a = *reinterpret_cast<const double2*>(row + open_col(lane, q));
+            v[q] = a.x;
+            v[q + 1] = a.y;
         }
     }
 }
@@ -1116,7 +1134,7 @@ __device__ __forceinline__ void open_chunk_grp(const Fe* __restrict__ feats, int
         for (int r = 0; r < nr; ++r, src += kOpenPass) {
             if constexpr (kFull) {
                 double v[kOpenPer];
-                load8<Fe>(src + kOpenPer * lane, v);
+                load8<Fe>(src, lane, v);
 #pragma unroll
                 for (int q = 0; q < kOpenPer; ++q) {
                     sz[q] += v[q];
@@ -1191,12 +1209,11 @@ __device__ __forceinline__ void open_voxel(const UpdateArgs& a, const KeyPack& k
         } else if (bulk && base + kOpenPass <= a.D) {   // full pass, contiguous columns per lane
             open_chunk_grp<Fe, true>(feats, a.D, base, buf, (int)k, sz, sz2, *bulk);
             if ((a.D & 3) == 0) {   // 16-byte aligned rows of mean / beta
-                nig_apply8<TS>(mrow, brow, base + kOpenPer * lane, isnew, sz, sz2, lam, lam_post, coef, nobs,
-                               b_bg);
+                nig_apply8<TS>(mrow, brow, base, lane, isnew, sz, sz2, lam, lam_post, coef, nobs, b_bg);
             } else {
 #pragma unroll
                 for (int q = 0; q < kOpenPer; ++q)
-                    nig_apply<TS>(mrow, brow, base + kOpenPer * lane + q, isnew, sz[q], sz2[q], lam, lam_post,
+                    nig_apply<TS>(mrow, brow, base + open_col(lane, q), isnew, sz[q], sz2[q], lam, lam_post,
                                   coef, nobs, b_bg);
             }
             continue;
