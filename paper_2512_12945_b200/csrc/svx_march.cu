@@ -204,28 +204,68 @@ __device__ __forceinline__ void publish_tally(const Tally& t, FrameCtr* ctr) {
     }
 }
 
-// Open-set validation (features all finite), warp-cooperative: the warp
-// checks its lanes' feature rows one after another with coalesced loads
-// (a per-thread loop over D would read 32 rows with stride D).  Called by
-// all 32 lanes; `has` = this lane has a point to check.
+// Open-set validation (features all finite), warp-cooperative.  The warp's
+// points are consecutive (i = tile base + lane) and the valid ones a prefix,
+// so their feature rows are one contiguous block: the lanes stream it with
+// independent 16-byte loads, several in flight per lane, and collect a
+// bit per bad row; one OR-reduction gives every lane its verdict.  (The
+// features are the frame's largest input -- 2.8 GB at cfg5 -- and this scan
+// is its first read.)  Other lane patterns take the row-by-row loop.  Called
+// by all 32 lanes; `has` = this lane has a point to check.
+#ifndef SVX_FEAT_UNROLL
+#define SVX_FEAT_UNROLL 8
+#endif
+__device__ __forceinline__ bool finite4(const float4 v) {
+    const unsigned e = 0x7f800000u;
+    return ((__float_as_uint(v.x) & e) != e) & ((__float_as_uint(v.y) & e) != e) &
+           ((__float_as_uint(v.z) & e) != e) & ((__float_as_uint(v.w) & e) != e);
+}
+
 template <class Fe>
 __device__ __forceinline__ bool warp_feats_finite(const Fe* __restrict__ feats, int D, long long i,
                                                   bool has) {
     const int lane = threadIdx.x & 31;
+    const unsigned todo = __ballot_sync(0xffffffffu, has);
+    if (!todo) return true;
+    if constexpr (sizeof(Fe) == 4) {
+    const long long i0 = __shfl_sync(0xffffffffu, i, 0);
+    const bool contiguous = __all_sync(0xffffffffu, i == i0 + lane) && (todo & (todo + 1u)) == 0u;
+    if ((D & 3) == 0 && D < 46336 && contiguous) {
+        const int nrows = __popc(todo);
+        const unsigned d4 = (unsigned)D >> 2;
+        const unsigned total = (unsigned)nrows * d4;       // float4 chunks of the block
+        // row = c / d4 by a multiply-high: exact while c * d4 < 2^32 (c < 32 d4, D < 46336)
+        const unsigned magic = d4 > 1u ? (unsigned)((0x100000000ULL + d4 - 1) / d4) : 0u;
+        const float4* f4 = reinterpret_cast<const float4*>(feats + i0 * D);
+        unsigned bad = 0u;
+        for (unsigned c0 = lane; c0 < total; c0 += 32u * SVX_FEAT_UNROLL) {
+            float4 v[SVX_FEAT_UNROLL];
+#pragma unroll
+            for (int u = 0; u < SVX_FEAT_UNROLL; ++u) {
+                const unsigned c = c0 + 32u * u;
+                v[u] = c < total ? __ldg(f4 + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int u = 0; u < SVX_FEAT_UNROLL; ++u) {
+                const unsigned c = c0 + 32u * u;
+                if (!finite4(v[u])) bad |= 1u << (d4 > 1u ? __umulhi(c, magic) : c);
+            }
+        }
+        bad = __reduce_or_sync(0xffffffffu, bad);
+        return ((bad >> lane) & 1u) == 0u;
+    }
+    }
     bool mine = true;
-    unsigned todo = __ballot_sync(0xffffffffu, has);
-    while (todo) {
-        const int src = __ffs(todo) - 1;
-        todo &= todo - 1;
+    unsigned left = todo;
+    while (left) {
+        const int src = __ffs(left) - 1;
+        left &= left - 1;
         const long long pi = __shfl_sync(0xffffffffu, i, src);
         const Fe* f = feats + pi * D;
         bool ok = true;
         if (sizeof(Fe) == 4 && (D & 3) == 0) {
             const float4* f4 = reinterpret_cast<const float4*>(f);
-            for (int c = lane; c < (D >> 2); c += 32) {
-                const float4 v = __ldg(f4 + c);
-                ok = ok && isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w);
-            }
+            for (int c = lane; c < (D >> 2); c += 32) ok = ok && finite4(__ldg(f4 + c));
         } else {
             for (int c = lane; c < D; c += 32) ok = ok && isfinite((double)f[c]);
         }

@@ -544,3 +544,38 @@ def test_open_huge_voxels_vs_oracle(D, feat_dtype):
     assert np.array_equal(c1, c2)
     assert np.array_equal(d1, d2) and np.array_equal(w1, w2)
     assert np.array_equal(m1, m2) and np.array_equal(b1, b2)
+
+
+@pytest.mark.parametrize("D", [4, 6, 512])
+def test_nonfinite_features_vs_oracle(D):
+    """Open-set frames whose feature rows carry NaN / inf at scattered rows
+    and positions (first and last element, several per warp, a ragged tail of
+    points): the walk's feature scan must mask exactly the rows the reference
+    masks (fusion.py:246-256).  D = 4 and 512 take the contiguous block scan,
+    D = 6 the row-by-row loop."""
+    from paper_2512_12945_b200 import Mapper
+    from oracle.oracle import OracleMap
+
+    kw = dict(voxel_size=0.1, truncation=0.3, feature_dim=D, max_range=12.0)
+    m = Mapper(**kw)
+    om = OracleMap(**kw)
+    rng = np.random.default_rng(7)
+    for pts, origin in _random_world_frames(3, 1000 + 37, 3, 0.1):
+        n = pts.shape[0]
+        feat = rng.normal(size=(n, D)).astype(np.float32)
+        bad = rng.choice(n, size=n // 20, replace=False)
+        pos = rng.integers(0, D, bad.size)
+        pos[: bad.size // 3] = D - 1
+        pos[bad.size // 3: 2 * bad.size // 3] = 0
+        vals = np.array([np.nan, np.inf, -np.inf], np.float32)[rng.integers(0, 3, bad.size)]
+        feat[bad, pos] = vals
+        feat[n - 1, D - 1] = np.nan                   # last element of the array
+        feat[32:40, D // 2] = np.inf                   # a run inside one warp
+        r1 = m.integrate_world(pts, origin, features=feat)
+        r2 = om.integrate_world(pts, origin, features=feat)
+        assert np.array_equal(report_rows([r1]), report_rows([r2]))
+        assert r1.skipped_bad_label > 0   # the reference counts bad feature rows as bad payload
+    c, d, w, s0, s1 = m._export()
+    oc, od, ow, os0, os1 = om.export()
+    assert np.array_equal(c, oc) and np.array_equal(d, od) and np.array_equal(w, ow)
+    assert np.array_equal(s0, os0) and np.array_equal(s1, os1)
