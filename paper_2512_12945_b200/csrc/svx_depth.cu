@@ -138,6 +138,14 @@ svx_status integrate_depth_impl(svx_map* m, const void* depth, int depth_dtype, 
     SVX_CUDA(cudaMemcpyAsync(&inv, d_inv, sizeof(inv), cudaMemcpyDeviceToHost, s));
     SVX_CUDA(cudaStreamSynchronize(s));
     // invalid pixels are not points of the reference's Frame
+    // host-link bytes of this call: the rasters staged from host memory
+    // (integrate_impl saw device pointers), the report mirror and `inv`
+    int64_t h2d = 0;
+    if (dd != depth) h2d += (int64_t)npix * (int64_t)dsz;
+    if (ld && ld != (const void*)labels) h2d += (int64_t)npix * 4;
+    if (fd && fd != feats) h2d += (int64_t)npix * (int64_t)fsz;
+    m->io_h2d = h2d;
+    m->io_d2h += (int64_t)sizeof(inv);
     if (g_trace_depth)
         fprintf(stderr, "svx depth us: backproject %.1f integrate %.1f tail %.1f\n", t1 - t0, t2 - t1,
                 depth_now_us() - t2);

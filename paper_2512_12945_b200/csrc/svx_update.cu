@@ -1081,7 +1081,7 @@ __device__ __forceinline__ void load8(const Fe* row, int lane, double* v) {
 // (lanes 0 .. kOpenGrp-1 issue one bulk copy each); kOpenBulkRing slots, i.e.
 // kOpenBulkRing * kOpenGrp rows in flight per warp.  Same in-order sums.
 #ifndef SVX_OPEN_GRP
-#define SVX_OPEN_GRP 6
+#define SVX_OPEN_GRP 4   // 4 rows x 2 slots x 8 warps fit 3 CTAs per SM (6 rows: 2 CTAs)
 #endif
 constexpr int kOpenGrp = SVX_OPEN_GRP;
 #ifndef SVX_OPEN_UNROLL
@@ -1239,7 +1239,8 @@ __device__ __forceinline__ void open_voxel(const UpdateArgs& a, const KeyPack& k
 // K5 open: every listed voxel; huge segments are deferred to k_update_open_huge.
 template <class TD, class TS, class Fe>
 #ifndef SVX_OPEN_MINB
-#define SVX_OPEN_MINB 2   // 2 CTAs per SM (<= 128 registers, no spills): cfg3 update -38 %, cfg5 -39 % vs 1
+#define SVX_OPEN_MINB 3   // 2 CTAs per SM (<= 128 registers): cfg3 update -38 %, cfg5 -39 % vs 1; 3 CTAs
+                          // (<= 80 registers, 40 B spilled, 4-row groups): a further -3 % / -2 %
 #endif
 __global__ void __launch_bounds__(32 * kWarpsPerCta, SVX_OPEN_MINB) k_update_open(UpdateArgs a, TD* vt, TS* mean,
                                                                    TS* beta) {

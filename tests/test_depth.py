@@ -67,6 +67,14 @@ def test_gpu_integrate_depth_matches_reference(name, device_inputs):
             pay = torch.from_numpy(np.ascontiguousarray(pay)).cuda()
         reps.append(m.integrate_depth(depth, pay, cam, pose=g[f"pose_{i}"]))
     assert np.array_equal(report_rows(reps), g["reports"])
+    # host-link bytes the library reports for the last call (bench e2e)
+    io = m.engine_stats()
+    last_d = np.asarray(g[f"depth_{g['n_frames'] - 1}"])
+    last_p = np.asarray(g[f"payload_{g['n_frames'] - 1}"])
+    pay_bytes = last_p.size * 4   # labels go in as int32, features as float32 here
+    want = 0 if device_inputs else last_d.nbytes + pay_bytes
+    assert io["last_h2d_bytes"] == want
+    assert io["last_d2h_bytes"] > 0
     tsdf, sem = m.grids
     coords, (d, w) = tsdf.active_values()
     assert np.array_equal(coords, g["coords"])
