@@ -177,6 +177,7 @@ struct FrameCtr {
 //   seg   base of the voxel's row segment (segment mode)
 //   key   the voxel's frame key (written by its first toucher)
 //   cur   segment fill cursor (segment mode)
+//   wold  open-set voxels: pre-frame TSDF weight (k_open_prep -> k_update_open)
 // Slot mode keeps each voxel's rows in vslot[vid * kSlots + j] = RowSlot
 // {point, label, d}: the row's distance was computed by the walk, so the
 // update reads everything it needs from the slots (rows 0-1 share a sector).
@@ -186,7 +187,8 @@ struct alignas(32) VoxFrame {
     unsigned seg;
     unsigned long long key;
     unsigned cur;
-    unsigned pad[3];
+    unsigned pad;
+    double wold;   // open-set: the pre-frame weight, left by k_open_prep for k_update_open
 };
 // Slot mode touched entry: the voxel id (bit 31 = created this frame;
 // 0xFFFFFFFF = its claim failed) and its bslot index (leaf * 512 + slot).

@@ -1162,16 +1162,24 @@ __device__ __forceinline__ void open_voxel(const UpdateArgs& a, const KeyPack& k
                                            const PoseParams& pp, TD* vt, TS* mean, TS* beta,
                                            const Fe* feats, int vid, unsigned c, int* buf,
                                            unsigned* bm, bool huge, Fe* ring = nullptr,
-                                           BulkRing<Fe>* bulk = nullptr) {
+                                           BulkRing<Fe>* bulk = nullptr, bool prepped = false) {
     const int lane = threadIdx.x & 31;
     const unsigned k = c & ~kNewBit;
     const bool isnew = (c & kNewBit) != 0u;
 #if SVX_OPEN_PREFETCH
     if (!isnew) prefetch_rows_l2(mean + (long long)vid * a.D, beta + (long long)vid * a.D, a.D * (int)sizeof(TS));
 #endif
-    const Center cc = center_of(a.rec[vid].key, kp, a.h, pp);
     int minr = 0;
     long long nwords = 0;
+    double w_old = 0.0;
+    if (prepped) {
+        // k_open_prep sorted the segment in place and applied the TSDF sums
+        const unsigned seg = a.rec[vid].seg;
+        for (unsigned j = lane; j < k; j += 32) buf[j] = __ldcg(a.srid + seg + j);
+        w_old = __ldcg(&a.rec[vid].wold);
+        __syncwarp();
+    } else {
+    const Center cc = center_of(a.rec[vid].key, kp, a.h, pp);
     if (huge) bitmap_build(a.srid, a.rec[vid].seg, k, bm, minr, nwords);
     else warp_sort_segment(a.srid, a.rec[vid].seg, (int)k, buf);
     // TSDF sums in point order
@@ -1185,9 +1193,9 @@ __device__ __forceinline__ void open_voxel(const UpdateArgs& a, const KeyPack& k
     } else {
         warp_tsdf_chunk<float>(a, nullptr, buf, (int)k, cc, acc, nullptr, false);
     }
-    double w_old = 0.0;
     if (lane == 0) w_old = apply_tsdf<TD>(vt, vid, isnew, a.trunc, acc.sw, acc.swd, acc.mind, acc.maxd);
     w_old = __shfl_sync(0xffffffffu, w_old, 0);
+    }
     // NIG batch update with lambda from the pre-frame weight (_pycore.py:438)
     const double nobs = (double)k;
     const double lam = fmax(w_old, a.lambda_floor);
@@ -1236,6 +1244,50 @@ __device__ __forceinline__ void open_voxel(const UpdateArgs& a, const KeyPack& k
     __syncwarp();
 }
 
+// K5 open prologue (SVX_OPEN_PREP): per listed voxel of <= kOpenCtaMin rows,
+// one warp sorts the voxel's row segment in place (ascending point index,
+// the reference's order) and applies its TSDF sums (_pycore.py:399-417);
+// the pre-frame weight the NIG update needs goes to rec[vid].wold.
+// k_update_open then runs only the feature passes, so its warps (3 per
+// scheduler, big rings) no longer wait on each segment's scattered ray
+// loads; this kernel hides them with 8 small CTAs per SM.
+#ifndef SVX_OPEN_PREP
+#define SVX_OPEN_PREP 0   // measured slower (update +11 % cfg3, +8 % cfg5): the prologue was already hidden
+#endif
+template <class TD>
+__global__ void __launch_bounds__(32 * kWarpsPerCta) k_open_prep(UpdateArgs a, TD* vt, int* srid) {
+    grid_dep_wait();
+    __shared__ int sbuf[kWarpsPerCta][kOpenCtaMin];
+    FrameCtr* ctr = a.ctr;
+    KSpan _ks(ctr, kSpanUpdate);
+    __shared__ FrameCtr s_ctr_;
+    snapshot_ctr(ctr, s_ctr_);
+    const FrameCtr* cv = &s_ctr_;
+    if (cv->abort | cv->err_cap) return;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const long long L = (long long)cv->n_list;
+    const KeyPack kp = cv->p.kp;
+    const PoseParams pp = cv->p.pp;
+    int* buf = sbuf[wib];
+    for (long long e = (long long)blockIdx.x * kWarpsPerCta + wib; e < L;
+         e += (long long)gridDim.x * kWarpsPerCta) {
+        const int vid = a.mlist[e];
+        const unsigned c = a.rec[vid].cnt;
+        const unsigned k = c & ~kNewBit;
+        if (k > (unsigned)kOpenCtaMin) continue;   // k_huge_prep sorts these
+        const unsigned seg = a.rec[vid].seg;
+        warp_sort_segment(srid, seg, (int)k, buf);
+        for (unsigned j = lane; j < k; j += 32) srid[seg + j] = buf[j];
+        const Center cc = center_of(a.rec[vid].key, kp, a.h, pp);
+        TsdfAcc acc{0.0, 0.0, INFINITY, -INFINITY, 0};
+        warp_tsdf_chunk<float>(a, nullptr, buf, (int)k, cc, acc, nullptr, false);
+        if (lane == 0)
+            a.rec[vid].wold = apply_tsdf<TD>(vt, vid, (c & kNewBit) != 0u, a.trunc, acc.sw, acc.swd, acc.mind,
+                                             acc.maxd);
+        __syncwarp();
+    }
+}
+
 // K5 open: every listed voxel; huge segments are deferred to k_update_open_huge.
 template <class TD, class TS, class Fe>
 #ifndef SVX_OPEN_MINB
@@ -1250,7 +1302,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, SVX_OPEN_MINB) k_update_ope
     extern __shared__ __align__(128) unsigned char oring[];
 #endif
     FrameCtr* ctr = a.ctr;
-    KSpan _ks(ctr, kSpanUpdate);
+    KSpan _ks(ctr, kSpanUpdate, SVX_OPEN_PREP != 0);   // the stage spans k_open_prep too
     __shared__ FrameCtr s_ctr_;
     snapshot_ctr(ctr, s_ctr_);
     const FrameCtr* cv = &s_ctr_;
@@ -1292,15 +1344,17 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, SVX_OPEN_MINB) k_update_ope
 #if SVX_OPEN_BULK
         if (use_bulk) {
             open_voxel<TD, TS, Fe>(a, kp, pp, vt, mean, beta, feats, vid, c, sbuf[wib], nullptr, false,
-                                   nullptr, &bulk);
+                                   nullptr, &bulk, SVX_OPEN_PREP != 0);
             continue;
         }
 #endif
 #if SVX_OPEN_RING
         Fe* ring = reinterpret_cast<Fe*>(oring) + (size_t)wib * kOpenRingS * kOpenRingR * kOpenPass;
-        open_voxel<TD, TS, Fe>(a, kp, pp, vt, mean, beta, feats, vid, c, sbuf[wib], nullptr, false, ring);
+        open_voxel<TD, TS, Fe>(a, kp, pp, vt, mean, beta, feats, vid, c, sbuf[wib], nullptr, false, ring,
+                               nullptr, SVX_OPEN_PREP != 0);
 #else
-        open_voxel<TD, TS, Fe>(a, kp, pp, vt, mean, beta, feats, vid, c, sbuf[wib], nullptr, false);
+        open_voxel<TD, TS, Fe>(a, kp, pp, vt, mean, beta, feats, vid, c, sbuf[wib], nullptr, false, nullptr,
+                               nullptr, SVX_OPEN_PREP != 0);
 #endif
     }
 }
@@ -1942,6 +1996,11 @@ svx_status closed_b(svx_map* m, cudaStream_t s) {
 
 template <class TD, class TS, class Fe>
 svx_status open_a(svx_map* m, cudaStream_t s) {
+    if (SVX_OPEN_PREP) {
+        SVX_CUDA(launch_pdl(k_open_prep<TD>, kLongBlocks, 32 * kWarpsPerCta, 0, s, make_args(m), ptr<TD>(m->vt),
+                            ptr<int>(m->srid)));
+        SVX_LAUNCHED();
+    }
     int ring = SVX_OPEN_RING ? kWarpsPerCta * kOpenRingS * kOpenRingR * kOpenPass * (int)sizeof(Fe) : 0;
     if (SVX_OPEN_BULK) ring = std::max(ring, kWarpsPerCta * kOpenBulkRing * kOpenGrp * kOpenPass * (int)sizeof(Fe));
     if (ring > 0) {
