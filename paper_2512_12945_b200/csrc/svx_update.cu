@@ -1084,6 +1084,9 @@ __device__ __forceinline__ void load8(const Fe* row, int lane, double* v) {
 #define SVX_OPEN_GRP 4   // 4 rows x 2 slots x 8 warps fit 3 CTAs per SM (6 rows: 2 CTAs)
 #endif
 constexpr int kOpenGrp = SVX_OPEN_GRP;
+#ifndef SVX_OPEN_LDGSTS
+#define SVX_OPEN_LDGSTS 0   // 1: group slices by per-lane 16-byte cp.async instead of one bulk copy per row
+#endif
 #ifndef SVX_OPEN_UNROLL
 #define SVX_OPEN_UNROLL 2   // A/B with 4-row groups: 2 beats 3 and 4 by ~3 %
 #endif
@@ -1107,6 +1110,29 @@ __device__ __forceinline__ void open_chunk_grp(const Fe* __restrict__ feats, int
     const int nd = kFull ? kOpenPass : min(kOpenPass, D - base);
     const unsigned bytes = (unsigned)(nd * (int)sizeof(Fe));
     const int ng = (cnt + kOpenGrp - 1) / kOpenGrp;
+#if SVX_OPEN_LDGSTS
+    // every lane moves 16-byte pieces of the group's row slices (cp.async);
+    // one commit group per slot, waited per lane, then a warp barrier
+    const unsigned nchunk = bytes >> 4;
+    auto issue = [&](int g) {
+        if (g < ng) {
+            const int sl = g % kOpenBulkRing, j0 = g * kOpenGrp;
+            const int nr = min(kOpenGrp, cnt - j0);
+            for (int r = 0; r < nr; ++r) {
+                const char* src = reinterpret_cast<const char*>(feats + (long long)buf[j0 + r] * D + base);
+                char* dst = reinterpret_cast<char*>(R.slot + (sl * kOpenGrp + r) * kOpenPass);
+                for (unsigned q = lane; q < nchunk; q += 32) __pipeline_memcpy_async(dst + 16 * q, src + 16 * q, 16);
+            }
+        }
+        __pipeline_commit();
+    };
+    __syncwarp();
+    for (int g = 0; g < kOpenBulkRing; ++g) issue(g);
+    for (int g = 0; g < ng; ++g) {
+        const int sl = g % kOpenBulkRing;
+        __pipeline_wait_prior(kOpenBulkRing - 1);
+        __syncwarp();
+#else
     auto issue = [&](int g) {
         const int sl = g % kOpenBulkRing, j0 = g * kOpenGrp;
         const int nr = min(kOpenGrp, cnt - j0);
@@ -1128,6 +1154,7 @@ __device__ __forceinline__ void open_chunk_grp(const Fe* __restrict__ feats, int
         const int sl = g % kOpenBulkRing;
         mbar_wait(R.bar + sl, (R.phase >> sl) & 1u);
         R.phase ^= 1u << sl;
+#endif
         const int nr = min(kOpenGrp, cnt - g * kOpenGrp);
         const Fe* src = R.slot + sl * kOpenGrp * kOpenPass;
 #pragma unroll (kOpenUnroll)
@@ -1153,8 +1180,15 @@ __device__ __forceinline__ void open_chunk_grp(const Fe* __restrict__ feats, int
             }
         }
         __syncwarp();
+#if SVX_OPEN_LDGSTS
+        issue(g + kOpenBulkRing);
+#else
         if (g + kOpenBulkRing < ng) issue(g + kOpenBulkRing);
+#endif
     }
+#if SVX_OPEN_LDGSTS
+    __pipeline_wait_prior(0);
+#endif
 }
 
 template <class TD, class TS, class Fe>
