@@ -130,6 +130,9 @@ __device__ __forceinline__ void clear_voxel_frame(const UpdateArgs& a, int vid) 
 }
 
 // ---- K4: scatter, single-row voxels finished in ray order --------------------------
+#ifndef SVX_SCATTER_AGG
+#define SVX_SCATTER_AGG 1   // warp-aggregated segment cursors
+#endif
 // One thread per row.  A voxel with exactly one row needs no ordering: its
 // sums are the row's own (0.0 + w * d exactly as the reference's sequential
 // sum, _core.pyx:793-795), so closed/geometry maps update it right here;
@@ -170,8 +173,23 @@ __global__ void SVX_LB_SCATTER k_scatter(UpdateArgs a, const int* __restrict__ r
         const int vid = rowvid[t];
         const unsigned c = a.rec[vid].cnt;
         if (!singles || (c & ~kNewBit) > 1u) {
+#if SVX_SCATTER_AGG
+            // lanes here with the same voxel take consecutive places with one
+            // atomic (neighbouring rays share voxels; a camera close to a wall
+            // sends ~10^4 rows into each of a few voxels): the segment's order
+            // is irrelevant, the update sorts it by point index
+            const unsigned act = __activemask();
+            const unsigned peers = __match_any_sync(act, vid);
+            const int lane = threadIdx.x & 31;
+            const int leader = __ffs(peers) - 1;
+            unsigned off = 0u;
+            if (lane == leader) off = atomicAdd(&a.rec[vid].cur, (unsigned)__popc(peers));
+            off = __shfl_sync(peers, off, leader) + (unsigned)__popc(peers & ((1u << lane) - 1u));
+            srid[a.rec[vid].seg + off] = (int)i;
+#else
             const unsigned pos = a.rec[vid].seg + atomicAdd(&a.rec[vid].cur, 1u);
             srid[pos] = (int)i;
+#endif
             continue;
         }
         const unsigned long long key = rowkey[t];
