@@ -1448,7 +1448,10 @@ constexpr int kHugeStageBytes = SVX_HUGE_STAGE_KB * 1024;
 constexpr int kHugeItemCtas = 148 * SVX_HUGE_ITEM_CPS;   // CTAs per SM x SMs (4 stages of shared memory each)
 // Voxels of up to kGiantRows rows: one CTA each (k_update_open_huge, all
 // dimensions); bigger ones: dimension slices over many SMs (k_huge_items).
-constexpr int kGiantRows = 8192;
+#ifndef SVX_GIANT_ROWS
+#define SVX_GIANT_ROWS 8192
+#endif
+constexpr int kGiantRows = SVX_GIANT_ROWS;
 // k_huge_items: warps folding one item's dimensions (32 each); the SM folds
 // kHugeFold * 32 dimension chains at once (1 = one fold warp per SM).
 #ifndef SVX_HUGE_FOLD
