@@ -1449,7 +1449,7 @@ constexpr int kHugeItemCtas = 148 * SVX_HUGE_ITEM_CPS;   // CTAs per SM x SMs (4
 // Voxels of up to kGiantRows rows: one CTA each (k_update_open_huge, all
 // dimensions); bigger ones: dimension slices over many SMs (k_huge_items).
 #ifndef SVX_GIANT_ROWS
-#define SVX_GIANT_ROWS 8192
+#define SVX_GIANT_ROWS 4096   // A/B: cfg3 close-wall frames update_b -18 % vs 8192, cfg5 neutral; 16384 worse
 #endif
 constexpr int kGiantRows = SVX_GIANT_ROWS;
 // k_huge_items: warps folding one item's dimensions (32 each); the SM folds
